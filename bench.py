@@ -1,0 +1,306 @@
+#!/usr/bin/env python
+"""bench.py — trace events analysed per second on B200 (BASELINE.json metric), with the HBM
+roofline fraction and the CPU oracle beside it.
+
+One step = one pass of the whole hot path (scan_match_collectives + scan_detect + scan_localize,
+SURVEY.md §8(a) rows A1-A8) over one synthetic trace resident in HBM.
+Default workload (N=1): configs[2] "C3" — 1024 ranks TP8xPP8xDP16, 1000 iterations,
+960,768,000 events, mixed throttling + link jitter (the north-star target workload).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--iters I] [--impl reference]
+
+N>1 (torchrun): every rank analyses its own iteration-window shard of the same job (weak scaling
+of the generated trace); see DESIGN.md §Multi-GPU for the status of the exchange step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "trace events analysed/sec (1/2/4/8 B200) and % of HBM roofline vs CPU oracle"
+WORKLOADS = {
+    "c1": "C1 8-rank TP2xPP2xDP2, L_s=12, M=8, 10 it, rank 5 throttled x2.0",
+    "c2": "C2 64-rank TP8xPP4xDP2, L_s=8, M=16, 200 it, jitter on the 16 fwd links leaving stage 1",
+    "c3": "C3 1024-rank TP8xPP8xDP16, L_s=8, M=8, 1000 it, rank 299 x1.6 [200,600), rank 862 x2.5 [500,900), "
+          "jitter on the 128 fwd links leaving stage 4",
+    "c4": "C4 3072-rank TP8xPP64xDP6, L_s=2, M=16, 500 it, one rank x1.5 + one link x0.5",
+    "c5": "C5 512-rank TP8xPP8xDP8, L_s=8, M=8, 100 it, cascading victims (whole trace)",
+}
+
+
+def alg_bytes_per_event(comm_frac: float) -> float:
+    """read dur 4 + kind_op 2 + meta 2 + comm 4 + payload 4 = 16 B/event; write
+    inst_id 4 + wait 4 per comm event and a 1 B slow flag per compute event."""
+    return 16.0 + 8.0 * comm_frac + 1.0 * (1.0 - comm_frac)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.rows: list[list[str]] = []
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+        return self
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.p:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=2)
+            except Exception:
+                self.p.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+                for n, v in zip(names, r[3:7]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+            except Exception:
+                pass
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_trace(name: str, iters: int | None, seed: int, pinned: bool, it_range=None):
+    import tracegen as tg
+    from tracegen import configs
+    cfg = configs.CONFIGS[name](seed=seed) if iters is None else configs.CONFIGS[name](seed=seed, iterations=iters)
+    ro = tg.count(cfg)
+    n = int(ro[-1])
+    out = None
+    if pinned:
+        import torch
+        out = {}
+        for k, dt in (("dur_ns", torch.int32), ("kind_op", torch.int16), ("meta", torch.int16), ("comm", torch.int32),
+                      ("payload", torch.int32)):
+            t = torch.empty(n, dtype=dt, pin_memory=True)
+            out[k] = t.numpy().view({torch.int32: np.uint32, torch.int16: np.uint16}[dt])
+    return tg.generate(cfg, out=out, with_start=False), cfg
+
+
+def cpu_oracle_rate(name: str, sample_iters: int, seed: int) -> dict:
+    import oracle
+    tr, _ = make_trace(name, sample_iters, seed, pinned=False)
+    t0 = time.perf_counter()
+    oracle.run(tr)
+    dt = time.perf_counter() - t0
+    return {"value": tr.n_events / dt, "unit": "events/s", "cores": 1, "kind": "oracle",
+            "sample": f"{name} shape, iterations [0,{sample_iters}) = {tr.n_events} events, single-threaded C++ oracle, "
+                      f"{dt:.2f} s", "seconds": dt}
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    sample_iters = args.ref_iters
+    rates = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_oracle_rate(args.config, sample_iters, args.seed)
+        if i >= args.warmup:
+            rates.append(r)
+    v = float(np.median([r["value"] for r in rates]))
+    secs = float(np.median([r["seconds"] for r in rates]))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "events/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config] + f" (sample: iterations [0,{sample_iters}))"},
+            "cpu_baseline": {"value": v, "unit": "events/s", "cores": 1, "kind": "oracle", "sample": rates[0]["sample"]},
+            "e2e": {"value": v, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--iters", type=int, default=None, help="override the config's iteration count")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--cpu-iters", type=int, default=40, help="oracle sample (iterations) for cpu_baseline")
+    ap.add_argument("--ref-iters", type=int, default=10, help="oracle sample per step for --impl reference")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--breakdown", action="store_true", default=True)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import paper_2507_19845_b200 as ms
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    # ---- synthetic trace: host (pinned) -> device columns ----
+    iters = args.iters
+    seed = args.seed + (rank if world > 1 else 0)
+    t_gen = time.perf_counter()
+    tr, cfg = make_trace(args.config, iters, seed, pinned=True)
+    t_gen = time.perf_counter() - t_gen
+    N = tr.n_events
+    comm_frac = float(((tr.kind_op & 7) != 0).mean()) if N <= 50_000_000 else float(
+        ((tr.kind_op[: 50_000_000] & 7) != 0).mean())
+    host = {k: getattr(tr, k) for k in ("dur_ns", "kind_op", "meta", "comm", "payload")}
+    dev = {k: torch.from_numpy(v.view(np.int16 if v.dtype == np.uint16 else np.int32)).cuda(local, non_blocking=True)
+           for k, v in host.items()}
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(local)
+    s = ms.Scan(local, stream.cuda_stream)
+    s.load(tr, device_ptrs=True, cols=dev)
+
+    def step():
+        s.match()
+        s.detect()
+        s.localize()
+
+    for _ in range(args.warmup):
+        step()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms_total = ev0.elapsed_time(ev1)
+    launches = s.kernel_launches()
+    t_local = torch.tensor([ms_total], dtype=torch.float64, device=f"cuda:{local}")
+    n_tot = torch.tensor([float(N)], dtype=torch.float64, device=f"cuda:{local}")
+    if dist:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+        dist.all_reduce(n_tot, op=dist.ReduceOp.SUM)
+    ms_step = float(t_local.item()) / args.steps
+    value = float(n_tot.item()) / (ms_step / 1e3)
+
+    # per-kernel breakdown (separate, untimed-for-value pass with CUDA events on the launch stream)
+    kernels = {}
+    if args.breakdown:
+        s.set_timing(True)
+        step()
+        kernels = s.kernel_timing()
+        s.set_timing(False)
+    # verdicts for the record
+    verdict = s.export("wl_verdict")
+    flagged = {int(r): int(v) for r, v in enumerate(verdict) if v}
+
+    # ---- e2e: host pinned columns through the public API, H2D + analysis + D2H of the verdicts ----
+    e2e = None
+    if not args.no_e2e:
+        s2 = ms.Scan(local, stream.cuda_stream)
+        h2d = sum(v.nbytes for v in host.values())
+        times = []
+        for i in range(2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            s2.load(tr)
+            s2.match()
+            s2.detect()
+            s2.localize()
+            out_v = s2.export("wl_verdict")
+            out_l = s2.export("lb_label")
+            times.append(time.perf_counter() - t0)
+        s2.close()
+        d2h = out_v.nbytes + out_l.nbytes
+        e2e = {"value": N / min(times), "unit": "events/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "seconds_per_step": min(times)}
+
+    if rank != 0:
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    bpe = alg_bytes_per_event(comm_frac)
+    achieved = bpe * N / (ms_step / 1e3) / 1e9
+    dom = max(kernels.items(), key=lambda kv: kv[1][0]) if kernels else None
+    kern_ms = sum(v[0] for v in kernels.values()) if kernels else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            if tj.get("config") == args.config and tj.get("iters") == (iters or cfg.iterations):
+                traffic = tj.get("dram_bytes_per_step")
+        except Exception:
+            traffic = None
+    cpu = None
+    if not args.no_cpu and world == 1:
+        cpu = cpu_oracle_rate(args.config, args.cpu_iters, args.seed)
+        cpu.pop("seconds", None)
+    line = {
+        "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config] + (f" [{iters} it]" if iters else ""), "events": N,
+                   "comm_fraction": round(comm_frac, 4), "parallelism": f"trace shard per GPU x{world}",
+                   "l2": "inputs (16 B/event, %.1f GB) >> 126 MB L2: no flush needed" % (16 * N / 1e9),
+                   "generator_s": round(t_gen, 1)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
+                     "bytes_per_event": round(bpe, 3), "scope": "whole step (all kernels); see kernels",
+                     "dominant_kernel": ({"name": dom[0], "ms": dom[1][0], "launches": dom[1][1],
+                                          "share": dom[1][0] / kern_ms} if dom else None)},
+        "kernels": {k: {"ms": round(v[0], 4), "launches": v[1]} for k, v in sorted(kernels.items(), key=lambda kv: -kv[1][0])},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches) * args.steps,
+        "clocks": clk.summary(),
+        "verdicts": {"flagged": flagged},
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,244 @@
+/*
+ * megascan/scan.h — C ABI of the B200-native MegaScan trace-analysis hot path.
+ *
+ * The operation is MegaScan's analysis pass (§3.2, lines 127-154 of
+ * /root/reference/PAPER.md, cited below as P:Lnn): given per-rank CUDA-event
+ * operator traces of a TP x PP x DP Megatron job it
+ *   (1) matches each collective / P2P instance across the ranks of its
+ *       communicator ("Dependency reconstruction"),
+ *   (2) derives per-operator compute / wait / transfer times (end-simultaneity,
+ *       P:L133; reading R5/R6),
+ *   (3) flags slow ranks: stage 1 cross-DP comparison, stage 2
+ *       collective start lag, stage 3 P2P effective bandwidth
+ *       (P:L150-154),
+ *   (4) separates anomaly sources from victims by walking the wait-for
+ *       structure (reading R17).
+ * Every decision is integer / exact-rational; f64 appears only in reported
+ * ratios (reading R19).
+ *
+ * Conventions
+ *  - All functions are extern "C", all integers fixed width.
+ *  - Pointers are HOST pointers unless the argument or flag says DEVICE.
+ *  - All device work is enqueued on the stream given to scan_create(); every
+ *    call returns after its work completed (it synchronises that stream).
+ *  - A context is not thread-safe. Result arrays are owned by the context and
+ *    stay valid until the next scan_load_events() or scan_destroy().
+ *  - Errors: a negative scan_status; scan_last_error() gives a message.
+ *    No CPU fallback exists: without a CUDA device every call fails with
+ *    SCAN_E_CUDA.
+ */
+#ifndef MEGASCAN_SCAN_H
+#define MEGASCAN_SCAN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t scan_status;
+#define SCAN_OK               0
+#define SCAN_PARTIAL          1   /* success, but unmatched / inconsistent instances were reported */
+#define SCAN_E_INVALID_ARG   -1
+#define SCAN_E_SCHEMA        -2   /* event fails the schema (kind, comm id, membership, peer) */
+#define SCAN_E_INTEGRITY     -3   /* only with SCAN_STRICT: any unmatched / mismatched instance */
+#define SCAN_E_ORDER         -4   /* call sequence violated (detect before match, ...) */
+#define SCAN_E_CUDA          -5
+#define SCAN_E_NCCL          -6
+#define SCAN_E_OOM           -7
+#define SCAN_E_UNSUPPORTED   -8   /* a documented capacity limit was exceeded */
+
+typedef struct scan_ctx scan_ctx;
+
+/* ---- event schema (P:L105-114 CUDA-event ops + tracers.scope metadata) ---------------- */
+/* kind_op u16 = kind:3 | iter_end:1 | op_id:12                                             */
+#define SCAN_KIND_COMPUTE        0
+#define SCAN_KIND_ALLREDUCE      1
+#define SCAN_KIND_ALLGATHER      2
+#define SCAN_KIND_REDUCESCATTER  3
+#define SCAN_KIND_BROADCAST      4
+#define SCAN_KIND_SEND           5
+#define SCAN_KIND_RECV           6
+/* meta u16 = mb:10 | chunk:3 | bwd:1 | warmup:1 | rsv:1  (warmup: forward send issued before
+   the sender's first backward of its iteration, reading R13)                     */
+
+typedef struct scan_topology {
+    int32_t tp, pp, dp;      /* world = tp*pp*dp ranks                                         */
+    uint32_t rank_order;     /* must be 0: rank = tp + TP*(dp + DP*pp) (reading R1) */
+} scan_topology;
+
+typedef struct scan_comm_table {     /* collective communicators ("global ID list")    */
+    uint32_t n_comms;
+    const uint64_t* offsets;         /* HOST [n_comms+1], CSR into members                      */
+    const uint32_t* members;         /* HOST, ascending rank ids per communicator               */
+} scan_comm_table;
+
+typedef struct scan_event_columns {  /* structure-of-arrays, events grouped by rank, program order */
+    uint64_t n_events;
+    const uint64_t* rank_offsets;    /* HOST [world+1], monotone; rank r owns [off[r], off[r+1]) */
+    const int64_t*  start_ns;        /* optional (may be NULL): local-clock start; never read     */
+    const uint32_t* dur_ns;          /* CUDA-event duration, ns                                    */
+    const uint16_t* kind_op;
+    const uint16_t* meta;
+    const uint32_t* comm;            /* collective: communicator id; SEND/RECV: peer rank          */
+    const uint32_t* payload_bytes;   /* P2P payload; ignored for other kinds                       */
+} scan_event_columns;
+
+/* scan_load_events flags */
+#define SCAN_HOST_PTRS    0u   /* columns are host memory: copied H2D (pinned memory recommended) */
+#define SCAN_DEVICE_PTRS  1u   /* columns are device memory on the ctx device: borrowed, zero-copy;
+                                  caller keeps them alive and unchanged until the next load/destroy;
+                                  each column must be 16-byte aligned                              */
+#define SCAN_STRICT       2u   /* scan_match_collectives returns SCAN_E_INTEGRITY on any report    */
+
+/* ---- results ----------------------------------------------------------------------------- */
+typedef struct scan_match_result {
+    uint64_t n_events, n_comm_events, n_compute_events;
+    uint64_t n_channels, n_p2p_channels, n_instances;
+    uint64_t n_incomplete, n_kind_mismatch, n_payload_mismatch;
+    uint64_t n_iters;
+} scan_match_result;
+
+typedef struct scan_detect_config {   /* stage 1; defaults from SPEC S:L294 as rationals */
+    uint32_t slow_num, slow_den;       /* slow iff slow_den*dur > slow_num*ref     (3, 2)            */
+    uint64_t slow_margin_ns;           /*      and dur - ref > margin              (50000)           */
+    uint32_t cand_num, cand_den;       /* candidate iff cand_den*slow > cand_num*total (3, 10)       */
+    uint32_t min_samples;              /*      and total >= min_samples            (10)              */
+    uint32_t window_iters;             /* 0 = whole trace, else sliding windows of k iterations      */
+    uint32_t want_ref;                 /* 1: also materialise the per-event reference (ref_ns)       */
+    uint32_t pad;
+} scan_detect_config;
+
+typedef struct scan_detect_result {
+    uint64_t n_windows, n_compared, n_slow, n_candidates, n_class_mismatch;
+} scan_detect_result;
+
+typedef struct scan_localize_config {  /* stages 2-3 + walk                 */
+    uint64_t late_margin_ns;           /* late iff unique last arriver and dmax-dmin > margin (100000) */
+    uint32_t late_num, late_den;       /* ComputeSlow iff late_den*late >= late_num*joined (7, 10)    */
+    uint32_t bw_num, bw_den;           /* LinkSlow iff bw_den*p_l*t_g < bw_num*p_g*t_l     (7, 10)    */
+    uint32_t min_samples;              /* (10)                                                         */
+    uint32_t stage2_classes;           /* bit0 TP groups, bit1 DP groups (3)                           */
+    uint32_t stage2_mode;              /* 0 CONDITIONAL (reading R11), 1 UNCONDITIONAL   */
+    uint32_t pad;
+    uint64_t wait_margin_ns;           /* wait-for edge iff wait > margin (100000)                     */
+} scan_localize_config;
+
+typedef struct scan_localize_result {
+    uint64_t n_windows, n_links, n_link_slow;
+    uint64_t n_compute_slow, n_link_slow_ranks, n_both, n_exonerated, n_insufficient;
+    uint64_t n_roots, n_victims, n_unattributed, n_edges;
+} scan_localize_result;
+
+/* verdicts (per window, rank) */
+#define SCAN_V_NONE           0
+#define SCAN_V_COMPUTE_SLOW   1
+#define SCAN_V_LINK_SLOW      2
+#define SCAN_V_BOTH           3
+#define SCAN_V_EXONERATED     4
+#define SCAN_V_INSUFFICIENT   5
+/* labels (per window, rank) */
+#define SCAN_L_CLEAN          0
+#define SCAN_L_SOURCE_RANK    1
+#define SCAN_L_SOURCE_LINK    2
+#define SCAN_L_VICTIM         3
+#define SCAN_L_UNATTRIBUTED   4
+/* instance flags */
+#define SCAN_F_COMPLETE     1u
+#define SCAN_F_KIND_OK      2u
+#define SCAN_F_PAYLOAD_OK   4u
+#define SCAN_F_VALID        8u
+#define SCAN_F_UNIQUE_LAST 16u
+#define SCAN_F_WARMUP      32u
+
+/* ---- lifecycle ------------------------------------------------------------------------- */
+/* cuda_stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream), or NULL for the
+   legacy default stream. Errors: SCAN_E_INVALID_ARG, SCAN_E_CUDA.                            */
+scan_status scan_create(scan_ctx** out, int cuda_device, void* cuda_stream);
+void        scan_destroy(scan_ctx* ctx);
+const char* scan_last_error(const scan_ctx* ctx);   /* owned by ctx; "" if none               */
+
+/* A0 ingest: validate sizes, place the columns on the device, build the comm tables.
+   Per-event schema validation happens in scan_match_collectives (one pass).
+   Errors: SCAN_E_INVALID_ARG (sizes, alignment, rank_order), SCAN_E_UNSUPPORTED
+   (world > 65535 or n_comms + world^2 >= 2^32), SCAN_E_OOM, SCAN_E_CUDA.                    */
+scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const scan_comm_table* comms,
+                             const scan_event_columns* cols, uint32_t flags);
+
+/* A1-A3: sequence numbers per (rank, channel), instance ids = base(channel) + k, completeness,
+   integrity, per-instance dmin/dmax/last arriver, per-event wait, per-rank sums.
+   Channels: communicators by id, then P2P (src,dst) pairs ascending (reading R2-R4).
+   Returns SCAN_OK, SCAN_PARTIAL (reports present), SCAN_E_SCHEMA (first bad event in the
+   message), SCAN_E_INTEGRITY (with SCAN_STRICT), SCAN_E_UNSUPPORTED (a rank touching more than
+   256 channels, >2^32-1 instances), SCAN_E_ORDER (no load).                                   */
+scan_status scan_match_collectives(scan_ctx* ctx, scan_match_result* out);
+
+/* A4: stage 1 (leave-one-out lower median of the other DP peers, common op-id prefix).
+   Requires a match (else SCAN_E_ORDER). cfg NULL = defaults.                                  */
+scan_status scan_detect(scan_ctx* ctx, const scan_detect_config* cfg, scan_detect_result* out);
+
+/* A5-A8: stage 2, stage 3, verdicts, wait-for edges, frontier walk. Uses the windows of the
+   preceding scan_detect. Requires detect (else SCAN_E_ORDER). cfg NULL = defaults.            */
+scan_status scan_localize(scan_ctx* ctx, const scan_localize_config* cfg, scan_localize_result* out);
+
+/* ---- result export ------------------------------------------------------------------------ */
+typedef enum scan_output {
+    /* per event, event order (expanded from the compact native layouts) */
+    SCAN_OUT_EV_INST = 0,      /* u32, UINT32_MAX for compute events                   */
+    SCAN_OUT_EV_WAIT,          /* u32 ns, 0 for compute events / invalid instances     */
+    SCAN_OUT_EV_SLOW,          /* u8, 1 = stage-1 slow compute event                   */
+    SCAN_OUT_EV_REF,           /* u32 ns, UINT32_MAX if not compared (needs want_ref)  */
+    /* channels [n_channels] */
+    SCAN_OUT_CH_KIND, SCAN_OUT_CH_A, SCAN_OUT_CH_B, SCAN_OUT_CH_NMEM, SCAN_OUT_CH_NMAX, SCAN_OUT_CH_NMIN,
+    SCAN_OUT_CH_BASE,          /* u8 kind (0 coll, 1 p2p), u32 a (comm / src), u32 b (dst or MAX),
+                                  u32 members, u32 max count, u32 min count, u64 first instance id */
+    /* instances [n_instances] */
+    SCAN_OUT_IN_CHANNEL, SCAN_OUT_IN_K, SCAN_OUT_IN_FLAGS, SCAN_OUT_IN_DMIN, SCAN_OUT_IN_DMAX,
+    SCAN_OUT_IN_LAST, SCAN_OUT_IN_NPRESENT, SCAN_OUT_IN_PAYLOAD,
+    /* per rank [world] */
+    SCAN_OUT_RK_SUM_COMPUTE, SCAN_OUT_RK_SUM_WAIT, SCAN_OUT_RK_SUM_TRANSFER,   /* u64 ns */
+    /* per peer class (tp,pp) [tp*pp], class = pp*tp_size + tp */
+    SCAN_OUT_CL_J, SCAN_OUT_CL_MISMATCH,
+    /* per (window, rank) [n_windows*world] */
+    SCAN_OUT_WD_TOTAL, SCAN_OUT_WD_SLOW, SCAN_OUT_WD_CAND, SCAN_OUT_WD_FRAC,
+    SCAN_OUT_WL_JOINED, SCAN_OUT_WL_LATE, SCAN_OUT_WL_LATE_FRAC, SCAN_OUT_WL_VERDICT, SCAN_OUT_WL_LINK_SLOW,
+    /* per (window, P2P channel) [n_windows*n_p2p_channels] */
+    SCAN_OUT_LK_WINDOW, SCAN_OUT_LK_SRC, SCAN_OUT_LK_DST, SCAN_OUT_LK_N, SCAN_OUT_LK_MED_PAYLOAD,
+    SCAN_OUT_LK_MED_TRANSFER, SCAN_OUT_LK_USED_WARM, SCAN_OUT_LK_SLOW, SCAN_OUT_LK_DIR, SCAN_OUT_LK_ELIGIBLE,
+    SCAN_OUT_LK_MED_BW,
+    /* per (window, rank) labels */
+    SCAN_OUT_LB_LABEL, SCAN_OUT_LB_ROOT_KIND, SCAN_OUT_LB_ROOT_RANK, SCAN_OUT_LB_ROOT_SRC, SCAN_OUT_LB_DEPTH,
+    SCAN_OUT_LB_TOTAL_WAIT,
+    /* wait-for edges, sorted by (window, waiter, waited-on) [n_edges] */
+    SCAN_OUT_EG_WINDOW, SCAN_OUT_EG_SRC, SCAN_OUT_EG_DST, SCAN_OUT_EG_WEIGHT,
+    /* native compact layouts (zero-copy via scan_output_device_ptr) */
+    SCAN_OUT_COMM_INST,        /* u32 per comm event, ranks concatenated, program order       */
+    SCAN_OUT_COMM_WAIT,        /* u32 per comm event                                          */
+    SCAN_OUT_SLOW_BITS,        /* u32 words, per rank ceil(n_compute/32) words, bit j = slow  */
+    SCAN_OUT__COUNT
+} scan_output;
+
+/* Byte size of an output (0 if not yet computed). */
+scan_status scan_output_size(scan_ctx* ctx, scan_output which, uint64_t* bytes);
+/* Copy an output into dst (host or device memory of dst_bytes >= size). Export of the event-order
+   arrays runs a (untimed) expansion kernel. */
+scan_status scan_export(scan_ctx* ctx, scan_output which, void* dst, uint64_t dst_bytes, int dst_is_device);
+/* Device pointer of a native compact output (SCAN_OUT_COMM_INST, _COMM_WAIT, _SLOW_BITS); NULL otherwise. */
+const void* scan_output_device_ptr(scan_ctx* ctx, scan_output which);
+
+/* Number of hot-path kernel launches issued by the last match+detect+localize sequence. */
+uint64_t scan_kernel_launches(const scan_ctx* ctx);
+
+/* Optional per-kernel timing with CUDA events recorded on the ctx stream around every launch
+   (enable = 1), accumulated until scan_timing_reset(). scan_kernel_timing() returns the number of
+   distinct kernels; for 0 <= i < that number it fills the kernel name (static string), total
+   milliseconds and launch count. Timing adds one event pair per launch; keep it off for the
+   headline number. */
+scan_status scan_set_timing(scan_ctx* ctx, int enable);
+void        scan_timing_reset(scan_ctx* ctx);
+int         scan_kernel_timing(scan_ctx* ctx, int i, const char** name, double* total_ms, uint64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MEGASCAN_SCAN_H */

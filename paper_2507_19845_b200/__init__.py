@@ -1,0 +1,334 @@
+"""paper_2507_19845_b200 — B200-native MegaScan trace-analysis hot path (arXiv 2507.19845 §3.2).
+
+Thin ctypes binding over the C ABI in ``include/megascan/scan.h`` (``libmegascan.so``, built
+in-tree for sm_100a). Argument marshalling only: every analysis step runs in the CUDA kernels.
+There is no CPU fallback — if the library or a CUDA device is missing, calls raise.
+
+Same names as the C ABI: ``scan_create``, ``scan_load_events``, ``scan_match_collectives``,
+``scan_detect``, ``scan_localize``, ``scan_export``; plus the ``Scan`` convenience class.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _build
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+
+SCAN_OK, SCAN_PARTIAL = 0, 1
+SCAN_HOST_PTRS, SCAN_DEVICE_PTRS, SCAN_STRICT = 0, 1, 2
+_STATUS = {0: "SCAN_OK", 1: "SCAN_PARTIAL", -1: "SCAN_E_INVALID_ARG", -2: "SCAN_E_SCHEMA", -3: "SCAN_E_INTEGRITY",
+           -4: "SCAN_E_ORDER", -5: "SCAN_E_CUDA", -6: "SCAN_E_NCCL", -7: "SCAN_E_OOM", -8: "SCAN_E_UNSUPPORTED"}
+
+# export names, in scan_output enum order, with dtypes
+OUTPUTS = [
+    ("ev_inst", np.uint32), ("ev_wait", np.uint32), ("ev_slow", np.uint8), ("ev_ref", np.uint32),
+    ("ch_kind", np.uint8), ("ch_a", np.uint32), ("ch_b", np.uint32), ("ch_nmem", np.uint32), ("ch_nmax", np.uint32),
+    ("ch_nmin", np.uint32), ("ch_base", np.uint64),
+    ("in_channel", np.uint32), ("in_k", np.uint32), ("in_flags", np.uint8), ("in_dmin", np.uint32),
+    ("in_dmax", np.uint32), ("in_last", np.uint32), ("in_npresent", np.uint32), ("in_payload", np.uint32),
+    ("rk_sum_compute", np.uint64), ("rk_sum_wait", np.uint64), ("rk_sum_transfer", np.uint64),
+    ("cl_J", np.uint32), ("cl_mismatch", np.uint8),
+    ("wd_total", np.uint32), ("wd_slow", np.uint32), ("wd_cand", np.uint8), ("wd_frac", np.float64),
+    ("wl_joined", np.uint32), ("wl_late", np.uint32), ("wl_late_frac", np.float64), ("wl_verdict", np.uint8),
+    ("wl_link_slow", np.uint8),
+    ("lk_window", np.uint32), ("lk_src", np.uint32), ("lk_dst", np.uint32), ("lk_n", np.uint32),
+    ("lk_med_payload", np.uint32), ("lk_med_transfer", np.uint32), ("lk_used_warm", np.uint8), ("lk_slow", np.uint8),
+    ("lk_dir", np.uint8), ("lk_eligible", np.uint8), ("lk_med_bw", np.float64),
+    ("lb_label", np.uint8), ("lb_root_kind", np.uint8), ("lb_root_rank", np.uint32), ("lb_root_src", np.uint32),
+    ("lb_depth", np.uint32), ("lb_total_wait", np.uint64),
+    ("eg_window", np.uint32), ("eg_src", np.uint32), ("eg_dst", np.uint32), ("eg_weight", np.uint64),
+    ("comm_inst", np.uint32), ("comm_wait", np.uint32), ("slow_bits", np.uint32),
+]
+OUT_INDEX = {n: i for i, (n, _) in enumerate(OUTPUTS)}
+OUT_DTYPE = dict(OUTPUTS)
+
+
+class ScanError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Topo(ctypes.Structure):
+    _fields_ = [("tp", ctypes.c_int32), ("pp", ctypes.c_int32), ("dp", ctypes.c_int32), ("rank_order", ctypes.c_uint32)]
+
+
+class _Comms(ctypes.Structure):
+    _fields_ = [("n_comms", ctypes.c_uint32), ("offsets", ctypes.c_void_p), ("members", ctypes.c_void_p)]
+
+
+class _Cols(ctypes.Structure):
+    _fields_ = [("n_events", ctypes.c_uint64), ("rank_offsets", ctypes.c_void_p), ("start_ns", ctypes.c_void_p),
+                ("dur_ns", ctypes.c_void_p), ("kind_op", ctypes.c_void_p), ("meta", ctypes.c_void_p),
+                ("comm", ctypes.c_void_p), ("payload_bytes", ctypes.c_void_p)]
+
+
+class _MatchRes(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in ("n_events", "n_comm_events", "n_compute_events", "n_channels",
+                                               "n_p2p_channels", "n_instances", "n_incomplete", "n_kind_mismatch",
+                                               "n_payload_mismatch", "n_iters")]
+
+
+class _DetectCfg(ctypes.Structure):
+    _fields_ = [("slow_num", ctypes.c_uint32), ("slow_den", ctypes.c_uint32), ("slow_margin_ns", ctypes.c_uint64),
+                ("cand_num", ctypes.c_uint32), ("cand_den", ctypes.c_uint32), ("min_samples", ctypes.c_uint32),
+                ("window_iters", ctypes.c_uint32), ("want_ref", ctypes.c_uint32), ("pad", ctypes.c_uint32)]
+
+
+class _DetectRes(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in ("n_windows", "n_compared", "n_slow", "n_candidates", "n_class_mismatch")]
+
+
+class _LocCfg(ctypes.Structure):
+    _fields_ = [("late_margin_ns", ctypes.c_uint64), ("late_num", ctypes.c_uint32), ("late_den", ctypes.c_uint32),
+                ("bw_num", ctypes.c_uint32), ("bw_den", ctypes.c_uint32), ("min_samples", ctypes.c_uint32),
+                ("stage2_classes", ctypes.c_uint32), ("stage2_mode", ctypes.c_uint32), ("pad", ctypes.c_uint32),
+                ("wait_margin_ns", ctypes.c_uint64)]
+
+
+class _LocRes(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in ("n_windows", "n_links", "n_link_slow", "n_compute_slow",
+                                               "n_link_slow_ranks", "n_both", "n_exonerated", "n_insufficient",
+                                               "n_roots", "n_victims", "n_unattributed", "n_edges")]
+
+
+_lib = None
+
+
+def library_path() -> str:
+    return _build.SO
+
+
+def _load_lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_build.SO) or _build.stale():
+        _build.build()
+    lib = ctypes.CDLL(_build.SO)
+    P = ctypes.c_void_p
+    lib.scan_create.argtypes = [ctypes.POINTER(P), ctypes.c_int, P]
+    lib.scan_destroy.argtypes = [P]
+    lib.scan_last_error.argtypes = [P]
+    lib.scan_last_error.restype = ctypes.c_char_p
+    lib.scan_load_events.argtypes = [P, ctypes.POINTER(_Topo), ctypes.POINTER(_Comms), ctypes.POINTER(_Cols), ctypes.c_uint32]
+    lib.scan_match_collectives.argtypes = [P, ctypes.POINTER(_MatchRes)]
+    lib.scan_detect.argtypes = [P, ctypes.POINTER(_DetectCfg), ctypes.POINTER(_DetectRes)]
+    lib.scan_localize.argtypes = [P, ctypes.POINTER(_LocCfg), ctypes.POINTER(_LocRes)]
+    lib.scan_output_size.argtypes = [P, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]
+    lib.scan_export.argtypes = [P, ctypes.c_int, P, ctypes.c_uint64, ctypes.c_int]
+    lib.scan_output_device_ptr.argtypes = [P, ctypes.c_int]
+    lib.scan_output_device_ptr.restype = P
+    lib.scan_kernel_launches.argtypes = [P]
+    lib.scan_kernel_launches.restype = ctypes.c_uint64
+    lib.scan_set_timing.argtypes = [P, ctypes.c_int]
+    lib.scan_set_timing.restype = ctypes.c_int32
+    lib.scan_timing_reset.argtypes = [P]
+    lib.scan_kernel_timing.argtypes = [P, ctypes.c_int, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
+                                       ctypes.POINTER(ctypes.c_uint64)]
+    lib.scan_kernel_timing.restype = ctypes.c_int
+    for f in ("scan_create", "scan_load_events", "scan_match_collectives", "scan_detect", "scan_localize",
+              "scan_output_size", "scan_export"):
+        getattr(lib, f).restype = ctypes.c_int32
+    _lib = lib
+    return lib
+
+
+EXPORTED_SYMBOLS = ["scan_create", "scan_destroy", "scan_last_error", "scan_load_events", "scan_match_collectives",
+                    "scan_detect", "scan_localize", "scan_output_size", "scan_export", "scan_output_device_ptr",
+                    "scan_kernel_launches", "scan_set_timing", "scan_timing_reset", "scan_kernel_timing"]
+
+
+@dataclass
+class DetectConfig:
+    """Stage-1 thresholds (SPEC S:L294 defaults as exact rationals)."""
+    slow_num: int = 3
+    slow_den: int = 2
+    slow_margin_ns: int = 50_000
+    cand_num: int = 3
+    cand_den: int = 10
+    min_samples: int = 10
+    window_iters: int = 0
+    want_ref: bool = False
+
+
+@dataclass
+class LocalizeConfig:
+    """Stage-2/3 + walk thresholds."""
+    late_margin_ns: int = 100_000
+    late_num: int = 7
+    late_den: int = 10
+    bw_num: int = 7
+    bw_den: int = 10
+    min_samples: int = 10
+    stage2_classes: int = 3
+    stage2_mode: int = 0
+    wait_margin_ns: int = 100_000
+
+
+def _check(ctx, st):
+    if st < 0:
+        raise ScanError(st, _load_lib().scan_last_error(ctx).decode())
+    return st
+
+
+def _ptr(x):
+    """Pointer of a numpy array or a torch tensor (host or device)."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    return x.ctypes.data
+
+
+# ---- C-ABI mirrors ------------------------------------------------------------------------
+def scan_create(device: int = 0, stream: int | None = None):
+    lib = _load_lib()
+    h = ctypes.c_void_p()
+    st = lib.scan_create(ctypes.byref(h), device, stream)
+    if st < 0:
+        raise ScanError(st, "scan_create failed (no CUDA device?)")
+    return h
+
+
+def scan_load_events(ctx, tp, pp, dp, rank_offsets, comm_offsets, comm_members, dur, kind_op, meta, comm, payload,
+                     flags: int = SCAN_HOST_PTRS, keep: list | None = None):
+    lib = _load_lib()
+    ro = np.ascontiguousarray(rank_offsets, dtype=np.uint64)
+    co = np.ascontiguousarray(comm_offsets, dtype=np.uint64)
+    cm = np.ascontiguousarray(comm_members, dtype=np.uint32)
+    if keep is not None:
+        keep += [ro, co, cm]
+    topo = _Topo(tp, pp, dp, 0)
+    comms = _Comms(len(co) - 1, co.ctypes.data, cm.ctypes.data if len(cm) else None)
+    cols = _Cols(int(ro[-1]), ro.ctypes.data, None, _ptr(dur), _ptr(kind_op), _ptr(meta), _ptr(comm), _ptr(payload))
+    return _check(ctx, lib.scan_load_events(ctx, ctypes.byref(topo), ctypes.byref(comms), ctypes.byref(cols), flags))
+
+
+def scan_match_collectives(ctx) -> tuple[int, dict]:
+    r = _MatchRes()
+    st = _check(ctx, _load_lib().scan_match_collectives(ctx, ctypes.byref(r)))
+    return st, {n: getattr(r, n) for n, _ in r._fields_}
+
+
+def scan_detect(ctx, cfg: DetectConfig | None = None) -> dict:
+    cfg = cfg or DetectConfig()
+    c = _DetectCfg(cfg.slow_num, cfg.slow_den, cfg.slow_margin_ns, cfg.cand_num, cfg.cand_den, cfg.min_samples,
+                   cfg.window_iters, 1 if cfg.want_ref else 0, 0)
+    r = _DetectRes()
+    _check(ctx, _load_lib().scan_detect(ctx, ctypes.byref(c), ctypes.byref(r)))
+    return {n: getattr(r, n) for n, _ in r._fields_}
+
+
+def scan_localize(ctx, cfg: LocalizeConfig | None = None) -> dict:
+    cfg = cfg or LocalizeConfig()
+    c = _LocCfg(cfg.late_margin_ns, cfg.late_num, cfg.late_den, cfg.bw_num, cfg.bw_den, cfg.min_samples,
+                cfg.stage2_classes, cfg.stage2_mode, 0, cfg.wait_margin_ns)
+    r = _LocRes()
+    _check(ctx, _load_lib().scan_localize(ctx, ctypes.byref(c), ctypes.byref(r)))
+    return {n: getattr(r, n) for n, _ in r._fields_}
+
+
+def scan_export(ctx, name: str) -> np.ndarray:
+    lib = _load_lib()
+    idx = OUT_INDEX[name]
+    nb = ctypes.c_uint64()
+    _check(ctx, lib.scan_output_size(ctx, idx, ctypes.byref(nb)))
+    dt = np.dtype(OUT_DTYPE[name])
+    out = np.empty(nb.value // dt.itemsize, dtype=dt)
+    if nb.value:
+        _check(ctx, lib.scan_export(ctx, idx, out.ctypes.data, nb.value, 0))
+    return out
+
+
+def scan_destroy(ctx):
+    if ctx:
+        _load_lib().scan_destroy(ctx)
+
+
+# ---- convenience ----------------------------------------------------------------------------
+class Scan:
+    """One analysis context on one GPU. ``load`` accepts a trace with numpy host columns
+    (copied H2D by the library) or torch CUDA tensors (``device_ptrs=True``, zero-copy)."""
+
+    def __init__(self, device: int = 0, stream=None):
+        if stream is None:
+            try:
+                import torch
+                if torch.cuda.is_available():
+                    stream = torch.cuda.current_stream(device).cuda_stream
+            except Exception:
+                stream = None
+        self.ctx = scan_create(device, stream)
+        self._keep: list = []
+
+    def close(self):
+        if self.ctx:
+            scan_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def load(self, trace, device_ptrs: bool = False, strict: bool = False, cols: dict | None = None):
+        self._keep = [trace]
+        c = cols or {k: getattr(trace, k) for k in ("dur_ns", "kind_op", "meta", "comm", "payload")}
+        if not device_ptrs:
+            c = {k: np.ascontiguousarray(v) for k, v in c.items()}
+        self._keep.append(c)
+        flags = (SCAN_DEVICE_PTRS if device_ptrs else SCAN_HOST_PTRS) | (SCAN_STRICT if strict else 0)
+        return scan_load_events(self.ctx, trace.tp, trace.pp, trace.dp, trace.rank_offsets, trace.comm_offsets,
+                                trace.comm_members, c["dur_ns"], c["kind_op"], c["meta"], c["comm"], c["payload"],
+                                flags, keep=self._keep)
+
+    def match(self):
+        return scan_match_collectives(self.ctx)
+
+    def detect(self, cfg: DetectConfig | None = None):
+        return scan_detect(self.ctx, cfg)
+
+    def localize(self, cfg: LocalizeConfig | None = None):
+        return scan_localize(self.ctx, cfg)
+
+    def run(self, dcfg: DetectConfig | None = None, lcfg: LocalizeConfig | None = None) -> dict:
+        st, m = self.match()
+        d = self.detect(dcfg)
+        l_ = self.localize(lcfg)
+        return {"status": st, "match": m, "detect": d, "localize": l_}
+
+    def export(self, name: str) -> np.ndarray:
+        return scan_export(self.ctx, name)
+
+    def export_all(self, names=None) -> dict:
+        names = names or [n for n, _ in OUTPUTS if n not in ("comm_inst", "comm_wait", "slow_bits")]
+        return {n: self.export(n) for n in names}
+
+    def device_ptr(self, name: str) -> int:
+        return _load_lib().scan_output_device_ptr(self.ctx, OUT_INDEX[name]) or 0
+
+    def kernel_launches(self) -> int:
+        return int(_load_lib().scan_kernel_launches(self.ctx))
+
+    def set_timing(self, on: bool):
+        lib = _load_lib()
+        lib.scan_set_timing(self.ctx, 1 if on else 0)
+        lib.scan_timing_reset(self.ctx)
+
+    def kernel_timing(self) -> dict:
+        """{kernel name: (total ms, launches)} accumulated since set_timing(True)."""
+        lib = _load_lib()
+        n = lib.scan_kernel_timing(self.ctx, -1, None, None, None)
+        out = {}
+        for i in range(n):
+            nm, ms_, cnt = ctypes.c_char_p(), ctypes.c_double(), ctypes.c_uint64()
+            lib.scan_kernel_timing(self.ctx, i, ctypes.byref(nm), ctypes.byref(ms_), ctypes.byref(cnt))
+            out[nm.value.decode()] = (ms_.value, cnt.value)
+        return out

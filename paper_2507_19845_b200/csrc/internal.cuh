@@ -1,0 +1,283 @@
+// internal.cuh — context, device buffers and warp utilities of the megascan CUDA library.
+// Product code (sm_100a). Shares nothing with oracle/.
+#pragma once
+
+#include <cstdint>
+#include <cstddef>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "../../include/megascan/scan.h"
+
+namespace ms {
+
+constexpr uint32_t NONE32 = 0xFFFFFFFFu;
+constexpr int TILE_EV = 2048;   // events per warp tile (one rank, program order)
+constexpr int KCAP = 32;        // distinct channels per warp tile (one per lane)
+constexpr int RCAP = 256;       // distinct channels per rank
+constexpr int PCAP = 32;        // distinct P2P peers per rank
+constexpr int LINK_CAP = 16384; // samples per (window, link) held in shared memory for the median
+
+// ----------------------------------------------------------------------------- device buffers
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap && p) return cudaSuccess;
+    if (p) { cudaFree(p); p = nullptr; cap = 0; }
+    size_t b = bytes ? bytes : 16;
+    b = (b + 255) & ~size_t(255);
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e == cudaSuccess) cap = b;
+    return e;
+  }
+  void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+// Device counters written by kernels, read back once per call.
+struct Counters {
+  unsigned long long bad_event;      // atomicMin, ~0 = none
+  unsigned int bad_reason;
+  unsigned int overflow;             // bit0 tile keys, bit1 rank keys, bit2 p2p peers, bit3 link samples, bit4 link count
+  unsigned long long n_incomplete, n_kind_mismatch, n_payload_mismatch;
+  unsigned long long n_p2p;          // P2P channels
+  unsigned long long n_comm, n_comp; // totals
+  unsigned int max_niter;            // max iter_end count over ranks
+  unsigned int n_iters;              // max (iteration index of last event) + 1
+  unsigned long long n_instances, n_slots, p2p_slot0, p2p_inst0;
+  unsigned long long n_bits_words;
+  unsigned int max_ncomp;
+  unsigned int pad;
+  unsigned long long n_compared, n_slow, n_candidates, n_class_mismatch;
+  unsigned long long n_link_slow, n_roots, n_victims, n_unattributed;
+  unsigned long long v_count[6];
+  unsigned long long n_edges;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  uint64_t launches = 0;
+
+  // topology / inputs
+  int TP = 0, PP = 0, DP = 0, W = 0;
+  uint32_t n_comms = 0;
+  uint64_t N = 0;
+  bool loaded = false, matched = false, detected = false, localized = false;
+  uint32_t flags = 0;
+  std::vector<uint64_t> h_rank_off;
+  DevBuf own_dur, own_kind, own_meta, own_comm, own_pay;
+  const uint32_t* d_dur = nullptr; const uint16_t* d_kind = nullptr; const uint16_t* d_meta = nullptr;
+  const uint32_t* d_comm = nullptr; const uint32_t* d_pay = nullptr;
+  DevBuf rank_off;                 // u64 [W+1]
+  DevBuf coff, cmem, ccls;         // comm table (u64, u32) + stage-2 class per comm (u8)
+  DevBuf rcomm_off, rcomm;         // rank -> comms CSR (u32 offsets, u32)
+  DevBuf nbc_off, nbc;             // rank -> collective neighbours CSR (u64 offsets, u32)
+  uint64_t nnz_c = 0;
+  // tiles
+  uint64_t n_tiles = 0;
+  DevBuf tile_rank, tile_start, rank_tile0;  // u32, u64, u32 [W+1]
+  std::vector<uint32_t> h_rank_tile0;
+
+  // match workspaces
+  DevBuf t_nkeys, t_keys, t_cnt, t_pref, t_ncomm, t_niter, t_last, t_commpre, t_iterpre, t_prevj;
+  DevBuf r_nkeys, r_keys, r_cnt, r_ncomm, r_niter, r_ncomp, r_lastit;
+  DevBuf r_comm_off, r_comp_off, r_bits_off;          // u64 [W+1]
+  DevBuf bitmap, bitpre;                               // P2P channel bitmap (u32 words) + word prefix
+  uint64_t n_bm_words = 0;
+  DevBuf counters;                                     // Counters
+  Counters hc{};
+  DevBuf ch_nmax, ch_nmin, ch_base, ch_slot, ch_nsend, ch_nrecv;   // channels
+  uint64_t NCH = 0, n_p2p = 0, n_comm = 0, n_comp = 0, n_inst = 0, n_slots = 0, p2p_slot0 = 0, p2p_inst0 = 0;
+  uint32_t NIT = 0;        // citer row length - 1 (max iter_end count)
+  uint32_t n_iters = 0;
+  DevBuf inst_c, wait_c;                 // per comm event
+  DevBuf cdur, cop;                      // per compute event (rank-compacted)
+  DevBuf sdur, skind, p2p_pay, p2p_warm, p2p_iter;  // per slot / per P2P instance
+  DevBuf inst_rec;                       // uint4 per instance {dmin, dmax, last_rank, flags | cls<<8}
+  DevBuf citer;                          // u32 [W][NIT+1]
+  DevBuf nbp, nbp_n;                     // P2P neighbours per rank [W][PCAP]
+  DevBuf rk_sum;                         // u64 [3][W]
+
+  // detect
+  scan_detect_config dcfg{};
+  uint32_t NW = 1;
+  DevBuf bits, cref, cl_J, cl_max, cl_min;
+  DevBuf wd_total, wd_slow, wd_cand, wd_frac;
+  uint32_t max_ncomp = 0;
+  uint64_t n_bits_words = 0;
+
+  // localize
+  scan_localize_config lcfg{};
+  DevBuf wl_joined, wl_late, wl_frac, wl_verdict, wl_link_slow;
+  DevBuf ewc, ewp;                       // edge weights [NW][nnz_c], [NW][W*PCAP]
+  DevBuf lk_n, lk_used, lk_medp, lk_medt, lk_bw, lk_slow, lk_dir, lk_elig;
+  DevBuf lb_label, lb_rkind, lb_rrank, lb_rsrc, lb_depth, lb_twait;
+  DevBuf scratch;                        // export scratch
+
+  // optional per-kernel timing
+  bool timing = false;
+  struct Pending { int k; cudaEvent_t a, b; };
+  std::vector<Pending> pend;
+  std::vector<std::string> knames;
+  std::vector<double> kms;
+  std::vector<uint64_t> kcnt;
+  std::vector<cudaEvent_t> evpool;
+
+  bool fail(scan_status, const std::string& m) { err = m; return false; }
+};
+
+// Launch wrapper: records an event pair around a launcher when timing is on.
+template <class F>
+int timed(Ctx& c, const char* name, F&& f) {
+  if (!c.timing) return f();
+  int k = -1;
+  for (size_t i = 0; i < c.knames.size(); ++i) if (c.knames[i] == name) k = (int)i;
+  if (k < 0) { c.knames.push_back(name); c.kms.push_back(0); c.kcnt.push_back(0); k = (int)c.knames.size() - 1; }
+  cudaEvent_t a, b;
+  if (c.evpool.size() >= 2) { a = c.evpool.back(); c.evpool.pop_back(); b = c.evpool.back(); c.evpool.pop_back(); }
+  else { cudaEventCreate(&a); cudaEventCreate(&b); }
+  cudaEventRecord(a, c.stream);
+  int n = f();
+  cudaEventRecord(b, c.stream);
+  c.pend.push_back({k, a, b});
+  return n;
+}
+void resolve_timing(Ctx& c);
+
+// ----------------------------------------------------------------------------- device helpers
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t t = __shfl_up_sync(0xFFFFFFFFu, v, o);
+    if (lane_id() >= (uint32_t)o) v += t;
+  }
+  return v;
+}
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t& total) {
+  uint32_t inc = warp_incl_scan(v);
+  total = __shfl_sync(0xFFFFFFFFu, inc, 31);
+  return inc - v;
+}
+__device__ __forceinline__ int32_t warp_incl_max(int32_t v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int32_t t = __shfl_up_sync(0xFFFFFFFFu, v, o);
+    if (lane_id() >= (uint32_t)o) v = max(v, t);
+  }
+  return v;
+}
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
+  return __reduce_add_sync(0xFFFFFFFFu, v);
+}
+
+// 8 consecutive events starting at group index g (multiple of 8) — vectorised when in bounds.
+__device__ __forceinline__ void load8_u16(const uint16_t* __restrict__ p, uint64_t g, uint64_t n, uint16_t out[8]) {
+  if (g + 8 <= n) {
+    uint4 v = __ldg(reinterpret_cast<const uint4*>(p + g));
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int s = 0; s < 8; ++s) out[s] = (uint16_t)(w[s >> 1] >> ((s & 1) * 16));
+  } else {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) out[s] = (g + s < n) ? p[g + s] : 0;
+  }
+}
+__device__ __forceinline__ void load8_u32(const uint32_t* __restrict__ p, uint64_t g, uint64_t n, uint32_t out[8]) {
+  if (g + 8 <= n) {
+    uint4 a = __ldg(reinterpret_cast<const uint4*>(p + g));
+    uint4 b = __ldg(reinterpret_cast<const uint4*>(p + g + 4));
+    out[0] = a.x; out[1] = a.y; out[2] = a.z; out[3] = a.w;
+    out[4] = b.x; out[5] = b.y; out[6] = b.z; out[7] = b.w;
+  } else {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) out[s] = (g + s < n) ? p[g + s] : 0;
+  }
+}
+
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t n, uint32_t x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) { uint32_t m = (lo + hi) >> 1; if (a[m] < x) lo = m + 1; else hi = m; }
+  return lo;
+}
+// index of the last element <= x in a sorted u64 array of length n (a[0] <= x assumed)
+__device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* a, uint64_t n, uint64_t x) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) { uint64_t m = (lo + hi) >> 1; if (a[m] <= x) lo = m + 1; else hi = m; }
+  return lo;
+}
+
+// exact ratio order p_a/t_a < p_b/t_b  (t > 0)
+__device__ __forceinline__ bool ratio_less(uint32_t pa, uint32_t ta, uint32_t pb, uint32_t tb) {
+  return (unsigned long long)pa * tb < (unsigned long long)pb * ta;
+}
+
+// ----------------------------------------------------------------------------- block scans
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_sum(uint32_t v, uint32_t& total, uint32_t* sm /*[32]*/) {
+  const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+  uint32_t inc = warp_incl_scan(v);
+  if (lane == 31) sm[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t x = lane < NT / 32 ? sm[lane] : 0;
+    uint32_t xi = warp_incl_scan(x);
+    sm[lane] = xi - x;
+    if (lane == 31) sm[32] = xi;
+  }
+  __syncthreads();
+  uint32_t r = sm[wid] + inc - v;
+  total = sm[32];
+  __syncthreads();
+  return r;
+}
+template <int NT>
+__device__ __forceinline__ int32_t block_excl_max(int32_t v, int32_t& total, int32_t* sm /*[33]*/) {
+  const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+  int32_t inc = warp_incl_max(v);
+  int32_t ex = __shfl_up_sync(0xFFFFFFFFu, inc, 1);
+  if (lane == 0) ex = INT32_MIN;
+  if (lane == 31) sm[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int32_t x = lane < NT / 32 ? sm[lane] : INT32_MIN;
+    int32_t xi = warp_incl_max(x);
+    int32_t xe = __shfl_up_sync(0xFFFFFFFFu, xi, 1);
+    sm[lane] = lane == 0 ? INT32_MIN : xe;
+    if (lane == 31) sm[32] = xi;
+  }
+  __syncthreads();
+  int32_t r = max(sm[wid], ex);
+  total = sm[32];
+  __syncthreads();
+  return r;
+}
+
+// ----------------------------------------------------------------------------- kernel launchers
+// (each returns the number of kernel launches it enqueued)
+int launch_tile_scan(Ctx& c);
+int launch_rank_scan(Ctx& c);
+int launch_rank_prefix(Ctx& c);
+int launch_p2p_channels(Ctx& c);
+int launch_assign(Ctx& c);
+int launch_inst_reduce(Ctx& c);
+int launch_stage1(Ctx& c);
+int launch_stage1_counts(Ctx& c);
+int launch_event_pass(Ctx& c);
+int launch_links(Ctx& c);
+int launch_verdict_walk(Ctx& c);
+// exports
+int launch_expand_events(Ctx& c, scan_output which, void* dst);
+int launch_instance_export(Ctx& c, scan_output which, void* dst);
+
+}  // namespace ms

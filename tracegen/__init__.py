@@ -145,7 +145,7 @@ def _ptr(a):
     return None if a is None else a.ctypes.data
 
 
-def generate(cfg: GenConfig, ground_truth: bool = False, out: dict | None = None) -> Trace:
+def generate(cfg: GenConfig, ground_truth: bool = False, out: dict | None = None, with_start: bool = True) -> Trace:
     """Run the DES. ``out`` may supply preallocated (e.g. pinned) column arrays."""
     lib = _load()
     c, keep = _cfg_struct(cfg)
@@ -158,7 +158,7 @@ def generate(cfg: GenConfig, ground_truth: bool = False, out: dict | None = None
     lib.gen_comm_table(ctypes.byref(c), coff.ctypes.data, mem.ctypes.data if len(mem) else None)
     out = out or {}
     cols = {
-        "start_ns": out.get("start_ns", np.empty(n, dtype=np.int64)),
+        "start_ns": out.get("start_ns", np.empty(n, dtype=np.int64)) if with_start else None,
         "dur_ns": out.get("dur_ns", np.empty(n, dtype=np.uint32)),
         "kind_op": out.get("kind_op", np.empty(n, dtype=np.uint16)),
         "meta": out.get("meta", np.empty(n, dtype=np.uint16)),
