@@ -153,8 +153,8 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--iters", type=int, default=None, help="override the config's iteration count")
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--cpu-iters", type=int, default=40, help="oracle sample (iterations) for cpu_baseline")
-    ap.add_argument("--ref-iters", type=int, default=10, help="oracle sample per step for --impl reference")
+    ap.add_argument("--cpu-iters", type=int, default=16, help="oracle sample (iterations) for cpu_baseline")
+    ap.add_argument("--ref-iters", type=int, default=4, help="oracle sample per step for --impl reference")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--breakdown", action="store_true", default=True)

@@ -79,7 +79,8 @@ __global__ void __launch_bounds__(256) k_tile_scan(TileArgs a, uint32_t* t_nkeys
     }
     ncomm += warp_sum_u32(__popc(pending));
     niter += warp_sum_u32(__popc(itm));
-    last = max(last, __reduce_max_sync(0xFFFFFFFFu, (unsigned)(mylast + 1)) - 1);
+    const int32_t round_last = (int32_t)__reduce_max_sync(0xFFFFFFFFu, (unsigned)(mylast + 1)) - 1;
+    last = max(last, round_last);
     // count per distinct key (one iteration per distinct key in this round)
     while (__any_sync(0xFFFFFFFFu, pending != 0)) {
       const uint32_t leader = __ffs(__ballot_sync(0xFFFFFFFFu, pending != 0)) - 1;
