@@ -192,9 +192,7 @@ def main():
     s.load(tr, device_ptrs=True, cols=dev)
 
     def step():
-        s.match()
-        s.detect()
-        s.localize()
+        s.analyze()
 
     for _ in range(args.warmup):
         step()
@@ -226,6 +224,7 @@ def main():
         kernels = s.kernel_timing()
         s.set_timing(False)
     # verdicts for the record
+    fused = bool(s.analyze()["fused"])
     verdict = s.export("wl_verdict")
     flagged = {int(r): int(v) for r, v in enumerate(verdict) if v}
 
@@ -239,9 +238,7 @@ def main():
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             s2.load(tr)
-            s2.match()
-            s2.detect()
-            s2.localize()
+            s2.analyze()
             out_v = s2.export("wl_verdict")
             out_l = s2.export("lb_label")
             times.append(time.perf_counter() - t0)
@@ -295,6 +292,7 @@ def main():
         "gpu_launches": int(launches) * args.steps,
         "clocks": clk.summary(),
         "verdicts": {"flagged": flagged},
+        "path": "fused SPMD stage-tile pass (K9)" if fused else "general path",
     }
     print(json.dumps(line), flush=True)
     if dist:

@@ -181,6 +181,20 @@ scan_status scan_detect(scan_ctx* ctx, const scan_detect_config* cfg, scan_detec
    preceding scan_detect. Requires detect (else SCAN_E_ORDER). cfg NULL = defaults.            */
 scan_status scan_localize(scan_ctx* ctx, const scan_localize_config* cfg, scan_localize_result* out);
 
+/* A1-A8 in one call: equivalent to scan_match_collectives + scan_detect + scan_localize with the
+   given configs (NULL = defaults) and the same outputs. When every pipeline-stage block of the
+   trace is SPMD (equal per-rank event counts, same communicator roles; checked at load) it runs
+   the fused stage-tile pass (K9): one streaming read of the event columns, every event
+   verified against its stage template; if any event fails verification the call transparently
+   reruns the general path, so results never depend on the SPMD assumption. Returns as
+   scan_match_collectives. Any of the result pointers may be NULL.                              */
+scan_status scan_analyze(scan_ctx* ctx, const scan_detect_config* dcfg, const scan_localize_config* lcfg,
+                         scan_match_result* mres, scan_detect_result* dres, scan_localize_result* lres);
+/* 1 if the last scan_analyze used the fused path, 0 if it ran the general path.                 */
+int scan_used_fused(const scan_ctx* ctx);
+/* Disable (1) / re-enable (0) the fused path for this context (testing / comparison).          */
+scan_status scan_force_general(scan_ctx* ctx, int force);
+
 /* ---- result export ------------------------------------------------------------------------ */
 typedef enum scan_output {
     /* per event, event order (expanded from the compact native layouts) */

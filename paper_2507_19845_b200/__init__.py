@@ -132,8 +132,13 @@ def _load_lib():
     lib.scan_kernel_timing.argtypes = [P, ctypes.c_int, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
                                        ctypes.POINTER(ctypes.c_uint64)]
     lib.scan_kernel_timing.restype = ctypes.c_int
+    lib.scan_analyze.argtypes = [P, ctypes.POINTER(_DetectCfg), ctypes.POINTER(_LocCfg), ctypes.POINTER(_MatchRes),
+                                 ctypes.POINTER(_DetectRes), ctypes.POINTER(_LocRes)]
+    lib.scan_used_fused.argtypes = [P]
+    lib.scan_used_fused.restype = ctypes.c_int
+    lib.scan_force_general.argtypes = [P, ctypes.c_int]
     for f in ("scan_create", "scan_load_events", "scan_match_collectives", "scan_detect", "scan_localize",
-              "scan_output_size", "scan_export"):
+              "scan_output_size", "scan_export", "scan_analyze", "scan_force_general"):
         getattr(lib, f).restype = ctypes.c_int32
     _lib = lib
     return lib
@@ -141,7 +146,8 @@ def _load_lib():
 
 EXPORTED_SYMBOLS = ["scan_create", "scan_destroy", "scan_last_error", "scan_load_events", "scan_match_collectives",
                     "scan_detect", "scan_localize", "scan_output_size", "scan_export", "scan_output_device_ptr",
-                    "scan_kernel_launches", "scan_set_timing", "scan_timing_reset", "scan_kernel_timing"]
+                    "scan_kernel_launches", "scan_set_timing", "scan_timing_reset", "scan_kernel_timing",
+                    "scan_analyze", "scan_used_fused", "scan_force_general"]
 
 
 @dataclass
@@ -234,6 +240,28 @@ def scan_localize(ctx, cfg: LocalizeConfig | None = None) -> dict:
     return {n: getattr(r, n) for n, _ in r._fields_}
 
 
+def _dcfg(cfg):
+    cfg = cfg or DetectConfig()
+    return _DetectCfg(cfg.slow_num, cfg.slow_den, cfg.slow_margin_ns, cfg.cand_num, cfg.cand_den, cfg.min_samples,
+                      cfg.window_iters, 1 if cfg.want_ref else 0, 0)
+
+
+def _lcfg(cfg):
+    cfg = cfg or LocalizeConfig()
+    return _LocCfg(cfg.late_margin_ns, cfg.late_num, cfg.late_den, cfg.bw_num, cfg.bw_den, cfg.min_samples,
+                   cfg.stage2_classes, cfg.stage2_mode, 0, cfg.wait_margin_ns)
+
+
+def scan_analyze(ctx, dcfg: DetectConfig | None = None, lcfg: LocalizeConfig | None = None) -> dict:
+    """A1-A8 in one call (fused SPMD stage-tile pass when applicable, else the general path)."""
+    m, d, l_ = _MatchRes(), _DetectRes(), _LocRes()
+    st = _check(ctx, _load_lib().scan_analyze(ctx, ctypes.byref(_dcfg(dcfg)), ctypes.byref(_lcfg(lcfg)), ctypes.byref(m),
+                                              ctypes.byref(d), ctypes.byref(l_)))
+    return {"status": st, "match": {n: getattr(m, n) for n, _ in m._fields_},
+            "detect": {n: getattr(d, n) for n, _ in d._fields_}, "localize": {n: getattr(l_, n) for n, _ in l_._fields_},
+            "fused": bool(_load_lib().scan_used_fused(ctx))}
+
+
 def scan_export(ctx, name: str) -> np.ndarray:
     lib = _load_lib()
     idx = OUT_INDEX[name]
@@ -303,6 +331,12 @@ class Scan:
         d = self.detect(dcfg)
         l_ = self.localize(lcfg)
         return {"status": st, "match": m, "detect": d, "localize": l_}
+
+    def analyze(self, dcfg: DetectConfig | None = None, lcfg: LocalizeConfig | None = None) -> dict:
+        return scan_analyze(self.ctx, dcfg, lcfg)
+
+    def force_general(self, on: bool = True):
+        _check(self.ctx, _load_lib().scan_force_general(self.ctx, 1 if on else 0))
 
     def export(self, name: str) -> np.ndarray:
         return scan_export(self.ctx, name)

@@ -135,6 +135,7 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
   Ctx& c = ctx->c;
   CK(cudaSetDevice(c.device));
   c.loaded = c.matched = c.detected = c.localized = false;
+  c.fused_used = false; c.tiles_ready = false;
   c.err.clear();
   if (topo->tp < 1 || topo->pp < 1 || topo->dp < 1 || topo->rank_order != 0) {
     c.err = "topology: tp, pp, dp must be >= 1 and rank_order 0";
@@ -220,6 +221,50 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
       (st = upload(c, c.nbc_off, nbo)) || (st = upload(c, c.nbc, nb)) || (st = upload(c, c.tile_rank, trank)) ||
       (st = upload(c, c.tile_start, tstart)) || (st = upload(c, c.rank_tile0, rt0)))
     return st;
+  // fused-path (K9) tables: every stage block SPMD-compatible? role -> communicator / slot
+  {
+    c.spmd = false;
+    const uint32_t R = (uint32_t)(topo->tp * topo->dp);
+    bool ok = N > 0 && R <= 256;
+    std::vector<uint32_t> rcmm((size_t)W * CROLES, NONE32), rslt((size_t)W * CROLES, NONE32), ncr(topo->pp, 0);
+    std::vector<uint8_t> rty((size_t)topo->pp * ROLES, 0);
+    std::vector<uint32_t> stt0(topo->pp + 1, 0), stnp(topo->pp, 0);
+    bool aligned = true;
+    for (int r = 0; r < W; ++r) aligned &= (ro[r] % 4) == 0;
+    for (int s = 0; ok && s < topo->pp; ++s) {
+      const uint32_t r0 = s * R;
+      const uint64_t ns = ro[r0 + 1] - ro[r0];
+      if (rcl[r0].size() > (size_t)CROLES) { ok = false; break; }
+      ncr[s] = (uint32_t)rcl[r0].size();
+      for (uint32_t q = 0; q < ncr[s]; ++q) {
+        const uint8_t k = ccls[rcl[r0][q]];
+        rty[s * ROLES + q] = k == 1 ? 1 : (k == 2 ? 2 : 3);
+      }
+      for (uint32_t r = r0; ok && r < r0 + R; ++r) {
+        if (ro[r + 1] - ro[r] != ns || rcl[r].size() != ncr[s]) { ok = false; break; }
+        for (uint32_t q = 0; q < ncr[s]; ++q) {
+          const uint32_t k = rcl[r][q];
+          if (ccls[k] != ccls[rcl[r0][q]]) { ok = false; break; }
+          rcmm[(size_t)r * CROLES + q] = k;
+          rslt[(size_t)r * CROLES + q] = (uint32_t)(std::lower_bound(cmem.begin() + coff[k], cmem.begin() + coff[k + 1], r) -
+                                                    (cmem.begin() + coff[k]));
+        }
+      }
+      stnp[s] = (uint32_t)ns;
+    }
+    if (ok) {
+      uint32_t T = (16384u / R) / 32u * 32u;
+      T = std::max(64u, std::min(1024u, T));
+      uint32_t nt = 0;
+      for (int s = 0; s < topo->pp; ++s) { stt0[s] = nt; nt += (stnp[s] + T - 1) / T; }
+      stt0[topo->pp] = nt;
+      c.FT = T; c.FR = R; c.n_ftiles = nt; c.h_st_tile0 = stt0; c.h_st_npos = stnp; c.rows_aligned = aligned;
+      if ((st = upload(c, c.st_tile0, stt0)) || (st = upload(c, c.st_npos, stnp)) || (st = upload(c, c.role_comm, rcmm)) ||
+          (st = upload(c, c.role_slot, rslt)) || (st = upload(c, c.role_type, rty)) || (st = upload(c, c.ncroles, ncr)))
+        return st;
+      c.spmd = nt > 0;
+    }
+  }
   // event columns
   if (flags & SCAN_DEVICE_PTRS) {
     const void* ptrs[] = {cols->dur_ns, cols->kind_op, cols->meta, cols->comm, cols->payload_bytes};
@@ -244,18 +289,22 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
   return SCAN_OK;
 }
 
-// ----------------------------------------------------------------------------- A1-A3 match
-scan_status scan_match_collectives(scan_ctx* ctx, scan_match_result* out) {
-  if (!ctx) return SCAN_E_INVALID_ARG;
-  Ctx& c = ctx->c;
-  if (!c.loaded) { c.err = "scan_match_collectives before scan_load_events"; return SCAN_E_ORDER; }
-  CK(cudaSetDevice(c.device));
-  c.matched = c.detected = c.localized = false;
-  c.launches = 0;
+// ----------------------------------------------------------------------------- shared stages
+}  // extern "C"
+
+namespace {
+
+const scan_detect_config kDefDetect{3, 2, 50000, 3, 10, 10, 0, 0, 0};
+const scan_localize_config kDefLocalize{100000, 7, 10, 7, 10, 10, 3, 0, 0, 100000};
+
+// per-rank / channel workspaces and counter reset (both paths)
+scan_status prep_ws(Ctx& c, bool tiles) {
   const uint64_t T = std::max<uint64_t>(c.n_tiles, 1), W = c.W;
-  CK(c.t_nkeys.ensure(T * 4)); CK(c.t_keys.ensure(T * KCAP * 4)); CK(c.t_cnt.ensure(T * KCAP * 4));
-  CK(c.t_pref.ensure(T * KCAP * 4)); CK(c.t_ncomm.ensure(T * 4)); CK(c.t_niter.ensure(T * 4)); CK(c.t_last.ensure(T * 4));
-  CK(c.t_commpre.ensure(T * 4)); CK(c.t_iterpre.ensure(T * 4)); CK(c.t_prevj.ensure(T * 4));
+  if (tiles) {
+    CK(c.t_nkeys.ensure(T * 4)); CK(c.t_keys.ensure(T * KCAP * 4)); CK(c.t_cnt.ensure(T * KCAP * 4));
+    CK(c.t_pref.ensure(T * KCAP * 4)); CK(c.t_ncomm.ensure(T * 4)); CK(c.t_niter.ensure(T * 4)); CK(c.t_last.ensure(T * 4));
+    CK(c.t_commpre.ensure(T * 4)); CK(c.t_iterpre.ensure(T * 4)); CK(c.t_prevj.ensure(T * 4));
+  }
   CK(c.r_nkeys.ensure(W * 4)); CK(c.r_keys.ensure(W * RCAP * 4)); CK(c.r_cnt.ensure(W * RCAP * 4));
   CK(c.r_ncomm.ensure(W * 4)); CK(c.r_niter.ensure(W * 4)); CK(c.r_ncomp.ensure(W * 4));
   CK(c.r_comm_off.ensure((W + 1) * 8)); CK(c.r_comp_off.ensure((W + 1) * 8)); CK(c.r_bits_off.ensure((W + 1) * 8));
@@ -270,25 +319,30 @@ scan_status scan_match_collectives(scan_ctx* ctx, scan_match_result* out) {
   CK(cudaMemsetAsync(c.ch_nmax.p, 0, ch_cap * 4, c.stream));
   CK(cudaMemsetAsync(c.ch_nmin.p, 0xFF, ch_cap * 4, c.stream));
   CK(cudaMemsetAsync(c.bitmap.p, 0, c.n_bm_words * 4, c.stream));
-  c.launches += timed(c, "k_tile_scan", [&] { return launch_tile_scan(c); });
-  c.launches += timed(c, "k_rank_scan", [&] { return launch_rank_scan(c); });
-  c.launches += timed(c, "k_rank_prefix", [&] { return launch_rank_prefix(c); });
+  return SCAN_OK;
+}
+
+// after the per-rank census (general: k_rank_scan, fused: k_fused_census) + k_rank_prefix:
+// read totals, build channel bases, allocate the per-event / per-instance buffers.
+scan_status channels_and_buffers(Ctx& c, bool fused) {
   scan_status st = sync_read(c);
   if (st) return st;
+  if (fused && (c.hc.overflow & 32u)) return 2;  // not SPMD: caller falls back
   if (c.hc.bad_event != ~0ull) {
     std::ostringstream m;
     m << "schema error at event " << c.hc.bad_event << " (kind > 6, comm id out of range, rank not a member, or bad peer)";
     c.err = m.str();
     return SCAN_E_SCHEMA;
   }
-  if (c.hc.overflow) {
+  if (c.hc.overflow & 7u) {
+    if (fused) return 2;
     c.err = "capacity exceeded: " + std::string((c.hc.overflow & 1) ? "more than 32 channels in a 2048-event tile " : "") +
             ((c.hc.overflow & 2) ? "more than 256 channels on a rank " : "") + ((c.hc.overflow & 4) ? "more than 32 P2P peers on a rank" : "");
     return SCAN_E_UNSUPPORTED;
   }
+  const uint64_t W = c.W;
   c.n_p2p = c.hc.n_p2p; c.NCH = c.n_comms + c.n_p2p; c.n_comm = c.hc.n_comm; c.n_comp = c.hc.n_comp;
   c.NIT = c.hc.max_niter; c.n_iters = c.hc.n_iters; c.max_ncomp = c.hc.max_ncomp; c.n_bits_words = c.hc.n_bits_words;
-  // channels
   CK(c.ch_base.ensure((c.NCH + 1) * 8)); CK(c.ch_slot.ensure((c.NCH + 1) * 8));
   CK(c.ch_nsend.ensure(std::max<uint64_t>(2 * c.n_p2p, 1) * 4)); CK(c.ch_nrecv.ensure(std::max<uint64_t>(2 * c.n_p2p, 1) * 4));
   if (c.n_p2p) {
@@ -299,88 +353,35 @@ scan_status scan_match_collectives(scan_ctx* ctx, scan_match_result* out) {
   if ((st = sync_read(c))) return st;
   if (c.hc.n_instances >= 0xFFFFFFFFull) { c.err = "more than 2^32-1 instances"; return SCAN_E_UNSUPPORTED; }
   c.n_inst = c.hc.n_instances; c.n_slots = c.hc.n_slots; c.p2p_slot0 = c.hc.p2p_slot0; c.p2p_inst0 = c.hc.p2p_inst0;
-  // per-event / per-slot / per-instance buffers
   CK(c.inst_c.ensure(c.n_comm * 4)); CK(c.wait_c.ensure(c.n_comm * 4));
-  CK(c.cdur.ensure(c.n_comp * 4)); CK(c.cop.ensure(c.n_comp * 2));
+  if (!fused) { CK(c.cdur.ensure(c.n_comp * 4)); CK(c.cop.ensure(c.n_comp * 2)); }
   CK(c.sdur.ensure(c.n_slots * 4)); CK(c.skind.ensure(c.n_slots));
+  if (fused) { CK(c.sci.ensure(c.n_slots * 4)); CK(c.sit.ensure(c.n_slots * 4)); }
   const uint64_t np_slots = c.n_slots - c.p2p_slot0, np_inst = c.n_inst - c.p2p_inst0;
   CK(c.p2p_pay.ensure(np_slots * 4)); CK(c.p2p_warm.ensure(np_inst)); CK(c.p2p_iter.ensure(np_inst * 4));
   CK(c.inst_rec.ensure(c.n_inst * 16));
   const uint32_t NIT1 = c.NIT + 1;
-  CK(c.citer.ensure((uint64_t)W * NIT1 * 4));
+  CK(c.citer.ensure(W * NIT1 * 4));
   if (np_inst) CK(cudaMemsetAsync(c.p2p_warm.p, 0, np_inst, c.stream));
-  {
-    const uint64_t n = (uint64_t)W * NIT1;
-    k_citer_fill<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(c.W, NIT1, c.r_ncomp.as<uint32_t>(), c.citer.as<uint32_t>());
-    c.launches += 1;
-  }
-  c.launches += timed(c, "k_assign", [&] { return launch_assign(c); });
-  c.launches += timed(c, "k_inst_reduce", [&] { return launch_inst_reduce(c); });
-  if ((st = sync_read(c))) return st;
-  c.matched = true;
-  if (out) {
-    out->n_events = c.N; out->n_comm_events = c.n_comm; out->n_compute_events = c.n_comp;
-    out->n_channels = c.NCH; out->n_p2p_channels = c.n_p2p; out->n_instances = c.n_inst;
-    out->n_incomplete = c.hc.n_incomplete; out->n_kind_mismatch = c.hc.n_kind_mismatch;
-    out->n_payload_mismatch = c.hc.n_payload_mismatch; out->n_iters = c.n_iters;
-  }
-  const bool reports = c.hc.n_incomplete || c.hc.n_kind_mismatch || c.hc.n_payload_mismatch;
-  if (reports && (c.flags & SCAN_STRICT)) { c.err = "integrity: unmatched or inconsistent instances"; return SCAN_E_INTEGRITY; }
-  return reports ? SCAN_PARTIAL : SCAN_OK;
+  const uint64_t n = W * NIT1;
+  k_citer_fill<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(c.W, NIT1, c.r_ncomp.as<uint32_t>(), c.citer.as<uint32_t>());
+  c.launches += 1;
+  return SCAN_OK;
 }
 
-// ----------------------------------------------------------------------------- A4 detect
-scan_status scan_detect(scan_ctx* ctx, const scan_detect_config* cfg, scan_detect_result* out) {
-  if (!ctx) return SCAN_E_INVALID_ARG;
-  Ctx& c = ctx->c;
-  if (!c.matched) { c.err = "scan_detect before scan_match_collectives"; return SCAN_E_ORDER; }
-  CK(cudaSetDevice(c.device));
-  c.detected = c.localized = false;
-  scan_detect_config d{3, 2, 50000, 3, 10, 10, 0, 0, 0};
-  if (cfg) d = *cfg;
-  if (d.slow_den == 0 || d.cand_den == 0) { c.err = "zero denominator"; return SCAN_E_INVALID_ARG; }
-  c.dcfg = d;
+scan_status alloc_detect(Ctx& c) {
+  const scan_detect_config& d = c.dcfg;
   c.NW = d.window_iters ? std::max<uint32_t>(1, (c.n_iters + d.window_iters - 1) / d.window_iters) : 1;
   const uint64_t ncl = (uint64_t)c.TP * c.PP, items = (uint64_t)c.NW * c.W;
   CK(c.bits.ensure(std::max<uint64_t>(c.n_bits_words, 1) * 4));
   CK(cudaMemsetAsync(c.bits.p, 0, std::max<uint64_t>(c.n_bits_words, 1) * 4, c.stream));
-  if (d.want_ref) { CK(c.cref.ensure(c.n_comp * 4)); CK(cudaMemsetAsync(c.cref.p, 0xFF, c.n_comp * 4, c.stream)); }
+  if (d.want_ref) { CK(c.cref.ensure(std::max<uint64_t>(c.n_comp, 1) * 4)); CK(cudaMemsetAsync(c.cref.p, 0xFF, c.n_comp * 4, c.stream)); }
   CK(c.cl_J.ensure(ncl * 4)); CK(c.cl_max.ensure(ncl * 4)); CK(c.cl_min.ensure(ncl * 4));
   CK(c.wd_total.ensure(items * 4)); CK(c.wd_slow.ensure(items * 4)); CK(c.wd_cand.ensure(items)); CK(c.wd_frac.ensure(items * 8));
-  Counters z = c.hc;
-  z.n_compared = z.n_slow = z.n_candidates = z.n_class_mismatch = 0;
-  CK(cudaMemcpyAsync(c.counters.p, &z, sizeof(Counters), cudaMemcpyHostToDevice, c.stream));
-  const int l1 = timed(c, "k_stage1", [&] { return launch_stage1(c); });
-  if (l1 < 0) { c.err = "stage 1: dp unsupported"; return SCAN_E_UNSUPPORTED; }
-  c.launches += l1;
-  c.launches += timed(c, "k_stage1_counts", [&] { return launch_stage1_counts(c); });
-  scan_status st = sync_read(c);
-  if (st) return st;
-  // class mismatch count (J != max count), read back the tiny class arrays
-  std::vector<uint32_t> J(ncl), mx(ncl);
-  CK(cudaMemcpy(J.data(), c.cl_J.p, ncl * 4, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(mx.data(), c.cl_max.p, ncl * 4, cudaMemcpyDeviceToHost));
-  uint64_t mism = 0;
-  if (c.DP >= 2) for (uint64_t i = 0; i < ncl; ++i) mism += J[i] != mx[i];
-  c.detected = true;
-  if (out) {
-    out->n_windows = c.NW; out->n_compared = c.hc.n_compared; out->n_slow = c.hc.n_slow;
-    out->n_candidates = c.hc.n_candidates; out->n_class_mismatch = mism;
-  }
   return SCAN_OK;
 }
 
-// ----------------------------------------------------------------------------- A5-A8 localize
-scan_status scan_localize(scan_ctx* ctx, const scan_localize_config* cfg, scan_localize_result* out) {
-  if (!ctx) return SCAN_E_INVALID_ARG;
-  Ctx& c = ctx->c;
-  if (!c.detected) { c.err = "scan_localize before scan_detect"; return SCAN_E_ORDER; }
-  CK(cudaSetDevice(c.device));
-  c.localized = false;
-  scan_localize_config L{100000, 7, 10, 7, 10, 10, 3, 0, 0, 100000};
-  if (cfg) L = *cfg;
-  if (L.late_den == 0 || L.bw_den == 0) { c.err = "zero denominator"; return SCAN_E_INVALID_ARG; }
-  c.lcfg = L;
+scan_status alloc_localize(Ctx& c) {
   const uint64_t items = (uint64_t)c.NW * c.W, nlk = (uint64_t)c.NW * c.n_p2p;
   const uint64_t nnz_tot = c.nnz_c + (uint64_t)c.W * PCAP;
   CK(c.wl_joined.ensure(items * 4)); CK(c.wl_late.ensure(items * 4)); CK(c.wl_frac.ensure(items * 8));
@@ -391,7 +392,7 @@ scan_status scan_localize(scan_ctx* ctx, const scan_localize_config* cfg, scan_l
   CK(c.lk_dir.ensure(nlk + 1)); CK(c.lk_elig.ensure(nlk + 1));
   CK(c.lb_label.ensure(items)); CK(c.lb_rkind.ensure(items)); CK(c.lb_rrank.ensure(items * 4));
   CK(c.lb_rsrc.ensure(items * 4)); CK(c.lb_depth.ensure(items * 4)); CK(c.lb_twait.ensure(items * 8));
-  CK(c.scratch.ensure((2 * items + c.NW + 2) * 4));
+  CK(c.scratch.ensure(std::max<size_t>(c.scratch.cap, (2 * items + c.NW + 2) * 4)));
   CK(cudaMemsetAsync(c.wl_joined.p, 0, items * 4, c.stream));
   CK(cudaMemsetAsync(c.wl_late.p, 0, items * 4, c.stream));
   CK(cudaMemsetAsync(c.wl_link_slow.p, 0, items, c.stream));
@@ -399,6 +400,84 @@ scan_status scan_localize(scan_ctx* ctx, const scan_localize_config* cfg, scan_l
   CK(cudaMemsetAsync(c.rk_sum.p, 0, 3ull * c.W * 8, c.stream));
   CK(cudaMemsetAsync(c.lk_slow.p, 0, nlk + 1, c.stream));
   CK(cudaMemsetAsync(c.scratch.as<uint32_t>() + 2 * items, 0, (c.NW + 2) * 4, c.stream));
+  return SCAN_OK;
+}
+
+void fill_match(Ctx& c, scan_match_result* out) {
+  if (!out) return;
+  out->n_events = c.N; out->n_comm_events = c.n_comm; out->n_compute_events = c.n_comp;
+  out->n_channels = c.NCH; out->n_p2p_channels = c.n_p2p; out->n_instances = c.n_inst;
+  out->n_incomplete = c.hc.n_incomplete; out->n_kind_mismatch = c.hc.n_kind_mismatch;
+  out->n_payload_mismatch = c.hc.n_payload_mismatch; out->n_iters = c.n_iters;
+}
+
+scan_status match_status(Ctx& c) {
+  const bool reports = c.hc.n_incomplete || c.hc.n_kind_mismatch || c.hc.n_payload_mismatch;
+  if (reports && (c.flags & SCAN_STRICT)) { c.err = "integrity: unmatched or inconsistent instances"; return SCAN_E_INTEGRITY; }
+  return reports ? SCAN_PARTIAL : SCAN_OK;
+}
+
+scan_status detect_tail(Ctx& c, scan_detect_result* out) {
+  const uint64_t ncl = (uint64_t)c.TP * c.PP;
+  std::vector<uint32_t> J(ncl), mx(ncl);
+  CK(cudaMemcpy(J.data(), c.cl_J.p, ncl * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(mx.data(), c.cl_max.p, ncl * 4, cudaMemcpyDeviceToHost));
+  uint64_t mism = 0;
+  if (c.DP >= 2) for (uint64_t i = 0; i < ncl; ++i) mism += J[i] != mx[i];
+  if (out) {
+    out->n_windows = c.NW; out->n_compared = c.hc.n_compared; out->n_slow = c.hc.n_slow;
+    out->n_candidates = c.hc.n_candidates; out->n_class_mismatch = mism;
+  }
+  return SCAN_OK;
+}
+
+void fill_localize(Ctx& c, scan_localize_result* out) {
+  if (!out) return;
+  out->n_windows = c.NW; out->n_links = (uint64_t)c.NW * c.n_p2p; out->n_link_slow = c.hc.n_link_slow;
+  out->n_compute_slow = c.hc.v_count[SCAN_V_COMPUTE_SLOW]; out->n_link_slow_ranks = c.hc.v_count[SCAN_V_LINK_SLOW];
+  out->n_both = c.hc.v_count[SCAN_V_BOTH]; out->n_exonerated = c.hc.v_count[SCAN_V_EXONERATED];
+  out->n_insufficient = c.hc.v_count[SCAN_V_INSUFFICIENT]; out->n_roots = c.hc.n_roots;
+  out->n_victims = c.hc.n_victims; out->n_unattributed = c.hc.n_unattributed; out->n_edges = 0;
+}
+
+// ---- the general path, stage by stage
+scan_status general_match(Ctx& c) {
+  c.matched = c.detected = c.localized = false;
+  scan_status st = prep_ws(c, true);
+  if (st) return st;
+  c.launches += timed(c, "k_tile_scan", [&] { return launch_tile_scan(c); });
+  c.launches += timed(c, "k_rank_scan", [&] { return launch_rank_scan(c); });
+  c.launches += timed(c, "k_rank_prefix", [&] { return launch_rank_prefix(c); });
+  c.tiles_ready = true;
+  c.fused_used = false;
+  if ((st = channels_and_buffers(c, false))) return st;
+  c.launches += timed(c, "k_assign", [&] { return launch_assign(c); });
+  c.launches += timed(c, "k_inst_reduce", [&] { return launch_inst_reduce(c); });
+  if ((st = sync_read(c))) return st;
+  c.matched = true;
+  return SCAN_OK;
+}
+
+scan_status general_detect(Ctx& c) {
+  c.detected = c.localized = false;
+  scan_status st = alloc_detect(c);
+  if (st) return st;
+  Counters z = c.hc;
+  z.n_compared = z.n_slow = z.n_candidates = z.n_class_mismatch = 0;
+  CK(cudaMemcpyAsync(c.counters.p, &z, sizeof(Counters), cudaMemcpyHostToDevice, c.stream));
+  const int l1 = timed(c, "k_stage1", [&] { return launch_stage1(c); });
+  if (l1 < 0) { c.err = "stage 1: dp unsupported"; return SCAN_E_UNSUPPORTED; }
+  c.launches += l1;
+  c.launches += timed(c, "k_stage1_counts", [&] { return launch_stage1_counts(c); });
+  if ((st = sync_read(c))) return st;
+  c.detected = true;
+  return SCAN_OK;
+}
+
+scan_status general_localize(Ctx& c) {
+  c.localized = false;
+  scan_status st = alloc_localize(c);
+  if (st) return st;
   Counters z = c.hc;
   z.n_link_slow = z.n_roots = z.n_victims = z.n_unattributed = 0;
   for (auto& v : z.v_count) v = 0;
@@ -406,20 +485,135 @@ scan_status scan_localize(scan_ctx* ctx, const scan_localize_config* cfg, scan_l
   c.launches += timed(c, "k_event_pass", [&] { return launch_event_pass(c); });
   c.launches += timed(c, "k_links", [&] { return launch_links(c); });
   c.launches += timed(c, "k_walk", [&] { return launch_verdict_walk(c); });
-  scan_status st = sync_read(c);
-  if (st) return st;
+  if ((st = sync_read(c))) return st;
   if (c.hc.overflow & 24u) {
     c.err = "capacity exceeded: more than 16384 samples on a link / links in a direction class";
     return SCAN_E_UNSUPPORTED;
   }
   c.localized = true;
-  if (out) {
-    out->n_windows = c.NW; out->n_links = nlk; out->n_link_slow = c.hc.n_link_slow;
-    out->n_compute_slow = c.hc.v_count[SCAN_V_COMPUTE_SLOW]; out->n_link_slow_ranks = c.hc.v_count[SCAN_V_LINK_SLOW];
-    out->n_both = c.hc.v_count[SCAN_V_BOTH]; out->n_exonerated = c.hc.v_count[SCAN_V_EXONERATED];
-    out->n_insufficient = c.hc.v_count[SCAN_V_INSUFFICIENT]; out->n_roots = c.hc.n_roots;
-    out->n_victims = c.hc.n_victims; out->n_unattributed = c.hc.n_unattributed; out->n_edges = 0;
+  return SCAN_OK;
+}
+
+// ---- the fused SPMD path (K9); returns 2 when the trace is not SPMD (caller falls back)
+scan_status fused_all(Ctx& c) {
+  c.matched = c.detected = c.localized = false;
+  scan_status st = prep_ws(c, false);
+  if (st) return st;
+  CK(c.ft_cols.ensure((uint64_t)FCOLS * c.n_ftiles * 4)); CK(c.ft_base.ensure((uint64_t)FCOLS * c.n_ftiles * 4));
+  CK(c.st_tot.ensure((uint64_t)c.PP * FCOLS * 4));
+  c.launches += timed(c, "k_fused_prepass", [&] { return launch_fused_prepass(c); });
+  c.launches += timed(c, "k_fused_census", [&] { return launch_fused_census(c); });
+  c.launches += timed(c, "k_rank_prefix", [&] { return launch_rank_prefix(c); });
+  c.tiles_ready = false;
+  if ((st = channels_and_buffers(c, true))) return st;
+  if ((st = alloc_detect(c)) || (st = alloc_localize(c))) return st;
+  CK(c.dlate.ensure((uint64_t)c.n_ftiles * ((c.FR + 31) / 32) * 4 + 4));
+  CK(cudaMemsetAsync(c.dlate.p, 0, (uint64_t)c.n_ftiles * ((c.FR + 31) / 32) * 4 + 4, c.stream));
+  CK(c.dinfo.ensure((uint64_t)c.n_ftiles * 16 + 16));
+  Counters z = c.hc;
+  z.n_compared = z.n_slow = z.n_candidates = z.n_class_mismatch = 0;
+  z.n_link_slow = z.n_roots = z.n_victims = z.n_unattributed = 0;
+  for (auto& v : z.v_count) v = 0;
+  CK(cudaMemcpyAsync(c.counters.p, &z, sizeof(Counters), cudaMemcpyHostToDevice, c.stream));
+  c.launches += timed(c, "k_class_counts", [&] { return launch_class_counts(c); });
+  c.launches += timed(c, "k_fused", [&] { return launch_fused(c); });
+  c.launches += timed(c, "k_cross_reduce", [&] { return launch_cross_reduce(c); });
+  c.launches += timed(c, "k_deferred", [&] { return launch_deferred(c); });
+  c.launches += timed(c, "k_stage1_counts", [&] { return launch_stage1_counts(c); });
+  if ((st = sync_read(c))) return st;
+  if (c.hc.overflow & 32u) return 2;
+  c.matched = c.detected = true;
+  c.launches += timed(c, "k_links", [&] { return launch_links(c); });
+  c.launches += timed(c, "k_walk", [&] { return launch_verdict_walk(c); });
+  if ((st = sync_read(c))) return st;
+  if (c.hc.overflow & 24u) {
+    c.err = "capacity exceeded: more than 16384 samples on a link / links in a direction class";
+    return SCAN_E_UNSUPPORTED;
   }
+  c.localized = true;
+  c.fused_used = true;
+  return SCAN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+// ----------------------------------------------------------------------------- A1-A3 match
+scan_status scan_match_collectives(scan_ctx* ctx, scan_match_result* out) {
+  if (!ctx) return SCAN_E_INVALID_ARG;
+  Ctx& c = ctx->c;
+  if (!c.loaded) { c.err = "scan_match_collectives before scan_load_events"; return SCAN_E_ORDER; }
+  CK(cudaSetDevice(c.device));
+  c.launches = 0;
+  scan_status st = general_match(c);
+  if (st) return st;
+  fill_match(c, out);
+  return match_status(c);
+}
+
+// ----------------------------------------------------------------------------- A4 detect
+scan_status scan_detect(scan_ctx* ctx, const scan_detect_config* cfg, scan_detect_result* out) {
+  if (!ctx) return SCAN_E_INVALID_ARG;
+  Ctx& c = ctx->c;
+  if (!c.matched) { c.err = "scan_detect before scan_match_collectives"; return SCAN_E_ORDER; }
+  CK(cudaSetDevice(c.device));
+  scan_detect_config d = cfg ? *cfg : kDefDetect;
+  if (d.slow_den == 0 || d.cand_den == 0) { c.err = "zero denominator"; return SCAN_E_INVALID_ARG; }
+  if (c.fused_used) { c.err = "scan_detect after scan_analyze: call scan_match_collectives first"; return SCAN_E_ORDER; }
+  c.dcfg = d;
+  scan_status st = general_detect(c);
+  if (st) return st;
+  return detect_tail(c, out);
+}
+
+// ----------------------------------------------------------------------------- A5-A8 localize
+scan_status scan_localize(scan_ctx* ctx, const scan_localize_config* cfg, scan_localize_result* out) {
+  if (!ctx) return SCAN_E_INVALID_ARG;
+  Ctx& c = ctx->c;
+  if (!c.detected || c.fused_used) { c.err = "scan_localize before scan_detect"; return SCAN_E_ORDER; }
+  CK(cudaSetDevice(c.device));
+  scan_localize_config L = cfg ? *cfg : kDefLocalize;
+  if (L.late_den == 0 || L.bw_den == 0) { c.err = "zero denominator"; return SCAN_E_INVALID_ARG; }
+  c.lcfg = L;
+  scan_status st = general_localize(c);
+  if (st) return st;
+  fill_localize(c, out);
+  return SCAN_OK;
+}
+
+// ----------------------------------------------------------------------------- A1-A8 fused
+scan_status scan_analyze(scan_ctx* ctx, const scan_detect_config* dcfg, const scan_localize_config* lcfg,
+                         scan_match_result* mres, scan_detect_result* dres, scan_localize_result* lres) {
+  if (!ctx) return SCAN_E_INVALID_ARG;
+  Ctx& c = ctx->c;
+  if (!c.loaded) { c.err = "scan_analyze before scan_load_events"; return SCAN_E_ORDER; }
+  CK(cudaSetDevice(c.device));
+  scan_detect_config d = dcfg ? *dcfg : kDefDetect;
+  scan_localize_config L = lcfg ? *lcfg : kDefLocalize;
+  if (d.slow_den == 0 || d.cand_den == 0 || L.late_den == 0 || L.bw_den == 0) { c.err = "zero denominator"; return SCAN_E_INVALID_ARG; }
+  c.dcfg = d; c.lcfg = L;
+  c.launches = 0;
+  scan_status st = 2;
+  if (c.spmd && !c.force_general) {
+    st = fused_all(c);
+    if (st < 0) return st;
+  }
+  if (st == 2) {  // not SPMD (or forced): the general path
+    c.launches = 0;
+    if ((st = general_match(c)) || (st = general_detect(c)) || (st = general_localize(c))) return st;
+  }
+  fill_match(c, mres);
+  if ((st = detect_tail(c, dres))) return st;
+  fill_localize(c, lres);
+  return match_status(c);
+}
+
+int scan_used_fused(const scan_ctx* ctx) { return ctx && ctx->c.fused_used ? 1 : 0; }
+
+scan_status scan_force_general(scan_ctx* ctx, int force) {
+  if (!ctx) return SCAN_E_INVALID_ARG;
+  ctx->c.force_general = force != 0;
   return SCAN_OK;
 }
 
@@ -582,6 +776,17 @@ scan_status scan_export(scan_ctx* ctx, scan_output which, void* dst, uint64_t ds
     return SCAN_OK;
   }
   const bool ev = which <= SCAN_OUT_EV_REF, in = which >= SCAN_OUT_IN_CHANNEL && which <= SCAN_OUT_IN_PAYLOAD;
+  if (ev && !c.tiles_ready) {  // fused results: build the general tile prefixes once (untimed)
+    const uint64_t T = std::max<uint64_t>(c.n_tiles, 1);
+    CK(c.t_nkeys.ensure(T * 4)); CK(c.t_keys.ensure(T * KCAP * 4)); CK(c.t_cnt.ensure(T * KCAP * 4));
+    CK(c.t_pref.ensure(T * KCAP * 4)); CK(c.t_ncomm.ensure(T * 4)); CK(c.t_niter.ensure(T * 4)); CK(c.t_last.ensure(T * 4));
+    CK(c.t_commpre.ensure(T * 4)); CK(c.t_iterpre.ensure(T * 4)); CK(c.t_prevj.ensure(T * 4));
+    launch_tile_scan(c);
+    launch_rank_scan(c);
+    CK(cudaStreamSynchronize(c.stream));
+    CK(cudaGetLastError());
+    c.tiles_ready = true;
+  }
   if (ev || in) {
     const uint64_t nb = ev ? ev_bytes(c, which) : in_bytes(c, which);
     if (dst_bytes < nb) { c.err = "destination too small"; return SCAN_E_INVALID_ARG; }

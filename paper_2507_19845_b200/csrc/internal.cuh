@@ -18,6 +18,10 @@ constexpr int KCAP = 32;        // distinct channels per warp tile (one per lane
 constexpr int RCAP = 256;       // distinct channels per rank
 constexpr int PCAP = 32;        // distinct P2P peers per rank
 constexpr int LINK_CAP = 16384; // samples per (window, link) held in shared memory for the median
+// fused SPMD stage-tile path (K9)
+constexpr int ROLES = 32;       // 0..15 collective roles (index in the rank's sorted comm list), 16..31 P2P roles
+constexpr int CROLES = 16;
+constexpr int FCOLS = ROLES + 4;  // per-tile pre-pass columns: roles, ncomp, ncomm, niter, cc_last
 
 // ----------------------------------------------------------------------------- device buffers
 struct DevBuf {
@@ -118,6 +122,18 @@ struct Ctx {
   DevBuf lb_label, lb_rkind, lb_rrank, lb_rsrc, lb_depth, lb_twait;
   DevBuf scratch;                        // export scratch
 
+  // fused SPMD path (K9): host-built role tables, template pre-pass, per-tile bases
+  bool spmd = false;                     // every stage block is SPMD-compatible (checked at load)
+  bool fused_used = false;               // results of the last analysis come from the fused path
+  bool tiles_ready = false;              // general tile prefixes exist (needed by event-order exports)
+  uint32_t FT = 0, FR = 0, n_ftiles = 0; // positions per fused tile, ranks per stage, fused tiles
+  std::vector<uint32_t> h_st_tile0, h_st_npos;
+  DevBuf st_tile0, st_npos, role_comm, role_slot, role_type, ncroles;
+  DevBuf ft_cols, ft_base, ft_last, st_tot;   // pre-pass counts [FCOLS][tiles], scanned bases, last comm, stage totals
+  DevBuf sci, sit;                       // per slot: comm index, iteration of the member event (cross instances)
+  DevBuf dlate, dinfo;                   // deferred stage-2 positions (first comm position of a tile)
+  bool rows_aligned = false;
+  bool force_general = false;
   // optional per-kernel timing
   bool timing = false;
   struct Pending { int k; cudaEvent_t a, b; };
@@ -272,6 +288,7 @@ int launch_p2p_channels(Ctx& c);
 int launch_assign(Ctx& c);
 int launch_inst_reduce(Ctx& c);
 int launch_stage1(Ctx& c);
+int launch_class_counts(Ctx& c);
 int launch_stage1_counts(Ctx& c);
 int launch_event_pass(Ctx& c);
 int launch_links(Ctx& c);
@@ -279,5 +296,11 @@ int launch_verdict_walk(Ctx& c);
 // exports
 int launch_expand_events(Ctx& c, scan_output which, void* dst);
 int launch_instance_export(Ctx& c, scan_output which, void* dst);
+// fused path
+int launch_fused_prepass(Ctx& c);
+int launch_fused_census(Ctx& c);
+int launch_fused(Ctx& c);
+int launch_cross_reduce(Ctx& c);
+int launch_deferred(Ctx& c);
 
 }  // namespace ms

@@ -59,6 +59,8 @@ __global__ void __launch_bounds__(256) k_stage1(S1Args a) {
   uint32_t x[P], s[P];
   uint16_t op0 = 0;
   bool mis = false;
+  const int q = (a.DP - 2) / 2;
+  const int L = P / 2 - 1 - q;  // low sentinels: s[q], s[q+1] land at fixed indices P/2-1, P/2
 #pragma unroll
   for (int d = 0; d < P; ++d) {
     x[d] = 0xFFFFFFFFu;
@@ -69,15 +71,12 @@ __global__ void __launch_bounds__(256) k_stage1(S1Args a) {
       const uint16_t op = a.cop[off];
       if (d == 0) op0 = op; else mis |= (op != op0);
     }
-    s[d] = x[d];
+    s[d] = d < a.DP ? x[d] : (d < a.DP + L ? 0u : 0xFFFFFFFFu);
   }
   const unsigned mm = __ballot_sync(0xFFFFFFFFu, mis);
   if (mm && lane == 0) atomicMin(&a.cl_J[cl], chunk * 32u + (uint32_t)(__ffs(mm) - 1));
   bitonic_regs<P>(s);
-  const int q = (a.DP - 2) / 2;
-  uint32_t va = 0, vb = 0;
-#pragma unroll
-  for (int i = 0; i < P; ++i) { if (i == q) va = s[i]; if (i == q + 1) vb = s[i]; }
+  const uint32_t va = s[P / 2 - 1], vb = s[P / 2];
 #pragma unroll
   for (int d = 0; d < P; ++d) {
     if (d >= a.DP) break;
@@ -106,10 +105,16 @@ __global__ void k_class_counts(int TP, int PP, int DP, const uint32_t* r_ncomp, 
   cl_min[cl] = mn; cl_max[cl] = mx; cl_J[cl] = mn;
 }
 
-int launch_stage1(Ctx& c) {
+int launch_class_counts(Ctx& c) {
   const int ncl = c.TP * c.PP;
   k_class_counts<<<(ncl + 255) / 256, 256, 0, c.stream>>>(c.TP, c.PP, c.DP, c.r_ncomp.as<uint32_t>(), c.cl_min.as<uint32_t>(),
                                                           c.cl_max.as<uint32_t>(), c.cl_J.as<uint32_t>());
+  return 1;
+}
+
+int launch_stage1(Ctx& c) {
+  const int ncl = c.TP * c.PP;
+  launch_class_counts(c);
   if (c.DP < 2 || c.max_ncomp == 0) return 1;
   S1Args a{c.TP, c.PP, c.DP, (c.max_ncomp + 31) / 32, c.r_comp_off.as<uint64_t>(), c.r_bits_off.as<uint64_t>(),
            c.cdur.as<uint32_t>(), c.cop.as<uint16_t>(), c.bits.as<uint32_t>(),

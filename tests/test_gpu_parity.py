@@ -15,6 +15,18 @@ FLOAT_KEYS = {"wd_frac", "wl_late_frac", "lk_med_bw"}
 SKIP_KEYS = set()
 
 
+MODE = {"mode": "analyze"}
+
+
+@pytest.fixture(params=["analyze", "separate"], autouse=True)
+def _mode(request):
+    """Every parity case runs twice: through scan_analyze (fused SPMD stage-tile pass when the trace
+    is SPMD, else the general path) and through scan_match_collectives + scan_detect + scan_localize
+    (general path)."""
+    MODE["mode"] = request.param
+    yield
+
+
 def _gpu(trace, dcfg=None, lcfg=None, device_ptrs=False):
     import paper_2507_19845_b200 as ms
     s = ms.Scan(0)
@@ -25,7 +37,11 @@ def _gpu(trace, dcfg=None, lcfg=None, device_ptrs=False):
         s.load(trace, device_ptrs=True, cols=cols)
     else:
         s.load(trace)
-    res = s.run(dcfg, lcfg)
+    if MODE["mode"] == "analyze":
+        res = s.analyze(dcfg, lcfg)
+    else:
+        res = s.run(dcfg, lcfg)
+        res["fused"] = False
     out = s.export_all()
     out["_res"] = res
     s.close()
@@ -81,12 +97,14 @@ def test_c1_full(seed):
     o, g = _run_both(tg.generate(configs.c1(seed=seed)))
     compare(o, g)
     assert list(np.nonzero(g["wl_verdict"])[0]) == [5]
+    assert g["_res"]["fused"] == (MODE["mode"] == "analyze")
 
 
 def test_c2_short():
     """configs[1] shape (64 ranks TP8xPP4xDP2, jittered links) on 12 iterations."""
     o, g = _run_both(tg.generate(configs.c2(iterations=12)))
     compare(o, g)
+    assert g["_res"]["fused"] == (MODE["mode"] == "analyze")
 
 
 def test_c5_windows_cascade():
@@ -134,6 +152,7 @@ def test_ragged_and_corrupt():
     o, g = _run_both(tr)
     assert o["status"] == 1
     compare(o, g)
+    assert not g["_res"]["fused"]  # not SPMD: scan_analyze falls back to the general path
 
 
 def test_schema_error_matches():
@@ -144,7 +163,7 @@ def test_schema_error_matches():
     s = ms.Scan(0)
     s.load(tr)
     with pytest.raises(ms.ScanError) as ei:
-        s.match()
+        s.analyze() if MODE["mode"] == "analyze" else s.match()
     assert ei.value.status == -2 and f"event {o['bad_event']}" in str(ei.value)
 
 
@@ -162,9 +181,31 @@ def test_rerun_same_context_deterministic():
     tr = tg.generate(configs.c1(seed=2, iterations=4))
     s = ms.Scan(0)
     s.load(tr)
-    s.run()
+    run = s.analyze if MODE["mode"] == "analyze" else s.run
+    run()
     a = s.export_all()
-    s.run()
+    run()
     b = s.export_all()
     for k in a:
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_spmd_violation_falls_back():
+    """A trace that is SPMD at load (equal counts, same roles) but whose events disagree with the
+    stage template (one op id changed on one rank) fails verification inside the fused pass; the
+    call must transparently produce the general path's (oracle-equal) results."""
+    tr = tg.generate(configs.c1(seed=3, iterations=3))
+    e = int(tr.rank_offsets[6]) + 1000
+    assert (tr.kind_op[e] & 7) == 0
+    tr.kind_op[e] = (tr.kind_op[e] & 0xF) | (((tr.kind_op[e] >> 4) ^ 5) << 4)
+    o, g = _run_both(tr)
+    compare(o, g)
+    assert not g["_res"]["fused"]
+
+
+@pytest.mark.parametrize("dp", [3, 5, 6])
+def test_fused_odd_dp(dp):
+    """Non-power-of-two DP groups (padding of the sorting network)."""
+    tr = tg.generate(tg.GenConfig(2, 2, dp, 2, 4, 3, seed=dp, faults=[tg.Fault(tg.THROTTLE, 3, factor=2.0)]))
+    o, g = _run_both(tr)
+    compare(o, g)
