@@ -691,6 +691,7 @@ __device__ __forceinline__ void x_edge(const XArgs& a, uint32_t r, uint32_t L, u
 }
 
 __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
+  if (*((volatile unsigned*)&a.cnt->overflow) & NOT_SPMD) return;  // fused results void: general path reruns
   uint32_t inc = 0, kmis = 0, pmis = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n_inst; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t ch = upper_bound_u64(a.ch_base, a.NCH + 1, i) - 1;
@@ -786,9 +787,10 @@ int launch_cross_reduce(Ctx& c) {
 // pslow from the global slow bits (complete after k_fused), late flags from dlate.
 __global__ void k_deferred(uint32_t n_ftiles, int PP, uint32_t R, int W, const uint32_t* st_tile0, const uint32_t* dinfo,
                            const uint32_t* dlate, const uint64_t* bits_off, const uint32_t* bits, uint32_t classes,
-                           uint32_t* wl_joined, uint32_t* wl_late) {
+                           uint32_t* wl_joined, uint32_t* wl_late, const Counters* cnt) {
   const uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (it >= (uint64_t)n_ftiles * R) return;
+  if (*((volatile const unsigned*)&cnt->overflow) & NOT_SPMD) return;
   const uint32_t tile = (uint32_t)(it / R), row = (uint32_t)(it % R);
   const uint32_t* di = dinfo + (uint64_t)tile * 4;
   if (!(di[3] & 1u)) return;
@@ -821,7 +823,7 @@ int launch_deferred(Ctx& c) {
   k_deferred<<<(unsigned)((items + 255) / 256), 256, 0, c.stream>>>(
       c.n_ftiles, c.PP, c.FR, c.W, c.st_tile0.as<uint32_t>(), c.dinfo.as<uint32_t>(), c.dlate.as<uint32_t>(),
       c.r_bits_off.as<uint64_t>(), c.bits.as<uint32_t>(), c.lcfg.stage2_classes, c.wl_joined.as<uint32_t>(),
-      c.wl_late.as<uint32_t>());
+      c.wl_late.as<uint32_t>(), c.counters.as<Counters>());
   return 1;
 }
 
