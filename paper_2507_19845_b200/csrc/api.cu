@@ -83,7 +83,10 @@ static void release_all(Ctx& c) {
                     &c.rk_sum, &c.bits, &c.cref, &c.cl_J, &c.cl_max, &c.cl_min, &c.wd_total, &c.wd_slow, &c.wd_cand,
                     &c.wd_frac, &c.wl_joined, &c.wl_late, &c.wl_frac, &c.wl_verdict, &c.wl_link_slow, &c.ewc, &c.ewp,
                     &c.lk_n, &c.lk_used, &c.lk_medp, &c.lk_medt, &c.lk_bw, &c.lk_slow, &c.lk_dir, &c.lk_elig,
-                    &c.lb_label, &c.lb_rkind, &c.lb_rrank, &c.lb_rsrc, &c.lb_depth, &c.lb_twait, &c.scratch};
+                    &c.lb_label, &c.lb_rkind, &c.lb_rrank, &c.lb_rsrc, &c.lb_depth, &c.lb_twait, &c.scratch,
+                    &c.st_tile0, &c.st_npos, &c.role_comm, &c.role_slot, &c.role_type, &c.ncroles, &c.ft_cols,
+                    &c.ft_base, &c.ft_last, &c.st_tot, &c.sci, &c.sit, &c.dlate, &c.dinfo, &c.ft_posA, &c.ft_posB,
+                    &c.ft_posK};
   for (DevBuf* b : bufs) b->release();
 }
 
@@ -255,6 +258,8 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
     if (ok) {
       uint32_t T = (16384u / R) / 32u * 32u;
       T = std::max(64u, std::min(1024u, T));
+      // two CTAs per SM: keep the fused kernel's shared memory under ~110 KB
+      while (T > 64 && fused_smem_bytes(T, R, topo->tp, topo->dp) > 110u * 1024u) T -= 32;
       uint32_t nt = 0;
       for (int s = 0; s < topo->pp; ++s) { stt0[s] = nt; nt += (stnp[s] + T - 1) / T; }
       stt0[topo->pp] = nt;
@@ -501,6 +506,8 @@ scan_status fused_all(Ctx& c) {
   if (st) return st;
   CK(c.ft_cols.ensure((uint64_t)FCOLS * c.n_ftiles * 4)); CK(c.ft_base.ensure((uint64_t)FCOLS * c.n_ftiles * 4));
   CK(c.st_tot.ensure((uint64_t)c.PP * FCOLS * 4));
+  CK(c.ft_posA.ensure((uint64_t)c.n_ftiles * c.FT * 4)); CK(c.ft_posB.ensure((uint64_t)c.n_ftiles * c.FT * 4));
+  CK(c.ft_posK.ensure((uint64_t)c.n_ftiles * c.FT * 2));
   c.launches += timed(c, "k_fused_prepass", [&] { return launch_fused_prepass(c); });
   c.launches += timed(c, "k_fused_census", [&] { return launch_fused_census(c); });
   c.launches += timed(c, "k_rank_prefix", [&] { return launch_rank_prefix(c); });

@@ -130,6 +130,7 @@ struct Ctx {
   std::vector<uint32_t> h_st_tile0, h_st_npos;
   DevBuf st_tile0, st_npos, role_comm, role_slot, role_type, ncroles;
   DevBuf ft_cols, ft_base, ft_last, st_tot;   // pre-pass counts [FCOLS][tiles], scanned bases, last comm, stage totals
+  DevBuf ft_posA, ft_posB, ft_posK;           // per template position packed info + template kind_op
   DevBuf sci, sit;                       // per slot: comm index, iteration of the member event (cross instances)
   DevBuf dlate, dinfo;                   // deferred stage-2 positions (first comm position of a tile)
   bool rows_aligned = false;
@@ -300,6 +301,7 @@ int launch_instance_export(Ctx& c, scan_output which, void* dst);
 int launch_fused_prepass(Ctx& c);
 int launch_fused_census(Ctx& c);
 int launch_fused(Ctx& c);
+size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP);
 int launch_cross_reduce(Ctx& c);
 int launch_deferred(Ctx& c);
 

@@ -42,13 +42,18 @@ __device__ __forceinline__ int role_of(uint32_t kind, uint32_t cm, uint32_t r0, 
 }
 
 // ----------------------------------------------------------------------------- F0 pre-pass
-// One warp per fused tile reads the template rank's row only (1/R of the data): role counts,
-// compute / comm / iter_end counts, compute count before the last comm position.
+// One warp per fused tile reads the template rank's row only (1/R of the data) and derives
+// everything the fused kernel needs per position, relative to the tile: role and type, compute /
+// comm / iteration index, occurrence index k within the role, compute index of the previous comm
+// position. Also the per-tile column totals that k_fused_scan turns into tile bases.
+// Packed position words (10-bit fields; positions per tile <= 1024):
+//   posA = j_rel | m_rel << 10 | jprev_rel << 20 | first_comm << 30 | iter_end << 31
+//   posB = it_rel | k_rel << 10 | role << 20 | type << 25
 struct PreArgs {
   const uint16_t* kind; const uint32_t* comm; const uint64_t* rank_off; int W, PP;
   uint32_t T, R, n_ftiles; const uint32_t* st_tile0; const uint32_t* st_npos;
-  const uint32_t* role_comm; const uint32_t* ncroles;
-  uint32_t* cols; Counters* cnt;
+  const uint32_t* role_comm; const uint32_t* ncroles; const uint8_t* role_type;
+  uint32_t* cols; uint32_t* posA; uint32_t* posB; uint16_t* posK; Counters* cnt;
 };
 
 __global__ void __launch_bounds__(256) k_fused_prepass(PreArgs a) {
@@ -66,32 +71,54 @@ __global__ void __launch_bounds__(256) k_fused_prepass(PreArgs a) {
   const uint64_t g0 = a.rank_off[r0] + p0;
   const uint32_t* rc = a.role_comm + (uint64_t)r0 * CROLES;
   const uint32_t ncr = a.ncroles[s];
-  uint32_t ncomp = 0, ncomm = 0, niter = 0;
-  int32_t lastc = -1;
+  uint32_t cj = 0, cm = 0, ci = 0;
+  int32_t lastj = -1;
   bool bad = false;
-  for (uint32_t q = lane; q < np; q += 32) {
-    const uint16_t ko = a.kind[g0 + q];
+  const unsigned lt = (1u << lane) - 1u;
+  for (uint32_t base = 0; base < np; base += 32) {
+    const uint32_t p = base + lane;
+    const bool in = p < np;
+    const uint16_t ko = in ? a.kind[g0 + p] : 0;
     const uint32_t kind = ko & 7u;
-    niter += (ko >> 3) & 1u;
-    if (kind == 0) { ++ncomp; continue; }
-    const int role = role_of(kind, a.comm[g0 + q], r0, rc, ncr, a.R, a.W);
-    if (role < 0) { bad = true; continue; }
-    ++ncomm;
-    atomicAdd(&rcnt[wid][role], 1u);
-    lastc = (int32_t)q;
+    const bool isc = in && kind == 0, iscomm = in && kind != 0, ie = in && ((ko >> 3) & 1u);
+    int role = 31;
+    uint32_t type = 0;
+    if (iscomm) {
+      role = role_of(kind, a.comm[g0 + p], r0, rc, ncr, a.R, a.W);
+      if (role < 0) { bad = true; role = 0; }
+      type = role >= 16 ? 4u : a.role_type[s * ROLES + role];
+    }
+    const unsigned bc = __ballot_sync(0xFFFFFFFFu, isc), bm = __ballot_sync(0xFFFFFFFFu, iscomm),
+                   bi = __ballot_sync(0xFFFFFFFFu, ie);
+    const uint32_t jx = cj + __popc(bc & lt), mx = cm + __popc(bm & lt), ix = ci + __popc(bi & lt);
+    const unsigned grp = __match_any_sync(0xFFFFFFFFu, iscomm ? (uint32_t)role : 0xFFu) & bm;
+    uint32_t kr = 0;
+    if (iscomm) kr = rcnt[wid][role] + __popc(grp & lt);
+    __syncwarp();
+    if (iscomm && lane == (uint32_t)(__ffs(grp) - 1)) rcnt[wid][role] += __popc(grp);
+    __syncwarp();
+    const int32_t inc = warp_incl_max(iscomm ? (int32_t)jx : -1);
+    int32_t ex = __shfl_up_sync(0xFFFFFFFFu, inc, 1);
+    if (lane == 0) ex = -1;
+    const int32_t prev = max(lastj, ex);
+    const uint32_t first = iscomm && prev < 0 ? 1u : 0u;
+    if (in) {
+      a.posA[(uint64_t)tile * a.T + p] = jx | (mx << 10) | ((uint32_t)max(prev, 0) << 20) | (first << 30) | ((ie ? 1u : 0u) << 31);
+      a.posB[(uint64_t)tile * a.T + p] = ix | (kr << 10) | ((uint32_t)role << 20) | (type << 25);
+      a.posK[(uint64_t)tile * a.T + p] = ko;
+    }
+    lastj = max(lastj, __shfl_sync(0xFFFFFFFFu, inc, 31));
+    cj += __popc(bc); cm += __popc(bm); ci += __popc(bi);
   }
-  ncomp = warp_sum_u32(ncomp); ncomm = warp_sum_u32(ncomm); niter = warp_sum_u32(niter);
-  const int32_t lq = (int32_t)__reduce_max_sync(0xFFFFFFFFu, (unsigned)(lastc + 1)) - 1;
   if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(&a.cnt->overflow, NOT_SPMD);
   __syncwarp();
   const uint64_t n = a.n_ftiles;
   a.cols[(uint64_t)lane * n + tile] = rcnt[wid][lane];
   if (lane == 0) {
-    a.cols[(uint64_t)(ROLES + 0) * n + tile] = ncomp;
-    a.cols[(uint64_t)(ROLES + 1) * n + tile] = ncomm;
-    a.cols[(uint64_t)(ROLES + 2) * n + tile] = niter;
-    // compute positions before the last comm position (cc_last), or 0xFFFFFFFF
-    a.cols[(uint64_t)(ROLES + 3) * n + tile] = lq >= 0 ? (uint32_t)lq - (ncomm - 1) : NONE32;
+    a.cols[(uint64_t)(ROLES + 0) * n + tile] = cj;
+    a.cols[(uint64_t)(ROLES + 1) * n + tile] = cm;
+    a.cols[(uint64_t)(ROLES + 2) * n + tile] = ci;
+    a.cols[(uint64_t)(ROLES + 3) * n + tile] = lastj >= 0 ? (uint32_t)lastj : NONE32;  // cc_last
   }
 }
 
@@ -136,7 +163,8 @@ __global__ void __launch_bounds__(SC_NT) k_fused_scan(uint32_t n_ftiles, const u
 
 int launch_fused_prepass(Ctx& c) {
   PreArgs a{c.d_kind, c.d_comm, c.rank_off.as<uint64_t>(), c.W, c.PP, c.FT, c.FR, c.n_ftiles, c.st_tile0.as<uint32_t>(),
-            c.st_npos.as<uint32_t>(), c.role_comm.as<uint32_t>(), c.ncroles.as<uint32_t>(), c.ft_cols.as<uint32_t>(),
+            c.st_npos.as<uint32_t>(), c.role_comm.as<uint32_t>(), c.ncroles.as<uint32_t>(), c.role_type.as<uint8_t>(),
+            c.ft_cols.as<uint32_t>(), c.ft_posA.as<uint32_t>(), c.ft_posB.as<uint32_t>(), c.ft_posK.as<uint16_t>(),
             c.counters.as<Counters>()};
   k_fused_prepass<<<(c.n_ftiles + 7) / 8, 256, 0, c.stream>>>(a);
   k_fused_scan<<<dim3(c.PP, ROLES + 3), SC_NT, 0, c.stream>>>(c.n_ftiles, c.st_tile0.as<uint32_t>(), c.ft_cols.as<uint32_t>(),
@@ -226,9 +254,10 @@ int launch_fused_census(Ctx& c) {
 // ----------------------------------------------------------------------------- F1 fused tile kernel
 struct FusedArgs {
   const uint32_t* dur; const uint16_t* kind; const uint16_t* meta; const uint32_t* comm; const uint32_t* pay;
-  const uint64_t* rank_off; int TP, DP, PP, W; uint32_t n_comms; uint32_t T, R, n_ftiles; bool aligned;
+  const uint64_t* rank_off; int TP, DP, PP, W; uint32_t n_comms; uint32_t T, R, n_ftiles, G; bool aligned;
   const uint32_t* st_tile0; const uint32_t* st_npos; const uint32_t* ft_base;
-  const uint32_t* role_comm; const uint32_t* role_slot; const uint8_t* role_type; const uint32_t* ncroles;
+  const uint32_t* posA; const uint32_t* posB; const uint16_t* posK;
+  const uint32_t* role_comm; const uint32_t* role_slot; const uint32_t* ncroles;
   const uint64_t* coff;
   const uint64_t* ch_base; const uint64_t* ch_slot; const uint32_t* bitmap; const uint32_t* bitpre;
   const uint64_t* comm_off; const uint64_t* comp_off; const uint64_t* bits_off;
@@ -244,7 +273,7 @@ struct FusedArgs {
   Counters* cnt;
 };
 
-constexpr int F_NT = 256;
+constexpr int F_NT = 512;
 
 __device__ __forceinline__ void add_edge(const FusedArgs& a, uint32_t r, uint32_t L, uint32_t win, uint32_t wait) {
   const uint64_t nb0 = a.nbc_off[r], nb1 = a.nbc_off[r + 1];
@@ -267,207 +296,154 @@ __device__ __forceinline__ bool sbits_any(const uint32_t* sb, uint32_t wb, uint3
   return false;
 }
 
+// Duration tile in shared memory: row-major [R][T], 16-byte granules XOR-swizzled per row so that
+// both TP groups (consecutive rows) and DP groups (rows TP apart) read a column conflict-light.
+__device__ __forceinline__ uint32_t sw_idx(uint32_t row, uint32_t p, uint32_t T) {
+  const uint32_t sw = (row ^ (row >> 3)) & 7u;
+  return row * T + ((((p >> 2) ^ sw)) << 2) + (p & 3u);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
 template <int P>
-__global__ void __launch_bounds__(F_NT) k_fused(FusedArgs a) {
+__global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  const uint32_t T = a.T, R = a.R, TP = (uint32_t)a.TP, DP = (uint32_t)a.DP;
-  const uint32_t T1 = T + 1;
+  const uint32_t T = a.T, R = a.R, TP = (uint32_t)a.TP, DP = (uint32_t)a.DP, G = a.G;
   const uint32_t SW = T / 32 + 2;
-  // ---- shared memory carve-up
-  uint32_t* sd = (uint32_t*)smem_raw;                       // R x (T+1) durations
-  uint32_t* sbits = sd + (uint64_t)R * T1;                  // R x SW slow bits
-  unsigned long long* rsum = (unsigned long long*)(sbits + (uint64_t)R * SW + ((R * T1 + R * SW) & 1));  // R x 2
-  unsigned long long* gsum = rsum + 2 * R;                  // DP (TP groups) + TP (DP groups)
-  uint32_t* sjoin = (uint32_t*)(gsum + DP + TP);            // R
-  uint32_t* slate = sjoin + R;                              // R
-  uint32_t* pk = slate + R;                                 // T
-  uint32_t* pj = pk + T;
-  uint32_t* pm = pj + T;
-  uint32_t* pit = pm + T;
-  uint32_t* pjp = pit + T;
-  uint32_t* tc = pjp + T;                                   // template comm
-  uint16_t* tk = (uint16_t*)(tc + T);                       // template kind_op
-  uint16_t* lst = tk + T;                                   // position lists (4 x T)
-  uint8_t* ptype = (uint8_t*)(lst + 4 * T);
-  uint8_t* prole = ptype + T;
-  __shared__ uint32_t rcnt[33][ROLES];
-  __shared__ uint32_t scan_sm[33];
-  __shared__ int32_t scan_smi[33];
-  __shared__ uint32_t nlist[5];
+  // ---- shared memory carve-up (see fused_smem_bytes)
+  uint32_t* sd = (uint32_t*)smem_raw;                                   // R x T (swizzled)
+  unsigned long long* gsum = (unsigned long long*)(sd + (uint64_t)R * T);  // DP + TP
+  unsigned long long* coffr = gsum + DP + TP;                           // R comm offsets
+  uint32_t* sinst = (uint32_t*)(coffr + R);                             // T x G
+  uint32_t* sbits = sinst + (uint64_t)T * G;                            // R x SW
+  uint32_t* rcs = sbits + (uint64_t)R * SW;                             // R x CROLES
+  uint32_t* pa = rcs + (uint64_t)R * CROLES;                            // T
+  uint32_t* pb = pa + T;                                                // T
+  uint32_t* sjoin = pb + T;                                             // R
+  uint32_t* slate = sjoin + R;                                          // R
+  uint16_t* pk = (uint16_t*)(slate + R);                                // T (template kind_op)
+  uint16_t* lst = pk + T;                                               // 4 x T
+  uint16_t* cl = lst + 4 * T;                                           // T (comm positions by m)
+  __shared__ uint32_t kbase[ROLES];
+  __shared__ uint32_t nlist[4];
   __shared__ int32_t dpos;
   __shared__ uint32_t bad;
 
   const uint32_t tile = blockIdx.x;
+  const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
   uint32_t s = 0;
   while (s + 1 < (uint32_t)a.PP && a.st_tile0[s + 1] <= tile) ++s;
   const uint32_t p0 = (tile - a.st_tile0[s]) * T;
   const uint32_t np = min(T, a.st_npos[s] - p0);
   const uint32_t sbase = s * R;
   const uint64_t n = a.n_ftiles;
+
+  // ---- (1) stream the duration rows of all R ranks into shared memory (async, 16 B granules)
+  const uint32_t ngr = (np + 3) / 4;
+  for (uint32_t i = tid; i < R * ngr; i += F_NT) {
+    const uint32_t row = i / ngr, gi = i % ngr;
+    const uint64_t g = a.rank_off[sbase + row] + p0 + 4 * gi;
+    uint32_t* dst = sd + sw_idx(row, 4 * gi, T);
+    if (a.aligned && 4 * gi + 4 <= np) {
+      cp_async16(dst, a.dur + g);
+    } else {
+      for (uint32_t q = 0; q < 4; ++q) dst[q] = 4 * gi + q < np ? a.dur[g + q] : 0u;
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+  // ---- (2) per-tile tables and template position info (from the pre-pass)
   const uint32_t j0 = a.ft_base[(uint64_t)ROLES * n + tile];
   const uint32_t m0 = a.ft_base[(uint64_t)(ROLES + 1) * n + tile];
   const uint32_t it0 = a.ft_base[(uint64_t)(ROLES + 2) * n + tile];
   const uint32_t jp0 = a.ft_base[(uint64_t)(ROLES + 3) * n + tile];
   const uint32_t wb = j0 >> 5;
   const uint32_t w_tile = a.wi ? it0 / a.wi : 0;
-  const uint32_t tid = threadIdx.x;
   const uint32_t ncr = a.ncroles[s];
-  const uint32_t* rc0 = a.role_comm + (uint64_t)sbase * CROLES;
-
-  // ---- (1) template row + shared-memory init
-  if (tid < 5) nlist[tid] = 0;
+  if (tid < ROLES) kbase[tid] = a.ft_base[(uint64_t)tid * n + tile];
+  if (tid < 4) nlist[tid] = 0;
   if (tid == 0) { dpos = -1; bad = 0; }
   for (uint32_t i = tid; i < R * SW; i += F_NT) sbits[i] = 0;
-  for (uint32_t i = tid; i < R; i += F_NT) { rsum[2 * i] = 0; rsum[2 * i + 1] = 0; sjoin[i] = 0; slate[i] = 0; }
+  for (uint32_t i = tid; i < R; i += F_NT) { sjoin[i] = 0; slate[i] = 0; coffr[i] = a.comm_off[sbase + i]; }
   for (uint32_t i = tid; i < DP + TP; i += F_NT) gsum[i] = 0;
-  for (uint32_t i = tid; i < 33 * ROLES; i += F_NT) (&rcnt[0][0])[i] = 0;
-  const uint64_t g0 = a.rank_off[sbase] + p0;
-  for (uint32_t p = tid; p < T; p += F_NT) {
-    if (p < np) { tk[p] = a.kind[g0 + p]; tc[p] = a.comm[g0 + p]; }
-    else { tk[p] = 0; tc[p] = 0; }
+  for (uint32_t i = tid; i < R * ncr; i += F_NT) {
+    const uint32_t row = i / ncr, ro = i % ncr;
+    rcs[row * CROLES + ro] = a.role_comm[(uint64_t)(sbase + row) * CROLES + ro];
+  }
+  for (uint32_t p = tid; p < np; p += F_NT) {
+    pa[p] = a.posA[(uint64_t)tile * T + p];
+    pb[p] = a.posB[(uint64_t)tile * T + p];
+    pk[p] = a.posK[(uint64_t)tile * T + p];
   }
   __syncthreads();
-  // ---- (2) per-position info from the template row: type, role, j, m, iteration, k, jprev
-  const uint32_t PPT = (T + F_NT - 1) / F_NT;
-  uint32_t lc = 0, lm = 0, li = 0;
-  for (uint32_t q = 0; q < PPT; ++q) {
-    const uint32_t p = tid * PPT + q;
-    if (p >= np) break;
-    const uint32_t kind = tk[p] & 7u;
-    int role = -1;
-    uint8_t ty = TY_COMPUTE;
-    if (kind) {
-      role = role_of(kind, tc[p], sbase, rc0, ncr, R, a.W);
-      if (role < 0) { bad = 1; role = 0; }
-      ty = role >= 16 ? (uint8_t)TY_P2P : a.role_type[s * ROLES + role];
-      ++lm;
-    } else {
-      ++lc;
-    }
-    ptype[p] = ty; prole[p] = (uint8_t)(role < 0 ? 255 : role);
-    li += (tk[p] >> 3) & 1u;
-  }
-  uint32_t tc_, tm_, ti_;
-  uint32_t ec = block_excl_sum<F_NT>(lc, tc_, scan_sm);
-  uint32_t em = block_excl_sum<F_NT>(lm, tm_, scan_sm);
-  uint32_t ei = block_excl_sum<F_NT>(li, ti_, scan_sm);
-  int32_t mylastj = -1;
-  for (uint32_t q = 0; q < PPT; ++q) {
-    const uint32_t p = tid * PPT + q;
-    if (p >= np) break;
-    pj[p] = j0 + ec; pm[p] = m0 + em; pit[p] = it0 + ei;
-    const bool isc = (tk[p] & 7u) == 0;
-    if (!isc) mylastj = (int32_t)(j0 + ec);
-    ec += isc; em += !isc; ei += (tk[p] >> 3) & 1u;
-  }
-  // jprev: compute index of the previous comm position (or the tile base)
-  int32_t totj;
-  int32_t exj = block_excl_max<F_NT>(mylastj, totj, scan_smi);
-  int32_t run = max((int32_t)jp0, exj);
-  for (uint32_t q = 0; q < PPT; ++q) {
-    const uint32_t p = tid * PPT + q;
-    if (p >= np) break;
-    if (tk[p] & 7u) { pjp[p] = (uint32_t)run; run = (int32_t)pj[p]; }
-  }
-  // in-tile occurrence rank per role (warp-chunked match) + lists
-  for (uint32_t ch = tid >> 5; ch * 32 < T; ch += F_NT / 32) {
-    const uint32_t p = ch * 32 + lane_id();
-    const bool in = p < np && (tk[p] & 7u);
-    const uint32_t role = in ? prole[p] : 0xFFFFu;
-    const unsigned act = __ballot_sync(0xFFFFFFFFu, in);
-    const unsigned mm = __match_any_sync(0xFFFFFFFFu, role);
-    if (in) {
-      const unsigned grp = mm & act;
-      pk[p] = __popc(grp & ((1u << lane_id()) - 1u));
-      if (lane_id() == (uint32_t)(__ffs(grp) - 1)) rcnt[ch][role] = __popc(grp);
-    }
-    if (p < np) {
-      const uint8_t ty = ptype[p];
-      const uint32_t li_ = (tk[p] & 7u) == 0 ? 0u : (ty == TY_TP ? 1u : (ty == TY_DP ? 2u : 3u));
-      const uint32_t slot = atomicAdd(&nlist[li_], 1u);
-      lst[li_ * T + slot] = (uint16_t)p;
-      if ((tk[p] >> 3) & 1u) { const uint32_t sl = atomicAdd(&nlist[4], 1u); (void)sl; }
+  // position lists by type (order irrelevant), comm positions in m order, deferred position
+  for (uint32_t p = tid; p < np; p += F_NT) {
+    const uint32_t A = pa[p], B = pb[p];
+    const uint32_t ty = (B >> 25) & 7u;
+    const bool isc = (pk[p] & 7u) == 0;
+    const uint32_t li = isc ? 0u : (ty == TY_TP ? 1u : (ty == TY_DP ? 2u : 3u));
+    const uint32_t sl = atomicAdd(&nlist[li], 1u);
+    lst[li * T + sl] = (uint16_t)p;
+    if (!isc) {
+      cl[(A >> 10) & 1023u] = (uint16_t)p;
+      if (((A >> 30) & 1u) && (ty == TY_TP || ty == TY_DP) && a.mode == 0 && jp0 < j0) dpos = (int32_t)p;
     }
   }
-  __syncthreads();
-  if (tid < ROLES) {
-    uint32_t acc = a.ft_base[(uint64_t)tid * n + tile];
-    for (uint32_t ch = 0; ch * 32 < T; ++ch) { const uint32_t v = rcnt[ch][tid]; rcnt[ch][tid] = acc; acc += v; }
-  }
-  __syncthreads();
-  for (uint32_t p = tid; p < np; p += F_NT)
-    if (tk[p] & 7u) pk[p] += rcnt[p >> 5][prole[p]];
-  if (tid == 0 && a.mode == 0) {
-    // the first comm position of the tile reaches back across the tile start: defer its stage-2
-    for (uint32_t p = 0; p < np; ++p)
-      if (tk[p] & 7u) {
-        if ((ptype[p] == TY_TP || ptype[p] == TY_DP) && pjp[p] < j0) dpos = (int32_t)p;
-        break;
+  // ---- (3) verify every rank row against the template (kind_op; communicator / peer of the role)
+  {
+    const uint32_t nch = (np + 127) / 128;
+    for (uint32_t wq = wid; wq < R * nch; wq += F_NT / 32) {
+      const uint32_t row = wq / nch, ch = wq % nch;
+      const uint32_t r = sbase + row;
+      const uint32_t pbase = ch * 128 + lane * 4;
+      const uint64_t g = a.rank_off[r] + p0 + pbase;
+      uint16_t ko[4]; uint32_t cm[4];
+      if (a.aligned && pbase + 4 <= np) {
+        const uint2 kv = __ldg(reinterpret_cast<const uint2*>(a.kind + g));
+        const uint4 cv = __ldg(reinterpret_cast<const uint4*>(a.comm + g));
+        ko[0] = (uint16_t)kv.x; ko[1] = (uint16_t)(kv.x >> 16); ko[2] = (uint16_t)kv.y; ko[3] = (uint16_t)(kv.y >> 16);
+        cm[0] = cv.x; cm[1] = cv.y; cm[2] = cv.z; cm[3] = cv.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const bool v = pbase + i < np;
+          ko[i] = v ? a.kind[g + i] : 0; cm[i] = v ? a.comm[g + i] : 0;
+        }
       }
-  }
-  // ---- (3) stream every rank row of the tile: verify against the template, stage durations
-  for (uint32_t wq = tid >> 5; wq < R * ((T + 127) / 128); wq += F_NT / 32) {
-    const uint32_t row = wq / ((T + 127) / 128), chunk = wq % ((T + 127) / 128);
-    const uint32_t r = sbase + row;
-    const uint32_t pb = chunk * 128 + lane_id() * 4;
-    const uint64_t g = a.rank_off[r] + p0 + pb;
-    uint16_t ko[4]; uint32_t cm[4], du[4];
-    if (a.aligned && pb + 4 <= np) {
-      const uint2 kv = __ldg(reinterpret_cast<const uint2*>(a.kind + g));
-      const uint4 cv = __ldg(reinterpret_cast<const uint4*>(a.comm + g));
-      const uint4 dv = __ldg(reinterpret_cast<const uint4*>(a.dur + g));
-      ko[0] = (uint16_t)kv.x; ko[1] = (uint16_t)(kv.x >> 16); ko[2] = (uint16_t)kv.y; ko[3] = (uint16_t)(kv.y >> 16);
-      cm[0] = cv.x; cm[1] = cv.y; cm[2] = cv.z; cm[3] = cv.w;
-      du[0] = dv.x; du[1] = dv.y; du[2] = dv.z; du[3] = dv.w;
-    } else {
+      bool mis = false;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const bool v = pb + i < np;
-        ko[i] = v ? a.kind[g + i] : 0; cm[i] = v ? a.comm[g + i] : 0; du[i] = v ? a.dur[g + i] : 0;
+        const uint32_t p = pbase + i;
+        if (p < np) {
+          const uint16_t tko = pk[p];
+          if (ko[i] != tko) mis = true;
+          if (tko & 7u) {
+            const uint32_t role = (pb[p] >> 20) & 31u;
+            if (role < 16) mis |= cm[i] != rcs[row * CROLES + role];
+            else mis |= (int)cm[i] != (int)r + ((int)(role & 7u) - 4) * (int)R;
+          }
+        }
       }
-    }
-    unsigned long long scomp = 0, sinb = 0;
-    bool mis = false;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t p = pb + i;
-      if (p >= np) break;
-      if (ko[i] != tk[p]) mis = true;
-      const uint8_t ty = ptype[p];
-      const uint32_t role = prole[p];
-      if ((tk[p] & 7u) == 0) {
-        scomp += du[i];
-      } else if (role < 16) {
-        if (cm[i] != a.role_comm[(uint64_t)r * CROLES + role]) mis = true;
-        if (ty == TY_TP || ty == TY_DP) sinb += du[i];
-      } else {
-        const int ds = (int)(role & 7u) - 4;
-        if ((int)cm[i] != (int)r + ds * (int)R) mis = true;
-      }
-      sd[row * T1 + p] = du[i];
-    }
-    if (__any_sync(0xFFFFFFFFu, mis) && lane_id() == 0) bad = 1;
-    scomp = warp_sum_u64(scomp); sinb = warp_sum_u64(sinb);
-    if (lane_id() == 0) {
-      if (scomp) atomicAdd(&rsum[2 * row], scomp);
-      if (sinb) atomicAdd(&rsum[2 * row + 1], sinb);
+      if (__any_sync(0xFFFFFFFFu, mis) && lane == 0) bad = 1;
     }
   }
+  cp_async_wait_all();
   __syncthreads();
   if (bad) { if (tid == 0) atomicOr(&a.cnt->overflow, NOT_SPMD); return; }
   // ---- (4) phase A: stage 1 on every compute position (LOO lower median over the DP peers)
   const uint32_t nc = nlist[0];
   if (P >= 2) {
     const int q = ((int)DP - 2) / 2;
+    const int L = P / 2 - 1 - q;  // low sentinels put s[q], s[q+1] at the fixed indices P/2-1, P/2
     for (uint32_t it = tid; it < nc * TP; it += F_NT) {
       const uint32_t p = lst[it / TP], tp = it % TP;
-      // pad to P with L low (0) and P-DP-L high (max) sentinels so that the two order statistics
-      // needed, s[q] and s[q+1] with q = floor((DP-2)/2), land at the fixed indices P/2-1, P/2
-      const int L = P / 2 - 1 - q;
       uint32_t x[P], v[P];
 #pragma unroll
       for (int d = 0; d < P; ++d) {
-        x[d] = d < (int)DP ? sd[(tp + TP * d) * T1 + p] : 0xFFFFFFFFu;
+        x[d] = d < (int)DP ? sd[sw_idx(tp + TP * d, p, T)] : 0xFFFFFFFFu;
         v[d] = d < (int)DP ? x[d] : (d < (int)DP + L ? 0u : 0xFFFFFFFFu);
       }
 #pragma unroll
@@ -484,7 +460,7 @@ __global__ void __launch_bounds__(F_NT) k_fused(FusedArgs a) {
             }
           }
       const uint32_t va = v[P / 2 - 1], vb = v[P / 2];
-      const uint32_t j = pj[p];
+      const uint32_t j = j0 + (pa[p] & 1023u);
 #pragma unroll
       for (int d = 0; d < P; ++d) {
         if (d < (int)DP) {
@@ -499,11 +475,12 @@ __global__ void __launch_bounds__(F_NT) k_fused(FusedArgs a) {
       }
     }
   }
-  // iteration boundaries (compute index at which the next iteration starts), for every rank
+  // iteration boundaries (compute index at which the next iteration starts), every rank
   for (uint32_t p = tid; p < np; p += F_NT) {
-    if (!((tk[p] >> 3) & 1u)) continue;
-    const uint32_t v = pj[p] + ((tk[p] & 7u) == 0 ? 1u : 0u);
-    for (uint32_t row = 0; row < R; ++row) a.citer[(uint64_t)(sbase + row) * a.NIT1 + pit[p] + 1] = v;
+    if (!(pa[p] >> 31)) continue;
+    const uint32_t v = j0 + (pa[p] & 1023u) + ((pk[p] & 7u) == 0 ? 1u : 0u);
+    const uint32_t itp = it0 + (pb[p] & 1023u);
+    for (uint32_t row = 0; row < R; ++row) a.citer[(uint64_t)(sbase + row) * a.NIT1 + itp + 1] = v;
   }
   __syncthreads();
   // ---- (5) phase B: TP / DP instances (all members in the tile) and cross-stage scatters
@@ -515,12 +492,13 @@ __global__ void __launch_bounds__(F_NT) k_fused(FusedArgs a) {
       const uint32_t p = istp ? lst[T + it / DP] : lst[2 * T + (it - I1) / TP];
       const uint32_t g = istp ? it % DP : (it - I1) % TP;
       const uint32_t nm = istp ? TP : DP, stride = istp ? 1u : TP, row0 = istp ? TP * g : g;
-      const uint32_t role = prole[p];
-      const uint32_t cid = a.role_comm[(uint64_t)(sbase + row0) * CROLES + role];
-      const uint64_t inst = a.ch_base[cid] + pk[p];
+      const uint32_t A = pa[p], B = pb[p];
+      const uint32_t role = (B >> 20) & 31u;
+      const uint32_t cid = rcs[row0 * CROLES + role];
+      const uint64_t inst = a.ch_base[cid] + kbase[role] + ((B >> 10) & 1023u);
       uint32_t dmin = 0xFFFFFFFFu, dmax = 0, ls = 0, nat = 0;
       for (uint32_t q = 0; q < nm; ++q) {
-        const uint32_t d = sd[(row0 + q * stride) * T1 + p];
+        const uint32_t d = sd[sw_idx(row0 + q * stride, p, T)];
         if (d < dmin) { dmin = d; ls = q; nat = 1; } else if (d == dmin) ++nat;
         dmax = max(dmax, d);
       }
@@ -528,17 +506,18 @@ __global__ void __launch_bounds__(F_NT) k_fused(FusedArgs a) {
       const uint32_t last = sbase + row0 + ls * stride;
       a.rec[inst] = make_uint4(dmin, dmax, last, (SCAN_F_COMPLETE | SCAN_F_KIND_OK | SCAN_F_PAYLOAD_OK | SCAN_F_VALID |
                                                   (nat == 1 ? SCAN_F_UNIQUE_LAST : 0u)) | (cls << 8));
+      sinst[p * G + g] = (uint32_t)inst;
       atomicAdd(&gsum[istp ? g : DP + g], (unsigned long long)dmin);
-      const uint32_t win = a.wi ? pit[p] / a.wi : 0;
+      const uint32_t win = a.wi ? (it0 + (B & 1023u)) / a.wi : 0;
       const bool elig = (a.classes >> (cls - 1)) & 1u;
       const bool late_ok = nat == 1 && (unsigned long long)(dmax - dmin) > a.late_margin;
+      const uint32_t jp = j0 + (A & 1023u);
+      const uint32_t jprev = ((A >> 30) & 1u) ? jp0 : j0 + ((A >> 20) & 1023u);
       for (uint32_t q = 0; q < nm; ++q) {
         const uint32_t row = row0 + q * stride, r = sbase + row;
-        const uint32_t d = sd[row * T1 + p];
-        const uint64_t ci = a.comm_off[r] + pm[p];
-        a.inst_c[ci] = (uint32_t)inst;
-        const uint32_t wait = d - dmin;
-        a.wait_c[ci] = wait;
+        const uint32_t idx = sw_idx(row, p, T);
+        const uint32_t wait = sd[idx] - dmin;
+        sd[idx] = wait;  // the duration tile now holds the wait at in-block comm positions
         if (q != ls && (unsigned long long)wait > a.wait_margin) add_edge(a, r, last, win, wait);
         if (!elig) continue;
         const bool lt = q == ls && late_ok;
@@ -546,7 +525,7 @@ __global__ void __launch_bounds__(F_NT) k_fused(FusedArgs a) {
           if (lt) atomicOr(&a.dlate[(uint64_t)tile * ((R + 31) / 32) + row / 32], 1u << (row & 31));
           continue;
         }
-        const bool pslow = a.mode ? true : sbits_any(sbits + row * SW, wb, pjp[p], pj[p]);
+        const bool pslow = a.mode ? true : sbits_any(sbits + row * SW, wb, jprev, jp);
         if (!pslow) continue;
         if (win == w_tile) { atomicAdd(&sjoin[row], 1u); if (lt) atomicAdd(&slate[row], 1u); }
         else { atomicAdd(&a.wl_joined[(uint64_t)win * a.W + r], 1u); if (lt) atomicAdd(&a.wl_late[(uint64_t)win * a.W + r], 1u); }
@@ -554,12 +533,13 @@ __global__ void __launch_bounds__(F_NT) k_fused(FusedArgs a) {
     } else {
       const uint32_t x = it - I2;
       const uint32_t p = lst[3 * T + x / R], row = x % R, r = sbase + row;
-      const uint32_t role = prole[p];
+      const uint32_t A = pa[p], B = pb[p];
+      const uint32_t role = (B >> 20) & 31u;
       const uint64_t e = a.rank_off[r] + p0 + p;
       uint64_t ch; uint32_t nm, slot;
       bool send = false;
       if (role < 16) {
-        const uint32_t cid = a.role_comm[(uint64_t)r * CROLES + role];
+        const uint32_t cid = rcs[row * CROLES + role];
         ch = cid; nm = (uint32_t)(a.coff[cid + 1] - a.coff[cid]); slot = a.role_slot[(uint64_t)r * CROLES + role];
       } else {
         const int ds = (int)(role & 7u) - 4;
@@ -570,28 +550,58 @@ __global__ void __launch_bounds__(F_NT) k_fused(FusedArgs a) {
         ch = a.n_comms + a.bitpre[xk >> 5] + __popc(a.bitmap[xk >> 5] & ((1u << (xk & 31)) - 1u));
         nm = 2; slot = send ? 0 : 1;
       }
-      const uint64_t inst = a.ch_base[ch] + pk[p];
-      const uint64_t si = a.ch_slot[ch] + (uint64_t)pk[p] * nm + slot;
-      const uint64_t ci = a.comm_off[r] + pm[p];
-      a.inst_c[ci] = (uint32_t)inst;
-      a.sdur[si] = sd[row * T1 + p];
-      a.skind[si] = (uint8_t)(tk[p] & 7u);
-      a.sci[si] = (uint32_t)ci;
-      a.sit[si] = pit[p];
+      const uint32_t kk = kbase[role] + ((B >> 10) & 1023u);
+      const uint64_t inst = a.ch_base[ch] + kk;
+      const uint64_t si = a.ch_slot[ch] + (uint64_t)kk * nm + slot;
+      const uint32_t idx = sw_idx(row, p, T);
+      const uint32_t itp = it0 + (B & 1023u);
+      a.sdur[si] = sd[idx];
+      a.skind[si] = (uint8_t)(pk[p] & 7u);
+      a.sci[si] = (uint32_t)(coffr[row] + m0 + ((A >> 10) & 1023u));
+      a.sit[si] = itp;
+      sd[idx] = (uint32_t)inst;  // cross positions: the tile now holds the instance id
       if (role >= 16) {
         a.p2p_pay[si - a.p2p_slot0] = a.pay[e];
         if (send) {
           a.p2p_warm[inst - a.p2p_inst0] = (uint8_t)((a.meta[e] >> 14) & 1u);
-          a.p2p_iter[inst - a.p2p_inst0] = pit[p];
+          a.p2p_iter[inst - a.p2p_inst0] = itp;
         }
       }
     }
   }
   __syncthreads();
-  // ---- (6) flush: slow bits, per-rank sums, stage-2 counters, deferred position
-  const uint32_t nct = nlist[0];
-  if (nct) {
-    const uint32_t w_first = j0 >> 5, w_last = (j0 + nct - 1) >> 5;
+  // ---- (6) flush: coalesced per-rank inst / wait rows, per-rank sums, slow bits, counters
+  const uint32_t ncm = nlist[1] + nlist[2] + nlist[3];
+  for (uint32_t row = wid; row < R; row += F_NT / 32) {
+    const uint32_t r = sbase + row;
+    const uint64_t cb = coffr[row] + m0;
+    unsigned long long scomp = 0, swait = 0;
+    for (uint32_t j = lane; j < ncm; j += 32) {
+      const uint32_t p = cl[j];
+      const uint32_t ty = (pb[p] >> 25) & 7u;
+      const uint32_t v = sd[sw_idx(row, p, T)];
+      if (ty == TY_TP || ty == TY_DP) {
+        const uint32_t g = ty == TY_TP ? row / TP : row % TP;
+        a.inst_c[cb + j] = sinst[p * G + g];
+        a.wait_c[cb + j] = v;
+        swait += v;
+      } else {
+        a.inst_c[cb + j] = v;
+      }
+    }
+    for (uint32_t q = lane; q < nc; q += 32) scomp += sd[sw_idx(row, lst[q], T)];
+    scomp = warp_sum_u64(scomp); swait = warp_sum_u64(swait);
+    if (lane == 0) {
+      const unsigned long long tr = gsum[row / TP] + gsum[DP + row % TP];
+      if (scomp) atomicAdd(&a.rk_sum[r], scomp);
+      if (swait) atomicAdd(&a.rk_sum[a.W + r], swait);
+      if (tr) atomicAdd(&a.rk_sum[2 * a.W + r], tr);
+      if (sjoin[row]) atomicAdd(&a.wl_joined[(uint64_t)w_tile * a.W + r], sjoin[row]);
+      if (slate[row]) atomicAdd(&a.wl_late[(uint64_t)w_tile * a.W + r], slate[row]);
+    }
+  }
+  if (nc) {
+    const uint32_t w_first = j0 >> 5, w_last = (j0 + nc - 1) >> 5;
     const uint32_t nw = w_last - w_first + 1;
     for (uint32_t i = tid; i < R * nw; i += F_NT) {
       const uint32_t row = i / nw, w = w_first + i % nw;
@@ -599,20 +609,12 @@ __global__ void __launch_bounds__(F_NT) k_fused(FusedArgs a) {
       if (v) atomicOr(&a.bits[a.bits_off[sbase + row] + w], v);
     }
   }
-  for (uint32_t row = tid; row < R; row += F_NT) {
-    const uint32_t r = sbase + row;
-    const unsigned long long tr = gsum[row / TP] + gsum[DP + row % TP];
-    if (rsum[2 * row]) atomicAdd(&a.rk_sum[r], rsum[2 * row]);
-    if (rsum[2 * row + 1] - tr) atomicAdd(&a.rk_sum[a.W + r], rsum[2 * row + 1] - tr);
-    if (tr) atomicAdd(&a.rk_sum[2 * a.W + r], tr);
-    if (sjoin[row]) atomicAdd(&a.wl_joined[(uint64_t)w_tile * a.W + r], sjoin[row]);
-    if (slate[row]) atomicAdd(&a.wl_late[(uint64_t)w_tile * a.W + r], slate[row]);
-  }
   if (tid == 0) {
     uint32_t* di = a.dinfo + (uint64_t)tile * 4;
     if (dpos >= 0) {
       const uint32_t p = (uint32_t)dpos;
-      di[0] = pj[p]; di[1] = pjp[p]; di[2] = a.wi ? pit[p] / a.wi : 0; di[3] = 1u | ((uint32_t)ptype[p] << 8);
+      const uint32_t ty = (pb[p] >> 25) & 7u;
+      di[0] = j0 + (pa[p] & 1023u); di[1] = jp0; di[2] = a.wi ? (it0 + (pb[p] & 1023u)) / a.wi : 0; di[3] = 1u | (ty << 8);
     } else {
       di[3] = 0;
     }
@@ -620,9 +622,9 @@ __global__ void __launch_bounds__(F_NT) k_fused(FusedArgs a) {
 }
 
 size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP) {
-  const uint32_t SW = T / 32 + 2;
-  size_t b = (size_t)R * (T + 1) * 4 + (size_t)R * SW * 4 + 4 /*align*/ + (size_t)R * 16 + (size_t)(DP + TP) * 8 +
-             (size_t)R * 8 + (size_t)T * 4 * 6 + (size_t)T * 2 + (size_t)T * 2 * 4 + (size_t)T * 2;
+  const uint32_t SW = T / 32 + 2, G = TP > DP ? TP : DP;
+  size_t b = (size_t)R * T * 4 + (size_t)(DP + TP) * 8 + (size_t)R * 8 + (size_t)T * G * 4 + (size_t)R * SW * 4 +
+             (size_t)R * CROLES * 4 + (size_t)T * 8 + (size_t)R * 8 + (size_t)T * 2 + (size_t)T * 8 + (size_t)T * 2;
   return (b + 15) & ~size_t(15);
 }
 
@@ -630,9 +632,10 @@ int launch_fused(Ctx& c) {
   FusedArgs a;
   a.dur = c.d_dur; a.kind = c.d_kind; a.meta = c.d_meta; a.comm = c.d_comm; a.pay = c.d_pay;
   a.rank_off = c.rank_off.as<uint64_t>(); a.TP = c.TP; a.DP = c.DP; a.PP = c.PP; a.W = c.W; a.n_comms = c.n_comms;
-  a.T = c.FT; a.R = c.FR; a.n_ftiles = c.n_ftiles; a.aligned = c.rows_aligned;
+  a.T = c.FT; a.R = c.FR; a.n_ftiles = c.n_ftiles; a.G = (uint32_t)std::max(c.TP, c.DP); a.aligned = c.rows_aligned;
   a.st_tile0 = c.st_tile0.as<uint32_t>(); a.st_npos = c.st_npos.as<uint32_t>(); a.ft_base = c.ft_base.as<uint32_t>();
-  a.role_comm = c.role_comm.as<uint32_t>(); a.role_slot = c.role_slot.as<uint32_t>(); a.role_type = c.role_type.as<uint8_t>();
+  a.posA = c.ft_posA.as<uint32_t>(); a.posB = c.ft_posB.as<uint32_t>(); a.posK = c.ft_posK.as<uint16_t>();
+  a.role_comm = c.role_comm.as<uint32_t>(); a.role_slot = c.role_slot.as<uint32_t>();
   a.ncroles = c.ncroles.as<uint32_t>(); a.coff = c.coff.as<uint64_t>();
   a.ch_base = c.ch_base.as<uint64_t>(); a.ch_slot = c.ch_slot.as<uint64_t>(); a.bitmap = c.bitmap.as<uint32_t>();
   a.bitpre = c.bitpre.as<uint32_t>(); a.comm_off = c.r_comm_off.as<uint64_t>(); a.comp_off = c.r_comp_off.as<uint64_t>();
