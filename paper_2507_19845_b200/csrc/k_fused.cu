@@ -392,43 +392,60 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
       if (((A >> 30) & 1u) && (ty == TY_TP || ty == TY_DP) && a.mode == 0 && jp0 < j0) dpos = (int32_t)p;
     }
   }
-  // ---- (3) verify every rank row against the template (kind_op; communicator / peer of the role)
+  // ---- (3) verify every rank row against the template (kind_op; communicator / peer of the role).
+  // Units of (row, 128 positions); each lane checks 4 consecutive events. VU units are loaded
+  // before any is checked so that every warp keeps VU x 24 B per lane in flight.
   {
+    constexpr int VU = 4;
     const uint32_t nch = (np + 127) / 128;
-    for (uint32_t wq = wid; wq < R * nch; wq += F_NT / 32) {
-      const uint32_t row = wq / nch, ch = wq % nch;
-      const uint32_t r = sbase + row;
-      const uint32_t pbase = ch * 128 + lane * 4;
-      const uint64_t g = a.rank_off[r] + p0 + pbase;
-      uint16_t ko[4]; uint32_t cm[4];
-      if (a.aligned && pbase + 4 <= np) {
-        const uint2 kv = __ldg(reinterpret_cast<const uint2*>(a.kind + g));
-        const uint4 cv = __ldg(reinterpret_cast<const uint4*>(a.comm + g));
-        ko[0] = (uint16_t)kv.x; ko[1] = (uint16_t)(kv.x >> 16); ko[2] = (uint16_t)kv.y; ko[3] = (uint16_t)(kv.y >> 16);
-        cm[0] = cv.x; cm[1] = cv.y; cm[2] = cv.z; cm[3] = cv.w;
-      } else {
+    const uint32_t units = R * nch;
+    bool mis = false;
+    for (uint32_t ub = wid; ub < units; ub += VU * (F_NT / 32)) {
+      uint2 kv[VU]; uint4 cv[VU];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const bool v = pbase + i < np;
-          ko[i] = v ? a.kind[g + i] : 0; cm[i] = v ? a.comm[g + i] : 0;
-        }
-      }
-      bool mis = false;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t p = pbase + i;
-        if (p < np) {
-          const uint16_t tko = pk[p];
-          if (ko[i] != tko) mis = true;
-          if (tko & 7u) {
-            const uint32_t role = (pb[p] >> 20) & 31u;
-            if (role < 16) mis |= cm[i] != rcs[row * CROLES + role];
-            else mis |= (int)cm[i] != (int)r + ((int)(role & 7u) - 4) * (int)R;
+      for (int u = 0; u < VU; ++u) {
+        const uint32_t wq = ub + u * (F_NT / 32);
+        kv[u] = make_uint2(0, 0); cv[u] = make_uint4(0, 0, 0, 0);
+        if (wq < units) {
+          const uint32_t row = wq / nch, ch = wq % nch;
+          const uint32_t pbase = ch * 128 + lane * 4;
+          const uint64_t g = a.rank_off[sbase + row] + p0 + pbase;
+          if (a.aligned && pbase + 4 <= np) {
+            kv[u] = __ldg(reinterpret_cast<const uint2*>(a.kind + g));
+            cv[u] = __ldg(reinterpret_cast<const uint4*>(a.comm + g));
+          } else if (pbase < np) {
+            uint16_t k4[4] = {0, 0, 0, 0}; uint32_t c4[4] = {0, 0, 0, 0};
+            for (uint32_t i = 0; i < 4 && pbase + i < np; ++i) { k4[i] = a.kind[g + i]; c4[i] = a.comm[g + i]; }
+            kv[u] = make_uint2(k4[0] | ((uint32_t)k4[1] << 16), k4[2] | ((uint32_t)k4[3] << 16));
+            cv[u] = make_uint4(c4[0], c4[1], c4[2], c4[3]);
           }
         }
       }
-      if (__any_sync(0xFFFFFFFFu, mis) && lane == 0) bad = 1;
+#pragma unroll
+      for (int u = 0; u < VU; ++u) {
+        const uint32_t wq = ub + u * (F_NT / 32);
+        if (wq >= units) continue;
+        const uint32_t row = wq / nch, ch = wq % nch;
+        const uint32_t r = sbase + row;
+        const uint32_t pbase = ch * 128 + lane * 4;
+        const uint16_t ko[4] = {(uint16_t)kv[u].x, (uint16_t)(kv[u].x >> 16), (uint16_t)kv[u].y, (uint16_t)(kv[u].y >> 16)};
+        const uint32_t cm[4] = {cv[u].x, cv[u].y, cv[u].z, cv[u].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t p = pbase + i;
+          if (p < np) {
+            const uint16_t tko = pk[p];
+            if (ko[i] != tko) mis = true;
+            if (tko & 7u) {
+              const uint32_t role = (pb[p] >> 20) & 31u;
+              if (role < 16) mis |= cm[i] != rcs[row * CROLES + role];
+              else mis |= (int)cm[i] != (int)r + ((int)(role & 7u) - 4) * (int)R;
+            }
+          }
+        }
+      }
     }
+    if (__any_sync(0xFFFFFFFFu, mis) && lane == 0) bad = 1;
   }
   cp_async_wait_all();
   __syncthreads();
