@@ -86,7 +86,7 @@ static void release_all(Ctx& c) {
                     &c.lb_label, &c.lb_rkind, &c.lb_rrank, &c.lb_rsrc, &c.lb_depth, &c.lb_twait, &c.scratch,
                     &c.st_tile0, &c.st_npos, &c.role_comm, &c.role_slot, &c.role_type, &c.ncroles, &c.ft_cols,
                     &c.ft_base, &c.ft_last, &c.st_tot, &c.sci, &c.sit, &c.dlate, &c.dinfo, &c.ft_posA, &c.ft_posB,
-                    &c.ft_posK};
+                    &c.ft_posK, &c.eidx};
   for (DevBuf* b : bufs) b->release();
 }
 
@@ -255,11 +255,31 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
       }
       stnp[s] = (uint32_t)ns;
     }
+    uint32_t ncrm = 1;
+    for (int s = 0; s < topo->pp; ++s) ncrm = std::max(ncrm, ncr[s]);
+    // edge slot of every TP-group / DP-group partner in the rank's collective neighbour list
+    std::vector<uint32_t> eidx;
+    if (ok) {
+      const int TPn = topo->tp, DPn = topo->dp, E = TPn + DPn;
+      eidx.assign((size_t)W * E, 0);
+      for (int r = 0; r < W && ok; ++r) {
+        const int t = r % TPn, d = (r / TPn) % DPn, s = r / (TPn * DPn);
+        for (int q = 0; q < E; ++q) {
+          const int partner = q < TPn ? (q + TPn * (d + DPn * s)) : (t + TPn * ((q - TPn) + DPn * s));
+          if (partner == r) continue;
+          auto b0 = nb.begin() + nbo[r], b1 = nb.begin() + nbo[r + 1];
+          auto it = std::lower_bound(b0, b1, (uint32_t)partner);
+          eidx[(size_t)r * E + q] = (it != b1 && *it == (uint32_t)partner) ? (uint32_t)(it - nb.begin()) : 0u;
+        }
+      }
+    }
     if (ok) {
       uint32_t T = (16384u / R) / 32u * 32u;
       T = std::max(64u, std::min(1024u, T));
       // two CTAs per SM: keep the fused kernel's shared memory under ~110 KB
-      while (T > 64 && fused_smem_bytes(T, R, topo->tp, topo->dp) > 110u * 1024u) T -= 32;
+      while (T > 64 && fused_smem_bytes(T, R, topo->tp, topo->dp, ncrm) > 110u * 1024u) T -= 32;
+      c.NCRM = ncrm;
+      if ((st = upload(c, c.eidx, eidx))) return st;
       uint32_t nt = 0;
       for (int s = 0; s < topo->pp; ++s) { stt0[s] = nt; nt += (stnp[s] + T - 1) / T; }
       stt0[topo->pp] = nt;

@@ -135,6 +135,8 @@ struct Ctx {
   DevBuf dlate, dinfo;                   // deferred stage-2 positions (first comm position of a tile)
   bool rows_aligned = false;
   bool force_general = false;
+  uint32_t NCRM = 1;                     // max collective roles of a rank over the stages
+  DevBuf eidx;                           // [W][TP+DP] edge slot of each TP-/DP-group partner
   // optional per-kernel timing
   bool timing = false;
   struct Pending { int k; cudaEvent_t a, b; };
@@ -301,7 +303,7 @@ int launch_instance_export(Ctx& c, scan_output which, void* dst);
 int launch_fused_prepass(Ctx& c);
 int launch_fused_census(Ctx& c);
 int launch_fused(Ctx& c);
-size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP);
+size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM);
 int launch_cross_reduce(Ctx& c);
 int launch_deferred(Ctx& c);
 

@@ -257,7 +257,8 @@ struct FusedArgs {
   const uint64_t* rank_off; int TP, DP, PP, W; uint32_t n_comms; uint32_t T, R, n_ftiles, G; bool aligned;
   const uint32_t* st_tile0; const uint32_t* st_npos; const uint32_t* ft_base;
   const uint32_t* posA; const uint32_t* posB; const uint16_t* posK;
-  const uint32_t* role_comm; const uint32_t* role_slot; const uint32_t* ncroles;
+  const uint32_t* role_comm; const uint32_t* role_slot; const uint32_t* ncroles; uint32_t NCRM;
+  const uint32_t* eidx;  // [W][TP+DP] wait-for edge slot of each TP-group / DP-group partner
   const uint64_t* coff;
   const uint64_t* ch_base; const uint64_t* ch_slot; const uint32_t* bitmap; const uint32_t* bitpre;
   const uint64_t* comm_off; const uint64_t* comp_off; const uint64_t* bits_off;
@@ -315,13 +316,16 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   const uint32_t T = a.T, R = a.R, TP = (uint32_t)a.TP, DP = (uint32_t)a.DP, G = a.G;
   const uint32_t SW = T / 32 + 2;
   // ---- shared memory carve-up (see fused_smem_bytes)
+  const uint32_t E = TP + DP, NCRM = a.NCRM;
   uint32_t* sd = (uint32_t*)smem_raw;                                   // R x T (swizzled)
   unsigned long long* gsum = (unsigned long long*)(sd + (uint64_t)R * T);  // DP + TP
   unsigned long long* coffr = gsum + DP + TP;                           // R comm offsets
-  uint32_t* sinst = (uint32_t*)(coffr + R);                             // T x G
+  unsigned long long* sedge = coffr + R;                                // R x (TP+DP) wait-for weights
+  unsigned long long* rcb = sedge + (uint64_t)R * E;                    // R x NCRM channel bases
+  uint32_t* sinst = (uint32_t*)(rcb + (uint64_t)R * NCRM);              // T x G
   uint32_t* sbits = sinst + (uint64_t)T * G;                            // R x SW
-  uint32_t* rcs = sbits + (uint64_t)R * SW;                             // R x CROLES
-  uint32_t* pa = rcs + (uint64_t)R * CROLES;                            // T
+  uint32_t* rcs = sbits + (uint64_t)R * SW;                             // R x NCRM
+  uint32_t* pa = rcs + (uint64_t)R * NCRM;                              // T
   uint32_t* pb = pa + T;                                                // T
   uint32_t* sjoin = pb + T;                                             // R
   uint32_t* slate = sjoin + R;                                          // R
@@ -338,15 +342,17 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   uint32_t s = 0;
   while (s + 1 < (uint32_t)a.PP && a.st_tile0[s + 1] <= tile) ++s;
   const uint32_t p0 = (tile - a.st_tile0[s]) * T;
-  const uint32_t np = min(T, a.st_npos[s] - p0);
+  const uint32_t npos = a.st_npos[s];
+  const uint32_t np = min(T, npos - p0);
   const uint32_t sbase = s * R;
   const uint64_t n = a.n_ftiles;
+  const uint64_t rbase = a.rank_off[sbase];  // SPMD stage: equal counts, rank_off[sbase+row] = rbase + row*npos
 
   // ---- (1) stream the duration rows of all R ranks into shared memory (async, 16 B granules)
   const uint32_t ngr = (np + 3) / 4;
   for (uint32_t i = tid; i < R * ngr; i += F_NT) {
     const uint32_t row = i / ngr, gi = i % ngr;
-    const uint64_t g = a.rank_off[sbase + row] + p0 + 4 * gi;
+    const uint64_t g = rbase + (uint64_t)row * npos + p0 + 4 * gi;
     uint32_t* dst = sd + sw_idx(row, 4 * gi, T);
     if (a.aligned && 4 * gi + 4 <= np) {
       cp_async16(dst, a.dur + g);
@@ -369,9 +375,12 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   for (uint32_t i = tid; i < R * SW; i += F_NT) sbits[i] = 0;
   for (uint32_t i = tid; i < R; i += F_NT) { sjoin[i] = 0; slate[i] = 0; coffr[i] = a.comm_off[sbase + i]; }
   for (uint32_t i = tid; i < DP + TP; i += F_NT) gsum[i] = 0;
+  for (uint32_t i = tid; i < R * E; i += F_NT) sedge[i] = 0;
   for (uint32_t i = tid; i < R * ncr; i += F_NT) {
     const uint32_t row = i / ncr, ro = i % ncr;
-    rcs[row * CROLES + ro] = a.role_comm[(uint64_t)(sbase + row) * CROLES + ro];
+    const uint32_t cid = a.role_comm[(uint64_t)(sbase + row) * CROLES + ro];
+    rcs[row * NCRM + ro] = cid;
+    rcb[row * NCRM + ro] = a.ch_base[cid];
   }
   for (uint32_t p = tid; p < np; p += F_NT) {
     pa[p] = a.posA[(uint64_t)tile * T + p];
@@ -409,7 +418,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
         if (wq < units) {
           const uint32_t row = wq / nch, ch = wq % nch;
           const uint32_t pbase = ch * 128 + lane * 4;
-          const uint64_t g = a.rank_off[sbase + row] + p0 + pbase;
+          const uint64_t g = rbase + (uint64_t)row * npos + p0 + pbase;
           if (a.aligned && pbase + 4 <= np) {
             kv[u] = __ldg(reinterpret_cast<const uint2*>(a.kind + g));
             cv[u] = __ldg(reinterpret_cast<const uint4*>(a.comm + g));
@@ -438,7 +447,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
             if (ko[i] != tko) mis = true;
             if (tko & 7u) {
               const uint32_t role = (pb[p] >> 20) & 31u;
-              if (role < 16) mis |= cm[i] != rcs[row * CROLES + role];
+              if (role < 16) mis |= cm[i] != rcs[row * NCRM + role];
               else mis |= (int)cm[i] != (int)r + ((int)(role & 7u) - 4) * (int)R;
             }
           }
@@ -511,8 +520,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
       const uint32_t nm = istp ? TP : DP, stride = istp ? 1u : TP, row0 = istp ? TP * g : g;
       const uint32_t A = pa[p], B = pb[p];
       const uint32_t role = (B >> 20) & 31u;
-      const uint32_t cid = rcs[row0 * CROLES + role];
-      const uint64_t inst = a.ch_base[cid] + kbase[role] + ((B >> 10) & 1023u);
+      const uint64_t inst = rcb[row0 * NCRM + role] + kbase[role] + ((B >> 10) & 1023u);
       uint32_t dmin = 0xFFFFFFFFu, dmax = 0, ls = 0, nat = 0;
       for (uint32_t q = 0; q < nm; ++q) {
         const uint32_t d = sd[sw_idx(row0 + q * stride, p, T)];
@@ -535,7 +543,11 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
         const uint32_t idx = sw_idx(row, p, T);
         const uint32_t wait = sd[idx] - dmin;
         sd[idx] = wait;  // the duration tile now holds the wait at in-block comm positions
-        if (q != ls && (unsigned long long)wait > a.wait_margin) add_edge(a, r, last, win, wait);
+        if (q != ls && (unsigned long long)wait > a.wait_margin) {
+          const uint32_t slot = istp ? ls : TP + ls;  // partner = TP-group member ls / DP-group member ls
+          if (win == w_tile) atomicAdd(&sedge[row * E + slot], (unsigned long long)wait);
+          else atomicAdd(&a.ew[(uint64_t)win * a.nnz_tot + a.eidx[(uint64_t)r * E + slot]], (unsigned long long)wait);
+        }
         if (!elig) continue;
         const bool lt = q == ls && late_ok;
         if ((int32_t)p == dpos) {
@@ -552,11 +564,11 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
       const uint32_t p = lst[3 * T + x / R], row = x % R, r = sbase + row;
       const uint32_t A = pa[p], B = pb[p];
       const uint32_t role = (B >> 20) & 31u;
-      const uint64_t e = a.rank_off[r] + p0 + p;
+      const uint64_t e = rbase + (uint64_t)row * npos + p0 + p;
       uint64_t ch; uint32_t nm, slot;
       bool send = false;
       if (role < 16) {
-        const uint32_t cid = rcs[row * CROLES + role];
+        const uint32_t cid = rcs[row * NCRM + role];
         ch = cid; nm = (uint32_t)(a.coff[cid + 1] - a.coff[cid]); slot = a.role_slot[(uint64_t)r * CROLES + role];
       } else {
         const int ds = (int)(role & 7u) - 4;
@@ -617,6 +629,10 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
       if (slate[row]) atomicAdd(&a.wl_late[(uint64_t)w_tile * a.W + r], slate[row]);
     }
   }
+  for (uint32_t i = tid; i < R * E; i += F_NT) {
+    const unsigned long long v = sedge[i];
+    if (v) atomicAdd(&a.ew[(uint64_t)w_tile * a.nnz_tot + a.eidx[(uint64_t)sbase * E + i]], v);
+  }
   if (nc) {
     const uint32_t w_first = j0 >> 5, w_last = (j0 + nc - 1) >> 5;
     const uint32_t nw = w_last - w_first + 1;
@@ -638,10 +654,11 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   }
 }
 
-size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP) {
+size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM) {
   const uint32_t SW = T / 32 + 2, G = TP > DP ? TP : DP;
-  size_t b = (size_t)R * T * 4 + (size_t)(DP + TP) * 8 + (size_t)R * 8 + (size_t)T * G * 4 + (size_t)R * SW * 4 +
-             (size_t)R * CROLES * 4 + (size_t)T * 8 + (size_t)R * 8 + (size_t)T * 2 + (size_t)T * 8 + (size_t)T * 2;
+  size_t b = (size_t)R * T * 4 + (size_t)(DP + TP) * 8 + (size_t)R * 8 + (size_t)R * (TP + DP) * 8 +
+             (size_t)R * NCRM * 8 + (size_t)T * G * 4 + (size_t)R * SW * 4 + (size_t)R * NCRM * 4 + (size_t)T * 8 +
+             (size_t)R * 8 + (size_t)T * 2 + (size_t)T * 8 + (size_t)T * 2;
   return (b + 15) & ~size_t(15);
 }
 
@@ -653,7 +670,7 @@ int launch_fused(Ctx& c) {
   a.st_tile0 = c.st_tile0.as<uint32_t>(); a.st_npos = c.st_npos.as<uint32_t>(); a.ft_base = c.ft_base.as<uint32_t>();
   a.posA = c.ft_posA.as<uint32_t>(); a.posB = c.ft_posB.as<uint32_t>(); a.posK = c.ft_posK.as<uint16_t>();
   a.role_comm = c.role_comm.as<uint32_t>(); a.role_slot = c.role_slot.as<uint32_t>();
-  a.ncroles = c.ncroles.as<uint32_t>(); a.coff = c.coff.as<uint64_t>();
+  a.ncroles = c.ncroles.as<uint32_t>(); a.NCRM = c.NCRM; a.eidx = c.eidx.as<uint32_t>(); a.coff = c.coff.as<uint64_t>();
   a.ch_base = c.ch_base.as<uint64_t>(); a.ch_slot = c.ch_slot.as<uint64_t>(); a.bitmap = c.bitmap.as<uint32_t>();
   a.bitpre = c.bitpre.as<uint32_t>(); a.comm_off = c.r_comm_off.as<uint64_t>(); a.comp_off = c.r_comp_off.as<uint64_t>();
   a.bits_off = c.r_bits_off.as<uint64_t>(); a.inst_c = c.inst_c.as<uint32_t>(); a.wait_c = c.wait_c.as<uint32_t>();
@@ -670,7 +687,7 @@ int launch_fused(Ctx& c) {
   a.wi = c.dcfg.window_iters; a.classes = c.lcfg.stage2_classes; a.mode = c.lcfg.stage2_mode;
   a.late_margin = c.lcfg.late_margin_ns; a.wait_margin = c.lcfg.wait_margin_ns; a.want_ref = c.dcfg.want_ref ? 1 : 0;
   a.cnt = c.counters.as<Counters>();
-  const size_t sm = fused_smem_bytes(c.FT, c.FR, c.TP, c.DP);
+  const size_t sm = fused_smem_bytes(c.FT, c.FR, c.TP, c.DP, c.NCRM);
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     kern<<<c.n_ftiles, F_NT, sm, c.stream>>>(a);
