@@ -310,6 +310,11 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
+// q = x / d by multiply-high with m = ceil(2^32 / d); exact for x < 2^22 and d <= 1024 (x * (m*d - 2^32) < 2^32).
+struct FDiv { uint32_t d, m; };
+__device__ __forceinline__ FDiv fdiv_make(uint32_t d) { return FDiv{d, d <= 1 ? 0u : (uint32_t)((0x100000000ull + d - 1) / d)}; }
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, FDiv f) { return f.d <= 1 ? x : __umulhi(x, f.m); }
+
 template <int P>
 __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -326,12 +331,12 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   uint32_t* sbits = sinst + (uint64_t)T * G;                            // R x SW
   uint32_t* rcs = sbits + (uint64_t)R * SW;                             // R x NCRM
   uint32_t* pa = rcs + (uint64_t)R * NCRM;                              // T
-  uint32_t* pb = pa + T;                                                // T
+  uint32_t* pb = pa + T;                                                // T  (later: verification descriptor)
   uint32_t* sjoin = pb + T;                                             // R
   uint32_t* slate = sjoin + R;                                          // R
-  uint16_t* pk = (uint16_t*)(slate + R);                                // T (template kind_op)
+  uint16_t* pk = (uint16_t*)(((uintptr_t)(slate + R) + 7) & ~(uintptr_t)7);  // T (template kind_op), 8 B aligned
   uint16_t* lst = pk + T;                                               // 4 x T
-  uint16_t* cl = lst + 4 * T;                                           // T (comm positions by m)
+  uint16_t* cl = lst + 4 * T;                                           // T: comm positions by m, | class << 14
   __shared__ uint32_t kbase[ROLES];
   __shared__ uint32_t nlist[4];
   __shared__ int32_t dpos;
@@ -347,20 +352,24 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   const uint32_t sbase = s * R;
   const uint64_t n = a.n_ftiles;
   const uint64_t rbase = a.rank_off[sbase];  // SPMD stage: equal counts, rank_off[sbase+row] = rbase + row*npos
+  const FDiv fTP = fdiv_make(TP), fDP = fdiv_make(DP), fR = fdiv_make(R);
 
   // ---- (1) stream the duration rows of all R ranks into shared memory (async, 16 B granules)
-  const uint32_t ngr = (np + 3) / 4;
-  for (uint32_t i = tid; i < R * ngr; i += F_NT) {
-    const uint32_t row = i / ngr, gi = i % ngr;
-    const uint64_t g = rbase + (uint64_t)row * npos + p0 + 4 * gi;
-    uint32_t* dst = sd + sw_idx(row, 4 * gi, T);
-    if (a.aligned && 4 * gi + 4 <= np) {
-      cp_async16(dst, a.dur + g);
-    } else {
-      for (uint32_t q = 0; q < 4; ++q) dst[q] = 4 * gi + q < np ? a.dur[g + q] : 0u;
+  {
+    const uint32_t ngr = (np + 3) / 4;
+    const FDiv fg = fdiv_make(ngr);
+    for (uint32_t i = tid; i < R * ngr; i += F_NT) {
+      const uint32_t row = fdiv(i, fg), gi = i - row * ngr;
+      const uint64_t g = rbase + (uint64_t)row * npos + p0 + 4 * gi;
+      uint32_t* dst = sd + sw_idx(row, 4 * gi, T);
+      if (a.aligned && 4 * gi + 4 <= np) {
+        cp_async16(dst, a.dur + g);
+      } else {
+        for (uint32_t q = 0; q < 4; ++q) dst[q] = 4 * gi + q < np ? a.dur[g + q] : 0u;
+      }
     }
+    asm volatile("cp.async.commit_group;\n" ::);
   }
-  asm volatile("cp.async.commit_group;\n" ::);
   // ---- (2) per-tile tables and template position info (from the pre-pass)
   const uint32_t j0 = a.ft_base[(uint64_t)ROLES * n + tile];
   const uint32_t m0 = a.ft_base[(uint64_t)(ROLES + 1) * n + tile];
@@ -377,15 +386,15 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   for (uint32_t i = tid; i < DP + TP; i += F_NT) gsum[i] = 0;
   for (uint32_t i = tid; i < R * E; i += F_NT) sedge[i] = 0;
   for (uint32_t i = tid; i < R * ncr; i += F_NT) {
-    const uint32_t row = i / ncr, ro = i % ncr;
+    const uint32_t row = i / ncr, ro = i - row * ncr;
     const uint32_t cid = a.role_comm[(uint64_t)(sbase + row) * CROLES + ro];
     rcs[row * NCRM + ro] = cid;
     rcb[row * NCRM + ro] = a.ch_base[cid];
   }
-  for (uint32_t p = tid; p < np; p += F_NT) {
-    pa[p] = a.posA[(uint64_t)tile * T + p];
-    pb[p] = a.posB[(uint64_t)tile * T + p];
-    pk[p] = a.posK[(uint64_t)tile * T + p];
+  for (uint32_t p = tid; p < T; p += F_NT) {
+    pa[p] = p < np ? a.posA[(uint64_t)tile * T + p] : 0u;
+    pb[p] = p < np ? a.posB[(uint64_t)tile * T + p] : 0u;
+    pk[p] = p < np ? a.posK[(uint64_t)tile * T + p] : (uint16_t)0;
   }
   __syncthreads();
   // position lists by type (order irrelevant), comm positions in m order, deferred position
@@ -397,16 +406,19 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
     const uint32_t sl = atomicAdd(&nlist[li], 1u);
     lst[li * T + sl] = (uint16_t)p;
     if (!isc) {
-      cl[(A >> 10) & 1023u] = (uint16_t)p;
+      cl[(A >> 10) & 1023u] = (uint16_t)(p | ((li - 1u) << 14));
       if (((A >> 30) & 1u) && (ty == TY_TP || ty == TY_DP) && a.mode == 0 && jp0 < j0) dpos = (int32_t)p;
     }
   }
-  // ---- (3) verify every rank row against the template (kind_op; communicator / peer of the role).
-  // Units of (row, 128 positions); each lane checks 4 consecutive events. VU units are loaded
-  // before any is checked so that every warp keeps VU x 24 B per lane in flight.
+  __syncthreads();
+  // ---- (3) verify every rank row against the template: kind_op equal, and the comm field equal to
+  // the communicator of the role (collectives) / the peer of the role (P2P). Verification descriptor
+  // per position (in pb's place is not possible: pb is needed later) -> vd: 0 none, 1|role<<2 coll,
+  // 2|(delta*R + 2^20)<<2 P2P; stored in the high bits of a private register table per unit.
   {
     constexpr int VU = 4;
     const uint32_t nch = (np + 127) / 128;
+    const FDiv fch = fdiv_make(nch);
     const uint32_t units = R * nch;
     bool mis = false;
     for (uint32_t ub = wid; ub < units; ub += VU * (F_NT / 32)) {
@@ -416,7 +428,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
         const uint32_t wq = ub + u * (F_NT / 32);
         kv[u] = make_uint2(0, 0); cv[u] = make_uint4(0, 0, 0, 0);
         if (wq < units) {
-          const uint32_t row = wq / nch, ch = wq % nch;
+          const uint32_t row = fdiv(wq, fch), ch = wq - row * nch;
           const uint32_t pbase = ch * 128 + lane * 4;
           const uint64_t g = rbase + (uint64_t)row * npos + p0 + pbase;
           if (a.aligned && pbase + 4 <= np) {
@@ -434,22 +446,21 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
       for (int u = 0; u < VU; ++u) {
         const uint32_t wq = ub + u * (F_NT / 32);
         if (wq >= units) continue;
-        const uint32_t row = wq / nch, ch = wq % nch;
-        const uint32_t r = sbase + row;
+        const uint32_t row = fdiv(wq, fch), ch = wq - row * nch;
         const uint32_t pbase = ch * 128 + lane * 4;
-        const uint16_t ko[4] = {(uint16_t)kv[u].x, (uint16_t)(kv[u].x >> 16), (uint16_t)kv[u].y, (uint16_t)(kv[u].y >> 16)};
+        if (pbase >= np) continue;
+        // template kinds of the 4 positions (pk is 8-byte aligned at pbase: pbase % 4 == 0)
+        const uint2 tk2 = *reinterpret_cast<const uint2*>(pk + pbase);
+        mis |= (kv[u].x != tk2.x) | (kv[u].y != tk2.y);
+        const uint32_t tkv[4] = {tk2.x & 0xFFFFu, tk2.x >> 16, tk2.y & 0xFFFFu, tk2.y >> 16};
         const uint32_t cm[4] = {cv[u].x, cv[u].y, cv[u].z, cv[u].w};
+        const uint32_t r = sbase + row;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const uint32_t p = pbase + i;
-          if (p < np) {
-            const uint16_t tko = pk[p];
-            if (ko[i] != tko) mis = true;
-            if (tko & 7u) {
-              const uint32_t role = (pb[p] >> 20) & 31u;
-              if (role < 16) mis |= cm[i] != rcs[row * NCRM + role];
-              else mis |= (int)cm[i] != (int)r + ((int)(role & 7u) - 4) * (int)R;
-            }
+          if (tkv[i] & 7u) {
+            const uint32_t role = (pb[pbase + i] >> 20) & 31u;
+            const uint32_t expect = role < 16 ? rcs[row * NCRM + role] : (uint32_t)((int)r + ((int)(role & 7u) - 4) * (int)R);
+            mis |= cm[i] != expect;
           }
         }
       }
@@ -465,11 +476,15 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
     const int q = ((int)DP - 2) / 2;
     const int L = P / 2 - 1 - q;  // low sentinels put s[q], s[q+1] at the fixed indices P/2-1, P/2
     for (uint32_t it = tid; it < nc * TP; it += F_NT) {
-      const uint32_t p = lst[it / TP], tp = it % TP;
+      const uint32_t pi = fdiv(it, fTP), tp = it - pi * TP;
+      const uint32_t p = lst[pi];
+      const uint32_t pq = p & ~3u, pr = p & 3u;
       uint32_t x[P], v[P];
 #pragma unroll
       for (int d = 0; d < P; ++d) {
-        x[d] = d < (int)DP ? sd[sw_idx(tp + TP * d, p, T)] : 0xFFFFFFFFu;
+        const uint32_t row = tp + TP * (uint32_t)d;
+        const uint32_t sw4 = ((row ^ (row >> 3)) & 7u) << 2;
+        x[d] = d < (int)DP ? sd[row * T + (pq ^ sw4) + pr] : 0xFFFFFFFFu;
         v[d] = d < (int)DP ? x[d] : (d < (int)DP + L ? 0u : 0xFFFFFFFFu);
       }
 #pragma unroll
@@ -487,6 +502,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
           }
       const uint32_t va = v[P / 2 - 1], vb = v[P / 2];
       const uint32_t j = j0 + (pa[p] & 1023u);
+      const uint32_t jw = (j >> 5) - wb, jb = 1u << (j & 31);
 #pragma unroll
       for (int d = 0; d < P; ++d) {
         if (d < (int)DP) {
@@ -495,7 +511,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
           const bool slow = (unsigned long long)a.slow_den * du > (unsigned long long)a.slow_num * ref &&
                             du > (unsigned long long)ref + a.slow_margin;
           const uint32_t row = tp + TP * d;
-          if (slow) atomicOr(&sbits[row * SW + (j >> 5) - wb], 1u << (j & 31));
+          if (slow) atomicOr(&sbits[row * SW + jw], jb);
           if (a.want_ref) a.cref[a.comp_off[sbase + row] + j] = ref;
         }
       }
@@ -515,15 +531,18 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   for (uint32_t it = tid; it < I3; it += F_NT) {
     if (it < I2) {
       const bool istp = it < I1;
-      const uint32_t p = istp ? lst[T + it / DP] : lst[2 * T + (it - I1) / TP];
-      const uint32_t g = istp ? it % DP : (it - I1) % TP;
+      uint32_t p, g;
+      if (istp) { const uint32_t pi = fdiv(it, fDP); g = it - pi * DP; p = lst[T + pi]; }
+      else { const uint32_t x = it - I1, pi = fdiv(x, fTP); g = x - pi * TP; p = lst[2 * T + pi]; }
       const uint32_t nm = istp ? TP : DP, stride = istp ? 1u : TP, row0 = istp ? TP * g : g;
       const uint32_t A = pa[p], B = pb[p];
       const uint32_t role = (B >> 20) & 31u;
       const uint64_t inst = rcb[row0 * NCRM + role] + kbase[role] + ((B >> 10) & 1023u);
+      const uint32_t pq = p & ~3u, pr = p & 3u;
       uint32_t dmin = 0xFFFFFFFFu, dmax = 0, ls = 0, nat = 0;
       for (uint32_t q = 0; q < nm; ++q) {
-        const uint32_t d = sd[sw_idx(row0 + q * stride, p, T)];
+        const uint32_t row = row0 + q * stride;
+        const uint32_t d = sd[row * T + (pq ^ (((row ^ (row >> 3)) & 7u) << 2)) + pr];
         if (d < dmin) { dmin = d; ls = q; nat = 1; } else if (d == dmin) ++nat;
         dmax = max(dmax, d);
       }
@@ -538,15 +557,15 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
       const bool late_ok = nat == 1 && (unsigned long long)(dmax - dmin) > a.late_margin;
       const uint32_t jp = j0 + (A & 1023u);
       const uint32_t jprev = ((A >> 30) & 1u) ? jp0 : j0 + ((A >> 20) & 1023u);
+      const uint32_t eslot = istp ? ls : TP + ls;  // partner slot of the last arriver
       for (uint32_t q = 0; q < nm; ++q) {
-        const uint32_t row = row0 + q * stride, r = sbase + row;
-        const uint32_t idx = sw_idx(row, p, T);
+        const uint32_t row = row0 + q * stride;
+        const uint32_t idx = row * T + (pq ^ (((row ^ (row >> 3)) & 7u) << 2)) + pr;
         const uint32_t wait = sd[idx] - dmin;
         sd[idx] = wait;  // the duration tile now holds the wait at in-block comm positions
         if (q != ls && (unsigned long long)wait > a.wait_margin) {
-          const uint32_t slot = istp ? ls : TP + ls;  // partner = TP-group member ls / DP-group member ls
-          if (win == w_tile) atomicAdd(&sedge[row * E + slot], (unsigned long long)wait);
-          else atomicAdd(&a.ew[(uint64_t)win * a.nnz_tot + a.eidx[(uint64_t)r * E + slot]], (unsigned long long)wait);
+          if (win == w_tile) atomicAdd(&sedge[row * E + eslot], (unsigned long long)wait);
+          else atomicAdd(&a.ew[(uint64_t)win * a.nnz_tot + a.eidx[(uint64_t)(sbase + row) * E + eslot]], (unsigned long long)wait);
         }
         if (!elig) continue;
         const bool lt = q == ls && late_ok;
@@ -557,11 +576,16 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
         const bool pslow = a.mode ? true : sbits_any(sbits + row * SW, wb, jprev, jp);
         if (!pslow) continue;
         if (win == w_tile) { atomicAdd(&sjoin[row], 1u); if (lt) atomicAdd(&slate[row], 1u); }
-        else { atomicAdd(&a.wl_joined[(uint64_t)win * a.W + r], 1u); if (lt) atomicAdd(&a.wl_late[(uint64_t)win * a.W + r], 1u); }
+        else {
+          const uint32_t r = sbase + row;
+          atomicAdd(&a.wl_joined[(uint64_t)win * a.W + r], 1u);
+          if (lt) atomicAdd(&a.wl_late[(uint64_t)win * a.W + r], 1u);
+        }
       }
     } else {
       const uint32_t x = it - I2;
-      const uint32_t p = lst[3 * T + x / R], row = x % R, r = sbase + row;
+      const uint32_t pi = fdiv(x, fR), row = x - pi * R, r = sbase + row;
+      const uint32_t p = lst[3 * T + pi];
       const uint32_t A = pa[p], B = pb[p];
       const uint32_t role = (B >> 20) & 31u;
       const uint64_t e = rbase + (uint64_t)row * npos + p0 + p;
@@ -604,24 +628,28 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   for (uint32_t row = wid; row < R; row += F_NT / 32) {
     const uint32_t r = sbase + row;
     const uint64_t cb = coffr[row] + m0;
+    const uint32_t gt = fdiv(row, fTP), gd = row - gt * TP;
+    const uint32_t rT = row * T, sw4 = ((row ^ (row >> 3)) & 7u) << 2;
     unsigned long long scomp = 0, swait = 0;
     for (uint32_t j = lane; j < ncm; j += 32) {
-      const uint32_t p = cl[j];
-      const uint32_t ty = (pb[p] >> 25) & 7u;
-      const uint32_t v = sd[sw_idx(row, p, T)];
-      if (ty == TY_TP || ty == TY_DP) {
-        const uint32_t g = ty == TY_TP ? row / TP : row % TP;
-        a.inst_c[cb + j] = sinst[p * G + g];
+      const uint32_t cv = cl[j];
+      const uint32_t p = cv & 0x3FFFu, cls = cv >> 14;  // 0 TP, 1 DP, 2 cross
+      const uint32_t v = sd[rT + ((p & ~3u) ^ sw4) + (p & 3u)];
+      if (cls < 2) {
+        a.inst_c[cb + j] = sinst[p * G + (cls == 0 ? gt : gd)];
         a.wait_c[cb + j] = v;
         swait += v;
       } else {
         a.inst_c[cb + j] = v;
       }
     }
-    for (uint32_t q = lane; q < nc; q += 32) scomp += sd[sw_idx(row, lst[q], T)];
+    for (uint32_t q = lane; q < nc; q += 32) {
+      const uint32_t p = lst[q];
+      scomp += sd[rT + ((p & ~3u) ^ sw4) + (p & 3u)];
+    }
     scomp = warp_sum_u64(scomp); swait = warp_sum_u64(swait);
     if (lane == 0) {
-      const unsigned long long tr = gsum[row / TP] + gsum[DP + row % TP];
+      const unsigned long long tr = gsum[gt] + gsum[DP + gd];
       if (scomp) atomicAdd(&a.rk_sum[r], scomp);
       if (swait) atomicAdd(&a.rk_sum[a.W + r], swait);
       if (tr) atomicAdd(&a.rk_sum[2 * a.W + r], tr);
@@ -637,7 +665,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
     const uint32_t w_first = j0 >> 5, w_last = (j0 + nc - 1) >> 5;
     const uint32_t nw = w_last - w_first + 1;
     for (uint32_t i = tid; i < R * nw; i += F_NT) {
-      const uint32_t row = i / nw, w = w_first + i % nw;
+      const uint32_t row = i / nw, w = w_first + (i - row * nw);
       const uint32_t v = sbits[row * SW + (w - wb)];
       if (v) atomicOr(&a.bits[a.bits_off[sbase + row] + w], v);
     }
@@ -658,7 +686,7 @@ size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32
   const uint32_t SW = T / 32 + 2, G = TP > DP ? TP : DP;
   size_t b = (size_t)R * T * 4 + (size_t)(DP + TP) * 8 + (size_t)R * 8 + (size_t)R * (TP + DP) * 8 +
              (size_t)R * NCRM * 8 + (size_t)T * G * 4 + (size_t)R * SW * 4 + (size_t)R * NCRM * 4 + (size_t)T * 8 +
-             (size_t)R * 8 + (size_t)T * 2 + (size_t)T * 8 + (size_t)T * 2;
+             (size_t)R * 8 + (size_t)T * 2 + (size_t)T * 8 + (size_t)T * 2 + 8;
   return (b + 15) & ~size_t(15);
 }
 
