@@ -86,7 +86,7 @@ static void release_all(Ctx& c) {
                     &c.lb_label, &c.lb_rkind, &c.lb_rrank, &c.lb_rsrc, &c.lb_depth, &c.lb_twait, &c.scratch,
                     &c.st_tile0, &c.st_npos, &c.role_comm, &c.role_slot, &c.role_type, &c.ncroles, &c.ft_cols,
                     &c.ft_base, &c.ft_last, &c.st_tot, &c.sci, &c.sit, &c.dlate, &c.dinfo, &c.ft_posA, &c.ft_posB,
-                    &c.ft_posK, &c.eidx};
+                    &c.ft_posK, &c.eidx, &c.tile_stage};
   for (DevBuf* b : bufs) b->release();
 }
 
@@ -284,10 +284,14 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
       for (int s = 0; s < topo->pp; ++s) { stt0[s] = nt; nt += (stnp[s] + T - 1) / T; }
       stt0[topo->pp] = nt;
       c.FT = T; c.FR = R; c.n_ftiles = nt; c.h_st_tile0 = stt0; c.h_st_npos = stnp; c.rows_aligned = aligned;
+      std::vector<uint8_t> tstage(nt);
+      for (int s = 0; s < topo->pp; ++s) for (uint32_t t = stt0[s]; t < stt0[s + 1]; ++t) tstage[t] = (uint8_t)s;
+      if (topo->pp > 255) ok = false;
+      if ((st = upload(c, c.tile_stage, tstage))) return st;
       if ((st = upload(c, c.st_tile0, stt0)) || (st = upload(c, c.st_npos, stnp)) || (st = upload(c, c.role_comm, rcmm)) ||
           (st = upload(c, c.role_slot, rslt)) || (st = upload(c, c.role_type, rty)) || (st = upload(c, c.ncroles, ncr)))
         return st;
-      c.spmd = nt > 0;
+      c.spmd = ok && nt > 0;
     }
   }
   // event columns

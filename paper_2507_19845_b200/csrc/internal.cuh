@@ -137,6 +137,7 @@ struct Ctx {
   bool force_general = false;
   uint32_t NCRM = 1;                     // max collective roles of a rank over the stages
   DevBuf eidx;                           // [W][TP+DP] edge slot of each TP-/DP-group partner
+  DevBuf tile_stage;                     // [n_ftiles] stage of each fused tile (u8)
   // optional per-kernel timing
   bool timing = false;
   struct Pending { int k; cudaEvent_t a, b; };

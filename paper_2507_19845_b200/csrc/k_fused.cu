@@ -252,10 +252,18 @@ int launch_fused_census(Ctx& c) {
 }
 
 // ----------------------------------------------------------------------------- F1 fused tile kernel
+// q = x / d by multiply-high with m = ceil(2^32 / d); exact for x < 2^22 and d <= 1024 (x * (m*d - 2^32) < 2^32).
+struct FDiv { uint32_t d, m; };
+__host__ __device__ __forceinline__ FDiv fdiv_make(uint32_t d) {
+  return FDiv{d, d <= 1 ? 0u : (uint32_t)((0x100000000ull + d - 1) / d)};
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, FDiv f) { return f.d <= 1 ? x : __umulhi(x, f.m); }
+
 struct FusedArgs {
   const uint32_t* dur; const uint16_t* kind; const uint16_t* meta; const uint32_t* comm; const uint32_t* pay;
   const uint64_t* rank_off; int TP, DP, PP, W; uint32_t n_comms; uint32_t T, R, n_ftiles, G; bool aligned;
-  const uint32_t* st_tile0; const uint32_t* st_npos; const uint32_t* ft_base;
+  const uint32_t* st_tile0; const uint32_t* st_npos; const uint32_t* ft_base; const uint8_t* tile_stage;
+  FDiv fTP, fDP, fR, fG, fCH;
   const uint32_t* posA; const uint32_t* posB; const uint16_t* posK;
   const uint32_t* role_comm; const uint32_t* role_slot; const uint32_t* ncroles; uint32_t NCRM;
   const uint32_t* eidx;  // [W][TP+DP] wait-for edge slot of each TP-group / DP-group partner
@@ -310,11 +318,6 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
-// q = x / d by multiply-high with m = ceil(2^32 / d); exact for x < 2^22 and d <= 1024 (x * (m*d - 2^32) < 2^32).
-struct FDiv { uint32_t d, m; };
-__device__ __forceinline__ FDiv fdiv_make(uint32_t d) { return FDiv{d, d <= 1 ? 0u : (uint32_t)((0x100000000ull + d - 1) / d)}; }
-__device__ __forceinline__ uint32_t fdiv(uint32_t x, FDiv f) { return f.d <= 1 ? x : __umulhi(x, f.m); }
-
 template <int P>
 __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -327,49 +330,55 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   unsigned long long* coffr = gsum + DP + TP;                           // R comm offsets
   unsigned long long* sedge = coffr + R;                                // R x (TP+DP) wait-for weights
   unsigned long long* rcb = sedge + (uint64_t)R * E;                    // R x NCRM channel bases
-  uint32_t* sinst = (uint32_t*)(rcb + (uint64_t)R * NCRM);              // T x G
+  unsigned long long* rsum = rcb + (uint64_t)R * NCRM;                  // R x 2: compute, in-block comm durations
+  uint32_t* sinst = (uint32_t*)(rsum + 2 * (uint64_t)R);                // T x G
   uint32_t* sbits = sinst + (uint64_t)T * G;                            // R x SW
   uint32_t* rcs = sbits + (uint64_t)R * SW;                             // R x NCRM
   uint32_t* pa = rcs + (uint64_t)R * NCRM;                              // T
-  uint32_t* pb = pa + T;                                                // T  (later: verification descriptor)
-  uint32_t* sjoin = pb + T;                                             // R
+  uint32_t* pb = pa + T;                                                // T
+  uint32_t* vd = pb + T;                                                // T verification descriptor
+  uint32_t* sgw = vd + T;                                               // T pslow segment: word lo | word hi << 16
+  uint32_t* sgm0 = sgw + T;                                             // T mask of the low word
+  uint32_t* sgm1 = sgm0 + T;                                            // T mask of the high word
+  uint32_t* sjoin = sgm1 + T;                                           // R
   uint32_t* slate = sjoin + R;                                          // R
-  uint16_t* pk = (uint16_t*)(((uintptr_t)(slate + R) + 7) & ~(uintptr_t)7);  // T (template kind_op), 8 B aligned
+  uint32_t* rslow = slate + R;                                          // R: row has a slow bit in this tile
+  uint8_t* gmask = (uint8_t*)(rslow + R);                               // T/4 granule masks: compute | in-block << 4
+  uint16_t* pk = (uint16_t*)(((uintptr_t)(gmask + T / 4) + 7) & ~(uintptr_t)7);  // T template kind_op, 8 B aligned
   uint16_t* lst = pk + T;                                               // 4 x T
   uint16_t* cl = lst + 4 * T;                                           // T: comm positions by m, | class << 14
   __shared__ uint32_t kbase[ROLES];
   __shared__ uint32_t nlist[4];
   __shared__ int32_t dpos;
-  __shared__ uint32_t bad;
+  __shared__ uint32_t bad, anyslow;
 
   const uint32_t tile = blockIdx.x;
   const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
-  uint32_t s = 0;
-  while (s + 1 < (uint32_t)a.PP && a.st_tile0[s + 1] <= tile) ++s;
+  const uint32_t s = a.tile_stage[tile];
   const uint32_t p0 = (tile - a.st_tile0[s]) * T;
   const uint32_t npos = a.st_npos[s];
   const uint32_t np = min(T, npos - p0);
   const uint32_t sbase = s * R;
   const uint64_t n = a.n_ftiles;
   const uint64_t rbase = a.rank_off[sbase];  // SPMD stage: equal counts, rank_off[sbase+row] = rbase + row*npos
-  const FDiv fTP = fdiv_make(TP), fDP = fdiv_make(DP), fR = fdiv_make(R);
+  const FDiv fTP = a.fTP, fDP = a.fDP, fR = a.fR;
+  const uint32_t ngr = (np + 3) / 4;
+  const uint32_t nch = (np + 127) / 128;
+  const FDiv fg = ngr == T / 4 ? a.fG : fdiv_make(ngr);
+  const FDiv fch = nch == (T + 127) / 128 ? a.fCH : fdiv_make(nch);
 
   // ---- (1) stream the duration rows of all R ranks into shared memory (async, 16 B granules)
-  {
-    const uint32_t ngr = (np + 3) / 4;
-    const FDiv fg = fdiv_make(ngr);
-    for (uint32_t i = tid; i < R * ngr; i += F_NT) {
-      const uint32_t row = fdiv(i, fg), gi = i - row * ngr;
-      const uint64_t g = rbase + (uint64_t)row * npos + p0 + 4 * gi;
-      uint32_t* dst = sd + sw_idx(row, 4 * gi, T);
-      if (a.aligned && 4 * gi + 4 <= np) {
-        cp_async16(dst, a.dur + g);
-      } else {
-        for (uint32_t q = 0; q < 4; ++q) dst[q] = 4 * gi + q < np ? a.dur[g + q] : 0u;
-      }
+  for (uint32_t i = tid; i < R * ngr; i += F_NT) {
+    const uint32_t row = fdiv(i, fg), gi = i - row * ngr;
+    const uint64_t g = rbase + (uint64_t)row * npos + p0 + 4 * gi;
+    uint32_t* dst = sd + row * T + (((4 * gi) ^ (((row ^ (row >> 3)) & 7u) << 2)));
+    if (a.aligned && 4 * gi + 4 <= np) {
+      cp_async16(dst, a.dur + g);
+    } else {
+      for (uint32_t q = 0; q < 4; ++q) dst[q] = 4 * gi + q < np ? a.dur[g + q] : 0u;
     }
-    asm volatile("cp.async.commit_group;\n" ::);
   }
+  asm volatile("cp.async.commit_group;\n" ::);
   // ---- (2) per-tile tables and template position info (from the pre-pass)
   const uint32_t j0 = a.ft_base[(uint64_t)ROLES * n + tile];
   const uint32_t m0 = a.ft_base[(uint64_t)(ROLES + 1) * n + tile];
@@ -380,11 +389,12 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   const uint32_t ncr = a.ncroles[s];
   if (tid < ROLES) kbase[tid] = a.ft_base[(uint64_t)tid * n + tile];
   if (tid < 4) nlist[tid] = 0;
-  if (tid == 0) { dpos = -1; bad = 0; }
+  if (tid == 0) { dpos = -1; bad = 0; anyslow = 0; }
   for (uint32_t i = tid; i < R * SW; i += F_NT) sbits[i] = 0;
   for (uint32_t i = tid; i < R; i += F_NT) { sjoin[i] = 0; slate[i] = 0; coffr[i] = a.comm_off[sbase + i]; }
   for (uint32_t i = tid; i < DP + TP; i += F_NT) gsum[i] = 0;
   for (uint32_t i = tid; i < R * E; i += F_NT) sedge[i] = 0;
+  for (uint32_t i = tid; i < T / 4; i += F_NT) gmask[i] = 0;
   for (uint32_t i = tid; i < R * ncr; i += F_NT) {
     const uint32_t row = i / ncr, ro = i - row * ncr;
     const uint32_t cid = a.role_comm[(uint64_t)(sbase + row) * CROLES + ro];
@@ -397,28 +407,41 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
     pk[p] = p < np ? a.posK[(uint64_t)tile * T + p] : (uint16_t)0;
   }
   __syncthreads();
-  // position lists by type (order irrelevant), comm positions in m order, deferred position
+  // position lists, comm positions in m order, verification descriptors, pslow segments, granule masks
   for (uint32_t p = tid; p < np; p += F_NT) {
     const uint32_t A = pa[p], B = pb[p];
-    const uint32_t ty = (B >> 25) & 7u;
+    const uint32_t ty = (B >> 25) & 7u, role = (B >> 20) & 31u;
     const bool isc = (pk[p] & 7u) == 0;
     const uint32_t li = isc ? 0u : (ty == TY_TP ? 1u : (ty == TY_DP ? 2u : 3u));
     const uint32_t sl = atomicAdd(&nlist[li], 1u);
     lst[li * T + sl] = (uint16_t)p;
-    if (!isc) {
+    if (isc) {
+      vd[p] = 0;
+      atomicOr((uint32_t*)(gmask + ((p >> 2) & ~3u)), 1u << (8 * ((p >> 2) & 3u) + (p & 3u)));
+    } else {
       cl[(A >> 10) & 1023u] = (uint16_t)(p | ((li - 1u) << 14));
-      if (((A >> 30) & 1u) && (ty == TY_TP || ty == TY_DP) && a.mode == 0 && jp0 < j0) dpos = (int32_t)p;
+      vd[p] = role < 16 ? (1u | (role << 2)) : (2u | ((uint32_t)(((int)(role & 7u) - 4) * (int)R + 0x100000) << 2));
+      if (li < 3) atomicOr((uint32_t*)(gmask + ((p >> 2) & ~3u)), 1u << (8 * ((p >> 2) & 3u) + 4 + (p & 3u)));
+      if (((A >> 30) & 1u) && li < 3 && a.mode == 0 && jp0 < j0) dpos = (int32_t)p;
+      const uint32_t jp = j0 + (A & 1023u);
+      const uint32_t jprev = ((A >> 30) & 1u) ? jp0 : j0 + ((A >> 20) & 1023u);
+      if (jprev < jp && jprev >= j0) {
+        const uint32_t w0 = jprev >> 5, w1 = (jp - 1) >> 5;
+        uint32_t m0_ = 0xFFFFFFFFu << (jprev & 31), m1_ = 0xFFFFFFFFu >> (31 - ((jp - 1) & 31));
+        if (w0 == w1) { m0_ &= m1_; m1_ = 0; }
+        sgw[p] = (w0 - wb) | ((w1 - wb) << 16);
+        sgm0[p] = m0_; sgm1[p] = m1_;   // segments span at most two words when shorter than 33 ops
+        if (w1 > w0 + 1) sgm0[p] = 0xFFFFFFFFu, sgm1[p] = 0xFFFFFFFFu, sgw[p] |= 0x80000000u;  // long: slow path
+      } else {
+        sgw[p] = 0; sgm0[p] = 0; sgm1[p] = 0;
+      }
     }
   }
   __syncthreads();
   // ---- (3) verify every rank row against the template: kind_op equal, and the comm field equal to
-  // the communicator of the role (collectives) / the peer of the role (P2P). Verification descriptor
-  // per position (in pb's place is not possible: pb is needed later) -> vd: 0 none, 1|role<<2 coll,
-  // 2|(delta*R + 2^20)<<2 P2P; stored in the high bits of a private register table per unit.
+  // the communicator of the role (collectives) / the peer of the role (P2P).
   {
     constexpr int VU = 4;
-    const uint32_t nch = (np + 127) / 128;
-    const FDiv fch = fdiv_make(nch);
     const uint32_t units = R * nch;
     bool mis = false;
     for (uint32_t ub = wid; ub < units; ub += VU * (F_NT / 32)) {
@@ -449,19 +472,17 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
         const uint32_t row = fdiv(wq, fch), ch = wq - row * nch;
         const uint32_t pbase = ch * 128 + lane * 4;
         if (pbase >= np) continue;
-        // template kinds of the 4 positions (pk is 8-byte aligned at pbase: pbase % 4 == 0)
         const uint2 tk2 = *reinterpret_cast<const uint2*>(pk + pbase);
         mis |= (kv[u].x != tk2.x) | (kv[u].y != tk2.y);
-        const uint32_t tkv[4] = {tk2.x & 0xFFFFu, tk2.x >> 16, tk2.y & 0xFFFFu, tk2.y >> 16};
+        const uint4 d4 = *reinterpret_cast<const uint4*>(vd + pbase);
+        const uint32_t dv[4] = {d4.x, d4.y, d4.z, d4.w};
         const uint32_t cm[4] = {cv[u].x, cv[u].y, cv[u].z, cv[u].w};
         const uint32_t r = sbase + row;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          if (tkv[i] & 7u) {
-            const uint32_t role = (pb[pbase + i] >> 20) & 31u;
-            const uint32_t expect = role < 16 ? rcs[row * NCRM + role] : (uint32_t)((int)r + ((int)(role & 7u) - 4) * (int)R);
-            mis |= cm[i] != expect;
-          }
+          const uint32_t t = dv[i] & 3u;
+          if (t == 1) mis |= cm[i] != rcs[row * NCRM + (dv[i] >> 2)];
+          else if (t == 2) mis |= cm[i] != r + (dv[i] >> 2) - 0x100000u;
         }
       }
     }
@@ -470,7 +491,26 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   cp_async_wait_all();
   __syncthreads();
   if (bad) { if (tid == 0) atomicOr(&a.cnt->overflow, NOT_SPMD); return; }
-  // ---- (4) phase A: stage 1 on every compute position (LOO lower median over the DP peers)
+  // per-rank sums of compute durations and in-block comm durations: one thread per row walks its
+  // row by 16-byte granules (granule masks from the template) — no cross-lane reductions
+  for (uint32_t row = tid; row < R; row += F_NT) {
+    const uint32_t rT = row * T, sw4 = ((row ^ (row >> 3)) & 7u) << 2;
+    unsigned long long sc = 0, si = 0;
+    for (uint32_t gi = 0; gi < ngr; ++gi) {
+      const uint32_t gm = gmask[gi];
+      if (!gm) continue;
+      const uint4 v = *reinterpret_cast<const uint4*>(sd + rT + ((4 * gi) ^ sw4));
+      const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if ((gm >> q) & 1u) sc += vv[q];
+        if ((gm >> (4 + q)) & 1u) si += vv[q];
+      }
+    }
+    rsum[2 * row] = sc; rsum[2 * row + 1] = si;
+  }
+  // ---- (4) phase A: stage 1 on every compute position (LOO lower median over the DP peers).
+  // Exact quick reject: if den*max <= num*min over the group, no member can be slow (ref >= min).
   const uint32_t nc = nlist[0];
   if (P >= 2) {
     const int q = ((int)DP - 2) / 2;
@@ -479,14 +519,20 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
       const uint32_t pi = fdiv(it, fTP), tp = it - pi * TP;
       const uint32_t p = lst[pi];
       const uint32_t pq = p & ~3u, pr = p & 3u;
-      uint32_t x[P], v[P];
+      uint32_t x[P];
+      uint32_t mn = 0xFFFFFFFFu, mx = 0;
 #pragma unroll
       for (int d = 0; d < P; ++d) {
         const uint32_t row = tp + TP * (uint32_t)d;
         const uint32_t sw4 = ((row ^ (row >> 3)) & 7u) << 2;
-        x[d] = d < (int)DP ? sd[row * T + (pq ^ sw4) + pr] : 0xFFFFFFFFu;
-        v[d] = d < (int)DP ? x[d] : (d < (int)DP + L ? 0u : 0xFFFFFFFFu);
+        x[d] = d < (int)DP ? sd[row * T + (pq ^ sw4) + pr] : 0u;
+        if (d < (int)DP) { mn = min(mn, x[d]); mx = max(mx, x[d]); }
       }
+      const bool maybe = (unsigned long long)a.slow_den * mx > (unsigned long long)a.slow_num * mn;
+      if (!maybe && !a.want_ref) continue;
+      uint32_t v[P];
+#pragma unroll
+      for (int d = 0; d < P; ++d) v[d] = d < (int)DP ? x[d] : (d < (int)DP + L ? 0u : 0xFFFFFFFFu);
 #pragma unroll
       for (int k = 2; k <= P; k <<= 1)
 #pragma unroll
@@ -508,10 +554,10 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
         if (d < (int)DP) {
           const uint32_t ref = x[d] > va ? va : vb;
           const unsigned long long du = x[d];
-          const bool slow = (unsigned long long)a.slow_den * du > (unsigned long long)a.slow_num * ref &&
+          const bool slow = maybe && (unsigned long long)a.slow_den * du > (unsigned long long)a.slow_num * ref &&
                             du > (unsigned long long)ref + a.slow_margin;
           const uint32_t row = tp + TP * d;
-          if (slow) atomicOr(&sbits[row * SW + jw], jb);
+          if (slow) { atomicOr(&sbits[row * SW + jw], jb); anyslow = 1; }
           if (a.want_ref) a.cref[a.comp_off[sbase + row] + j] = ref;
         }
       }
@@ -525,6 +571,14 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
     for (uint32_t row = 0; row < R; ++row) a.citer[(uint64_t)(sbase + row) * a.NIT1 + itp + 1] = v;
   }
   __syncthreads();
+  const bool tslow = anyslow != 0;
+  if (tslow)
+    for (uint32_t row = tid; row < R; row += F_NT) {
+      uint32_t o = 0;
+      for (uint32_t w = 0; w < SW; ++w) o |= sbits[row * SW + w];
+      rslow[row] = o != 0;
+    }
+  __syncthreads();
   // ---- (5) phase B: TP / DP instances (all members in the tile) and cross-stage scatters
   const uint32_t ntp = nlist[1], ndp = nlist[2], nx = nlist[3];
   const uint32_t I1 = ntp * DP, I2 = I1 + ndp * TP, I3 = I2 + nx * R;
@@ -535,7 +589,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
       if (istp) { const uint32_t pi = fdiv(it, fDP); g = it - pi * DP; p = lst[T + pi]; }
       else { const uint32_t x = it - I1, pi = fdiv(x, fTP); g = x - pi * TP; p = lst[2 * T + pi]; }
       const uint32_t nm = istp ? TP : DP, stride = istp ? 1u : TP, row0 = istp ? TP * g : g;
-      const uint32_t A = pa[p], B = pb[p];
+      const uint32_t B = pb[p];
       const uint32_t role = (B >> 20) & 31u;
       const uint64_t inst = rcb[row0 * NCRM + role] + kbase[role] + ((B >> 10) & 1023u);
       const uint32_t pq = p & ~3u, pr = p & 3u;
@@ -555,9 +609,10 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
       const uint32_t win = a.wi ? (it0 + (B & 1023u)) / a.wi : 0;
       const bool elig = (a.classes >> (cls - 1)) & 1u;
       const bool late_ok = nat == 1 && (unsigned long long)(dmax - dmin) > a.late_margin;
-      const uint32_t jp = j0 + (A & 1023u);
-      const uint32_t jprev = ((A >> 30) & 1u) ? jp0 : j0 + ((A >> 20) & 1023u);
       const uint32_t eslot = istp ? ls : TP + ls;  // partner slot of the last arriver
+      const bool isdef = (int32_t)p == dpos;
+      const bool chk = elig && (a.mode || tslow || isdef);
+      const uint32_t gw = sgw[p], g0 = sgm0[p], g1 = sgm1[p];
       for (uint32_t q = 0; q < nm; ++q) {
         const uint32_t row = row0 + q * stride;
         const uint32_t idx = row * T + (pq ^ (((row ^ (row >> 3)) & 7u) << 2)) + pr;
@@ -567,13 +622,22 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
           if (win == w_tile) atomicAdd(&sedge[row * E + eslot], (unsigned long long)wait);
           else atomicAdd(&a.ew[(uint64_t)win * a.nnz_tot + a.eidx[(uint64_t)(sbase + row) * E + eslot]], (unsigned long long)wait);
         }
-        if (!elig) continue;
+        if (!chk) continue;
         const bool lt = q == ls && late_ok;
-        if ((int32_t)p == dpos) {
+        if (isdef) {
           if (lt) atomicOr(&a.dlate[(uint64_t)tile * ((R + 31) / 32) + row / 32], 1u << (row & 31));
           continue;
         }
-        const bool pslow = a.mode ? true : sbits_any(sbits + row * SW, wb, jprev, jp);
+        bool pslow = a.mode != 0;
+        if (!pslow && rslow[row]) {
+          const uint32_t* sb = sbits + row * SW;
+          if (gw & 0x80000000u) {
+            const uint32_t jp = j0 + (pa[p] & 1023u);
+            pslow = sbits_any(sb, wb, ((pa[p] >> 30) & 1u) ? jp0 : j0 + ((pa[p] >> 20) & 1023u), jp);
+          } else {
+            pslow = (sb[gw & 0xFFFFu] & g0) | (sb[gw >> 16] & g1);
+          }
+        }
         if (!pslow) continue;
         if (win == w_tile) { atomicAdd(&sjoin[row], 1u); if (lt) atomicAdd(&slate[row], 1u); }
         else {
@@ -626,11 +690,9 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   // ---- (6) flush: coalesced per-rank inst / wait rows, per-rank sums, slow bits, counters
   const uint32_t ncm = nlist[1] + nlist[2] + nlist[3];
   for (uint32_t row = wid; row < R; row += F_NT / 32) {
-    const uint32_t r = sbase + row;
     const uint64_t cb = coffr[row] + m0;
     const uint32_t gt = fdiv(row, fTP), gd = row - gt * TP;
     const uint32_t rT = row * T, sw4 = ((row ^ (row >> 3)) & 7u) << 2;
-    unsigned long long scomp = 0, swait = 0;
     for (uint32_t j = lane; j < ncm; j += 32) {
       const uint32_t cv = cl[j];
       const uint32_t p = cv & 0x3FFFu, cls = cv >> 14;  // 0 TP, 1 DP, 2 cross
@@ -638,30 +700,26 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
       if (cls < 2) {
         a.inst_c[cb + j] = sinst[p * G + (cls == 0 ? gt : gd)];
         a.wait_c[cb + j] = v;
-        swait += v;
       } else {
         a.inst_c[cb + j] = v;
       }
     }
-    for (uint32_t q = lane; q < nc; q += 32) {
-      const uint32_t p = lst[q];
-      scomp += sd[rT + ((p & ~3u) ^ sw4) + (p & 3u)];
-    }
-    scomp = warp_sum_u64(scomp); swait = warp_sum_u64(swait);
-    if (lane == 0) {
-      const unsigned long long tr = gsum[gt] + gsum[DP + gd];
-      if (scomp) atomicAdd(&a.rk_sum[r], scomp);
-      if (swait) atomicAdd(&a.rk_sum[a.W + r], swait);
-      if (tr) atomicAdd(&a.rk_sum[2 * a.W + r], tr);
-      if (sjoin[row]) atomicAdd(&a.wl_joined[(uint64_t)w_tile * a.W + r], sjoin[row]);
-      if (slate[row]) atomicAdd(&a.wl_late[(uint64_t)w_tile * a.W + r], slate[row]);
-    }
+  }
+  for (uint32_t row = tid; row < R; row += F_NT) {
+    const uint32_t r = sbase + row;
+    const uint32_t gt = fdiv(row, fTP), gd = row - gt * TP;
+    const unsigned long long tr = gsum[gt] + gsum[DP + gd];
+    if (rsum[2 * row]) atomicAdd(&a.rk_sum[r], rsum[2 * row]);
+    if (rsum[2 * row + 1] - tr) atomicAdd(&a.rk_sum[a.W + r], rsum[2 * row + 1] - tr);
+    if (tr) atomicAdd(&a.rk_sum[2 * a.W + r], tr);
+    if (sjoin[row]) atomicAdd(&a.wl_joined[(uint64_t)w_tile * a.W + r], sjoin[row]);
+    if (slate[row]) atomicAdd(&a.wl_late[(uint64_t)w_tile * a.W + r], slate[row]);
   }
   for (uint32_t i = tid; i < R * E; i += F_NT) {
     const unsigned long long v = sedge[i];
     if (v) atomicAdd(&a.ew[(uint64_t)w_tile * a.nnz_tot + a.eidx[(uint64_t)sbase * E + i]], v);
   }
-  if (nc) {
+  if (nc && tslow) {
     const uint32_t w_first = j0 >> 5, w_last = (j0 + nc - 1) >> 5;
     const uint32_t nw = w_last - w_first + 1;
     for (uint32_t i = tid; i < R * nw; i += F_NT) {
@@ -685,8 +743,8 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
 size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM) {
   const uint32_t SW = T / 32 + 2, G = TP > DP ? TP : DP;
   size_t b = (size_t)R * T * 4 + (size_t)(DP + TP) * 8 + (size_t)R * 8 + (size_t)R * (TP + DP) * 8 +
-             (size_t)R * NCRM * 8 + (size_t)T * G * 4 + (size_t)R * SW * 4 + (size_t)R * NCRM * 4 + (size_t)T * 8 +
-             (size_t)R * 8 + (size_t)T * 2 + (size_t)T * 8 + (size_t)T * 2 + 8;
+             (size_t)R * NCRM * 8 + (size_t)R * 16 + (size_t)T * G * 4 + (size_t)R * SW * 4 + (size_t)R * NCRM * 4 +
+             (size_t)T * 4 * 6 + (size_t)R * 12 + (size_t)T / 4 + 8 + (size_t)T * 2 + (size_t)T * 8 + (size_t)T * 2;
   return (b + 15) & ~size_t(15);
 }
 
@@ -696,6 +754,9 @@ int launch_fused(Ctx& c) {
   a.rank_off = c.rank_off.as<uint64_t>(); a.TP = c.TP; a.DP = c.DP; a.PP = c.PP; a.W = c.W; a.n_comms = c.n_comms;
   a.T = c.FT; a.R = c.FR; a.n_ftiles = c.n_ftiles; a.G = (uint32_t)std::max(c.TP, c.DP); a.aligned = c.rows_aligned;
   a.st_tile0 = c.st_tile0.as<uint32_t>(); a.st_npos = c.st_npos.as<uint32_t>(); a.ft_base = c.ft_base.as<uint32_t>();
+  a.tile_stage = c.tile_stage.as<uint8_t>();
+  a.fTP = fdiv_make(c.TP); a.fDP = fdiv_make(c.DP); a.fR = fdiv_make(c.FR); a.fG = fdiv_make(c.FT / 4);
+  a.fCH = fdiv_make((c.FT + 127) / 128);
   a.posA = c.ft_posA.as<uint32_t>(); a.posB = c.ft_posB.as<uint32_t>(); a.posK = c.ft_posK.as<uint16_t>();
   a.role_comm = c.role_comm.as<uint32_t>(); a.role_slot = c.role_slot.as<uint32_t>();
   a.ncroles = c.ncroles.as<uint32_t>(); a.NCRM = c.NCRM; a.eidx = c.eidx.as<uint32_t>(); a.coff = c.coff.as<uint64_t>();
