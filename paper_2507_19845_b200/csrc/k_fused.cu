@@ -326,7 +326,8 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   // ---- shared memory carve-up (see fused_smem_bytes)
   const uint32_t E = TP + DP, NCRM = a.NCRM;
   uint32_t* sd = (uint32_t*)smem_raw;                                   // R x T (swizzled)
-  unsigned long long* gsum = (unsigned long long*)(sd + (uint64_t)R * T);  // DP + TP
+  uint32_t* vd = sd + (uint64_t)R * T;                                  // T verification descriptor (16 B aligned)
+  unsigned long long* gsum = (unsigned long long*)(vd + T);             // DP + TP
   unsigned long long* coffr = gsum + DP + TP;                           // R comm offsets
   unsigned long long* sedge = coffr + R;                                // R x (TP+DP) wait-for weights
   unsigned long long* rcb = sedge + (uint64_t)R * E;                    // R x NCRM channel bases
@@ -336,8 +337,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   uint32_t* rcs = sbits + (uint64_t)R * SW;                             // R x NCRM
   uint32_t* pa = rcs + (uint64_t)R * NCRM;                              // T
   uint32_t* pb = pa + T;                                                // T
-  uint32_t* vd = pb + T;                                                // T verification descriptor
-  uint32_t* sgw = vd + T;                                               // T pslow segment: word lo | word hi << 16
+  uint32_t* sgw = pb + T;                                               // T pslow segment: word lo | word hi << 16
   uint32_t* sgm0 = sgw + T;                                             // T mask of the low word
   uint32_t* sgm1 = sgm0 + T;                                            // T mask of the high word
   uint32_t* sjoin = sgm1 + T;                                           // R
