@@ -86,7 +86,7 @@ static void release_all(Ctx& c) {
                     &c.lb_label, &c.lb_rkind, &c.lb_rrank, &c.lb_rsrc, &c.lb_depth, &c.lb_twait, &c.scratch,
                     &c.st_tile0, &c.st_npos, &c.role_comm, &c.role_slot, &c.role_type, &c.ncroles, &c.ft_cols,
                     &c.ft_base, &c.ft_last, &c.st_tot, &c.sci, &c.sit, &c.dlate, &c.dinfo, &c.ft_posA, &c.ft_posB,
-                    &c.ft_posK, &c.eidx, &c.tile_stage};
+                    &c.ft_posK, &c.eidx, &c.tile_stage, &c.xbase};
   for (DevBuf* b : bufs) b->release();
 }
 
@@ -372,7 +372,7 @@ scan_status channels_and_buffers(Ctx& c, bool fused) {
   const uint64_t W = c.W;
   c.n_p2p = c.hc.n_p2p; c.NCH = c.n_comms + c.n_p2p; c.n_comm = c.hc.n_comm; c.n_comp = c.hc.n_comp;
   c.NIT = c.hc.max_niter; c.n_iters = c.hc.n_iters; c.max_ncomp = c.hc.max_ncomp; c.n_bits_words = c.hc.n_bits_words;
-  CK(c.ch_base.ensure((c.NCH + 1) * 8)); CK(c.ch_slot.ensure((c.NCH + 1) * 8));
+  CK(c.ch_base.ensure((c.NCH + 1) * 8)); CK(c.ch_slot.ensure((c.NCH + 1) * 8)); CK(c.xbase.ensure((c.NCH + 1) * 8));
   CK(c.ch_nsend.ensure(std::max<uint64_t>(2 * c.n_p2p, 1) * 4)); CK(c.ch_nrecv.ensure(std::max<uint64_t>(2 * c.n_p2p, 1) * 4));
   if (c.n_p2p) {
     CK(cudaMemsetAsync(c.ch_nsend.p, 0, 2 * c.n_p2p * 4, c.stream));
@@ -382,6 +382,7 @@ scan_status channels_and_buffers(Ctx& c, bool fused) {
   if ((st = sync_read(c))) return st;
   if (c.hc.n_instances >= 0xFFFFFFFFull) { c.err = "more than 2^32-1 instances"; return SCAN_E_UNSUPPORTED; }
   c.n_inst = c.hc.n_instances; c.n_slots = c.hc.n_slots; c.p2p_slot0 = c.hc.p2p_slot0; c.p2p_inst0 = c.hc.p2p_inst0;
+  c.n_xinst = c.hc.n_xinst;
   CK(c.inst_c.ensure(c.n_comm * 4)); CK(c.wait_c.ensure(c.n_comm * 4));
   if (!fused) { CK(c.cdur.ensure(c.n_comp * 4)); CK(c.cop.ensure(c.n_comp * 2)); }
   CK(c.sdur.ensure(c.n_slots * 4)); CK(c.skind.ensure(c.n_slots));
@@ -546,11 +547,16 @@ scan_status fused_all(Ctx& c) {
   z.n_link_slow = z.n_roots = z.n_victims = z.n_unattributed = 0;
   for (auto& v : z.v_count) v = 0;
   CK(cudaMemcpyAsync(c.counters.p, &z, sizeof(Counters), cudaMemcpyHostToDevice, c.stream));
+  {
+    const uint64_t items = (uint64_t)c.NW * c.W;
+    CK(cudaMemsetAsync(c.wd_total.p, 0, items * 4, c.stream));
+    CK(cudaMemsetAsync(c.wd_slow.p, 0, items * 4, c.stream));
+  }
   c.launches += timed(c, "k_class_counts", [&] { return launch_class_counts(c); });
   c.launches += timed(c, "k_fused", [&] { return launch_fused(c); });
   c.launches += timed(c, "k_cross_reduce", [&] { return launch_cross_reduce(c); });
   c.launches += timed(c, "k_deferred", [&] { return launch_deferred(c); });
-  c.launches += timed(c, "k_stage1_counts", [&] { return launch_stage1_counts(c); });
+  c.launches += timed(c, "k_wd_finish", [&] { return launch_wd_finish(c); });
   if ((st = sync_read(c))) return st;
   if (c.hc.overflow & 32u) return 2;
   c.matched = c.detected = true;

@@ -58,6 +58,7 @@ struct Counters {
   unsigned long long n_link_slow, n_roots, n_victims, n_unattributed;
   unsigned long long v_count[6];
   unsigned long long n_edges;
+  unsigned long long n_xinst;
 };
 
 struct Ctx {
@@ -138,6 +139,8 @@ struct Ctx {
   uint32_t NCRM = 1;                     // max collective roles of a rank over the stages
   DevBuf eidx;                           // [W][TP+DP] edge slot of each TP-/DP-group partner
   DevBuf tile_stage;                     // [n_ftiles] stage of each fused tile (u8)
+  DevBuf xbase;                          // [NCH+1] cross-stage instance index
+  uint64_t n_xinst = 0;
   // optional per-kernel timing
   bool timing = false;
   struct Pending { int k; cudaEvent_t a, b; };
@@ -307,5 +310,6 @@ int launch_fused(Ctx& c);
 size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM);
 int launch_cross_reduce(Ctx& c);
 int launch_deferred(Ctx& c);
+int launch_wd_finish(Ctx& c);
 
 }  // namespace ms

@@ -276,6 +276,7 @@ struct FusedArgs {
   uint32_t* citer; uint32_t NIT1;
   const uint64_t* nbc_off; const uint32_t* nbc; const uint32_t* nbp; const uint32_t* nbp_n; uint64_t nnz_tot, nnz_c;
   unsigned long long* ew; unsigned long long* rk_sum; uint32_t* wl_joined; uint32_t* wl_late;
+  uint32_t* wd_total; uint32_t* wd_slow;
   uint32_t* dlate; uint32_t* dinfo;
   uint32_t slow_num, slow_den; unsigned long long slow_margin;
   uint32_t wi, classes, mode; unsigned long long late_margin, wait_margin; int want_ref;
@@ -478,11 +479,13 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
         const uint32_t dv[4] = {d4.x, d4.y, d4.z, d4.w};
         const uint32_t cm[4] = {cv[u].x, cv[u].y, cv[u].z, cv[u].w};
         const uint32_t r = sbase + row;
+        const uint32_t* rc = rcs + row * NCRM;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint32_t t = dv[i] & 3u;
-          if (t == 1) mis |= cm[i] != rcs[row * NCRM + (dv[i] >> 2)];
-          else if (t == 2) mis |= cm[i] != r + (dv[i] >> 2) - 0x100000u;
+        for (int i = 0; i < 4; ++i) {  // branch-free: both expectations, select by descriptor type
+          const uint32_t t = dv[i] & 3u, x = dv[i] >> 2;
+          const uint32_t e1 = rc[t == 1 ? x : 0u];
+          const uint32_t e2 = r + x - 0x100000u;
+          mis |= (t != 0) & (cm[i] != (t == 1 ? e1 : e2));
         }
       }
     }
@@ -689,19 +692,39 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   __syncthreads();
   // ---- (6) flush: coalesced per-rank inst / wait rows, per-rank sums, slow bits, counters
   const uint32_t ncm = nlist[1] + nlist[2] + nlist[3];
-  for (uint32_t row = wid; row < R; row += F_NT / 32) {
-    const uint64_t cb = coffr[row] + m0;
-    const uint32_t gt = fdiv(row, fTP), gd = row - gt * TP;
-    const uint32_t rT = row * T, sw4 = ((row ^ (row >> 3)) & 7u) << 2;
-    for (uint32_t j = lane; j < ncm; j += 32) {
+  {
+    const FDiv fm = fdiv_make(ncm > 0 ? ncm : 1u);
+    for (uint32_t i = tid; i < R * ncm; i += F_NT) {  // consecutive threads: consecutive comm events of a rank
+      const uint32_t row = fdiv(i, fm), j = i - row * ncm;
+      const uint32_t gt = fdiv(row, fTP), gd = row - gt * TP;
       const uint32_t cv = cl[j];
       const uint32_t p = cv & 0x3FFFu, cls = cv >> 14;  // 0 TP, 1 DP, 2 cross
-      const uint32_t v = sd[rT + ((p & ~3u) ^ sw4) + (p & 3u)];
-      if (cls < 2) {
-        a.inst_c[cb + j] = sinst[p * G + (cls == 0 ? gt : gd)];
-        a.wait_c[cb + j] = v;
-      } else {
-        a.inst_c[cb + j] = v;
+      const uint32_t v = sd[row * T + ((p & ~3u) ^ (((row ^ (row >> 3)) & 7u) << 2)) + (p & 3u)];
+      const uint32_t si = sinst[cls < 2 ? p * G + (cls == 0 ? gt : gd) : 0u];
+      uint32_t* dst = a.inst_c + coffr[row] + m0 + j;
+      *dst = cls < 2 ? si : v;
+      if (cls < 2) a.wait_c[dst - a.inst_c] = v;
+    }
+  }
+  // stage-1 counters per (window, rank): total = compute positions of the tile, slow = its slow bits
+  const uint32_t it_last = it0 + (np ? (pb[np - 1] & 1023u) : 0u);
+  const bool one_window = !a.wi || (it0 / a.wi == it_last / a.wi);
+  if (P >= 2 && nc) {
+    if (one_window) {
+      for (uint32_t row = tid; row < R; row += F_NT) {
+        const uint32_t r = sbase + row;
+        uint32_t sl = 0;
+        if (tslow) for (uint32_t w = 0; w < SW; ++w) sl += __popc(sbits[row * SW + w]);
+        atomicAdd(&a.wd_total[(uint64_t)w_tile * a.W + r], nc);
+        if (sl) atomicAdd(&a.wd_slow[(uint64_t)w_tile * a.W + r], sl);
+      }
+    } else {
+      for (uint32_t i = tid; i < R * nc; i += F_NT) {
+        const uint32_t row = i / nc, p = lst[i - row * nc], r = sbase + row;
+        const uint32_t win = (it0 + (pb[p] & 1023u)) / a.wi;
+        const uint32_t j = j0 + (pa[p] & 1023u);
+        atomicAdd(&a.wd_total[(uint64_t)win * a.W + r], 1u);
+        if ((sbits[row * SW + (j >> 5) - wb] >> (j & 31)) & 1u) atomicAdd(&a.wd_slow[(uint64_t)win * a.W + r], 1u);
       }
     }
   }
@@ -771,6 +794,7 @@ int launch_fused(Ctx& c) {
   a.nbp_n = c.nbp_n.as<uint32_t>(); a.nnz_tot = c.nnz_c + (uint64_t)c.W * PCAP; a.nnz_c = c.nnz_c;
   a.ew = c.ewc.as<unsigned long long>(); a.rk_sum = c.rk_sum.as<unsigned long long>();
   a.wl_joined = c.wl_joined.as<uint32_t>(); a.wl_late = c.wl_late.as<uint32_t>();
+  a.wd_total = c.wd_total.as<uint32_t>(); a.wd_slow = c.wd_slow.as<uint32_t>();
   a.dlate = c.dlate.as<uint32_t>(); a.dinfo = c.dinfo.as<uint32_t>();
   a.slow_num = c.dcfg.slow_num; a.slow_den = c.dcfg.slow_den; a.slow_margin = c.dcfg.slow_margin_ns;
   a.wi = c.dcfg.window_iters; a.classes = c.lcfg.stage2_classes; a.mode = c.lcfg.stage2_mode;
@@ -795,7 +819,7 @@ int launch_fused(Ctx& c) {
 // communicator): integrity + decomposition (as k_inst_reduce), then the members' waits,
 // per-rank sums and wait-for edges from the slot arrays written by k_fused.
 struct XArgs {
-  uint64_t n_inst, NCH; uint32_t n_comms; int W;
+  uint64_t n_xinst, NCH; uint32_t n_comms; int W; const uint64_t* xbase;
   const uint64_t* ch_base; const uint64_t* ch_slot; const uint32_t* ch_nmin; const uint64_t* coff; const uint32_t* cmem;
   const uint8_t* ccls; const uint32_t* nsend; const uint32_t* nrecv; const uint32_t* psrc; const uint32_t* pdst;
   const uint32_t* r_nkeys; const uint32_t* r_keys; const uint32_t* r_cnt;
@@ -819,20 +843,23 @@ __device__ __forceinline__ void x_edge(const XArgs& a, uint32_t r, uint32_t L, u
 __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
   if (*((volatile unsigned*)&a.cnt->overflow) & NOT_SPMD) return;  // fused results void: general path reruns
   uint32_t inc = 0, kmis = 0, pmis = 0;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n_inst; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t ch = upper_bound_u64(a.ch_base, a.NCH + 1, i) - 1;
-    const bool isp = ch >= a.n_comms;
-    uint32_t cls = 0, nm = 2;
-    if (!isp) {
-      cls = a.ccls[ch];
-      if (cls == 1 || cls == 2) continue;  // TP / DP group: finished inside k_fused
-      nm = (uint32_t)(a.coff[ch + 1] - a.coff[ch]);
+  const uint32_t lane = lane_id();
+  const uint64_t wstride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t wbase = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wbase < a.n_xinst; wbase += wstride) {
+    const uint64_t xi = wbase + lane;
+    const bool act = xi < a.n_xinst;
+    uint64_t ch = 0, k = 0, i = 0;
+    if (act) {
+      ch = upper_bound_u64(a.xbase, a.NCH + 1, xi) - 1;
+      k = xi - a.xbase[ch];
+      i = a.ch_base[ch] + k;
     }
-    const uint64_t k = i - a.ch_base[ch];
+    // one channel across the whole warp (the common case): its members are the same for every lane
+    const uint64_t ch0 = __shfl_sync(0xFFFFFFFFu, ch, 0);
+    const bool uni = __all_sync(0xFFFFFFFFu, act && ch == ch0);
+    const bool isp = ch >= a.n_comms;
+    const uint32_t nm = isp ? 2u : (uint32_t)(a.coff[ch + 1] - a.coff[ch]);
     const uint64_t sb = a.ch_slot[ch] + k * nm;
-    uint32_t flags = 0;
-    if (isp && a.p2p_warm[i - a.p2p_inst0]) flags |= SCAN_F_WARMUP;
-    uint32_t dmin = 0, dmax = 0, last = NONE32;
     auto member = [&](uint32_t q) -> uint32_t {
       return isp ? (q == 0 ? a.psrc[ch - a.n_comms] : a.pdst[ch - a.n_comms]) : a.cmem[a.coff[ch] + q];
     };
@@ -843,45 +870,73 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
       const uint32_t p = lower_bound_u32(a.r_keys + (uint64_t)m * RCAP, C, (uint32_t)ch);
       return p < C && a.r_keys[(uint64_t)m * RCAP + p] == (uint32_t)ch && a.r_cnt[(uint64_t)m * RCAP + p] > k;
     };
+    uint32_t flags = 0, dmin = 0, dmax = 0, last = NONE32;
     bool valid = false;
-    if (k < a.ch_nmin[ch]) {
-      flags |= SCAN_F_COMPLETE;
-      bool kind_ok = true, pay_ok = true;
-      if (!isp) {
-        const uint8_t k0 = a.skind[sb];
-        for (uint32_t q = 1; q < nm; ++q) if (a.skind[sb + q] != k0) kind_ok = false;
-      } else {
-        pay_ok = a.p2p_pay[sb - a.p2p_slot0] == a.p2p_pay[sb + 1 - a.p2p_slot0];
-      }
-      if (kind_ok) flags |= SCAN_F_KIND_OK; else ++kmis;
-      if (pay_ok) flags |= SCAN_F_PAYLOAD_OK; else ++pmis;
-      if (kind_ok && pay_ok) {
-        valid = true;
-        flags |= SCAN_F_VALID;
-        dmin = NONE32;
-        uint32_t ls = 0, nat = 0;
-        for (uint32_t q = 0; q < nm; ++q) {
-          const uint32_t d = a.sdur[sb + q];
-          if (d < dmin) { dmin = d; ls = q; nat = 1; } else if (d == dmin) ++nat;
-          dmax = max(dmax, d);
+    if (act) {
+      if (isp && a.p2p_warm[i - a.p2p_inst0]) flags |= SCAN_F_WARMUP;
+      if (k < a.ch_nmin[ch]) {
+        flags |= SCAN_F_COMPLETE;
+        bool kind_ok = true, pay_ok = true;
+        if (!isp) {
+          const uint8_t k0 = a.skind[sb];
+          for (uint32_t q = 1; q < nm; ++q) if (a.skind[sb + q] != k0) kind_ok = false;
+        } else {
+          pay_ok = a.p2p_pay[sb - a.p2p_slot0] == a.p2p_pay[sb + 1 - a.p2p_slot0];
         }
-        if (nat == 1) flags |= SCAN_F_UNIQUE_LAST;
-        last = member(ls);
+        if (kind_ok) flags |= SCAN_F_KIND_OK; else ++kmis;
+        if (pay_ok) flags |= SCAN_F_PAYLOAD_OK; else ++pmis;
+        if (kind_ok && pay_ok) {
+          valid = true;
+          flags |= SCAN_F_VALID;
+          dmin = NONE32;
+          uint32_t ls = 0, nat = 0;
+          for (uint32_t q = 0; q < nm; ++q) {
+            const uint32_t d = a.sdur[sb + q];
+            if (d < dmin) { dmin = d; ls = q; nat = 1; } else if (d == dmin) ++nat;
+            dmax = max(dmax, d);
+          }
+          if (nat == 1) flags |= SCAN_F_UNIQUE_LAST;
+          last = member(ls);
+        }
+      } else {
+        ++inc;
       }
-    } else {
-      ++inc;
+      a.rec[i] = make_uint4(dmin, dmax, last, flags | ((isp ? 0u : a.ccls[ch]) << 8));
     }
-    a.rec[i] = make_uint4(dmin, dmax, last, flags | (cls << 8));
-    for (uint32_t q = 0; q < nm; ++q) {
-      if (!(flags & SCAN_F_COMPLETE) && !present(q)) continue;
-      const uint32_t ci = a.sci[sb + q];
-      if (!valid) { a.wait_c[ci] = 0; continue; }
-      const uint32_t m = member(q);
-      const uint32_t wait = a.sdur[sb + q] - dmin;
-      a.wait_c[ci] = wait;
-      if (wait) atomicAdd(&a.rk_sum[a.W + m], (unsigned long long)wait);
-      if (dmin) atomicAdd(&a.rk_sum[2 * a.W + m], (unsigned long long)dmin);
-      if (m != last && (unsigned long long)wait > a.wait_margin) x_edge(a, m, last, a.wi ? a.sit[sb + q] / a.wi : 0, wait);
+    if (uni) {
+      // aggregated per-member sums (members identical across lanes)
+      for (uint32_t q = 0; q < nm; ++q) {
+        unsigned long long w = 0, t = 0;
+        if (act && (flags & SCAN_F_COMPLETE || present(q))) {
+          const uint32_t ci = a.sci[sb + q];
+          if (!valid) a.wait_c[ci] = 0;
+          else {
+            const uint32_t m = member(q);
+            const uint32_t wait = a.sdur[sb + q] - dmin;
+            a.wait_c[ci] = wait;
+            w = wait; t = dmin;
+            if (m != last && (unsigned long long)wait > a.wait_margin) x_edge(a, m, last, a.wi ? a.sit[sb + q] / a.wi : 0, wait);
+          }
+        }
+        w = warp_sum_u64(w); t = warp_sum_u64(t);
+        if (lane == 0) {
+          const uint32_t m = member(q);
+          if (w) atomicAdd(&a.rk_sum[a.W + m], w);
+          if (t) atomicAdd(&a.rk_sum[2 * a.W + m], t);
+        }
+      }
+    } else if (act) {
+      for (uint32_t q = 0; q < nm; ++q) {
+        if (!(flags & SCAN_F_COMPLETE) && !present(q)) continue;
+        const uint32_t ci = a.sci[sb + q];
+        if (!valid) { a.wait_c[ci] = 0; continue; }
+        const uint32_t m = member(q);
+        const uint32_t wait = a.sdur[sb + q] - dmin;
+        a.wait_c[ci] = wait;
+        if (wait) atomicAdd(&a.rk_sum[a.W + m], (unsigned long long)wait);
+        if (dmin) atomicAdd(&a.rk_sum[2 * a.W + m], (unsigned long long)dmin);
+        if (m != last && (unsigned long long)wait > a.wait_margin) x_edge(a, m, last, a.wi ? a.sit[sb + q] / a.wi : 0, wait);
+      }
     }
   }
   inc = warp_sum_u32(inc); kmis = warp_sum_u32(kmis); pmis = warp_sum_u32(pmis);
@@ -893,8 +948,7 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
 }
 
 int launch_cross_reduce(Ctx& c) {
-  if (c.n_inst == 0) return 0;
-  XArgs a{c.n_inst, c.NCH, c.n_comms, c.W, c.ch_base.as<uint64_t>(), c.ch_slot.as<uint64_t>(), c.ch_nmin.as<uint32_t>(),
+  XArgs a{c.n_xinst, c.NCH, c.n_comms, c.W, c.xbase.as<uint64_t>(), c.ch_base.as<uint64_t>(), c.ch_slot.as<uint64_t>(), c.ch_nmin.as<uint32_t>(),
           c.coff.as<uint64_t>(), c.cmem.as<uint32_t>(), c.ccls.as<uint8_t>(), c.ch_nsend.as<uint32_t>(),
           c.ch_nrecv.as<uint32_t>(), c.ch_nsend.as<uint32_t>() + c.n_p2p, c.ch_nrecv.as<uint32_t>() + c.n_p2p,
           c.r_nkeys.as<uint32_t>(), c.r_keys.as<uint32_t>(), c.r_cnt.as<uint32_t>(), c.sdur.as<uint32_t>(),
@@ -903,7 +957,8 @@ int launch_cross_reduce(Ctx& c) {
           c.nbc_off.as<uint64_t>(), c.nbc.as<uint32_t>(), c.nbp.as<uint32_t>(), c.nbp_n.as<uint32_t>(),
           c.nnz_c + (uint64_t)c.W * PCAP, c.nnz_c, c.ewc.as<unsigned long long>(), c.rk_sum.as<unsigned long long>(),
           c.dcfg.window_iters, (unsigned long long)c.lcfg.wait_margin_ns, c.counters.as<Counters>()};
-  unsigned blocks = (unsigned)std::min<uint64_t>((c.n_inst + 255) / 256, 148ull * 16);
+  if (c.n_xinst == 0) return 0;
+  unsigned blocks = (unsigned)std::min<uint64_t>((c.n_xinst + 255) / 256, 148ull * 16);
   k_cross_reduce<<<blocks, 256, 0, c.stream>>>(a);
   return 1;
 }
@@ -953,4 +1008,29 @@ int launch_deferred(Ctx& c) {
   return 1;
 }
 
+}  // namespace ms
+
+namespace ms {
+// Stage-1 verdict inputs per (window, rank) from the counters k_fused accumulated.
+__global__ void k_wd_finish(uint64_t items, const uint32_t* wd_total, const uint32_t* wd_slow, uint8_t* wd_cand,
+                            double* wd_frac, uint32_t cand_num, uint32_t cand_den, uint32_t min_samples, Counters* cnt) {
+  const uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= items) return;
+  const uint32_t total = wd_total[it], slow = wd_slow[it];
+  const bool cand = total >= min_samples && (unsigned long long)cand_den * slow > (unsigned long long)cand_num * total;
+  wd_cand[it] = cand ? 1 : 0;
+  wd_frac[it] = total ? (double)slow / (double)total : 0.0;
+  if (total) atomicAdd(&cnt->n_compared, (unsigned long long)total);
+  if (slow) atomicAdd(&cnt->n_slow, (unsigned long long)slow);
+  if (cand) atomicAdd(&cnt->n_candidates, 1ull);
+}
+
+int launch_wd_finish(Ctx& c) {
+  const uint64_t items = (uint64_t)c.NW * c.W;
+  k_wd_finish<<<(unsigned)((items + 255) / 256), 256, 0, c.stream>>>(items, c.wd_total.as<uint32_t>(), c.wd_slow.as<uint32_t>(),
+                                                                     c.wd_cand.as<uint8_t>(), c.wd_frac.as<double>(),
+                                                                     c.dcfg.cand_num, c.dcfg.cand_den, c.dcfg.min_samples,
+                                                                     c.counters.as<Counters>());
+  return 1;
+}
 }  // namespace ms

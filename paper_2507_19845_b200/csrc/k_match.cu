@@ -438,6 +438,37 @@ __global__ void k_channel_tail(uint32_t n_comms, const uint64_t* base, const uin
   cnt->p2p_slot0 = slot[n_comms];
 }
 
+// Index of the cross-stage instances (every channel except TP-/DP-class communicators): exclusive
+// scan of their instance counts, so k_cross_reduce runs over exactly those instances.
+__global__ void __launch_bounds__(RP_NT) k_cross_index(uint32_t n_comms, uint64_t NCH, const uint8_t* ccls,
+                                                       const uint32_t* nmax, uint64_t* xbase, Counters* cnt) {
+  __shared__ unsigned long long sm[32];
+  __shared__ unsigned long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+  for (uint64_t b = 0; b < NCH; b += RP_NT) {
+    const uint64_t ch = b + threadIdx.x;
+    unsigned long long v = 0;
+    if (ch < NCH) v = (ch >= n_comms || (ccls[ch] != 1 && ccls[ch] != 2)) ? nmax[ch] : 0;
+    unsigned long long inc = v;
+    for (int o = 1; o < 32; o <<= 1) { unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, inc, o); if (lane >= (uint32_t)o) inc += t; }
+    if (lane == 31) sm[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      unsigned long long x = sm[lane], xi = x;
+      for (int o = 1; o < 32; o <<= 1) { unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, xi, o); if (lane >= (uint32_t)o) xi += t; }
+      sm[lane] = xi - x;
+    }
+    __syncthreads();
+    if (ch < NCH) xbase[ch] = carry + sm[wid] + inc - v;
+    __syncthreads();
+    if (threadIdx.x == RP_NT - 1) carry += sm[wid] + inc;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { xbase[NCH] = carry; cnt->n_xinst = carry; }
+}
+
 int launch_p2p_channels(Ctx& c) {
   int n = 0;
   if (c.n_p2p) {
@@ -451,7 +482,9 @@ int launch_p2p_channels(Ctx& c) {
                                         c.ch_nmin.as<uint32_t>(), c.ch_nsend.as<uint32_t>(), c.ch_nrecv.as<uint32_t>(),
                                         c.ch_base.as<uint64_t>(), c.ch_slot.as<uint64_t>(), c.counters.as<Counters>());
   k_channel_tail<<<1, 1, 0, c.stream>>>(c.n_comms, c.ch_base.as<uint64_t>(), c.ch_slot.as<uint64_t>(), c.counters.as<Counters>());
-  return n + 2;
+  k_cross_index<<<1, RP_NT, 0, c.stream>>>(c.n_comms, c.NCH, c.ccls.as<uint8_t>(), c.ch_nmax.as<uint32_t>(),
+                                           c.xbase.as<uint64_t>(), c.counters.as<Counters>());
+  return n + 3;
 }
 
 // ----------------------------------------------------------------------------- K1c assign

@@ -160,13 +160,17 @@ __device__ __forceinline__ uint32_t iter_start(const uint32_t* citer_r, uint32_t
   return i > NIT ? ncomp : citer_r[i];
 }
 
-__global__ void k_stage1_counts(int W, int TP, int DP, uint32_t NW, uint32_t wi, uint32_t NIT,
-                                const uint32_t* r_ncomp, const uint64_t* r_bits_off, const uint32_t* bits,
-                                const uint32_t* citer, const uint32_t* cl_J, uint32_t* wd_total, uint32_t* wd_slow,
-                                uint8_t* wd_cand, double* wd_frac, uint32_t cand_num, uint32_t cand_den,
-                                uint32_t min_samples, Counters* cnt) {
-  const uint64_t item = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// One warp per (window, rank): popcount of the slow bits in the window's compute range, lanes
+// striding over the bit words.
+__global__ void __launch_bounds__(256) k_stage1_counts(int W, int TP, int DP, uint32_t NW, uint32_t wi, uint32_t NIT,
+                                                       const uint32_t* r_ncomp, const uint64_t* r_bits_off,
+                                                       const uint32_t* bits, const uint32_t* citer, const uint32_t* cl_J,
+                                                       uint32_t* wd_total, uint32_t* wd_slow, uint8_t* wd_cand,
+                                                       double* wd_frac, uint32_t cand_num, uint32_t cand_den,
+                                                       uint32_t min_samples, Counters* cnt) {
+  const uint64_t item = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (item >= (uint64_t)NW * W) return;
+  const uint32_t lane = lane_id();
   const uint32_t w = (uint32_t)(item / W), r = (uint32_t)(item % W);
   const uint32_t ncomp = r_ncomp[r];
   uint32_t J = 0;
@@ -179,7 +183,19 @@ __global__ void k_stage1_counts(int W, int TP, int DP, uint32_t NW, uint32_t wi,
   if (wi) { lo = iter_start(citer_r, NIT, ncomp, (uint64_t)w * wi); hi = iter_start(citer_r, NIT, ncomp, (uint64_t)(w + 1) * wi); }
   hi = min(hi, J);
   const uint32_t total = hi > lo ? hi - lo : 0;
-  const uint32_t slow = bits_count(bits + r_bits_off[r], lo, hi);
+  uint32_t slow = 0;
+  if (total) {
+    const uint32_t* b = bits + r_bits_off[r];
+    const uint32_t w0 = lo >> 5, w1 = (hi - 1) >> 5;
+    for (uint32_t x = w0 + lane; x <= w1; x += 32) {
+      uint32_t m = b[x];
+      if (x == w0) m &= 0xFFFFFFFFu << (lo & 31);
+      if (x == w1) m &= 0xFFFFFFFFu >> (31 - ((hi - 1) & 31));
+      slow += __popc(m);
+    }
+    slow = warp_sum_u32(slow);
+  }
+  if (lane) return;
   const bool cand = total >= min_samples && (unsigned long long)cand_den * slow > (unsigned long long)cand_num * total;
   wd_total[item] = total; wd_slow[item] = slow; wd_cand[item] = cand ? 1 : 0;
   wd_frac[item] = total ? (double)slow / (double)total : 0.0;
@@ -190,7 +206,7 @@ __global__ void k_stage1_counts(int W, int TP, int DP, uint32_t NW, uint32_t wi,
 
 int launch_stage1_counts(Ctx& c) {
   const uint64_t items = (uint64_t)c.NW * c.W;
-  k_stage1_counts<<<(unsigned)((items + 255) / 256), 256, 0, c.stream>>>(
+  k_stage1_counts<<<(unsigned)((items + 7) / 8), 256, 0, c.stream>>>(
       c.W, c.TP, c.DP, c.NW, c.dcfg.window_iters, c.NIT, c.r_ncomp.as<uint32_t>(), c.r_bits_off.as<uint64_t>(),
       c.bits.as<uint32_t>(), c.citer.as<uint32_t>(), c.cl_J.as<uint32_t>(), c.wd_total.as<uint32_t>(),
       c.wd_slow.as<uint32_t>(), c.wd_cand.as<uint8_t>(), c.wd_frac.as<double>(), c.dcfg.cand_num, c.dcfg.cand_den,
@@ -390,6 +406,12 @@ struct LKArgs {
   Counters* cnt;
 };
 
+// Order key of a sample: the f64 ratio p/t (exactly rounded, monotone in the exact ratio) as
+// sortable bits; exact ties between distinct ratios with equal f64 are resolved afterwards.
+__device__ __forceinline__ unsigned long long ratio_key(uint32_t p, uint32_t t) {
+  return (unsigned long long)__double_as_longlong((double)p / (double)t);  // positive: bit order = value order
+}
+
 __global__ void __launch_bounds__(LK_NT) k_link_median(LKArgs a) {
   extern __shared__ uint32_t smem[];
   uint32_t* sp = smem;
@@ -397,6 +419,9 @@ __global__ void __launch_bounds__(LK_NT) k_link_median(LKArgs a) {
   uint32_t* si = smem + 2 * LINK_CAP;
   __shared__ uint32_t scan_sm[33];
   __shared__ uint32_t cnt_all, cnt_warm;
+  __shared__ uint32_t hist[256];
+  __shared__ unsigned long long s_prefix;
+  __shared__ uint32_t s_target, s_less, s_tie, s_pick, s_exact_eq, s_ref;
   const uint32_t o = blockIdx.x;
   const uint32_t w = o / a.n_p2p, pid = o % a.n_p2p;
   const uint64_t ch = a.n_comms + pid;
@@ -429,7 +454,7 @@ __global__ void __launch_bounds__(LK_NT) k_link_median(LKArgs a) {
     if (nu > LINK_CAP) atomicOr(&a.cnt->overflow, 8u);
   }
   if (nu == 0 || nu > LINK_CAP) return;
-  // ordered compaction of the selected samples
+  // compaction of the selected samples (order irrelevant: selection below is order-free)
   uint32_t carry = 0;
   for (uint32_t kb = 0; kb < n; kb += LK_NT) {
     const uint32_t k = kb + threadIdx.x;
@@ -440,17 +465,84 @@ __global__ void __launch_bounds__(LK_NT) k_link_median(LKArgs a) {
     const uint32_t ex = block_excl_sum<LK_NT>(sel ? 1u : 0u, tot, scan_sm);
     if (sel) {
       const uint32_t pos = carry + ex;
-      const uint4 rc = a.rec[b + k];
       sp[pos] = a.p2p_pay[sb + (uint64_t)k * 2 - a.p2p_slot0];
-      st[pos] = rc.x;
+      st[pos] = a.rec[b + k].x;
       si[pos] = (uint32_t)(b + k);
     }
     carry += tot;
   }
+  // radix select of the lower-median rank q on the 64-bit f64 key, 8 bits per pass
+  if (threadIdx.x == 0) { s_prefix = 0; s_target = (nu - 1) / 2; s_less = 0; }
   __syncthreads();
-  smem_bitonic<LK_NT>(sp, st, si, nu);
-  if (threadIdx.x == 0) {
-    const uint32_t m = (nu - 1) / 2;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (uint32_t i = threadIdx.x; i < 256; i += LK_NT) hist[i] = 0;
+    __syncthreads();
+    const unsigned long long pre = s_prefix;
+    const unsigned long long hmask = shift == 56 ? 0ull : (~0ull << (shift + 8));
+    for (uint32_t i = threadIdx.x; i < nu; i += LK_NT) {
+      const unsigned long long key = ratio_key(sp[i], st[i]);
+      if ((key & hmask) == pre) atomicAdd(&hist[(key >> shift) & 0xFFu], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t acc = 0, tg = s_target, d = 0;
+      for (; d < 256; ++d) { if (acc + hist[d] > tg) break; acc += hist[d]; }
+      s_target = tg - acc; s_less += acc; s_prefix = pre | ((unsigned long long)d << shift);
+    }
+    __syncthreads();
+  }
+  // tie group: samples whose f64 key equals the selected key; order within it is (exact p/t, id)
+  const unsigned long long K = s_prefix;
+  if (threadIdx.x == 0) { s_tie = 0; s_exact_eq = 1; s_ref = NONE32; }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < nu; i += LK_NT)
+    if (ratio_key(sp[i], st[i]) == K) { atomicAdd(&s_tie, 1u); atomicMin(&s_ref, i); }
+  __syncthreads();
+  const uint32_t ref = s_ref;
+  for (uint32_t i = threadIdx.x; i < nu; i += LK_NT)
+    if (ratio_key(sp[i], st[i]) == K && (unsigned long long)sp[i] * st[ref] != (unsigned long long)sp[ref] * st[i]) s_exact_eq = 0;
+  __syncthreads();
+  const uint32_t tg = s_target;  // rank inside the tie group
+  if (s_exact_eq) {
+    // all tied samples share one exact ratio: the tg-th smallest instance id among them
+    if (threadIdx.x == 0) s_prefix = 0;
+    __syncthreads();
+    uint32_t tgt = tg;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (uint32_t i = threadIdx.x; i < 256; i += LK_NT) hist[i] = 0;
+      __syncthreads();
+      const uint32_t pre = (uint32_t)s_prefix;
+      const uint32_t hmask = shift == 24 ? 0u : (0xFFFFFFFFu << (shift + 8));
+      for (uint32_t i = threadIdx.x; i < nu; i += LK_NT)
+        if (ratio_key(sp[i], st[i]) == K && (si[i] & hmask) == pre) atomicAdd(&hist[(si[i] >> shift) & 0xFFu], 1u);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t acc = 0, d = 0;
+        for (; d < 256; ++d) { if (acc + hist[d] > tgt) break; acc += hist[d]; }
+        s_target = tgt - acc; s_prefix = pre | (d << shift);
+      }
+      __syncthreads();
+      tgt = s_target;
+    }
+    if (threadIdx.x == 0) s_pick = NONE32;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nu; i += LK_NT)
+      if (ratio_key(sp[i], st[i]) == K && si[i] == (uint32_t)s_prefix) s_pick = i;
+  } else {
+    // distinct exact ratios behind one f64 value (rare): rank every tied sample exactly
+    if (threadIdx.x == 0) s_pick = NONE32;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nu; i += LK_NT) {
+      if (ratio_key(sp[i], st[i]) != K) continue;
+      uint32_t rk = 0;
+      for (uint32_t j2 = 0; j2 < nu; ++j2)
+        if (j2 != i && ratio_key(sp[j2], st[j2]) == K && samp_less(sp[j2], st[j2], si[j2], sp[i], st[i], si[i])) ++rk;
+      if (rk == tg) s_pick = i;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && s_pick != NONE32) {
+    const uint32_t m = s_pick;
     a.lk_medp[o] = sp[m]; a.lk_medt[o] = st[m];
     a.lk_bw[o] = (double)sp[m] / (double)st[m];
   }
