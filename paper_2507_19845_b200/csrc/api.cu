@@ -86,7 +86,7 @@ static void release_all(Ctx& c) {
                     &c.lb_label, &c.lb_rkind, &c.lb_rrank, &c.lb_rsrc, &c.lb_depth, &c.lb_twait, &c.scratch,
                     &c.st_tile0, &c.st_npos, &c.role_comm, &c.role_slot, &c.role_type, &c.ncroles, &c.ft_cols,
                     &c.ft_base, &c.ft_last, &c.st_tot, &c.sci, &c.sit, &c.dlate, &c.dinfo, &c.ft_posA, &c.ft_posB,
-                    &c.ft_posK, &c.eidx, &c.tile_stage, &c.xbase};
+                    &c.ft_posK, &c.eidx, &c.tile_stage, &c.xbase, &c.lk_scratch};
   for (DevBuf* b : bufs) b->release();
 }
 

@@ -140,6 +140,7 @@ struct Ctx {
   DevBuf eidx;                           // [W][TP+DP] edge slot of each TP-/DP-group partner
   DevBuf tile_stage;                     // [n_ftiles] stage of each fused tile (u8)
   DevBuf xbase;                          // [NCH+1] cross-stage instance index
+  DevBuf lk_scratch;                     // link-median scratch for links above the shared-memory capacity
   uint64_t n_xinst = 0;
   // optional per-kernel timing
   bool timing = false;

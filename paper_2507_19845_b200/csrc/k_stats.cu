@@ -404,6 +404,7 @@ struct LKArgs {
   uint32_t min_samples;
   uint32_t* lk_n; uint8_t* lk_used; uint32_t* lk_medp; uint32_t* lk_medt; double* lk_bw; uint8_t* lk_dir; uint8_t* lk_elig;
   Counters* cnt;
+  unsigned long long* gkey; uint32_t* gid;  // global scratch for links with more than LM_CAP samples
 };
 
 // Order key of a sample: the f64 ratio p/t (exactly rounded, monotone in the exact ratio) as
@@ -412,16 +413,34 @@ __device__ __forceinline__ unsigned long long ratio_key(uint32_t p, uint32_t t) 
   return (unsigned long long)__double_as_longlong((double)p / (double)t);  // positive: bit order = value order
 }
 
-__global__ void __launch_bounds__(LK_NT) k_link_median(LKArgs a) {
-  extern __shared__ uint32_t smem[];
-  uint32_t* sp = smem;
-  uint32_t* st = smem + LINK_CAP;
-  uint32_t* si = smem + 2 * LINK_CAP;
+constexpr int LM_NT = 256;
+constexpr uint32_t LM_CAP = 8192;  // samples per link held in shared memory (larger links use global scratch)
+
+// warp 0 finds the bin holding rank tgt in a 256-bin histogram: returns (bin, count below it)
+__device__ __forceinline__ void hist_find(const uint32_t* hist, uint32_t tgt, uint32_t& bin, uint32_t& below) {
+  const uint32_t lane = lane_id();
+  uint32_t v[8], sum = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { v[i] = hist[lane * 8 + i]; sum += v[i]; }
+  const uint32_t inc = warp_incl_scan(sum), ex = inc - sum;
+  const unsigned hit = __ballot_sync(0xFFFFFFFFu, ex <= tgt && tgt < inc);
+  const uint32_t L = __ffs(hit) - 1;
+  uint32_t acc = __shfl_sync(0xFFFFFFFFu, ex, L), b = 0;
+  if (lane == L) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { if (acc + v[i] > tgt) { b = i; break; } acc += v[i]; }
+  }
+  bin = L * 8 + __shfl_sync(0xFFFFFFFFu, b, L);
+  below = __shfl_sync(0xFFFFFFFFu, acc, L);
+}
+
+__global__ void __launch_bounds__(LM_NT) k_link_median(LKArgs a) {
+  extern __shared__ __align__(8) uint8_t lsm[];
   __shared__ uint32_t scan_sm[33];
   __shared__ uint32_t cnt_all, cnt_warm;
   __shared__ uint32_t hist[256];
   __shared__ unsigned long long s_prefix;
-  __shared__ uint32_t s_target, s_less, s_tie, s_pick, s_exact_eq, s_ref;
+  __shared__ uint32_t s_target, s_tie, s_pick, s_exact_eq, s_ref;
   const uint32_t o = blockIdx.x;
   const uint32_t w = o / a.n_p2p, pid = o % a.n_p2p;
   const uint64_t ch = a.n_comms + pid;
@@ -438,7 +457,7 @@ __global__ void __launch_bounds__(LK_NT) k_link_median(LKArgs a) {
     in = true; warm = (rc.w & SCAN_F_WARMUP) != 0;
   };
   uint32_t la = 0, lw = 0;
-  for (uint32_t k = threadIdx.x; k < n; k += LK_NT) { bool in, wm; sample(k, in, wm); la += in; lw += (in && wm); }
+  for (uint32_t k = threadIdx.x; k < n; k += LM_NT) { bool in, wm; sample(k, in, wm); la += in; lw += (in && wm); }
   la = warp_sum_u32(la); lw = warp_sum_u32(lw);
   if (lane_id() == 0) { atomicAdd(&cnt_all, la); atomicAdd(&cnt_warm, lw); }
   __syncthreads();
@@ -451,100 +470,104 @@ __global__ void __launch_bounds__(LK_NT) k_link_median(LKArgs a) {
     a.lk_n[o] = nu; a.lk_used[o] = use_warm ? 1 : 0;
     a.lk_elig[o] = nu >= a.min_samples ? 1 : 0;
     a.lk_medp[o] = 0; a.lk_medt[o] = 0; a.lk_bw[o] = 0.0;
-    if (nu > LINK_CAP) atomicOr(&a.cnt->overflow, 8u);
   }
-  if (nu == 0 || nu > LINK_CAP) return;
-  // compaction of the selected samples (order irrelevant: selection below is order-free)
+  if (nu == 0) return;
+  // selected samples as (f64 key, instance id); shared memory, or this link's global scratch slice
+  unsigned long long* sk;
+  uint32_t* si;
+  if (nu <= LM_CAP) { sk = (unsigned long long*)lsm; si = (uint32_t*)(lsm + (size_t)LM_CAP * 8); }
+  else { sk = a.gkey + (b - a.p2p_inst0); si = a.gid + (b - a.p2p_inst0); }
   uint32_t carry = 0;
-  for (uint32_t kb = 0; kb < n; kb += LK_NT) {
+  for (uint32_t kb = 0; kb < n; kb += LM_NT) {
     const uint32_t k = kb + threadIdx.x;
     bool in = false, wm = false;
     if (k < n) sample(k, in, wm);
     const bool sel = in && (!use_warm || wm);
     uint32_t tot;
-    const uint32_t ex = block_excl_sum<LK_NT>(sel ? 1u : 0u, tot, scan_sm);
+    const uint32_t ex = block_excl_sum<LM_NT>(sel ? 1u : 0u, tot, scan_sm);
     if (sel) {
       const uint32_t pos = carry + ex;
-      sp[pos] = a.p2p_pay[sb + (uint64_t)k * 2 - a.p2p_slot0];
-      st[pos] = a.rec[b + k].x;
-      si[pos] = (uint32_t)(b + k);
+      sk[pos] = ratio_key(a.p2p_pay[sb + (uint64_t)k * 2 - a.p2p_slot0], a.rec[b + k].x);
+      si[pos] = k;
     }
     carry += tot;
   }
-  // radix select of the lower-median rank q on the 64-bit f64 key, 8 bits per pass
-  if (threadIdx.x == 0) { s_prefix = 0; s_target = (nu - 1) / 2; s_less = 0; }
+  // radix select of the lower-median rank (nu-1)/2 on the key, 8 bits per pass
+  if (threadIdx.x == 0) { s_prefix = 0; s_target = (nu - 1) / 2; }
   __syncthreads();
   for (int shift = 56; shift >= 0; shift -= 8) {
-    for (uint32_t i = threadIdx.x; i < 256; i += LK_NT) hist[i] = 0;
+    hist[threadIdx.x] = 0;
     __syncthreads();
     const unsigned long long pre = s_prefix;
     const unsigned long long hmask = shift == 56 ? 0ull : (~0ull << (shift + 8));
-    for (uint32_t i = threadIdx.x; i < nu; i += LK_NT) {
-      const unsigned long long key = ratio_key(sp[i], st[i]);
+    for (uint32_t i = threadIdx.x; i < nu; i += LM_NT) {
+      const unsigned long long key = sk[i];
       if ((key & hmask) == pre) atomicAdd(&hist[(key >> shift) & 0xFFu], 1u);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t acc = 0, tg = s_target, d = 0;
-      for (; d < 256; ++d) { if (acc + hist[d] > tg) break; acc += hist[d]; }
-      s_target = tg - acc; s_less += acc; s_prefix = pre | ((unsigned long long)d << shift);
+    if (threadIdx.x < 32) {
+      uint32_t bin, below;
+      hist_find(hist, s_target, bin, below);
+      if (threadIdx.x == 0) { s_target -= below; s_prefix = pre | ((unsigned long long)bin << shift); }
     }
     __syncthreads();
   }
-  // tie group: samples whose f64 key equals the selected key; order within it is (exact p/t, id)
+  // tie group = samples with the selected key; order inside it is (exact p/t, instance id)
   const unsigned long long K = s_prefix;
-  if (threadIdx.x == 0) { s_tie = 0; s_exact_eq = 1; s_ref = NONE32; }
+  const uint32_t tg = s_target;
+  if (threadIdx.x == 0) { s_tie = 0; s_exact_eq = 1; s_ref = NONE32; s_pick = NONE32; }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < nu; i += LK_NT)
-    if (ratio_key(sp[i], st[i]) == K) { atomicAdd(&s_tie, 1u); atomicMin(&s_ref, i); }
+  for (uint32_t i = threadIdx.x; i < nu; i += LM_NT)
+    if (sk[i] == K) { atomicAdd(&s_tie, 1u); atomicMin(&s_ref, i); }
   __syncthreads();
-  const uint32_t ref = s_ref;
-  for (uint32_t i = threadIdx.x; i < nu; i += LK_NT)
-    if (ratio_key(sp[i], st[i]) == K && (unsigned long long)sp[i] * st[ref] != (unsigned long long)sp[ref] * st[i]) s_exact_eq = 0;
-  __syncthreads();
-  const uint32_t tg = s_target;  // rank inside the tie group
-  if (s_exact_eq) {
-    // all tied samples share one exact ratio: the tg-th smallest instance id among them
-    if (threadIdx.x == 0) s_prefix = 0;
-    __syncthreads();
-    uint32_t tgt = tg;
-    for (int shift = 24; shift >= 0; shift -= 8) {
-      for (uint32_t i = threadIdx.x; i < 256; i += LK_NT) hist[i] = 0;
-      __syncthreads();
-      const uint32_t pre = (uint32_t)s_prefix;
-      const uint32_t hmask = shift == 24 ? 0u : (0xFFFFFFFFu << (shift + 8));
-      for (uint32_t i = threadIdx.x; i < nu; i += LK_NT)
-        if (ratio_key(sp[i], st[i]) == K && (si[i] & hmask) == pre) atomicAdd(&hist[(si[i] >> shift) & 0xFFu], 1u);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        uint32_t acc = 0, d = 0;
-        for (; d < 256; ++d) { if (acc + hist[d] > tgt) break; acc += hist[d]; }
-        s_target = tgt - acc; s_prefix = pre | (d << shift);
-      }
-      __syncthreads();
-      tgt = s_target;
-    }
-    if (threadIdx.x == 0) s_pick = NONE32;
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < nu; i += LK_NT)
-      if (ratio_key(sp[i], st[i]) == K && si[i] == (uint32_t)s_prefix) s_pick = i;
+  auto P_ = [&](uint32_t i) { return a.p2p_pay[sb + (uint64_t)si[i] * 2 - a.p2p_slot0]; };
+  auto T_ = [&](uint32_t i) { return a.rec[b + si[i]].x; };
+  if (s_tie == 1) {
+    if (sk[threadIdx.x < nu ? threadIdx.x : 0] == K && threadIdx.x < nu) s_pick = threadIdx.x;
+    for (uint32_t i = threadIdx.x + LM_NT; i < nu; i += LM_NT) if (sk[i] == K) s_pick = i;
   } else {
-    // distinct exact ratios behind one f64 value (rare): rank every tied sample exactly
-    if (threadIdx.x == 0) s_pick = NONE32;
+    const uint32_t ref = s_ref;
+    const uint32_t pr = P_(ref), tr = T_(ref);
+    for (uint32_t i = threadIdx.x; i < nu; i += LM_NT)
+      if (sk[i] == K && (unsigned long long)P_(i) * tr != (unsigned long long)pr * T_(i)) s_exact_eq = 0;
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < nu; i += LK_NT) {
-      if (ratio_key(sp[i], st[i]) != K) continue;
-      uint32_t rk = 0;
-      for (uint32_t j2 = 0; j2 < nu; ++j2)
-        if (j2 != i && ratio_key(sp[j2], st[j2]) == K && samp_less(sp[j2], st[j2], si[j2], sp[i], st[i], si[i])) ++rk;
-      if (rk == tg) s_pick = i;
+    if (s_exact_eq) {
+      // one exact ratio: the tg-th smallest instance id of the tie group (radix select on ids)
+      uint32_t tgt = tg, pre = 0;
+      for (int shift = 24; shift >= 0; shift -= 8) {
+        hist[threadIdx.x] = 0;
+        __syncthreads();
+        const uint32_t hmask = shift == 24 ? 0u : (0xFFFFFFFFu << (shift + 8));
+        for (uint32_t i = threadIdx.x; i < nu; i += LM_NT)
+          if (sk[i] == K && (si[i] & hmask) == pre) atomicAdd(&hist[(si[i] >> shift) & 0xFFu], 1u);
+        __syncthreads();
+        if (threadIdx.x < 32) {
+          uint32_t bin, below;
+          hist_find(hist, tgt, bin, below);
+          if (threadIdx.x == 0) { s_target = tgt - below; s_prefix = pre | (bin << shift); }
+        }
+        __syncthreads();
+        tgt = s_target; pre = (uint32_t)s_prefix;
+      }
+      for (uint32_t i = threadIdx.x; i < nu; i += LM_NT)
+        if (sk[i] == K && si[i] == pre) s_pick = i;
+    } else {
+      // distinct exact ratios behind one f64 value (rare): rank the tie group exactly
+      for (uint32_t i = threadIdx.x; i < nu; i += LM_NT) {
+        if (sk[i] != K) continue;
+        const uint32_t pi = P_(i), ti = T_(i);
+        uint32_t rk = 0;
+        for (uint32_t j2 = 0; j2 < nu; ++j2)
+          if (j2 != i && sk[j2] == K && samp_less(P_(j2), T_(j2), si[j2], pi, ti, si[i])) ++rk;
+        if (rk == tg) s_pick = i;
+      }
     }
   }
   __syncthreads();
   if (threadIdx.x == 0 && s_pick != NONE32) {
-    const uint32_t m = s_pick;
-    a.lk_medp[o] = sp[m]; a.lk_medt[o] = st[m];
-    a.lk_bw[o] = (double)sp[m] / (double)st[m];
+    const uint32_t pm = P_(s_pick), tm = T_(s_pick);
+    a.lk_medp[o] = pm; a.lk_medt[o] = tm;
+    a.lk_bw[o] = (double)pm / (double)tm;
   }
 }
 
@@ -592,16 +615,20 @@ __global__ void __launch_bounds__(LK_NT) k_link_flags(uint32_t n_p2p, int W, con
 
 int launch_links(Ctx& c) {
   if (c.n_p2p == 0) return 0;
+  const uint64_t np_inst = std::max<uint64_t>(c.n_inst - c.p2p_inst0, 1);
+  if (c.lk_scratch.ensure(np_inst * 12) != cudaSuccess) return 0;
   LKArgs a{c.n_comms, (uint32_t)c.n_p2p, c.NW, c.dcfg.window_iters, c.W, c.TP, c.DP, c.ch_base.as<uint64_t>(),
            c.ch_nmax.as<uint32_t>(), c.ch_nsend.as<uint32_t>() + c.n_p2p, c.ch_nrecv.as<uint32_t>() + c.n_p2p,
            c.inst_rec.as<uint4>(), c.p2p_iter.as<uint32_t>(), c.p2p_pay.as<uint32_t>(), c.ch_slot.as<uint64_t>(),
            c.p2p_inst0, c.p2p_slot0, c.lcfg.min_samples, c.lk_n.as<uint32_t>(), c.lk_used.as<uint8_t>(),
            c.lk_medp.as<uint32_t>(), c.lk_medt.as<uint32_t>(), c.lk_bw.as<double>(), c.lk_dir.as<uint8_t>(),
-           c.lk_elig.as<uint8_t>(), c.counters.as<Counters>()};
+           c.lk_elig.as<uint8_t>(), c.counters.as<Counters>(), c.lk_scratch.as<unsigned long long>(),
+           (uint32_t*)(c.lk_scratch.as<unsigned long long>() + np_inst)};
+  const size_t smm = (size_t)LM_CAP * 12;
   const size_t sm = 3 * LINK_CAP * sizeof(uint32_t);
-  cudaFuncSetAttribute(k_link_median, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(k_link_median, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smm);
   cudaFuncSetAttribute(k_link_flags, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_link_median<<<(unsigned)(c.NW * c.n_p2p), LK_NT, sm, c.stream>>>(a);
+  k_link_median<<<(unsigned)(c.NW * c.n_p2p), LM_NT, smm, c.stream>>>(a);
   k_link_flags<<<c.NW, LK_NT, sm, c.stream>>>((uint32_t)c.n_p2p, c.W, c.ch_nsend.as<uint32_t>() + c.n_p2p,
                                                c.lk_medp.as<uint32_t>(), c.lk_medt.as<uint32_t>(), c.lk_dir.as<uint8_t>(),
                                                c.lk_elig.as<uint8_t>(), c.lk_slow.as<uint8_t>(), c.wl_link_slow.as<uint8_t>(),

@@ -209,3 +209,20 @@ def test_fused_odd_dp(dp):
     tr = tg.generate(tg.GenConfig(2, 2, dp, 2, 4, 3, seed=dp, faults=[tg.Fault(tg.THROTTLE, 3, factor=2.0)]))
     o, g = _run_both(tr)
     compare(o, g)
+
+
+def test_link_median_global_scratch():
+    """More samples on a link than the shared-memory capacity of the median kernel (8192)."""
+    tr = tg.generate(tg.GenConfig(1, 2, 1, 1, 64, 140, seed=9, faults=[tg.Fault(tg.LINK_JITTER, 0, 1)]))
+    o, g = _run_both(tr)
+    assert o["lk_n"].max() > 8192
+    compare(o, g)
+
+
+def test_link_median_exact_ties():
+    """Zero jitter: every transfer on a link has the same payload and duration, so the median is
+    decided by the instance-id tie-break alone."""
+    tr = tg.generate(tg.GenConfig(2, 4, 2, 1, 12, 3, seed=2, jitter=0.0, clock_skew=False,
+                                  faults=[tg.Fault(tg.LINK_DEGRADE, 2, 6, factor=0.5)]))
+    o, g = _run_both(tr)
+    compare(o, g)
