@@ -232,8 +232,8 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
     std::vector<uint32_t> rcmm((size_t)W * CROLES, NONE32), rslt((size_t)W * CROLES, NONE32), ncr(topo->pp, 0);
     std::vector<uint8_t> rty((size_t)topo->pp * ROLES, 0);
     std::vector<uint32_t> stt0(topo->pp + 1, 0), stnp(topo->pp, 0);
-    bool aligned = true;
-    for (int r = 0; r < W; ++r) aligned &= (ro[r] % 4) == 0;
+    bool aligned = true, aligned8 = true;
+    for (int r = 0; r < W; ++r) { aligned &= (ro[r] % 4) == 0; aligned8 &= (ro[r] % 8) == 0; }
     for (int s = 0; ok && s < topo->pp; ++s) {
       const uint32_t r0 = s * R;
       const uint64_t ns = ro[r0 + 1] - ro[r0];
@@ -283,7 +283,7 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
       uint32_t nt = 0;
       for (int s = 0; s < topo->pp; ++s) { stt0[s] = nt; nt += (stnp[s] + T - 1) / T; }
       stt0[topo->pp] = nt;
-      c.FT = T; c.FR = R; c.n_ftiles = nt; c.h_st_tile0 = stt0; c.h_st_npos = stnp; c.rows_aligned = aligned;
+      c.FT = T; c.FR = R; c.n_ftiles = nt; c.h_st_tile0 = stt0; c.h_st_npos = stnp; c.rows_aligned = aligned; c.rows_aligned8 = aligned8;
       std::vector<uint8_t> tstage(nt);
       for (int s = 0; s < topo->pp; ++s) for (uint32_t t = stt0[s]; t < stt0[s + 1]; ++t) tstage[t] = (uint8_t)s;
       if (topo->pp > 255) ok = false;

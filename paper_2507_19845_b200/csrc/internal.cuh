@@ -134,7 +134,7 @@ struct Ctx {
   DevBuf ft_posA, ft_posB, ft_posK;           // per template position packed info + template kind_op
   DevBuf sci, sit;                       // per slot: comm index, iteration of the member event (cross instances)
   DevBuf dlate, dinfo;                   // deferred stage-2 positions (first comm position of a tile)
-  bool rows_aligned = false;
+  bool rows_aligned = false, rows_aligned8 = false;
   bool force_general = false;
   uint32_t NCRM = 1;                     // max collective roles of a rank over the stages
   DevBuf eidx;                           // [W][TP+DP] edge slot of each TP-/DP-group partner

@@ -261,7 +261,7 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t x, FDiv f) { return f.d <= 1 ?
 
 struct FusedArgs {
   const uint32_t* dur; const uint16_t* kind; const uint16_t* meta; const uint32_t* comm; const uint32_t* pay;
-  const uint64_t* rank_off; int TP, DP, PP, W; uint32_t n_comms; uint32_t T, R, n_ftiles, G; bool aligned;
+  const uint64_t* rank_off; int TP, DP, PP, W; uint32_t n_comms; uint32_t T, R, n_ftiles, G; bool aligned, aligned8;
   const uint32_t* st_tile0; const uint32_t* st_npos; const uint32_t* ft_base; const uint8_t* tile_stage;
   FDiv fTP, fDP, fR, fG, fCH;
   const uint32_t* posA; const uint32_t* posB; const uint16_t* posK;
@@ -319,6 +319,15 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
+// exact 64-bit accumulation in shared memory with native 32-bit atomics (a 64-bit shared atomicAdd
+// compiles to a CAS loop on sm_100a): add to the low word, carry into the high word on wrap-around
+__device__ __forceinline__ void add64_lohi(uint32_t* lo, uint32_t* hi, unsigned long long v) {
+  const uint32_t vl = (uint32_t)v, vh = (uint32_t)(v >> 32);
+  const uint32_t old = atomicAdd(lo, vl);
+  const uint32_t carry = (old + vl < old) ? 1u : 0u;
+  if (vh + carry) atomicAdd(hi, vh + carry);
+}
+
 template <int P>
 __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -328,12 +337,13 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   const uint32_t E = TP + DP, NCRM = a.NCRM;
   uint32_t* sd = (uint32_t*)smem_raw;                                   // R x T (swizzled)
   uint32_t* vd = sd + (uint64_t)R * T;                                  // T verification descriptor (16 B aligned)
-  unsigned long long* gsum = (unsigned long long*)(vd + T);             // DP + TP
-  unsigned long long* coffr = gsum + DP + TP;                           // R comm offsets
-  unsigned long long* sedge = coffr + R;                                // R x (TP+DP) wait-for weights
-  unsigned long long* rcb = sedge + (uint64_t)R * E;                    // R x NCRM channel bases
-  unsigned long long* rsum = rcb + (uint64_t)R * NCRM;                  // R x 2: compute, in-block comm durations
-  uint32_t* sinst = (uint32_t*)(rsum + 2 * (uint64_t)R);                // T x G
+  unsigned long long* coffr = (unsigned long long*)(vd + T);            // R comm offsets
+  unsigned long long* rcb = coffr + R;                                  // R x NCRM channel bases
+  unsigned long long* rsum = rcb + (uint64_t)R * NCRM;                  // R x 2: compute durations, waits
+  uint32_t* gsum = (uint32_t*)(rsum + 2 * (uint64_t)R);                 // 2 x (DP + TP): lo / hi words
+  uint32_t* sedge = gsum + 2 * (DP + TP);                               // 2 x R x (TP+DP): lo / hi words
+  uint32_t* rowg = sedge + 2 * (uint64_t)R * E;                         // R: tp-group | dp-group << 16
+  uint32_t* sinst = rowg + R;                                           // T x G
   uint32_t* sbits = sinst + (uint64_t)T * G;                            // R x SW
   uint32_t* rcs = sbits + (uint64_t)R * SW;                             // R x NCRM
   uint32_t* pa = rcs + (uint64_t)R * NCRM;                              // T
@@ -345,7 +355,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   uint32_t* slate = sjoin + R;                                          // R
   uint32_t* rslow = slate + R;                                          // R: row has a slow bit in this tile
   uint8_t* gmask = (uint8_t*)(rslow + R);                               // T/4 granule masks: compute | in-block << 4
-  uint16_t* pk = (uint16_t*)(((uintptr_t)(gmask + T / 4) + 7) & ~(uintptr_t)7);  // T template kind_op, 8 B aligned
+  uint16_t* pk = (uint16_t*)(((uintptr_t)(gmask + T / 4) + 15) & ~(uintptr_t)15);  // T template kind_op, 16 B aligned
   uint16_t* lst = pk + T;                                               // 4 x T
   uint16_t* cl = lst + 4 * T;                                           // T: comm positions by m, | class << 14
   __shared__ uint32_t kbase[ROLES];
@@ -392,9 +402,13 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   if (tid < 4) nlist[tid] = 0;
   if (tid == 0) { dpos = -1; bad = 0; anyslow = 0; }
   for (uint32_t i = tid; i < R * SW; i += F_NT) sbits[i] = 0;
-  for (uint32_t i = tid; i < R; i += F_NT) { sjoin[i] = 0; slate[i] = 0; coffr[i] = a.comm_off[sbase + i]; }
-  for (uint32_t i = tid; i < DP + TP; i += F_NT) gsum[i] = 0;
-  for (uint32_t i = tid; i < R * E; i += F_NT) sedge[i] = 0;
+  for (uint32_t i = tid; i < R; i += F_NT) {
+    sjoin[i] = 0; slate[i] = 0; coffr[i] = a.comm_off[sbase + i];
+    const uint32_t gt = fdiv(i, fTP);
+    rowg[i] = gt | ((i - gt * TP) << 16);
+  }
+  for (uint32_t i = tid; i < 2 * (DP + TP); i += F_NT) gsum[i] = 0;
+  for (uint32_t i = tid; i < 2 * R * E; i += F_NT) sedge[i] = 0;
   for (uint32_t i = tid; i < T / 4; i += F_NT) gmask[i] = 0;
   for (uint32_t i = tid; i < R * ncr; i += F_NT) {
     const uint32_t row = i / ncr, ro = i - row * ncr;
@@ -439,54 +453,22 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
     }
   }
   __syncthreads();
-  // ---- (3) verify every rank row against the template: kind_op equal, and the comm field equal to
-  // the communicator of the role (collectives) / the peer of the role (P2P).
+  // ---- (3) verify every rank row's kind_op column against the template, 8 positions per 16-byte
+  // load (the comm field is verified in the flush, which visits every comm event anyway)
   {
-    constexpr int VU = 4;
-    const uint32_t units = R * nch;
+    const uint32_t n8 = (np + 7) / 8;
+    const FDiv f8 = fdiv_make(n8);
     bool mis = false;
-    for (uint32_t ub = wid; ub < units; ub += VU * (F_NT / 32)) {
-      uint2 kv[VU]; uint4 cv[VU];
-#pragma unroll
-      for (int u = 0; u < VU; ++u) {
-        const uint32_t wq = ub + u * (F_NT / 32);
-        kv[u] = make_uint2(0, 0); cv[u] = make_uint4(0, 0, 0, 0);
-        if (wq < units) {
-          const uint32_t row = fdiv(wq, fch), ch = wq - row * nch;
-          const uint32_t pbase = ch * 128 + lane * 4;
-          const uint64_t g = rbase + (uint64_t)row * npos + p0 + pbase;
-          if (a.aligned && pbase + 4 <= np) {
-            kv[u] = __ldg(reinterpret_cast<const uint2*>(a.kind + g));
-            cv[u] = __ldg(reinterpret_cast<const uint4*>(a.comm + g));
-          } else if (pbase < np) {
-            uint16_t k4[4] = {0, 0, 0, 0}; uint32_t c4[4] = {0, 0, 0, 0};
-            for (uint32_t i = 0; i < 4 && pbase + i < np; ++i) { k4[i] = a.kind[g + i]; c4[i] = a.comm[g + i]; }
-            kv[u] = make_uint2(k4[0] | ((uint32_t)k4[1] << 16), k4[2] | ((uint32_t)k4[3] << 16));
-            cv[u] = make_uint4(c4[0], c4[1], c4[2], c4[3]);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < VU; ++u) {
-        const uint32_t wq = ub + u * (F_NT / 32);
-        if (wq >= units) continue;
-        const uint32_t row = fdiv(wq, fch), ch = wq - row * nch;
-        const uint32_t pbase = ch * 128 + lane * 4;
-        if (pbase >= np) continue;
-        const uint2 tk2 = *reinterpret_cast<const uint2*>(pk + pbase);
-        mis |= (kv[u].x != tk2.x) | (kv[u].y != tk2.y);
-        const uint4 d4 = *reinterpret_cast<const uint4*>(vd + pbase);
-        const uint32_t dv[4] = {d4.x, d4.y, d4.z, d4.w};
-        const uint32_t cm[4] = {cv[u].x, cv[u].y, cv[u].z, cv[u].w};
-        const uint32_t r = sbase + row;
-        const uint32_t* rc = rcs + row * NCRM;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {  // branch-free: both expectations, select by descriptor type
-          const uint32_t t = dv[i] & 3u, x = dv[i] >> 2;
-          const uint32_t e1 = rc[t == 1 ? x : 0u];
-          const uint32_t e2 = r + x - 0x100000u;
-          mis |= (t != 0) & (cm[i] != (t == 1 ? e1 : e2));
-        }
+    for (uint32_t i = tid; i < R * n8; i += F_NT) {
+      const uint32_t row = fdiv(i, f8), g8 = i - row * n8;
+      const uint32_t pbase = g8 * 8;
+      const uint64_t g = rbase + (uint64_t)row * npos + p0 + pbase;
+      const uint4 tv = *reinterpret_cast<const uint4*>(pk + pbase);
+      if (a.aligned8 && pbase + 8 <= np) {
+        const uint4 kv = __ldg(reinterpret_cast<const uint4*>(a.kind + g));
+        mis |= (kv.x != tv.x) | (kv.y != tv.y) | (kv.z != tv.z) | (kv.w != tv.w);
+      } else {
+        for (uint32_t q = 0; q < 8 && pbase + q < np; ++q) mis |= a.kind[g + q] != pk[pbase + q];
       }
     }
     if (__any_sync(0xFFFFFFFFu, mis) && lane == 0) bad = 1;
@@ -494,24 +476,6 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   cp_async_wait_all();
   __syncthreads();
   if (bad) { if (tid == 0) atomicOr(&a.cnt->overflow, NOT_SPMD); return; }
-  // per-rank sums of compute durations and in-block comm durations: one thread per row walks its
-  // row by 16-byte granules (granule masks from the template) — no cross-lane reductions
-  for (uint32_t row = tid; row < R; row += F_NT) {
-    const uint32_t rT = row * T, sw4 = ((row ^ (row >> 3)) & 7u) << 2;
-    unsigned long long sc = 0, si = 0;
-    for (uint32_t gi = 0; gi < ngr; ++gi) {
-      const uint32_t gm = gmask[gi];
-      if (!gm) continue;
-      const uint4 v = *reinterpret_cast<const uint4*>(sd + rT + ((4 * gi) ^ sw4));
-      const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if ((gm >> q) & 1u) sc += vv[q];
-        if ((gm >> (4 + q)) & 1u) si += vv[q];
-      }
-    }
-    rsum[2 * row] = sc; rsum[2 * row + 1] = si;
-  }
   // ---- (4) phase A: stage 1 on every compute position (LOO lower median over the DP peers).
   // Exact quick reject: if den*max <= num*min over the group, no member can be slow (ref >= min).
   const uint32_t nc = nlist[0];
@@ -608,7 +572,10 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
       a.rec[inst] = make_uint4(dmin, dmax, last, (SCAN_F_COMPLETE | SCAN_F_KIND_OK | SCAN_F_PAYLOAD_OK | SCAN_F_VALID |
                                                   (nat == 1 ? SCAN_F_UNIQUE_LAST : 0u)) | (cls << 8));
       sinst[p * G + g] = (uint32_t)inst;
-      atomicAdd(&gsum[istp ? g : DP + g], (unsigned long long)dmin);
+      {
+        const uint32_t gi = istp ? g : DP + g;
+        add64_lohi(&gsum[gi], &gsum[DP + TP + gi], dmin);
+      }
       const uint32_t win = a.wi ? (it0 + (B & 1023u)) / a.wi : 0;
       const bool elig = (a.classes >> (cls - 1)) & 1u;
       const bool late_ok = nat == 1 && (unsigned long long)(dmax - dmin) > a.late_margin;
@@ -622,7 +589,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
         const uint32_t wait = sd[idx] - dmin;
         sd[idx] = wait;  // the duration tile now holds the wait at in-block comm positions
         if (q != ls && (unsigned long long)wait > a.wait_margin) {
-          if (win == w_tile) atomicAdd(&sedge[row * E + eslot], (unsigned long long)wait);
+          if (win == w_tile) add64_lohi(&sedge[row * E + eslot], &sedge[R * E + row * E + eslot], wait);
           else atomicAdd(&a.ew[(uint64_t)win * a.nnz_tot + a.eidx[(uint64_t)(sbase + row) * E + eslot]], (unsigned long long)wait);
         }
         if (!chk) continue;
@@ -694,17 +661,42 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   const uint32_t ncm = nlist[1] + nlist[2] + nlist[3];
   {
     const FDiv fm = fdiv_make(ncm > 0 ? ncm : 1u);
+    bool mis = false;
     for (uint32_t i = tid; i < R * ncm; i += F_NT) {  // consecutive threads: consecutive comm events of a rank
       const uint32_t row = fdiv(i, fm), j = i - row * ncm;
-      const uint32_t gt = fdiv(row, fTP), gd = row - gt * TP;
+      const uint32_t rg = rowg[row];
       const uint32_t cv = cl[j];
       const uint32_t p = cv & 0x3FFFu, cls = cv >> 14;  // 0 TP, 1 DP, 2 cross
+      const uint32_t cm = __ldg(a.comm + rbase + (uint64_t)row * npos + p0 + p);
+      // verify the comm field: communicator of the role (collective) or peer of the role (P2P)
+      const uint32_t dv = vd[p], t = dv & 3u, x = dv >> 2;
+      const uint32_t e1 = rcs[row * NCRM + (t == 1 ? x : 0u)];
+      mis |= cm != (t == 1 ? e1 : sbase + row + x - 0x100000u);
       const uint32_t v = sd[row * T + ((p & ~3u) ^ (((row ^ (row >> 3)) & 7u) << 2)) + (p & 3u)];
-      const uint32_t si = sinst[cls < 2 ? p * G + (cls == 0 ? gt : gd) : 0u];
+      const uint32_t si = sinst[cls < 2 ? p * G + (cls == 0 ? (rg & 0xFFFFu) : (rg >> 16)) : 0u];
       uint32_t* dst = a.inst_c + coffr[row] + m0 + j;
       *dst = cls < 2 ? si : v;
       if (cls < 2) a.wait_c[dst - a.inst_c] = v;
     }
+    if (__any_sync(0xFFFFFFFFu, mis) && lane == 0) atomicOr(&a.cnt->overflow, NOT_SPMD);
+  }
+  // per-rank sums: compute durations and waits (the tile now holds waits at in-block comm positions);
+  // one thread per row walks its row by 16-byte granules -> no cross-lane reductions
+  for (uint32_t row = tid; row < R; row += F_NT) {
+    const uint32_t rT = row * T, sw4 = ((row ^ (row >> 3)) & 7u) << 2;
+    unsigned long long sc = 0, sw = 0;
+    for (uint32_t gi = 0; gi < ngr; ++gi) {
+      const uint32_t gm = gmask[gi];
+      if (!gm) continue;
+      const uint4 v = *reinterpret_cast<const uint4*>(sd + rT + ((4 * gi) ^ sw4));
+      const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if ((gm >> q) & 1u) sc += vv[q];
+        if ((gm >> (4 + q)) & 1u) sw += vv[q];
+      }
+    }
+    rsum[2 * row] = sc; rsum[2 * row + 1] = sw;
   }
   // stage-1 counters per (window, rank): total = compute positions of the tile, slow = its slow bits
   const uint32_t it_last = it0 + (np ? (pb[np - 1] & 1023u) : 0u);
@@ -730,16 +722,18 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   }
   for (uint32_t row = tid; row < R; row += F_NT) {
     const uint32_t r = sbase + row;
-    const uint32_t gt = fdiv(row, fTP), gd = row - gt * TP;
-    const unsigned long long tr = gsum[gt] + gsum[DP + gd];
+    const uint32_t gt = rowg[row] & 0xFFFFu, gd = rowg[row] >> 16;
+    const uint32_t GO = DP + TP;
+    const unsigned long long tr = ((unsigned long long)gsum[GO + gt] << 32 | gsum[gt]) +
+                                  ((unsigned long long)gsum[GO + DP + gd] << 32 | gsum[DP + gd]);
     if (rsum[2 * row]) atomicAdd(&a.rk_sum[r], rsum[2 * row]);
-    if (rsum[2 * row + 1] - tr) atomicAdd(&a.rk_sum[a.W + r], rsum[2 * row + 1] - tr);
+    if (rsum[2 * row + 1]) atomicAdd(&a.rk_sum[a.W + r], rsum[2 * row + 1]);
     if (tr) atomicAdd(&a.rk_sum[2 * a.W + r], tr);
     if (sjoin[row]) atomicAdd(&a.wl_joined[(uint64_t)w_tile * a.W + r], sjoin[row]);
     if (slate[row]) atomicAdd(&a.wl_late[(uint64_t)w_tile * a.W + r], slate[row]);
   }
   for (uint32_t i = tid; i < R * E; i += F_NT) {
-    const unsigned long long v = sedge[i];
+    const unsigned long long v = (unsigned long long)sedge[R * E + i] << 32 | sedge[i];
     if (v) atomicAdd(&a.ew[(uint64_t)w_tile * a.nnz_tot + a.eidx[(uint64_t)sbase * E + i]], v);
   }
   if (nc && tslow) {
@@ -765,9 +759,10 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
 
 size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM) {
   const uint32_t SW = T / 32 + 2, G = TP > DP ? TP : DP;
-  size_t b = (size_t)R * T * 4 + (size_t)(DP + TP) * 8 + (size_t)R * 8 + (size_t)R * (TP + DP) * 8 +
-             (size_t)R * NCRM * 8 + (size_t)R * 16 + (size_t)T * G * 4 + (size_t)R * SW * 4 + (size_t)R * NCRM * 4 +
-             (size_t)T * 4 * 6 + (size_t)R * 12 + (size_t)T / 4 + 8 + (size_t)T * 2 + (size_t)T * 8 + (size_t)T * 2;
+  size_t b = (size_t)R * T * 4 + (size_t)T * 4 + (size_t)R * 8 + (size_t)R * NCRM * 8 + (size_t)R * 16 +
+             (size_t)(DP + TP) * 8 + (size_t)R * (TP + DP) * 8 + (size_t)R * 4 + (size_t)T * G * 4 +
+             (size_t)R * SW * 4 + (size_t)R * NCRM * 4 + (size_t)T * 4 * 5 + (size_t)R * 12 + (size_t)T / 4 + 8 +
+             (size_t)T * 2 + (size_t)T * 8 + (size_t)T * 2 + 16;
   return (b + 15) & ~size_t(15);
 }
 
@@ -776,6 +771,7 @@ int launch_fused(Ctx& c) {
   a.dur = c.d_dur; a.kind = c.d_kind; a.meta = c.d_meta; a.comm = c.d_comm; a.pay = c.d_pay;
   a.rank_off = c.rank_off.as<uint64_t>(); a.TP = c.TP; a.DP = c.DP; a.PP = c.PP; a.W = c.W; a.n_comms = c.n_comms;
   a.T = c.FT; a.R = c.FR; a.n_ftiles = c.n_ftiles; a.G = (uint32_t)std::max(c.TP, c.DP); a.aligned = c.rows_aligned;
+  a.aligned8 = c.rows_aligned8;
   a.st_tile0 = c.st_tile0.as<uint32_t>(); a.st_npos = c.st_npos.as<uint32_t>(); a.ft_base = c.ft_base.as<uint32_t>();
   a.tile_stage = c.tile_stage.as<uint8_t>();
   a.fTP = fdiv_make(c.TP); a.fDP = fdiv_make(c.DP); a.fR = fdiv_make(c.FR); a.fG = fdiv_make(c.FT / 4);

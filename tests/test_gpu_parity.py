@@ -226,3 +226,21 @@ def test_link_median_exact_ties():
                                   faults=[tg.Fault(tg.LINK_DEGRADE, 2, 6, factor=0.5)]))
     o, g = _run_both(tr)
     compare(o, g)
+
+
+def test_spmd_comm_violation_falls_back():
+    """A collective whose communicator differs from the stage template's role (still a communicator the
+    rank belongs to, so the trace stays schema-valid) must be caught by the fused path's comm check."""
+    tr = tg.generate(configs.c1(seed=5, iterations=3))
+    r = 6
+    lo, hi = int(tr.rank_offsets[r]), int(tr.rank_offsets[r + 1])
+    kinds = tr.kind_op[lo:hi] & 7
+    comms = tr.comm[lo:hi]
+    # first TP all-reduce of rank 6 -> its DP communicator (both contain rank 6)
+    tp_comm = int(comms[np.nonzero(kinds == 1)[0][0]])
+    others = sorted(set(int(c) for c in comms[kinds == 1]) - {tp_comm})
+    e = lo + int(np.nonzero((kinds == 1) & (comms == tp_comm))[0][0])
+    tr.comm[e] = others[0]
+    o, g = _run_both(tr)
+    compare(o, g)
+    assert not g["_res"]["fused"]
