@@ -137,8 +137,9 @@ def _load_lib():
     lib.scan_used_fused.argtypes = [P]
     lib.scan_used_fused.restype = ctypes.c_int
     lib.scan_force_general.argtypes = [P, ctypes.c_int]
+    lib.scan_fused_variant.argtypes = [P, ctypes.c_int]
     for f in ("scan_create", "scan_load_events", "scan_match_collectives", "scan_detect", "scan_localize",
-              "scan_output_size", "scan_export", "scan_analyze", "scan_force_general"):
+              "scan_output_size", "scan_export", "scan_analyze", "scan_force_general", "scan_fused_variant"):
         getattr(lib, f).restype = ctypes.c_int32
     _lib = lib
     return lib
@@ -147,7 +148,7 @@ def _load_lib():
 EXPORTED_SYMBOLS = ["scan_create", "scan_destroy", "scan_last_error", "scan_load_events", "scan_match_collectives",
                     "scan_detect", "scan_localize", "scan_output_size", "scan_export", "scan_output_device_ptr",
                     "scan_kernel_launches", "scan_set_timing", "scan_timing_reset", "scan_kernel_timing",
-                    "scan_analyze", "scan_used_fused", "scan_force_general"]
+                    "scan_analyze", "scan_used_fused", "scan_force_general", "scan_fused_variant"]
 
 
 @dataclass
@@ -334,6 +335,10 @@ class Scan:
 
     def analyze(self, dcfg: DetectConfig | None = None, lcfg: LocalizeConfig | None = None) -> dict:
         return scan_analyze(self.ctx, dcfg, lcfg)
+
+    def fused_variant(self, variant: int):
+        """-1 automatic, 0 generic tile kernel, 1 transposed warp-per-position kernel (next load)."""
+        _check(self.ctx, _load_lib().scan_fused_variant(self.ctx, variant))
 
     def force_general(self, on: bool = True):
         _check(self.ctx, _load_lib().scan_force_general(self.ctx, 1 if on else 0))

@@ -274,10 +274,15 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
       }
     }
     if (ok) {
+      const bool tp_pow2 = topo->tp <= 32 && (32 % topo->tp) == 0;
+      c.fused_t = tp_pow2 && R <= 256 && c.fused_variant != 0;
       uint32_t T = (16384u / R) / 32u * 32u;
       T = std::max(64u, std::min(1024u, T));
       // two CTAs per SM: keep the fused kernel's shared memory under ~110 KB
-      while (T > 64 && fused_smem_bytes(T, R, topo->tp, topo->dp, ncrm) > 110u * 1024u) T -= 32;
+      auto smem = [&](uint32_t t) {
+        return c.fused_t ? fused_t_smem_bytes(t, R, topo->tp, topo->dp, ncrm) : fused_smem_bytes(t, R, topo->tp, topo->dp, ncrm);
+      };
+      while (T > 64 && smem(T) > 110u * 1024u) T -= 32;
       c.NCRM = ncrm;
       if ((st = upload(c, c.eidx, eidx))) return st;
       uint32_t nt = 0;
@@ -647,6 +652,12 @@ scan_status scan_analyze(scan_ctx* ctx, const scan_detect_config* dcfg, const sc
 }
 
 int scan_used_fused(const scan_ctx* ctx) { return ctx && ctx->c.fused_used ? 1 : 0; }
+
+scan_status scan_fused_variant(scan_ctx* ctx, int variant) {
+  if (!ctx || variant < -1 || variant > 1) return SCAN_E_INVALID_ARG;
+  ctx->c.fused_variant = variant;
+  return SCAN_OK;
+}
 
 scan_status scan_force_general(scan_ctx* ctx, int force) {
   if (!ctx) return SCAN_E_INVALID_ARG;

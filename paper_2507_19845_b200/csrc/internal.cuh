@@ -136,6 +136,8 @@ struct Ctx {
   DevBuf dlate, dinfo;                   // deferred stage-2 positions (first comm position of a tile)
   bool rows_aligned = false, rows_aligned8 = false;
   bool force_general = false;
+  bool fused_t = false;                  // transposed fused kernel (TP divides 32, R <= 256)
+  int fused_variant = -1;                // testing: -1 auto, 0 generic fused, 1 transposed
   uint32_t NCRM = 1;                     // max collective roles of a rank over the stages
   DevBuf eidx;                           // [W][TP+DP] edge slot of each TP-/DP-group partner
   DevBuf tile_stage;                     // [n_ftiles] stage of each fused tile (u8)
@@ -309,6 +311,7 @@ int launch_fused_prepass(Ctx& c);
 int launch_fused_census(Ctx& c);
 int launch_fused(Ctx& c);
 size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM);
+size_t fused_t_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM);
 int launch_cross_reduce(Ctx& c);
 int launch_deferred(Ctx& c);
 int launch_wd_finish(Ctx& c);

@@ -757,6 +757,462 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   }
 }
 
+// =============================================================================================
+// k_fused_t — transposed variant (TP divides 32, R = TP*DP <= 256): the tile is stored position-
+// major, sd[p][row] with a padded row of R+1 words, and one warp processes one position at a time:
+// lane l owns rows l + 32k. A TP group (TP consecutive rows) sits in TP consecutive lanes of one
+// register; a DP group (rows with equal row mod TP) is every lane with equal l mod TP, so both
+// reductions are butterflies of shuffles. The load pass transposes in registers and verifies the
+// kind_op and comm columns while the data is in registers.
+constexpr int FT_NT = 512, FT_NW = FT_NT / 32, NRLM = 8;
+
+template <int P>
+__device__ void loo_group(const FusedArgs& a, const uint32_t* col, uint32_t tp, uint32_t TP, uint32_t DP, uint32_t j,
+                          uint32_t* sbits, uint32_t SW, uint32_t wb, uint32_t sbase, bool& slow_any) {
+  const int q = ((int)DP - 2) / 2;
+  const int L = P / 2 - 1 - q;
+  uint32_t x[P], v[P];
+#pragma unroll
+  for (int d = 0; d < P; ++d) {
+    x[d] = d < (int)DP ? col[tp + TP * d] : 0u;
+    v[d] = d < (int)DP ? x[d] : (d < (int)DP + L ? 0u : 0xFFFFFFFFu);
+  }
+#pragma unroll
+  for (int k = 2; k <= P; k <<= 1)
+#pragma unroll
+    for (int jj = k >> 1; jj > 0; jj >>= 1)
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const int ixj = i ^ jj;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          const uint32_t lo = min(v[i], v[ixj]), hi = max(v[i], v[ixj]);
+          v[i] = up ? lo : hi; v[ixj] = up ? hi : lo;
+        }
+      }
+  const uint32_t va = v[P / 2 - 1], vb = v[P / 2];
+  const uint32_t jw = (j >> 5) - wb, jb = 1u << (j & 31);
+#pragma unroll
+  for (int d = 0; d < P; ++d) {
+    if (d < (int)DP) {
+      const uint32_t ref = x[d] > va ? va : vb;
+      const unsigned long long du = x[d];
+      const bool slow = (unsigned long long)a.slow_den * du > (unsigned long long)a.slow_num * ref &&
+                        du > (unsigned long long)ref + a.slow_margin;
+      const uint32_t row = tp + TP * d;
+      if (slow) { atomicOr(&sbits[row * SW + jw], jb); slow_any = true; }
+      if (a.want_ref) a.cref[a.comp_off[sbase + row] + j] = ref;
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t* al16(void* p) { return (uint32_t*)(((uintptr_t)p + 15) & ~(uintptr_t)15); }
+
+template <int P>
+__global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const uint32_t T = a.T, R = a.R, TP = (uint32_t)a.TP, DP = (uint32_t)a.DP, G = a.G;
+  const uint32_t SW = T / 32 + 2, E = TP + DP, NCRM = a.NCRM, RP = R + 1;
+  const uint32_t nrb = (R + 31) / 32;  // row blocks (lane l owns rows l + 32k, k < nrb)
+  // ---- shared memory carve-up (see fused_t_smem_bytes)
+  uint32_t* sd = (uint32_t*)smem_raw;                                  // T x (R+1), position-major
+  unsigned long long* rcb = (unsigned long long*)al16(sd + (uint64_t)T * RP);  // R x NCRM channel bases
+  unsigned long long* coffr = rcb + (uint64_t)R * NCRM;                // R comm offsets
+  uint32_t* sinst = (uint32_t*)(coffr + R);                            // T x G instance ids of in-block groups
+  uint32_t* sbits = sinst + (uint64_t)T * G;                           // R x SW slow bits
+  uint32_t* sedge = sbits + (uint64_t)R * SW;                          // R x E wait-for weights (low word)
+  uint32_t* rcs = sedge + (uint64_t)R * E;                             // R x NCRM communicator of each role
+  uint32_t* rsum = rcs + (uint64_t)R * NCRM;                           // R x 4: compute lo/hi, in-block lo/hi
+  uint32_t* gsum = rsum + 4 * (uint64_t)R;                             // 2 x (DP+TP): lo / hi
+  uint32_t* sjoin = gsum + 2 * (DP + TP);                              // R
+  uint32_t* slate = sjoin + R;                                         // R
+  uint32_t* rslow = slate + R;                                         // R
+  uint32_t* pa = al16(rslow + R);                                      // T
+  uint32_t* pb = pa + T;                                               // T
+  uint32_t* vd = pb + T;                                               // T verification descriptors (16 B aligned)
+  uint16_t* pk = (uint16_t*)(vd + T);                                  // T template kind_op (16 B aligned)
+  uint16_t* lst = pk + T;                                              // 4 x T position lists
+  uint16_t* cl = lst + 4 * T;                                          // T comm positions by m | class << 14
+  uint8_t* pcode = (uint8_t*)(cl + T);                                 // T: 0 compute 1 TP 2 DP 3 cross
+  __shared__ uint32_t kbase[ROLES];
+  __shared__ uint32_t nlist[4];
+  __shared__ int32_t dpos;
+  __shared__ uint32_t bad, anyslow;
+
+  const uint32_t tile = blockIdx.x;
+  const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
+  const uint32_t s = a.tile_stage[tile];
+  const uint32_t p0 = (tile - a.st_tile0[s]) * T;
+  const uint32_t npos = a.st_npos[s];
+  const uint32_t np = min(T, npos - p0);
+  const uint32_t sbase = s * R;
+  const uint64_t n = a.n_ftiles;
+  const uint64_t rbase = a.rank_off[sbase];
+  const uint32_t j0 = a.ft_base[(uint64_t)ROLES * n + tile];
+  const uint32_t m0 = a.ft_base[(uint64_t)(ROLES + 1) * n + tile];
+  const uint32_t it0 = a.ft_base[(uint64_t)(ROLES + 2) * n + tile];
+  const uint32_t jp0 = a.ft_base[(uint64_t)(ROLES + 3) * n + tile];
+  const uint32_t wb = j0 >> 5;
+  const uint32_t w_tile = a.wi ? it0 / a.wi : 0;
+  const uint32_t ncr = a.ncroles[s];
+
+  // ---- (0) tables and template info
+  if (tid < ROLES) kbase[tid] = a.ft_base[(uint64_t)tid * n + tile];
+  if (tid < 4) nlist[tid] = 0;
+  if (tid == 0) { dpos = -1; bad = 0; anyslow = 0; }
+  for (uint32_t i = tid; i < R * SW; i += FT_NT) sbits[i] = 0;
+  for (uint32_t i = tid; i < R * E; i += FT_NT) sedge[i] = 0;
+  for (uint32_t i = tid; i < 4 * R; i += FT_NT) rsum[i] = 0;
+  for (uint32_t i = tid; i < 2 * (DP + TP); i += FT_NT) gsum[i] = 0;
+  for (uint32_t i = tid; i < R; i += FT_NT) { sjoin[i] = 0; slate[i] = 0; coffr[i] = a.comm_off[sbase + i]; }
+  for (uint32_t i = tid; i < R * ncr; i += FT_NT) {
+    const uint32_t row = i / ncr, ro = i - row * ncr;
+    const uint32_t cid = a.role_comm[(uint64_t)(sbase + row) * CROLES + ro];
+    rcs[row * NCRM + ro] = cid;
+    rcb[row * NCRM + ro] = a.ch_base[cid];
+  }
+  __syncthreads();  // nlist / dpos initialised before the position loop below
+  for (uint32_t p = tid; p < T; p += FT_NT) {
+    if (p >= np) { pa[p] = 0; pb[p] = 0; pk[p] = 0; vd[p] = 0; pcode[p] = 4; continue; }
+    const uint32_t A = a.posA[(uint64_t)tile * T + p], B = a.posB[(uint64_t)tile * T + p];
+    const uint16_t K = a.posK[(uint64_t)tile * T + p];
+    pa[p] = A; pb[p] = B; pk[p] = K;
+    const uint32_t ty = (B >> 25) & 7u, role = (B >> 20) & 31u;
+    const bool isc = (K & 7u) == 0;
+    const uint32_t li = isc ? 0u : (ty == TY_TP ? 1u : (ty == TY_DP ? 2u : 3u));
+    pcode[p] = (uint8_t)li;
+    const uint32_t sl = atomicAdd(&nlist[li], 1u);
+    lst[li * T + sl] = (uint16_t)p;
+    if (isc) {
+      vd[p] = 0;
+    } else {
+      cl[(A >> 10) & 1023u] = (uint16_t)(p | ((li - 1u) << 14));
+      vd[p] = role < 16 ? (1u | (role << 2)) : (2u | ((uint32_t)(((int)(role & 7u) - 4) * (int)R + 0x100000) << 2));
+      if (((A >> 30) & 1u) && li < 3 && a.mode == 0 && jp0 < j0) dpos = (int32_t)p;
+    }
+  }
+  __syncthreads();
+  // ---- (1) load every rank row of the tile (8 positions per lane), verify kind_op and comm against
+  // the template, transpose into sd, accumulate per-rank compute / in-block comm duration sums
+  {
+    const uint32_t n8 = (np + 7) / 8;
+    bool mis = false;
+    for (uint32_t u = wid; u < nrb * n8; u += FT_NW) {
+      const uint32_t c8 = u / nrb, rb = u - c8 * nrb;
+      const uint32_t row = rb * 32 + lane, q0 = c8 * 8;
+      const bool valid = row < R;
+      uint32_t kk[4] = {0, 0, 0, 0}, cm[8] = {0, 0, 0, 0, 0, 0, 0, 0}, du[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (valid) {
+        const uint64_t g = rbase + (uint64_t)row * npos + p0 + q0;
+        if (a.aligned8 && q0 + 8 <= np) {
+          const uint4 kv = __ldg(reinterpret_cast<const uint4*>(a.kind + g));
+          const uint4 c0 = __ldg(reinterpret_cast<const uint4*>(a.comm + g));
+          const uint4 c1 = __ldg(reinterpret_cast<const uint4*>(a.comm + g + 4));
+          const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(a.dur + g));
+          const uint4 d1 = __ldg(reinterpret_cast<const uint4*>(a.dur + g + 4));
+          kk[0] = kv.x; kk[1] = kv.y; kk[2] = kv.z; kk[3] = kv.w;
+          cm[0] = c0.x; cm[1] = c0.y; cm[2] = c0.z; cm[3] = c0.w; cm[4] = c1.x; cm[5] = c1.y; cm[6] = c1.z; cm[7] = c1.w;
+          du[0] = d0.x; du[1] = d0.y; du[2] = d0.z; du[3] = d0.w; du[4] = d1.x; du[5] = d1.y; du[6] = d1.z; du[7] = d1.w;
+        } else {
+          for (uint32_t i = 0; i < 8 && q0 + i < np; ++i) {
+            kk[i >> 1] |= (uint32_t)a.kind[g + i] << (16 * (i & 1));
+            cm[i] = a.comm[g + i];
+            du[i] = a.dur[g + i];
+          }
+        }
+      }
+      const uint4 tk = *reinterpret_cast<const uint4*>(pk + q0);
+      const uint4 v0 = *reinterpret_cast<const uint4*>(vd + q0), v1 = *reinterpret_cast<const uint4*>(vd + q0 + 4);
+      const uint32_t dv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      if (valid) {
+        mis |= (kk[0] != tk.x) | (kk[1] != tk.y) | (kk[2] != tk.z) | (kk[3] != tk.w);
+        const uint32_t r = sbase + row;
+        const uint32_t* rc = rcs + row * NCRM;
+        uint32_t sc_lo = 0, sc_hi = 0, si_lo = 0, si_hi = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t t = dv[i] & 3u, x = dv[i] >> 2;
+          const uint32_t e1 = rc[t == 1 ? x : 0u];
+          mis |= (t != 0) & (cm[i] != (t == 1 ? e1 : r + x - 0x100000u));
+          if (q0 + i < np) {
+            sd[(q0 + i) * RP + row] = du[i];
+            const uint32_t pc = pcode[q0 + i];
+            if (pc == 0) { const uint32_t o = sc_lo; sc_lo += du[i]; sc_hi += sc_lo < o; }
+            else if (pc < 3) { const uint32_t o = si_lo; si_lo += du[i]; si_hi += si_lo < o; }
+          }
+        }
+        if (sc_lo | sc_hi) add64_lohi(&rsum[4 * row], &rsum[4 * row + 1], ((unsigned long long)sc_hi << 32) | sc_lo);
+        if (si_lo | si_hi) add64_lohi(&rsum[4 * row + 2], &rsum[4 * row + 3], ((unsigned long long)si_hi << 32) | si_lo);
+      }
+    }
+    if (__any_sync(0xFFFFFFFFu, mis) && lane == 0) bad = 1;
+  }
+  __syncthreads();
+  if (bad) { if (tid == 0) atomicOr(&a.cnt->overflow, NOT_SPMD); return; }
+  // ---- (2) phase A: stage 1. Exact quick reject per DP group: den*max <= num*min -> nobody slow.
+  const uint32_t nc = nlist[0];
+  if (P >= 2) {
+    bool sl_any = false;
+    for (uint32_t i = wid; i < nc; i += FT_NW) {
+      const uint32_t p = lst[i];
+      const uint32_t* col = sd + p * RP;
+      uint32_t mn = 0xFFFFFFFFu, mx = 0;
+#pragma unroll
+      for (int k = 0; k < NRLM; ++k) {
+        const uint32_t row = lane + 32u * k;
+        if (k < (int)nrb && row < R) { const uint32_t v = col[row]; mn = min(mn, v); mx = max(mx, v); }
+      }
+      for (uint32_t m = TP; m < 32; m <<= 1) {
+        mn = min(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, m));
+        mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, m));
+      }
+      const bool maybe = (unsigned long long)a.slow_den * mx > (unsigned long long)a.slow_num * mn;
+      const unsigned need = __ballot_sync(0xFFFFFFFFu, lane < TP && (maybe || a.want_ref));
+      if (need & (1u << lane)) loo_group<P>(a, col, lane, TP, DP, j0 + (pa[p] & 1023u), sbits, SW, wb, sbase, sl_any);
+    }
+    if (sl_any) anyslow = 1;
+  }
+  for (uint32_t p = tid; p < np; p += FT_NT) {
+    if (!(pa[p] >> 31)) continue;
+    const uint32_t v = j0 + (pa[p] & 1023u) + ((pk[p] & 7u) == 0 ? 1u : 0u);
+    const uint32_t itp = it0 + (pb[p] & 1023u);
+    for (uint32_t row = 0; row < R; ++row) a.citer[(uint64_t)(sbase + row) * a.NIT1 + itp + 1] = v;
+  }
+  __syncthreads();
+  const bool tslow = anyslow != 0;
+  if (tslow)
+    for (uint32_t row = tid; row < R; row += FT_NT) {
+      uint32_t o = 0;
+      for (uint32_t w = 0; w < SW; ++w) o |= sbits[row * SW + w];
+      rslow[row] = o != 0;
+    }
+  __syncthreads();
+  // ---- (3) phase B: one warp per comm position
+  const uint32_t ncm = nlist[1] + nlist[2] + nlist[3];
+  for (uint32_t jj = wid; jj < ncm; jj += FT_NW) {
+    const uint32_t cv = cl[jj];
+    const uint32_t p = cv & 0x3FFFu, cls = cv >> 14;  // 0 TP, 1 DP, 2 cross
+    const uint32_t A = pa[p], B = pb[p];
+    const uint32_t role = (B >> 20) & 31u;
+    const uint32_t krel = (B >> 10) & 1023u;
+    const uint32_t itp = it0 + (B & 1023u);
+    uint32_t* col = sd + p * RP;
+    if (cls == 2) {
+      const uint32_t kk = kbase[role] + krel;
+      for (uint32_t k = 0; k < nrb; ++k) {
+        const uint32_t row = lane + 32 * k;
+        if (row >= R) break;
+        const uint32_t r = sbase + row;
+        uint64_t ch; uint32_t nm, slot;
+        bool send = false;
+        if (role < 16) {
+          const uint32_t cid = rcs[row * NCRM + role];
+          ch = cid; nm = (uint32_t)(a.coff[cid + 1] - a.coff[cid]); slot = a.role_slot[(uint64_t)r * CROLES + role];
+        } else {
+          const int ds = (int)(role & 7u) - 4;
+          send = (role >> 3) & 1u;
+          const uint32_t peer = (uint32_t)((int)r + ds * (int)R);
+          const uint32_t src = send ? r : peer, dst = send ? peer : r;
+          const uint32_t xk = src * (uint32_t)a.W + dst;
+          ch = a.n_comms + a.bitpre[xk >> 5] + __popc(a.bitmap[xk >> 5] & ((1u << (xk & 31)) - 1u));
+          nm = 2; slot = send ? 0 : 1;
+        }
+        const uint64_t inst = a.ch_base[ch] + kk;
+        const uint64_t si = a.ch_slot[ch] + (uint64_t)kk * nm + slot;
+        const uint64_t e = rbase + (uint64_t)row * npos + p0 + p;
+        a.sdur[si] = col[row];
+        a.skind[si] = (uint8_t)(pk[p] & 7u);
+        a.sci[si] = (uint32_t)(coffr[row] + m0 + ((A >> 10) & 1023u));
+        a.sit[si] = itp;
+        col[row] = (uint32_t)inst;  // cross positions: the tile now holds the instance id
+        if (role >= 16) {
+          a.p2p_pay[si - a.p2p_slot0] = a.pay[e];
+          if (send) {
+            a.p2p_warm[inst - a.p2p_inst0] = (uint8_t)((a.meta[e] >> 14) & 1u);
+            a.p2p_iter[inst - a.p2p_inst0] = itp;
+          }
+        }
+      }
+      continue;
+    }
+    const bool istp = cls == 0;
+    const uint32_t win = a.wi ? itp / a.wi : 0;
+    const uint32_t clsid = istp ? 1u : 2u;
+    const bool elig = (a.classes >> (clsid - 1)) & 1u;
+    const bool isdef = (int32_t)p == dpos;
+    const bool chk = elig && (a.mode || tslow || isdef);
+    const uint32_t jp = j0 + (A & 1023u);
+    const uint32_t jprev = ((A >> 30) & 1u) ? jp0 : j0 + ((A >> 20) & 1023u);
+    const uint32_t kinst = kbase[role] + krel;
+    // one group instance: min / max / last arriver (lowest slot with the min) / tie count, then the
+    // members' waits, wait-for edges and stage-2 counters
+    auto apply = [&](uint32_t row, uint32_t d, uint32_t mn, uint32_t mx, uint32_t lastrow, uint32_t slot, uint32_t g,
+                     uint32_t row0, bool leader, uint32_t nat) {
+      const uint32_t last = sbase + lastrow;
+      const bool islast = row == lastrow;
+      if (leader) {
+        const uint64_t inst = rcb[row0 * NCRM + role] + kinst;
+        a.rec[inst] = make_uint4(mn, mx, last, (SCAN_F_COMPLETE | SCAN_F_KIND_OK | SCAN_F_PAYLOAD_OK | SCAN_F_VALID |
+                                                (nat == 1 ? SCAN_F_UNIQUE_LAST : 0u)) | (clsid << 8));
+        sinst[p * G + g] = (uint32_t)inst;
+        const uint32_t gi = istp ? g : DP + g;
+        add64_lohi(&gsum[gi], &gsum[DP + TP + gi], mn);
+      }
+      const uint32_t wait = d - mn;
+      col[row] = wait;  // in-block comm positions now hold the wait
+      if (!islast && (unsigned long long)wait > a.wait_margin) {
+        if (win == w_tile) {
+          const uint32_t old = atomicAdd(&sedge[row * E + slot], wait);
+          if (old + wait < old)
+            atomicAdd(&a.ew[(uint64_t)w_tile * a.nnz_tot + a.eidx[(uint64_t)(sbase + row) * E + slot]], 1ull << 32);
+        } else {
+          atomicAdd(&a.ew[(uint64_t)win * a.nnz_tot + a.eidx[(uint64_t)(sbase + row) * E + slot]], (unsigned long long)wait);
+        }
+      }
+      if (!chk) return;
+      const bool lt = islast && nat == 1 && (unsigned long long)(mx - mn) > a.late_margin;
+      if (isdef) {
+        if (lt) atomicOr(&a.dlate[(uint64_t)tile * ((R + 31) / 32) + row / 32], 1u << (row & 31));
+        return;
+      }
+      const bool pslow = a.mode != 0 || (rslow[row] && sbits_any(sbits + row * SW, wb, jprev, jp));
+      if (!pslow) return;
+      if (win == w_tile) { atomicAdd(&sjoin[row], 1u); if (lt) atomicAdd(&slate[row], 1u); }
+      else {
+        const uint32_t r = sbase + row;
+        atomicAdd(&a.wl_joined[(uint64_t)win * a.W + r], 1u);
+        if (lt) atomicAdd(&a.wl_late[(uint64_t)win * a.W + r], 1u);
+      }
+    };
+    if (istp) {
+      const uint32_t gm = TP >= 32 ? 0xFFFFFFFFu : (((1u << TP) - 1u) << (lane & ~(TP - 1u)));
+      for (uint32_t k = 0; k < nrb; ++k) {
+        const uint32_t row = lane + 32u * k;
+        const bool valid = row < R;
+        const uint32_t d = valid ? col[row] : 0xFFFFFFFFu;
+        uint32_t mn = d, mx = valid ? d : 0u;
+        for (uint32_t m = 1; m < TP; m <<= 1) {
+          mn = min(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, m));
+          mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, m));
+        }
+        const unsigned eq = __ballot_sync(0xFFFFFFFFu, valid && d == mn) & gm;
+        const uint32_t ls = eq ? (uint32_t)(__ffs(eq) - 1) : 0u;
+        if (valid) {
+          const uint32_t g = row / TP;
+          apply(row, d, mn, mx, ls + 32u * k, ls & (TP - 1u), g, g * TP, (lane & (TP - 1u)) == 0, __popc(eq));
+        }
+      }
+    } else {
+      uint32_t mn = 0xFFFFFFFFu, mx = 0;
+      for (uint32_t k = 0; k < nrb; ++k) {
+        const uint32_t row = lane + 32u * k;
+        if (row < R) { const uint32_t d = col[row]; mn = min(mn, d); mx = max(mx, d); }
+      }
+      for (uint32_t m = TP; m < 32; m <<= 1) {
+        mn = min(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, m));
+        mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, m));
+      }
+      uint32_t lsd = 0xFFFFFFFFu, nat = 0;  // lowest DP index with d == min, tie count
+      for (uint32_t k = 0; k < nrb; ++k) {
+        const uint32_t row = lane + 32u * k;
+        if (row < R && col[row] == mn) { lsd = min(lsd, row / TP); ++nat; }
+      }
+      for (uint32_t m = TP; m < 32; m <<= 1) {
+        lsd = min(lsd, __shfl_xor_sync(0xFFFFFFFFu, lsd, m));
+        nat += __shfl_xor_sync(0xFFFFFFFFu, nat, m);
+      }
+      for (uint32_t k = 0; k < nrb; ++k) {
+        const uint32_t row = lane + 32u * k;
+        if (row >= R) break;
+        const uint32_t g = row & (TP - 1u);
+        apply(row, col[row], mn, mx, g + TP * lsd, TP + lsd, g, g, row < TP, nat);
+      }
+    }
+  }
+  __syncthreads();
+  // ---- (4) flush: coalesced per-rank inst / wait rows
+  {
+    const FDiv fm = fdiv_make(ncm > 0 ? ncm : 1u);
+    for (uint32_t i = tid; i < R * ncm; i += FT_NT) {
+      const uint32_t row = fdiv(i, fm), j = i - row * ncm;
+      const uint32_t cv = cl[j];
+      const uint32_t p = cv & 0x3FFFu, cls = cv >> 14;
+      const uint32_t v = sd[p * RP + row];
+      const uint32_t gi = cls == 0 ? row / TP : row & (TP - 1u);
+      const uint32_t si = sinst[cls < 2 ? p * G + gi : 0u];
+      uint32_t* dst = a.inst_c + coffr[row] + m0 + j;
+      *dst = cls < 2 ? si : v;
+      if (cls < 2) a.wait_c[dst - a.inst_c] = v;
+    }
+  }
+  // stage-1 counters per (window, rank)
+  const uint32_t it_last = it0 + (np ? (pb[np - 1] & 1023u) : 0u);
+  const bool one_window = !a.wi || (it0 / a.wi == it_last / a.wi);
+  if (P >= 2 && nc) {
+    if (one_window) {
+      for (uint32_t row = tid; row < R; row += FT_NT) {
+        const uint32_t r = sbase + row;
+        uint32_t sl = 0;
+        if (tslow) for (uint32_t w = 0; w < SW; ++w) sl += __popc(sbits[row * SW + w]);
+        atomicAdd(&a.wd_total[(uint64_t)w_tile * a.W + r], nc);
+        if (sl) atomicAdd(&a.wd_slow[(uint64_t)w_tile * a.W + r], sl);
+      }
+    } else {
+      for (uint32_t i = tid; i < R * nc; i += FT_NT) {
+        const uint32_t row = i / nc, p = lst[i - row * nc], r = sbase + row;
+        const uint32_t win = (it0 + (pb[p] & 1023u)) / a.wi;
+        const uint32_t j = j0 + (pa[p] & 1023u);
+        atomicAdd(&a.wd_total[(uint64_t)win * a.W + r], 1u);
+        if ((sbits[row * SW + (j >> 5) - wb] >> (j & 31)) & 1u) atomicAdd(&a.wd_slow[(uint64_t)win * a.W + r], 1u);
+      }
+    }
+  }
+  for (uint32_t row = tid; row < R; row += FT_NT) {
+    const uint32_t r = sbase + row;
+    const uint32_t gt = row / TP, gd = row & (TP - 1u), GO = DP + TP;
+    const unsigned long long tr = ((unsigned long long)gsum[GO + gt] << 32 | gsum[gt]) * (TP > 1 ? 1ull : 0ull) +
+                                  ((unsigned long long)gsum[GO + DP + gd] << 32 | gsum[DP + gd]) * (DP > 1 ? 1ull : 0ull);
+    const unsigned long long comp = (unsigned long long)rsum[4 * row + 1] << 32 | rsum[4 * row];
+    const unsigned long long inb = (unsigned long long)rsum[4 * row + 3] << 32 | rsum[4 * row + 2];
+    if (comp) atomicAdd(&a.rk_sum[r], comp);
+    if (inb - tr) atomicAdd(&a.rk_sum[a.W + r], inb - tr);
+    if (tr) atomicAdd(&a.rk_sum[2 * a.W + r], tr);
+    if (sjoin[row]) atomicAdd(&a.wl_joined[(uint64_t)w_tile * a.W + r], sjoin[row]);
+    if (slate[row]) atomicAdd(&a.wl_late[(uint64_t)w_tile * a.W + r], slate[row]);
+  }
+  for (uint32_t i = tid; i < R * E; i += FT_NT) {
+    const uint32_t v = sedge[i];
+    if (v) atomicAdd(&a.ew[(uint64_t)w_tile * a.nnz_tot + a.eidx[(uint64_t)sbase * E + i]], (unsigned long long)v);
+  }
+  if (nc && tslow) {
+    const uint32_t w_first = j0 >> 5, w_last = (j0 + nc - 1) >> 5;
+    const uint32_t nw = w_last - w_first + 1;
+    for (uint32_t i = tid; i < R * nw; i += FT_NT) {
+      const uint32_t row = i / nw, w = w_first + (i - row * nw);
+      const uint32_t v = sbits[row * SW + (w - wb)];
+      if (v) atomicOr(&a.bits[a.bits_off[sbase + row] + w], v);
+    }
+  }
+  if (tid == 0) {
+    uint32_t* di = a.dinfo + (uint64_t)tile * 4;
+    if (dpos >= 0) {
+      const uint32_t p = (uint32_t)dpos;
+      const uint32_t ty = (pb[p] >> 25) & 7u;
+      di[0] = j0 + (pa[p] & 1023u); di[1] = jp0; di[2] = a.wi ? (it0 + (pb[p] & 1023u)) / a.wi : 0; di[3] = 1u | (ty << 8);
+    } else {
+      di[3] = 0;
+    }
+  }
+}
+
+size_t fused_t_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM) {
+  const uint32_t SW = T / 32 + 2, G = TP > DP ? TP : DP, E = TP + DP;
+  size_t b = (size_t)T * (R + 1) * 4 + 16 + (size_t)R * NCRM * 8 + (size_t)R * 8 + (size_t)T * G * 4 + (size_t)R * SW * 4 +
+             (size_t)R * E * 4 + (size_t)R * NCRM * 4 + (size_t)R * 16 + (size_t)(DP + TP) * 8 + (size_t)R * 12 + 16 +
+             (size_t)T * 12 + (size_t)T * 2 + (size_t)T * 8 + (size_t)T * 2 + (size_t)T;
+  return (b + 15) & ~size_t(15);
+}
+
 size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM) {
   const uint32_t SW = T / 32 + 2, G = TP > DP ? TP : DP;
   size_t b = (size_t)R * T * 4 + (size_t)T * 4 + (size_t)R * 8 + (size_t)R * NCRM * 8 + (size_t)R * 16 +
@@ -796,6 +1252,20 @@ int launch_fused(Ctx& c) {
   a.wi = c.dcfg.window_iters; a.classes = c.lcfg.stage2_classes; a.mode = c.lcfg.stage2_mode;
   a.late_margin = c.lcfg.late_margin_ns; a.wait_margin = c.lcfg.wait_margin_ns; a.want_ref = c.dcfg.want_ref ? 1 : 0;
   a.cnt = c.counters.as<Counters>();
+  if (c.fused_t) {
+    const size_t sm = fused_t_smem_bytes(c.FT, c.FR, c.TP, c.DP, c.NCRM);
+    auto go = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      kern<<<c.n_ftiles, FT_NT, sm, c.stream>>>(a);
+    };
+    if (c.DP < 2) go(k_fused_t<1>);
+    else if (c.DP <= 2) go(k_fused_t<2>);
+    else if (c.DP <= 4) go(k_fused_t<4>);
+    else if (c.DP <= 8) go(k_fused_t<8>);
+    else if (c.DP <= 16) go(k_fused_t<16>);
+    else go(k_fused_t<32>);
+    return 1;
+  }
   const size_t sm = fused_smem_bytes(c.FT, c.FR, c.TP, c.DP, c.NCRM);
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

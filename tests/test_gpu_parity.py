@@ -244,3 +244,41 @@ def test_spmd_comm_violation_falls_back():
     o, g = _run_both(tr)
     compare(o, g)
     assert not g["_res"]["fused"]
+
+
+def _gpu_variant(trace, variant, dcfg=None, lcfg=None):
+    import paper_2507_19845_b200 as ms
+    s = ms.Scan(0)
+    s.fused_variant(variant)
+    s.load(trace)
+    res = s.analyze(dcfg, lcfg)
+    out = s.export_all()
+    out["_res"] = res
+    s.close()
+    return out
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c5w", "tp3"])
+def test_fused_generic_tile_kernel(name):
+    """The generic fused tile kernel (used when TP does not divide 32) against the oracle, also forced on
+    the shapes the transposed kernel normally takes."""
+    if MODE["mode"] != "analyze":
+        pytest.skip("analyze-only")
+    kw = {}
+    if name == "c1":
+        tr = tg.generate(configs.c1(seed=6, iterations=4))
+    elif name == "c2":
+        tr = tg.generate(configs.c2(iterations=6))
+    elif name == "c5w":
+        cfg = configs.c5(iterations=6)
+        cfg.faults = [tg.Fault(tg.THROTTLE, 208, it0=2, factor=2.5)]
+        tr = tg.generate(cfg)
+        kw = dict(window_iters=2)
+    else:
+        tr = tg.generate(tg.GenConfig(3, 2, 4, 2, 6, 3, seed=3, faults=[tg.Fault(tg.THROTTLE, 4, factor=2.0)]))
+    d, l_, oc = _cfgs(**kw)
+    o = oracle.run(tr, oc)
+    for variant in (0, -1):
+        g = _gpu_variant(tr, variant, d, l_)
+        compare(o, g)
+        assert g["_res"]["fused"]
