@@ -464,9 +464,10 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
       const uint32_t pbase = g8 * 8;
       const uint64_t g = rbase + (uint64_t)row * npos + p0 + pbase;
       const uint4 tv = *reinterpret_cast<const uint4*>(pk + pbase);
-      if (a.aligned8 && pbase + 8 <= np) {
-        const uint4 kv = __ldg(reinterpret_cast<const uint4*>(a.kind + g));
-        mis |= (kv.x != tv.x) | (kv.y != tv.y) | (kv.z != tv.z) | (kv.w != tv.w);
+      if (a.aligned && pbase + 8 <= np) {
+        const uint2 ka = __ldg(reinterpret_cast<const uint2*>(a.kind + g));
+        const uint2 kb = __ldg(reinterpret_cast<const uint2*>(a.kind + g + 4));
+        mis |= (ka.x != tv.x) | (ka.y != tv.y) | (kb.x != tv.z) | (kb.y != tv.w);
       } else {
         for (uint32_t q = 0; q < 8 && pbase + q < np; ++q) mis |= a.kind[g + q] != pk[pbase + q];
       }
@@ -904,13 +905,14 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
       uint32_t kk[4] = {0, 0, 0, 0}, cm[8] = {0, 0, 0, 0, 0, 0, 0, 0}, du[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       if (valid) {
         const uint64_t g = rbase + (uint64_t)row * npos + p0 + q0;
-        if (a.aligned8 && q0 + 8 <= np) {
-          const uint4 kv = __ldg(reinterpret_cast<const uint4*>(a.kind + g));
+        if (a.aligned && q0 + 8 <= np) {  // 4-event aligned rows: 8-byte kind loads, 16-byte comm / dur loads
+          const uint2 ka = __ldg(reinterpret_cast<const uint2*>(a.kind + g));
+          const uint2 kb = __ldg(reinterpret_cast<const uint2*>(a.kind + g + 4));
           const uint4 c0 = __ldg(reinterpret_cast<const uint4*>(a.comm + g));
           const uint4 c1 = __ldg(reinterpret_cast<const uint4*>(a.comm + g + 4));
           const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(a.dur + g));
           const uint4 d1 = __ldg(reinterpret_cast<const uint4*>(a.dur + g + 4));
-          kk[0] = kv.x; kk[1] = kv.y; kk[2] = kv.z; kk[3] = kv.w;
+          kk[0] = ka.x; kk[1] = ka.y; kk[2] = kb.x; kk[3] = kb.y;
           cm[0] = c0.x; cm[1] = c0.y; cm[2] = c0.z; cm[3] = c0.w; cm[4] = c1.x; cm[5] = c1.y; cm[6] = c1.z; cm[7] = c1.w;
           du[0] = d0.x; du[1] = d0.y; du[2] = d0.z; du[3] = d0.w; du[4] = d1.x; du[5] = d1.y; du[6] = d1.z; du[7] = d1.w;
         } else {
