@@ -970,7 +970,9 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
       }
       const bool maybe = (unsigned long long)a.slow_den * mx > (unsigned long long)a.slow_num * mn;
       const unsigned need = __ballot_sync(0xFFFFFFFFu, lane < TP && (maybe || a.want_ref));
-      if (need & (1u << lane)) loo_group<P>(a, col, lane, TP, DP, j0 + (pa[p] & 1023u), sbits, SW, wb, sbase, sl_any);
+      if (need) {  // warp-uniform: the rare full LOO path is branched around, not predicated
+        if ((need >> lane) & 1u) loo_group<P>(a, col, lane, TP, DP, j0 + (pa[p] & 1023u), sbits, SW, wb, sbase, sl_any);
+      }
     }
     if (sl_any) anyslow = 1;
   }
