@@ -768,7 +768,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
 constexpr int FT_NT = 512, FT_NW = FT_NT / 32, NRLM = 8;
 
 template <int P>
-__device__ void loo_group(const FusedArgs& a, const uint32_t* col, uint32_t tp, uint32_t TP, uint32_t DP, uint32_t j,
+__device__ __noinline__ void loo_group(const FusedArgs& a, const uint32_t* col, uint32_t tp, uint32_t TP, uint32_t DP, uint32_t j,
                           uint32_t* sbits, uint32_t SW, uint32_t wb, uint32_t sbase, bool& slow_any) {
   const int q = ((int)DP - 2) / 2;
   const int L = P / 2 - 1 - q;
