@@ -15,6 +15,7 @@
 // Cross-stage instances (model-parallel, embedding, P2P) are scattered to their slots and
 // finished by k_cross_reduce. Any verification failure sets a flag and the whole analysis is
 // redone by the general path (api.cu), so results never depend on the SPMD assumption.
+#include <type_traits>
 #include "internal.cuh"
 
 namespace ms {
@@ -355,7 +356,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   uint32_t* slate = sjoin + R;                                          // R
   uint32_t* rslow = slate + R;                                          // R: row has a slow bit in this tile
   uint8_t* gmask = (uint8_t*)(rslow + R);                               // T/4 granule masks: compute | in-block << 4
-  uint16_t* pk = (uint16_t*)(((uintptr_t)(gmask + T / 4) + 15) & ~(uintptr_t)15);  // T template kind_op, 16 B aligned
+  uint16_t* pk = reinterpret_cast<uint16_t*>(smem_raw + ((((uint8_t*)(gmask + T / 4) - smem_raw) + 15) & ~15));  // 16 B aligned
   uint16_t* lst = pk + T;                                               // 4 x T
   uint16_t* cl = lst + 4 * T;                                           // T: comm positions by m, | class << 14
   __shared__ uint32_t kbase[ROLES];
@@ -768,7 +769,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
 constexpr int FT_NT = 512, FT_NW = FT_NT / 32, NRLM = 8;
 
 template <int P>
-__device__ __noinline__ void loo_group(const FusedArgs& a, const uint32_t* col, uint32_t tp, uint32_t TP, uint32_t DP, uint32_t j,
+__device__ __forceinline__ void loo_group(const FusedArgs& a, const uint32_t* col, uint32_t tp, uint32_t TP, uint32_t DP, uint32_t j,
                           uint32_t* sbits, uint32_t SW, uint32_t wb, uint32_t sbase, bool& slow_any) {
   const int q = ((int)DP - 2) / 2;
   const int L = P / 2 - 1 - q;
@@ -807,34 +808,45 @@ __device__ __noinline__ void loo_group(const FusedArgs& a, const uint32_t* col, 
   }
 }
 
-__device__ __forceinline__ uint32_t* al16(void* p) { return (uint32_t*)(((uintptr_t)p + 15) & ~(uintptr_t)15); }
+__device__ __forceinline__ void loo_dispatch(const FusedArgs& a, const uint32_t* col, uint32_t tp, uint32_t TP, uint32_t DP,
+                                             uint32_t j, uint32_t* sbits, uint32_t SW, uint32_t wb, uint32_t sbase, bool& any) {
+  if (DP <= 2) loo_group<2>(a, col, tp, TP, DP, j, sbits, SW, wb, sbase, any);
+  else if (DP <= 4) loo_group<4>(a, col, tp, TP, DP, j, sbits, SW, wb, sbase, any);
+  else if (DP <= 8) loo_group<8>(a, col, tp, TP, DP, j, sbits, SW, wb, sbase, any);
+  else if (DP <= 16) loo_group<16>(a, col, tp, TP, DP, j, sbits, SW, wb, sbase, any);
+  else loo_group<32>(a, col, tp, TP, DP, j, sbits, SW, wb, sbase, any);
+}
 
-template <int P>
+template <int P, int NRB>
 __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const uint32_t T = a.T, R = a.R, TP = (uint32_t)a.TP, DP = (uint32_t)a.DP, G = a.G;
   const uint32_t SW = T / 32 + 2, E = TP + DP, NCRM = a.NCRM, RP = R + 1;
-  const uint32_t nrb = (R + 31) / 32;  // row blocks (lane l owns rows l + 32k, k < nrb)
-  // ---- shared memory carve-up (see fused_t_smem_bytes)
-  uint32_t* sd = (uint32_t*)smem_raw;                                  // T x (R+1), position-major
-  unsigned long long* rcb = (unsigned long long*)al16(sd + (uint64_t)T * RP);  // R x NCRM channel bases
-  unsigned long long* coffr = rcb + (uint64_t)R * NCRM;                // R comm offsets
-  uint32_t* sinst = (uint32_t*)(coffr + R);                            // T x G instance ids of in-block groups
-  uint32_t* sbits = sinst + (uint64_t)T * G;                           // R x SW slow bits
-  uint32_t* sedge = sbits + (uint64_t)R * SW;                          // R x E wait-for weights (low word)
-  uint32_t* rcs = sedge + (uint64_t)R * E;                             // R x NCRM communicator of each role
-  uint32_t* rsum = rcs + (uint64_t)R * NCRM;                           // R x 4: compute lo/hi, in-block lo/hi
-  uint32_t* gsum = rsum + 4 * (uint64_t)R;                             // 2 x (DP+TP): lo / hi
-  uint32_t* sjoin = gsum + 2 * (DP + TP);                              // R
-  uint32_t* slate = sjoin + R;                                         // R
-  uint32_t* rslow = slate + R;                                         // R
-  uint32_t* pa = al16(rslow + R);                                      // T
-  uint32_t* pb = pa + T;                                               // T
-  uint32_t* vd = pb + T;                                               // T verification descriptors (16 B aligned)
-  uint16_t* pk = (uint16_t*)(vd + T);                                  // T template kind_op (16 B aligned)
-  uint16_t* lst = pk + T;                                              // 4 x T position lists
-  uint16_t* cl = lst + 4 * T;                                          // T comm positions by m | class << 14
-  uint8_t* pcode = (uint8_t*)(cl + T);                                 // T: 0 compute 1 TP 2 DP 3 cross
+  constexpr uint32_t nrb = NRB;        // row blocks (lane l owns rows l + 32k, k < NRB); R <= 32*NRB
+  const uint32_t tpsh = __ffs(TP) - 1;  // TP is a power of two here
+  // ---- shared memory carve-up (see fused_t_smem_bytes): byte offsets from smem_raw so every array
+  // stays in the shared address space (LDS/STS, no generic-pointer conversion)
+  uint32_t off = 0;
+  auto take = [&](uint32_t bytes, uint32_t align) { off = (off + align - 1) & ~(align - 1); const uint32_t o = off; off += bytes; return o; };
+  uint32_t* sd = reinterpret_cast<uint32_t*>(smem_raw + take(T * RP * 4, 16));               // T x (R+1), position-major
+  unsigned long long* rcb = reinterpret_cast<unsigned long long*>(smem_raw + take(R * NCRM * 8, 16));  // channel bases
+  unsigned long long* coffr = reinterpret_cast<unsigned long long*>(smem_raw + take(R * 8, 8));       // comm offsets
+  uint32_t* sinst = reinterpret_cast<uint32_t*>(smem_raw + take(T * G * 4, 4));              // T x G in-block inst ids
+  uint32_t* sbits = reinterpret_cast<uint32_t*>(smem_raw + take(R * SW * 4, 4));             // R x SW slow bits
+  uint32_t* sedge = reinterpret_cast<uint32_t*>(smem_raw + take(R * E * 4, 4));              // R x E edge weights (low)
+  uint32_t* rcs = reinterpret_cast<uint32_t*>(smem_raw + take(R * NCRM * 4, 4));             // R x NCRM role comms
+  uint32_t* rsum = reinterpret_cast<uint32_t*>(smem_raw + take(R * 16, 4));                  // R x 4 sums lo/hi
+  uint32_t* gsum = reinterpret_cast<uint32_t*>(smem_raw + take((DP + TP) * 8, 4));           // 2 x (DP+TP)
+  uint32_t* sjoin = reinterpret_cast<uint32_t*>(smem_raw + take(R * 4, 4));
+  uint32_t* slate = reinterpret_cast<uint32_t*>(smem_raw + take(R * 4, 4));
+  uint32_t* rslow = reinterpret_cast<uint32_t*>(smem_raw + take(R * 4, 4));
+  uint32_t* pa = reinterpret_cast<uint32_t*>(smem_raw + take(T * 4, 16));
+  uint32_t* pb = reinterpret_cast<uint32_t*>(smem_raw + take(T * 4, 16));
+  uint32_t* vd = reinterpret_cast<uint32_t*>(smem_raw + take(T * 4, 16));                   // verification descriptors
+  uint16_t* pk = reinterpret_cast<uint16_t*>(smem_raw + take(T * 2, 16));                   // template kind_op
+  uint16_t* lst = reinterpret_cast<uint16_t*>(smem_raw + take(T * 8, 4));                   // 4 x T position lists
+  uint16_t* cl = reinterpret_cast<uint16_t*>(smem_raw + take(T * 2, 4));                    // comm positions by m
+  uint8_t* pcode = reinterpret_cast<uint8_t*>(smem_raw + take(T, 4));                       // 0 comp 1 TP 2 DP 3 cross
   __shared__ uint32_t kbase[ROLES];
   __shared__ uint32_t nlist[4];
   __shared__ int32_t dpos;
@@ -953,16 +965,16 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
   if (bad) { if (tid == 0) atomicOr(&a.cnt->overflow, NOT_SPMD); return; }
   // ---- (2) phase A: stage 1. Exact quick reject per DP group: den*max <= num*min -> nobody slow.
   const uint32_t nc = nlist[0];
-  if (P >= 2) {
+  if (DP >= 2) {
     bool sl_any = false;
     for (uint32_t i = wid; i < nc; i += FT_NW) {
       const uint32_t p = lst[i];
       const uint32_t* col = sd + p * RP;
       uint32_t mn = 0xFFFFFFFFu, mx = 0;
 #pragma unroll
-      for (int k = 0; k < NRLM; ++k) {
+      for (int k = 0; k < NRB; ++k) {
         const uint32_t row = lane + 32u * k;
-        if (k < (int)nrb && row < R) { const uint32_t v = col[row]; mn = min(mn, v); mx = max(mx, v); }
+        if (row < R) { const uint32_t v = col[row]; mn = min(mn, v); mx = max(mx, v); }
       }
       for (uint32_t m = TP; m < 32; m <<= 1) {
         mn = min(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, m));
@@ -1003,6 +1015,7 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
     uint32_t* col = sd + p * RP;
     if (cls == 2) {
       const uint32_t kk = kbase[role] + krel;
+#pragma unroll
       for (uint32_t k = 0; k < nrb; ++k) {
         const uint32_t row = lane + 32 * k;
         if (row >= R) break;
@@ -1090,6 +1103,7 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
     };
     if (istp) {
       const uint32_t gm = TP >= 32 ? 0xFFFFFFFFu : (((1u << TP) - 1u) << (lane & ~(TP - 1u)));
+#pragma unroll
       for (uint32_t k = 0; k < nrb; ++k) {
         const uint32_t row = lane + 32u * k;
         const bool valid = row < R;
@@ -1102,12 +1116,13 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
         const unsigned eq = __ballot_sync(0xFFFFFFFFu, valid && d == mn) & gm;
         const uint32_t ls = eq ? (uint32_t)(__ffs(eq) - 1) : 0u;
         if (valid) {
-          const uint32_t g = row / TP;
-          apply(row, d, mn, mx, ls + 32u * k, ls & (TP - 1u), g, g * TP, (lane & (TP - 1u)) == 0, __popc(eq));
+          const uint32_t g = row >> tpsh;
+          apply(row, d, mn, mx, ls + 32u * k, ls & (TP - 1u), g, g << tpsh, (lane & (TP - 1u)) == 0, __popc(eq));
         }
       }
     } else {
       uint32_t mn = 0xFFFFFFFFu, mx = 0;
+#pragma unroll
       for (uint32_t k = 0; k < nrb; ++k) {
         const uint32_t row = lane + 32u * k;
         if (row < R) { const uint32_t d = col[row]; mn = min(mn, d); mx = max(mx, d); }
@@ -1117,19 +1132,21 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
         mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, m));
       }
       uint32_t lsd = 0xFFFFFFFFu, nat = 0;  // lowest DP index with d == min, tie count
+#pragma unroll
       for (uint32_t k = 0; k < nrb; ++k) {
         const uint32_t row = lane + 32u * k;
-        if (row < R && col[row] == mn) { lsd = min(lsd, row / TP); ++nat; }
+        if (row < R && col[row] == mn) { lsd = min(lsd, row >> tpsh); ++nat; }
       }
       for (uint32_t m = TP; m < 32; m <<= 1) {
         lsd = min(lsd, __shfl_xor_sync(0xFFFFFFFFu, lsd, m));
         nat += __shfl_xor_sync(0xFFFFFFFFu, nat, m);
       }
+#pragma unroll
       for (uint32_t k = 0; k < nrb; ++k) {
         const uint32_t row = lane + 32u * k;
         if (row >= R) break;
         const uint32_t g = row & (TP - 1u);
-        apply(row, col[row], mn, mx, g + TP * lsd, TP + lsd, g, g, row < TP, nat);
+        apply(row, col[row], mn, mx, g + (lsd << tpsh), TP + lsd, g, g, row < TP, nat);
       }
     }
   }
@@ -1142,7 +1159,7 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
       const uint32_t cv = cl[j];
       const uint32_t p = cv & 0x3FFFu, cls = cv >> 14;
       const uint32_t v = sd[p * RP + row];
-      const uint32_t gi = cls == 0 ? row / TP : row & (TP - 1u);
+      const uint32_t gi = cls == 0 ? row >> tpsh : row & (TP - 1u);
       const uint32_t si = sinst[cls < 2 ? p * G + gi : 0u];
       uint32_t* dst = a.inst_c + coffr[row] + m0 + j;
       *dst = cls < 2 ? si : v;
@@ -1152,7 +1169,7 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
   // stage-1 counters per (window, rank)
   const uint32_t it_last = it0 + (np ? (pb[np - 1] & 1023u) : 0u);
   const bool one_window = !a.wi || (it0 / a.wi == it_last / a.wi);
-  if (P >= 2 && nc) {
+  if (DP >= 2 && nc) {
     if (one_window) {
       for (uint32_t row = tid; row < R; row += FT_NT) {
         const uint32_t r = sbase + row;
@@ -1173,7 +1190,7 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
   }
   for (uint32_t row = tid; row < R; row += FT_NT) {
     const uint32_t r = sbase + row;
-    const uint32_t gt = row / TP, gd = row & (TP - 1u), GO = DP + TP;
+    const uint32_t gt = row >> tpsh, gd = row & (TP - 1u), GO = DP + TP;
     const unsigned long long tr = ((unsigned long long)gsum[GO + gt] << 32 | gsum[gt]) * (TP > 1 ? 1ull : 0ull) +
                                   ((unsigned long long)gsum[GO + DP + gd] << 32 | gsum[DP + gd]) * (DP > 1 ? 1ull : 0ull);
     const unsigned long long comp = (unsigned long long)rsum[4 * row + 1] << 32 | rsum[4 * row];
@@ -1210,11 +1227,15 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
 }
 
 size_t fused_t_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM) {
-  const uint32_t SW = T / 32 + 2, G = TP > DP ? TP : DP, E = TP + DP;
-  size_t b = (size_t)T * (R + 1) * 4 + 16 + (size_t)R * NCRM * 8 + (size_t)R * 8 + (size_t)T * G * 4 + (size_t)R * SW * 4 +
-             (size_t)R * E * 4 + (size_t)R * NCRM * 4 + (size_t)R * 16 + (size_t)(DP + TP) * 8 + (size_t)R * 12 + 16 +
-             (size_t)T * 12 + (size_t)T * 2 + (size_t)T * 8 + (size_t)T * 2 + (size_t)T;
-  return (b + 15) & ~size_t(15);
+  const uint32_t SW = T / 32 + 2, G = TP > DP ? TP : DP, E = TP + DP, RP = R + 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes, size_t align) { off = (off + align - 1) & ~(align - 1); off += bytes; };
+  take((size_t)T * RP * 4, 16); take((size_t)R * NCRM * 8, 16); take((size_t)R * 8, 8); take((size_t)T * G * 4, 4);
+  take((size_t)R * SW * 4, 4); take((size_t)R * E * 4, 4); take((size_t)R * NCRM * 4, 4); take((size_t)R * 16, 4);
+  take((size_t)(DP + TP) * 8, 4); take((size_t)R * 4, 4); take((size_t)R * 4, 4); take((size_t)R * 4, 4);
+  take((size_t)T * 4, 16); take((size_t)T * 4, 16); take((size_t)T * 4, 16); take((size_t)T * 2, 16);
+  take((size_t)T * 8, 4); take((size_t)T * 2, 4); take((size_t)T, 4);
+  return (off + 15) & ~size_t(15);
 }
 
 size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM) {
@@ -1262,12 +1283,20 @@ int launch_fused(Ctx& c) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       kern<<<c.n_ftiles, FT_NT, sm, c.stream>>>(a);
     };
-    if (c.DP < 2) go(k_fused_t<1>);
-    else if (c.DP <= 2) go(k_fused_t<2>);
-    else if (c.DP <= 4) go(k_fused_t<4>);
-    else if (c.DP <= 8) go(k_fused_t<8>);
-    else if (c.DP <= 16) go(k_fused_t<16>);
-    else go(k_fused_t<32>);
+    const uint32_t nrb = (c.FR + 31) / 32;
+    auto go_p = [&](auto tagP) {
+      constexpr int PP_ = decltype(tagP)::value;
+      if (nrb <= 1) go(k_fused_t<PP_, 1>);
+      else if (nrb <= 2) go(k_fused_t<PP_, 2>);
+      else if (nrb <= 4) go(k_fused_t<PP_, 4>);
+      else go(k_fused_t<PP_, 8>);
+    };
+    if (c.DP < 2) go_p(std::integral_constant<int, 1>{});
+    else if (c.DP <= 2) go_p(std::integral_constant<int, 2>{});
+    else if (c.DP <= 4) go_p(std::integral_constant<int, 4>{});
+    else if (c.DP <= 8) go_p(std::integral_constant<int, 8>{});
+    else if (c.DP <= 16) go_p(std::integral_constant<int, 16>{});
+    else go_p(std::integral_constant<int, 32>{});
     return 1;
   }
   const size_t sm = fused_smem_bytes(c.FT, c.FR, c.TP, c.DP, c.NCRM);
