@@ -905,58 +905,44 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
     }
   }
   __syncthreads();
-  // ---- (1) load every rank row of the tile (8 positions per lane), verify kind_op and comm against
-  // the template, transpose into sd, accumulate per-rank compute / in-block comm duration sums
+  // ---- (1) load every rank row of the tile: one warp per (row, 128 positions), lanes along positions
+  // (fully coalesced), verify kind_op / comm against the template, transpose into sd[p][row]
   {
-    const uint32_t n8 = (np + 7) / 8;
+    const uint32_t nq = (np + 127) / 128;
+    const FDiv fq = fdiv_make(nq);
     bool mis = false;
-    for (uint32_t u = wid; u < nrb * n8; u += FT_NW) {
-      const uint32_t c8 = u / nrb, rb = u - c8 * nrb;
-      const uint32_t row = rb * 32 + lane, q0 = c8 * 8;
-      const bool valid = row < R;
-      uint32_t kk[4] = {0, 0, 0, 0}, cm[8] = {0, 0, 0, 0, 0, 0, 0, 0}, du[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      if (valid) {
-        const uint64_t g = rbase + (uint64_t)row * npos + p0 + q0;
-        if (a.aligned && q0 + 8 <= np) {  // 4-event aligned rows: 8-byte kind loads, 16-byte comm / dur loads
-          const uint2 ka = __ldg(reinterpret_cast<const uint2*>(a.kind + g));
-          const uint2 kb = __ldg(reinterpret_cast<const uint2*>(a.kind + g + 4));
-          const uint4 c0 = __ldg(reinterpret_cast<const uint4*>(a.comm + g));
-          const uint4 c1 = __ldg(reinterpret_cast<const uint4*>(a.comm + g + 4));
-          const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(a.dur + g));
-          const uint4 d1 = __ldg(reinterpret_cast<const uint4*>(a.dur + g + 4));
-          kk[0] = ka.x; kk[1] = ka.y; kk[2] = kb.x; kk[3] = kb.y;
-          cm[0] = c0.x; cm[1] = c0.y; cm[2] = c0.z; cm[3] = c0.w; cm[4] = c1.x; cm[5] = c1.y; cm[6] = c1.z; cm[7] = c1.w;
-          du[0] = d0.x; du[1] = d0.y; du[2] = d0.z; du[3] = d0.w; du[4] = d1.x; du[5] = d1.y; du[6] = d1.z; du[7] = d1.w;
-        } else {
-          for (uint32_t i = 0; i < 8 && q0 + i < np; ++i) {
-            kk[i >> 1] |= (uint32_t)a.kind[g + i] << (16 * (i & 1));
-            cm[i] = a.comm[g + i];
-            du[i] = a.dur[g + i];
-          }
+    for (uint32_t u = wid; u < R * nq; u += FT_NW) {
+      const uint32_t row = fdiv(u, fq), q = u - row * nq;
+      const uint32_t pbase = q * 128 + lane * 4;
+      if (pbase >= np) continue;
+      const uint64_t g = rbase + (uint64_t)row * npos + p0 + pbase;
+      uint32_t kk0 = 0, kk1 = 0, cm[4] = {0, 0, 0, 0}, du[4] = {0, 0, 0, 0};
+      if (a.aligned && pbase + 4 <= np) {
+        const uint2 kv = __ldg(reinterpret_cast<const uint2*>(a.kind + g));
+        const uint4 cv = __ldg(reinterpret_cast<const uint4*>(a.comm + g));
+        const uint4 dv4 = __ldg(reinterpret_cast<const uint4*>(a.dur + g));
+        kk0 = kv.x; kk1 = kv.y;
+        cm[0] = cv.x; cm[1] = cv.y; cm[2] = cv.z; cm[3] = cv.w;
+        du[0] = dv4.x; du[1] = dv4.y; du[2] = dv4.z; du[3] = dv4.w;
+      } else {
+        for (uint32_t i = 0; i < 4 && pbase + i < np; ++i) {
+          if (i < 2) kk0 |= (uint32_t)a.kind[g + i] << (16 * i); else kk1 |= (uint32_t)a.kind[g + i] << (16 * (i - 2));
+          cm[i] = a.comm[g + i];
+          du[i] = a.dur[g + i];
         }
       }
-      const uint4 tk = *reinterpret_cast<const uint4*>(pk + q0);
-      const uint4 v0 = *reinterpret_cast<const uint4*>(vd + q0), v1 = *reinterpret_cast<const uint4*>(vd + q0 + 4);
-      const uint32_t dv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-      if (valid) {
-        mis |= (kk[0] != tk.x) | (kk[1] != tk.y) | (kk[2] != tk.z) | (kk[3] != tk.w);
-        const uint32_t r = sbase + row;
-        const uint32_t* rc = rcs + row * NCRM;
-        uint32_t sc_lo = 0, sc_hi = 0, si_lo = 0, si_hi = 0;
+      const uint2 tk = *reinterpret_cast<const uint2*>(pk + pbase);
+      const uint4 v4 = *reinterpret_cast<const uint4*>(vd + pbase);
+      const uint32_t dvd[4] = {v4.x, v4.y, v4.z, v4.w};
+      mis |= (kk0 != tk.x) | (kk1 != tk.y);
+      const uint32_t r = sbase + row;
+      const uint32_t* rc = rcs + row * NCRM;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint32_t t = dv[i] & 3u, x = dv[i] >> 2;
-          const uint32_t e1 = rc[t == 1 ? x : 0u];
-          mis |= (t != 0) & (cm[i] != (t == 1 ? e1 : r + x - 0x100000u));
-          if (q0 + i < np) {
-            sd[(q0 + i) * RP + row] = du[i];
-            const uint32_t pc = pcode[q0 + i];
-            if (pc == 0) { const uint32_t o = sc_lo; sc_lo += du[i]; sc_hi += sc_lo < o; }
-            else if (pc < 3) { const uint32_t o = si_lo; si_lo += du[i]; si_hi += si_lo < o; }
-          }
-        }
-        if (sc_lo | sc_hi) add64_lohi(&rsum[4 * row], &rsum[4 * row + 1], ((unsigned long long)sc_hi << 32) | sc_lo);
-        if (si_lo | si_hi) add64_lohi(&rsum[4 * row + 2], &rsum[4 * row + 3], ((unsigned long long)si_hi << 32) | si_lo);
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t t = dvd[i] & 3u, x = dvd[i] >> 2;
+        const uint32_t e1 = rc[t == 1 ? x : 0u];
+        mis |= (t != 0) & (cm[i] != (t == 1 ? e1 : r + x - 0x100000u));
+        if (pbase + i < np) sd[(pbase + i) * RP + row] = du[i];
       }
     }
     if (__any_sync(0xFFFFFFFFu, mis) && lane == 0) bad = 1;
@@ -1166,6 +1152,26 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
       if (cls < 2) a.wait_c[dst - a.inst_c] = v;
     }
   }
+  // per-rank sums from the tile (compute positions hold durations, in-block comm positions hold waits):
+  // warp = (row block, position slice), lane = row -> conflict-free column reads, register sums
+  {
+    constexpr uint32_t NSL = FT_NW / NRB;  // position slices per row block
+    const uint32_t rb = wid % NRB, sl = wid / NRB;
+    const uint32_t row = rb * 32 + lane;
+    const uint32_t plo = sl * ((np + NSL - 1) / NSL), phi = min(np, plo + (np + NSL - 1) / NSL);
+    unsigned long long sc = 0, sw = 0;
+    if (row < R)
+      for (uint32_t p = plo; p < phi; ++p) {
+        const uint32_t pc = pcode[p];
+        const uint32_t v = sd[p * RP + row];
+        if (pc == 0) sc += v; else if (pc < 3) sw += v;
+      }
+    if (row < R) {
+      if (sc) add64_lohi(&rsum[4 * row], &rsum[4 * row + 1], sc);
+      if (sw) add64_lohi(&rsum[4 * row + 2], &rsum[4 * row + 3], sw);
+    }
+  }
+  __syncthreads();
   // stage-1 counters per (window, rank)
   const uint32_t it_last = it0 + (np ? (pb[np - 1] & 1023u) : 0u);
   const bool one_window = !a.wi || (it0 / a.wi == it_last / a.wi);
@@ -1194,9 +1200,9 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
     const unsigned long long tr = ((unsigned long long)gsum[GO + gt] << 32 | gsum[gt]) * (TP > 1 ? 1ull : 0ull) +
                                   ((unsigned long long)gsum[GO + DP + gd] << 32 | gsum[DP + gd]) * (DP > 1 ? 1ull : 0ull);
     const unsigned long long comp = (unsigned long long)rsum[4 * row + 1] << 32 | rsum[4 * row];
-    const unsigned long long inb = (unsigned long long)rsum[4 * row + 3] << 32 | rsum[4 * row + 2];
+    const unsigned long long wsum = (unsigned long long)rsum[4 * row + 3] << 32 | rsum[4 * row + 2];
     if (comp) atomicAdd(&a.rk_sum[r], comp);
-    if (inb - tr) atomicAdd(&a.rk_sum[a.W + r], inb - tr);
+    if (wsum) atomicAdd(&a.rk_sum[a.W + r], wsum);
     if (tr) atomicAdd(&a.rk_sum[2 * a.W + r], tr);
     if (sjoin[row]) atomicAdd(&a.wl_joined[(uint64_t)w_tile * a.W + r], sjoin[row]);
     if (slate[row]) atomicAdd(&a.wl_late[(uint64_t)w_tile * a.W + r], slate[row]);
