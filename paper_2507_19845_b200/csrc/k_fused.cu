@@ -282,6 +282,9 @@ struct FusedArgs {
   uint32_t slow_num, slow_den; unsigned long long slow_margin;
   uint32_t wi, classes, mode; unsigned long long late_margin, wait_margin; int want_ref;
   Counters* cnt;
+  // byte offsets of the transposed kernel's shared-memory arrays (host-computed, fused_t_layout)
+  uint32_t o_rcb, o_coffr, o_sinst, o_sbits, o_sedge, o_rcs, o_rsum, o_gsum, o_sjoin, o_slate, o_rslow, o_pa, o_pb, o_vd,
+      o_pk, o_lst, o_cl, o_pcode;
 };
 
 constexpr int F_NT = 512;
@@ -824,29 +827,27 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
   const uint32_t SW = T / 32 + 2, E = TP + DP, NCRM = a.NCRM, RP = R + 1;
   constexpr uint32_t nrb = NRB;        // row blocks (lane l owns rows l + 32k, k < NRB); R <= 32*NRB
   const uint32_t tpsh = __ffs(TP) - 1;  // TP is a power of two here
-  // ---- shared memory carve-up (see fused_t_smem_bytes): byte offsets from smem_raw so every array
-  // stays in the shared address space (LDS/STS, no generic-pointer conversion)
-  uint32_t off = 0;
-  auto take = [&](uint32_t bytes, uint32_t align) { off = (off + align - 1) & ~(align - 1); const uint32_t o = off; off += bytes; return o; };
-  uint32_t* sd = reinterpret_cast<uint32_t*>(smem_raw + take(T * RP * 4, 16));               // T x (R+1), position-major
-  unsigned long long* rcb = reinterpret_cast<unsigned long long*>(smem_raw + take(R * NCRM * 8, 16));  // channel bases
-  unsigned long long* coffr = reinterpret_cast<unsigned long long*>(smem_raw + take(R * 8, 8));       // comm offsets
-  uint32_t* sinst = reinterpret_cast<uint32_t*>(smem_raw + take(T * G * 4, 4));              // T x G in-block inst ids
-  uint32_t* sbits = reinterpret_cast<uint32_t*>(smem_raw + take(R * SW * 4, 4));             // R x SW slow bits
-  uint32_t* sedge = reinterpret_cast<uint32_t*>(smem_raw + take(R * E * 4, 4));              // R x E edge weights (low)
-  uint32_t* rcs = reinterpret_cast<uint32_t*>(smem_raw + take(R * NCRM * 4, 4));             // R x NCRM role comms
-  uint32_t* rsum = reinterpret_cast<uint32_t*>(smem_raw + take(R * 16, 4));                  // R x 4 sums lo/hi
-  uint32_t* gsum = reinterpret_cast<uint32_t*>(smem_raw + take((DP + TP) * 8, 4));           // 2 x (DP+TP)
-  uint32_t* sjoin = reinterpret_cast<uint32_t*>(smem_raw + take(R * 4, 4));
-  uint32_t* slate = reinterpret_cast<uint32_t*>(smem_raw + take(R * 4, 4));
-  uint32_t* rslow = reinterpret_cast<uint32_t*>(smem_raw + take(R * 4, 4));
-  uint32_t* pa = reinterpret_cast<uint32_t*>(smem_raw + take(T * 4, 16));
-  uint32_t* pb = reinterpret_cast<uint32_t*>(smem_raw + take(T * 4, 16));
-  uint32_t* vd = reinterpret_cast<uint32_t*>(smem_raw + take(T * 4, 16));                   // verification descriptors
-  uint16_t* pk = reinterpret_cast<uint16_t*>(smem_raw + take(T * 2, 16));                   // template kind_op
-  uint16_t* lst = reinterpret_cast<uint16_t*>(smem_raw + take(T * 8, 4));                   // 4 x T position lists
-  uint16_t* cl = reinterpret_cast<uint16_t*>(smem_raw + take(T * 2, 4));                    // comm positions by m
-  uint8_t* pcode = reinterpret_cast<uint8_t*>(smem_raw + take(T, 4));                       // 0 comp 1 TP 2 DP 3 cross
+  // ---- shared memory carve-up: host-computed byte offsets from smem_raw (fused_t_layout), so every
+  // array stays in the shared address space and no per-use offset arithmetic is rematerialised
+  uint32_t* sd = reinterpret_cast<uint32_t*>(smem_raw);                              // T x (R+1), position-major
+  unsigned long long* rcb = reinterpret_cast<unsigned long long*>(smem_raw + a.o_rcb);
+  unsigned long long* coffr = reinterpret_cast<unsigned long long*>(smem_raw + a.o_coffr);
+  uint32_t* sinst = reinterpret_cast<uint32_t*>(smem_raw + a.o_sinst);
+  uint32_t* sbits = reinterpret_cast<uint32_t*>(smem_raw + a.o_sbits);
+  uint32_t* sedge = reinterpret_cast<uint32_t*>(smem_raw + a.o_sedge);
+  uint32_t* rcs = reinterpret_cast<uint32_t*>(smem_raw + a.o_rcs);
+  uint32_t* rsum = reinterpret_cast<uint32_t*>(smem_raw + a.o_rsum);
+  uint32_t* gsum = reinterpret_cast<uint32_t*>(smem_raw + a.o_gsum);
+  uint32_t* sjoin = reinterpret_cast<uint32_t*>(smem_raw + a.o_sjoin);
+  uint32_t* slate = reinterpret_cast<uint32_t*>(smem_raw + a.o_slate);
+  uint32_t* rslow = reinterpret_cast<uint32_t*>(smem_raw + a.o_rslow);
+  uint32_t* pa = reinterpret_cast<uint32_t*>(smem_raw + a.o_pa);
+  uint32_t* pb = reinterpret_cast<uint32_t*>(smem_raw + a.o_pb);
+  uint32_t* vd = reinterpret_cast<uint32_t*>(smem_raw + a.o_vd);
+  uint16_t* pk = reinterpret_cast<uint16_t*>(smem_raw + a.o_pk);
+  uint16_t* lst = reinterpret_cast<uint16_t*>(smem_raw + a.o_lst);
+  uint16_t* cl = reinterpret_cast<uint16_t*>(smem_raw + a.o_cl);
+  uint8_t* pcode = reinterpret_cast<uint8_t*>(smem_raw + a.o_pcode);
   __shared__ uint32_t kbase[ROLES];
   __shared__ uint32_t nlist[4];
   __shared__ int32_t dpos;
@@ -905,18 +906,29 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
     }
   }
   __syncthreads();
-  // ---- (1) load every rank row of the tile: one warp per (row, 128 positions), lanes along positions
-  // (fully coalesced), verify kind_op / comm against the template, transpose into sd[p][row]
+  // ---- (1) load every rank row of the tile: warps over rows, lanes along positions (fully coalesced),
+  // two rows in flight per warp; verify kind_op / comm against the template, transpose into sd[p][row]
   {
-    const uint32_t nq = (np + 127) / 128;
-    const FDiv fq = fdiv_make(nq);
     bool mis = false;
-    for (uint32_t u = wid; u < R * nq; u += FT_NW) {
-      const uint32_t row = fdiv(u, fq), q = u - row * nq;
-      const uint32_t pbase = q * 128 + lane * 4;
-      if (pbase >= np) continue;
+    const uint32_t* rcsb = rcs;
+    auto check_store = [&](uint32_t row, uint32_t pbase, uint32_t kk0, uint32_t kk1, const uint32_t (&cm)[4],
+                           const uint32_t (&du)[4]) {
+      const uint2 tk = *reinterpret_cast<const uint2*>(pk + pbase);
+      const uint4 v4 = *reinterpret_cast<const uint4*>(vd + pbase);
+      const uint32_t dvd[4] = {v4.x, v4.y, v4.z, v4.w};
+      mis |= (kk0 != tk.x) | (kk1 != tk.y);
+      const uint32_t r = sbase + row;
+      const uint32_t* rc = rcsb + row * NCRM;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t t = dvd[i] & 3u, x = dvd[i] >> 2;
+        const uint32_t e1 = rc[t == 1 ? x : 0u];
+        mis |= (t != 0) & (cm[i] != (t == 1 ? e1 : r + x - 0x100000u));
+        if (pbase + i < np) sd[(pbase + i) * RP + row] = du[i];
+      }
+    };
+    auto load4 = [&](uint32_t row, uint32_t pbase, uint32_t& kk0, uint32_t& kk1, uint32_t (&cm)[4], uint32_t (&du)[4]) {
       const uint64_t g = rbase + (uint64_t)row * npos + p0 + pbase;
-      uint32_t kk0 = 0, kk1 = 0, cm[4] = {0, 0, 0, 0}, du[4] = {0, 0, 0, 0};
       if (a.aligned && pbase + 4 <= np) {
         const uint2 kv = __ldg(reinterpret_cast<const uint2*>(a.kind + g));
         const uint4 cv = __ldg(reinterpret_cast<const uint4*>(a.comm + g));
@@ -925,24 +937,27 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
         cm[0] = cv.x; cm[1] = cv.y; cm[2] = cv.z; cm[3] = cv.w;
         du[0] = dv4.x; du[1] = dv4.y; du[2] = dv4.z; du[3] = dv4.w;
       } else {
+        kk0 = kk1 = 0;
+        for (int i = 0; i < 4; ++i) { cm[i] = 0; du[i] = 0; }
         for (uint32_t i = 0; i < 4 && pbase + i < np; ++i) {
           if (i < 2) kk0 |= (uint32_t)a.kind[g + i] << (16 * i); else kk1 |= (uint32_t)a.kind[g + i] << (16 * (i - 2));
           cm[i] = a.comm[g + i];
           du[i] = a.dur[g + i];
         }
       }
-      const uint2 tk = *reinterpret_cast<const uint2*>(pk + pbase);
-      const uint4 v4 = *reinterpret_cast<const uint4*>(vd + pbase);
-      const uint32_t dvd[4] = {v4.x, v4.y, v4.z, v4.w};
-      mis |= (kk0 != tk.x) | (kk1 != tk.y);
-      const uint32_t r = sbase + row;
-      const uint32_t* rc = rcs + row * NCRM;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t t = dvd[i] & 3u, x = dvd[i] >> 2;
-        const uint32_t e1 = rc[t == 1 ? x : 0u];
-        mis |= (t != 0) & (cm[i] != (t == 1 ? e1 : r + x - 0x100000u));
-        if (pbase + i < np) sd[(pbase + i) * RP + row] = du[i];
+    };
+    for (uint32_t pq = 0; pq < np; pq += 128) {
+      const uint32_t pbase = pq + lane * 4;
+      const bool pin = pbase < np;
+      uint32_t row = wid;
+      for (; row + FT_NW < R; row += 2 * FT_NW) {  // two rows per iteration
+        uint32_t ka0, ka1, kb0, kb1, cma[4], cmb[4], dua[4], dub[4];
+        if (pin) { load4(row, pbase, ka0, ka1, cma, dua); load4(row + FT_NW, pbase, kb0, kb1, cmb, dub); }
+        if (pin) { check_store(row, pbase, ka0, ka1, cma, dua); check_store(row + FT_NW, pbase, kb0, kb1, cmb, dub); }
+      }
+      for (; row < R; row += FT_NW) {
+        uint32_t ka0, ka1, cma[4], dua[4];
+        if (pin) { load4(row, pbase, ka0, ka1, cma, dua); check_store(row, pbase, ka0, ka1, cma, dua); }
       }
     }
     if (__any_sync(0xFFFFFFFFu, mis) && lane == 0) bad = 1;
@@ -991,9 +1006,11 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
   __syncthreads();
   // ---- (3) phase B: one warp per comm position
   const uint32_t ncm = nlist[1] + nlist[2] + nlist[3];
-  for (uint32_t jj = wid; jj < ncm; jj += FT_NW) {
+  for (uint32_t un = wid; un < ncm * NRB; un += FT_NW) {  // unit = (comm position, row block)
+    const uint32_t jj = un / NRB, kb = un - jj * NRB;
     const uint32_t cv = cl[jj];
     const uint32_t p = cv & 0x3FFFu, cls = cv >> 14;  // 0 TP, 1 DP, 2 cross
+    if (cls == 1 && kb != 0) continue;  // a DP group spans every row block: one unit handles it
     const uint32_t A = pa[p], B = pb[p];
     const uint32_t role = (B >> 20) & 31u;
     const uint32_t krel = (B >> 10) & 1023u;
@@ -1001,10 +1018,9 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
     uint32_t* col = sd + p * RP;
     if (cls == 2) {
       const uint32_t kk = kbase[role] + krel;
-#pragma unroll
-      for (uint32_t k = 0; k < nrb; ++k) {
-        const uint32_t row = lane + 32 * k;
-        if (row >= R) break;
+      {
+        const uint32_t row = lane + 32 * kb;
+        if (row >= R) continue;
         const uint32_t r = sbase + row;
         uint64_t ch; uint32_t nm, slot;
         bool send = false;
@@ -1089,8 +1105,8 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
     };
     if (istp) {
       const uint32_t gm = TP >= 32 ? 0xFFFFFFFFu : (((1u << TP) - 1u) << (lane & ~(TP - 1u)));
-#pragma unroll
-      for (uint32_t k = 0; k < nrb; ++k) {
+      {
+        const uint32_t k = kb;
         const uint32_t row = lane + 32u * k;
         const bool valid = row < R;
         const uint32_t d = valid ? col[row] : 0xFFFFFFFFu;
@@ -1138,10 +1154,8 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
   }
   __syncthreads();
   // ---- (4) flush: coalesced per-rank inst / wait rows
-  {
-    const FDiv fm = fdiv_make(ncm > 0 ? ncm : 1u);
-    for (uint32_t i = tid; i < R * ncm; i += FT_NT) {
-      const uint32_t row = fdiv(i, fm), j = i - row * ncm;
+  for (uint32_t row = wid; row < R; row += FT_NW) {
+    for (uint32_t j = lane; j < ncm; j += 32) {
       const uint32_t cv = cl[j];
       const uint32_t p = cv & 0x3FFFu, cls = cv >> 14;
       const uint32_t v = sd[p * RP + row];
@@ -1232,16 +1246,27 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
   }
 }
 
-size_t fused_t_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM) {
+static size_t fused_t_layout(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM, FusedArgs* a) {
   const uint32_t SW = T / 32 + 2, G = TP > DP ? TP : DP, E = TP + DP, RP = R + 1;
   size_t off = 0;
-  auto take = [&](size_t bytes, size_t align) { off = (off + align - 1) & ~(align - 1); off += bytes; };
-  take((size_t)T * RP * 4, 16); take((size_t)R * NCRM * 8, 16); take((size_t)R * 8, 8); take((size_t)T * G * 4, 4);
-  take((size_t)R * SW * 4, 4); take((size_t)R * E * 4, 4); take((size_t)R * NCRM * 4, 4); take((size_t)R * 16, 4);
-  take((size_t)(DP + TP) * 8, 4); take((size_t)R * 4, 4); take((size_t)R * 4, 4); take((size_t)R * 4, 4);
-  take((size_t)T * 4, 16); take((size_t)T * 4, 16); take((size_t)T * 4, 16); take((size_t)T * 2, 16);
-  take((size_t)T * 8, 4); take((size_t)T * 2, 4); take((size_t)T, 4);
+  auto take = [&](size_t bytes, size_t align) { off = (off + align - 1) & ~(align - 1); const size_t o = off; off += bytes; return (uint32_t)o; };
+  take((size_t)T * RP * 4, 16);
+  const uint32_t o_rcb = take((size_t)R * NCRM * 8, 16), o_coffr = take((size_t)R * 8, 8), o_sinst = take((size_t)T * G * 4, 4);
+  const uint32_t o_sbits = take((size_t)R * SW * 4, 4), o_sedge = take((size_t)R * E * 4, 4), o_rcs = take((size_t)R * NCRM * 4, 4);
+  const uint32_t o_rsum = take((size_t)R * 16, 4), o_gsum = take((size_t)(DP + TP) * 8, 4), o_sjoin = take((size_t)R * 4, 4);
+  const uint32_t o_slate = take((size_t)R * 4, 4), o_rslow = take((size_t)R * 4, 4), o_pa = take((size_t)T * 4, 16);
+  const uint32_t o_pb = take((size_t)T * 4, 16), o_vd = take((size_t)T * 4, 16), o_pk = take((size_t)T * 2, 16);
+  const uint32_t o_lst = take((size_t)T * 8, 4), o_cl = take((size_t)T * 2, 4), o_pcode = take((size_t)T, 4);
+  if (a) {
+    a->o_rcb = o_rcb; a->o_coffr = o_coffr; a->o_sinst = o_sinst; a->o_sbits = o_sbits; a->o_sedge = o_sedge; a->o_rcs = o_rcs;
+    a->o_rsum = o_rsum; a->o_gsum = o_gsum; a->o_sjoin = o_sjoin; a->o_slate = o_slate; a->o_rslow = o_rslow; a->o_pa = o_pa;
+    a->o_pb = o_pb; a->o_vd = o_vd; a->o_pk = o_pk; a->o_lst = o_lst; a->o_cl = o_cl; a->o_pcode = o_pcode;
+  }
   return (off + 15) & ~size_t(15);
+}
+
+size_t fused_t_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM) {
+  return fused_t_layout(T, R, TP, DP, NCRM, nullptr);
 }
 
 size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM) {
@@ -1284,7 +1309,7 @@ int launch_fused(Ctx& c) {
   a.late_margin = c.lcfg.late_margin_ns; a.wait_margin = c.lcfg.wait_margin_ns; a.want_ref = c.dcfg.want_ref ? 1 : 0;
   a.cnt = c.counters.as<Counters>();
   if (c.fused_t) {
-    const size_t sm = fused_t_smem_bytes(c.FT, c.FR, c.TP, c.DP, c.NCRM);
+    const size_t sm = fused_t_layout(c.FT, c.FR, c.TP, c.DP, c.NCRM, &a);
     auto go = [&](auto kern) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       kern<<<c.n_ftiles, FT_NT, sm, c.stream>>>(a);
