@@ -158,6 +158,34 @@ scan_status scan_create(scan_ctx** out, int cuda_device, void* cuda_stream);
 void        scan_destroy(scan_ctx* ctx);
 const char* scan_last_error(const scan_ctx* ctx);   /* owned by ctx; "" if none               */
 
+/* ---- multi-GPU: iteration-window shards ----------------------------
+   One process per GPU. Shard g of n_shards loads, with scan_load_events(), the events of EVERY
+   rank for a contiguous block of whole iterations; shards are ordered by iteration (shard g's
+   block follows shard g-1's). Iterations are the natural unit: no instance straddles an
+   iteration (the tracer records per-iteration step events; reading R23).
+   scan_analyze() on a sharded context is a COLLECTIVE call (every shard must call it, same
+   configs) that returns the job-wide analysis:
+     * per-event outputs (EV_*, COMM_*, SLOW_BITS) cover this shard's events, in its own order;
+     * instance ids are the job-wide ids of the unsharded run; this shard's instances are the
+       ranges given by CH_SHARD_K0 / CH_SHARD_N; IN_* rows outside them are unspecified;
+     * channel, per-rank, per-window, per-link, verdict, walk and edge outputs and all result
+       structs are job-wide and identical on every shard (and to the unsharded run).
+   Exchange: two small ncclAllGather (per-channel counts, P2P channel bitmap) for the global
+   numbering, one grouped ncclSend/ncclRecv all-to-all that ships each P2P instance record
+   (24 B) to the shard owning its link (link pid % n_shards), one grouped ncclAllReduce of the
+   per-rank / per-window / per-link partial results.
+   Preconditions (else SCAN_E_UNSUPPORTED on every shard): the trace is SPMD (fused path), and
+   every shard but the last ends on an iteration boundary of every rank with all members of
+   every communicator / P2P pair / DP class in step. Only scan_analyze is available.
+   scan_nccl_unique_id: ncclGetUniqueId into out[128]; the caller broadcasts it (e.g. over a
+   torch.distributed group) and every shard passes it to scan_create_sharded, which creates
+   the context's own NCCL communicator (destroyed by scan_destroy).
+   Errors: SCAN_E_INVALID_ARG (n_shards < 1, shard out of range, null id), SCAN_E_NCCL (NCCL
+   failure; message in scan_last_error), SCAN_E_CUDA.                                                  */
+scan_status scan_nccl_unique_id(uint8_t out[128]);
+scan_status scan_create_sharded(scan_ctx** out, int cuda_device, void* cuda_stream, int n_shards, int shard,
+                                const uint8_t nccl_unique_id[128]);
+
 /* A0 ingest: validate sizes, place the columns on the device, build the comm tables.
    Per-event schema validation happens in scan_match_collectives (one pass).
    Errors: SCAN_E_INVALID_ARG (sizes, alignment, rank_order), SCAN_E_UNSUPPORTED
@@ -233,6 +261,11 @@ typedef enum scan_output {
     SCAN_OUT_COMM_INST,        /* u32 per comm event, ranks concatenated, program order       */
     SCAN_OUT_COMM_WAIT,        /* u32 per comm event                                          */
     SCAN_OUT_SLOW_BITS,        /* u32 words, per rank ceil(n_compute/32) words, bit j = slow  */
+    /* shard view (per channel): this context's instances of channel c are the occurrences
+       [CH_SHARD_K0[c], CH_SHARD_K0[c] + CH_SHARD_N[c]), i.e. instance ids CH_BASE[c] + k.
+       Unsharded: K0 = 0, N = CH_NMAX.                                                          */
+    SCAN_OUT_CH_SHARD_K0,      /* u64 */
+    SCAN_OUT_CH_SHARD_N,       /* u32 */
     SCAN_OUT__COUNT
 } scan_output;
 

@@ -43,7 +43,9 @@ OUTPUTS = [
     ("lb_depth", np.uint32), ("lb_total_wait", np.uint64),
     ("eg_window", np.uint32), ("eg_src", np.uint32), ("eg_dst", np.uint32), ("eg_weight", np.uint64),
     ("comm_inst", np.uint32), ("comm_wait", np.uint32), ("slow_bits", np.uint32),
+    ("ch_shard_k0", np.uint64), ("ch_shard_n", np.uint32),
 ]
+NATIVE_ONLY = ("comm_inst", "comm_wait", "slow_bits", "ch_shard_k0", "ch_shard_n")  # no oracle counterpart
 OUT_INDEX = {n: i for i, (n, _) in enumerate(OUTPUTS)}
 OUT_DTYPE = dict(OUTPUTS)
 
@@ -138,8 +140,11 @@ def _load_lib():
     lib.scan_used_fused.restype = ctypes.c_int
     lib.scan_force_general.argtypes = [P, ctypes.c_int]
     lib.scan_fused_variant.argtypes = [P, ctypes.c_int]
+    lib.scan_nccl_unique_id.argtypes = [P]
+    lib.scan_create_sharded.argtypes = [ctypes.POINTER(P), ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P]
     for f in ("scan_create", "scan_load_events", "scan_match_collectives", "scan_detect", "scan_localize",
-              "scan_output_size", "scan_export", "scan_analyze", "scan_force_general", "scan_fused_variant"):
+              "scan_output_size", "scan_export", "scan_analyze", "scan_force_general", "scan_fused_variant",
+              "scan_nccl_unique_id", "scan_create_sharded"):
         getattr(lib, f).restype = ctypes.c_int32
     _lib = lib
     return lib
@@ -148,7 +153,8 @@ def _load_lib():
 EXPORTED_SYMBOLS = ["scan_create", "scan_destroy", "scan_last_error", "scan_load_events", "scan_match_collectives",
                     "scan_detect", "scan_localize", "scan_output_size", "scan_export", "scan_output_device_ptr",
                     "scan_kernel_launches", "scan_set_timing", "scan_timing_reset", "scan_kernel_timing",
-                    "scan_analyze", "scan_used_fused", "scan_force_general", "scan_fused_variant"]
+                    "scan_analyze", "scan_used_fused", "scan_force_general", "scan_fused_variant",
+                    "scan_nccl_unique_id", "scan_create_sharded"]
 
 
 @dataclass
@@ -200,6 +206,29 @@ def scan_create(device: int = 0, stream: int | None = None):
     st = lib.scan_create(ctypes.byref(h), device, stream)
     if st < 0:
         raise ScanError(st, "scan_create failed (no CUDA device?)")
+    return h
+
+
+def scan_nccl_unique_id() -> bytes:
+    lib = _load_lib()
+    buf = (ctypes.c_uint8 * 128)()
+    st = lib.scan_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p))
+    if st < 0:
+        raise ScanError(st, "ncclGetUniqueId failed")
+    return bytes(buf)
+
+
+def scan_create_sharded(device: int, stream, n_shards: int, shard: int, unique_id: bytes | None):
+    lib = _load_lib()
+    h = ctypes.c_void_p()
+    idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(unique_id) if unique_id is not None else None
+    st = lib.scan_create_sharded(ctypes.byref(h), device, stream, n_shards, shard,
+                                 ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None)
+    if st < 0:
+        msg = lib.scan_last_error(h).decode() if h else "scan_create_sharded failed"
+        if h:
+            lib.scan_destroy(h)
+        raise ScanError(st, msg)
     return h
 
 
@@ -285,7 +314,9 @@ class Scan:
     """One analysis context on one GPU. ``load`` accepts a trace with numpy host columns
     (copied H2D by the library) or torch CUDA tensors (``device_ptrs=True``, zero-copy)."""
 
-    def __init__(self, device: int = 0, stream=None):
+    def __init__(self, device: int = 0, stream=None, shards: tuple | None = None):
+        """``shards=(n_shards, shard, nccl_unique_id)``: one iteration-window shard of a multi-GPU
+        analysis (scan.h "multi-GPU"); ``analyze`` is then a collective call over the shards."""
         if stream is None:
             try:
                 import torch
@@ -293,7 +324,10 @@ class Scan:
                     stream = torch.cuda.current_stream(device).cuda_stream
             except Exception:
                 stream = None
-        self.ctx = scan_create(device, stream)
+        if shards is not None and shards[0] > 1:
+            self.ctx = scan_create_sharded(device, stream, int(shards[0]), int(shards[1]), shards[2])
+        else:
+            self.ctx = scan_create(device, stream)
         self._keep: list = []
 
     def close(self):
@@ -347,7 +381,7 @@ class Scan:
         return scan_export(self.ctx, name)
 
     def export_all(self, names=None) -> dict:
-        names = names or [n for n, _ in OUTPUTS if n not in ("comm_inst", "comm_wait", "slow_bits")]
+        names = names or [n for n, _ in OUTPUTS if n not in NATIVE_ONLY]
         return {n: self.export(n) for n in names}
 
     def device_ptr(self, name: str) -> int:
@@ -371,3 +405,43 @@ class Scan:
             lib.scan_kernel_timing(self.ctx, i, ctypes.byref(nm), ctypes.byref(ms_), ctypes.byref(cnt))
             out[nm.value.decode()] = (ms_.value, cnt.value)
         return out
+
+
+# ---- multi-GPU plumbing (host side) -------------------------------------------------------------
+def shard_iterations(n_iters: int, n_shards: int, shard: int) -> tuple[int, int]:
+    """Iteration block [b, e) of ``shard``: contiguous, ordered, sizes differ by at most one."""
+    q, r = divmod(n_iters, n_shards)
+    b = shard * q + min(shard, r)
+    return b, b + q + (1 if shard < r else 0)
+
+
+def slice_iterations(trace, b: int, e: int):
+    """The events of iterations [b, e) of every rank of a host trace (iteration = events up to and
+    including an iter_end-flagged event), as a trace with the same topology and comm table."""
+    from dataclasses import replace
+    W = trace.world
+    ro = np.asarray(trace.rank_offsets, dtype=np.uint64)
+    ends = (np.asarray(trace.kind_op) & 8) != 0
+    lo = np.zeros(W, np.uint64)
+    hi = np.zeros(W, np.uint64)
+    for r in range(W):
+        a0, a1 = int(ro[r]), int(ro[r + 1])
+        cut = np.flatnonzero(ends[a0:a1]) + 1  # event index after each iteration end
+        starts = np.concatenate([[0], cut])
+        lo[r] = a0 + (starts[b] if b < len(starts) else a1 - a0)
+        hi[r] = a0 + (starts[e] if e < len(starts) else a1 - a0)
+    idx = np.concatenate([np.arange(int(lo[r]), int(hi[r]), dtype=np.int64) for r in range(W)]) if W else np.zeros(0, np.int64)
+    nro = np.zeros(W + 1, np.uint64)
+    nro[1:] = np.cumsum(hi - lo)
+    cols = {k: np.ascontiguousarray(getattr(trace, k)[idx]) for k in ("dur_ns", "kind_op", "meta", "comm", "payload")}
+    st = getattr(trace, "start_ns", None)
+    return replace(trace, rank_offsets=nro, start_ns=(np.ascontiguousarray(st[idx]) if st is not None else None),
+                   gt_inst=None, gt_true_start=None, **cols)
+
+
+def shard_unique_id(group=None) -> bytes:
+    """NCCL unique id made on rank 0 of a torch.distributed group and broadcast to its ranks."""
+    import torch.distributed as dist
+    obj = [scan_nccl_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return obj[0]

@@ -2,6 +2,7 @@
 from __future__ import annotations
 
 import glob
+import importlib.util
 import os
 import subprocess
 import sys
@@ -13,12 +14,27 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr"]
 
 
+def nccl_paths() -> tuple[str, str]:
+    """(include dir, lib dir) of the NCCL torch ships (same libnccl.so.2 the process loads)."""
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec and spec.submodule_search_locations:
+        root = list(spec.submodule_search_locations)[0]
+        inc, lib = os.path.join(root, "include"), os.path.join(root, "lib")
+        if os.path.exists(os.path.join(inc, "nccl.h")) and os.path.exists(os.path.join(lib, "libnccl.so.2")):
+            return inc, lib
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
+
+
 def sources():
     return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
 
 
 def deps():
     return sources() + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(HERE, "..", "include", "megascan", "scan.h")]
+
+
+def headers():
+    return glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(HERE, "..", "include", "megascan", "scan.h")]
 
 
 def stale() -> bool:
@@ -28,6 +44,13 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
+def obj_stale(src: str, obj: str) -> bool:
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    return any(os.path.getmtime(p) > t for p in [src, *headers()])
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return SO
@@ -35,13 +58,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
+    inc, lib = nccl_paths()
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        objs.append(obj)
+        if not force and not obj_stale(src, obj):
+            continue
+        cmd = [NVCC, *ARCH, *FLAGS, "-I", inc, "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT), src))
-        objs.append(obj)
     for p, src in procs:
         out = p.communicate()[0].decode()
         if p.returncode != 0:
@@ -49,7 +75,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose and out:
             sys.stderr.write(out)
     tmp = SO + ".tmp"
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"])
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", f"-L{lib}", "-l:libnccl.so.2",
+                           f"-Xlinker=-rpath={lib}"])
     os.replace(tmp, SO)
     return SO
 

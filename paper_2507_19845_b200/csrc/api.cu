@@ -18,20 +18,8 @@ void ms::resolve_timing(Ctx& c) {
   c.pend.clear();
 }
 
-struct scan_ctx { Ctx c; };
 
-namespace {
-
-#define CK(x)                                                                          \
-  do {                                                                                 \
-    cudaError_t _e = (x);                                                              \
-    if (_e != cudaSuccess) {                                                           \
-      c.err = std::string("CUDA error: ") + cudaGetErrorString(_e) + " at " #x;        \
-      return _e == cudaErrorMemoryAllocation ? SCAN_E_OOM : SCAN_E_CUDA;               \
-    }                                                                                  \
-  } while (0)
-
-scan_status sync_read(Ctx& c) {
+scan_status ms::sync_read(Ctx& c) {
   CK(cudaMemcpyAsync(&c.hc, c.counters.p, sizeof(Counters), cudaMemcpyDeviceToHost, c.stream));
   CK(cudaStreamSynchronize(c.stream));
   CK(cudaGetLastError());
@@ -39,18 +27,13 @@ scan_status sync_read(Ctx& c) {
   return SCAN_OK;
 }
 
+namespace {
+
 __global__ void k_citer_fill(int W, uint32_t NIT1, const uint32_t* r_ncomp, uint32_t* citer) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (uint64_t)W * NIT1) return;
   const uint32_t r = (uint32_t)(i / NIT1), q = (uint32_t)(i % NIT1);
   citer[i] = q == 0 ? 0u : r_ncomp[r];
-}
-
-template <class T>
-scan_status upload(Ctx& c, DevBuf& b, const std::vector<T>& v) {
-  CK(b.ensure(v.size() * sizeof(T)));
-  if (!v.empty()) CK(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, c.stream));
-  return SCAN_OK;
 }
 
 }  // namespace
@@ -86,7 +69,8 @@ static void release_all(Ctx& c) {
                     &c.lb_label, &c.lb_rkind, &c.lb_rrank, &c.lb_rsrc, &c.lb_depth, &c.lb_twait, &c.scratch,
                     &c.st_tile0, &c.st_npos, &c.role_comm, &c.role_slot, &c.role_type, &c.ncroles, &c.ft_cols,
                     &c.ft_base, &c.ft_last, &c.st_tot, &c.sci, &c.sit, &c.dlate, &c.dinfo, &c.ft_posA, &c.ft_posB,
-                    &c.ft_posK, &c.eidx, &c.tile_stage, &c.xbase, &c.lk_scratch};
+                    &c.ft_posK, &c.eidx, &c.tile_stage, &c.xbase, &c.lk_scratch, &c.g_base, &c.g_slot,
+                    &c.g_nmax, &c.g_nmin, &c.g_k0, &c.x_send, &c.x_recv, &c.headtail, &c.lk_sendmap, &c.lk_recvmap};
   for (DevBuf* b : bufs) b->release();
 }
 
@@ -96,6 +80,7 @@ void scan_destroy(scan_ctx* ctx) {
   if (ctx->c.stream) cudaStreamSynchronize(ctx->c.stream);
   for (auto& p : ctx->c.pend) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   for (auto e : ctx->c.evpool) cudaEventDestroy(e);
+  shard_release(ctx->c);
   release_all(ctx->c);
   delete ctx;
 }
@@ -217,6 +202,7 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
   }
   rt0[W] = (uint32_t)trank.size();
   c.TP = topo->tp; c.PP = topo->pp; c.DP = topo->dp; c.W = W; c.n_comms = nc; c.N = N; c.flags = flags;
+  c.h_ccls = ccls; c.h_coff = coff;
   c.h_rank_off = ro; c.h_rank_tile0 = rt0; c.n_tiles = trank.size(); c.nnz_c = nb.size();
   scan_status st;
   if ((st = upload(c, c.rank_off, ro)) || (st = upload(c, c.coff, coff)) || (st = upload(c, c.cmem, cmem)) ||
@@ -331,8 +317,10 @@ namespace {
 const scan_detect_config kDefDetect{3, 2, 50000, 3, 10, 10, 0, 0, 0};
 const scan_localize_config kDefLocalize{100000, 7, 10, 7, 10, 10, 3, 0, 0, 100000};
 
+}  // namespace
+
 // per-rank / channel workspaces and counter reset (both paths)
-scan_status prep_ws(Ctx& c, bool tiles) {
+scan_status ms::prep_ws(Ctx& c, bool tiles) {
   const uint64_t T = std::max<uint64_t>(c.n_tiles, 1), W = c.W;
   if (tiles) {
     CK(c.t_nkeys.ensure(T * 4)); CK(c.t_keys.ensure(T * KCAP * 4)); CK(c.t_cnt.ensure(T * KCAP * 4));
@@ -349,12 +337,15 @@ scan_status prep_ws(Ctx& c, bool tiles) {
   CK(c.nbp.ensure(W * PCAP * 4)); CK(c.nbp_n.ensure(W * 4));
   Counters z{};
   z.bad_event = ~0ull;
+  z.min_niter = ~0u;
   CK(cudaMemcpyAsync(c.counters.p, &z, sizeof(Counters), cudaMemcpyHostToDevice, c.stream));
   CK(cudaMemsetAsync(c.ch_nmax.p, 0, ch_cap * 4, c.stream));
   CK(cudaMemsetAsync(c.ch_nmin.p, 0xFF, ch_cap * 4, c.stream));
   CK(cudaMemsetAsync(c.bitmap.p, 0, c.n_bm_words * 4, c.stream));
   return SCAN_OK;
 }
+
+namespace {
 
 // after the per-rank census (general: k_rank_scan, fused: k_fused_census) + k_rank_prefix:
 // read totals, build channel bases, allocate the per-event / per-instance buffers.
@@ -388,6 +379,14 @@ scan_status channels_and_buffers(Ctx& c, bool fused) {
   if (c.hc.n_instances >= 0xFFFFFFFFull) { c.err = "more than 2^32-1 instances"; return SCAN_E_UNSUPPORTED; }
   c.n_inst = c.hc.n_instances; c.n_slots = c.hc.n_slots; c.p2p_slot0 = c.hc.p2p_slot0; c.p2p_inst0 = c.hc.p2p_inst0;
   c.n_xinst = c.hc.n_xinst;
+  return alloc_match_buffers(c, fused);
+}
+
+}  // namespace
+
+// per-event / per-slot / per-instance buffers once the channel tables are final
+scan_status ms::alloc_match_buffers(Ctx& c, bool fused) {
+  const uint64_t W = c.W;
   CK(c.inst_c.ensure(c.n_comm * 4)); CK(c.wait_c.ensure(c.n_comm * 4));
   if (!fused) { CK(c.cdur.ensure(c.n_comp * 4)); CK(c.cop.ensure(c.n_comp * 2)); }
   CK(c.sdur.ensure(c.n_slots * 4)); CK(c.skind.ensure(c.n_slots));
@@ -404,7 +403,7 @@ scan_status channels_and_buffers(Ctx& c, bool fused) {
   return SCAN_OK;
 }
 
-scan_status alloc_detect(Ctx& c) {
+scan_status ms::alloc_detect(Ctx& c) {
   const scan_detect_config& d = c.dcfg;
   c.NW = d.window_iters ? std::max<uint32_t>(1, (c.n_iters + d.window_iters - 1) / d.window_iters) : 1;
   const uint64_t ncl = (uint64_t)c.TP * c.PP, items = (uint64_t)c.NW * c.W;
@@ -416,7 +415,7 @@ scan_status alloc_detect(Ctx& c) {
   return SCAN_OK;
 }
 
-scan_status alloc_localize(Ctx& c) {
+scan_status ms::alloc_localize(Ctx& c) {
   const uint64_t items = (uint64_t)c.NW * c.W, nlk = (uint64_t)c.NW * c.n_p2p;
   const uint64_t nnz_tot = c.nnz_c + (uint64_t)c.W * PCAP;
   CK(c.wl_joined.ensure(items * 4)); CK(c.wl_late.ensure(items * 4)); CK(c.wl_frac.ensure(items * 8));
@@ -438,9 +437,13 @@ scan_status alloc_localize(Ctx& c) {
   return SCAN_OK;
 }
 
+namespace {
+
 void fill_match(Ctx& c, scan_match_result* out) {
   if (!out) return;
-  out->n_events = c.N; out->n_comm_events = c.n_comm; out->n_compute_events = c.n_comp;
+  const bool sh = c.n_shards > 1;  // sharded: job-wide totals
+  out->n_events = sh ? c.g_N : c.N; out->n_comm_events = sh ? c.g_ncomm : c.n_comm;
+  out->n_compute_events = sh ? c.g_ncomp : c.n_comp;
   out->n_channels = c.NCH; out->n_p2p_channels = c.n_p2p; out->n_instances = c.n_inst;
   out->n_incomplete = c.hc.n_incomplete; out->n_kind_mismatch = c.hc.n_kind_mismatch;
   out->n_payload_mismatch = c.hc.n_payload_mismatch; out->n_iters = c.n_iters;
@@ -586,6 +589,7 @@ scan_status scan_match_collectives(scan_ctx* ctx, scan_match_result* out) {
   if (!ctx) return SCAN_E_INVALID_ARG;
   Ctx& c = ctx->c;
   if (!c.loaded) { c.err = "scan_match_collectives before scan_load_events"; return SCAN_E_ORDER; }
+  if (c.n_shards > 1) { c.err = "a sharded context runs scan_analyze only"; return SCAN_E_UNSUPPORTED; }
   CK(cudaSetDevice(c.device));
   c.launches = 0;
   scan_status st = general_match(c);
@@ -637,6 +641,13 @@ scan_status scan_analyze(scan_ctx* ctx, const scan_detect_config* dcfg, const sc
   c.dcfg = d; c.lcfg = L;
   c.launches = 0;
   scan_status st = 2;
+  if (c.n_shards > 1) {  // iteration-window shard of a multi-GPU job (shard.cu): collective call
+    if ((st = sharded_all(c))) return st;
+    fill_match(c, mres);
+    if ((st = detect_tail(c, dres))) return st;
+    fill_localize(c, lres);
+    return match_status(c);
+  }
   if (c.spmd && !c.force_general) {
     st = fused_all(c);
     if (st < 0) return st;
@@ -679,6 +690,7 @@ scan_status host_table(Ctx& c, scan_output which, std::vector<uint8_t>& out) {
     return cudaMemcpy(dst, (const uint8_t*)b.p + off, bytes, cudaMemcpyDeviceToHost);
   };
   const uint64_t NCH = c.NCH, np = c.n_p2p, nc = c.n_comms;
+  const bool sh = c.n_shards > 1;
   std::vector<uint32_t> psrc(np), pdst(np);
   CK(d2h(c.ch_nsend, np * 4, np * 4, psrc.data()));
   CK(d2h(c.ch_nrecv, np * 4, np * 4, pdst.data()));
@@ -697,9 +709,20 @@ scan_status host_table(Ctx& c, scan_output which, std::vector<uint8_t>& out) {
       for (uint64_t i = 0; i < NCH; ++i) v[i] = i < nc ? (uint32_t)(co[i + 1] - co[i]) : 2;
       put(v); return SCAN_OK;
     }
-    case SCAN_OUT_CH_NMAX: { std::vector<uint32_t> v(NCH); CK(d2h(c.ch_nmax, 0, NCH * 4, v.data())); put(v); return SCAN_OK; }
-    case SCAN_OUT_CH_NMIN: { std::vector<uint32_t> v(NCH); CK(d2h(c.ch_nmin, 0, NCH * 4, v.data())); put(v); return SCAN_OK; }
-    case SCAN_OUT_CH_BASE: { std::vector<uint64_t> v(NCH); CK(d2h(c.ch_base, 0, NCH * 8, v.data())); put(v); return SCAN_OK; }
+    // sharded contexts: the job-wide tables (the kernels' ch_* are this shard's shifted / local ones)
+    case SCAN_OUT_CH_NMAX: { std::vector<uint32_t> v(NCH); CK(d2h(sh ? c.g_nmax : c.ch_nmax, 0, NCH * 4, v.data())); put(v); return SCAN_OK; }
+    case SCAN_OUT_CH_NMIN: { std::vector<uint32_t> v(NCH); CK(d2h(sh ? c.g_nmin : c.ch_nmin, 0, NCH * 4, v.data())); put(v); return SCAN_OK; }
+    case SCAN_OUT_CH_BASE: { std::vector<uint64_t> v(NCH); CK(d2h(sh ? c.g_base : c.ch_base, 0, NCH * 8, v.data())); put(v); return SCAN_OK; }
+    case SCAN_OUT_CH_SHARD_K0: {
+      std::vector<uint64_t> v(NCH, 0);
+      if (sh) v = c.h_shard_k0;
+      put(v); return SCAN_OK;
+    }
+    case SCAN_OUT_CH_SHARD_N: {
+      std::vector<uint32_t> v(NCH);
+      if (sh) v = c.h_shard_n; else CK(d2h(c.ch_nmax, 0, NCH * 4, v.data()));
+      put(v); return SCAN_OK;
+    }
     case SCAN_OUT_CL_MISMATCH: {
       const uint64_t ncl = (uint64_t)c.TP * c.PP;
       std::vector<uint32_t> J(ncl), mx(ncl);

@@ -22,6 +22,7 @@ constexpr int LINK_CAP = 16384; // samples per (window, link) held in shared mem
 constexpr int ROLES = 32;       // 0..15 collective roles (index in the rank's sorted comm list), 16..31 P2P roles
 constexpr int CROLES = 16;
 constexpr int FCOLS = ROLES + 4;  // per-tile pre-pass columns: roles, ncomp, ncomm, niter, cc_last
+constexpr uint32_t NOT_SPMD = 32u;  // Counters.overflow bit: fused path not applicable
 
 // ----------------------------------------------------------------------------- device buffers
 struct DevBuf {
@@ -59,6 +60,8 @@ struct Counters {
   unsigned long long v_count[6];
   unsigned long long n_edges;
   unsigned long long n_xinst;
+  unsigned int min_niter;            // min iter_end count over ranks (shard regularity check)
+  unsigned int n_end_ranks;          // ranks whose last event ends an iteration
 };
 
 struct Ctx {
@@ -144,6 +147,17 @@ struct Ctx {
   DevBuf xbase;                          // [NCH+1] cross-stage instance index
   DevBuf lk_scratch;                     // link-median scratch for links above the shared-memory capacity
   uint64_t n_xinst = 0;
+  // multi-GPU iteration-window shards (row A9, shard.cu); n_shards == 1: unsharded
+  int n_shards = 1, shard = 0;
+  void* nccl = nullptr;                  // ncclComm_t owned by the context
+  uint32_t it_off = 0;                   // global iteration of this shard's first iteration
+  DevBuf g_base, g_slot, g_nmax, g_nmin, g_k0; // global channel tables + this shard's first occurrence per channel; (kernels use the shard-shifted ch_base/ch_slot)
+  std::vector<uint64_t> h_shard_k0;      // [NCH] global occurrence index of this shard's first instance
+  std::vector<uint32_t> h_shard_n;       // [NCH] this shard's instance count per channel
+  std::vector<uint8_t> h_ccls;           // host copy of the stage-2 class per comm
+  std::vector<uint64_t> h_coff;          // host copy of the comm offsets
+  uint64_t g_N = 0, g_ncomm = 0, g_ncomp = 0;  // job-wide totals (sharded)
+  DevBuf x_send, x_recv, headtail, lk_sendmap, lk_recvmap;
   // optional per-kernel timing
   bool timing = false;
   struct Pending { int k; cudaEvent_t a, b; };
@@ -173,6 +187,38 @@ int timed(Ctx& c, const char* name, F&& f) {
   return n;
 }
 void resolve_timing(Ctx& c);
+
+// CUDA error -> scan_status with the message in c.err (host orchestration code; needs `Ctx& c`)
+#define CK(x)                                                                          \
+  do {                                                                                 \
+    cudaError_t _e = (x);                                                              \
+    if (_e != cudaSuccess) {                                                           \
+      c.err = std::string("CUDA error: ") + cudaGetErrorString(_e) + " at " #x;        \
+      return _e == cudaErrorMemoryAllocation ? SCAN_E_OOM : SCAN_E_CUDA;               \
+    }                                                                                  \
+  } while (0)
+
+// read back the device counters (synchronises the context stream)
+scan_status sync_read(Ctx& c);
+template <class T>
+scan_status upload(Ctx& c, DevBuf& b, const std::vector<T>& v) {
+  CK(b.ensure(v.size() * sizeof(T)));
+  if (!v.empty()) CK(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, c.stream));
+  return SCAN_OK;
+}
+// host orchestration shared by the single-GPU paths (api.cu) and the shard path (shard.cu)
+scan_status prep_ws(Ctx& c, bool tiles);
+scan_status alloc_match_buffers(Ctx& c, bool fused);
+scan_status alloc_detect(Ctx& c);
+scan_status alloc_localize(Ctx& c);
+scan_status sharded_all(Ctx& c);
+void shard_release(Ctx& c);
+
+}  // namespace ms
+
+struct scan_ctx { ms::Ctx c; };  // the opaque handle of scan.h
+
+namespace ms {
 
 // ----------------------------------------------------------------------------- device helpers
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
@@ -302,6 +348,9 @@ int launch_class_counts(Ctx& c);
 int launch_stage1_counts(Ctx& c);
 int launch_event_pass(Ctx& c);
 int launch_links(Ctx& c);
+int launch_link_median(Ctx& c);
+int launch_link_flags(Ctx& c);
+int launch_p2p_counts(Ctx& c);
 int launch_verdict_walk(Ctx& c);
 // exports
 int launch_expand_events(Ctx& c, scan_output which, void* dst);

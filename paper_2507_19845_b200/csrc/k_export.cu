@@ -77,10 +77,11 @@ __global__ void k_inst_export(uint64_t n_inst, uint64_t NCH, uint32_t n_comms, c
                               const uint64_t* ch_slot, const uint32_t* ch_nmin, const uint64_t* coff, const uint32_t* cmem,
                               const uint32_t* nsend, const uint32_t* nrecv, const uint32_t* r_nkeys, const uint32_t* r_keys,
                               const uint32_t* r_cnt, const uint4* rec, const uint32_t* p2p_pay, uint64_t p2p_slot0,
-                              int which, void* dst) {
+                              const uint64_t* kshift, int which, void* dst) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_inst; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t ch = upper_bound_u64(ch_base, NCH + 1, i) - 1;
     const uint64_t k = i - ch_base[ch];
+    const uint64_t kl = kshift ? k - kshift[ch] : k;  // occurrence index among this shard's events
     const uint4 rc = rec[i];
     const bool isp = ch >= n_comms;
     switch (which) {
@@ -94,16 +95,16 @@ __global__ void k_inst_export(uint64_t n_inst, uint64_t NCH, uint32_t n_comms, c
         uint32_t n = 0;
         if (!isp) {
           const uint32_t nm = (uint32_t)(coff[ch + 1] - coff[ch]);
-          if (k < ch_nmin[ch]) n = nm;
+          if (kl < ch_nmin[ch]) n = nm;
           else
             for (uint32_t q = 0; q < nm; ++q) {
               const uint32_t m = cmem[coff[ch] + q];
               const uint32_t C = r_nkeys[m];
               const uint32_t p = lower_bound_u32(r_keys + (uint64_t)m * RCAP, C, (uint32_t)ch);
-              if (p < C && r_keys[(uint64_t)m * RCAP + p] == (uint32_t)ch && r_cnt[(uint64_t)m * RCAP + p] > k) ++n;
+              if (p < C && r_keys[(uint64_t)m * RCAP + p] == (uint32_t)ch && r_cnt[(uint64_t)m * RCAP + p] > kl) ++n;
             }
         } else {
-          n = (nsend[ch - n_comms] > k) + (nrecv[ch - n_comms] > k);
+          n = (nsend[ch - n_comms] > kl) + (nrecv[ch - n_comms] > kl);
         }
         ((uint32_t*)dst)[i] = n;
         break;
@@ -112,8 +113,8 @@ __global__ void k_inst_export(uint64_t n_inst, uint64_t NCH, uint32_t n_comms, c
         uint32_t v = 0;
         if (isp) {
           const uint64_t sb = ch_slot[ch] + k * 2 - p2p_slot0;
-          if (nsend[ch - n_comms] > k) v = p2p_pay[sb];
-          else if (nrecv[ch - n_comms] > k) v = p2p_pay[sb + 1];
+          if (nsend[ch - n_comms] > kl) v = p2p_pay[sb];
+          else if (nrecv[ch - n_comms] > kl) v = p2p_pay[sb + 1];
         }
         ((uint32_t*)dst)[i] = v;
         break;
@@ -126,11 +127,15 @@ __global__ void k_inst_export(uint64_t n_inst, uint64_t NCH, uint32_t n_comms, c
 int launch_instance_export(Ctx& c, scan_output which, void* dst) {
   if (c.n_inst == 0) return 0;
   unsigned blocks = (unsigned)std::min<uint64_t>((c.n_inst + 255) / 256, 148ull * 16);
-  k_inst_export<<<blocks, 256, 0, c.stream>>>(c.n_inst, c.NCH, c.n_comms, c.ch_base.as<uint64_t>(), c.ch_slot.as<uint64_t>(),
+  // sharded: global channel tables; member counts are this shard's (valid for its own instance ranges)
+  const bool sh = c.n_shards > 1;
+  k_inst_export<<<blocks, 256, 0, c.stream>>>(c.n_inst, c.NCH, c.n_comms, (sh ? c.g_base : c.ch_base).as<uint64_t>(),
+                                              (sh ? c.g_slot : c.ch_slot).as<uint64_t>(),
                                               c.ch_nmin.as<uint32_t>(), c.coff.as<uint64_t>(), c.cmem.as<uint32_t>(),
                                               c.ch_nsend.as<uint32_t>(), c.ch_nrecv.as<uint32_t>(), c.r_nkeys.as<uint32_t>(),
                                               c.r_keys.as<uint32_t>(), c.r_cnt.as<uint32_t>(), c.inst_rec.as<uint4>(),
-                                              c.p2p_pay.as<uint32_t>(), c.p2p_slot0, (int)which, dst);
+                                              c.p2p_pay.as<uint32_t>(), c.p2p_slot0, sh ? c.g_k0.as<uint64_t>() : nullptr,
+                                              (int)which, dst);
   return 1;
 }
 

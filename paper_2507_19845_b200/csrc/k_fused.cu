@@ -21,7 +21,6 @@
 namespace ms {
 
 enum { TY_COMPUTE = 0, TY_TP = 1, TY_DP = 2, TY_XCOLL = 3, TY_P2P = 4 };
-constexpr uint32_t NOT_SPMD = 32u;  // Counters.overflow bit: fused path not applicable
 
 // Role of an event on the template rank of its stage: index of its communicator in the rank's
 // sorted communicator list (collectives), 16 + 8*send + (stage delta + 4) for P2P; -1 = none.
@@ -220,9 +219,11 @@ __global__ void k_fused_census(CensusArgs a) {
   atomicAdd(&a.cnt->n_comm, (unsigned long long)ncomm);
   atomicAdd(&a.cnt->n_comp, (unsigned long long)ncomp);
   atomicMax(&a.cnt->max_niter, niter);
+  atomicMin(&a.cnt->min_niter, niter);
   atomicMax(&a.cnt->max_ncomp, ncomp);
   const uint64_t e1 = a.rank_off[r + 1];
   if (e1 > a.rank_off[r]) atomicMax(&a.cnt->n_iters, niter - ((a.kind[e1 - 1] & 8u) ? 1u : 0u) + 1u);
+  if (e1 > a.rank_off[r] && (a.kind[e1 - 1] & 8u)) atomicAdd(&a.cnt->n_end_ranks, 1u);
   for (uint32_t q = a.rcomm_off[r]; q < a.rcomm_off[r + 1]; ++q) {
     const uint32_t cid = a.rcomm[q];
     uint32_t v = 0;
@@ -281,6 +282,7 @@ struct FusedArgs {
   uint32_t* dlate; uint32_t* dinfo;
   uint32_t slow_num, slow_den; unsigned long long slow_margin;
   uint32_t wi, classes, mode; unsigned long long late_margin, wait_margin; int want_ref;
+  uint32_t it_off;  // global iteration of this shard's first iteration (0 unsharded)
   Counters* cnt;
   // byte offsets of the transposed kernel's shared-memory arrays (host-computed, fused_t_layout)
   uint32_t o_rcb, o_coffr, o_sinst, o_sbits, o_sedge, o_rcs, o_rsum, o_gsum, o_sjoin, o_slate, o_rslow, o_pa, o_pb, o_vd,
@@ -397,10 +399,11 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   // ---- (2) per-tile tables and template position info (from the pre-pass)
   const uint32_t j0 = a.ft_base[(uint64_t)ROLES * n + tile];
   const uint32_t m0 = a.ft_base[(uint64_t)(ROLES + 1) * n + tile];
-  const uint32_t it0 = a.ft_base[(uint64_t)(ROLES + 2) * n + tile];
+  const uint32_t it0 = a.ft_base[(uint64_t)(ROLES + 2) * n + tile];  // shard-local iteration (citer index)
+  const uint32_t itg0 = it0 + a.it_off;  // global iteration: windows, sit, p2p_iter
   const uint32_t jp0 = a.ft_base[(uint64_t)(ROLES + 3) * n + tile];
   const uint32_t wb = j0 >> 5;
-  const uint32_t w_tile = a.wi ? it0 / a.wi : 0;
+  const uint32_t w_tile = a.wi ? itg0 / a.wi : 0;
   const uint32_t ncr = a.ncroles[s];
   if (tid < ROLES) kbase[tid] = a.ft_base[(uint64_t)tid * n + tile];
   if (tid < 4) nlist[tid] = 0;
@@ -581,7 +584,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
         const uint32_t gi = istp ? g : DP + g;
         add64_lohi(&gsum[gi], &gsum[DP + TP + gi], dmin);
       }
-      const uint32_t win = a.wi ? (it0 + (B & 1023u)) / a.wi : 0;
+      const uint32_t win = a.wi ? (itg0 + (B & 1023u)) / a.wi : 0;
       const bool elig = (a.classes >> (cls - 1)) & 1u;
       const bool late_ok = nat == 1 && (unsigned long long)(dmax - dmin) > a.late_margin;
       const uint32_t eslot = istp ? ls : TP + ls;  // partner slot of the last arriver
@@ -646,7 +649,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
       const uint64_t inst = a.ch_base[ch] + kk;
       const uint64_t si = a.ch_slot[ch] + (uint64_t)kk * nm + slot;
       const uint32_t idx = sw_idx(row, p, T);
-      const uint32_t itp = it0 + (B & 1023u);
+      const uint32_t itp = itg0 + (B & 1023u);
       a.sdur[si] = sd[idx];
       a.skind[si] = (uint8_t)(pk[p] & 7u);
       a.sci[si] = (uint32_t)(coffr[row] + m0 + ((A >> 10) & 1023u));
@@ -704,8 +707,8 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
     rsum[2 * row] = sc; rsum[2 * row + 1] = sw;
   }
   // stage-1 counters per (window, rank): total = compute positions of the tile, slow = its slow bits
-  const uint32_t it_last = it0 + (np ? (pb[np - 1] & 1023u) : 0u);
-  const bool one_window = !a.wi || (it0 / a.wi == it_last / a.wi);
+  const uint32_t it_last = itg0 + (np ? (pb[np - 1] & 1023u) : 0u);
+  const bool one_window = !a.wi || (itg0 / a.wi == it_last / a.wi);
   if (P >= 2 && nc) {
     if (one_window) {
       for (uint32_t row = tid; row < R; row += F_NT) {
@@ -718,7 +721,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
     } else {
       for (uint32_t i = tid; i < R * nc; i += F_NT) {
         const uint32_t row = i / nc, p = lst[i - row * nc], r = sbase + row;
-        const uint32_t win = (it0 + (pb[p] & 1023u)) / a.wi;
+        const uint32_t win = (itg0 + (pb[p] & 1023u)) / a.wi;
         const uint32_t j = j0 + (pa[p] & 1023u);
         atomicAdd(&a.wd_total[(uint64_t)win * a.W + r], 1u);
         if ((sbits[row * SW + (j >> 5) - wb] >> (j & 31)) & 1u) atomicAdd(&a.wd_slow[(uint64_t)win * a.W + r], 1u);
@@ -755,7 +758,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
     if (dpos >= 0) {
       const uint32_t p = (uint32_t)dpos;
       const uint32_t ty = (pb[p] >> 25) & 7u;
-      di[0] = j0 + (pa[p] & 1023u); di[1] = jp0; di[2] = a.wi ? (it0 + (pb[p] & 1023u)) / a.wi : 0; di[3] = 1u | (ty << 8);
+      di[0] = j0 + (pa[p] & 1023u); di[1] = jp0; di[2] = a.wi ? (itg0 + (pb[p] & 1023u)) / a.wi : 0; di[3] = 1u | (ty << 8);
     } else {
       di[3] = 0;
     }
@@ -864,10 +867,11 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
   const uint64_t rbase = a.rank_off[sbase];
   const uint32_t j0 = a.ft_base[(uint64_t)ROLES * n + tile];
   const uint32_t m0 = a.ft_base[(uint64_t)(ROLES + 1) * n + tile];
-  const uint32_t it0 = a.ft_base[(uint64_t)(ROLES + 2) * n + tile];
+  const uint32_t it0 = a.ft_base[(uint64_t)(ROLES + 2) * n + tile];  // shard-local iteration (citer index)
+  const uint32_t itg0 = it0 + a.it_off;  // global iteration: windows, sit, p2p_iter
   const uint32_t jp0 = a.ft_base[(uint64_t)(ROLES + 3) * n + tile];
   const uint32_t wb = j0 >> 5;
-  const uint32_t w_tile = a.wi ? it0 / a.wi : 0;
+  const uint32_t w_tile = a.wi ? itg0 / a.wi : 0;
   const uint32_t ncr = a.ncroles[s];
 
   // ---- (0) tables and template info
@@ -1014,7 +1018,7 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
     const uint32_t A = pa[p], B = pb[p];
     const uint32_t role = (B >> 20) & 31u;
     const uint32_t krel = (B >> 10) & 1023u;
-    const uint32_t itp = it0 + (B & 1023u);
+    const uint32_t itp = itg0 + (B & 1023u);
     uint32_t* col = sd + p * RP;
     if (cls == 2) {
       const uint32_t kk = kbase[role] + krel;
@@ -1187,8 +1191,8 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
   }
   __syncthreads();
   // stage-1 counters per (window, rank)
-  const uint32_t it_last = it0 + (np ? (pb[np - 1] & 1023u) : 0u);
-  const bool one_window = !a.wi || (it0 / a.wi == it_last / a.wi);
+  const uint32_t it_last = itg0 + (np ? (pb[np - 1] & 1023u) : 0u);
+  const bool one_window = !a.wi || (itg0 / a.wi == it_last / a.wi);
   if (DP >= 2 && nc) {
     if (one_window) {
       for (uint32_t row = tid; row < R; row += FT_NT) {
@@ -1201,7 +1205,7 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
     } else {
       for (uint32_t i = tid; i < R * nc; i += FT_NT) {
         const uint32_t row = i / nc, p = lst[i - row * nc], r = sbase + row;
-        const uint32_t win = (it0 + (pb[p] & 1023u)) / a.wi;
+        const uint32_t win = (itg0 + (pb[p] & 1023u)) / a.wi;
         const uint32_t j = j0 + (pa[p] & 1023u);
         atomicAdd(&a.wd_total[(uint64_t)win * a.W + r], 1u);
         if ((sbits[row * SW + (j >> 5) - wb] >> (j & 31)) & 1u) atomicAdd(&a.wd_slow[(uint64_t)win * a.W + r], 1u);
@@ -1239,7 +1243,7 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
     if (dpos >= 0) {
       const uint32_t p = (uint32_t)dpos;
       const uint32_t ty = (pb[p] >> 25) & 7u;
-      di[0] = j0 + (pa[p] & 1023u); di[1] = jp0; di[2] = a.wi ? (it0 + (pb[p] & 1023u)) / a.wi : 0; di[3] = 1u | (ty << 8);
+      di[0] = j0 + (pa[p] & 1023u); di[1] = jp0; di[2] = a.wi ? (itg0 + (pb[p] & 1023u)) / a.wi : 0; di[3] = 1u | (ty << 8);
     } else {
       di[3] = 0;
     }
@@ -1306,6 +1310,7 @@ int launch_fused(Ctx& c) {
   a.dlate = c.dlate.as<uint32_t>(); a.dinfo = c.dinfo.as<uint32_t>();
   a.slow_num = c.dcfg.slow_num; a.slow_den = c.dcfg.slow_den; a.slow_margin = c.dcfg.slow_margin_ns;
   a.wi = c.dcfg.window_iters; a.classes = c.lcfg.stage2_classes; a.mode = c.lcfg.stage2_mode;
+  a.it_off = c.it_off;
   a.late_margin = c.lcfg.late_margin_ns; a.wait_margin = c.lcfg.wait_margin_ns; a.want_ref = c.dcfg.want_ref ? 1 : 0;
   a.cnt = c.counters.as<Counters>();
   if (c.fused_t) {

@@ -405,6 +405,7 @@ struct LKArgs {
   uint32_t* lk_n; uint8_t* lk_used; uint32_t* lk_medp; uint32_t* lk_medt; double* lk_bw; uint8_t* lk_dir; uint8_t* lk_elig;
   Counters* cnt;
   unsigned long long* gkey; uint32_t* gid;  // global scratch for links with more than LM_CAP samples
+  uint32_t n_shards, shard;                 // sharded: this shard computes the links with pid % n_shards == shard
 };
 
 // Order key of a sample: the f64 ratio p/t (exactly rounded, monotone in the exact ratio) as
@@ -447,6 +448,15 @@ __global__ void __launch_bounds__(LM_NT) k_link_median(LKArgs a) {
   const uint64_t b = a.ch_base[ch];
   const uint32_t n = a.ch_nmax[ch];
   const uint64_t sb = a.ch_slot[ch];
+  if (a.n_shards > 1 && pid % a.n_shards != a.shard) {  // another shard owns this link: zeros for the all-reduce
+    if (threadIdx.x == 0) {
+      const uint32_t src = a.psrc[pid], dst = a.pdst[pid];
+      const int dpp = (int)(dst / (uint32_t)(a.TP * a.DP)) - (int)(src / (uint32_t)(a.TP * a.DP));
+      a.lk_dir[o] = dpp == 1 ? 0 : (dpp == -1 ? 1 : 2);
+      a.lk_n[o] = 0; a.lk_used[o] = 0; a.lk_elig[o] = 0; a.lk_medp[o] = 0; a.lk_medt[o] = 0; a.lk_bw[o] = 0.0;
+    }
+    return;
+  }
   if (threadIdx.x == 0) { cnt_all = 0; cnt_warm = 0; }
   __syncthreads();
   auto sample = [&](uint32_t k, bool& in, bool& warm) {
@@ -613,28 +623,38 @@ __global__ void __launch_bounds__(LK_NT) k_link_flags(uint32_t n_p2p, int W, con
   }
 }
 
-int launch_links(Ctx& c) {
+// Per-(window, link) medians. Sharded contexts read the job-wide channel tables: the instances of
+// an owned link are all present after the shard exchange (shard.cu).
+int launch_link_median(Ctx& c) {
   if (c.n_p2p == 0) return 0;
   const uint64_t np_inst = std::max<uint64_t>(c.n_inst - c.p2p_inst0, 1);
   if (c.lk_scratch.ensure(np_inst * 12) != cudaSuccess) return 0;
-  LKArgs a{c.n_comms, (uint32_t)c.n_p2p, c.NW, c.dcfg.window_iters, c.W, c.TP, c.DP, c.ch_base.as<uint64_t>(),
-           c.ch_nmax.as<uint32_t>(), c.ch_nsend.as<uint32_t>() + c.n_p2p, c.ch_nrecv.as<uint32_t>() + c.n_p2p,
-           c.inst_rec.as<uint4>(), c.p2p_iter.as<uint32_t>(), c.p2p_pay.as<uint32_t>(), c.ch_slot.as<uint64_t>(),
+  const bool sh = c.n_shards > 1;
+  LKArgs a{c.n_comms, (uint32_t)c.n_p2p, c.NW, c.dcfg.window_iters, c.W, c.TP, c.DP, (sh ? c.g_base : c.ch_base).as<uint64_t>(),
+           (sh ? c.g_nmax : c.ch_nmax).as<uint32_t>(), c.ch_nsend.as<uint32_t>() + c.n_p2p, c.ch_nrecv.as<uint32_t>() + c.n_p2p,
+           c.inst_rec.as<uint4>(), c.p2p_iter.as<uint32_t>(), c.p2p_pay.as<uint32_t>(), (sh ? c.g_slot : c.ch_slot).as<uint64_t>(),
            c.p2p_inst0, c.p2p_slot0, c.lcfg.min_samples, c.lk_n.as<uint32_t>(), c.lk_used.as<uint8_t>(),
            c.lk_medp.as<uint32_t>(), c.lk_medt.as<uint32_t>(), c.lk_bw.as<double>(), c.lk_dir.as<uint8_t>(),
            c.lk_elig.as<uint8_t>(), c.counters.as<Counters>(), c.lk_scratch.as<unsigned long long>(),
-           (uint32_t*)(c.lk_scratch.as<unsigned long long>() + np_inst)};
+           (uint32_t*)(c.lk_scratch.as<unsigned long long>() + np_inst), (uint32_t)c.n_shards, (uint32_t)c.shard};
   const size_t smm = (size_t)LM_CAP * 12;
-  const size_t sm = 3 * LINK_CAP * sizeof(uint32_t);
   cudaFuncSetAttribute(k_link_median, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smm);
-  cudaFuncSetAttribute(k_link_flags, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_link_median<<<(unsigned)(c.NW * c.n_p2p), LM_NT, smm, c.stream>>>(a);
+  return 1;
+}
+
+int launch_link_flags(Ctx& c) {
+  if (c.n_p2p == 0) return 0;
+  const size_t sm = 3 * LINK_CAP * sizeof(uint32_t);
+  cudaFuncSetAttribute(k_link_flags, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_link_flags<<<c.NW, LK_NT, sm, c.stream>>>((uint32_t)c.n_p2p, c.W, c.ch_nsend.as<uint32_t>() + c.n_p2p,
                                                c.lk_medp.as<uint32_t>(), c.lk_medt.as<uint32_t>(), c.lk_dir.as<uint8_t>(),
                                                c.lk_elig.as<uint8_t>(), c.lk_slow.as<uint8_t>(), c.wl_link_slow.as<uint8_t>(),
                                                c.lcfg.bw_num, c.lcfg.bw_den, c.counters.as<Counters>());
-  return 2;
+  return 1;
 }
+
+int launch_links(Ctx& c) { return launch_link_median(c) + launch_link_flags(c); }
 
 // ----------------------------------------------------------------------------- K7+K8 verdicts + walk
 // Cooperative grid: verdicts per (window, rank); roots (ComputeSlow/Both ranks, dst of LinkSlow

@@ -32,7 +32,8 @@ class _Config(ctypes.Structure):
                 ("layers_per_stage", ctypes.c_int32), ("microbatches", ctypes.c_int32),
                 ("iterations", ctypes.c_int32), ("seed", ctypes.c_uint64), ("hidden", ctypes.c_int64),
                 ("jitter", ctypes.c_double), ("clock_skew", ctypes.c_int32), ("n_faults", ctypes.c_int32),
-                ("faults", ctypes.POINTER(_Fault)), ("n_threads", ctypes.c_int32), ("pad", ctypes.c_int32)]
+                ("faults", ctypes.POINTER(_Fault)), ("n_threads", ctypes.c_int32), ("it_begin", ctypes.c_int32),
+                ("it_end", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 def build(force: bool = False) -> str:
@@ -121,19 +122,21 @@ class Trace:
         return len(self.comm_offsets) - 1
 
 
-def _cfg_struct(cfg: GenConfig):
+def _cfg_struct(cfg: GenConfig, iter_range=None):
     arr = (_Fault * max(1, len(cfg.faults)))()
     for i, f in enumerate(cfg.faults):
         arr[i] = _Fault(f.type, f.a, f.b, f.it0, f.it1, 0, f.factor, f.prob)
+    b, e = iter_range if iter_range is not None else (0, 0)
     c = _Config(cfg.tp, cfg.pp, cfg.dp, cfg.layers_per_stage, cfg.microbatches, cfg.iterations,
                 cfg.seed, cfg.hidden, cfg.jitter, 1 if cfg.clock_skew else 0, len(cfg.faults),
-                ctypes.cast(arr, ctypes.POINTER(_Fault)), cfg.threads, 0)
+                ctypes.cast(arr, ctypes.POINTER(_Fault)), cfg.threads, b, e, 0)
     return c, arr
 
 
-def count(cfg: GenConfig) -> np.ndarray:
+def count(cfg: GenConfig, iter_range=None) -> np.ndarray:
+    """Per-rank event offsets [W+1] of the whole trace, or of iterations [b, e) when ``iter_range``."""
     lib = _load()
-    c, keep = _cfg_struct(cfg)
+    c, keep = _cfg_struct(cfg, iter_range)
     ro = np.zeros(cfg.world + 1, dtype=np.uint64)
     n = lib.gen_count(ctypes.byref(c), ro.ctypes.data)
     if n < 0:
@@ -145,11 +148,19 @@ def _ptr(a):
     return None if a is None else a.ctypes.data
 
 
-def generate(cfg: GenConfig, ground_truth: bool = False, out: dict | None = None, with_start: bool = True) -> Trace:
-    """Run the DES. ``out`` may supply preallocated (e.g. pinned) column arrays."""
+def generate(cfg: GenConfig, ground_truth: bool = False, out: dict | None = None, with_start: bool = True,
+             iter_range: tuple[int, int] | None = None) -> Trace:
+    """Run the DES. ``out`` may supply preallocated (e.g. pinned) column arrays.
+
+    ``iter_range=(b, e)`` emits only iterations [b, e) of the same job: per rank, exactly the events
+    the full trace holds for those iterations (iterations are simulated independently from
+    (seed, iteration, ...)-keyed draws), without start times or ground truth.
+    """
     lib = _load()
-    c, keep = _cfg_struct(cfg)
-    ro = count(cfg)
+    if iter_range is not None and (with_start or ground_truth):
+        raise ValueError("an iteration range carries durations only: pass with_start=False, ground_truth=False")
+    c, keep = _cfg_struct(cfg, iter_range)
+    ro = count(cfg, iter_range)
     n = int(ro[-1])
     nc = lib.gen_comm_table(ctypes.byref(c), None, None)
     coff = np.zeros(nc + 1, dtype=np.uint64)

@@ -58,7 +58,8 @@ typedef struct gen_config_c {
   double jitter;
   int32_t clock_skew, n_faults;
   const gen_fault_c* faults;
-  int32_t n_threads, pad;
+  int32_t n_threads, it_begin;  // iteration range [it_begin, it_end) to emit; it_end = 0: all iterations
+  int32_t it_end, pad;
 } gen_config_c;
 
 }
@@ -111,6 +112,7 @@ struct Cfg {
   int skew;
   std::vector<Fault> faults;
   int threads;
+  int it_begin = 0, it_end = 0;  // emitted iteration range (events of iteration it land at it - it_begin)
 };
 
 inline uint16_t KO(uint16_t kind, uint16_t op, bool iter_end = false) {
@@ -303,7 +305,7 @@ struct IterSim {
   }
 
   uint64_t ev_index(int r, uint32_t local) const {
-    return rank_off[r] + (uint64_t)it * progs[T.pp_of(r)].n_events + local;
+    return rank_off[r] + (uint64_t)(it - c.it_begin) * progs[T.pp_of(r)].n_events + local;
   }
 
   double throttle_factor(int r, uint64_t opidx) const {
@@ -451,6 +453,7 @@ Cfg to_cfg(const gen_config_c* g) {
   c.tp = g->tp; c.pp = g->pp; c.dp = g->dp; c.ls = g->layers_per_stage; c.m = g->microbatches;
   c.iters = g->iterations; c.seed = g->seed; c.hidden = g->hidden; c.jitter = g->jitter;
   c.skew = g->clock_skew; c.threads = g->n_threads;
+  c.it_begin = g->it_begin; c.it_end = g->it_end ? g->it_end : g->iterations;
   for (int i = 0; i < g->n_faults; ++i) {
     const gen_fault_c& f = g->faults[i];
     c.faults.push_back(Fault{f.type, f.a, f.b, f.it0, f.it1, f.factor, f.prob});
@@ -465,11 +468,12 @@ extern "C" {
 int64_t gen_count(const gen_config_c* g, uint64_t* rank_offsets) {
   Cfg c = to_cfg(g);
   if (c.tp < 1 || c.pp < 1 || c.dp < 1 || c.m < 1 || c.iters < 0 || c.ls < 1) return -1;
+  if (c.it_begin < 0 || c.it_end < c.it_begin || c.it_end > c.iters) return -1;
   Topo T = make_topo(c);
   std::vector<uint32_t> per_stage(c.pp);
   for (int s = 0; s < c.pp; ++s) per_stage[s] = build_program(c, s).n_events;
   uint64_t off = 0;
-  for (int r = 0; r < T.W; ++r) { rank_offsets[r] = off; off += (uint64_t)per_stage[T.pp_of(r)] * c.iters; }
+  for (int r = 0; r < T.W; ++r) { rank_offsets[r] = off; off += (uint64_t)per_stage[T.pp_of(r)] * (c.it_end - c.it_begin); }
   rank_offsets[T.W] = off;
   return (int64_t)off;
 }
@@ -496,6 +500,9 @@ int gen_fill(const gen_config_c* g, const uint64_t* rank_offsets, int64_t* start
              uint64_t* gt_inst, int64_t* gt_true_start) {
   Cfg c = to_cfg(g);
   if (c.tp < 1 || c.pp < 1 || c.dp < 1) return -2;
+  const bool ranged = c.it_begin != 0 || c.it_end != c.iters;
+  if (ranged && (start_ns || gt_inst || gt_true_start)) return -2;  // a range carries durations only
+  if (c.it_begin < 0 || c.it_end < c.it_begin || c.it_end > c.iters) return -2;
   Topo T = make_topo(c);
   std::vector<Program> progs;
   for (int s = 0; s < c.pp; ++s) progs.push_back(build_program(c, s));
@@ -504,8 +511,8 @@ int gen_fill(const gen_config_c* g, const uint64_t* rank_offsets, int64_t* start
   for (uint32_t cid = 0; cid < T.n_comms; ++cid) { T.members(cid, cmem[cid]); csize[cid] = (uint32_t)cmem[cid].size(); }
   std::vector<int64_t> makespan(c.iters, 0);
   int nth = c.threads > 0 ? c.threads : (int)std::max(1u, std::thread::hardware_concurrency());
-  nth = std::max(1, std::min(nth, std::max(1, c.iters)));
-  std::atomic<int> next{0};
+  nth = std::max(1, std::min(nth, std::max(1, c.it_end - c.it_begin)));
+  std::atomic<int> next{c.it_begin};
   std::atomic<int> fail{0};
   auto worker = [&]() {
     IterSim sim(c, T, progs, rank_offsets, csize, cmem);
@@ -513,7 +520,7 @@ int gen_fill(const gen_config_c* g, const uint64_t* rank_offsets, int64_t* start
     sim.payload = payload; sim.gt_inst = gt_inst;
     for (;;) {
       int it = next.fetch_add(1);
-      if (it >= c.iters) break;
+      if (it >= c.it_end) break;
       sim.makespan_out = &makespan[it];
       sim.run(it);
       if (makespan[it] < 0) fail = 1;
