@@ -9,8 +9,10 @@ Default workload (N=1): configs[2] "C3" — 1024 ranks TP8xPP8xDP16, 1000 iterat
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--iters I] [--impl reference]
 
-N>1 (torchrun): every rank analyses its own iteration-window shard of the same job (weak scaling
-of the generated trace); see DESIGN.md §Multi-GPU for the status of the exchange step.
+N>1 (torchrun): the SAME job is split into N iteration-window shards (strong scaling): rank g
+generates iterations shard_iterations(I, N, g) of every rank and analyses them through one sharded
+context (scan_create_sharded; NCCL all-gather / all-to-all / all-reduce inside scan_analyze), so
+every rank ends with the job-wide verdicts. value = all events / max-over-ranks step time.
 """
 from __future__ import annotations
 
@@ -100,7 +102,7 @@ def make_trace(name: str, iters: int | None, seed: int, pinned: bool, it_range=N
     import tracegen as tg
     from tracegen import configs
     cfg = configs.CONFIGS[name](seed=seed) if iters is None else configs.CONFIGS[name](seed=seed, iterations=iters)
-    ro = tg.count(cfg)
+    ro = tg.count(cfg, it_range)
     n = int(ro[-1])
     out = None
     if pinned:
@@ -110,7 +112,7 @@ def make_trace(name: str, iters: int | None, seed: int, pinned: bool, it_range=N
                       ("payload", torch.int32)):
             t = torch.empty(n, dtype=dt, pin_memory=True)
             out[k] = t.numpy().view({torch.int32: np.uint32, torch.int16: np.uint16}[dt])
-    return tg.generate(cfg, out=out, with_start=False), cfg
+    return tg.generate(cfg, out=out, with_start=False, iter_range=it_range), cfg
 
 
 def cpu_oracle_rate(name: str, sample_iters: int, seed: int) -> dict:
@@ -136,7 +138,7 @@ def run_reference(args, rank: int, world: int):
     v = float(np.median([r["value"] for r in rates]))
     secs = float(np.median([r["seconds"] for r in rates]))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "events/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.config] + f" (sample: iterations [0,{sample_iters}))"},
             "cpu_baseline": {"value": v, "unit": "events/s", "cores": 1, "kind": "oracle", "sample": rates[0]["sample"]},
@@ -174,11 +176,14 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    # ---- synthetic trace: host (pinned) -> device columns ----
+    # ---- synthetic trace: host (pinned) -> device columns; N>1: this rank's iteration block ----
+    from tracegen import configs as _cf
     iters = args.iters
-    seed = args.seed + (rank if world > 1 else 0)
+    total_iters = iters if iters is not None else _cf.CONFIGS[args.config]().iterations
+    blk = ms.shard_iterations(total_iters, world, rank) if world > 1 else None
+    uid = ms.shard_unique_id() if world > 1 else None
     t_gen = time.perf_counter()
-    tr, cfg = make_trace(args.config, iters, seed, pinned=True)
+    tr, cfg = make_trace(args.config, iters, args.seed, pinned=True, it_range=blk)
     t_gen = time.perf_counter() - t_gen
     N = tr.n_events
     comm_frac = float(((tr.kind_op & 7) != 0).mean()) if N <= 50_000_000 else float(
@@ -188,7 +193,7 @@ def main():
            for k, v in host.items()}
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream(local)
-    s = ms.Scan(local, stream.cuda_stream)
+    s = ms.Scan(local, stream.cuda_stream, shards=(world, rank, uid) if world > 1 else None)
     s.load(tr, device_ptrs=True, cols=dev)
 
     def step():
@@ -200,6 +205,8 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # per-kernel CUDA events (library timing mode, recorded on the launch stream) over the timed steps
+    s.set_timing(args.breakdown)
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
@@ -208,6 +215,8 @@ def main():
         torch.cuda.synchronize()
     ms_total = ev0.elapsed_time(ev1)
     launches = s.kernel_launches()
+    kernels = s.kernel_timing() if args.breakdown else {}
+    s.set_timing(False)
     t_local = torch.tensor([ms_total], dtype=torch.float64, device=f"cuda:{local}")
     n_tot = torch.tensor([float(N)], dtype=torch.float64, device=f"cuda:{local}")
     if dist:
@@ -216,13 +225,6 @@ def main():
     ms_step = float(t_local.item()) / args.steps
     value = float(n_tot.item()) / (ms_step / 1e3)
 
-    # per-kernel breakdown (separate, untimed-for-value pass with CUDA events on the launch stream)
-    kernels = {}
-    if args.breakdown:
-        s.set_timing(True)
-        step()
-        kernels = s.kernel_timing()
-        s.set_timing(False)
     # verdicts for the record
     fused = bool(s.analyze()["fused"])
     verdict = s.export("wl_verdict")
@@ -231,11 +233,13 @@ def main():
     # ---- e2e: host pinned columns through the public API, H2D + analysis + D2H of the verdicts ----
     e2e = None
     if not args.no_e2e:
-        s2 = ms.Scan(local, stream.cuda_stream)
+        s2 = ms.Scan(local, stream.cuda_stream, shards=(world, rank, ms.shard_unique_id()) if world > 1 else None)
         h2d = sum(v.nbytes for v in host.values())
         times = []
         for i in range(2):
             torch.cuda.synchronize()
+            if dist:
+                dist.barrier()
             t0 = time.perf_counter()
             s2.load(tr)
             s2.analyze()
@@ -244,8 +248,16 @@ def main():
             times.append(time.perf_counter() - t0)
         s2.close()
         d2h = out_v.nbytes + out_l.nbytes
-        e2e = {"value": N / min(times), "unit": "events/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "seconds_per_step": min(times)}
+        t_e2e = torch.tensor([min(times)], dtype=torch.float64, device=f"cuda:{local}")
+        h2d_t = torch.tensor([float(h2d)], dtype=torch.float64, device=f"cuda:{local}")
+        if dist:
+            dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+            dist.all_reduce(h2d_t, op=dist.ReduceOp.SUM)
+        e2e = {"value": float(n_tot.item()) / float(t_e2e.item()), "unit": "events/s",
+               "h2d_bytes_per_step": int(h2d_t.item()), "d2h_bytes_per_step": int(d2h) * world,
+               "seconds_per_step": float(t_e2e.item()),
+               "path": "pinned host columns -> scan_load_events(SCAN_HOST_PTRS) -> scan_analyze -> scan_export"
+                       " (verdicts + labels), wall clock" + (", max over ranks" if dist else "")}
 
     if rank != 0:
         if dist:
@@ -257,16 +269,20 @@ def main():
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
     bpe = alg_bytes_per_event(comm_frac)
-    achieved = bpe * N / (ms_step / 1e3) / 1e9
     dom = max(kernels.items(), key=lambda kv: kv[1][0]) if kernels else None
     kern_ms = sum(v[0] for v in kernels.values()) if kernels else None
+    # dominant kernel (k_fused: reads every event column once and writes every per-event output, so
+    # its algorithmic bytes per launch are the path's bpe x this GPU's events) / its mean launch time
+    dom_ms = dom[1][0] / max(dom[1][1], 1) if dom else ms_step
+    achieved = bpe * N / (dom_ms / 1e3) / 1e9
+    step_achieved = bpe * N / (ms_step / 1e3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath))
-            if tj.get("config") == args.config and tj.get("iters") == (iters or cfg.iterations):
-                traffic = tj.get("dram_bytes_per_step")
+            if tj.get("config") == args.config and tj.get("iters") == total_iters and tj.get("n_gpus", 1) == world:
+                traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     cpu = None
@@ -275,18 +291,25 @@ def main():
         cpu.pop("seconds", None)
     line = {
         "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config] + (f" [{iters} it]" if iters else ""), "events": N,
-                   "comm_fraction": round(comm_frac, 4), "parallelism": f"trace shard per GPU x{world}",
+        "config": {"workload": WORKLOADS[args.config] + (f" [{iters} it]" if iters else ""), "events": int(n_tot.item()),
+                   "events_per_gpu": N, "comm_fraction": round(comm_frac, 4),
+                   "parallelism": (f"{world} iteration-window shards (rank 0: iterations {blk[0]}..{blk[1] - 1}), "
+                                   "NCCL all-gather + all-to-all + all-reduce inside scan_analyze") if world > 1
+                                  else "1 GPU, whole trace",
                    "l2": "inputs (16 B/event, %.1f GB) >> 126 MB L2: no flush needed" % (16 * N / 1e9),
                    "generator_s": round(t_gen, 1)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
-                     "bytes_per_event": round(bpe, 3), "scope": "whole step (all kernels); see kernels",
-                     "dominant_kernel": ({"name": dom[0], "ms": dom[1][0], "launches": dom[1][1],
+                     "bytes_per_event": round(bpe, 3),
+                     "scope": "dominant kernel: algorithmic bytes per launch / its mean launch time (CUDA events on the "
+                              "launch stream over the timed steps)",
+                     "step_achieved": step_achieved, "step_frac": step_achieved / peak,
+                     "dominant_kernel": ({"name": dom[0], "ms_per_launch": dom_ms, "launches": dom[1][1],
                                           "share": dom[1][0] / kern_ms} if dom else None)},
-        "kernels": {k: {"ms": round(v[0], 4), "launches": v[1]} for k, v in sorted(kernels.items(), key=lambda kv: -kv[1][0])},
+        "kernels": {k: {"ms_per_step": round(v[0] / args.steps, 4), "launches": v[1]}
+                    for k, v in sorted(kernels.items(), key=lambda kv: -kv[1][0])},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(launches) * args.steps,
