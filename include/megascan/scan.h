@@ -172,7 +172,7 @@ const char* scan_last_error(const scan_ctx* ctx);   /* owned by ctx; "" if none 
        structs are job-wide and identical on every shard (and to the unsharded run).
    Exchange: two small ncclAllGather (per-channel counts, P2P channel bitmap) for the global
    numbering, one grouped ncclSend/ncclRecv all-to-all that ships each P2P instance record
-   (24 B) to the shard owning its link (link pid % n_shards), one grouped ncclAllReduce of the
+   (12 B) to the shard owning its link (link pid % n_shards), one grouped ncclAllReduce of the
    per-rank / per-window / per-link partial results.
    Preconditions (else SCAN_E_UNSUPPORTED on every shard): the trace is SPMD (fused path), and
    every shard but the last ends on an iteration boundary of every rank with all members of

@@ -218,6 +218,7 @@ __global__ void k_fused_census(CensusArgs a) {
   a.r_ncomm[r] = ncomm; a.r_ncomp[r] = ncomp; a.r_niter[r] = niter;
   atomicAdd(&a.cnt->n_comm, (unsigned long long)ncomm);
   atomicAdd(&a.cnt->n_comp, (unsigned long long)ncomp);
+  atomicAdd(&a.cnt->n_bits_words, (unsigned long long)((ncomp + 31) / 32));  // k_rank_prefix rewrites the same sum
   atomicMax(&a.cnt->max_niter, niter);
   atomicMin(&a.cnt->min_niter, niter);
   atomicMax(&a.cnt->max_ncomp, ncomp);

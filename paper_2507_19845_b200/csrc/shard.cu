@@ -9,13 +9,13 @@
 //      => host: job-wide channel bases / slots (the unsharded k_channels numbering) and this
 //         shard's first occurrence per channel `pre`; the shard's kernels get base + pre and
 //         slot + pre*|M|, so every instance id / slot they write is the job-wide one
-//   X3 grouped ncclSend/ncclRecv  the 24-byte record of each P2P instance to the shard owning
+//   X3 grouped ncclSend/ncclRecv  the 12-byte record of each P2P instance to the shard owning
 //      its link (pid % G), which then holds every sample of the link for the stage-3 median
 //   X4 grouped ncclAllReduce(sum)  per-(window, rank) stage-1/2 counters, wait-for edge weights,
 //      per-rank sums, link medians (zero on non-owners), per-rank stage-2 boundary records
 //   => every shard: stage-2 boundary fix-up, candidates, LinkSlow flags, verdicts + walk
 //      (replicated on identical inputs, so every shard reports the same job-wide tables).
-// Exchange volume on C3 at G = 8: X3 ~ 24 B x 14.5e6 P2P instances x 7/8 spread over 8 GPUs;
+// Exchange volume on C3 at G = 8: X3 ~ 12 B x 14.5e6 P2P instances x 7/8 spread over 8 GPUs;
 // X4 ~ 0.6 MB. The per-shard fused pass dominates.
 #include <nccl.h>
 #include <algorithm>
@@ -35,7 +35,9 @@ namespace {
     }                                                                                    \
   } while (0)
 
-constexpr uint32_t LREC = 6;  // u32 words per shipped P2P instance: rec {dmin, dmax, last, flags}, iteration, payload
+// u32 words per shipped P2P instance: what the stage-3 median reads (k_link_median): transfer time
+// (rec.x = dmin), payload, and iteration << 8 | instance flags (VALID, WARMUP; P2P class bits are 0)
+constexpr uint32_t LREC = 3;
 
 struct LinkMap { unsigned long long flat, inst0, slot0; uint32_t n, pad; };
 
@@ -47,21 +49,24 @@ __global__ void k_link_pack(const LinkMap* map, const uint4* rec, const uint32_t
     const uint64_t i = m.inst0 + k;
     const uint4 r = rec[i];
     uint32_t* o = buf + (m.flat + k) * LREC;
-    o[0] = r.x; o[1] = r.y; o[2] = r.z; o[3] = r.w;
-    o[4] = p2p_iter[i - p2p_inst0];
-    o[5] = p2p_pay[m.slot0 + 2ull * k - p2p_slot0];
+    o[0] = r.x;
+    o[1] = p2p_pay[m.slot0 + 2ull * k - p2p_slot0];
+    o[2] = (p2p_iter[i - p2p_inst0] << 8) | (r.w & 0xFFu);
   }
 }
 
+// rows of links this shard owns; only the fields the median reads are written (the rest of an
+// unowned-range row stays unspecified, scan.h)
 __global__ void k_link_unpack(const LinkMap* map, const uint32_t* buf, uint4* rec, uint32_t* p2p_iter, uint32_t* p2p_pay,
                               uint64_t p2p_inst0, uint64_t p2p_slot0) {
   const LinkMap m = map[blockIdx.x];
   for (uint32_t k = threadIdx.x; k < m.n; k += blockDim.x) {
     const uint64_t i = m.inst0 + k;
     const uint32_t* v = buf + (m.flat + k) * LREC;
-    rec[i] = make_uint4(v[0], v[1], v[2], v[3]);
-    p2p_iter[i - p2p_inst0] = v[4];
-    p2p_pay[m.slot0 + 2ull * k - p2p_slot0] = v[5];
+    rec[i].x = v[0];
+    rec[i].w = v[2] & 0xFFu;
+    p2p_pay[m.slot0 + 2ull * k - p2p_slot0] = v[1];
+    p2p_iter[i - p2p_inst0] = v[2] >> 8;
   }
 }
 
@@ -157,19 +162,64 @@ __global__ void k_shard_fixup(int W, int G, const unsigned long long* ht, uint32
   }
 }
 
-scan_status allgather_u32(Ctx& c, const std::vector<uint32_t>& mine, size_t n, std::vector<uint32_t>& all) {
+// X1 send buffer, packed on the device: header from the census counters, per-comm member-count
+// extremes, P2P channel bitmap words
+__global__ void k_x1_pack(const Counters* cnt, uint32_t force_status, unsigned long long N, const uint32_t* nmin,
+                          const uint32_t* nmax, const uint32_t* bitmap, uint32_t nc, uint64_t nbm, uint32_t* out) {
+  const uint64_t L = 16 + 2ull * nc + nbm;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t v = 0;
+    if (i < 16) {
+      const unsigned long long be = cnt->bad_event;
+      switch ((int)i) {
+        case 0: v = force_status ? force_status : (cnt->overflow & NOT_SPMD) ? 1u : be != ~0ull ? 2u : (cnt->overflow & 7u) ? 3u : 0u; break;
+        case 1: v = cnt->max_niter; break;
+        case 2: v = cnt->min_niter; break;
+        case 3: v = cnt->n_end_ranks; break;
+        case 4: v = cnt->n_iters; break;
+        case 5: v = (uint32_t)N; break;
+        case 6: v = (uint32_t)(N >> 32); break;
+        case 7: v = (uint32_t)be; break;
+        case 8: v = (uint32_t)(be >> 32); break;
+        case 9: v = (uint32_t)cnt->n_comm; break;
+        case 10: v = (uint32_t)(cnt->n_comm >> 32); break;
+        case 11: v = (uint32_t)cnt->n_comp; break;
+        case 12: v = (uint32_t)(cnt->n_comp >> 32); break;
+        case 13: v = cnt->max_ncomp; break;
+        case 14: v = (uint32_t)cnt->n_bits_words; break;
+        default: v = (uint32_t)(cnt->n_bits_words >> 32); break;
+      }
+    } else if (i < 16 + nc) {
+      v = nmin[i - 16];
+    } else if (i < 16 + 2ull * nc) {
+      v = nmax[i - 16 - nc];
+    } else {
+      v = bitmap[i - 16 - 2ull * nc];
+    }
+    out[i] = v;
+  }
+}
+
+// status + match counters of this shard for the X4 all-reduce (no host round trip)
+__global__ void k_x4_status(const Counters* cnt, const uint32_t* cl_J, const uint32_t* cl_max, uint32_t ncl, int check_class,
+                            unsigned long long* e) {
+  if (threadIdx.x || blockIdx.x) return;
+  unsigned long long bad = 0;
+  if (check_class)
+    for (uint32_t i = 0; i < ncl; ++i) bad |= cl_J[i] != cl_max[i];
+  e[0] = (cnt->overflow & NOT_SPMD) ? 1ull : 0ull;
+  e[1] = bad;
+  e[2] = cnt->n_incomplete; e[3] = cnt->n_kind_mismatch; e[4] = cnt->n_payload_mismatch;
+}
+
+// all-gather of n u32 already packed in c.x_send; the gathered words land on the host
+scan_status allgather_dev(Ctx& c, size_t n, std::vector<uint32_t>& all) {
   const size_t G = (size_t)c.n_shards;
-  CK(c.x_send.ensure(n * 4)); CK(c.x_recv.ensure(n * 4 * G));
-  CK(cudaMemcpyAsync(c.x_send.p, mine.data(), n * 4, cudaMemcpyHostToDevice, c.stream));
+  CK(c.x_recv.ensure(n * 4 * G));
   NCK(ncclAllGather(c.x_send.p, c.x_recv.p, n, ncclUint32, (ncclComm_t)c.nccl, c.stream));
   all.assign(n * G, 0);
   CK(cudaMemcpyAsync(all.data(), c.x_recv.p, n * 4 * G, cudaMemcpyDeviceToHost, c.stream));
   CK(cudaStreamSynchronize(c.stream));
-  return SCAN_OK;
-}
-
-scan_status d2h_async(Ctx& c, void* dst, const DevBuf& b, uint64_t off, uint64_t bytes) {
-  if (bytes) CK(cudaMemcpyAsync(dst, (const uint8_t*)b.p + off, bytes, cudaMemcpyDeviceToHost, c.stream));
   return SCAN_OK;
 }
 
@@ -183,8 +233,7 @@ scan_status sharded_all(Ctx& c) {
   ncclComm_t comm = (ncclComm_t)c.nccl;
   scan_status st;
   if ((st = prep_ws(c, false))) return st;
-  // ---- local census (the fused pre-pass of this shard)
-  uint32_t status = 0;  // 1 not SPMD, 2 schema error, 3 capacity
+  // ---- local census (the fused pre-pass of this shard) + X1, packed on the device (one sync)
   if (c.spmd) {
     CK(c.ft_cols.ensure((uint64_t)FCOLS * c.n_ftiles * 4)); CK(c.ft_base.ensure((uint64_t)FCOLS * c.n_ftiles * 4));
     CK(c.st_tot.ensure((uint64_t)c.PP * FCOLS * 4));
@@ -192,27 +241,16 @@ scan_status sharded_all(Ctx& c) {
     CK(c.ft_posK.ensure((uint64_t)c.n_ftiles * c.FT * 2));
     c.launches += timed(c, "k_fused_prepass", [&] { return launch_fused_prepass(c); });
     c.launches += timed(c, "k_fused_census", [&] { return launch_fused_census(c); });
-    if ((st = sync_read(c))) return st;
-    if (c.hc.overflow & NOT_SPMD) status = 1;
-    else if (c.hc.bad_event != ~0ull) status = 2;
-    else if (c.hc.overflow & 7u) status = 3;
-  } else {
-    status = 1;
   }
-  // ---- X1: status, iteration counts, per-comm member-count extremes, P2P channel bitmap
   const uint64_t nbm = c.n_bm_words;
   const size_t HA = 16, LA = HA + 2 * (size_t)nc + nbm;
-  std::vector<uint32_t> A(LA, 0), AA;
-  A[0] = status; A[1] = c.hc.max_niter; A[2] = c.hc.min_niter; A[3] = c.hc.n_end_ranks; A[4] = c.hc.n_iters;
-  A[5] = (uint32_t)c.N; A[6] = (uint32_t)(c.N >> 32);
-  A[7] = (uint32_t)c.hc.bad_event; A[8] = (uint32_t)(c.hc.bad_event >> 32);
-  A[9] = (uint32_t)c.hc.n_comm; A[10] = (uint32_t)(c.hc.n_comm >> 32);
-  A[11] = (uint32_t)c.hc.n_comp; A[12] = (uint32_t)(c.hc.n_comp >> 32);
-  if ((st = d2h_async(c, A.data() + HA, c.ch_nmin, 0, (uint64_t)nc * 4))) return st;
-  if ((st = d2h_async(c, A.data() + HA + nc, c.ch_nmax, 0, (uint64_t)nc * 4))) return st;
-  if ((st = d2h_async(c, A.data() + HA + 2 * nc, c.bitmap, 0, nbm * 4))) return st;
-  CK(cudaStreamSynchronize(c.stream));
-  timed(c, "x1_allgather", [&] { st = allgather_u32(c, A, LA, AA); return 0; });
+  std::vector<uint32_t> AA;
+  CK(c.x_send.ensure(LA * 4));
+  k_x1_pack<<<(unsigned)std::min<uint64_t>((LA + 255) / 256, 1024), 256, 0, c.stream>>>(
+      c.counters.as<Counters>(), c.spmd ? 0u : 1u, (unsigned long long)c.N, c.ch_nmin.as<uint32_t>(), c.ch_nmax.as<uint32_t>(),
+      c.bitmap.as<uint32_t>(), nc, nbm, c.x_send.as<uint32_t>());
+  c.launches += 1;
+  timed(c, "x1_allgather", [&] { st = allgather_dev(c, LA, AA); return 0; });
   if (st) return st;
   auto hdr = [&](uint32_t s, size_t i) { return AA[(size_t)s * LA + i]; };
   auto u64at = [&](uint32_t s, size_t i) { return (uint64_t)hdr(s, i) | ((uint64_t)hdr(s, i + 1) << 32); };
@@ -243,19 +281,25 @@ scan_status sharded_all(Ctx& c) {
     n_iters += s + 1 < G ? hdr(s, 1) : hdr(s, 4);
   }
   c.it_off = it_off;
+  {  // fresh host counters: census values from this shard's own header
+    Counters z{};
+    z.bad_event = ~0ull; z.min_niter = hdr(g, 2);
+    z.max_niter = hdr(g, 1); z.n_end_ranks = hdr(g, 3); z.n_iters = hdr(g, 4);
+    z.n_comm = u64at(g, 9); z.n_comp = u64at(g, 11); z.max_ncomp = hdr(g, 13); z.n_bits_words = u64at(g, 14);
+    c.hc = z;
+  }
   c.g_N = c.g_ncomm = c.g_ncomp = 0;
   for (uint32_t s = 0; s < G; ++s) { c.g_N += u64at(s, 5); c.g_ncomm += u64at(s, 9); c.g_ncomp += u64at(s, 11); }
-  {
-    std::vector<uint32_t> bm(nbm, 0);
-    for (uint32_t s = 0; s < G; ++s)
-      for (uint64_t i = 0; i < nbm; ++i) bm[i] |= AA[(size_t)s * LA + HA + 2 * nc + i];
-    if (nbm) CK(cudaMemcpyAsync(c.bitmap.p, bm.data(), nbm * 4, cudaMemcpyHostToDevice, c.stream));
-  }
+  std::vector<uint32_t> bm(nbm, 0);  // job-wide P2P channel bitmap (OR over shards)
+  uint64_t np = 0;
+  for (uint32_t s = 0; s < G; ++s)
+    for (uint64_t i = 0; i < nbm; ++i) bm[i] |= AA[(size_t)s * LA + HA + 2 * nc + i];
+  for (uint64_t i = 0; i < nbm; ++i) np += (uint64_t)__builtin_popcount(bm[i]);
+  if (nbm) CK(cudaMemcpyAsync(c.bitmap.p, bm.data(), nbm * 4, cudaMemcpyHostToDevice, c.stream));
   c.launches += timed(c, "k_rank_prefix", [&] { return launch_rank_prefix(c); });
-  if ((st = sync_read(c))) return st;
   // ---- X2: P2P member counts per job-wide P2P channel
-  const uint64_t np = c.hc.n_p2p, NCH = nc + np;
-  c.n_p2p = np; c.NCH = NCH;
+  const uint64_t NCH = nc + np;
+  c.n_p2p = np; c.NCH = NCH; c.hc.n_p2p = np;
   CK(c.ch_nsend.ensure(std::max<uint64_t>(2 * np, 1) * 4)); CK(c.ch_nrecv.ensure(std::max<uint64_t>(2 * np, 1) * 4));
   if (np) {
     CK(cudaMemsetAsync(c.ch_nsend.p, 0, 2 * np * 4, c.stream));
@@ -263,18 +307,18 @@ scan_status sharded_all(Ctx& c) {
   }
   c.launches += timed(c, "k_p2p_counts", [&] { return launch_p2p_counts(c); });
   const size_t LB = std::max<size_t>(2 * np, 1);
-  std::vector<uint32_t> B(LB, 0), BB;
-  if ((st = d2h_async(c, B.data(), c.ch_nsend, 0, np * 4))) return st;
-  if ((st = d2h_async(c, B.data() + np, c.ch_nrecv, 0, np * 4))) return st;
-  CK(cudaStreamSynchronize(c.stream));
-  timed(c, "x2_allgather", [&] { st = allgather_u32(c, B, LB, BB); return 0; });
+  std::vector<uint32_t> BB;
+  CK(c.x_send.ensure(LB * 4));
+  CK(cudaMemsetAsync(c.x_send.p, 0, LB * 4, c.stream));
+  if (np) {
+    CK(cudaMemcpyAsync(c.x_send.p, c.ch_nsend.p, np * 4, cudaMemcpyDeviceToDevice, c.stream));
+    CK(cudaMemcpyAsync(c.x_send.as<uint32_t>() + np, c.ch_nrecv.p, np * 4, cudaMemcpyDeviceToDevice, c.stream));
+  }
+  timed(c, "x2_allgather", [&] { st = allgather_dev(c, LB, BB); return 0; });
   if (st) return st;
   // P2P endpoints in channel order (ascending src*W + dst, the bitmap order)
   std::vector<uint32_t> psrc(np), pdst(np);
   {
-    std::vector<uint32_t> bm(nbm);
-    CK(cudaMemcpyAsync(bm.data(), c.bitmap.p, nbm * 4, cudaMemcpyDeviceToHost, c.stream));
-    CK(cudaStreamSynchronize(c.stream));
     uint64_t p = 0;
     for (uint64_t wd = 0; wd < nbm; ++wd)
       for (uint32_t x = bm[wd]; x; x &= x - 1) {
@@ -333,6 +377,7 @@ scan_status sharded_all(Ctx& c) {
   }
   gbase[NCH] = kbase[NCH] = cb; gslot[NCH] = kslot[NCH] = cs; xb[NCH] = cx;
   if (cb >= 0xFFFFFFFFull) { c.err = "more than 2^32-1 instances"; return SCAN_E_UNSUPPORTED; }
+  if (n_iters >= (1u << 24)) { c.err = "sharded analysis supports < 2^24 iterations"; return SCAN_E_UNSUPPORTED; }
   CK(c.ch_base.ensure((NCH + 1) * 8)); CK(c.ch_slot.ensure((NCH + 1) * 8)); CK(c.xbase.ensure((NCH + 1) * 8));
   if ((st = upload(c, c.ch_base, kbase)) || (st = upload(c, c.ch_slot, kslot)) || (st = upload(c, c.xbase, xb)) ||
       (st = upload(c, c.g_base, gbase)) || (st = upload(c, c.g_slot, gslot)) || (st = upload(c, c.g_nmax, gmax)) ||
@@ -364,14 +409,6 @@ scan_status sharded_all(Ctx& c) {
   c.launches += timed(c, "k_fused", [&] { return launch_fused(c); });
   c.launches += timed(c, "k_cross_reduce", [&] { return launch_cross_reduce(c); });
   c.launches += timed(c, "k_deferred", [&] { return launch_deferred(c); });
-  if ((st = sync_read(c))) return st;
-  uint64_t bad_spmd = (c.hc.overflow & NOT_SPMD) ? 1 : 0, bad_class = 0;
-  if (g + 1 < G && c.DP >= 2) {
-    std::vector<uint32_t> J(ncl), mx(ncl);
-    if ((st = d2h_async(c, J.data(), c.cl_J, 0, ncl * 4)) || (st = d2h_async(c, mx.data(), c.cl_max, 0, ncl * 4))) return st;
-    CK(cudaStreamSynchronize(c.stream));
-    for (uint64_t i = 0; i < ncl; ++i) bad_class |= J[i] != mx[i];
-  }
   // ---- X3: P2P instance records to the owner of their link (pid % G)
   std::vector<LinkMap> smap, rmap;
   std::vector<size_t> scount(G, 0), rcount(G, 0), soff(G + 1, 0), roff(G + 1, 0);
@@ -444,10 +481,12 @@ scan_status sharded_all(Ctx& c) {
         c.lcfg.stage2_classes, (unsigned long long)c.lcfg.late_margin_ns, c.dcfg.window_iters, c.it_off, ht + (uint64_t)g * W);
     return 1;
   });
-  // job-wide counters ride along in the last 16 words of the record buffer
+  // this shard's status + match counters ride along in the last 16 words of the record buffer
   {
-    unsigned long long e[16] = {bad_spmd, bad_class, c.hc.n_incomplete, c.hc.n_kind_mismatch, c.hc.n_payload_mismatch};
-    CK(cudaMemcpyAsync(ht + (uint64_t)G * W, e, sizeof(e), cudaMemcpyHostToDevice, c.stream));
+    k_x4_status<<<1, 32, 0, c.stream>>>(c.counters.as<Counters>(), c.cl_J.as<uint32_t>(), c.cl_max.as<uint32_t>(),
+                                        (uint32_t)ncl, (g + 1 < G && c.DP >= 2) ? 1 : 0, ht + (uint64_t)G * W);
+    c.launches += 1;
+    unsigned long long e[16];
     // ---- X4: one grouped all-reduce (sum) of every partial result
     const uint64_t nnz_tot = c.nnz_c + W * PCAP;
     ncclResult_t xr = ncclSuccess;
