@@ -70,7 +70,7 @@ static void release_all(Ctx& c) {
                     &c.st_tile0, &c.st_npos, &c.role_comm, &c.role_slot, &c.role_type, &c.ncroles, &c.ft_cols,
                     &c.ft_base, &c.ft_last, &c.st_tot, &c.sci, &c.sit, &c.dlate, &c.dinfo, &c.ft_posA, &c.ft_posB,
                     &c.ft_posK, &c.eidx, &c.tile_stage, &c.xbase, &c.lk_scratch, &c.g_base, &c.g_slot,
-                    &c.g_nmax, &c.g_nmin, &c.g_k0, &c.x_send, &c.x_recv, &c.headtail, &c.lk_sendmap, &c.lk_recvmap};
+                    &c.g_nmax, &c.g_nmin, &c.g_k0, &c.p2p_eslot, &c.x_send, &c.x_recv, &c.headtail, &c.lk_sendmap, &c.lk_recvmap};
   for (DevBuf* b : bufs) b->release();
 }
 
@@ -123,7 +123,7 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
   Ctx& c = ctx->c;
   CK(cudaSetDevice(c.device));
   c.loaded = c.matched = c.detected = c.localized = false;
-  c.fused_used = false; c.tiles_ready = false;
+  c.fused_used = false; c.tiles_ready = false; c.xwait_pending = false;
   c.err.clear();
   if (topo->tp < 1 || topo->pp < 1 || topo->dp < 1 || topo->rank_order != 0) {
     c.err = "topology: tp, pp, dp must be >= 1 and rank_order 0";
@@ -488,6 +488,7 @@ scan_status general_match(Ctx& c) {
   c.launches += timed(c, "k_rank_prefix", [&] { return launch_rank_prefix(c); });
   c.tiles_ready = true;
   c.fused_used = false;
+  c.xwait_pending = false;
   if ((st = channels_and_buffers(c, false))) return st;
   c.launches += timed(c, "k_assign", [&] { return launch_assign(c); });
   c.launches += timed(c, "k_inst_reduce", [&] { return launch_inst_reduce(c); });
@@ -535,6 +536,7 @@ scan_status general_localize(Ctx& c) {
 // ---- the fused SPMD path (K9); returns 2 when the trace is not SPMD (caller falls back)
 scan_status fused_all(Ctx& c) {
   c.matched = c.detected = c.localized = false;
+  c.xwait_pending = false;
   scan_status st = prep_ws(c, false);
   if (st) return st;
   CK(c.ft_cols.ensure((uint64_t)FCOLS * c.n_ftiles * 4)); CK(c.ft_base.ensure((uint64_t)FCOLS * c.n_ftiles * 4));
@@ -577,6 +579,7 @@ scan_status fused_all(Ctx& c) {
   }
   c.localized = true;
   c.fused_used = true;
+  c.xwait_pending = true;
   return SCAN_OK;
 }
 
@@ -838,6 +841,12 @@ scan_status scan_export(scan_ctx* ctx, scan_output which, void* dst, uint64_t ds
   if (!c.matched) { c.err = "nothing to export before scan_match_collectives"; return SCAN_E_ORDER; }
   CK(cudaSetDevice(c.device));
   const cudaMemcpyKind kind = dst_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if ((which == SCAN_OUT_COMM_WAIT || which == SCAN_OUT_EV_WAIT) && c.xwait_pending && c.localized) {
+    launch_xwait_scatter(c);  // comm-order view of the cross-stage waits (once per analysis)
+    CK(cudaStreamSynchronize(c.stream));
+    CK(cudaGetLastError());
+    c.xwait_pending = false;
+  }
   OutDesc d;
   if (direct(c, which, d)) {
     if (stage_of(c) < d.stage) { c.err = "output not computed yet"; return SCAN_E_ORDER; }
@@ -885,6 +894,11 @@ const void* scan_output_device_ptr(scan_ctx* ctx, scan_output which) {
   OutDesc d;
   if (which != SCAN_OUT_COMM_INST && which != SCAN_OUT_COMM_WAIT && which != SCAN_OUT_SLOW_BITS) return nullptr;
   if (!direct(c, which, d) || stage_of(c) < d.stage) return nullptr;
+  if (which == SCAN_OUT_COMM_WAIT && c.xwait_pending) {
+    launch_xwait_scatter(c);
+    if (cudaStreamSynchronize(c.stream) != cudaSuccess) return nullptr;
+    c.xwait_pending = false;
+  }
   return (const uint8_t*)d.buf->p + d.off_bytes;
 }
 

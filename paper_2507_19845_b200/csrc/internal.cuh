@@ -130,6 +130,7 @@ struct Ctx {
   bool spmd = false;                     // every stage block is SPMD-compatible (checked at load)
   bool fused_used = false;               // results of the last analysis come from the fused path
   bool tiles_ready = false;              // general tile prefixes exist (needed by event-order exports)
+  bool xwait_pending = false;            // fused: cross-stage waits still in slot order (k_xwait_scatter on export)
   uint32_t FT = 0, FR = 0, n_ftiles = 0; // positions per fused tile, ranks per stage, fused tiles
   std::vector<uint32_t> h_st_tile0, h_st_npos;
   DevBuf st_tile0, st_npos, role_comm, role_slot, role_type, ncroles;
@@ -146,6 +147,7 @@ struct Ctx {
   DevBuf tile_stage;                     // [n_ftiles] stage of each fused tile (u8)
   DevBuf xbase;                          // [NCH+1] cross-stage instance index
   DevBuf lk_scratch;                     // link-median scratch for links above the shared-memory capacity
+  DevBuf p2p_eslot;                      // [n_p2p][2] wait-for edge column per P2P link direction
   uint64_t n_xinst = 0;
   // multi-GPU iteration-window shards (row A9, shard.cu); n_shards == 1: unsharded
   int n_shards = 1, shard = 0;
@@ -362,6 +364,7 @@ int launch_fused(Ctx& c);
 size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM);
 size_t fused_t_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM);
 int launch_cross_reduce(Ctx& c);
+int launch_xwait_scatter(Ctx& c);
 int launch_deferred(Ctx& c);
 int launch_wd_finish(Ctx& c);
 

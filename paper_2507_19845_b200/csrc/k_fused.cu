@@ -1362,36 +1362,64 @@ struct XArgs {
   const uint32_t* sdur; const uint8_t* skind; const uint32_t* sci; const uint32_t* sit; const uint32_t* p2p_pay;
   const uint8_t* p2p_warm; uint64_t p2p_slot0, p2p_inst0;
   uint4* rec; uint32_t* wait_c;
+  uint32_t* swait;  // = sdur: after the reduction a member slot holds that member's wait (instance order)
   const uint64_t* nbc_off; const uint32_t* nbc; const uint32_t* nbp; const uint32_t* nbp_n; uint64_t nnz_tot, nnz_c;
   unsigned long long* ew; unsigned long long* rk_sum; uint32_t wi; unsigned long long wait_margin;
   Counters* cnt;
+  const uint32_t* p2p_eslot;  // [n_p2p][2] edge column of src -> dst and dst -> src
+  int xb_smem;                // xbase staged in shared memory (NCH + 1 entries)
 };
 
-__device__ __forceinline__ void x_edge(const XArgs& a, uint32_t r, uint32_t L, uint32_t win, uint32_t wait) {
+// edge column of every P2P link direction (the search x_edge would do), once per analysis
+__global__ void k_p2p_eslot(uint32_t n_p2p, const uint32_t* psrc, const uint32_t* pdst, const uint64_t* nbc_off,
+                            const uint32_t* nbc, const uint32_t* nbp, const uint32_t* nbp_n, uint64_t nnz_c, uint32_t* out) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_p2p) return;
+  for (int q = 0; q < 2; ++q) {
+    const uint32_t r = q ? pdst[p] : psrc[p], L = q ? psrc[p] : pdst[p];
+    const uint64_t nb0 = nbc_off[r], nb1 = nbc_off[r + 1];
+    const uint32_t pc = lower_bound_u32(nbc + nb0, (uint32_t)(nb1 - nb0), L);
+    out[2 * p + q] = (uint32_t)((pc < nb1 - nb0 && nbc[nb0 + pc] == L)
+                                    ? nb0 + pc
+                                    : nnz_c + (uint64_t)r * PCAP + lower_bound_u32(nbp + (uint64_t)r * PCAP, nbp_n[r], L));
+  }
+}
+
+__device__ __forceinline__ void x_edge(const XArgs& a, uint32_t r, uint32_t L, uint32_t win, unsigned long long wait) {
   const uint64_t nb0 = a.nbc_off[r], nb1 = a.nbc_off[r + 1];
   uint64_t idx;
   const uint32_t pc = lower_bound_u32(a.nbc + nb0, (uint32_t)(nb1 - nb0), L);
   if (pc < nb1 - nb0 && a.nbc[nb0 + pc] == L) idx = nb0 + pc;
   else idx = a.nnz_c + (uint64_t)r * PCAP + lower_bound_u32(a.nbp + (uint64_t)r * PCAP, a.nbp_n[r], L);
-  atomicAdd(&a.ew[(uint64_t)win * a.nnz_tot + idx], (unsigned long long)wait);
+  atomicAdd(&a.ew[(uint64_t)win * a.nnz_tot + idx], wait);
 }
 
 __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
   if (*((volatile unsigned*)&a.cnt->overflow) & NOT_SPMD) return;  // fused results void: general path reruns
+  extern __shared__ unsigned long long xb_s[];
+  if (a.xb_smem) {
+    for (uint64_t q = threadIdx.x; q <= a.NCH; q += blockDim.x) xb_s[q] = a.xbase[q];
+    __syncthreads();
+  }
+  const uint64_t* XB = a.xb_smem ? reinterpret_cast<const uint64_t*>(xb_s) : a.xbase;
   uint32_t inc = 0, kmis = 0, pmis = 0;
   const uint32_t lane = lane_id();
   const uint64_t wstride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t wbase = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wbase < a.n_xinst; wbase += wstride) {
     const uint64_t xi = wbase + lane;
     const bool act = xi < a.n_xinst;
+    // channel of the warp's first instance (one search per warp); lanes past its end search alone
+    uint64_t ch0 = 0, end0 = 0;
+    if (lane == 0) { ch0 = upper_bound_u64(XB, a.NCH + 1, wbase) - 1; end0 = XB[ch0 + 1]; }
+    ch0 = __shfl_sync(0xFFFFFFFFu, ch0, 0);
+    end0 = __shfl_sync(0xFFFFFFFFu, end0, 0);
     uint64_t ch = 0, k = 0, i = 0;
     if (act) {
-      ch = upper_bound_u64(a.xbase, a.NCH + 1, xi) - 1;
-      k = xi - a.xbase[ch];
+      ch = xi < end0 ? ch0 : upper_bound_u64(XB, a.NCH + 1, xi) - 1;
+      k = xi - XB[ch];
       i = a.ch_base[ch] + k;
     }
     // one channel across the whole warp (the common case): its members are the same for every lane
-    const uint64_t ch0 = __shfl_sync(0xFFFFFFFFu, ch, 0);
     const bool uni = __all_sync(0xFFFFFFFFu, act && ch == ch0);
     const bool isp = ch >= a.n_comms;
     const uint32_t nm = isp ? 2u : (uint32_t)(a.coff[ch + 1] - a.coff[ch]);
@@ -1440,18 +1468,37 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
       a.rec[i] = make_uint4(dmin, dmax, last, flags | ((isp ? 0u : a.ccls[ch]) << 8));
     }
     if (uni) {
-      // aggregated per-member sums (members identical across lanes)
+      // aggregated per-member sums (members identical across lanes); the wait-for edge too when
+      // every contributing lane has the same target and window (always for a P2P link: the
+      // target is the other endpoint), else one atomic per lane
       for (uint32_t q = 0; q < nm; ++q) {
         unsigned long long w = 0, t = 0;
+        bool eg = false;
+        uint32_t ewin = 0, ewait = 0;
         if (act && (flags & SCAN_F_COMPLETE || present(q))) {
-          const uint32_t ci = a.sci[sb + q];
-          if (!valid) a.wait_c[ci] = 0;
+          if (!valid) a.swait[sb + q] = 0;
           else {
             const uint32_t m = member(q);
             const uint32_t wait = a.sdur[sb + q] - dmin;
-            a.wait_c[ci] = wait;
+            a.swait[sb + q] = wait;
             w = wait; t = dmin;
-            if (m != last && (unsigned long long)wait > a.wait_margin) x_edge(a, m, last, a.wi ? a.sit[sb + q] / a.wi : 0, wait);
+            if (m != last && (unsigned long long)wait > a.wait_margin) {
+              eg = true; ewait = wait; ewin = a.wi ? a.sit[sb + q] / a.wi : 0;
+            }
+          }
+        }
+        const unsigned em = __ballot_sync(0xFFFFFFFFu, eg);
+        if (em) {
+          const int L0 = __ffs(em) - 1;
+          const uint32_t tl = __shfl_sync(0xFFFFFFFFu, last, L0), tw = __shfl_sync(0xFFFFFFFFu, ewin, L0);
+          if (__all_sync(0xFFFFFFFFu, !eg || (last == tl && ewin == tw))) {
+            const unsigned long long ws = warp_sum_u64(eg ? (unsigned long long)ewait : 0ull);
+            if (lane == (uint32_t)L0) {
+              if (isp) atomicAdd(&a.ew[(uint64_t)tw * a.nnz_tot + a.p2p_eslot[2 * (ch - a.n_comms) + q]], ws);
+              else x_edge(a, member(q), tl, tw, ws);
+            }
+          } else if (eg) {
+            x_edge(a, member(q), last, ewin, ewait);
           }
         }
         w = warp_sum_u64(w); t = warp_sum_u64(t);
@@ -1464,11 +1511,10 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
     } else if (act) {
       for (uint32_t q = 0; q < nm; ++q) {
         if (!(flags & SCAN_F_COMPLETE) && !present(q)) continue;
-        const uint32_t ci = a.sci[sb + q];
-        if (!valid) { a.wait_c[ci] = 0; continue; }
+        if (!valid) { a.swait[sb + q] = 0; continue; }
         const uint32_t m = member(q);
         const uint32_t wait = a.sdur[sb + q] - dmin;
-        a.wait_c[ci] = wait;
+        a.swait[sb + q] = wait;
         if (wait) atomicAdd(&a.rk_sum[a.W + m], (unsigned long long)wait);
         if (dmin) atomicAdd(&a.rk_sum[2 * a.W + m], (unsigned long long)dmin);
         if (m != last && (unsigned long long)wait > a.wait_margin) x_edge(a, m, last, a.wi ? a.sit[sb + q] / a.wi : 0, wait);
@@ -1490,12 +1536,67 @@ int launch_cross_reduce(Ctx& c) {
           c.r_nkeys.as<uint32_t>(), c.r_keys.as<uint32_t>(), c.r_cnt.as<uint32_t>(), c.sdur.as<uint32_t>(),
           c.skind.as<uint8_t>(), c.sci.as<uint32_t>(), c.sit.as<uint32_t>(), c.p2p_pay.as<uint32_t>(),
           c.p2p_warm.as<uint8_t>(), c.p2p_slot0, c.p2p_inst0, c.inst_rec.as<uint4>(), c.wait_c.as<uint32_t>(),
-          c.nbc_off.as<uint64_t>(), c.nbc.as<uint32_t>(), c.nbp.as<uint32_t>(), c.nbp_n.as<uint32_t>(),
+          c.sdur.as<uint32_t>(), c.nbc_off.as<uint64_t>(), c.nbc.as<uint32_t>(), c.nbp.as<uint32_t>(), c.nbp_n.as<uint32_t>(),
           c.nnz_c + (uint64_t)c.W * PCAP, c.nnz_c, c.ewc.as<unsigned long long>(), c.rk_sum.as<unsigned long long>(),
-          c.dcfg.window_iters, (unsigned long long)c.lcfg.wait_margin_ns, c.counters.as<Counters>()};
+          c.dcfg.window_iters, (unsigned long long)c.lcfg.wait_margin_ns, c.counters.as<Counters>(),
+          c.p2p_eslot.as<uint32_t>(), 0};
   if (c.n_xinst == 0) return 0;
-  unsigned blocks = (unsigned)std::min<uint64_t>((c.n_xinst + 255) / 256, 148ull * 16);
-  k_cross_reduce<<<blocks, 256, 0, c.stream>>>(a);
+  int n = 0;
+  if (c.n_p2p) {
+    if (c.p2p_eslot.ensure(2 * c.n_p2p * 4) != cudaSuccess) return 0;
+    a.p2p_eslot = c.p2p_eslot.as<uint32_t>();
+    k_p2p_eslot<<<(unsigned)((c.n_p2p + 255) / 256), 256, 0, c.stream>>>(
+        (uint32_t)c.n_p2p, c.ch_nsend.as<uint32_t>() + c.n_p2p, c.ch_nrecv.as<uint32_t>() + c.n_p2p, c.nbc_off.as<uint64_t>(),
+        c.nbc.as<uint32_t>(), c.nbp.as<uint32_t>(), c.nbp_n.as<uint32_t>(), c.nnz_c, c.p2p_eslot.as<uint32_t>());
+    ++n;
+  }
+  const size_t xsm = (c.NCH + 1) * 8;
+  a.xb_smem = xsm <= 48 * 1024 ? 1 : 0;
+  unsigned blocks = (unsigned)std::min<uint64_t>((c.n_xinst + 255) / 256, 148ull * 8);
+  k_cross_reduce<<<blocks, 256, a.xb_smem ? xsm : 0, c.stream>>>(a);
+  return n + 1;
+}
+
+// Comm-order view of the cross-stage members' waits (COMM_WAIT / EV_WAIT exports): k_cross_reduce
+// leaves each member's wait in its slot (instance order, coalesced); this scatters them to
+// wait_c[comm index] once, on the first export that needs them. A sparse update of the comm-order
+// array costs a sector read + write per member, which the analysis itself does not pay.
+__global__ void __launch_bounds__(256) k_xwait_scatter(XArgs a) {
+  for (uint64_t xi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; xi < a.n_xinst; xi += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t ch = upper_bound_u64(a.xbase, a.NCH + 1, xi) - 1;
+    const uint64_t k = xi - a.xbase[ch];
+    const bool isp = ch >= a.n_comms;
+    const uint32_t nm = isp ? 2u : (uint32_t)(a.coff[ch + 1] - a.coff[ch]);
+    const uint64_t sb = a.ch_slot[ch] + k * nm;
+    const bool complete = k < a.ch_nmin[ch];
+    for (uint32_t q = 0; q < nm; ++q) {
+      bool present = complete;
+      if (!present) {
+        if (isp) {
+          present = (q == 0 ? a.nsend[ch - a.n_comms] : a.nrecv[ch - a.n_comms]) > k;
+        } else {
+          const uint32_t m = a.cmem[a.coff[ch] + q];
+          const uint32_t C = a.r_nkeys[m];
+          const uint32_t p = lower_bound_u32(a.r_keys + (uint64_t)m * RCAP, C, (uint32_t)ch);
+          present = p < C && a.r_keys[(uint64_t)m * RCAP + p] == (uint32_t)ch && a.r_cnt[(uint64_t)m * RCAP + p] > k;
+        }
+      }
+      if (present) a.wait_c[a.sci[sb + q]] = a.swait[sb + q];
+    }
+  }
+}
+
+int launch_xwait_scatter(Ctx& c) {
+  if (c.n_xinst == 0) return 0;
+  XArgs a{c.n_xinst, c.NCH, c.n_comms, c.W, c.xbase.as<uint64_t>(), c.ch_base.as<uint64_t>(), c.ch_slot.as<uint64_t>(), c.ch_nmin.as<uint32_t>(),
+          c.coff.as<uint64_t>(), c.cmem.as<uint32_t>(), c.ccls.as<uint8_t>(), c.ch_nsend.as<uint32_t>(),
+          c.ch_nrecv.as<uint32_t>(), c.ch_nsend.as<uint32_t>() + c.n_p2p, c.ch_nrecv.as<uint32_t>() + c.n_p2p,
+          c.r_nkeys.as<uint32_t>(), c.r_keys.as<uint32_t>(), c.r_cnt.as<uint32_t>(), c.sdur.as<uint32_t>(),
+          c.skind.as<uint8_t>(), c.sci.as<uint32_t>(), c.sit.as<uint32_t>(), c.p2p_pay.as<uint32_t>(),
+          c.p2p_warm.as<uint8_t>(), c.p2p_slot0, c.p2p_inst0, c.inst_rec.as<uint4>(), c.wait_c.as<uint32_t>(),
+          c.sdur.as<uint32_t>()};
+  unsigned blocks = (unsigned)std::min<uint64_t>((c.n_xinst + 255) / 256, 148ull * 8);
+  k_xwait_scatter<<<blocks, 256, 0, c.stream>>>(a);
   return 1;
 }
 

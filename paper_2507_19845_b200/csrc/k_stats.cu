@@ -414,7 +414,7 @@ __device__ __forceinline__ unsigned long long ratio_key(uint32_t p, uint32_t t) 
   return (unsigned long long)__double_as_longlong((double)p / (double)t);  // positive: bit order = value order
 }
 
-constexpr int LM_NT = 256;
+constexpr int LM_NT = 512;  // 2 CTAs x 16 warps per SM with the 96 KB sample buffer
 constexpr uint32_t LM_CAP = 8192;  // samples per link held in shared memory (larger links use global scratch)
 
 // warp 0 finds the bin holding rank tgt in a 256-bin histogram: returns (bin, count below it)
@@ -433,6 +433,13 @@ __device__ __forceinline__ void hist_find(const uint32_t* hist, uint32_t tgt, ui
   }
   bin = L * 8 + __shfl_sync(0xFFFFFFFFu, b, L);
   below = __shfl_sync(0xFFFFFFFFu, acc, L);
+}
+
+// shared 256-bin histogram add with the lanes of a warp that share a bin combined (bin 256 = none);
+// samples of one link cluster in a few bins in the top radix passes
+__device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t bin) {
+  const unsigned peers = __match_any_sync(0xFFFFFFFFu, bin);
+  if (bin < 256u && (lane_id() == (uint32_t)(__ffs(peers) - 1))) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
 }
 
 __global__ void __launch_bounds__(LM_NT) k_link_median(LKArgs a) {
@@ -506,13 +513,18 @@ __global__ void __launch_bounds__(LM_NT) k_link_median(LKArgs a) {
   if (threadIdx.x == 0) { s_prefix = 0; s_target = (nu - 1) / 2; }
   __syncthreads();
   for (int shift = 56; shift >= 0; shift -= 8) {
-    hist[threadIdx.x] = 0;
+    if (threadIdx.x < 256) hist[threadIdx.x] = 0;
     __syncthreads();
     const unsigned long long pre = s_prefix;
     const unsigned long long hmask = shift == 56 ? 0ull : (~0ull << (shift + 8));
-    for (uint32_t i = threadIdx.x; i < nu; i += LM_NT) {
-      const unsigned long long key = sk[i];
-      if ((key & hmask) == pre) atomicAdd(&hist[(key >> shift) & 0xFFu], 1u);
+    for (uint32_t ib = 0; ib < nu; ib += LM_NT) {  // whole warps per round: lanes with one bin add once
+      const uint32_t i = ib + threadIdx.x;
+      uint32_t bin = 256u;
+      if (i < nu) {
+        const unsigned long long key = sk[i];
+        if ((key & hmask) == pre) bin = (uint32_t)(key >> shift) & 0xFFu;
+      }
+      hist_add(hist, bin);
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -545,11 +557,15 @@ __global__ void __launch_bounds__(LM_NT) k_link_median(LKArgs a) {
       // one exact ratio: the tg-th smallest instance id of the tie group (radix select on ids)
       uint32_t tgt = tg, pre = 0;
       for (int shift = 24; shift >= 0; shift -= 8) {
-        hist[threadIdx.x] = 0;
+        if (threadIdx.x < 256) hist[threadIdx.x] = 0;
         __syncthreads();
         const uint32_t hmask = shift == 24 ? 0u : (0xFFFFFFFFu << (shift + 8));
-        for (uint32_t i = threadIdx.x; i < nu; i += LM_NT)
-          if (sk[i] == K && (si[i] & hmask) == pre) atomicAdd(&hist[(si[i] >> shift) & 0xFFu], 1u);
+        for (uint32_t ib = 0; ib < nu; ib += LM_NT) {
+          const uint32_t i = ib + threadIdx.x;
+          uint32_t bin = 256u;
+          if (i < nu && sk[i] == K && (si[i] & hmask) == pre) bin = (si[i] >> shift) & 0xFFu;
+          hist_add(hist, bin);
+        }
         __syncthreads();
         if (threadIdx.x < 32) {
           uint32_t bin, below;
@@ -782,11 +798,11 @@ int launch_verdict_walk(Ctx& c) {
            c.scratch.as<int32_t>(), c.scratch.as<uint32_t>() + (uint64_t)c.NW * c.W,
            c.scratch.as<uint32_t>() + 2ull * c.NW * c.W, c.scratch.as<uint32_t>() + 2ull * c.NW * c.W + c.NW,
            c.counters.as<Counters>()};
+  const uint64_t items = (uint64_t)c.NW * c.W;
   int nb = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_walk, 256, 0);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-  const uint64_t items = (uint64_t)c.NW * c.W;
   int blocks = (int)std::min<uint64_t>((items + 255) / 256, (uint64_t)std::max(1, nb) * sms);
   blocks = std::max(blocks, 1);
   void* args[] = {&a};

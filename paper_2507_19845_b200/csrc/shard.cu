@@ -227,7 +227,7 @@ scan_status allgather_dev(Ctx& c, size_t n, std::vector<uint32_t>& all) {
 
 scan_status sharded_all(Ctx& c) {
   c.matched = c.detected = c.localized = false;
-  c.fused_used = false; c.tiles_ready = false;
+  c.fused_used = false; c.tiles_ready = false; c.xwait_pending = false;
   const uint32_t G = (uint32_t)c.n_shards, g = (uint32_t)c.shard, nc = c.n_comms;
   const uint64_t W = c.W;
   ncclComm_t comm = (ncclComm_t)c.nccl;
@@ -533,6 +533,7 @@ scan_status sharded_all(Ctx& c) {
   }
   c.matched = c.detected = c.localized = true;
   c.fused_used = true;
+  c.xwait_pending = true;
   return SCAN_OK;
 }
 
