@@ -103,16 +103,18 @@ _lib = None
 
 
 def library_path() -> str:
-    return _build.SO
+    """The in-tree libmegascan.so (MEGASCAN_LIB may name another in-tree build, for A/B runs)."""
+    return os.environ.get("MEGASCAN_LIB") or _build.SO
 
 
 def _load_lib():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(_build.SO) or _build.stale():
+    path = library_path()
+    if path == _build.SO and (not os.path.exists(_build.SO) or _build.stale()):
         _build.build()
-    lib = ctypes.CDLL(_build.SO)
+    lib = ctypes.CDLL(path)
     P = ctypes.c_void_p
     lib.scan_create.argtypes = [ctypes.POINTER(P), ctypes.c_int, P]
     lib.scan_destroy.argtypes = [P]

@@ -12,6 +12,7 @@ SO = os.path.join(HERE, "libmegascan.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr"]
+FLAGS += os.environ.get("MS_NVCC_EXTRA", "").split()  # experiments only (e.g. -DMS_FT_NT=256)
 
 
 def nccl_paths() -> tuple[str, str]:

@@ -264,11 +264,13 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
       c.fused_t = tp_pow2 && R <= 256 && c.fused_variant != 0;
       uint32_t T = (16384u / R) / 32u * 32u;
       T = std::max(64u, std::min(1024u, T));
+      if (T < 128) T = 64;  // below 128 positions the load lane mapping needs a power of two
       // two CTAs per SM: keep the fused kernel's shared memory under ~110 KB
       auto smem = [&](uint32_t t) {
         return c.fused_t ? fused_t_smem_bytes(t, R, topo->tp, topo->dp, ncrm) : fused_smem_bytes(t, R, topo->tp, topo->dp, ncrm);
       };
-      while (T > 64 && smem(T) > 110u * 1024u) T -= 32;
+      const size_t cap = c.fused_t ? fused_t_smem_cap() : 110u * 1024u;  // 2 (generic) / FT_MINB (transposed) CTAs per SM
+      while (T > 32 && smem(T) > cap) T = T > 128 ? T - 32 : T / 2;  // below 128: powers of two (load lane mapping)
       c.NCRM = ncrm;
       if ((st = upload(c, c.eidx, eidx))) return st;
       uint32_t nt = 0;

@@ -363,6 +363,7 @@ int launch_fused_census(Ctx& c);
 int launch_fused(Ctx& c);
 size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM);
 size_t fused_t_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM);
+size_t fused_t_smem_cap();
 int launch_cross_reduce(Ctx& c);
 int launch_xwait_scatter(Ctx& c);
 int launch_deferred(Ctx& c);

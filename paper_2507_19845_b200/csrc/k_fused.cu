@@ -284,11 +284,18 @@ struct FusedArgs {
   uint32_t slow_num, slow_den; unsigned long long slow_margin;
   uint32_t wi, classes, mode; unsigned long long late_margin, wait_margin; int want_ref;
   uint32_t it_off;  // global iteration of this shard's first iteration (0 unsharded)
+  unsigned long long wi_m;  // ceil(2^64 / wi) for wi > 1: window = umulhi64(iteration, wi_m), exact for 32-bit iterations
   Counters* cnt;
   // byte offsets of the transposed kernel's shared-memory arrays (host-computed, fused_t_layout)
   uint32_t o_rcb, o_coffr, o_sinst, o_sbits, o_sedge, o_rcs, o_rsum, o_gsum, o_sjoin, o_slate, o_rslow, o_pa, o_pb, o_vd,
-      o_pk, o_lst, o_cl, o_pcode;
+      o_pk, o_lst, o_cl, o_pcode, o_cinf, o_citp;
 };
+
+// window of a (global) iteration, R18: floor(it / wi) by a 64-bit reciprocal, m = ceil(2^64 / wi):
+// it*m / 2^64 = it/wi + e with 0 <= e < it/2^64 < 2^-32 <= 1/wi, so the floor is exact
+__device__ __forceinline__ uint32_t win_of(const FusedArgs& a, uint32_t it) {
+  return a.wi == 0 ? 0u : (a.wi == 1 ? it : (uint32_t)__umul64hi((unsigned long long)it, a.wi_m));
+}
 
 constexpr int F_NT = 512;
 
@@ -404,7 +411,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   const uint32_t itg0 = it0 + a.it_off;  // global iteration: windows, sit, p2p_iter
   const uint32_t jp0 = a.ft_base[(uint64_t)(ROLES + 3) * n + tile];
   const uint32_t wb = j0 >> 5;
-  const uint32_t w_tile = a.wi ? itg0 / a.wi : 0;
+  const uint32_t w_tile = win_of(a, itg0);
   const uint32_t ncr = a.ncroles[s];
   if (tid < ROLES) kbase[tid] = a.ft_base[(uint64_t)tid * n + tile];
   if (tid < 4) nlist[tid] = 0;
@@ -585,7 +592,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
         const uint32_t gi = istp ? g : DP + g;
         add64_lohi(&gsum[gi], &gsum[DP + TP + gi], dmin);
       }
-      const uint32_t win = a.wi ? (itg0 + (B & 1023u)) / a.wi : 0;
+      const uint32_t win = win_of(a, itg0 + (B & 1023u));
       const bool elig = (a.classes >> (cls - 1)) & 1u;
       const bool late_ok = nat == 1 && (unsigned long long)(dmax - dmin) > a.late_margin;
       const uint32_t eslot = istp ? ls : TP + ls;  // partner slot of the last arriver
@@ -709,7 +716,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
   }
   // stage-1 counters per (window, rank): total = compute positions of the tile, slow = its slow bits
   const uint32_t it_last = itg0 + (np ? (pb[np - 1] & 1023u) : 0u);
-  const bool one_window = !a.wi || (itg0 / a.wi == it_last / a.wi);
+  const bool one_window = !a.wi || (win_of(a, itg0) == win_of(a, it_last));
   if (P >= 2 && nc) {
     if (one_window) {
       for (uint32_t row = tid; row < R; row += F_NT) {
@@ -722,7 +729,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
     } else {
       for (uint32_t i = tid; i < R * nc; i += F_NT) {
         const uint32_t row = i / nc, p = lst[i - row * nc], r = sbase + row;
-        const uint32_t win = (itg0 + (pb[p] & 1023u)) / a.wi;
+        const uint32_t win = win_of(a, itg0 + (pb[p] & 1023u));
         const uint32_t j = j0 + (pa[p] & 1023u);
         atomicAdd(&a.wd_total[(uint64_t)win * a.W + r], 1u);
         if ((sbits[row * SW + (j >> 5) - wb] >> (j & 31)) & 1u) atomicAdd(&a.wd_slow[(uint64_t)win * a.W + r], 1u);
@@ -759,7 +766,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
     if (dpos >= 0) {
       const uint32_t p = (uint32_t)dpos;
       const uint32_t ty = (pb[p] >> 25) & 7u;
-      di[0] = j0 + (pa[p] & 1023u); di[1] = jp0; di[2] = a.wi ? (itg0 + (pb[p] & 1023u)) / a.wi : 0; di[3] = 1u | (ty << 8);
+      di[0] = j0 + (pa[p] & 1023u); di[1] = jp0; di[2] = win_of(a, itg0 + (pb[p] & 1023u)); di[3] = 1u | (ty << 8);
     } else {
       di[3] = 0;
     }
@@ -773,7 +780,10 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
 // register; a DP group (rows with equal row mod TP) is every lane with equal l mod TP, so both
 // reductions are butterflies of shuffles. The load pass transposes in registers and verifies the
 // kind_op and comm columns while the data is in registers.
-constexpr int FT_NT = 512, FT_NW = FT_NT / 32, NRLM = 8;
+#ifndef MS_FT_NT
+#define MS_FT_NT 512
+#endif
+constexpr int FT_NT = MS_FT_NT, FT_NW = FT_NT / 32, NRLM = 8, FT_MINB = 1024 / FT_NT;  // 32 warps per SM
 
 template <int P>
 __device__ __forceinline__ void loo_group(const FusedArgs& a, const uint32_t* col, uint32_t tp, uint32_t TP, uint32_t DP, uint32_t j,
@@ -825,7 +835,7 @@ __device__ __forceinline__ void loo_dispatch(const FusedArgs& a, const uint32_t*
 }
 
 template <int P, int NRB>
-__global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
+__global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const uint32_t T = a.T, R = a.R, TP = (uint32_t)a.TP, DP = (uint32_t)a.DP, G = a.G;
   const uint32_t SW = T / 32 + 2, E = TP + DP, NCRM = a.NCRM, RP = R + 1;
@@ -852,6 +862,10 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
   uint16_t* lst = reinterpret_cast<uint16_t*>(smem_raw + a.o_lst);
   uint16_t* cl = reinterpret_cast<uint16_t*>(smem_raw + a.o_cl);
   uint8_t* pcode = reinterpret_cast<uint8_t*>(smem_raw + a.o_pcode);
+  // per comm position (indexed by its in-tile comm index): p | class << 14 | deferred << 16 | role << 17,
+  // occurrence index k, compute index j of the position, j of the previous comm position; global iteration
+  uint4* cinf = reinterpret_cast<uint4*>(smem_raw + a.o_cinf);
+  uint32_t* citp = reinterpret_cast<uint32_t*>(smem_raw + a.o_citp);
   __shared__ uint32_t kbase[ROLES];
   __shared__ uint32_t nlist[4];
   __shared__ int32_t dpos;
@@ -872,7 +886,7 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
   const uint32_t itg0 = it0 + a.it_off;  // global iteration: windows, sit, p2p_iter
   const uint32_t jp0 = a.ft_base[(uint64_t)(ROLES + 3) * n + tile];
   const uint32_t wb = j0 >> 5;
-  const uint32_t w_tile = a.wi ? itg0 / a.wi : 0;
+  const uint32_t w_tile = win_of(a, itg0);
   const uint32_t ncr = a.ncroles[s];
 
   // ---- (0) tables and template info
@@ -905,9 +919,14 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
     if (isc) {
       vd[p] = 0;
     } else {
-      cl[(A >> 10) & 1023u] = (uint16_t)(p | ((li - 1u) << 14));
+      const uint32_t mr = (A >> 10) & 1023u;
+      cl[mr] = (uint16_t)(p | ((li - 1u) << 14));
       vd[p] = role < 16 ? (1u | (role << 2)) : (2u | ((uint32_t)(((int)(role & 7u) - 4) * (int)R + 0x100000) << 2));
-      if (((A >> 30) & 1u) && li < 3 && a.mode == 0 && jp0 < j0) dpos = (int32_t)p;
+      const bool def = ((A >> 30) & 1u) && li < 3 && a.mode == 0 && jp0 < j0;
+      if (def) dpos = (int32_t)p;
+      cinf[mr] = make_uint4(p | ((li - 1u) << 14) | (def ? 1u << 16 : 0u) | (role << 17), kbase[role] + ((B >> 10) & 1023u),
+                            j0 + (A & 1023u), ((A >> 30) & 1u) ? jp0 : j0 + ((A >> 20) & 1023u));
+      citp[mr] = itg0 + (B & 1023u);
     }
   }
   __syncthreads();
@@ -951,16 +970,19 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
         }
       }
     };
-    for (uint32_t pq = 0; pq < np; pq += 128) {
-      const uint32_t pbase = pq + lane * 4;
+    // a warp covers 4*lpr positions of 32/lpr rows (lpr = T/4 lanes per row when T < 128)
+    const uint32_t lpr = T >= 128 ? 32u : T / 4u, rpw = 32u / lpr, rstep = FT_NW * rpw;
+    const uint32_t rsub = lane / lpr, lpos = lane % lpr;
+    for (uint32_t pq = 0; pq < np; pq += 4 * lpr) {
+      const uint32_t pbase = pq + lpos * 4;
       const bool pin = pbase < np;
-      uint32_t row = wid;
-      for (; row + FT_NW < R; row += 2 * FT_NW) {  // two rows per iteration
+      uint32_t row = wid * rpw + rsub;
+      for (; row + rstep < R; row += 2 * rstep) {  // two rows per iteration
         uint32_t ka0, ka1, kb0, kb1, cma[4], cmb[4], dua[4], dub[4];
-        if (pin) { load4(row, pbase, ka0, ka1, cma, dua); load4(row + FT_NW, pbase, kb0, kb1, cmb, dub); }
-        if (pin) { check_store(row, pbase, ka0, ka1, cma, dua); check_store(row + FT_NW, pbase, kb0, kb1, cmb, dub); }
+        if (pin) { load4(row, pbase, ka0, ka1, cma, dua); load4(row + rstep, pbase, kb0, kb1, cmb, dub); }
+        if (pin) { check_store(row, pbase, ka0, ka1, cma, dua); check_store(row + rstep, pbase, kb0, kb1, cmb, dub); }
       }
-      for (; row < R; row += FT_NW) {
+      for (; row < R; row += rstep) {
         uint32_t ka0, ka1, cma[4], dua[4];
         if (pin) { load4(row, pbase, ka0, ka1, cma, dua); check_store(row, pbase, ka0, ka1, cma, dua); }
       }
@@ -1013,16 +1035,14 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
   const uint32_t ncm = nlist[1] + nlist[2] + nlist[3];
   for (uint32_t un = wid; un < ncm * NRB; un += FT_NW) {  // unit = (comm position, row block)
     const uint32_t jj = un / NRB, kb = un - jj * NRB;
-    const uint32_t cv = cl[jj];
-    const uint32_t p = cv & 0x3FFFu, cls = cv >> 14;  // 0 TP, 1 DP, 2 cross
+    const uint4 cd = cinf[jj];
+    const uint32_t p = cd.x & 0x3FFFu, cls = (cd.x >> 14) & 3u;  // 0 TP, 1 DP, 2 cross
     if (cls == 1 && kb != 0) continue;  // a DP group spans every row block: one unit handles it
-    const uint32_t A = pa[p], B = pb[p];
-    const uint32_t role = (B >> 20) & 31u;
-    const uint32_t krel = (B >> 10) & 1023u;
-    const uint32_t itp = itg0 + (B & 1023u);
+    const uint32_t role = (cd.x >> 17) & 31u;
+    const uint32_t itp = citp[jj];
     uint32_t* col = sd + p * RP;
     if (cls == 2) {
-      const uint32_t kk = kbase[role] + krel;
+      const uint32_t kk = cd.y;
       {
         const uint32_t row = lane + 32 * kb;
         if (row >= R) continue;
@@ -1046,7 +1066,7 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
         const uint64_t e = rbase + (uint64_t)row * npos + p0 + p;
         a.sdur[si] = col[row];
         a.skind[si] = (uint8_t)(pk[p] & 7u);
-        a.sci[si] = (uint32_t)(coffr[row] + m0 + ((A >> 10) & 1023u));
+        a.sci[si] = (uint32_t)(coffr[row] + m0 + jj);
         a.sit[si] = itp;
         col[row] = (uint32_t)inst;  // cross positions: the tile now holds the instance id
         if (role >= 16) {
@@ -1060,14 +1080,14 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
       continue;
     }
     const bool istp = cls == 0;
-    const uint32_t win = a.wi ? itp / a.wi : 0;
+    const uint32_t win = win_of(a, itp);
     const uint32_t clsid = istp ? 1u : 2u;
     const bool elig = (a.classes >> (clsid - 1)) & 1u;
-    const bool isdef = (int32_t)p == dpos;
+    const bool isdef = (cd.x >> 16) & 1u;
     const bool chk = elig && (a.mode || tslow || isdef);
-    const uint32_t jp = j0 + (A & 1023u);
-    const uint32_t jprev = ((A >> 30) & 1u) ? jp0 : j0 + ((A >> 20) & 1023u);
-    const uint32_t kinst = kbase[role] + krel;
+    const uint32_t jp = cd.z;
+    const uint32_t jprev = cd.w;
+    const uint32_t kinst = cd.y;
     // one group instance: min / max / last arriver (lowest slot with the min) / tie count, then the
     // members' waits, wait-for edges and stage-2 counters
     auto apply = [&](uint32_t row, uint32_t d, uint32_t mn, uint32_t mx, uint32_t lastrow, uint32_t slot, uint32_t g,
@@ -1193,7 +1213,7 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
   __syncthreads();
   // stage-1 counters per (window, rank)
   const uint32_t it_last = itg0 + (np ? (pb[np - 1] & 1023u) : 0u);
-  const bool one_window = !a.wi || (itg0 / a.wi == it_last / a.wi);
+  const bool one_window = !a.wi || (win_of(a, itg0) == win_of(a, it_last));
   if (DP >= 2 && nc) {
     if (one_window) {
       for (uint32_t row = tid; row < R; row += FT_NT) {
@@ -1206,7 +1226,7 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
     } else {
       for (uint32_t i = tid; i < R * nc; i += FT_NT) {
         const uint32_t row = i / nc, p = lst[i - row * nc], r = sbase + row;
-        const uint32_t win = (itg0 + (pb[p] & 1023u)) / a.wi;
+        const uint32_t win = win_of(a, itg0 + (pb[p] & 1023u));
         const uint32_t j = j0 + (pa[p] & 1023u);
         atomicAdd(&a.wd_total[(uint64_t)win * a.W + r], 1u);
         if ((sbits[row * SW + (j >> 5) - wb] >> (j & 31)) & 1u) atomicAdd(&a.wd_slow[(uint64_t)win * a.W + r], 1u);
@@ -1244,7 +1264,7 @@ __global__ void __launch_bounds__(FT_NT, 2) k_fused_t(FusedArgs a) {
     if (dpos >= 0) {
       const uint32_t p = (uint32_t)dpos;
       const uint32_t ty = (pb[p] >> 25) & 7u;
-      di[0] = j0 + (pa[p] & 1023u); di[1] = jp0; di[2] = a.wi ? (itg0 + (pb[p] & 1023u)) / a.wi : 0; di[3] = 1u | (ty << 8);
+      di[0] = j0 + (pa[p] & 1023u); di[1] = jp0; di[2] = win_of(a, itg0 + (pb[p] & 1023u)); di[3] = 1u | (ty << 8);
     } else {
       di[3] = 0;
     }
@@ -1262,13 +1282,18 @@ static size_t fused_t_layout(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, u
   const uint32_t o_slate = take((size_t)R * 4, 4), o_rslow = take((size_t)R * 4, 4), o_pa = take((size_t)T * 4, 16);
   const uint32_t o_pb = take((size_t)T * 4, 16), o_vd = take((size_t)T * 4, 16), o_pk = take((size_t)T * 2, 16);
   const uint32_t o_lst = take((size_t)T * 8, 4), o_cl = take((size_t)T * 2, 4), o_pcode = take((size_t)T, 4);
+  const uint32_t o_cinf = take((size_t)T * 16, 16), o_citp = take((size_t)T * 4, 4);
   if (a) {
     a->o_rcb = o_rcb; a->o_coffr = o_coffr; a->o_sinst = o_sinst; a->o_sbits = o_sbits; a->o_sedge = o_sedge; a->o_rcs = o_rcs;
     a->o_rsum = o_rsum; a->o_gsum = o_gsum; a->o_sjoin = o_sjoin; a->o_slate = o_slate; a->o_rslow = o_rslow; a->o_pa = o_pa;
     a->o_pb = o_pb; a->o_vd = o_vd; a->o_pk = o_pk; a->o_lst = o_lst; a->o_cl = o_cl; a->o_pcode = o_pcode;
+    a->o_cinf = o_cinf; a->o_citp = o_citp;
   }
   return (off + 15) & ~size_t(15);
 }
+
+// shared-memory budget per CTA so that FT_MINB CTAs of the transposed kernel fit on one SM
+size_t fused_t_smem_cap() { return (size_t)220 * 1024 / FT_MINB; }
 
 size_t fused_t_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM) {
   return fused_t_layout(T, R, TP, DP, NCRM, nullptr);
@@ -1312,6 +1337,7 @@ int launch_fused(Ctx& c) {
   a.slow_num = c.dcfg.slow_num; a.slow_den = c.dcfg.slow_den; a.slow_margin = c.dcfg.slow_margin_ns;
   a.wi = c.dcfg.window_iters; a.classes = c.lcfg.stage2_classes; a.mode = c.lcfg.stage2_mode;
   a.it_off = c.it_off;
+  a.wi_m = c.dcfg.window_iters > 1 ? (~0ull / c.dcfg.window_iters) + 1ull : 0ull;
   a.late_margin = c.lcfg.late_margin_ns; a.wait_margin = c.lcfg.wait_margin_ns; a.want_ref = c.dcfg.want_ref ? 1 : 0;
   a.cnt = c.counters.as<Counters>();
   if (c.fused_t) {
