@@ -70,7 +70,7 @@ static void release_all(Ctx& c) {
                     &c.st_tile0, &c.st_npos, &c.role_comm, &c.role_slot, &c.role_type, &c.ncroles, &c.ft_cols,
                     &c.ft_base, &c.ft_last, &c.st_tot, &c.sci, &c.sit, &c.dlate, &c.dinfo, &c.ft_posA, &c.ft_posB,
                     &c.ft_posK, &c.eidx, &c.tile_stage, &c.xbase, &c.lk_scratch, &c.g_base, &c.g_slot,
-                    &c.g_nmax, &c.g_nmin, &c.g_k0, &c.p2p_eslot, &c.x_send, &c.x_recv, &c.headtail, &c.lk_sendmap, &c.lk_recvmap};
+                    &c.g_nmax, &c.g_nmin, &c.g_k0, &c.p2p_eslot, &c.x_send, &c.x_recv, &c.x_recv2, &c.x_ep, &c.x_stage, &c.headtail, &c.lk_sendmap, &c.lk_recvmap};
   for (DevBuf* b : bufs) b->release();
 }
 

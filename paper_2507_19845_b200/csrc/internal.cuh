@@ -159,7 +159,10 @@ struct Ctx {
   std::vector<uint8_t> h_ccls;           // host copy of the stage-2 class per comm
   std::vector<uint64_t> h_coff;          // host copy of the comm offsets
   uint64_t g_N = 0, g_ncomm = 0, g_ncomp = 0;  // job-wide totals (sharded)
-  DevBuf x_send, x_recv, headtail, lk_sendmap, lk_recvmap;
+  DevBuf x_send, x_recv, x_recv2, x_ep, x_stage, headtail, lk_sendmap, lk_recvmap;
+  void* h_pin = nullptr;                 // pinned host scratch (exchange read-backs, table staging)
+  size_t h_pin_cap = 0;
+  cudaEvent_t ev_x1 = nullptr, ev_x2 = nullptr;
   // optional per-kernel timing
   bool timing = false;
   struct Pending { int k; cudaEvent_t a, b; };
@@ -353,6 +356,7 @@ int launch_links(Ctx& c);
 int launch_link_median(Ctx& c);
 int launch_link_flags(Ctx& c);
 int launch_p2p_counts(Ctx& c);
+int launch_p2p_counts_to(Ctx& c, uint32_t* nsend, uint32_t* nrecv, uint32_t* psrc, uint32_t* pdst);
 int launch_verdict_walk(Ctx& c);
 // exports
 int launch_expand_events(Ctx& c, scan_output which, void* dst);

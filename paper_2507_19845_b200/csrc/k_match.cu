@@ -470,13 +470,17 @@ __global__ void __launch_bounds__(RP_NT) k_cross_index(uint32_t n_comms, uint64_
 }
 
 // P2P member counts only (the shard path builds the channel tables on the host after its exchange)
-int launch_p2p_counts(Ctx& c) {
-  if (!c.n_p2p) return 0;
+int launch_p2p_counts_to(Ctx& c, uint32_t* nsend, uint32_t* nrecv, uint32_t* psrc, uint32_t* pdst) {
   k_p2p_counts<<<c.W, 64, 0, c.stream>>>(c.W, c.n_comms, c.r_nkeys.as<uint32_t>(), c.r_keys.as<uint32_t>(),
                                           c.r_cnt.as<uint32_t>(), c.bitmap.as<uint32_t>(), c.bitpre.as<uint32_t>(),
-                                          c.ch_nsend.as<uint32_t>(), c.ch_nrecv.as<uint32_t>(),
-                                          c.ch_nsend.as<uint32_t>() + c.n_p2p, c.ch_nrecv.as<uint32_t>() + c.n_p2p);
+                                          nsend, nrecv, psrc, pdst);
   return 1;
+}
+
+int launch_p2p_counts(Ctx& c) {
+  if (!c.n_p2p) return 0;
+  return launch_p2p_counts_to(c, c.ch_nsend.as<uint32_t>(), c.ch_nrecv.as<uint32_t>(), c.ch_nsend.as<uint32_t>() + c.n_p2p,
+                              c.ch_nrecv.as<uint32_t>() + c.n_p2p);
 }
 
 int launch_p2p_channels(Ctx& c) {

@@ -19,6 +19,9 @@
 // X4 ~ 0.6 MB. The per-shard fused pass dominates.
 #include <nccl.h>
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 #include "internal.cuh"
@@ -200,6 +203,71 @@ __global__ void k_x1_pack(const Counters* cnt, uint32_t force_status, unsigned l
   }
 }
 
+// OR of every shard's P2P channel bitmap (rows of the gathered X1 buffer)
+__global__ void k_bitmap_or(const uint32_t* gathered, uint64_t stride, uint64_t off, uint64_t nbm, uint32_t G, uint32_t* out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nbm; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t v = 0;
+    for (uint32_t s = 0; s < G; ++s) v |= gathered[s * stride + off + i];
+    out[i] = v;
+  }
+}
+
+// (src, dst) of every job-wide P2P channel (channel id = popcount prefix, ascending src*W + dst)
+__global__ void k_p2p_endpoints(uint32_t W, const uint32_t* bitmap, const uint32_t* bitpre, uint64_t nbm, uint32_t* psrc,
+                                uint32_t* pdst) {
+  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nbm; w += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t x = bitmap[w], id = bitpre[w];
+    while (x) {
+      const uint64_t pair = w * 32 + (uint64_t)(__ffs(x) - 1);
+      psrc[id] = (uint32_t)(pair / W); pdst[id] = (uint32_t)(pair % W);
+      ++id; x &= x - 1;
+    }
+  }
+}
+
+// job-wide P2P neighbour list of every rank (ascending; they index the wait-for edge columns all
+// shards sum into): d is a neighbour of r iff a channel r->d or d->r exists. One warp per rank,
+// lanes over candidate neighbours, ballot compaction keeps the order.
+__global__ void k_p2p_peers(uint32_t W, const uint32_t* bitmap, uint32_t* nbp, uint32_t* nbp_n, Counters* cnt) {
+  const uint32_t r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= W) return;
+  const uint32_t lane = lane_id();
+  uint32_t n = 0;
+  bool over = false;
+  for (uint32_t d0 = 0; d0 < W; d0 += 32) {
+    const uint32_t d = d0 + lane;
+    bool e = false;
+    if (d < W && d != r) {
+      const uint64_t x = (uint64_t)r * W + d, y = (uint64_t)d * W + r;
+      e = ((bitmap[x >> 5] >> (x & 31)) & 1u) | ((bitmap[y >> 5] >> (y & 31)) & 1u);
+    }
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, e);
+    const uint32_t pos = n + __popc(m & ((1u << lane) - 1u));
+    if (e && pos < (uint32_t)PCAP) nbp[(uint64_t)r * PCAP + pos] = d;
+    n += __popc(m);
+    if (n > (uint32_t)PCAP) { over = true; break; }
+  }
+  if (lane == 0) {
+    nbp_n[r] = over ? (uint32_t)PCAP : n;
+    if (over) atomicOr(&cnt->overflow, 4u);
+  }
+}
+
+// scatter of the staged host tables into their device buffers (one launch instead of a copy each)
+struct Unstage { const uint8_t* src; uint8_t* dst[12]; uint64_t off[12], bytes[12]; int n; };
+__global__ void k_unstage(Unstage u) {
+  for (int k = 0; k < u.n; ++k)
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < u.bytes[k]; i += (uint64_t)gridDim.x * blockDim.x)
+      u.dst[k][i] = u.src[u.off[k] + i];
+}
+
+// X2 send row: this shard's send / recv counts of the n_p2p job-wide channels, zero-padded to cap
+__global__ void k_x2_pack(const Counters* cnt, const uint32_t* nsend, const uint32_t* nrecv, uint64_t cap, uint32_t* out) {
+  const uint64_t np = cnt->n_p2p;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * cap; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = i < np ? nsend[i] : (i < 2 * np ? nrecv[i - np] : 0u);
+}
+
 // status + match counters of this shard for the X4 all-reduce (no host round trip)
 __global__ void k_x4_status(const Counters* cnt, const uint32_t* cl_J, const uint32_t* cl_max, uint32_t ncl, int check_class,
                             unsigned long long* e) {
@@ -213,6 +281,24 @@ __global__ void k_x4_status(const Counters* cnt, const uint32_t* cl_J, const uin
 }
 
 // all-gather of n u32 already packed in c.x_send; the gathered words land on the host
+// pinned host scratch of the shard path (exchange read-backs, table staging)
+scan_status pin_ensure(Ctx& c, size_t bytes) {
+  if (bytes <= c.h_pin_cap && c.h_pin) return SCAN_OK;
+  if (c.h_pin) { CK(cudaStreamSynchronize(c.stream)); cudaFreeHost(c.h_pin); c.h_pin = nullptr; c.h_pin_cap = 0; }
+  CK(cudaMallocHost(&c.h_pin, bytes));
+  c.h_pin_cap = bytes;
+  return SCAN_OK;
+}
+// grow, keeping the current contents (read-backs already landed: the stream is synchronised)
+scan_status pin_ensure_keep(Ctx& c, size_t bytes) {
+  if (bytes <= c.h_pin_cap && c.h_pin) return SCAN_OK;
+  void* nb = nullptr;
+  CK(cudaMallocHost(&nb, bytes));
+  if (c.h_pin) { std::memcpy(nb, c.h_pin, c.h_pin_cap); cudaFreeHost(c.h_pin); }
+  c.h_pin = nb; c.h_pin_cap = bytes;
+  return SCAN_OK;
+}
+
 scan_status allgather_dev(Ctx& c, size_t n, std::vector<uint32_t>& all) {
   const size_t G = (size_t)c.n_shards;
   CK(c.x_recv.ensure(n * 4 * G));
@@ -226,6 +312,23 @@ scan_status allgather_dev(Ctx& c, size_t n, std::vector<uint32_t>& all) {
 }  // namespace
 
 scan_status sharded_all(Ctx& c) {
+  // MS_SHARD_PROFILE=1: host-side phase timestamps on stderr (diagnostics)
+  static const bool prof = std::getenv("MS_SHARD_PROFILE") != nullptr;
+  using clk = std::chrono::steady_clock;
+  const auto t_start = clk::now();
+  std::vector<std::pair<const char*, double>> marks;
+  auto mark = [&](const char* what) {
+    if (prof) marks.push_back({what, std::chrono::duration<double, std::micro>(clk::now() - t_start).count()});
+  };
+  struct Dump {
+    std::vector<std::pair<const char*, double>>& m; int g;
+    ~Dump() {
+      if (m.empty()) return;
+      std::fprintf(stderr, "[shard %d]", g);
+      for (auto& x : m) std::fprintf(stderr, " %s=%.0f", x.first, x.second);
+      std::fprintf(stderr, " (us)\n");
+    }
+  } dump{marks, c.shard};
   c.matched = c.detected = c.localized = false;
   c.fused_used = false; c.tiles_ready = false; c.xwait_pending = false;
   const uint32_t G = (uint32_t)c.n_shards, g = (uint32_t)c.shard, nc = c.n_comms;
@@ -243,36 +346,76 @@ scan_status sharded_all(Ctx& c) {
     c.launches += timed(c, "k_fused_census", [&] { return launch_fused_census(c); });
   }
   const uint64_t nbm = c.n_bm_words;
-  const size_t HA = 16, LA = HA + 2 * (size_t)nc + nbm;
-  std::vector<uint32_t> AA;
-  CK(c.x_send.ensure(LA * 4));
+  const size_t HA = 16, HL = HA + 2 * (size_t)nc, LA = HL + nbm;  // X1 row: header | nmin | nmax | bitmap
+  const uint64_t NPMAX = W * PCAP;                                  // P2P channels <= ranks x peers
+  const size_t LB = 2 * NPMAX;                                      // X2 row: nsend | nrecv (fixed capacity)
+  // pinned host regions: A = X1 rows without bitmaps, C = counters, B = X2 rows (2*np used), D = staging
+  const size_t offA = 0, offC = (offA + (size_t)G * HL * 4 + 63) & ~size_t(63), offB = (offC + sizeof(Counters) + 63) & ~size_t(63);
+  CK(c.x_send.ensure(std::max(LA, LB) * 4)); CK(c.x_recv.ensure((size_t)G * LA * 4)); CK(c.x_recv2.ensure((size_t)G * LB * 4));
+  CK(c.ch_nsend.ensure(LB * 4)); CK(c.ch_nrecv.ensure(LB * 4)); CK(c.x_ep.ensure(LB * 4));
+  CK(cudaMemsetAsync(c.ch_nsend.p, 0, NPMAX * 4, c.stream));
+  CK(cudaMemsetAsync(c.ch_nrecv.p, 0, NPMAX * 4, c.stream));
+  if (!c.ev_x1) { CK(cudaEventCreateWithFlags(&c.ev_x1, cudaEventDisableTiming)); CK(cudaEventCreateWithFlags(&c.ev_x2, cudaEventDisableTiming)); }
+  if ((st = pin_ensure(c, offB + (size_t)G * LB * 4))) return st;
+  uint8_t* pin = static_cast<uint8_t*>(c.h_pin);
+  // ---- X1 (device-packed) and, right behind it, the device-side P2P channel set and X2: no host
+  // round trip between the two all-gathers
   k_x1_pack<<<(unsigned)std::min<uint64_t>((LA + 255) / 256, 1024), 256, 0, c.stream>>>(
       c.counters.as<Counters>(), c.spmd ? 0u : 1u, (unsigned long long)c.N, c.ch_nmin.as<uint32_t>(), c.ch_nmax.as<uint32_t>(),
       c.bitmap.as<uint32_t>(), nc, nbm, c.x_send.as<uint32_t>());
   c.launches += 1;
-  timed(c, "x1_allgather", [&] { st = allgather_dev(c, LA, AA); return 0; });
-  if (st) return st;
-  auto hdr = [&](uint32_t s, size_t i) { return AA[(size_t)s * LA + i]; };
+  mark("launch");
+  ncclResult_t xr = ncclSuccess;
+  timed(c, "x1_allgather", [&] { xr = ncclAllGather(c.x_send.p, c.x_recv.p, LA, ncclUint32, comm, c.stream); return 0; });
+  if (xr != ncclSuccess) { c.err = std::string("NCCL all-gather: ") + ncclGetErrorString(xr); return SCAN_E_NCCL; }
+  CK(cudaMemcpy2DAsync(pin + offA, HL * 4, c.x_recv.p, LA * 4, HL * 4, G, cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaEventRecord(c.ev_x1, c.stream));
+  c.launches += timed(c, "k_p2p_set", [&] {
+    k_bitmap_or<<<(unsigned)std::min<uint64_t>((nbm + 255) / 256, 4096), 256, 0, c.stream>>>(
+        c.x_recv.as<uint32_t>(), LA, HL, nbm, G, c.bitmap.as<uint32_t>());
+    launch_rank_prefix(c);  // channel ids = popcount prefix of the job-wide bitmap; n_p2p
+    k_p2p_endpoints<<<(unsigned)std::min<uint64_t>((nbm + 255) / 256, 4096), 256, 0, c.stream>>>(
+        (uint32_t)W, c.bitmap.as<uint32_t>(), c.bitpre.as<uint32_t>(), nbm, c.x_ep.as<uint32_t>(), c.x_ep.as<uint32_t>() + NPMAX);
+    k_p2p_peers<<<(unsigned)((W + 7) / 8), 256, 0, c.stream>>>((uint32_t)W, c.bitmap.as<uint32_t>(), c.nbp.as<uint32_t>(),
+                                                              c.nbp_n.as<uint32_t>(), c.counters.as<Counters>());
+    launch_p2p_counts_to(c, c.ch_nsend.as<uint32_t>(), c.ch_nrecv.as<uint32_t>(), c.x_ep.as<uint32_t>(),
+                         c.x_ep.as<uint32_t>() + NPMAX);
+    k_x2_pack<<<(unsigned)std::min<uint64_t>((LB + 255) / 256, 4096), 256, 0, c.stream>>>(
+        c.counters.as<Counters>(), c.ch_nsend.as<uint32_t>(), c.ch_nrecv.as<uint32_t>(), NPMAX, c.x_send.as<uint32_t>());
+    return 6;
+  });
+  CK(cudaMemcpyAsync(pin + offC, c.counters.p, sizeof(Counters), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaEventRecord(c.ev_x2, c.stream));
+  timed(c, "x2_allgather", [&] { xr = ncclAllGather(c.x_send.p, c.x_recv2.p, LB, ncclUint32, comm, c.stream); return 0; });
+  if (xr != ncclSuccess) { c.err = std::string("NCCL all-gather: ") + ncclGetErrorString(xr); return SCAN_E_NCCL; }
+  // host: X1 headers while the device works on the P2P channel set (identical data on every shard ->
+  // identical decisions; every shard has enqueued the same collectives before any early return)
+  CK(cudaEventSynchronize(c.ev_x1));
+  mark("x1");
+  const uint32_t* AA = reinterpret_cast<const uint32_t*>(pin + offA);
+  auto hdr = [&](uint32_t s, size_t i) { return AA[(size_t)s * HL + i]; };
   auto u64at = [&](uint32_t s, size_t i) { return (uint64_t)hdr(s, i) | ((uint64_t)hdr(s, i + 1) << 32); };
-  for (uint32_t s = 0; s < G; ++s) {  // identical data on every shard -> identical decisions
+  auto fail_all = [&](scan_status code, const std::string& m) { CK(cudaStreamSynchronize(c.stream)); c.err = m; return code; };
+  for (uint32_t s = 0; s < G; ++s) {
     const uint32_t x = hdr(s, 0);
     if (!x) continue;
     std::ostringstream m;
-    if (x == 1) { m << "sharded analysis needs an SPMD trace on every shard (shard " << s << " is not)"; c.err = m.str(); return SCAN_E_UNSUPPORTED; }
-    if (x == 2) { m << "schema error at event " << u64at(s, 7) << " of shard " << s; c.err = m.str(); return SCAN_E_SCHEMA; }
-    m << "capacity exceeded on shard " << s; c.err = m.str(); return SCAN_E_UNSUPPORTED;
+    if (x == 1) { m << "sharded analysis needs an SPMD trace on every shard (shard " << s << " is not)"; return fail_all(SCAN_E_UNSUPPORTED, m.str()); }
+    if (x == 2) { m << "schema error at event " << u64at(s, 7) << " of shard " << s; return fail_all(SCAN_E_SCHEMA, m.str()); }
+    m << "capacity exceeded on shard " << s;
+    return fail_all(SCAN_E_UNSUPPORTED, m.str());
   }
   for (uint32_t s = 0; s + 1 < G; ++s) {
     if (hdr(s, 2) != hdr(s, 1) || hdr(s, 3) != W) {
       std::ostringstream m;
       m << "shard " << s << " does not end on an iteration boundary of every rank";
-      c.err = m.str(); return SCAN_E_UNSUPPORTED;
+      return fail_all(SCAN_E_UNSUPPORTED, m.str());
     }
     for (uint32_t k = 0; k < nc; ++k)
       if (c.h_coff[k + 1] > c.h_coff[k] && hdr(s, HA + k) != hdr(s, HA + nc + k)) {
         std::ostringstream m;
         m << "communicator " << k << " has unequal member counts inside shard " << s;
-        c.err = m.str(); return SCAN_E_UNSUPPORTED;
+        return fail_all(SCAN_E_UNSUPPORTED, m.str());
       }
   }
   uint32_t it_off = 0, n_iters = 0;
@@ -290,78 +433,55 @@ scan_status sharded_all(Ctx& c) {
   }
   c.g_N = c.g_ncomm = c.g_ncomp = 0;
   for (uint32_t s = 0; s < G; ++s) { c.g_N += u64at(s, 5); c.g_ncomm += u64at(s, 9); c.g_ncomp += u64at(s, 11); }
-  std::vector<uint32_t> bm(nbm, 0);  // job-wide P2P channel bitmap (OR over shards)
-  uint64_t np = 0;
-  for (uint32_t s = 0; s < G; ++s)
-    for (uint64_t i = 0; i < nbm; ++i) bm[i] |= AA[(size_t)s * LA + HA + 2 * nc + i];
-  for (uint64_t i = 0; i < nbm; ++i) np += (uint64_t)__builtin_popcount(bm[i]);
-  if (nbm) CK(cudaMemcpyAsync(c.bitmap.p, bm.data(), nbm * 4, cudaMemcpyHostToDevice, c.stream));
-  c.launches += timed(c, "k_rank_prefix", [&] { return launch_rank_prefix(c); });
-  // ---- X2: P2P member counts per job-wide P2P channel
+  // P2P channel count (device prefix of the OR'ed bitmap), then exactly the X2 words in use
+  CK(cudaEventSynchronize(c.ev_x2));
+  const Counters* dc = reinterpret_cast<const Counters*>(pin + offC);
+  const uint64_t np = dc->n_p2p;
+  if (dc->overflow & 4u) return fail_all(SCAN_E_UNSUPPORTED, "capacity exceeded: more than 32 P2P peers on a rank");
+  const size_t LBu = std::max<size_t>(2 * np, 1);
+  if (np) CK(cudaMemcpy2DAsync(pin + offB, LBu * 4, c.x_recv2.p, LB * 4, 2 * np * 4, G, cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  mark("x2");
+  const uint32_t* BB = reinterpret_cast<const uint32_t*>(pin + offB);
   const uint64_t NCH = nc + np;
   c.n_p2p = np; c.NCH = NCH; c.hc.n_p2p = np;
-  CK(c.ch_nsend.ensure(std::max<uint64_t>(2 * np, 1) * 4)); CK(c.ch_nrecv.ensure(std::max<uint64_t>(2 * np, 1) * 4));
-  if (np) {
-    CK(cudaMemsetAsync(c.ch_nsend.p, 0, 2 * np * 4, c.stream));
-    CK(cudaMemsetAsync(c.ch_nrecv.p, 0, 2 * np * 4, c.stream));
-  }
-  c.launches += timed(c, "k_p2p_counts", [&] { return launch_p2p_counts(c); });
-  const size_t LB = std::max<size_t>(2 * np, 1);
-  std::vector<uint32_t> BB;
-  CK(c.x_send.ensure(LB * 4));
-  CK(cudaMemsetAsync(c.x_send.p, 0, LB * 4, c.stream));
-  if (np) {
-    CK(cudaMemcpyAsync(c.x_send.p, c.ch_nsend.p, np * 4, cudaMemcpyDeviceToDevice, c.stream));
-    CK(cudaMemcpyAsync(c.x_send.as<uint32_t>() + np, c.ch_nrecv.p, np * 4, cudaMemcpyDeviceToDevice, c.stream));
-  }
-  timed(c, "x2_allgather", [&] { st = allgather_dev(c, LB, BB); return 0; });
-  if (st) return st;
-  // P2P endpoints in channel order (ascending src*W + dst, the bitmap order)
-  std::vector<uint32_t> psrc(np), pdst(np);
-  {
-    uint64_t p = 0;
-    for (uint64_t wd = 0; wd < nbm; ++wd)
-      for (uint32_t x = bm[wd]; x; x &= x - 1) {
-        const uint64_t pair = wd * 32 + (uint64_t)__builtin_ctz(x);
-        psrc[p] = (uint32_t)(pair / W); pdst[p] = (uint32_t)(pair % W); ++p;
-      }
-  }
-  {  // job-wide P2P neighbour lists: they index the wait-for edge columns every shard sums into
-    std::vector<std::vector<uint32_t>> peers(W);
-    for (uint64_t p = 0; p < np; ++p) { peers[psrc[p]].push_back(pdst[p]); peers[pdst[p]].push_back(psrc[p]); }
-    std::vector<uint32_t> nbp(W * PCAP, 0), nbpn(W, 0);
-    for (uint64_t r = 0; r < W; ++r) {
-      auto& v = peers[r];
-      std::sort(v.begin(), v.end());
-      v.erase(std::unique(v.begin(), v.end()), v.end());
-      if (v.size() > (size_t)PCAP) { c.err = "capacity exceeded: more than 32 P2P peers on a rank"; return SCAN_E_UNSUPPORTED; }
-      nbpn[r] = (uint32_t)v.size();
-      for (size_t i = 0; i < v.size(); ++i) nbp[r * PCAP + i] = v[i];
-    }
-    CK(cudaMemcpyAsync(c.nbp.p, nbp.data(), W * PCAP * 4, cudaMemcpyHostToDevice, c.stream));
-    CK(cudaMemcpyAsync(c.nbp_n.p, nbpn.data(), W * 4, cudaMemcpyHostToDevice, c.stream));
-  }
   for (uint32_t s = 0; s + 1 < G; ++s)
     for (uint64_t p = 0; p < np; ++p)
-      if (BB[(size_t)s * LB + p] != BB[(size_t)s * LB + np + p]) {
+      if (BB[(size_t)s * LBu + p] != BB[(size_t)s * LBu + np + p]) {
         std::ostringstream m;
-        m << "P2P pair " << psrc[p] << "->" << pdst[p] << " has unequal send / recv counts inside shard " << s;
+        m << "P2P channel " << p << " has unequal send / recv counts inside shard " << s;
         c.err = m.str(); return SCAN_E_UNSUPPORTED;
       }
   // ---- job-wide channel tables (the unsharded k_channels numbering) + this shard's offsets
   auto nmem = [&](uint64_t ch) -> uint64_t { return ch < nc ? c.h_coff[ch + 1] - c.h_coff[ch] : 2; };
   auto lmax = [&](uint32_t s, uint64_t ch) -> uint32_t {
-    if (ch < nc) return nmem(ch) ? AA[(size_t)s * LA + HA + nc + ch] : 0u;
+    if (ch < nc) return nmem(ch) ? hdr(s, HA + nc + ch) : 0u;
     const uint64_t p = ch - nc;
-    return std::max(BB[(size_t)s * LB + p], BB[(size_t)s * LB + np + p]);
+    return std::max(BB[(size_t)s * LBu + p], BB[(size_t)s * LBu + np + p]);
   };
   auto lmin = [&](uint32_t s, uint64_t ch) -> uint32_t {
-    if (ch < nc) return nmem(ch) ? AA[(size_t)s * LA + HA + ch] : 0u;
+    if (ch < nc) return nmem(ch) ? hdr(s, HA + ch) : 0u;
     const uint64_t p = ch - nc;
-    return std::min(BB[(size_t)s * LB + p], BB[(size_t)s * LB + np + p]);
+    return std::min(BB[(size_t)s * LBu + p], BB[(size_t)s * LBu + np + p]);
   };
-  std::vector<uint64_t> gbase(NCH + 1), gslot(NCH + 1), kbase(NCH + 1), kslot(NCH + 1), pre(NCH), xb(NCH + 1);
-  std::vector<uint32_t> gmax(NCH), gmin(NCH), lmx(NCH), lmn(NCH);
+  // staging layout (u64 arrays, then u32 arrays) in pinned memory after region B; one H2D copy
+  const size_t n1 = NCH + 1, offD = (offB + (size_t)G * LBu * 4 + 63) & ~size_t(63);
+  const size_t bytesD = 5 * n1 * 8 + NCH * 8 + 4 * NCH * 4 + sizeof(Counters) + 64;
+  if ((st = pin_ensure_keep(c, offD + bytesD))) return st;
+  pin = static_cast<uint8_t*>(c.h_pin);
+  BB = reinterpret_cast<const uint32_t*>(pin + offB);
+  AA = reinterpret_cast<const uint32_t*>(pin + offA);
+  uint64_t* gbase = reinterpret_cast<uint64_t*>(pin + offD);
+  uint64_t* gslot = gbase + n1;
+  uint64_t* kbase = gslot + n1;
+  uint64_t* kslot = kbase + n1;
+  uint64_t* xb = kslot + n1;
+  uint64_t* pre = xb + n1;
+  uint32_t* gmax = reinterpret_cast<uint32_t*>(pre + NCH);
+  uint32_t* gmin = gmax + NCH;
+  uint32_t* lmx = gmin + NCH;
+  uint32_t* lmn = lmx + NCH;
+  Counters* hcs = reinterpret_cast<Counters*>((reinterpret_cast<uintptr_t>(lmn + NCH) + 15) & ~uintptr_t(15));
   uint64_t cb = 0, cs = 0, cx = 0;
   for (uint64_t ch = 0; ch < NCH; ++ch) {
     uint64_t tot = 0, pr = 0;
@@ -378,24 +498,35 @@ scan_status sharded_all(Ctx& c) {
   gbase[NCH] = kbase[NCH] = cb; gslot[NCH] = kslot[NCH] = cs; xb[NCH] = cx;
   if (cb >= 0xFFFFFFFFull) { c.err = "more than 2^32-1 instances"; return SCAN_E_UNSUPPORTED; }
   if (n_iters >= (1u << 24)) { c.err = "sharded analysis supports < 2^24 iterations"; return SCAN_E_UNSUPPORTED; }
-  CK(c.ch_base.ensure((NCH + 1) * 8)); CK(c.ch_slot.ensure((NCH + 1) * 8)); CK(c.xbase.ensure((NCH + 1) * 8));
-  if ((st = upload(c, c.ch_base, kbase)) || (st = upload(c, c.ch_slot, kslot)) || (st = upload(c, c.xbase, xb)) ||
-      (st = upload(c, c.g_base, gbase)) || (st = upload(c, c.g_slot, gslot)) || (st = upload(c, c.g_nmax, gmax)) ||
-      (st = upload(c, c.g_nmin, gmin)) || (st = upload(c, c.g_k0, pre)))
-    return st;
-  CK(cudaMemcpyAsync(c.ch_nmax.p, lmx.data(), NCH * 4, cudaMemcpyHostToDevice, c.stream));
-  CK(cudaMemcpyAsync(c.ch_nmin.p, lmn.data(), NCH * 4, cudaMemcpyHostToDevice, c.stream));
-  if (np) {
-    CK(cudaMemcpyAsync(c.ch_nsend.as<uint32_t>() + np, psrc.data(), np * 4, cudaMemcpyHostToDevice, c.stream));
-    CK(cudaMemcpyAsync(c.ch_nrecv.as<uint32_t>() + np, pdst.data(), np * 4, cudaMemcpyHostToDevice, c.stream));
-  }
-  c.h_shard_k0 = pre; c.h_shard_n = lmx;
+  c.h_shard_k0.assign(pre, pre + NCH); c.h_shard_n.assign(lmx, lmx + NCH);
   c.hc.n_instances = cb; c.hc.n_slots = cs; c.hc.p2p_inst0 = gbase[nc]; c.hc.p2p_slot0 = gslot[nc];
   c.hc.n_xinst = cx; c.hc.n_iters = n_iters;
   c.n_comm = c.hc.n_comm; c.n_comp = c.hc.n_comp; c.NIT = c.hc.max_niter; c.n_iters = n_iters;
   c.max_ncomp = c.hc.max_ncomp; c.n_bits_words = c.hc.n_bits_words;
   c.n_inst = cb; c.n_slots = cs; c.p2p_slot0 = gslot[nc]; c.p2p_inst0 = gbase[nc]; c.n_xinst = cx;
-  CK(cudaMemcpyAsync(c.counters.p, &c.hc, sizeof(Counters), cudaMemcpyHostToDevice, c.stream));
+  *hcs = c.hc;
+  {  // one H2D of the staged tables, then device-side scatters into their buffers
+    const size_t used = reinterpret_cast<uint8_t*>(hcs + 1) - (pin + offD);
+    CK(c.x_stage.ensure(used));
+    CK(cudaMemcpyAsync(c.x_stage.p, pin + offD, used, cudaMemcpyHostToDevice, c.stream));
+    CK(c.ch_base.ensure(n1 * 8)); CK(c.ch_slot.ensure(n1 * 8)); CK(c.xbase.ensure(n1 * 8));
+    CK(c.g_base.ensure(n1 * 8)); CK(c.g_slot.ensure(n1 * 8)); CK(c.g_k0.ensure(NCH * 8 + 8));
+    CK(c.g_nmax.ensure(NCH * 4 + 4)); CK(c.g_nmin.ensure(NCH * 4 + 4));
+    const cudaMemcpyKind dd = cudaMemcpyDeviceToDevice;
+    Unstage u{static_cast<const uint8_t*>(c.x_stage.p), {}, {}, {}, 0};
+    auto add = [&](DevBuf& d, const void* h, uint64_t bytes) {
+      u.dst[u.n] = static_cast<uint8_t*>(d.p); u.off[u.n] = static_cast<const uint8_t*>(h) - (pin + offD); u.bytes[u.n] = bytes; ++u.n;
+    };
+    add(c.g_base, gbase, n1 * 8); add(c.g_slot, gslot, n1 * 8); add(c.ch_base, kbase, n1 * 8); add(c.ch_slot, kslot, n1 * 8);
+    add(c.xbase, xb, n1 * 8); add(c.g_k0, pre, NCH * 8); add(c.g_nmax, gmax, NCH * 4); add(c.g_nmin, gmin, NCH * 4);
+    add(c.ch_nmax, lmx, NCH * 4); add(c.ch_nmin, lmn, NCH * 4); add(c.counters, hcs, sizeof(Counters));
+    k_unstage<<<64, 256, 0, c.stream>>>(u);
+    c.launches += 1;
+    if (np) {  // endpoints behind the counts (the layout every P2P consumer reads)
+      CK(cudaMemcpyAsync(c.ch_nsend.as<uint32_t>() + np, c.x_ep.p, np * 4, dd, c.stream));
+      CK(cudaMemcpyAsync(c.ch_nrecv.as<uint32_t>() + np, c.x_ep.as<uint32_t>() + NPMAX, np * 4, dd, c.stream));
+    }
+  }
   if ((st = alloc_match_buffers(c, true))) return st;
   // ---- local fused pass (K9 + cross-stage reduce + deferred stage 2), job-wide ids / windows
   if ((st = alloc_detect(c)) || (st = alloc_localize(c))) return st;
@@ -405,6 +536,7 @@ scan_status sharded_all(Ctx& c) {
   const uint64_t items = (uint64_t)c.NW * W, nlk = (uint64_t)c.NW * np, ncl = (uint64_t)c.TP * c.PP;
   CK(cudaMemsetAsync(c.wd_total.p, 0, items * 4, c.stream));
   CK(cudaMemsetAsync(c.wd_slow.p, 0, items * 4, c.stream));
+  mark("tables");
   c.launches += timed(c, "k_class_counts", [&] { return launch_class_counts(c); });
   c.launches += timed(c, "k_fused", [&] { return launch_fused(c); });
   c.launches += timed(c, "k_cross_reduce", [&] { return launch_cross_reduce(c); });
@@ -469,6 +601,7 @@ scan_status sharded_all(Ctx& c) {
       c.launches += 1;
     }
   }
+  mark("x3enq");
   c.launches += timed(c, "k_link_median", [&] { return launch_link_median(c); });
   // ---- stage-2 boundary records of this shard's ranks
   CK(c.headtail.ensure(((uint64_t)G * W + 16) * 8));
@@ -504,8 +637,10 @@ scan_status sharded_all(Ctx& c) {
       return 0;
     });
     if (xr != ncclSuccess) { c.err = std::string("NCCL all-reduce: ") + ncclGetErrorString(xr); return SCAN_E_NCCL; }
+    mark("x4enq");
     CK(cudaMemcpyAsync(e, ht + (uint64_t)G * W, sizeof(e), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
+    mark("x4");
     if (e[0]) { c.err = "sharded analysis needs an SPMD trace on every shard (fused-pass verification failed)"; return SCAN_E_UNSUPPORTED; }
     if (e[1]) { c.err = "a DP class has unequal compute counts inside a shard other than the last"; return SCAN_E_UNSUPPORTED; }
     c.hc.n_incomplete = e[2]; c.hc.n_kind_mismatch = e[3]; c.hc.n_payload_mismatch = e[4];
@@ -527,6 +662,7 @@ scan_status sharded_all(Ctx& c) {
   c.launches += timed(c, "k_link_flags", [&] { return launch_link_flags(c); });
   c.launches += timed(c, "k_walk", [&] { return launch_verdict_walk(c); });
   if ((st = sync_read(c))) return st;
+  mark("end");
   if (c.hc.overflow & 24u) {
     c.err = "capacity exceeded: more than 16384 samples on a link / links in a direction class";
     return SCAN_E_UNSUPPORTED;
@@ -540,6 +676,10 @@ scan_status sharded_all(Ctx& c) {
 void shard_release(Ctx& c) {
   if (c.nccl) ncclCommDestroy((ncclComm_t)c.nccl);
   c.nccl = nullptr;
+  if (c.h_pin) cudaFreeHost(c.h_pin);
+  c.h_pin = nullptr; c.h_pin_cap = 0;
+  if (c.ev_x1) { cudaEventDestroy(c.ev_x1); cudaEventDestroy(c.ev_x2); }
+  c.ev_x1 = c.ev_x2 = nullptr;
 }
 
 }  // namespace ms
