@@ -719,12 +719,18 @@ __global__ void k_walk(WKArgs a) {
     } else {
       a.level[it] = -1; a.lb_label[it] = SCAN_L_CLEAN;
     }
-    // total wait (sum of out-edge weights)
-    const uint32_t w = (uint32_t)(it / a.W);
+  }
+  // total wait of every item (sum of its out-edge weights): one warp per item, lanes over neighbours
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t wstride = stride >> 5, wg = t0 >> 5;
+  for (uint64_t it = wg; it < items; it += wstride) {
+    const uint32_t w = (uint32_t)(it / a.W), r = (uint32_t)(it % a.W);
+    const unsigned long long* eww = a.ew + (uint64_t)w * a.nnz_tot;
     unsigned long long tw = 0;
-    for (uint64_t q = a.nbc_off[r]; q < a.nbc_off[r + 1]; ++q) tw += a.ew[(uint64_t)w * a.nnz_tot + q];
-    for (uint32_t q = 0; q < a.nbp_n[r]; ++q) tw += a.ew[(uint64_t)w * a.nnz_tot + a.nnz_c + (uint64_t)r * PCAP + q];
-    a.lb_twait[it] = tw;
+    for (uint64_t q = a.nbc_off[r] + lane; q < a.nbc_off[r + 1]; q += 32) tw += eww[q];
+    if (lane < a.nbp_n[r]) tw += eww[a.nnz_c + (uint64_t)r * PCAP + lane];
+    tw = warp_sum_u64(tw);
+    if (lane == 0) a.lb_twait[it] = tw;
   }
   grid.sync();
   for (uint64_t o = t0; o < (uint64_t)a.NW * a.n_p2p; o += stride)
@@ -742,27 +748,33 @@ __global__ void k_walk(WKArgs a) {
     }
   grid.sync();
   for (int d = 0;; ++d) {
-    for (uint64_t it = t0; it < items; it += stride) {
+    // one warp per unlabelled item: lanes over its neighbours, warp argmax (heaviest edge into
+    // level d, ties -> smallest rank)
+    for (uint64_t it = wg; it < items; it += wstride) {
       if (a.level[it] >= 0) continue;
       const uint32_t w = (uint32_t)(it / a.W), u = (uint32_t)(it % a.W);
       const uint64_t lw = (uint64_t)w * a.W;
       const unsigned long long* eww = a.ew + (uint64_t)w * a.nnz_tot;
       uint32_t best = NONE32; unsigned long long bw = 0;
-      for (uint64_t q = a.nbc_off[u]; q < a.nbc_off[u + 1]; ++q) {
+      auto take = [&](uint32_t v, unsigned long long x) {
+        if (v != NONE32 && (best == NONE32 || x > bw || (x == bw && v < best))) { best = v; bw = x; }
+      };
+      for (uint64_t q = a.nbc_off[u] + lane; q < a.nbc_off[u + 1]; q += 32) {
         const unsigned long long x = eww[q];
-        if (!x) continue;
-        const uint32_t v = a.nbc[q];
-        if (a.level[lw + v] != d) continue;
-        if (best == NONE32 || x > bw || (x == bw && v < best)) { best = v; bw = x; }
+        if (x && a.level[lw + a.nbc[q]] == d) take(a.nbc[q], x);
       }
-      for (uint32_t q = 0; q < a.nbp_n[u]; ++q) {
-        const unsigned long long x = eww[a.nnz_c + (uint64_t)u * PCAP + q];
-        if (!x) continue;
-        const uint32_t v = a.nbp[(uint64_t)u * PCAP + q];
-        if (a.level[lw + v] != d) continue;
-        if (best == NONE32 || x > bw || (x == bw && v < best)) { best = v; bw = x; }
+      if (lane < a.nbp_n[u]) {
+        const unsigned long long x = eww[a.nnz_c + (uint64_t)u * PCAP + lane];
+        const uint32_t v = a.nbp[(uint64_t)u * PCAP + lane];
+        if (x && a.level[lw + v] == d) take(v, x);
       }
-      if (best != NONE32) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint32_t ov = __shfl_xor_sync(0xFFFFFFFFu, best, o);
+        const unsigned long long ox = __shfl_xor_sync(0xFFFFFFFFu, bw, o);
+        take(ov, ox);
+      }
+      if (lane == 0 && best != NONE32) {
         a.level[it] = d + 1;
         a.lb_label[it] = SCAN_L_VICTIM;
         a.lb_rkind[it] = a.lb_rkind[lw + best];
@@ -803,7 +815,7 @@ int launch_verdict_walk(Ctx& c) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_walk, 256, 0);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-  int blocks = (int)std::min<uint64_t>((items + 255) / 256, (uint64_t)std::max(1, nb) * sms);
+  int blocks = (int)std::min<uint64_t>((items * 32 + 255) / 256, (uint64_t)std::max(1, nb) * sms);  // a warp per item
   blocks = std::max(blocks, 1);
   void* args[] = {&a};
   cudaLaunchCooperativeKernel((void*)k_walk, blocks, 256, args, 0, c.stream);
