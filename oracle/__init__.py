@@ -104,6 +104,9 @@ def _load():
         lib.orc_run.restype = ctypes.c_void_p
         lib.orc_run.argtypes = [ctypes.POINTER(_Input), ctypes.POINTER(_Config), ctypes.POINTER(ctypes.c_int32)]
         lib.orc_free.argtypes = [ctypes.c_void_p]
+        lib.orc_run_align.restype = ctypes.c_void_p
+        lib.orc_run_align.argtypes = [ctypes.POINTER(_Input), ctypes.POINTER(_Config), ctypes.c_void_p, ctypes.c_int32,
+                                      ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
         lib.orc_array.restype = ctypes.c_int
         lib.orc_array.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p),
                                   ctypes.POINTER(ctypes.c_uint64)]
@@ -115,7 +118,20 @@ def _c(a, dt):
     return np.ascontiguousarray(a, dtype=dt)
 
 
-def run(trace, cfg: Config | None = None) -> dict:
+_AL_ARRAYS = {"al_start": np.int64, "al_level": np.int32, "al_nanchor": np.uint32, "al_residual": np.uint64}
+
+
+def align(trace, reference: int = 0, cfg: Config | None = None) -> dict:
+    """run() plus the NEXT-1 timeline alignment (oracle.cpp ``align``, SPEC
+    S:L243-300; readings AL1-AL6). Needs ``trace.start_ns``. Adds al_start (i64 per event),
+    al_level (i32 per rank, -1 = not reached), al_nanchor, al_residual and al_status."""
+    cfg = cfg or Config()
+    lib = _load()
+    start = _c(trace.start_ns, np.int64)
+    return run(trace, cfg, _align=(start, int(reference)))
+
+
+def run(trace, cfg: Config | None = None, _align=None) -> dict:
     """Analyse ``trace`` (a tracegen.Trace or any object with the same columns). Returns a dict of
     numpy arrays (keys of ``_ARRAYS``) plus the scalar counters."""
     cfg = cfg or Config()
@@ -130,7 +146,13 @@ def run(trace, cfg: Config | None = None) -> dict:
                 cfg.late_num, cfg.late_den, cfg.late_margin_ns, cfg.bw_num, cfg.bw_den, cfg.wait_margin_ns,
                 cfg.window_iters, cfg.stage2_classes, cfg.stage2_mode, 0)
     st = ctypes.c_int32(0)
-    h = lib.orc_run(ctypes.byref(inp), ctypes.byref(c), ctypes.byref(st))
+    ast = ctypes.c_int32(0)
+    if _align is None:
+        h = lib.orc_run(ctypes.byref(inp), ctypes.byref(c), ctypes.byref(st))
+    else:
+        keep.append(_align[0])
+        h = lib.orc_run_align(ctypes.byref(inp), ctypes.byref(c), _align[0].ctypes.data, _align[1],
+                              ctypes.byref(st), ctypes.byref(ast))
     try:
         out = {}
         for name, dt in _ARRAYS.items():
@@ -140,6 +162,15 @@ def run(trace, cfg: Config | None = None) -> dict:
                 raise KeyError(name)
             n = nb.value // np.dtype(dt).itemsize
             out[name] = np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_uint8)), shape=(nb.value,)).view(dt)[:n].copy() if n else np.zeros(0, dt)
+        if _align is not None:
+            for name, dt in _AL_ARRAYS.items():
+                p = ctypes.c_void_p()
+                nb = ctypes.c_uint64()
+                if lib.orc_array(h, name.encode(), ctypes.byref(p), ctypes.byref(nb)) != 0:
+                    raise KeyError(name)
+                n = nb.value // np.dtype(dt).itemsize
+                out[name] = np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_uint8)), shape=(nb.value,)).view(dt)[:n].copy() if n else np.zeros(0, dt)
+            out["al_status"] = int(ast.value)
         sc = out.pop("scalars")
         for i, k in enumerate(_SCALARS):
             out[k] = int(np.int64(sc[i])) if k == "status" else int(sc[i])

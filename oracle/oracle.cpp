@@ -53,6 +53,10 @@ struct Result {
   std::vector<uint8_t> lb_label, lb_root_kind; std::vector<uint32_t> lb_root_rank, lb_root_src, lb_depth; std::vector<uint64_t> lb_total_wait;
   std::vector<uint32_t> eg_window, eg_src, eg_dst; std::vector<uint64_t> eg_weight;
   std::vector<uint64_t> scalars;
+  // NEXT-1 timeline alignment (orc_run_align)
+  std::vector<int64_t> al_start; std::vector<int32_t> al_level; std::vector<uint32_t> al_nanchor;
+  std::vector<uint64_t> al_residual;
+  int32_t al_status = 0;
 };
 
 }  // namespace
@@ -506,6 +510,110 @@ struct Oracle {
     return (R.n_incomplete || R.n_kind_mismatch || R.n_payload_mismatch) ? 1 : 0;
   }
 
+  // ---- NEXT-1 timeline alignment (members of a synchronous call "logically finish at the
+  // same moment"; a reference rank; the others aligned to it "iteratively", anchors at the identified
+  // instances; SPEC S:L243-300 ClockMap). Readings (AL1-AL6):
+  //   AL1 anchors = ends (start + dur) of a rank's collective events (kinds 1-4) whose instance is
+  //       VALID; P2P excluded
+  //   AL2 "iteratively" = BFS levels from the reference over "shares a valid collective instance";
+  //       level-k ranks use members of levels < k only (one level at a time)
+  //   AL3 target of an instance = the maximum aligned end over those members; anchor =
+  //       (local end, target - local end), in program order; an end equal to the previous
+  //       anchor's is skipped; decreasing candidate ends on a rank -> status -9 (unsupported)
+  //   AL4 offset(t): none -> 0; before the first / after the last anchor -> that anchor's offset;
+  //       between anchors i, i+1: o_i + floor((o_i+1 - o_i) * (t - t_i) / (t_i+1 - t_i)), exact
+  //   AL5 aligned start = start + offset(start); ranks not reached keep their local clock (level -1)
+  //   AL6 residual of a rank = max over its anchor candidates of (max aligned end over the
+  //       instance's aligned members - its own aligned end)
+  static int64_t floor_div(__int128 n, __int128 d) {
+    __int128 q = n / d;
+    if ((n % d != 0) && ((n < 0) != (d < 0))) q -= 1;
+    return (int64_t)q;
+  }
+  static int64_t offset_at(const std::vector<std::pair<int64_t, int64_t>>& a, int64_t t) {
+    if (a.empty()) return 0;
+    if (t <= a.front().first) return a.front().second;
+    if (t >= a.back().first) return a.back().second;
+    size_t i = std::upper_bound(a.begin(), a.end(), std::make_pair(t, INT64_MAX)) - a.begin() - 1;  // t_i <= t < t_i+1
+    const __int128 o0 = a[i].second, o1 = a[i + 1].second, t0 = a[i].first, t1 = a[i + 1].first;
+    return (int64_t)(o0 + floor_div((o1 - o0) * ((__int128)t - t0), t1 - t0));
+  }
+  int align(const int64_t* start, int ref, std::vector<int64_t>& al_start, std::vector<int32_t>& level,
+            std::vector<uint32_t>& nanchor, std::vector<uint64_t>& residual) {
+    const uint64_t N = in.n_events;
+    al_start.assign(start, start + N);
+    level.assign(W, -1); nanchor.assign(W, 0); residual.assign(W, 0);
+    if (ref < 0 || ref >= W) return -1;
+    std::vector<std::vector<uint64_t>> cand(W);
+    std::map<uint32_t, std::vector<std::pair<int, uint64_t>>> inst_ev;  // instance -> (rank, event)
+    for (int r = 0; r < W; ++r)
+      for (uint64_t e = in.rank_offsets[r]; e < in.rank_offsets[r + 1]; ++e) {
+        const int k = kind(e);
+        if (k < KIND_ALLREDUCE || k > KIND_BROADCAST) continue;
+        const uint32_t id = R.ev_inst[e];
+        if (!(R.in_flags[id] & F_VALID)) continue;
+        if (!cand[r].empty()) {
+          const uint64_t p = cand[r].back();
+          if (start[e] + (int64_t)in.dur[e] < start[p] + (int64_t)in.dur[p]) return -9;
+        }
+        cand[r].push_back(e);
+        inst_ev[id].push_back({r, e});
+      }
+    // BFS levels (AL2)
+    std::vector<std::set<int>> adj(W);
+    for (auto& kv : inst_ev)
+      for (auto& a : kv.second)
+        for (auto& b : kv.second)
+          if (a.first != b.first) adj[a.first].insert(b.first);
+    std::vector<int> order{ref};
+    level[ref] = 0;
+    for (size_t q = 0; q < order.size(); ++q)
+      for (int m : adj[order[q]])
+        if (level[m] < 0) { level[m] = level[order[q]] + 1; order.push_back(m); }
+    int maxlev = 0;
+    for (int r = 0; r < W; ++r) maxlev = std::max(maxlev, level[r]);
+    std::vector<int64_t> aend(N, 0);  // event -> aligned end (collective candidates of aligned ranks)
+    std::vector<std::vector<std::pair<int64_t, int64_t>>> anc(W);
+    for (uint64_t e : cand[ref]) aend[e] = start[e] + (int64_t)in.dur[e];
+    for (int k = 1; k <= maxlev; ++k) {
+      for (int r = 0; r < W; ++r) {  // AL3: anchors from members of earlier levels
+        if (level[r] != k) continue;
+        for (uint64_t e : cand[r]) {
+          const int64_t t = start[e] + (int64_t)in.dur[e];
+          bool have = false;
+          int64_t tgt = 0;
+          for (auto& m : inst_ev[R.ev_inst[e]])
+            if (m.first != r && level[m.first] >= 0 && level[m.first] < k) {
+              const int64_t v = aend[m.second];
+              if (!have || v > tgt) tgt = v;
+              have = true;
+            }
+          if (have && (anc[r].empty() || t > anc[r].back().first)) anc[r].push_back({t, tgt - t});
+        }
+      }
+      for (int r = 0; r < W; ++r) {
+        if (level[r] != k) continue;
+        for (uint64_t e : cand[r]) {
+          const int64_t t = start[e] + (int64_t)in.dur[e];
+          aend[e] = t + offset_at(anc[r], t);
+        }
+      }
+    }
+    for (int r = 0; r < W; ++r) {  // AL5, AL6
+      nanchor[r] = (uint32_t)anc[r].size();
+      if (level[r] < 0) continue;
+      for (uint64_t e = in.rank_offsets[r]; e < in.rank_offsets[r + 1]; ++e) al_start[e] = start[e] + offset_at(anc[r], start[e]);
+      uint64_t res = 0;
+      for (uint64_t e : cand[r]) {
+        int64_t fin = INT64_MIN;
+        for (auto& m : inst_ev[R.ev_inst[e]]) if (level[m.first] >= 0) fin = std::max(fin, aend[m.second]);
+        res = std::max<uint64_t>(res, (uint64_t)(fin - aend[e]));
+      }
+      residual[r] = res;
+    }
+    return 0;
+  }
+
   // stage-2 class of a communicator from the topology (reading R12): 1 = TP group, 2 = DP group
   uint8_t comm_class(const std::vector<uint32_t>& m) const {
     if (TP >= 2 && (int)m.size() == TP) {
@@ -546,6 +654,19 @@ void* orc_run(const orc_input* in, const orc_config* cfg, int32_t* status) {
   return R;
 }
 
+// run() then the timeline alignment on its instances; *al_status: 0 ok, -1 bad reference,
+// -9 decreasing collective end times on a rank
+void* orc_run_align(const orc_input* in, const orc_config* cfg, const int64_t* start_ns, int32_t reference,
+                    int32_t* status, int32_t* al_status) {
+  Result* R = static_cast<Result*>(orc_run(in, cfg, status));
+  *al_status = -1;
+  if (*status < 0 || !start_ns) return R;
+  Oracle o(*in, *cfg, *R);
+  R->al_status = o.align(start_ns, reference, R->al_start, R->al_level, R->al_nanchor, R->al_residual);
+  *al_status = R->al_status;
+  return R;
+}
+
 void orc_free(void* h) { delete (Result*)h; }
 
 // Named result arrays; returns 0 if found.
@@ -565,6 +686,7 @@ int orc_array(void* h, const char* name, void** ptr, uint64_t* nbytes) {
   X(lk_dir) X(lk_eligible) X(lk_med_bw)
   X(lb_label) X(lb_root_kind) X(lb_root_rank) X(lb_root_src) X(lb_depth) X(lb_total_wait)
   X(eg_window) X(eg_src) X(eg_dst) X(eg_weight)
+  X(al_start) X(al_level) X(al_nanchor) X(al_residual)
 #undef X
   return -1;
 }
