@@ -98,7 +98,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_trace(name: str, iters: int | None, seed: int, pinned: bool, it_range=None):
+def make_trace(name: str, iters: int | None, seed: int, pinned: bool, it_range=None, with_start: bool = False):
     import tracegen as tg
     from tracegen import configs
     cfg = configs.CONFIGS[name](seed=seed) if iters is None else configs.CONFIGS[name](seed=seed, iterations=iters)
@@ -112,7 +112,7 @@ def make_trace(name: str, iters: int | None, seed: int, pinned: bool, it_range=N
                       ("payload", torch.int32)):
             t = torch.empty(n, dtype=dt, pin_memory=True)
             out[k] = t.numpy().view({torch.int32: np.uint32, torch.int16: np.uint16}[dt])
-    return tg.generate(cfg, out=out, with_start=False, iter_range=it_range), cfg
+    return tg.generate(cfg, out=out, with_start=with_start, iter_range=it_range), cfg
 
 
 def cpu_oracle_rate(name: str, sample_iters: int, seed: int) -> dict:
@@ -160,6 +160,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--breakdown", action="store_true", default=True)
+    ap.add_argument("--no-align", action="store_true", help="skip the timeline-alignment measurement (N=1 only)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -183,7 +184,8 @@ def main():
     blk = ms.shard_iterations(total_iters, world, rank) if world > 1 else None
     uid = ms.shard_unique_id() if world > 1 else None
     t_gen = time.perf_counter()
-    tr, cfg = make_trace(args.config, iters, args.seed, pinned=True, it_range=blk)
+    do_align = world == 1 and not args.no_align
+    tr, cfg = make_trace(args.config, iters, args.seed, pinned=True, it_range=blk, with_start=do_align)
     t_gen = time.perf_counter() - t_gen
     N = tr.n_events
     comm_frac = float(((tr.kind_op & 7) != 0).mean()) if N <= 50_000_000 else float(
@@ -259,6 +261,44 @@ def main():
                "path": "pinned host columns -> scan_load_events(SCAN_HOST_PTRS) -> scan_analyze -> scan_export"
                        " (verdicts + labels), wall clock" + (", max over ranks" if dist else "")}
 
+    # ---- NEXT-1 timeline alignment (scan_align) on the same resident trace, N=1 only ----
+    alignment = None
+    if do_align:
+        dev["start_ns"] = torch.from_numpy(tr.start_ns).cuda(local)
+        torch.cuda.synchronize()
+        s.load(tr, device_ptrs=True, cols=dev)
+        s.analyze()  # instances (untimed here: the analysis is the main metric)
+        for _ in range(max(1, args.warmup)):
+            res_al = s.align(0)
+        torch.cuda.synchronize()
+        s.set_timing(True)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(args.steps):
+            res_al = s.align(0)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        akern = s.kernel_timing()
+        s.set_timing(False)
+        ams = a0.elapsed_time(a1) / args.steps
+        al_k = {k: v for k, v in akern.items() if k.startswith("k_al_")}
+        apply_ms = al_k["k_al_apply"][0] / max(al_k["k_al_apply"][1], 1) if "k_al_apply" in al_k else None
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+        pk = float(peaks.get("hbm_gbs", 6650.0))
+        alignment = {
+            "metric": "trace events aligned/sec (scan_align, reference rank 0)", "value": N / (ams / 1e3),
+            "unit": "events/s", "ms_per_call": ams, "result": {k: int(v) for k, v in res_al.items()},
+            "kernels": {k: {"ms_per_call": round(v[0] / args.steps, 4), "launches": v[1]}
+                        for k, v in sorted(al_k.items(), key=lambda kv: -kv[1][0])},
+            "roofline": ({"bound": "hbm", "kernel": "k_al_apply", "bytes_per_event": 16,
+                          "achieved": 16 * N / (apply_ms / 1e3) / 1e9, "peak": pk, "unit": "GB/s",
+                          "frac": 16 * N / (apply_ms / 1e3) / 1e9 / pk} if apply_ms else None),
+            "note": "start_ns resident in HBM; per call: candidate ends, monotonicity, BFS levels, per-level "
+                    "anchors + aligned ends, aligned start of every event, residuals",
+        }
+        del dev["start_ns"]
+
     if rank != 0:
         if dist:
             dist.barrier()
@@ -315,6 +355,7 @@ def main():
         "gpu_launches": int(launches) * args.steps,
         "clocks": clk.summary(),
         "verdicts": {"flagged": flagged},
+        "alignment": alignment,
         "path": "fused SPMD stage-tile pass (K9)" if fused else "general path",
     }
     print(json.dumps(line), flush=True)

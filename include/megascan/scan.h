@@ -76,7 +76,8 @@ typedef struct scan_comm_table {     /* collective communicators ("global
 typedef struct scan_event_columns {  /* structure-of-arrays, events grouped by rank, program order */
     uint64_t n_events;
     const uint64_t* rank_offsets;    /* HOST [world+1], monotone; rank r owns [off[r], off[r+1]) */
-    const int64_t*  start_ns;        /* optional (may be NULL): local-clock start; never read     */
+    const int64_t*  start_ns;        /* optional (may be NULL): local-clock start; read only by
+                                        scan_align (the analysis never reads it, reading R5)      */
     const uint32_t* dur_ns;          /* CUDA-event duration, ns                                    */
     const uint16_t* kind_op;
     const uint16_t* meta;
@@ -183,6 +184,29 @@ const char* scan_last_error(const scan_ctx* ctx);   /* owned by ctx; "" if none 
    Errors: SCAN_E_INVALID_ARG (n_shards < 1, shard out of range, null id), SCAN_E_NCCL (NCCL
    failure; message in scan_last_error), SCAN_E_CUDA.                                                  */
 scan_status scan_nccl_unique_id(uint8_t out[128]);
+
+/* ---- NEXT-1: timeline alignment (readings AL1-AL6) -----
+   Maps every rank's local clock onto the reference rank's, using the matched instances as anchors:
+   the members of a valid collective instance "logically finish at the same moment".
+   AL1 anchors = ends (start_ns + dur_ns) of a rank's collective events (kinds 1-4) of VALID
+       instances; P2P excluded.
+   AL2 ranks are aligned in BFS levels from the reference over "shares a valid collective instance";
+       a rank of level k uses members of levels < k.
+   AL3 target = max aligned end over those members; anchor = (local end, target - local end) in
+       program order, an end equal to the previous anchor's skipped.
+   AL4 offset(t) piecewise linear between anchors (floor of the exact rational), constant outside.
+   AL5 aligned start = start + offset(start); ranks not reached keep their clock (level -1).
+   Requires: a completed scan_analyze (or scan_match_collectives) and start_ns given at load.
+   Outputs SCAN_OUT_AL_*. Errors: SCAN_E_ORDER (no instances yet), SCAN_E_INVALID_ARG (no
+   start_ns, reference out of range), SCAN_E_UNSUPPORTED (collective end times decrease along a
+   rank's program order; sharded context), SCAN_E_OOM, SCAN_E_CUDA.                            */
+typedef struct scan_align_config { int32_t reference; uint32_t reserved; } scan_align_config;
+typedef struct scan_align_result {
+    uint64_t n_anchors;
+    uint32_t n_aligned_ranks, n_unaligned_ranks, max_level, reserved;
+    uint64_t max_residual_ns;
+} scan_align_result;
+scan_status scan_align(scan_ctx* ctx, const scan_align_config* cfg, scan_align_result* out);
 scan_status scan_create_sharded(scan_ctx** out, int cuda_device, void* cuda_stream, int n_shards, int shard,
                                 const uint8_t nccl_unique_id[128]);
 
@@ -266,6 +290,11 @@ typedef enum scan_output {
        Unsharded: K0 = 0, N = CH_NMAX.                                                          */
     SCAN_OUT_CH_SHARD_K0,      /* u64 */
     SCAN_OUT_CH_SHARD_N,       /* u32 */
+    /* timeline alignment (scan_align) */
+    SCAN_OUT_AL_START,         /* i64 per event: start on the reference rank's clock             */
+    SCAN_OUT_AL_LEVEL,         /* i32 per rank: BFS level from the reference, -1 = not reached     */
+    SCAN_OUT_AL_NANCHOR,       /* u32 per rank: anchors of its clock map                           */
+    SCAN_OUT_AL_RESIDUAL,      /* u64 per rank: max (instance aligned end - own aligned end), ns   */
     SCAN_OUT__COUNT
 } scan_output;
 

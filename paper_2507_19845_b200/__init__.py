@@ -44,8 +44,10 @@ OUTPUTS = [
     ("eg_window", np.uint32), ("eg_src", np.uint32), ("eg_dst", np.uint32), ("eg_weight", np.uint64),
     ("comm_inst", np.uint32), ("comm_wait", np.uint32), ("slow_bits", np.uint32),
     ("ch_shard_k0", np.uint64), ("ch_shard_n", np.uint32),
+    ("al_start", np.int64), ("al_level", np.int32), ("al_nanchor", np.uint32), ("al_residual", np.uint64),
 ]
-NATIVE_ONLY = ("comm_inst", "comm_wait", "slow_bits", "ch_shard_k0", "ch_shard_n")  # no oracle counterpart
+ALIGN_OUTPUTS = ("al_start", "al_level", "al_nanchor", "al_residual")
+NATIVE_ONLY = ("comm_inst", "comm_wait", "slow_bits", "ch_shard_k0", "ch_shard_n") + ALIGN_OUTPUTS
 OUT_INDEX = {n: i for i, (n, _) in enumerate(OUTPUTS)}
 OUT_DTYPE = dict(OUTPUTS)
 
@@ -62,6 +64,15 @@ class _Topo(ctypes.Structure):
 
 class _Comms(ctypes.Structure):
     _fields_ = [("n_comms", ctypes.c_uint32), ("offsets", ctypes.c_void_p), ("members", ctypes.c_void_p)]
+
+
+class _AlignCfg(ctypes.Structure):
+    _fields_ = [("reference", ctypes.c_int32), ("reserved", ctypes.c_uint32)]
+
+
+class _AlignRes(ctypes.Structure):
+    _fields_ = [("n_anchors", ctypes.c_uint64), ("n_aligned_ranks", ctypes.c_uint32), ("n_unaligned_ranks", ctypes.c_uint32),
+                ("max_level", ctypes.c_uint32), ("reserved", ctypes.c_uint32), ("max_residual_ns", ctypes.c_uint64)]
 
 
 class _Cols(ctypes.Structure):
@@ -143,10 +154,11 @@ def _load_lib():
     lib.scan_force_general.argtypes = [P, ctypes.c_int]
     lib.scan_fused_variant.argtypes = [P, ctypes.c_int]
     lib.scan_nccl_unique_id.argtypes = [P]
+    lib.scan_align.argtypes = [P, ctypes.POINTER(_AlignCfg), ctypes.POINTER(_AlignRes)]
     lib.scan_create_sharded.argtypes = [ctypes.POINTER(P), ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P]
     for f in ("scan_create", "scan_load_events", "scan_match_collectives", "scan_detect", "scan_localize",
               "scan_output_size", "scan_export", "scan_analyze", "scan_force_general", "scan_fused_variant",
-              "scan_nccl_unique_id", "scan_create_sharded"):
+              "scan_nccl_unique_id", "scan_create_sharded", "scan_align"):
         getattr(lib, f).restype = ctypes.c_int32
     _lib = lib
     return lib
@@ -156,7 +168,7 @@ EXPORTED_SYMBOLS = ["scan_create", "scan_destroy", "scan_last_error", "scan_load
                     "scan_detect", "scan_localize", "scan_output_size", "scan_export", "scan_output_device_ptr",
                     "scan_kernel_launches", "scan_set_timing", "scan_timing_reset", "scan_kernel_timing",
                     "scan_analyze", "scan_used_fused", "scan_force_general", "scan_fused_variant",
-                    "scan_nccl_unique_id", "scan_create_sharded"]
+                    "scan_nccl_unique_id", "scan_create_sharded", "scan_align"]
 
 
 @dataclass
@@ -235,7 +247,7 @@ def scan_create_sharded(device: int, stream, n_shards: int, shard: int, unique_i
 
 
 def scan_load_events(ctx, tp, pp, dp, rank_offsets, comm_offsets, comm_members, dur, kind_op, meta, comm, payload,
-                     flags: int = SCAN_HOST_PTRS, keep: list | None = None):
+                     flags: int = SCAN_HOST_PTRS, keep: list | None = None, start_ns=None):
     lib = _load_lib()
     ro = np.ascontiguousarray(rank_offsets, dtype=np.uint64)
     co = np.ascontiguousarray(comm_offsets, dtype=np.uint64)
@@ -244,8 +256,15 @@ def scan_load_events(ctx, tp, pp, dp, rank_offsets, comm_offsets, comm_members, 
         keep += [ro, co, cm]
     topo = _Topo(tp, pp, dp, 0)
     comms = _Comms(len(co) - 1, co.ctypes.data, cm.ctypes.data if len(cm) else None)
-    cols = _Cols(int(ro[-1]), ro.ctypes.data, None, _ptr(dur), _ptr(kind_op), _ptr(meta), _ptr(comm), _ptr(payload))
+    cols = _Cols(int(ro[-1]), ro.ctypes.data, _ptr(start_ns), _ptr(dur), _ptr(kind_op), _ptr(meta), _ptr(comm), _ptr(payload))
     return _check(ctx, lib.scan_load_events(ctx, ctypes.byref(topo), ctypes.byref(comms), ctypes.byref(cols), flags))
+
+
+def scan_align(ctx, reference: int = 0) -> dict:
+    """NEXT-1 timeline alignment (scan.h): needs start_ns at load and a completed analysis."""
+    r = _AlignRes()
+    _check(ctx, _load_lib().scan_align(ctx, ctypes.byref(_AlignCfg(int(reference), 0)), ctypes.byref(r)))
+    return {n: getattr(r, n) for n, _ in r._fields_ if n != "reserved"}
 
 
 def scan_match_collectives(ctx) -> tuple[int, dict]:
@@ -343,16 +362,19 @@ class Scan:
         except Exception:
             pass
 
-    def load(self, trace, device_ptrs: bool = False, strict: bool = False, cols: dict | None = None):
+    def load(self, trace, device_ptrs: bool = False, strict: bool = False, cols: dict | None = None,
+             start: bool = False):
+        """``start=True`` also hands over ``start_ns`` (only the timeline alignment reads it)."""
         self._keep = [trace]
-        c = cols or {k: getattr(trace, k) for k in ("dur_ns", "kind_op", "meta", "comm", "payload")}
+        names = ("dur_ns", "kind_op", "meta", "comm", "payload") + (("start_ns",) if start else ())
+        c = cols or {k: getattr(trace, k) for k in names}
         if not device_ptrs:
             c = {k: np.ascontiguousarray(v) for k, v in c.items()}
         self._keep.append(c)
         flags = (SCAN_DEVICE_PTRS if device_ptrs else SCAN_HOST_PTRS) | (SCAN_STRICT if strict else 0)
         return scan_load_events(self.ctx, trace.tp, trace.pp, trace.dp, trace.rank_offsets, trace.comm_offsets,
                                 trace.comm_members, c["dur_ns"], c["kind_op"], c["meta"], c["comm"], c["payload"],
-                                flags, keep=self._keep)
+                                flags, keep=self._keep, start_ns=c.get("start_ns"))
 
     def match(self):
         return scan_match_collectives(self.ctx)
@@ -371,6 +393,10 @@ class Scan:
 
     def analyze(self, dcfg: DetectConfig | None = None, lcfg: LocalizeConfig | None = None) -> dict:
         return scan_analyze(self.ctx, dcfg, lcfg)
+
+    def align(self, reference: int = 0) -> dict:
+        """Timeline alignment onto ``reference``'s clock (load with ``start=True`` first)."""
+        return scan_align(self.ctx, reference)
 
     def fused_variant(self, variant: int):
         """-1 automatic, 0 generic tile kernel, 1 transposed warp-per-position kernel (next load)."""

@@ -70,7 +70,8 @@ static void release_all(Ctx& c) {
                     &c.st_tile0, &c.st_npos, &c.role_comm, &c.role_slot, &c.role_type, &c.ncroles, &c.ft_cols,
                     &c.ft_base, &c.ft_last, &c.st_tot, &c.sci, &c.sit, &c.dlate, &c.dinfo, &c.ft_posA, &c.ft_posB,
                     &c.ft_posK, &c.eidx, &c.tile_stage, &c.xbase, &c.lk_scratch, &c.g_base, &c.g_slot,
-                    &c.g_nmax, &c.g_nmin, &c.g_k0, &c.p2p_eslot, &c.x_send, &c.x_recv, &c.x_recv2, &c.x_ep, &c.x_stage, &c.headtail, &c.lk_sendmap, &c.lk_recvmap};
+                    &c.g_nmax, &c.g_nmin, &c.g_k0, &c.p2p_eslot, &c.own_start, &c.al_tend, &c.al_aend, &c.al_anct,
+                    &c.al_anco, &c.al_slotci, &c.al_level, &c.al_nanc, &c.al_resid, &c.al_flag, &c.al_start, &c.al_ranks, &c.x_send, &c.x_recv, &c.x_recv2, &c.x_ep, &c.x_stage, &c.headtail, &c.lk_sendmap, &c.lk_recvmap};
   for (DevBuf* b : bufs) b->release();
 }
 
@@ -123,7 +124,8 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
   Ctx& c = ctx->c;
   CK(cudaSetDevice(c.device));
   c.loaded = c.matched = c.detected = c.localized = false;
-  c.fused_used = false; c.tiles_ready = false; c.xwait_pending = false;
+  c.fused_used = false; c.tiles_ready = false; c.xwait_pending = false; c.aligned = false;
+  c.d_start = nullptr;
   c.err.clear();
   if (topo->tp < 1 || topo->pp < 1 || topo->dp < 1 || topo->rank_order != 0) {
     c.err = "topology: tp, pp, dp must be >= 1 and rank_order 0";
@@ -202,7 +204,7 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
   }
   rt0[W] = (uint32_t)trank.size();
   c.TP = topo->tp; c.PP = topo->pp; c.DP = topo->dp; c.W = W; c.n_comms = nc; c.N = N; c.flags = flags;
-  c.h_ccls = ccls; c.h_coff = coff;
+  c.h_ccls = ccls; c.h_coff = coff; c.h_cmem = cmem; c.h_rcomm = rcm; c.h_rcomm_off = rco;
   c.h_rank_off = ro; c.h_rank_tile0 = rt0; c.n_tiles = trank.size(); c.nnz_c = nb.size();
   scan_status st;
   if ((st = upload(c, c.rank_off, ro)) || (st = upload(c, c.coff, coff)) || (st = upload(c, c.cmem, cmem)) ||
@@ -293,6 +295,8 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
     for (const void* p : ptrs)
       if (N && ((uintptr_t)p & 15)) { c.err = "device columns must be 16-byte aligned"; return SCAN_E_INVALID_ARG; }
     c.d_dur = cols->dur_ns; c.d_kind = cols->kind_op; c.d_meta = cols->meta; c.d_comm = cols->comm; c.d_pay = cols->payload_bytes;
+    if (cols->start_ns && ((uintptr_t)cols->start_ns & 15)) { c.err = "device columns must be 16-byte aligned"; return SCAN_E_INVALID_ARG; }
+    c.d_start = cols->start_ns;
   } else {
     CK(c.own_dur.ensure(N * 4)); CK(c.own_kind.ensure(N * 2)); CK(c.own_meta.ensure(N * 2));
     CK(c.own_comm.ensure(N * 4)); CK(c.own_pay.ensure(N * 4));
@@ -302,6 +306,11 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
       CK(cudaMemcpyAsync(c.own_meta.p, cols->meta, N * 2, cudaMemcpyHostToDevice, c.stream));
       CK(cudaMemcpyAsync(c.own_comm.p, cols->comm, N * 4, cudaMemcpyHostToDevice, c.stream));
       CK(cudaMemcpyAsync(c.own_pay.p, cols->payload_bytes, N * 4, cudaMemcpyHostToDevice, c.stream));
+    }
+    if (cols->start_ns) {  // only the timeline alignment reads start times
+      CK(c.own_start.ensure(N * 8));
+      if (N) CK(cudaMemcpyAsync(c.own_start.p, cols->start_ns, N * 8, cudaMemcpyHostToDevice, c.stream));
+      c.d_start = c.own_start.as<int64_t>();
     }
     c.d_dur = c.own_dur.as<uint32_t>(); c.d_kind = c.own_kind.as<uint16_t>(); c.d_meta = c.own_meta.as<uint16_t>();
     c.d_comm = c.own_comm.as<uint32_t>(); c.d_pay = c.own_pay.as<uint32_t>();
@@ -669,6 +678,24 @@ scan_status scan_analyze(scan_ctx* ctx, const scan_detect_config* dcfg, const sc
 
 int scan_used_fused(const scan_ctx* ctx) { return ctx && ctx->c.fused_used ? 1 : 0; }
 
+// ----------------------------------------------------------------------------- NEXT-1 alignment
+scan_status scan_align(scan_ctx* ctx, const scan_align_config* cfg, scan_align_result* out) {
+  if (!ctx) return SCAN_E_INVALID_ARG;
+  Ctx& c = ctx->c;
+  if (!c.matched) { c.err = "scan_align before scan_analyze / scan_match_collectives"; return SCAN_E_ORDER; }
+  if (c.n_shards > 1) { c.err = "scan_align on a sharded context is not supported"; return SCAN_E_UNSUPPORTED; }
+  if (!c.d_start) { c.err = "scan_align needs start_ns at scan_load_events"; return SCAN_E_INVALID_ARG; }
+  const int32_t ref = cfg ? cfg->reference : 0;
+  if (ref < 0 || ref >= c.W) { c.err = "reference rank out of range"; return SCAN_E_INVALID_ARG; }
+  CK(cudaSetDevice(c.device));
+  scan_status st = ensure_tiles(c);
+  if (st) return st;
+  c.aligned = false;
+  if ((st = align_all(c, ref, out))) return st;
+  c.aligned = true;
+  return SCAN_OK;
+}
+
 scan_status scan_fused_variant(scan_ctx* ctx, int variant) {
   if (!ctx || variant < -1 || variant > 1) return SCAN_E_INVALID_ARG;
   ctx->c.fused_variant = variant;
@@ -684,6 +711,22 @@ scan_status scan_force_general(scan_ctx* ctx, int force) {
 }  // extern "C"
 
 // ----------------------------------------------------------------------------- exports
+// general tile prefixes (per 2048-event tile: comm / iteration counts) for event-order work after a
+// fused analysis: built once per analysis, outside the timed step
+scan_status ms::ensure_tiles(Ctx& c) {
+  if (c.tiles_ready) return SCAN_OK;
+  const uint64_t T = std::max<uint64_t>(c.n_tiles, 1);
+  CK(c.t_nkeys.ensure(T * 4)); CK(c.t_keys.ensure(T * KCAP * 4)); CK(c.t_cnt.ensure(T * KCAP * 4));
+  CK(c.t_pref.ensure(T * KCAP * 4)); CK(c.t_ncomm.ensure(T * 4)); CK(c.t_niter.ensure(T * 4)); CK(c.t_last.ensure(T * 4));
+  CK(c.t_commpre.ensure(T * 4)); CK(c.t_iterpre.ensure(T * 4)); CK(c.t_prevj.ensure(T * 4));
+  launch_tile_scan(c);
+  launch_rank_scan(c);
+  CK(cudaStreamSynchronize(c.stream));
+  CK(cudaGetLastError());
+  c.tiles_ready = true;
+  return SCAN_OK;
+}
+
 namespace {
 
 struct OutDesc { const DevBuf* buf; uint64_t off_bytes; uint64_t bytes; int stage; };
@@ -808,6 +851,10 @@ bool direct(Ctx& c, scan_output which, OutDesc& d) {
     case SCAN_OUT_COMM_INST: d = {&c.inst_c, 0, c.n_comm * 4, 1}; return true;
     case SCAN_OUT_COMM_WAIT: d = {&c.wait_c, 0, c.n_comm * 4, 3}; return true;
     case SCAN_OUT_SLOW_BITS: d = {&c.bits, 0, c.n_bits_words * 4, 2}; return true;
+    case SCAN_OUT_AL_START: d = {&c.al_start, 0, c.aligned ? c.N * 8 : 0, 1}; return true;
+    case SCAN_OUT_AL_LEVEL: d = {&c.al_level, 0, c.aligned ? W * 4 : 0, 1}; return true;
+    case SCAN_OUT_AL_NANCHOR: d = {&c.al_nanc, 0, c.aligned ? W * 4 : 0, 1}; return true;
+    case SCAN_OUT_AL_RESIDUAL: d = {&c.al_resid, 0, c.aligned ? W * 8 : 0, 1}; return true;
     default: return false;
   }
 }
@@ -843,6 +890,7 @@ scan_status scan_export(scan_ctx* ctx, scan_output which, void* dst, uint64_t ds
   if (!c.matched) { c.err = "nothing to export before scan_match_collectives"; return SCAN_E_ORDER; }
   CK(cudaSetDevice(c.device));
   const cudaMemcpyKind kind = dst_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (which >= SCAN_OUT_AL_START && which <= SCAN_OUT_AL_RESIDUAL && !c.aligned) { c.err = "scan_align not run"; return SCAN_E_ORDER; }
   if ((which == SCAN_OUT_COMM_WAIT || which == SCAN_OUT_EV_WAIT) && c.xwait_pending && c.localized) {
     launch_xwait_scatter(c);  // comm-order view of the cross-stage waits (once per analysis)
     CK(cudaStreamSynchronize(c.stream));
@@ -858,16 +906,9 @@ scan_status scan_export(scan_ctx* ctx, scan_output which, void* dst, uint64_t ds
     return SCAN_OK;
   }
   const bool ev = which <= SCAN_OUT_EV_REF, in = which >= SCAN_OUT_IN_CHANNEL && which <= SCAN_OUT_IN_PAYLOAD;
-  if (ev && !c.tiles_ready) {  // fused results: build the general tile prefixes once (untimed)
-    const uint64_t T = std::max<uint64_t>(c.n_tiles, 1);
-    CK(c.t_nkeys.ensure(T * 4)); CK(c.t_keys.ensure(T * KCAP * 4)); CK(c.t_cnt.ensure(T * KCAP * 4));
-    CK(c.t_pref.ensure(T * KCAP * 4)); CK(c.t_ncomm.ensure(T * 4)); CK(c.t_niter.ensure(T * 4)); CK(c.t_last.ensure(T * 4));
-    CK(c.t_commpre.ensure(T * 4)); CK(c.t_iterpre.ensure(T * 4)); CK(c.t_prevj.ensure(T * 4));
-    launch_tile_scan(c);
-    launch_rank_scan(c);
-    CK(cudaStreamSynchronize(c.stream));
-    CK(cudaGetLastError());
-    c.tiles_ready = true;
+  if (ev) {  // fused results: build the general tile prefixes once (untimed)
+    scan_status st = ensure_tiles(c);
+    if (st) return st;
   }
   if (ev || in) {
     const uint64_t nb = ev ? ev_bytes(c, which) : in_bytes(c, which);

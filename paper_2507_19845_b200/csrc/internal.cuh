@@ -80,6 +80,8 @@ struct Ctx {
   DevBuf own_dur, own_kind, own_meta, own_comm, own_pay;
   const uint32_t* d_dur = nullptr; const uint16_t* d_kind = nullptr; const uint16_t* d_meta = nullptr;
   const uint32_t* d_comm = nullptr; const uint32_t* d_pay = nullptr;
+  const int64_t* d_start = nullptr;      // optional (timeline alignment only)
+  DevBuf own_start;
   DevBuf rank_off;                 // u64 [W+1]
   DevBuf coff, cmem, ccls;         // comm table (u64, u32) + stage-2 class per comm (u8)
   DevBuf rcomm_off, rcomm;         // rank -> comms CSR (u32 offsets, u32)
@@ -158,6 +160,10 @@ struct Ctx {
   std::vector<uint32_t> h_shard_n;       // [NCH] this shard's instance count per channel
   std::vector<uint8_t> h_ccls;           // host copy of the stage-2 class per comm
   std::vector<uint64_t> h_coff;          // host copy of the comm offsets
+  std::vector<uint32_t> h_cmem, h_rcomm, h_rcomm_off;  // host copies: comm members, rank -> comms CSR
+  // timeline alignment (k_align.cu)
+  bool aligned = false;
+  DevBuf al_tend, al_aend, al_anct, al_anco, al_slotci, al_level, al_nanc, al_resid, al_flag, al_start, al_ranks;
   uint64_t g_N = 0, g_ncomm = 0, g_ncomp = 0;  // job-wide totals (sharded)
   DevBuf x_send, x_recv, x_recv2, x_ep, x_stage, headtail, lk_sendmap, lk_recvmap;
   void* h_pin = nullptr;                 // pinned host scratch (exchange read-backs, table staging)
@@ -217,6 +223,8 @@ scan_status alloc_match_buffers(Ctx& c, bool fused);
 scan_status alloc_detect(Ctx& c);
 scan_status alloc_localize(Ctx& c);
 scan_status sharded_all(Ctx& c);
+scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out);
+scan_status ensure_tiles(Ctx& c);
 void shard_release(Ctx& c);
 
 }  // namespace ms

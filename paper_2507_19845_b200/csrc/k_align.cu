@@ -1,0 +1,391 @@
+// k_align.cu — NEXT-1 timeline alignment (the members of a synchronous call
+// "logically finish at the same moment", which "provides anchor points"; a reference rank, the
+// others aligned to it "iteratively"; SPEC S:L243-300 ClockMap; readings AL1-AL6).
+//
+// After an analysis has matched the instances, every rank's local clock is mapped onto the
+// reference rank's:
+//   AL1 anchors = ends (start + dur) of a rank's collective events whose instance is VALID
+//   AL2 ranks are taken in BFS levels from the reference over "shares a valid collective instance";
+//       level-k ranks use members of levels < k only
+//   AL3 target = max aligned end over those members; anchor = (local end, target - local end) in
+//       program order, an end equal to the previous anchor's skipped; decreasing candidate ends on
+//       a rank -> SCAN_E_UNSUPPORTED
+//   AL4 offset(t): piecewise linear between anchors, floor((o1-o0)(t-t0)/(t1-t0)) in exact 128-bit
+//       integers, constant outside, 0 without anchors
+//   AL5 aligned start = start + offset(start); unreached ranks keep their clock (level -1)
+//   AL6 residual of a rank = max over its candidates of (instance's max aligned end - own)
+// Kernels: candidate ends + member-slot index (one warp per 2048-event tile, as the exports),
+// communicator reachability, monotonicity (one CTA per rank), per-level anchors (one CTA per rank:
+// block scans keep program order and compact), per-level aligned ends, aligned starts, residuals.
+#include <algorithm>
+#include <sstream>
+#include "internal.cuh"
+
+namespace ms {
+namespace {
+
+constexpr long long AL_NONE = (long long)0x8000000000000000ull;  // INT64_MIN: not a candidate
+constexpr int AL_NT = 1024;
+
+struct AlArgs {
+  const uint32_t* tile_rank; const uint64_t* tile_start; const uint64_t* rank_off; const uint16_t* kind;
+  const uint32_t* dur; const int64_t* start; uint64_t N, n_tiles;
+  const uint32_t* t_commpre; const uint64_t* r_comm_off;
+  const uint32_t* inst_c; const uint4* rec;
+  const uint64_t* ch_base; const uint64_t* ch_slot; uint64_t NCH;
+  const uint64_t* coff; const uint32_t* cmem;
+  long long* tend;   // [n_comm] local end of a candidate (AL1), AL_NONE otherwise
+  uint32_t* slotci;  // [n_slots] comm index of the member event of a candidate slot
+};
+
+__device__ __forceinline__ void inst_slot(const AlArgs& a, uint32_t inst, uint32_t r, uint64_t& ch, uint64_t& kk, uint32_t& nm,
+                                          uint64_t& s0) {
+  ch = upper_bound_u64(a.ch_base, a.NCH + 1, inst) - 1;
+  kk = inst - a.ch_base[ch];
+  nm = (uint32_t)(a.coff[ch + 1] - a.coff[ch]);
+  s0 = a.ch_slot[ch] + kk * nm;
+  (void)r;
+}
+
+// candidate ends and the slot -> comm index map (AL1)
+__global__ void __launch_bounds__(256) k_al_ends(AlArgs a) {
+  const uint64_t tile = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (tile >= a.n_tiles) return;
+  const uint32_t lane = lane_id();
+  const uint32_t r = a.tile_rank[tile];
+  const uint64_t s = a.tile_start[tile];
+  const uint64_t e = min(s + (uint64_t)TILE_EV, a.rank_off[r + 1]);
+  uint32_t comm_carry = a.t_commpre[tile];
+  const uint64_t co = a.r_comm_off[r];
+  for (uint64_t base = s & ~7ull; base < e; base += 256) {
+    const uint64_t g = base + 8ull * lane;
+    uint16_t ko[8];
+    load8_u16(a.kind, g, a.N, ko);
+    uint32_t valid = 0, commm = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint64_t ev = g + q;
+      if (ev < s || ev >= e) continue;
+      valid |= 1u << q;
+      if (ko[q] & 7u) commm |= 1u << q;
+    }
+    uint32_t ctot;
+    const uint32_t cex = warp_excl_scan(__popc(commm), ctot) + comm_carry;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (!((commm >> q) & 1u)) continue;
+      const uint64_t ev = g + q;
+      const uint64_t ci = co + cex + __popc(commm & ((1u << q) - 1u));
+      const uint32_t k = ko[q] & 7u;
+      long long t = AL_NONE;
+      if (k >= 1 && k <= 4) {
+        const uint32_t inst = a.inst_c[ci];
+        if (a.rec[inst].w & SCAN_F_VALID) {
+          t = (long long)a.start[ev] + (long long)a.dur[ev];
+          uint64_t ch, kk, s0; uint32_t nm;
+          inst_slot(a, inst, r, ch, kk, nm, s0);
+          const uint32_t m = lower_bound_u32(a.cmem + a.coff[ch], nm, r);
+          a.slotci[s0 + m] = (uint32_t)ci;
+        }
+      }
+      a.tend[ci] = t;
+    }
+    comm_carry += ctot;
+  }
+}
+
+// communicators with at least one valid instance connect their members (AL2)
+__global__ void k_al_commflag(uint32_t n_comms, const uint64_t* ch_base, const uint4* rec, uint8_t* flag) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_comms) return;
+  uint8_t f = 0;
+  for (uint64_t i = ch_base[c]; i < ch_base[c + 1] && !f; ++i) f = (rec[i].w & SCAN_F_VALID) ? 1 : 0;
+  flag[c] = f;
+}
+
+// block-wide exclusive max of i64 (AL_NONE as identity); total = max over the block
+__device__ long long block_excl_max_i64(long long v, long long& total, long long* sm /*[33]*/) {
+  const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+  long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= (uint32_t)o) x = max(x, y);
+  }
+  if (lane == 31) sm[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    long long w = lane < (blockDim.x >> 5) ? sm[lane] : AL_NONE;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+      if (lane >= (uint32_t)o) w = max(w, y);
+    }
+    sm[lane] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  const long long before_warp = wid ? sm[wid - 1] : AL_NONE;
+  long long ex = __shfl_up_sync(0xFFFFFFFFu, x, 1);
+  if (lane == 0) ex = AL_NONE;
+  total = sm[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return max(before_warp, ex);
+}
+
+// AL3 precondition: candidate ends non-decreasing along each rank's program order
+__global__ void __launch_bounds__(AL_NT) k_al_mono(const uint64_t* r_comm_off, const long long* tend, uint32_t* bad_rank) {
+  __shared__ long long sm[33];
+  __shared__ long long carry;
+  const uint32_t r = blockIdx.x;
+  const uint64_t c0 = r_comm_off[r], c1 = r_comm_off[r + 1];
+  if (threadIdx.x == 0) carry = AL_NONE;
+  __syncthreads();
+  for (uint64_t b = c0; b < c1; b += AL_NT) {
+    const uint64_t ci = b + threadIdx.x;
+    const long long t = ci < c1 ? tend[ci] : AL_NONE;
+    long long tot;
+    const long long prev = max(block_excl_max_i64(t, tot, sm), carry);
+    if (t != AL_NONE && t < prev) atomicMin(bad_rank, r);
+    __syncthreads();
+    if (threadIdx.x == 0) carry = max(carry, tot);
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ long long al_offset(const long long* at, const long long* ao, uint32_t n, long long t) {
+  if (n == 0) return 0;
+  if (t <= at[0]) return ao[0];
+  if (t >= at[n - 1]) return ao[n - 1];
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t m = (lo + hi) >> 1;
+    if (at[m] <= t) lo = m + 1; else hi = m;
+  }
+  const uint32_t i = lo - 1;  // at[i] <= t < at[i+1]
+  const __int128 o0 = ao[i], o1 = ao[i + 1], t0 = at[i], t1 = at[i + 1];
+  const __int128 num = (o1 - o0) * ((__int128)t - t0), den = t1 - t0;
+  __int128 q = num / den;
+  if ((num % den) != 0 && num < 0) q -= 1;  // floor (den > 0)
+  return (long long)(o0 + q);
+}
+
+struct AnchorArgs {
+  AlArgs a;
+  const uint32_t* ranks;  // ranks of this level
+  const int32_t* level; int32_t k;
+  const long long* aend;  // aligned ends of earlier levels' candidates
+  long long* anc_t; long long* anc_o; uint32_t* nanc;
+};
+
+// AL3 for the ranks of level k: one CTA per rank, program order kept by block scans
+__global__ void __launch_bounds__(AL_NT) k_al_anchor(AnchorArgs A) {
+  const AlArgs& a = A.a;
+  __shared__ long long sm[33];
+  __shared__ uint32_t smu[33];
+  __shared__ long long last_t;
+  __shared__ uint32_t n_anc;
+  const uint32_t r = A.ranks[blockIdx.x];
+  const uint64_t c0 = a.r_comm_off[r], c1 = a.r_comm_off[r + 1];
+  if (threadIdx.x == 0) { last_t = AL_NONE; n_anc = 0; }
+  __syncthreads();
+  for (uint64_t b = c0; b < c1; b += AL_NT) {
+    const uint64_t ci = b + threadIdx.x;
+    const long long t = ci < c1 ? a.tend[ci] : AL_NONE;
+    bool have = false;
+    long long tgt = 0;
+    if (t != AL_NONE) {
+      uint64_t ch, kk, s0; uint32_t nm;
+      inst_slot(a, a.inst_c[ci], r, ch, kk, nm, s0);
+      for (uint32_t q = 0; q < nm; ++q) {
+        const uint32_t m = a.cmem[a.coff[ch] + q];
+        const int32_t lv = A.level[m];
+        if (m == r || lv < 0 || lv >= A.k) continue;
+        const long long v = A.aend[a.slotci[s0 + q]];
+        if (!have || v > tgt) tgt = v;
+        have = true;
+      }
+    }
+    long long tot;
+    const long long prev = max(block_excl_max_i64(have ? t : AL_NONE, tot, sm), last_t);
+    const bool anc = have && t > prev;
+    uint32_t ntot;
+    const uint32_t pos = block_excl_sum<AL_NT>(anc ? 1u : 0u, ntot, smu);
+    if (anc) {
+      A.anc_t[c0 + n_anc + pos] = t;
+      A.anc_o[c0 + n_anc + pos] = tgt - t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) { last_t = max(last_t, tot); n_anc += ntot; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) A.nanc[r] = n_anc;
+}
+
+// aligned ends of the candidates of level-k ranks (level 0: the reference, offset 0)
+__global__ void k_al_eval(uint64_t n_comm, int W, const uint64_t* r_comm_off, const int32_t* level, int32_t k,
+                          const long long* tend, const long long* anc_t, const long long* anc_o, const uint32_t* nanc,
+                          long long* aend) {
+  for (uint64_t ci = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; ci < n_comm; ci += (uint64_t)gridDim.x * blockDim.x) {
+    const long long t = tend[ci];
+    if (t == AL_NONE) continue;
+    const uint32_t r = (uint32_t)(upper_bound_u64(r_comm_off, (uint64_t)W + 1, ci) - 1);
+    if (level[r] != k) continue;
+    const uint64_t c0 = r_comm_off[r];
+    aend[ci] = t + al_offset(anc_t + c0, anc_o + c0, nanc[r], t);
+  }
+}
+
+// AL5: aligned start of every event
+__global__ void k_al_apply(uint64_t N, int W, const uint64_t* rank_off, const uint64_t* r_comm_off, const int32_t* level,
+                           const int64_t* start, const long long* anc_t, const long long* anc_o, const uint32_t* nanc,
+                           long long* out) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = (uint32_t)(upper_bound_u64(rank_off, (uint64_t)W + 1, e) - 1);
+    const long long s = start[e];
+    if (level[r] < 0) { out[e] = s; continue; }
+    const uint64_t c0 = r_comm_off[r];
+    out[e] = s + al_offset(anc_t + c0, anc_o + c0, nanc[r], s);
+  }
+}
+
+// AL6 residuals (ranks reached by the BFS)
+__global__ void k_al_residual(AlArgs a, uint64_t n_comm, int W, const int32_t* level, const long long* aend,
+                              unsigned long long* resid) {
+  for (uint64_t ci = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; ci < n_comm; ci += (uint64_t)gridDim.x * blockDim.x) {
+    if (a.tend[ci] == AL_NONE) continue;
+    const uint32_t r = (uint32_t)(upper_bound_u64(a.r_comm_off, (uint64_t)W + 1, ci) - 1);
+    if (level[r] < 0) continue;
+    uint64_t ch, kk, s0; uint32_t nm;
+    inst_slot(a, a.inst_c[ci], r, ch, kk, nm, s0);
+    long long fin = AL_NONE;
+    for (uint32_t q = 0; q < nm; ++q) {
+      const uint32_t m = a.cmem[a.coff[ch] + q];
+      if (level[m] >= 0) fin = max(fin, aend[a.slotci[s0 + q]]);
+    }
+    const unsigned long long d = (unsigned long long)(fin - aend[ci]);
+    if (d) atomicMax(&resid[r], d);
+  }
+}
+
+}  // namespace
+
+scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
+  const uint64_t W = c.W, nc = c.n_comm;
+  CK(c.al_tend.ensure(std::max<uint64_t>(nc, 1) * 8)); CK(c.al_aend.ensure(std::max<uint64_t>(nc, 1) * 8));
+  CK(c.al_anct.ensure(std::max<uint64_t>(nc, 1) * 8)); CK(c.al_anco.ensure(std::max<uint64_t>(nc, 1) * 8));
+  CK(c.al_slotci.ensure(std::max<uint64_t>(c.n_slots, 1) * 4)); CK(c.al_level.ensure(W * 4));
+  CK(c.al_nanc.ensure(W * 4)); CK(c.al_resid.ensure(W * 8));
+  CK(c.al_flag.ensure(((c.n_comms + 3) & ~3u) + 4));  // per-comm flags, then the first bad rank (u32)
+  CK(c.al_start.ensure(std::max<uint64_t>(c.N, 1) * 8)); CK(c.al_ranks.ensure(W * 4));
+  AlArgs a{c.tile_rank.as<uint32_t>(), c.tile_start.as<uint64_t>(), c.rank_off.as<uint64_t>(), c.d_kind, c.d_dur, c.d_start,
+           c.N, c.n_tiles, c.t_commpre.as<uint32_t>(), c.r_comm_off.as<uint64_t>(), c.inst_c.as<uint32_t>(),
+           c.inst_rec.as<uint4>(), c.ch_base.as<uint64_t>(), c.ch_slot.as<uint64_t>(), c.NCH, c.coff.as<uint64_t>(),
+           c.cmem.as<uint32_t>(), c.al_tend.as<long long>(), c.al_slotci.as<uint32_t>()};
+  int launches = 0;
+  if (c.n_tiles) launches += timed(c, "k_al_ends", [&] { k_al_ends<<<(unsigned)((c.n_tiles + 7) / 8), 256, 0, c.stream>>>(a); return 1; });
+  if (c.n_comms)
+    launches += timed(c, "k_al_commflag", [&] {
+      k_al_commflag<<<(c.n_comms + 255) / 256, 256, 0, c.stream>>>(c.n_comms, c.ch_base.as<uint64_t>(), c.inst_rec.as<uint4>(),
+                                                                   c.al_flag.as<uint8_t>());
+      return 1;
+    });
+  uint32_t* bad = reinterpret_cast<uint32_t*>(c.al_flag.as<uint8_t>() + ((c.n_comms + 3) & ~3u));
+  CK(cudaMemsetAsync(bad, 0xFF, 4, c.stream));
+  launches += timed(c, "k_al_mono", [&] {
+    k_al_mono<<<(unsigned)W, AL_NT, 0, c.stream>>>(c.r_comm_off.as<uint64_t>(), c.al_tend.as<long long>(), bad);
+    return 1;
+  });
+  std::vector<uint8_t> flag(c.n_comms + 8);
+  uint32_t bad_rank = 0;
+  if (c.n_comms) CK(cudaMemcpyAsync(flag.data(), c.al_flag.p, c.n_comms, cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaMemcpyAsync(&bad_rank, bad, 4, cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  CK(cudaGetLastError());
+  if (bad_rank != NONE32) {
+    std::ostringstream m;
+    m << "timeline alignment: collective end times decrease along the program order of rank " << bad_rank;
+    c.err = m.str();
+    return SCAN_E_UNSUPPORTED;
+  }
+  // AL2: BFS levels on the host over the communicators that have a valid instance
+  std::vector<int32_t> level(W, -1);
+  std::vector<uint32_t> order{(uint32_t)ref};
+  level[ref] = 0;
+  for (size_t q = 0; q < order.size(); ++q) {
+    const uint32_t u = order[q];
+    for (uint32_t x = c.h_rcomm_off[u]; x < c.h_rcomm_off[u + 1]; ++x) {
+      const uint32_t k = c.h_rcomm[x];
+      if (!flag[k]) continue;
+      for (uint64_t y = c.h_coff[k]; y < c.h_coff[k + 1]; ++y) {
+        const uint32_t v = c.h_cmem[y];
+        if (level[v] < 0) { level[v] = level[u] + 1; order.push_back(v); }
+      }
+    }
+  }
+  int32_t maxlev = 0;
+  for (int32_t l : level) maxlev = std::max(maxlev, l);
+  std::vector<uint32_t> by_level;  // ranks grouped by level (ascending)
+  std::vector<uint32_t> lvl_off(maxlev + 2, 0);
+  for (uint64_t r = 0; r < W; ++r) if (level[r] >= 0) ++lvl_off[level[r] + 1];
+  for (int32_t l = 0; l <= maxlev; ++l) lvl_off[l + 1] += lvl_off[l];
+  by_level.resize(lvl_off[maxlev + 1]);
+  {
+    std::vector<uint32_t> fill(lvl_off.begin(), lvl_off.end() - 1);
+    for (uint64_t r = 0; r < W; ++r) if (level[r] >= 0) by_level[fill[level[r]]++] = (uint32_t)r;
+  }
+  scan_status st;
+  if ((st = upload(c, c.al_level, level)) || (st = upload(c, c.al_ranks, by_level))) return st;
+  CK(cudaMemsetAsync(c.al_nanc.p, 0, W * 4, c.stream));
+  CK(cudaMemsetAsync(c.al_resid.p, 0, W * 8, c.stream));
+  const unsigned eg = (unsigned)std::min<uint64_t>((nc + 255) / 256, 148ull * 16);
+  auto eval = [&](int32_t k) {
+    if (nc)
+      launches += timed(c, "k_al_eval", [&] {
+        k_al_eval<<<eg, 256, 0, c.stream>>>(nc, c.W, c.r_comm_off.as<uint64_t>(), c.al_level.as<int32_t>(), k,
+                                            c.al_tend.as<long long>(), c.al_anct.as<long long>(), c.al_anco.as<long long>(),
+                                            c.al_nanc.as<uint32_t>(), c.al_aend.as<long long>());
+        return 1;
+      });
+  };
+  eval(0);
+  for (int32_t k = 1; k <= maxlev; ++k) {
+    const uint32_t n = lvl_off[k + 1] - lvl_off[k];
+    AnchorArgs A{a, c.al_ranks.as<uint32_t>() + lvl_off[k], c.al_level.as<int32_t>(), k, c.al_aend.as<long long>(),
+                 c.al_anct.as<long long>(), c.al_anco.as<long long>(), c.al_nanc.as<uint32_t>()};
+    if (n) launches += timed(c, "k_al_anchor", [&] { k_al_anchor<<<n, AL_NT, 0, c.stream>>>(A); return 1; });
+    eval(k);
+  }
+  if (c.N)
+    launches += timed(c, "k_al_apply", [&] {
+      k_al_apply<<<(unsigned)std::min<uint64_t>((c.N + 255) / 256, 148ull * 32), 256, 0, c.stream>>>(
+          c.N, c.W, c.rank_off.as<uint64_t>(), c.r_comm_off.as<uint64_t>(), c.al_level.as<int32_t>(), c.d_start,
+          c.al_anct.as<long long>(), c.al_anco.as<long long>(), c.al_nanc.as<uint32_t>(), c.al_start.as<long long>());
+      return 1;
+    });
+  if (nc)
+    launches += timed(c, "k_al_residual", [&] {
+      k_al_residual<<<eg, 256, 0, c.stream>>>(a, nc, c.W, c.al_level.as<int32_t>(), c.al_aend.as<long long>(),
+                                              c.al_resid.as<unsigned long long>());
+      return 1;
+    });
+  std::vector<uint32_t> nanc(W);
+  std::vector<uint64_t> resid(W);
+  CK(cudaMemcpyAsync(nanc.data(), c.al_nanc.p, W * 4, cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaMemcpyAsync(resid.data(), c.al_resid.p, W * 8, cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  CK(cudaGetLastError());
+  resolve_timing(c);
+  c.launches += launches;
+  if (out) {
+    out->n_anchors = 0; out->n_aligned_ranks = 0; out->n_unaligned_ranks = 0; out->max_level = (uint32_t)maxlev;
+    out->max_residual_ns = 0;
+    for (uint64_t r = 0; r < W; ++r) {
+      out->n_anchors += nanc[r];
+      if (level[r] >= 0) ++out->n_aligned_ranks; else ++out->n_unaligned_ranks;
+      out->max_residual_ns = std::max<uint64_t>(out->max_residual_ns, resid[r]);
+    }
+  }
+  return SCAN_OK;
+}
+
+}  // namespace ms
