@@ -71,7 +71,7 @@ static void release_all(Ctx& c) {
                     &c.ft_base, &c.ft_last, &c.st_tot, &c.sci, &c.sit, &c.dlate, &c.dinfo, &c.ft_posA, &c.ft_posB,
                     &c.ft_posK, &c.eidx, &c.tile_stage, &c.xbase, &c.lk_scratch, &c.g_base, &c.g_slot,
                     &c.g_nmax, &c.g_nmin, &c.g_k0, &c.p2p_eslot, &c.own_start, &c.al_tend, &c.al_aend, &c.al_anct,
-                    &c.al_anco, &c.al_slotci, &c.al_level, &c.al_nanc, &c.al_resid, &c.al_flag, &c.al_start, &c.al_ranks, &c.x_send, &c.x_recv, &c.x_recv2, &c.x_ep, &c.x_stage, &c.headtail, &c.lk_sendmap, &c.lk_recvmap};
+                    &c.al_anco, &c.al_slotci, &c.al_level, &c.al_nanc, &c.al_resid, &c.al_flag, &c.al_start, &c.al_ranks, &c.al_cch, &c.al_tgt, &c.x_send, &c.x_recv, &c.x_recv2, &c.x_ep, &c.x_stage, &c.headtail, &c.lk_sendmap, &c.lk_recvmap};
   for (DevBuf* b : bufs) b->release();
 }
 

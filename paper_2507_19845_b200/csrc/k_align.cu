@@ -36,15 +36,14 @@ struct AlArgs {
   const uint64_t* coff; const uint32_t* cmem;
   long long* tend;   // [n_comm] local end of a candidate (AL1), AL_NONE otherwise
   uint32_t* slotci;  // [n_slots] comm index of the member event of a candidate slot
+  const uint32_t* comm; uint32_t* cch;  // event communicator id -> [n_comm] channel of a candidate
 };
 
-__device__ __forceinline__ void inst_slot(const AlArgs& a, uint32_t inst, uint32_t r, uint64_t& ch, uint64_t& kk, uint32_t& nm,
-                                          uint64_t& s0) {
-  ch = upper_bound_u64(a.ch_base, a.NCH + 1, inst) - 1;
+// member slots of a collective instance: channel = communicator id (collective channels come first)
+__device__ __forceinline__ void inst_slot(const AlArgs& a, uint32_t inst, uint32_t ch, uint64_t& kk, uint32_t& nm, uint64_t& s0) {
   kk = inst - a.ch_base[ch];
   nm = (uint32_t)(a.coff[ch + 1] - a.coff[ch]);
   s0 = a.ch_slot[ch] + kk * nm;
-  (void)r;
 }
 
 // candidate ends and the slot -> comm index map (AL1)
@@ -82,10 +81,12 @@ __global__ void __launch_bounds__(256) k_al_ends(AlArgs a) {
         const uint32_t inst = a.inst_c[ci];
         if (a.rec[inst].w & SCAN_F_VALID) {
           t = (long long)a.start[ev] + (long long)a.dur[ev];
-          uint64_t ch, kk, s0; uint32_t nm;
-          inst_slot(a, inst, r, ch, kk, nm, s0);
+          const uint32_t ch = a.comm[ev];
+          uint64_t kk, s0; uint32_t nm;
+          inst_slot(a, inst, ch, kk, nm, s0);
           const uint32_t m = lower_bound_u32(a.cmem + a.coff[ch], nm, r);
           a.slotci[s0 + m] = (uint32_t)ci;
+          a.cch[ci] = ch;
         }
       }
       a.tend[ci] = t;
@@ -152,32 +153,86 @@ __global__ void __launch_bounds__(AL_NT) k_al_mono(const uint64_t* r_comm_off, c
   }
 }
 
-__device__ __forceinline__ long long al_offset(const long long* at, const long long* ao, uint32_t n, long long t) {
-  if (n == 0) return 0;
-  if (t <= at[0]) return ao[0];
-  if (t >= at[n - 1]) return ao[n - 1];
+// index of the last anchor with at[i] <= t (-1 if none): binary search
+__device__ __forceinline__ int32_t al_find(const long long* at, uint32_t n, long long t) {
   uint32_t lo = 0, hi = n;
   while (lo < hi) {
     const uint32_t m = (lo + hi) >> 1;
     if (at[m] <= t) lo = m + 1; else hi = m;
   }
-  const uint32_t i = lo - 1;  // at[i] <= t < at[i+1]
-  const __int128 o0 = ao[i], o1 = ao[i + 1], t0 = at[i], t1 = at[i + 1];
-  const __int128 num = (o1 - o0) * ((__int128)t - t0), den = t1 - t0;
-  __int128 q = num / den;
-  if ((num % den) != 0 && num < 0) q -= 1;  // floor (den > 0)
-  return (long long)(o0 + q);
+  return (int32_t)lo - 1;
 }
+// floor(num / den), den > 0, exact: a double-precision estimate corrected by 128-bit multiplies (a
+// 128-bit division is a long software routine on the GPU); exact division for huge quotients
+__device__ __forceinline__ __int128 floor_div128(__int128 num, __int128 den) {
+  const double qd = floor((double)num / (double)den);
+  if (fabs(qd) > 1e15) {
+    __int128 q = num / den;
+    if ((num % den) != 0 && num < 0) q -= 1;
+    return q;
+  }
+  __int128 q = (__int128)(long long)qd;
+  __int128 r = num - q * den;
+  while (r < 0) { q -= 1; r += den; }
+  while (r >= den) { q += 1; r -= den; }
+  return q;
+}
+// offset at t given i = al_find(at, n, t): AL4
+__device__ __forceinline__ long long al_offset_at(const long long* at, const long long* ao, uint32_t n, int32_t i, long long t) {
+  if (n == 0) return 0;
+  if (i < 0) return ao[0];
+  if ((uint32_t)i >= n - 1) return ao[n - 1];
+  const __int128 o0 = ao[i], o1 = ao[i + 1], t0 = at[i], t1 = at[i + 1];
+  return (long long)(o0 + floor_div128((o1 - o0) * ((__int128)t - t0), t1 - t0));
+}
+// advance i to the interval of t when t did not decrease (program-order walk), else search
+__device__ __forceinline__ int32_t al_walk(const long long* at, uint32_t n, int32_t i, long long tprev, long long t) {
+  if (t < tprev) return al_find(at, n, t);
+  while (i + 1 < (int32_t)n && at[i + 1] <= t) ++i;
+  return i;
+}
+
+constexpr uint32_t AL_SPLIT = 16;  // CTAs per rank in the per-rank passes (blockIdx.y)
 
 struct AnchorArgs {
   AlArgs a;
   const uint32_t* ranks;  // ranks of this level
   const int32_t* level; int32_t k;
   const long long* aend;  // aligned ends of earlier levels' candidates
+  long long* tgt;         // [n_comm] scratch: target of a candidate, AL_NONE if none
   long long* anc_t; long long* anc_o; uint32_t* nanc;
 };
 
-// AL3 for the ranks of level k: one CTA per rank, program order kept by block scans
+// AL3 targets for every candidate of the level-k ranks (AL_SPLIT CTAs per rank, fully parallel)
+__global__ void __launch_bounds__(256) k_al_target(AnchorArgs A) {
+  const AlArgs& a = A.a;
+  const uint32_t r = A.ranks[blockIdx.x];
+  const uint64_t c0 = a.r_comm_off[r], c1 = a.r_comm_off[r + 1];
+  const uint64_t per = (c1 - c0 + AL_SPLIT - 1) / AL_SPLIT;
+  const uint64_t b = c0 + per * blockIdx.y, e = min(c1, b + per);
+  for (uint64_t ci = b + threadIdx.x; ci < e; ci += blockDim.x) {
+    long long tg = AL_NONE;
+    if (a.tend[ci] != AL_NONE) {
+      const uint32_t ch = a.cch[ci];
+      uint64_t kk, s0; uint32_t nm;
+      inst_slot(a, a.inst_c[ci], ch, kk, nm, s0);
+      bool have = false;
+      for (uint32_t q = 0; q < nm; ++q) {
+        const uint32_t m = a.cmem[a.coff[ch] + q];
+        const int32_t lv = A.level[m];
+        if (m == r || lv < 0 || lv >= A.k) continue;
+        const long long v = A.aend[a.slotci[s0 + q]];
+        if (!have || v > tg) tg = v;
+        have = true;
+      }
+      if (!have) tg = AL_NONE;
+    }
+    A.tgt[ci] = tg;
+  }
+}
+
+// AL3 anchors of the level-k ranks: one CTA per rank, program order kept by block scans (dedupe
+// against the previous anchor's end, stable compaction)
 __global__ void __launch_bounds__(AL_NT) k_al_anchor(AnchorArgs A) {
   const AlArgs& a = A.a;
   __shared__ long long sm[33];
@@ -190,29 +245,17 @@ __global__ void __launch_bounds__(AL_NT) k_al_anchor(AnchorArgs A) {
   __syncthreads();
   for (uint64_t b = c0; b < c1; b += AL_NT) {
     const uint64_t ci = b + threadIdx.x;
-    const long long t = ci < c1 ? a.tend[ci] : AL_NONE;
-    bool have = false;
-    long long tgt = 0;
-    if (t != AL_NONE) {
-      uint64_t ch, kk, s0; uint32_t nm;
-      inst_slot(a, a.inst_c[ci], r, ch, kk, nm, s0);
-      for (uint32_t q = 0; q < nm; ++q) {
-        const uint32_t m = a.cmem[a.coff[ch] + q];
-        const int32_t lv = A.level[m];
-        if (m == r || lv < 0 || lv >= A.k) continue;
-        const long long v = A.aend[a.slotci[s0 + q]];
-        if (!have || v > tgt) tgt = v;
-        have = true;
-      }
-    }
+    const long long tg = ci < c1 ? A.tgt[ci] : AL_NONE;
+    const bool have = tg != AL_NONE;
+    const long long t = have ? a.tend[ci] : AL_NONE;
     long long tot;
-    const long long prev = max(block_excl_max_i64(have ? t : AL_NONE, tot, sm), last_t);
+    const long long prev = max(block_excl_max_i64(t, tot, sm), last_t);
     const bool anc = have && t > prev;
     uint32_t ntot;
     const uint32_t pos = block_excl_sum<AL_NT>(anc ? 1u : 0u, ntot, smu);
     if (anc) {
       A.anc_t[c0 + n_anc + pos] = t;
-      A.anc_o[c0 + n_anc + pos] = tgt - t;
+      A.anc_o[c0 + n_anc + pos] = tg - t;
     }
     __syncthreads();
     if (threadIdx.x == 0) { last_t = max(last_t, tot); n_anc += ntot; }
@@ -221,50 +264,87 @@ __global__ void __launch_bounds__(AL_NT) k_al_anchor(AnchorArgs A) {
   if (threadIdx.x == 0) A.nanc[r] = n_anc;
 }
 
-// aligned ends of the candidates of level-k ranks (level 0: the reference, offset 0)
-__global__ void k_al_eval(uint64_t n_comm, int W, const uint64_t* r_comm_off, const int32_t* level, int32_t k,
-                          const long long* tend, const long long* anc_t, const long long* anc_o, const uint32_t* nanc,
-                          long long* aend) {
-  for (uint64_t ci = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; ci < n_comm; ci += (uint64_t)gridDim.x * blockDim.x) {
-    const long long t = tend[ci];
-    if (t == AL_NONE) continue;
-    const uint32_t r = (uint32_t)(upper_bound_u64(r_comm_off, (uint64_t)W + 1, ci) - 1);
-    if (level[r] != k) continue;
-    const uint64_t c0 = r_comm_off[r];
-    aend[ci] = t + al_offset(anc_t + c0, anc_o + c0, nanc[r], t);
+// aligned ends of the candidates of level-k ranks (level 0: the reference, offset 0): one CTA per
+// rank; a warp takes 1024-event chunks, lane l the events l, l+32, ... (coalesced), one interval
+// search per lane and chunk, then a walk (candidate ends are non-decreasing)
+__global__ void __launch_bounds__(256) k_al_eval(const uint32_t* ranks, const uint64_t* r_comm_off, const long long* tend,
+                                                 const long long* anc_t, const long long* anc_o, const uint32_t* nanc,
+                                                 long long* aend) {
+  const uint32_t r = ranks[blockIdx.x];
+  const uint64_t c0 = r_comm_off[r], c1 = r_comm_off[r + 1];
+  const long long* at = anc_t + c0;
+  const long long* ao = anc_o + c0;
+  const uint32_t n = nanc[r], lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint32_t part = blockIdx.y, warp_g = part * nw + wid, nwg = nw * gridDim.y;
+  for (uint64_t b = c0 + 1024ull * warp_g; b < c1; b += 1024ull * nwg) {
+    int32_t i = -2;
+    long long tp = 0;
+    for (uint64_t ci = b + lane; ci < min(c1, b + 1024); ci += 32) {
+      const long long t = tend[ci];
+      if (t == AL_NONE) continue;
+      i = i == -2 ? al_find(at, n, t) : al_walk(at, n, i, tp, t);
+      tp = t;
+      aend[ci] = t + al_offset_at(at, ao, n, i, t);
+    }
   }
 }
 
-// AL5: aligned start of every event
-__global__ void k_al_apply(uint64_t N, int W, const uint64_t* rank_off, const uint64_t* r_comm_off, const int32_t* level,
-                           const int64_t* start, const long long* anc_t, const long long* anc_o, const uint32_t* nanc,
-                           long long* out) {
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t r = (uint32_t)(upper_bound_u64(rank_off, (uint64_t)W + 1, e) - 1);
-    const long long s = start[e];
-    if (level[r] < 0) { out[e] = s; continue; }
-    const uint64_t c0 = r_comm_off[r];
-    out[e] = s + al_offset(anc_t + c0, anc_o + c0, nanc[r], s);
+// AL5: aligned start of every event; one warp per 2048-event tile (rank known), a lane 8
+// consecutive events: one interval search, then a program-order walk
+__global__ void __launch_bounds__(256) k_al_apply(uint64_t n_tiles, const uint32_t* tile_rank, const uint64_t* tile_start,
+                                                  const uint64_t* rank_off, const uint64_t* r_comm_off, const int32_t* level,
+                                                  const int64_t* start, const long long* anc_t, const long long* anc_o,
+                                                  const uint32_t* nanc, long long* out) {
+  const uint64_t tile = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (tile >= n_tiles) return;
+  const uint32_t lane = lane_id();
+  const uint32_t r = tile_rank[tile];
+  const uint64_t s = tile_start[tile];
+  const uint64_t e = min(s + (uint64_t)TILE_EV, rank_off[r + 1]);
+  const bool on = level[r] >= 0;
+  const uint64_t c0 = r_comm_off[r];
+  const long long* at = anc_t + c0;
+  const long long* ao = anc_o + c0;
+  const uint32_t n = on ? nanc[r] : 0u;
+  for (uint64_t g = s + 8ull * lane; g < e; g += 256) {
+    const uint64_t ge = min(g + 8, e);
+    int32_t i = -2;
+    long long tp = 0;
+    for (uint64_t ev = g; ev < ge; ++ev) {
+      const long long t = start[ev];
+      if (!on || n == 0) { out[ev] = t; continue; }
+      i = i == -2 ? al_find(at, n, t) : al_walk(at, n, i, tp, t);
+      tp = t;
+      out[ev] = t + al_offset_at(at, ao, n, i, t);
+    }
   }
 }
 
-// AL6 residuals (ranks reached by the BFS)
-__global__ void k_al_residual(AlArgs a, uint64_t n_comm, int W, const int32_t* level, const long long* aend,
-                              unsigned long long* resid) {
-  for (uint64_t ci = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; ci < n_comm; ci += (uint64_t)gridDim.x * blockDim.x) {
+// AL6 residuals: one CTA per reached rank, threads over its comm events
+__global__ void __launch_bounds__(256) k_al_residual(AlArgs a, const uint32_t* ranks, const int32_t* level,
+                                                     const long long* aend, unsigned long long* resid) {
+  __shared__ unsigned long long best;
+  const uint32_t r = ranks[blockIdx.x];
+  if (threadIdx.x == 0) best = 0;
+  __syncthreads();
+  unsigned long long mine = 0;
+  const uint64_t c0 = a.r_comm_off[r], c1 = a.r_comm_off[r + 1], per = (c1 - c0 + AL_SPLIT - 1) / AL_SPLIT;
+  const uint64_t b0 = c0 + per * blockIdx.y, e0 = min(c1, b0 + per);
+  for (uint64_t ci = b0 + threadIdx.x; ci < e0; ci += blockDim.x) {
     if (a.tend[ci] == AL_NONE) continue;
-    const uint32_t r = (uint32_t)(upper_bound_u64(a.r_comm_off, (uint64_t)W + 1, ci) - 1);
-    if (level[r] < 0) continue;
-    uint64_t ch, kk, s0; uint32_t nm;
-    inst_slot(a, a.inst_c[ci], r, ch, kk, nm, s0);
+    const uint32_t ch = a.cch[ci];
+    uint64_t kk, s0; uint32_t nm;
+    inst_slot(a, a.inst_c[ci], ch, kk, nm, s0);
     long long fin = AL_NONE;
     for (uint32_t q = 0; q < nm; ++q) {
       const uint32_t m = a.cmem[a.coff[ch] + q];
       if (level[m] >= 0) fin = max(fin, aend[a.slotci[s0 + q]]);
     }
-    const unsigned long long d = (unsigned long long)(fin - aend[ci]);
-    if (d) atomicMax(&resid[r], d);
+    mine = max(mine, (unsigned long long)(fin - aend[ci]));
   }
+  if (mine) atomicMax(&best, mine);
+  __syncthreads();
+  if (threadIdx.x == 0 && best) atomicMax(&resid[r], best);
 }
 
 }  // namespace
@@ -277,10 +357,11 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
   CK(c.al_nanc.ensure(W * 4)); CK(c.al_resid.ensure(W * 8));
   CK(c.al_flag.ensure(((c.n_comms + 3) & ~3u) + 4));  // per-comm flags, then the first bad rank (u32)
   CK(c.al_start.ensure(std::max<uint64_t>(c.N, 1) * 8)); CK(c.al_ranks.ensure(W * 4));
+  CK(c.al_cch.ensure(std::max<uint64_t>(nc, 1) * 4)); CK(c.al_tgt.ensure(std::max<uint64_t>(nc, 1) * 8));
   AlArgs a{c.tile_rank.as<uint32_t>(), c.tile_start.as<uint64_t>(), c.rank_off.as<uint64_t>(), c.d_kind, c.d_dur, c.d_start,
            c.N, c.n_tiles, c.t_commpre.as<uint32_t>(), c.r_comm_off.as<uint64_t>(), c.inst_c.as<uint32_t>(),
            c.inst_rec.as<uint4>(), c.ch_base.as<uint64_t>(), c.ch_slot.as<uint64_t>(), c.NCH, c.coff.as<uint64_t>(),
-           c.cmem.as<uint32_t>(), c.al_tend.as<long long>(), c.al_slotci.as<uint32_t>()};
+           c.cmem.as<uint32_t>(), c.al_tend.as<long long>(), c.al_slotci.as<uint32_t>(), c.d_comm, c.al_cch.as<uint32_t>()};
   int launches = 0;
   if (c.n_tiles) launches += timed(c, "k_al_ends", [&] { k_al_ends<<<(unsigned)((c.n_tiles + 7) / 8), 256, 0, c.stream>>>(a); return 1; });
   if (c.n_comms)
@@ -337,13 +418,13 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
   if ((st = upload(c, c.al_level, level)) || (st = upload(c, c.al_ranks, by_level))) return st;
   CK(cudaMemsetAsync(c.al_nanc.p, 0, W * 4, c.stream));
   CK(cudaMemsetAsync(c.al_resid.p, 0, W * 8, c.stream));
-  const unsigned eg = (unsigned)std::min<uint64_t>((nc + 255) / 256, 148ull * 16);
   auto eval = [&](int32_t k) {
-    if (nc)
+    const uint32_t n = lvl_off[k + 1] - lvl_off[k];
+    if (nc && n)
       launches += timed(c, "k_al_eval", [&] {
-        k_al_eval<<<eg, 256, 0, c.stream>>>(nc, c.W, c.r_comm_off.as<uint64_t>(), c.al_level.as<int32_t>(), k,
-                                            c.al_tend.as<long long>(), c.al_anct.as<long long>(), c.al_anco.as<long long>(),
-                                            c.al_nanc.as<uint32_t>(), c.al_aend.as<long long>());
+        k_al_eval<<<dim3(n, AL_SPLIT), 256, 0, c.stream>>>(c.al_ranks.as<uint32_t>() + lvl_off[k], c.r_comm_off.as<uint64_t>(),
+                                           c.al_tend.as<long long>(), c.al_anct.as<long long>(), c.al_anco.as<long long>(),
+                                           c.al_nanc.as<uint32_t>(), c.al_aend.as<long long>());
         return 1;
       });
   };
@@ -351,21 +432,25 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
   for (int32_t k = 1; k <= maxlev; ++k) {
     const uint32_t n = lvl_off[k + 1] - lvl_off[k];
     AnchorArgs A{a, c.al_ranks.as<uint32_t>() + lvl_off[k], c.al_level.as<int32_t>(), k, c.al_aend.as<long long>(),
-                 c.al_anct.as<long long>(), c.al_anco.as<long long>(), c.al_nanc.as<uint32_t>()};
-    if (n) launches += timed(c, "k_al_anchor", [&] { k_al_anchor<<<n, AL_NT, 0, c.stream>>>(A); return 1; });
+                 c.al_tgt.as<long long>(), c.al_anct.as<long long>(), c.al_anco.as<long long>(), c.al_nanc.as<uint32_t>()};
+    if (n) {
+      launches += timed(c, "k_al_target", [&] { k_al_target<<<dim3(n, AL_SPLIT), 256, 0, c.stream>>>(A); return 1; });
+      launches += timed(c, "k_al_anchor", [&] { k_al_anchor<<<n, AL_NT, 0, c.stream>>>(A); return 1; });
+    }
     eval(k);
   }
-  if (c.N)
+  if (c.n_tiles)
     launches += timed(c, "k_al_apply", [&] {
-      k_al_apply<<<(unsigned)std::min<uint64_t>((c.N + 255) / 256, 148ull * 32), 256, 0, c.stream>>>(
-          c.N, c.W, c.rank_off.as<uint64_t>(), c.r_comm_off.as<uint64_t>(), c.al_level.as<int32_t>(), c.d_start,
-          c.al_anct.as<long long>(), c.al_anco.as<long long>(), c.al_nanc.as<uint32_t>(), c.al_start.as<long long>());
+      k_al_apply<<<(unsigned)((c.n_tiles + 7) / 8), 256, 0, c.stream>>>(
+          c.n_tiles, c.tile_rank.as<uint32_t>(), c.tile_start.as<uint64_t>(), c.rank_off.as<uint64_t>(),
+          c.r_comm_off.as<uint64_t>(), c.al_level.as<int32_t>(), c.d_start, c.al_anct.as<long long>(),
+          c.al_anco.as<long long>(), c.al_nanc.as<uint32_t>(), c.al_start.as<long long>());
       return 1;
     });
-  if (nc)
+  if (nc && !by_level.empty())
     launches += timed(c, "k_al_residual", [&] {
-      k_al_residual<<<eg, 256, 0, c.stream>>>(a, nc, c.W, c.al_level.as<int32_t>(), c.al_aend.as<long long>(),
-                                              c.al_resid.as<unsigned long long>());
+      k_al_residual<<<dim3((unsigned)by_level.size(), AL_SPLIT), 256, 0, c.stream>>>(a, c.al_ranks.as<uint32_t>(), c.al_level.as<int32_t>(),
+                                                                     c.al_aend.as<long long>(), c.al_resid.as<unsigned long long>());
       return 1;
     });
   std::vector<uint32_t> nanc(W);
