@@ -783,7 +783,10 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
 #ifndef MS_FT_NT
 #define MS_FT_NT 512
 #endif
-constexpr int FT_NT = MS_FT_NT, FT_NW = FT_NT / 32, NRLM = 8, FT_MINB = 1024 / FT_NT;  // 32 warps per SM
+#ifndef MS_FT_MINB
+#define MS_FT_MINB (1024 / MS_FT_NT)
+#endif
+constexpr int FT_NT = MS_FT_NT, FT_NW = FT_NT / 32, NRLM = 8, FT_MINB = MS_FT_MINB;  // 32 warps per SM by default
 
 template <int P>
 __device__ __forceinline__ void loo_group(const FusedArgs& a, const uint32_t* col, uint32_t tp, uint32_t TP, uint32_t DP, uint32_t j,
@@ -1038,6 +1041,9 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
     const uint4 cd = cinf[jj];
     const uint32_t p = cd.x & 0x3FFFu, cls = (cd.x >> 14) & 3u;  // 0 TP, 1 DP, 2 cross
     if (cls == 1 && kb != 0) continue;  // a DP group spans every row block: one unit handles it
+#if defined(MS_EXP_SKIP) && (MS_EXP_SKIP & 1)
+    if (cls == 0) continue;  // timing experiment only (results invalid)
+#endif
     const uint32_t role = (cd.x >> 17) & 31u;
     const uint32_t itp = citp[jj];
     uint32_t* col = sd + p * RP;
@@ -1178,17 +1184,26 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
     }
   }
   __syncthreads();
-  // ---- (4) flush: coalesced per-rank inst / wait rows
-  for (uint32_t row = wid; row < R; row += FT_NW) {
-    for (uint32_t j = lane; j < ncm; j += 32) {
+  // ---- (4) flush: coalesced per-rank inst / wait rows; flat (row, comm position) pairs over all
+  // threads (a tile holds a few dozen comm positions: warp-per-row left most lanes idle)
+#if defined(MS_EXP_SKIP) && (MS_EXP_SKIP & 2)
+  if (R == 0)  // timing experiment only (results invalid)
+#endif
+  if (ncm) {
+    const FDiv fn = fdiv_make(ncm);  // exact for R * ncm < 2^22
+    for (uint32_t idx = tid; idx < R * ncm; idx += FT_NT) {
+      const uint32_t row = fdiv(idx, fn), j = idx - row * ncm;
       const uint32_t cv = cl[j];
       const uint32_t p = cv & 0x3FFFu, cls = cv >> 14;
       const uint32_t v = sd[p * RP + row];
       const uint32_t gi = cls == 0 ? row >> tpsh : row & (TP - 1u);
-      const uint32_t si = sinst[cls < 2 ? p * G + gi : 0u];
-      uint32_t* dst = a.inst_c + coffr[row] + m0 + j;
-      *dst = cls < 2 ? si : v;
-      if (cls < 2) a.wait_c[dst - a.inst_c] = v;
+      const uint64_t o = coffr[row] + m0 + j;
+      if (cls < 2) {
+        a.inst_c[o] = sinst[p * G + gi];
+        a.wait_c[o] = v;
+      } else {
+        a.inst_c[o] = v;  // cross positions: the tile holds the instance id
+      }
     }
   }
   // per-rank sums from the tile (compute positions hold durations, in-block comm positions hold waits):
@@ -1199,6 +1214,9 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
     const uint32_t row = rb * 32 + lane;
     const uint32_t plo = sl * ((np + NSL - 1) / NSL), phi = min(np, plo + (np + NSL - 1) / NSL);
     unsigned long long sc = 0, sw = 0;
+#if defined(MS_EXP_SKIP) && (MS_EXP_SKIP & 4)
+    if (R == 0)  // timing experiment only (results invalid)
+#endif
     if (row < R)
       for (uint32_t p = plo; p < phi; ++p) {
         const uint32_t pc = pcode[p];
