@@ -842,6 +842,7 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const uint32_t T = a.T, R = a.R, TP = (uint32_t)a.TP, DP = (uint32_t)a.DP, G = a.G;
   const uint32_t SW = T / 32 + 2, E = TP + DP, NCRM = a.NCRM, RP = R + 1;
+  const uint32_t GS = G | 1u, ES = E | 1u;  // odd shared-memory strides (bank-conflict-free columns)
   constexpr uint32_t nrb = NRB;        // row blocks (lane l owns rows l + 32k, k < NRB); R <= 32*NRB
   const uint32_t tpsh = __ffs(TP) - 1;  // TP is a power of two here
   // ---- shared memory carve-up: host-computed byte offsets from smem_raw (fused_t_layout), so every
@@ -897,7 +898,7 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
   if (tid < 4) nlist[tid] = 0;
   if (tid == 0) { dpos = -1; bad = 0; anyslow = 0; }
   for (uint32_t i = tid; i < R * SW; i += FT_NT) sbits[i] = 0;
-  for (uint32_t i = tid; i < R * E; i += FT_NT) sedge[i] = 0;
+  for (uint32_t i = tid; i < R * ES; i += FT_NT) sedge[i] = 0;
   for (uint32_t i = tid; i < 4 * R; i += FT_NT) rsum[i] = 0;
   for (uint32_t i = tid; i < 2 * (DP + TP); i += FT_NT) gsum[i] = 0;
   for (uint32_t i = tid; i < R; i += FT_NT) { sjoin[i] = 0; slate[i] = 0; coffr[i] = a.comm_off[sbase + i]; }
@@ -1104,7 +1105,7 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
         const uint64_t inst = rcb[row0 * NCRM + role] + kinst;
         a.rec[inst] = make_uint4(mn, mx, last, (SCAN_F_COMPLETE | SCAN_F_KIND_OK | SCAN_F_PAYLOAD_OK | SCAN_F_VALID |
                                                 (nat == 1 ? SCAN_F_UNIQUE_LAST : 0u)) | (clsid << 8));
-        sinst[p * G + g] = (uint32_t)inst;
+        sinst[p * GS + g] = (uint32_t)inst;
         const uint32_t gi = istp ? g : DP + g;
         add64_lohi(&gsum[gi], &gsum[DP + TP + gi], mn);
       }
@@ -1112,7 +1113,7 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
       col[row] = wait;  // in-block comm positions now hold the wait
       if (!islast && (unsigned long long)wait > a.wait_margin) {
         if (win == w_tile) {
-          const uint32_t old = atomicAdd(&sedge[row * E + slot], wait);
+          const uint32_t old = atomicAdd(&sedge[row * ES + slot], wait);
           if (old + wait < old)
             atomicAdd(&a.ew[(uint64_t)w_tile * a.nnz_tot + a.eidx[(uint64_t)(sbase + row) * E + slot]], 1ull << 32);
         } else {
@@ -1199,7 +1200,7 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
       const uint32_t gi = cls == 0 ? row >> tpsh : row & (TP - 1u);
       const uint64_t o = coffr[row] + m0 + j;
       if (cls < 2) {
-        a.inst_c[o] = sinst[p * G + gi];
+        a.inst_c[o] = sinst[p * GS + gi];
         a.wait_c[o] = v;
       } else {
         a.inst_c[o] = v;  // cross positions: the tile holds the instance id
@@ -1264,9 +1265,13 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
     if (sjoin[row]) atomicAdd(&a.wl_joined[(uint64_t)w_tile * a.W + r], sjoin[row]);
     if (slate[row]) atomicAdd(&a.wl_late[(uint64_t)w_tile * a.W + r], slate[row]);
   }
-  for (uint32_t i = tid; i < R * E; i += FT_NT) {
-    const uint32_t v = sedge[i];
-    if (v) atomicAdd(&a.ew[(uint64_t)w_tile * a.nnz_tot + a.eidx[(uint64_t)sbase * E + i]], (unsigned long long)v);
+  {
+    const FDiv fe = fdiv_make(ES);
+    for (uint32_t i = tid; i < R * ES; i += FT_NT) {
+      const uint32_t row = fdiv(i, fe), slot = i - row * ES;
+      const uint32_t v = slot < E ? sedge[i] : 0u;
+      if (v) atomicAdd(&a.ew[(uint64_t)w_tile * a.nnz_tot + a.eidx[(uint64_t)(sbase + row) * E + slot]], (unsigned long long)v);
+    }
   }
   if (nc && tslow) {
     const uint32_t w_first = j0 >> 5, w_last = (j0 + nc - 1) >> 5;
@@ -1294,8 +1299,8 @@ static size_t fused_t_layout(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, u
   size_t off = 0;
   auto take = [&](size_t bytes, size_t align) { off = (off + align - 1) & ~(align - 1); const size_t o = off; off += bytes; return (uint32_t)o; };
   take((size_t)T * RP * 4, 16);
-  const uint32_t o_rcb = take((size_t)R * NCRM * 8, 16), o_coffr = take((size_t)R * 8, 8), o_sinst = take((size_t)T * G * 4, 4);
-  const uint32_t o_sbits = take((size_t)R * SW * 4, 4), o_sedge = take((size_t)R * E * 4, 4), o_rcs = take((size_t)R * NCRM * 4, 4);
+  const uint32_t o_rcb = take((size_t)R * NCRM * 8, 16), o_coffr = take((size_t)R * 8, 8), o_sinst = take((size_t)T * (G | 1u) * 4, 4);
+  const uint32_t o_sbits = take((size_t)R * SW * 4, 4), o_sedge = take((size_t)R * (E | 1u) * 4, 4), o_rcs = take((size_t)R * NCRM * 4, 4);
   const uint32_t o_rsum = take((size_t)R * 16, 4), o_gsum = take((size_t)(DP + TP) * 8, 4), o_sjoin = take((size_t)R * 4, 4);
   const uint32_t o_slate = take((size_t)R * 4, 4), o_rslow = take((size_t)R * 4, 4), o_pa = take((size_t)T * 4, 16);
   const uint32_t o_pb = take((size_t)T * 4, 16), o_vd = take((size_t)T * 4, 16), o_pk = take((size_t)T * 2, 16);
