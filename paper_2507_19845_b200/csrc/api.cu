@@ -578,12 +578,13 @@ scan_status fused_all(Ctx& c) {
   c.launches += timed(c, "k_cross_reduce", [&] { return launch_cross_reduce(c); });
   c.launches += timed(c, "k_deferred", [&] { return launch_deferred(c); });
   c.launches += timed(c, "k_wd_finish", [&] { return launch_wd_finish(c); });
-  if ((st = sync_read(c))) return st;
-  if (c.hc.overflow & 32u) return 2;
-  c.matched = c.detected = true;
+  // links and walk run before the SPMD verification result is read (one host sync less): on a
+  // failed verification their inputs are garbage but in bounds, and the call reruns the general path
   c.launches += timed(c, "k_links", [&] { return launch_links(c); });
   c.launches += timed(c, "k_walk", [&] { return launch_verdict_walk(c); });
   if ((st = sync_read(c))) return st;
+  if (c.hc.overflow & 32u) return 2;
+  c.matched = c.detected = true;
   if (c.hc.overflow & 24u) {
     c.err = "capacity exceeded: more than 16384 samples on a link / links in a direction class";
     return SCAN_E_UNSUPPORTED;
