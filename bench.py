@@ -253,6 +253,9 @@ def main():
 
     for _ in range(args.warmup):
         step()
+    import gc
+    gc.collect()
+    gc.disable()  # no collector pauses inside the timed steps (a late rank stalls every other at the first exchange)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -265,6 +268,7 @@ def main():
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
+    gc.enable()
     ms_total = ev0.elapsed_time(ev1)
     launches = s.kernel_launches()
     kernels = s.kernel_timing() if args.breakdown else {}

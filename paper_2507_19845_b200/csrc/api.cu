@@ -19,7 +19,41 @@ void ms::resolve_timing(Ctx& c) {
 }
 
 
+namespace {
+constexpr int FILL_MAX = 24;
+struct FillArgs { uint8_t* p[FILL_MAX]; uint64_t n[FILL_MAX]; uint32_t v[FILL_MAX]; int k; };
+// byte fills of up to FILL_MAX segments: 16-byte stores on the aligned body, bytes at the ends
+__global__ void k_fill(FillArgs a) {
+  const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, st = (uint64_t)gridDim.x * blockDim.x;
+  for (int s = 0; s < a.k; ++s) {
+    uint8_t* p = a.p[s];
+    const uint64_t n = a.n[s];
+    const uint32_t b = a.v[s] & 0xFFu, w = b * 0x01010101u;
+    const uint64_t h16 = (16 - ((uintptr_t)p & 15)) & 15, head = n < h16 ? n : h16, nv = (n - head) / 16;
+    for (uint64_t i = t0; i < head; i += st) p[i] = (uint8_t)b;
+    uint4* q = reinterpret_cast<uint4*>(p + head);
+    for (uint64_t i = t0; i < nv; i += st) q[i] = make_uint4(w, w, w, w);
+    for (uint64_t i = head + nv * 16 + t0; i < n; i += st) p[i] = (uint8_t)b;
+  }
+}
+}  // namespace
+
+int ms::flush_fills(Ctx& c) {
+  for (size_t i = 0; i < c.fills.size(); i += FILL_MAX) {
+    FillArgs a{};
+    a.k = (int)std::min<size_t>(FILL_MAX, c.fills.size() - i);
+    for (int j = 0; j < a.k; ++j) {
+      a.p[j] = static_cast<uint8_t*>(c.fills[i + j].p); a.n[j] = c.fills[i + j].n; a.v[j] = c.fills[i + j].v;
+    }
+    k_fill<<<296, 256, 0, c.stream>>>(a);
+    c.launches += 1;
+  }
+  c.fills.clear();
+  return 0;
+}
+
 scan_status ms::sync_read(Ctx& c) {
+  flush_fills(c);
   CK(cudaMemcpyAsync(&c.hc, c.counters.p, sizeof(Counters), cudaMemcpyDeviceToHost, c.stream));
   CK(cudaStreamSynchronize(c.stream));
   CK(cudaGetLastError());
@@ -350,9 +384,9 @@ scan_status ms::prep_ws(Ctx& c, bool tiles) {
   z.bad_event = ~0ull;
   z.min_niter = ~0u;
   CK(cudaMemcpyAsync(c.counters.p, &z, sizeof(Counters), cudaMemcpyHostToDevice, c.stream));
-  CK(cudaMemsetAsync(c.ch_nmax.p, 0, ch_cap * 4, c.stream));
-  CK(cudaMemsetAsync(c.ch_nmin.p, 0xFF, ch_cap * 4, c.stream));
-  CK(cudaMemsetAsync(c.bitmap.p, 0, c.n_bm_words * 4, c.stream));
+  queue_fill(c, c.ch_nmax.p, ch_cap * 4, 0);
+  queue_fill(c, c.ch_nmin.p, ch_cap * 4, 0xFF);
+  queue_fill(c, c.bitmap.p, c.n_bm_words * 4, 0);
   return SCAN_OK;
 }
 
@@ -407,8 +441,10 @@ scan_status ms::alloc_match_buffers(Ctx& c, bool fused) {
   CK(c.inst_rec.ensure(c.n_inst * 16));
   const uint32_t NIT1 = c.NIT + 1;
   CK(c.citer.ensure(W * NIT1 * 4));
-  if (np_inst) CK(cudaMemsetAsync(c.p2p_warm.p, 0, np_inst, c.stream));
+  queue_fill(c, c.p2p_warm.p, np_inst, 0);
   const uint64_t n = W * NIT1;
+  if (fused) return SCAN_OK;  // citer (compute index of each iteration start) is read by the general path only
+  flush_fills(c);
   k_citer_fill<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(c.W, NIT1, c.r_ncomp.as<uint32_t>(), c.citer.as<uint32_t>());
   c.launches += 1;
   return SCAN_OK;
@@ -419,8 +455,8 @@ scan_status ms::alloc_detect(Ctx& c) {
   c.NW = d.window_iters ? std::max<uint32_t>(1, (c.n_iters + d.window_iters - 1) / d.window_iters) : 1;
   const uint64_t ncl = (uint64_t)c.TP * c.PP, items = (uint64_t)c.NW * c.W;
   CK(c.bits.ensure(std::max<uint64_t>(c.n_bits_words, 1) * 4));
-  CK(cudaMemsetAsync(c.bits.p, 0, std::max<uint64_t>(c.n_bits_words, 1) * 4, c.stream));
-  if (d.want_ref) { CK(c.cref.ensure(std::max<uint64_t>(c.n_comp, 1) * 4)); CK(cudaMemsetAsync(c.cref.p, 0xFF, c.n_comp * 4, c.stream)); }
+  queue_fill(c, c.bits.p, std::max<uint64_t>(c.n_bits_words, 1) * 4, 0);
+  if (d.want_ref) { CK(c.cref.ensure(std::max<uint64_t>(c.n_comp, 1) * 4)); queue_fill(c, c.cref.p, c.n_comp * 4, 0xFF); }
   CK(c.cl_J.ensure(ncl * 4)); CK(c.cl_max.ensure(ncl * 4)); CK(c.cl_min.ensure(ncl * 4));
   CK(c.wd_total.ensure(items * 4)); CK(c.wd_slow.ensure(items * 4)); CK(c.wd_cand.ensure(items)); CK(c.wd_frac.ensure(items * 8));
   return SCAN_OK;
@@ -438,13 +474,13 @@ scan_status ms::alloc_localize(Ctx& c) {
   CK(c.lb_label.ensure(items)); CK(c.lb_rkind.ensure(items)); CK(c.lb_rrank.ensure(items * 4));
   CK(c.lb_rsrc.ensure(items * 4)); CK(c.lb_depth.ensure(items * 4)); CK(c.lb_twait.ensure(items * 8));
   CK(c.scratch.ensure(std::max<size_t>(c.scratch.cap, (2 * items + c.NW + 2) * 4)));
-  CK(cudaMemsetAsync(c.wl_joined.p, 0, items * 4, c.stream));
-  CK(cudaMemsetAsync(c.wl_late.p, 0, items * 4, c.stream));
-  CK(cudaMemsetAsync(c.wl_link_slow.p, 0, items, c.stream));
-  CK(cudaMemsetAsync(c.ewc.p, 0, c.NW * nnz_tot * 8, c.stream));
-  CK(cudaMemsetAsync(c.rk_sum.p, 0, 3ull * c.W * 8, c.stream));
-  CK(cudaMemsetAsync(c.lk_slow.p, 0, nlk + 1, c.stream));
-  CK(cudaMemsetAsync(c.scratch.as<uint32_t>() + 2 * items, 0, (c.NW + 2) * 4, c.stream));
+  queue_fill(c, c.wl_joined.p, items * 4, 0);
+  queue_fill(c, c.wl_late.p, items * 4, 0);
+  queue_fill(c, c.wl_link_slow.p, items, 0);
+  queue_fill(c, c.ewc.p, c.NW * nnz_tot * 8, 0);
+  queue_fill(c, c.rk_sum.p, 3ull * c.W * 8, 0);
+  queue_fill(c, c.lk_slow.p, nlk + 1, 0);
+  queue_fill(c, c.scratch.as<uint32_t>() + 2 * items, (c.NW + 2) * 4, 0);
   return SCAN_OK;
 }
 
@@ -561,7 +597,7 @@ scan_status fused_all(Ctx& c) {
   if ((st = channels_and_buffers(c, true))) return st;
   if ((st = alloc_detect(c)) || (st = alloc_localize(c))) return st;
   CK(c.dlate.ensure((uint64_t)c.n_ftiles * ((c.FR + 31) / 32) * 4 + 4));
-  CK(cudaMemsetAsync(c.dlate.p, 0, (uint64_t)c.n_ftiles * ((c.FR + 31) / 32) * 4 + 4, c.stream));
+  queue_fill(c, c.dlate.p, (uint64_t)c.n_ftiles * ((c.FR + 31) / 32) * 4 + 4, 0);
   CK(c.dinfo.ensure((uint64_t)c.n_ftiles * 16 + 16));
   Counters z = c.hc;
   z.n_compared = z.n_slow = z.n_candidates = z.n_class_mismatch = 0;
@@ -570,8 +606,8 @@ scan_status fused_all(Ctx& c) {
   CK(cudaMemcpyAsync(c.counters.p, &z, sizeof(Counters), cudaMemcpyHostToDevice, c.stream));
   {
     const uint64_t items = (uint64_t)c.NW * c.W;
-    CK(cudaMemsetAsync(c.wd_total.p, 0, items * 4, c.stream));
-    CK(cudaMemsetAsync(c.wd_slow.p, 0, items * 4, c.stream));
+    queue_fill(c, c.wd_total.p, items * 4, 0);
+    queue_fill(c, c.wd_slow.p, items * 4, 0);
   }
   c.launches += timed(c, "k_class_counts", [&] { return launch_class_counts(c); });
   c.launches += timed(c, "k_fused", [&] { return launch_fused(c); });
@@ -891,6 +927,7 @@ scan_status scan_export(scan_ctx* ctx, scan_output which, void* dst, uint64_t ds
   if (!c.matched) { c.err = "nothing to export before scan_match_collectives"; return SCAN_E_ORDER; }
   CK(cudaSetDevice(c.device));
   const cudaMemcpyKind kind = dst_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  flush_fills(c);
   if (which >= SCAN_OUT_AL_START && which <= SCAN_OUT_AL_RESIDUAL && !c.aligned) { c.err = "scan_align not run"; return SCAN_E_ORDER; }
   if ((which == SCAN_OUT_COMM_WAIT || which == SCAN_OUT_EV_WAIT) && c.xwait_pending && c.localized) {
     launch_xwait_scatter(c);  // comm-order view of the cross-stage waits (once per analysis)
@@ -938,6 +975,7 @@ const void* scan_output_device_ptr(scan_ctx* ctx, scan_output which) {
   OutDesc d;
   if (which != SCAN_OUT_COMM_INST && which != SCAN_OUT_COMM_WAIT && which != SCAN_OUT_SLOW_BITS) return nullptr;
   if (!direct(c, which, d) || stage_of(c) < d.stage) return nullptr;
+  flush_fills(c);
   if (which == SCAN_OUT_COMM_WAIT && c.xwait_pending) {
     launch_xwait_scatter(c);
     if (cudaStreamSynchronize(c.stream) != cudaSuccess) return nullptr;

@@ -169,6 +169,9 @@ struct Ctx {
   void* h_pin = nullptr;                 // pinned host scratch (exchange read-backs, table staging)
   size_t h_pin_cap = 0;
   cudaEvent_t ev_x1 = nullptr, ev_x2 = nullptr;
+  // queued zero / byte fills, flushed as one k_fill launch before the next kernel (flush_fills)
+  struct Fill { void* p; uint64_t n; uint32_t v; };
+  std::vector<Fill> fills;
   // optional per-kernel timing
   bool timing = false;
   struct Pending { int k; cudaEvent_t a, b; };
@@ -181,9 +184,15 @@ struct Ctx {
   bool fail(scan_status, const std::string& m) { err = m; return false; }
 };
 
+// queued buffer fills (instead of one cudaMemsetAsync API call each): every queued fill runs, in
+// queue order, before the next kernel launched through timed() or after an explicit flush_fills()
+inline void queue_fill(Ctx& c, void* p, uint64_t bytes, uint8_t v) { if (p && bytes) c.fills.push_back({p, bytes, v}); }
+int flush_fills(Ctx& c);
+
 // Launch wrapper: records an event pair around a launcher when timing is on.
 template <class F>
 int timed(Ctx& c, const char* name, F&& f) {
+  flush_fills(c);
   if (!c.timing) return f();
   int k = -1;
   for (size_t i = 0; i < c.knames.size(); ++i) if (c.knames[i] == name) k = (int)i;

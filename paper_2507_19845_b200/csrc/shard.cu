@@ -360,6 +360,7 @@ scan_status sharded_all(Ctx& c) {
   uint8_t* pin = static_cast<uint8_t*>(c.h_pin);
   // ---- X1 (device-packed) and, right behind it, the device-side P2P channel set and X2: no host
   // round trip between the two all-gathers
+  flush_fills(c);  // prep_ws fills (channel count extremes, bitmap) precede the census
   k_x1_pack<<<(unsigned)std::min<uint64_t>((LA + 255) / 256, 1024), 256, 0, c.stream>>>(
       c.counters.as<Counters>(), c.spmd ? 0u : 1u, (unsigned long long)c.N, c.ch_nmin.as<uint32_t>(), c.ch_nmax.as<uint32_t>(),
       c.bitmap.as<uint32_t>(), nc, nbm, c.x_send.as<uint32_t>());
@@ -531,11 +532,11 @@ scan_status sharded_all(Ctx& c) {
   // ---- local fused pass (K9 + cross-stage reduce + deferred stage 2), job-wide ids / windows
   if ((st = alloc_detect(c)) || (st = alloc_localize(c))) return st;
   CK(c.dlate.ensure((uint64_t)c.n_ftiles * ((c.FR + 31) / 32) * 4 + 4));
-  CK(cudaMemsetAsync(c.dlate.p, 0, (uint64_t)c.n_ftiles * ((c.FR + 31) / 32) * 4 + 4, c.stream));
+  queue_fill(c, c.dlate.p, (uint64_t)c.n_ftiles * ((c.FR + 31) / 32) * 4 + 4, 0);
   CK(c.dinfo.ensure((uint64_t)c.n_ftiles * 16 + 16));
   const uint64_t items = (uint64_t)c.NW * W, nlk = (uint64_t)c.NW * np, ncl = (uint64_t)c.TP * c.PP;
-  CK(cudaMemsetAsync(c.wd_total.p, 0, items * 4, c.stream));
-  CK(cudaMemsetAsync(c.wd_slow.p, 0, items * 4, c.stream));
+  queue_fill(c, c.wd_total.p, items * 4, 0);
+  queue_fill(c, c.wd_slow.p, items * 4, 0);
   mark("tables");
   c.launches += timed(c, "k_class_counts", [&] { return launch_class_counts(c); });
   c.launches += timed(c, "k_fused", [&] { return launch_fused(c); });
@@ -576,6 +577,7 @@ scan_status sharded_all(Ctx& c) {
     if ((st = upload(c, c.lk_sendmap, smap)) || (st = upload(c, c.lk_recvmap, rmap))) return st;
     CK(c.x_send.ensure(std::max<size_t>(soff[G], 1) * LREC * 4));
     CK(c.x_recv.ensure(std::max<size_t>(roff[G], 1) * LREC * 4));
+    flush_fills(c);
     if (!smap.empty()) {
       k_link_pack<<<(unsigned)smap.size(), 256, 0, c.stream>>>(c.lk_sendmap.as<LinkMap>(), c.inst_rec.as<uint4>(),
                                                               c.p2p_iter.as<uint32_t>(), c.p2p_pay.as<uint32_t>(),
