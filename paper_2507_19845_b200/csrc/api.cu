@@ -104,7 +104,7 @@ static void release_all(Ctx& c) {
                     &c.st_tile0, &c.st_npos, &c.role_comm, &c.role_slot, &c.role_type, &c.ncroles, &c.ft_cols,
                     &c.ft_base, &c.ft_last, &c.st_tot, &c.sci, &c.sit, &c.dlate, &c.dinfo, &c.ft_posA, &c.ft_posB,
                     &c.ft_posK, &c.eidx, &c.tile_stage, &c.xbase, &c.lk_scratch, &c.g_base, &c.g_slot,
-                    &c.g_nmax, &c.g_nmin, &c.g_k0, &c.p2p_eslot, &c.own_start, &c.al_tend, &c.al_aend, &c.al_anct,
+                    &c.g_nmax, &c.g_nmin, &c.g_k0, &c.p2p_eslot, &c.xe_off, &c.xe_col, &c.xbig, &c.own_start, &c.al_tend, &c.al_aend, &c.al_anct,
                     &c.al_anco, &c.al_slotci, &c.al_level, &c.al_nanc, &c.al_resid, &c.al_flag, &c.al_start, &c.al_ranks, &c.al_cch, &c.al_tgt, &c.x_send, &c.x_recv, &c.x_recv2, &c.x_ep, &c.x_stage, &c.headtail, &c.lk_sendmap, &c.lk_recvmap};
   for (DevBuf* b : bufs) b->release();
 }
@@ -239,6 +239,33 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
   rt0[W] = (uint32_t)trank.size();
   c.TP = topo->tp; c.PP = topo->pp; c.DP = topo->dp; c.W = W; c.n_comms = nc; c.N = N; c.flags = flags;
   c.h_ccls = ccls; c.h_coff = coff; c.h_cmem = cmem; c.h_rcomm = rcm; c.h_rcomm_off = rco;
+  {  // cross collectives (not TP/DP class) with <= 128 members: edge column of member q waiting on
+     // member t (the search k_cross_reduce would do per wait-for edge; all co-members are neighbours)
+    std::vector<uint64_t> xoff(std::max<uint32_t>(nc, 1), ~0ull);
+    std::vector<uint32_t> xcol;
+    for (uint32_t k = 0; k < nc; ++k) {
+      const uint64_t b = coff[k], n = coff[k + 1] - b;
+      if (ccls[k] == 1 || ccls[k] == 2 || n < 2 || n > 128) continue;
+      xoff[k] = xcol.size();
+      for (uint64_t q = 0; q < n; ++q) {
+        const uint32_t r = cmem[b + q];
+        for (uint64_t t = 0; t < n; ++t) {
+          const uint32_t L = cmem[b + t];
+          auto b0 = nb.begin() + nbo[r], b1 = nb.begin() + nbo[r + 1];
+          auto it = std::lower_bound(b0, b1, L);
+          xcol.push_back(q == t || it == b1 || *it != L ? 0u : (uint32_t)(it - nb.begin()));
+        }
+      }
+    }
+    if (xcol.empty()) xcol.push_back(0);
+    std::vector<uint32_t> big;
+    for (uint32_t k = 0; k < nc; ++k)
+      if (ccls[k] != 1 && ccls[k] != 2 && coff[k + 1] - coff[k] > 32) big.push_back(k);
+    c.n_big = (uint32_t)big.size();
+    if (big.empty()) big.push_back(0);
+    scan_status st0;
+    if ((st0 = upload(c, c.xe_off, xoff)) || (st0 = upload(c, c.xe_col, xcol)) || (st0 = upload(c, c.xbig, big))) return st0;
+  }
   c.h_rank_off = ro; c.h_rank_tile0 = rt0; c.n_tiles = trank.size(); c.nnz_c = nb.size();
   scan_status st;
   if ((st = upload(c, c.rank_off, ro)) || (st = upload(c, c.coff, coff)) || (st = upload(c, c.cmem, cmem)) ||

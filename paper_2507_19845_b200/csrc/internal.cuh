@@ -150,6 +150,8 @@ struct Ctx {
   DevBuf xbase;                          // [NCH+1] cross-stage instance index
   DevBuf lk_scratch;                     // link-median scratch for links above the shared-memory capacity
   DevBuf p2p_eslot;                      // [n_p2p][2] wait-for edge column per P2P link direction
+  DevBuf xe_off, xe_col;                 // cross collectives: member x member edge-column tables (built at load)
+  DevBuf xbig; uint32_t n_big = 0;       // cross collectives with more than 32 members (k_cross_big)
   uint64_t n_xinst = 0;
   // multi-GPU iteration-window shards (row A9, shard.cu); n_shards == 1: unsharded
   int n_shards = 1, shard = 0;

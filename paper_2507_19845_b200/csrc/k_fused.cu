@@ -1417,7 +1417,11 @@ struct XArgs {
   Counters* cnt;
   const uint32_t* p2p_eslot;  // [n_p2p][2] edge column of src -> dst and dst -> src
   int xb_smem;                // xbase staged in shared memory (NCH + 1 entries)
+  const uint64_t* xe_off;     // [n_comms] offset of a cross collective's member x member edge-column table, ~0 = none
+  const uint32_t* xe_col;     // table[q * nm + t]: edge column of member q waiting on member t
 };
+
+constexpr uint32_t XBIG = 32;  // cross collectives with more members go to k_cross_big
 
 // edge column of every P2P link direction (the search x_edge would do), once per analysis
 __global__ void k_p2p_eslot(uint32_t n_p2p, const uint32_t* psrc, const uint32_t* pdst, const uint64_t* nbc_off,
@@ -1456,7 +1460,7 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
   const uint64_t wstride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t wbase = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wbase < a.n_xinst; wbase += wstride) {
     const uint64_t xi = wbase + lane;
-    const bool act = xi < a.n_xinst;
+    bool act = xi < a.n_xinst;
     // channel of the warp's first instance (one search per warp); lanes past its end search alone
     uint64_t ch0 = 0, end0 = 0;
     if (lane == 0) { ch0 = upper_bound_u64(XB, a.NCH + 1, wbase) - 1; end0 = XB[ch0 + 1]; }
@@ -1467,6 +1471,7 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
       ch = xi < end0 ? ch0 : upper_bound_u64(XB, a.NCH + 1, xi) - 1;
       k = xi - XB[ch];
       i = a.ch_base[ch] + k;
+      if (ch < a.n_comms && a.coff[ch + 1] - a.coff[ch] > XBIG) act = false;  // k_cross_big (lanes over members)
     }
     // one channel across the whole warp (the common case): its members are the same for every lane
     const bool uni = __all_sync(0xFFFFFFFFu, act && ch == ch0);
@@ -1483,7 +1488,7 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
       const uint32_t p = lower_bound_u32(a.r_keys + (uint64_t)m * RCAP, C, (uint32_t)ch);
       return p < C && a.r_keys[(uint64_t)m * RCAP + p] == (uint32_t)ch && a.r_cnt[(uint64_t)m * RCAP + p] > k;
     };
-    uint32_t flags = 0, dmin = 0, dmax = 0, last = NONE32;
+    uint32_t flags = 0, dmin = 0, dmax = 0, last = NONE32, lsi = 0;
     bool valid = false;
     if (act) {
       if (isp && a.p2p_warm[i - a.p2p_inst0]) flags |= SCAN_F_WARMUP;
@@ -1510,6 +1515,7 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
           }
           if (nat == 1) flags |= SCAN_F_UNIQUE_LAST;
           last = member(ls);
+          lsi = ls;
         }
       } else {
         ++inc;
@@ -1540,10 +1546,12 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
         if (em) {
           const int L0 = __ffs(em) - 1;
           const uint32_t tl = __shfl_sync(0xFFFFFFFFu, last, L0), tw = __shfl_sync(0xFFFFFFFFu, ewin, L0);
+          const uint32_t tli = __shfl_sync(0xFFFFFFFFu, lsi, L0);
           if (__all_sync(0xFFFFFFFFu, !eg || (last == tl && ewin == tw))) {
             const unsigned long long ws = warp_sum_u64(eg ? (unsigned long long)ewait : 0ull);
             if (lane == (uint32_t)L0) {
               if (isp) atomicAdd(&a.ew[(uint64_t)tw * a.nnz_tot + a.p2p_eslot[2 * (ch - a.n_comms) + q]], ws);
+              else if (a.xe_off[ch] != ~0ull) atomicAdd(&a.ew[(uint64_t)tw * a.nnz_tot + a.xe_col[a.xe_off[ch] + (uint64_t)q * nm + tli]], ws);
               else x_edge(a, member(q), tl, tw, ws);
             }
           } else if (eg) {
@@ -1578,6 +1586,8 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
   }
 }
 
+__global__ void k_cross_big(XArgs a, const uint32_t* big, uint32_t n_big);
+
 int launch_cross_reduce(Ctx& c) {
   XArgs a{c.n_xinst, c.NCH, c.n_comms, c.W, c.xbase.as<uint64_t>(), c.ch_base.as<uint64_t>(), c.ch_slot.as<uint64_t>(), c.ch_nmin.as<uint32_t>(),
           c.coff.as<uint64_t>(), c.cmem.as<uint32_t>(), c.ccls.as<uint8_t>(), c.ch_nsend.as<uint32_t>(),
@@ -1588,7 +1598,7 @@ int launch_cross_reduce(Ctx& c) {
           c.sdur.as<uint32_t>(), c.nbc_off.as<uint64_t>(), c.nbc.as<uint32_t>(), c.nbp.as<uint32_t>(), c.nbp_n.as<uint32_t>(),
           c.nnz_c + (uint64_t)c.W * PCAP, c.nnz_c, c.ewc.as<unsigned long long>(), c.rk_sum.as<unsigned long long>(),
           c.dcfg.window_iters, (unsigned long long)c.lcfg.wait_margin_ns, c.counters.as<Counters>(),
-          c.p2p_eslot.as<uint32_t>(), 0};
+          c.p2p_eslot.as<uint32_t>(), 0, c.xe_off.as<uint64_t>(), c.xe_col.as<uint32_t>()};
   if (c.n_xinst == 0) return 0;
   int n = 0;
   if (c.n_p2p) {
@@ -1603,7 +1613,88 @@ int launch_cross_reduce(Ctx& c) {
   a.xb_smem = xsm <= 48 * 1024 ? 1 : 0;
   unsigned blocks = (unsigned)std::min<uint64_t>((c.n_xinst + 255) / 256, 148ull * 8);
   k_cross_reduce<<<blocks, 256, a.xb_smem ? xsm : 0, c.stream>>>(a);
+  if (c.n_big) {
+    k_cross_big<<<dim3(c.n_big, 32), 256, 0, c.stream>>>(a, c.xbig.as<uint32_t>(), c.n_big);
+    ++n;
+  }
   return n + 1;
+}
+
+// Cross collectives with more than XBIG members (e.g. a model-parallel group of TP*PP ranks): one
+// CTA per such communicator, one warp per instance, lanes over the members -- the same decisions
+// as k_cross_reduce, whose member loop would otherwise run serially in a single warp per instance.
+__global__ void __launch_bounds__(256) k_cross_big(XArgs a, const uint32_t* big, uint32_t n_big) {
+  if (*((volatile unsigned*)&a.cnt->overflow) & NOT_SPMD) return;
+  const uint32_t ch = big[blockIdx.x];
+  const uint32_t lane = lane_id(), nw = (blockDim.x >> 5) * gridDim.y;
+  const uint32_t wid = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);  // gridDim.y CTAs share a communicator
+  const uint32_t nm = (uint32_t)(a.coff[ch + 1] - a.coff[ch]);
+  const uint32_t* mem = a.cmem + a.coff[ch];
+  const uint32_t nk = (uint32_t)(a.xbase[ch + 1] - a.xbase[ch]), nmin = a.ch_nmin[ch];
+  uint32_t inc = 0, kmis = 0;
+  for (uint32_t k = wid; k < nk; k += nw) {
+    const uint64_t i = a.ch_base[ch] + k, sb = a.ch_slot[ch] + (uint64_t)k * nm;
+    const bool complete = k < nmin;
+    uint32_t flags = 0, dmin = 0, dmax = 0, last = NONE32;
+    bool valid = false;
+    if (complete) {
+      flags |= SCAN_F_COMPLETE;
+      const uint8_t k0 = a.skind[sb];
+      bool kok = true;
+      for (uint32_t q = lane; q < nm; q += 32) kok &= a.skind[sb + q] == k0;
+      kok = __all_sync(0xFFFFFFFFu, kok);
+      if (kok) flags |= SCAN_F_KIND_OK; else ++kmis;
+      flags |= SCAN_F_PAYLOAD_OK;  // collectives carry no payload check
+      if (!kok)
+        for (uint32_t q = lane; q < nm; q += 32) a.swait[sb + q] = 0;  // invalid instance: members wait 0
+      if (kok) {
+        valid = true;
+        flags |= SCAN_F_VALID;
+        uint32_t mn = NONE32, mx = 0;
+        for (uint32_t q = lane; q < nm; q += 32) { const uint32_t d = a.sdur[sb + q]; mn = min(mn, d); mx = max(mx, d); }
+        for (int o = 16; o > 0; o >>= 1) {
+          mn = min(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, o));
+          mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+        }
+        uint32_t ls = NONE32, nat = 0;  // lowest member with the minimum, tie count
+        for (uint32_t q = lane; q < nm; q += 32)
+          if (a.sdur[sb + q] == mn) { ls = min(ls, q); ++nat; }
+        for (int o = 16; o > 0; o >>= 1) {
+          ls = min(ls, __shfl_xor_sync(0xFFFFFFFFu, ls, o));
+          nat += __shfl_xor_sync(0xFFFFFFFFu, nat, o);
+        }
+        dmin = mn; dmax = mx; last = mem[ls];
+        if (nat == 1) flags |= SCAN_F_UNIQUE_LAST;
+        const uint64_t xo = a.xe_off[ch];
+        for (uint32_t q = lane; q < nm; q += 32) {
+          const uint32_t m = mem[q];
+          const uint32_t wait = a.sdur[sb + q] - dmin;
+          a.swait[sb + q] = wait;
+          if (wait) atomicAdd(&a.rk_sum[a.W + m], (unsigned long long)wait);
+          if (dmin) atomicAdd(&a.rk_sum[2 * a.W + m], (unsigned long long)dmin);
+          if (m != last && (unsigned long long)wait > a.wait_margin) {
+            const uint32_t win = a.wi ? a.sit[sb + q] / a.wi : 0;
+            if (xo != ~0ull) atomicAdd(&a.ew[(uint64_t)win * a.nnz_tot + a.xe_col[xo + (uint64_t)q * nm + ls]], (unsigned long long)wait);
+            else x_edge(a, m, last, win, wait);
+          }
+        }
+      }
+    } else {
+      ++inc;
+      for (uint32_t q = lane; q < nm; q += 32) {  // present members of an incomplete instance: wait 0
+        const uint32_t m = mem[q];
+        const uint32_t C = a.r_nkeys[m];
+        const uint32_t p = lower_bound_u32(a.r_keys + (uint64_t)m * RCAP, C, ch);
+        if (p < C && a.r_keys[(uint64_t)m * RCAP + p] == ch && a.r_cnt[(uint64_t)m * RCAP + p] > k) a.swait[sb + q] = 0;
+      }
+    }
+    if (lane == 0) a.rec[i] = make_uint4(dmin, dmax, last, flags | ((uint32_t)a.ccls[ch] << 8));
+    (void)valid;
+  }
+  if (lane == 0) {
+    if (inc) atomicAdd(&a.cnt->n_incomplete, (unsigned long long)inc);
+    if (kmis) atomicAdd(&a.cnt->n_kind_mismatch, (unsigned long long)kmis);
+  }
 }
 
 // Comm-order view of the cross-stage members' waits (COMM_WAIT / EV_WAIT exports): k_cross_reduce
