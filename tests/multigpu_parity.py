@@ -55,6 +55,24 @@ CASES = [
 ]
 
 
+def _random_cfg(seed):
+    rng = np.random.default_rng(seed)
+    tp, pp, dp = (int(x) for x in rng.integers(1, 5, 3))
+    if tp * pp * dp == 1:
+        dp = 2
+    W = tp * pp * dp
+    faults = [tg.Fault(tg.THROTTLE, int(rng.integers(0, W)), it0=int(rng.integers(0, 6)), factor=2.0)]
+    if pp > 1:
+        faults.append(tg.Fault(tg.LINK_DEGRADE, 0, tp * dp, factor=0.3))
+    return tg.GenConfig(tp, pp, dp, int(rng.integers(1, 4)), int(rng.integers(pp, pp + 4)), int(rng.integers(8, 13)),
+                        seed=seed, faults=faults)
+
+
+# random SPMD jobs (TP, PP, DP in 1..4), random windows / stage-2 mode / min samples
+CASES += [(f"random_{sd}", (lambda sd=sd: _random_cfg(sd)), int([0, 2, 3, 5][sd % 4]), sd % 2, [3, 10][sd % 2], None, None)
+          for sd in range(301, 311)]
+
+
 def main() -> int:
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))

@@ -88,3 +88,15 @@ def test_align_requires_start_and_analysis():
     s.analyze()
     with pytest.raises(ms.ScanError):
         s.align(0)  # start_ns not loaded
+
+
+@pytest.mark.parametrize("seed", range(201, 221))
+def test_fuzz_alignment(seed):
+    """Random small jobs (TP, PP, DP in 1..4) with clock skew + drift, random reference rank."""
+    rng = np.random.default_rng(seed)
+    tp, pp, dp = (int(x) for x in rng.integers(1, 5, 3))
+    if tp * pp * dp == 1:
+        dp = 2
+    cfg = tg.GenConfig(tp, pp, dp, int(rng.integers(1, 4)), int(rng.integers(pp, pp + 4)), int(rng.integers(2, 6)), seed=seed,
+                       faults=[tg.Fault(tg.THROTTLE, int(rng.integers(0, tp * pp * dp)), factor=2.0)])
+    _check(tg.generate(cfg), int(rng.integers(0, tp * pp * dp)), "fused" if seed % 2 else "general")
