@@ -207,6 +207,26 @@ typedef struct scan_align_result {
     uint64_t max_residual_ns;
 } scan_align_result;
 scan_status scan_align(scan_ctx* ctx, const scan_align_config* cfg, scan_align_result* out);
+
+/* ---- NEXT-3: sliding-window streaming ("on-line") -------------
+   The context keeps the last `window_iters` pushed iterations. After every scan_stream_push the
+   window-level outputs (RK_SUM_*, WD_*, WL_*, LK_*, LB_*, EG_*) equal scan_analyze on the
+   window's events as one analysis window (the dcfg window_iters is ignored), but each push
+   analyses only the new iteration: per-iteration partials are kept in a ring and recombined on
+   the device (instances never straddle an iteration, reading R30; stage-2 segments crossing an
+   iteration boundary are fixed up as between shards; link medians over the window's samples).
+   scan_stream_open: topology + comm table of the job (copied), window length (1..4096), configs.
+   scan_stream_push: `iteration` = the events of ONE whole iteration of every rank, the columns
+   as for scan_load_events (HOST or DEVICE pointers, borrowed only for the call). Returns SCAN_OK
+   or SCAN_PARTIAL (integrity reports in the window); out (optional) receives the window's
+   verdict / walk counts. Errors: SCAN_E_ORDER (push before open), SCAN_E_UNSUPPORTED (an
+   iteration is not SPMD, or its channel structure differs from the first one; sharded context),
+   load errors of scan_load_events. Other outputs are unavailable on a stream context
+   (SCAN_E_UNSUPPORTED). scan_stream_window: iterations currently in the window.               */
+scan_status scan_stream_open(scan_ctx* ctx, const scan_topology* topo, const scan_comm_table* comms, uint32_t window_iters,
+                             const scan_detect_config* dcfg, const scan_localize_config* lcfg);
+scan_status scan_stream_push(scan_ctx* ctx, const scan_event_columns* iteration, uint32_t flags, scan_localize_result* out);
+uint64_t    scan_stream_window(const scan_ctx* ctx);
 scan_status scan_create_sharded(scan_ctx** out, int cuda_device, void* cuda_stream, int n_shards, int shard,
                                 const uint8_t nccl_unique_id[128]);
 

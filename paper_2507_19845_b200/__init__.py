@@ -155,10 +155,15 @@ def _load_lib():
     lib.scan_fused_variant.argtypes = [P, ctypes.c_int]
     lib.scan_nccl_unique_id.argtypes = [P]
     lib.scan_align.argtypes = [P, ctypes.POINTER(_AlignCfg), ctypes.POINTER(_AlignRes)]
+    lib.scan_stream_open.argtypes = [P, ctypes.POINTER(_Topo), ctypes.POINTER(_Comms), ctypes.c_uint32,
+                                     ctypes.POINTER(_DetectCfg), ctypes.POINTER(_LocCfg)]
+    lib.scan_stream_push.argtypes = [P, ctypes.POINTER(_Cols), ctypes.c_uint32, ctypes.POINTER(_LocRes)]
+    lib.scan_stream_window.argtypes = [P]
+    lib.scan_stream_window.restype = ctypes.c_uint64
     lib.scan_create_sharded.argtypes = [ctypes.POINTER(P), ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P]
     for f in ("scan_create", "scan_load_events", "scan_match_collectives", "scan_detect", "scan_localize",
               "scan_output_size", "scan_export", "scan_analyze", "scan_force_general", "scan_fused_variant",
-              "scan_nccl_unique_id", "scan_create_sharded", "scan_align"):
+              "scan_nccl_unique_id", "scan_create_sharded", "scan_align", "scan_stream_open", "scan_stream_push"):
         getattr(lib, f).restype = ctypes.c_int32
     _lib = lib
     return lib
@@ -168,7 +173,8 @@ EXPORTED_SYMBOLS = ["scan_create", "scan_destroy", "scan_last_error", "scan_load
                     "scan_detect", "scan_localize", "scan_output_size", "scan_export", "scan_output_device_ptr",
                     "scan_kernel_launches", "scan_set_timing", "scan_timing_reset", "scan_kernel_timing",
                     "scan_analyze", "scan_used_fused", "scan_force_general", "scan_fused_variant",
-                    "scan_nccl_unique_id", "scan_create_sharded", "scan_align"]
+                    "scan_nccl_unique_id", "scan_create_sharded", "scan_align", "scan_stream_open", "scan_stream_push",
+                    "scan_stream_window"]
 
 
 @dataclass
@@ -397,6 +403,39 @@ class Scan:
     def align(self, reference: int = 0) -> dict:
         """Timeline alignment onto ``reference``'s clock (load with ``start=True`` first)."""
         return scan_align(self.ctx, reference)
+
+    # ---- NEXT-3 sliding-window streaming (scan.h)
+    STREAM_OUTPUTS = tuple(n for n, _ in OUTPUTS if n.startswith(("rk_sum", "wd_", "wl_", "lk_", "lb_", "eg_")))
+
+    def stream_open(self, trace, window_iters: int, dcfg: DetectConfig | None = None, lcfg: LocalizeConfig | None = None):
+        """Open a sliding window of ``window_iters`` iterations on ``trace``'s topology / comm table."""
+        lib = _load_lib()
+        co = np.ascontiguousarray(trace.comm_offsets, dtype=np.uint64)
+        cm = np.ascontiguousarray(trace.comm_members, dtype=np.uint32)
+        self._stream_keep = [co, cm]
+        dcfg, lcfg = dcfg or DetectConfig(), lcfg or LocalizeConfig()
+        d = _DetectCfg(dcfg.slow_num, dcfg.slow_den, dcfg.slow_margin_ns, dcfg.cand_num, dcfg.cand_den, dcfg.min_samples,
+                       0, 1 if dcfg.want_ref else 0, 0)
+        l_ = _LocCfg(lcfg.late_margin_ns, lcfg.late_num, lcfg.late_den, lcfg.bw_num, lcfg.bw_den, lcfg.min_samples,
+                     lcfg.stage2_classes, lcfg.stage2_mode, 0, lcfg.wait_margin_ns)
+        _check(self.ctx, lib.scan_stream_open(self.ctx, ctypes.byref(_Topo(trace.tp, trace.pp, trace.dp, 0)),
+                                              ctypes.byref(_Comms(len(co) - 1, co.ctypes.data, cm.ctypes.data if len(cm) else None)),
+                                              int(window_iters), ctypes.byref(d), ctypes.byref(l_)))
+
+    def stream_push(self, iteration, device_ptrs: bool = False, cols: dict | None = None) -> dict:
+        """Push one whole iteration (a trace holding exactly one iteration of every rank)."""
+        lib = _load_lib()
+        c = cols or {k: np.ascontiguousarray(getattr(iteration, k)) for k in ("dur_ns", "kind_op", "meta", "comm", "payload")}
+        ro = np.ascontiguousarray(iteration.rank_offsets, dtype=np.uint64)
+        cs = _Cols(int(ro[-1]), ro.ctypes.data, None, _ptr(c["dur_ns"]), _ptr(c["kind_op"]), _ptr(c["meta"]), _ptr(c["comm"]),
+                   _ptr(c["payload"]))
+        r = _LocRes()
+        st = _check(self.ctx, lib.scan_stream_push(self.ctx, ctypes.byref(cs), SCAN_DEVICE_PTRS if device_ptrs else SCAN_HOST_PTRS,
+                                                   ctypes.byref(r)))
+        out = {n: getattr(r, n) for n, _ in r._fields_}
+        out["status"] = st
+        out["window"] = int(lib.scan_stream_window(self.ctx))
+        return out
 
     def fused_variant(self, variant: int):
         """-1 automatic, 0 generic tile kernel, 1 transposed warp-per-position kernel (next load)."""

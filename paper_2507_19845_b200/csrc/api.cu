@@ -116,6 +116,7 @@ void scan_destroy(scan_ctx* ctx) {
   for (auto& p : ctx->c.pend) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   for (auto e : ctx->c.evpool) cudaEventDestroy(e);
   shard_release(ctx->c);
+  stream_release(ctx->c);
   release_all(ctx->c);
   delete ctx;
 }
@@ -159,6 +160,7 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
   CK(cudaSetDevice(c.device));
   c.loaded = c.matched = c.detected = c.localized = false;
   c.fused_used = false; c.tiles_ready = false; c.xwait_pending = false; c.aligned = false;
+  if (c.stream_mode) { stream_release(c); c.stream_mode = false; }
   c.d_start = nullptr;
   c.err.clear();
   if (topo->tp < 1 || topo->pp < 1 || topo->dp < 1 || topo->rank_order != 0) {
@@ -607,8 +609,10 @@ scan_status general_localize(Ctx& c) {
   return SCAN_OK;
 }
 
+}  // namespace
+
 // ---- the fused SPMD path (K9); returns 2 when the trace is not SPMD (caller falls back)
-scan_status fused_all(Ctx& c) {
+scan_status ms::fused_all(Ctx& c) {
   c.matched = c.detected = c.localized = false;
   c.xwait_pending = false;
   scan_status st = prep_ws(c, false);
@@ -640,6 +644,13 @@ scan_status fused_all(Ctx& c) {
   c.launches += timed(c, "k_fused", [&] { return launch_fused(c); });
   c.launches += timed(c, "k_cross_reduce", [&] { return launch_cross_reduce(c); });
   c.launches += timed(c, "k_deferred", [&] { return launch_deferred(c); });
+  if (c.partial_tail) {  // streaming: per-iteration partials only (stream.cu combines the window)
+    if ((st = sync_read(c))) return st;
+    if (c.hc.overflow & 32u) { c.err = "streaming needs an SPMD iteration (fused-pass verification failed)"; return SCAN_E_UNSUPPORTED; }
+    c.matched = c.detected = c.localized = true;
+    c.fused_used = true;
+    return SCAN_OK;
+  }
   c.launches += timed(c, "k_wd_finish", [&] { return launch_wd_finish(c); });
   // links and walk run before the SPMD verification result is read (one host sync less): on a
   // failed verification their inputs are garbage but in bounds, and the call reruns the general path
@@ -657,8 +668,6 @@ scan_status fused_all(Ctx& c) {
   c.xwait_pending = true;
   return SCAN_OK;
 }
-
-}  // namespace
 
 extern "C" {
 
@@ -932,10 +941,19 @@ uint64_t in_bytes(Ctx& c, scan_output w) { return w == SCAN_OUT_IN_FLAGS ? c.n_i
 
 extern "C" {
 
+static bool stream_output(scan_output which) {  // window-level outputs of a stream context
+  return (which >= SCAN_OUT_RK_SUM_COMPUTE && which <= SCAN_OUT_RK_SUM_TRANSFER) ||
+         (which >= SCAN_OUT_WD_TOTAL && which <= SCAN_OUT_EG_WEIGHT);
+}
+
 scan_status scan_output_size(scan_ctx* ctx, scan_output which, uint64_t* bytes) {
   if (!ctx || !bytes) return SCAN_E_INVALID_ARG;
   Ctx& c = ctx->c;
   *bytes = 0;
+  if (c.stream_mode && !stream_output(which)) {
+    c.err = "a stream context exports the window-level outputs only (RK_SUM_*, WD_*, WL_*, LK_*, LB_*, EG_*)";
+    return SCAN_E_UNSUPPORTED;
+  }
   if (!c.matched) return SCAN_OK;
   OutDesc d;
   if (direct(c, which, d)) { if (stage_of(c) >= d.stage) *bytes = d.bytes; return SCAN_OK; }
@@ -955,6 +973,10 @@ scan_status scan_export(scan_ctx* ctx, scan_output which, void* dst, uint64_t ds
   CK(cudaSetDevice(c.device));
   const cudaMemcpyKind kind = dst_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   flush_fills(c);
+  if (c.stream_mode && !stream_output(which)) {
+    c.err = "a stream context exports the window-level outputs only (RK_SUM_*, WD_*, WL_*, LK_*, LB_*, EG_*)";
+    return SCAN_E_UNSUPPORTED;
+  }
   if (which >= SCAN_OUT_AL_START && which <= SCAN_OUT_AL_RESIDUAL && !c.aligned) { c.err = "scan_align not run"; return SCAN_E_ORDER; }
   if ((which == SCAN_OUT_COMM_WAIT || which == SCAN_OUT_EV_WAIT) && c.xwait_pending && c.localized) {
     launch_xwait_scatter(c);  // comm-order view of the cross-stage waits (once per analysis)

@@ -133,6 +133,9 @@ struct Ctx {
   bool fused_used = false;               // results of the last analysis come from the fused path
   bool tiles_ready = false;              // general tile prefixes exist (needed by event-order exports)
   bool xwait_pending = false;            // fused: cross-stage waits still in slot order (k_xwait_scatter on export)
+  bool partial_tail = false;             // fused_all stops before candidates / links / walk (streaming sub-analysis)
+  bool stream_mode = false;              // window-level outputs of a sliding-window stream (stream.cu)
+  void* stream_state = nullptr;          // StreamState (stream.cu), owned
   uint32_t FT = 0, FR = 0, n_ftiles = 0; // positions per fused tile, ranks per stage, fused tiles
   std::vector<uint32_t> h_st_tile0, h_st_npos;
   DevBuf st_tile0, st_npos, role_comm, role_slot, role_type, ncroles;
@@ -234,9 +237,15 @@ scan_status alloc_match_buffers(Ctx& c, bool fused);
 scan_status alloc_detect(Ctx& c);
 scan_status alloc_localize(Ctx& c);
 scan_status sharded_all(Ctx& c);
+scan_status fused_all(Ctx& c);
+int launch_shard_head(Ctx& c, unsigned long long* out);
+int launch_shard_fixup(Ctx& c, int G, const unsigned long long* ht);
+int launch_link_median_window(Ctx& c, const uint64_t* base, const uint32_t* nmax, const uint64_t* slot, const uint4* rec,
+                              const uint32_t* iter, const uint32_t* pay, uint64_t n_inst);
 scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out);
 scan_status ensure_tiles(Ctx& c);
 void shard_release(Ctx& c);
+void stream_release(Ctx& c);
 
 }  // namespace ms
 

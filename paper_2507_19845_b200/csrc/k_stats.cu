@@ -659,6 +659,24 @@ int launch_link_median(Ctx& c) {
   return 1;
 }
 
+// Per-link medians over a caller-provided instance layout (streaming: the window's samples in
+// link-major, age-minor order; base / nmax / slot indexed by channel id n_comms + pid)
+int launch_link_median_window(Ctx& c, const uint64_t* base, const uint32_t* nmax, const uint64_t* slot, const uint4* rec,
+                              const uint32_t* iter, const uint32_t* pay, uint64_t n_inst) {
+  if (c.n_p2p == 0) return 0;
+  const uint64_t np_inst = std::max<uint64_t>(n_inst, 1);
+  if (c.lk_scratch.ensure(np_inst * 12) != cudaSuccess) return 0;
+  LKArgs a{c.n_comms, (uint32_t)c.n_p2p, c.NW, c.dcfg.window_iters, c.W, c.TP, c.DP, base, nmax,
+           c.ch_nsend.as<uint32_t>() + c.n_p2p, c.ch_nrecv.as<uint32_t>() + c.n_p2p, rec, iter, pay, slot, 0, 0,
+           c.lcfg.min_samples, c.lk_n.as<uint32_t>(), c.lk_used.as<uint8_t>(), c.lk_medp.as<uint32_t>(), c.lk_medt.as<uint32_t>(),
+           c.lk_bw.as<double>(), c.lk_dir.as<uint8_t>(), c.lk_elig.as<uint8_t>(), c.counters.as<Counters>(),
+           c.lk_scratch.as<unsigned long long>(), (uint32_t*)(c.lk_scratch.as<unsigned long long>() + np_inst), 1u, 0u};
+  const size_t smm = (size_t)LM_CAP * 12;
+  cudaFuncSetAttribute(k_link_median, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smm);
+  k_link_median<<<(unsigned)(c.NW * c.n_p2p), LM_NT, smm, c.stream>>>(a);
+  return 1;
+}
+
 int launch_link_flags(Ctx& c) {
   if (c.n_p2p == 0) return 0;
   const size_t sm = 3 * LINK_CAP * sizeof(uint32_t);

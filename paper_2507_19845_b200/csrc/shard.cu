@@ -675,6 +675,19 @@ scan_status sharded_all(Ctx& c) {
   return SCAN_OK;
 }
 
+int launch_shard_head(Ctx& c, unsigned long long* out) {
+  k_shard_head<<<(unsigned)((c.W + 7) / 8), 256, 0, c.stream>>>(
+      c.W, c.rank_off.as<uint64_t>(), c.d_kind, c.r_comm_off.as<uint64_t>(), c.r_bits_off.as<uint64_t>(),
+      c.r_ncomp.as<uint32_t>(), c.bits.as<uint32_t>(), c.inst_c.as<uint32_t>(), c.inst_rec.as<uint4>(),
+      c.lcfg.stage2_classes, (unsigned long long)c.lcfg.late_margin_ns, c.dcfg.window_iters, c.it_off, out);
+  return 1;
+}
+
+int launch_shard_fixup(Ctx& c, int G, const unsigned long long* ht) {
+  k_shard_fixup<<<(unsigned)((c.W + 255) / 256), 256, 0, c.stream>>>(c.W, G, ht, c.wl_joined.as<uint32_t>(), c.wl_late.as<uint32_t>());
+  return 1;
+}
+
 void shard_release(Ctx& c) {
   if (c.nccl) ncclCommDestroy((ncclComm_t)c.nccl);
   c.nccl = nullptr;
