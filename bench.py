@@ -155,7 +155,33 @@ def streaming_c5(ms, torch, local, stream) -> dict:
             det = w0 + K - 1
     s.close()
     lat = np.array(lat)
-    return {"workload": "C5 512-rank TP8xPP8xDP8, L_s=8, M=8, 100-it stream, 50-it window re-analysed per iteration "
+    # NEXT-3: the same stream pushed one iteration at a time into a sliding-window context
+    import time as _t
+    si = ms.Scan(local, stream.cuda_stream)
+    si.stream_open(full, K)
+    plat, pdet = [], None
+    for it in range(cfg.iterations):
+        lo = np.array([ro[r] + first[r][it] for r in range(W)])
+        hi = np.array([ro[r] + first[r][it + 1] for r in range(W)])
+        idx = torch.from_numpy(np.concatenate([np.arange(a, b) for a, b in zip(lo, hi)])).cuda(local)
+        cols = {k: v.index_select(0, idx) for k, v in dev.items()}
+        iro = np.zeros(W + 1, np.uint64)
+        iro[1:] = np.cumsum(hi - lo)
+        torch.cuda.synchronize()
+        t0 = _t.perf_counter()
+        si.stream_push(replace(full, rank_offsets=iro), device_ptrs=True, cols=cols)
+        plat.append((_t.perf_counter() - t0) * 1e3)
+        if it >= K - 1:
+            v = int(si.export("wl_verdict")[src])
+            if pdet is None and v in (1, 3):
+                pdet = it
+    si.close()
+    plat = np.array(plat[K - 1:])  # full windows
+    incremental = {"latency_ms_median": float(np.median(plat)), "latency_ms_p99": float(np.percentile(plat, 99)),
+                   "detected_at_iteration": pdet, "steps_to_detection": (pdet - onset + 1) if pdet is not None else None,
+                   "timing": "wall clock per scan_stream_push (synchronous call; device-resident iteration columns)"}
+    return {"incremental": incremental,
+            "workload": "C5 512-rank TP8xPP8xDP8, L_s=8, M=8, 100-it stream, 50-it window re-analysed per iteration "
                         "(51 windows); rank 208 x2.5 from it 30, its 7 TP peers x1.8 on 40% of ops",
             "window_events": nev, "windows": len(lat), "latency_ms_median": float(np.median(lat)),
             "latency_ms_p99": float(np.percentile(lat, 99)), "value": nev / (float(np.median(lat)) / 1e3),

@@ -611,6 +611,35 @@ scan_status general_localize(Ctx& c) {
 
 }  // namespace
 
+// ---- streaming fast path: the previous fused analysis of this context was on a trace with the same
+// per-rank event counts (a new iteration of an SPMD job): the template, tile bases, channel tables
+// and buffer sizes are reused; the fused kernel re-verifies every event against the cached
+// template (a deviation is reported, never silently analysed). Partials only (partial_tail).
+scan_status ms::fused_rerun(Ctx& c) {
+  c.matched = c.detected = c.localized = false;
+  scan_status st;
+  if ((st = alloc_match_buffers(c, true)) || (st = alloc_detect(c)) || (st = alloc_localize(c))) return st;
+  queue_fill(c, c.dlate.p, (uint64_t)c.n_ftiles * ((c.FR + 31) / 32) * 4 + 4, 0);
+  queue_fill(c, c.wd_total.p, (uint64_t)c.NW * c.W * 4, 0);
+  queue_fill(c, c.wd_slow.p, (uint64_t)c.NW * c.W * 4, 0);
+  Counters z = c.hc;
+  z.overflow = 0; z.bad_event = ~0ull;
+  z.n_incomplete = z.n_kind_mismatch = z.n_payload_mismatch = 0;
+  z.n_compared = z.n_slow = z.n_candidates = z.n_class_mismatch = 0;
+  z.n_link_slow = z.n_roots = z.n_victims = z.n_unattributed = 0;
+  for (auto& v : z.v_count) v = 0;
+  CK(cudaMemcpyAsync(c.counters.p, &z, sizeof(Counters), cudaMemcpyHostToDevice, c.stream));
+  c.launches += timed(c, "k_class_counts", [&] { return launch_class_counts(c); });
+  c.launches += timed(c, "k_fused", [&] { return launch_fused(c); });
+  c.launches += timed(c, "k_cross_reduce", [&] { return launch_cross_reduce(c); });
+  c.launches += timed(c, "k_deferred", [&] { return launch_deferred(c); });
+  if ((st = sync_read(c))) return st;
+  if (c.hc.overflow & 32u) { c.err = "streaming: an iteration deviates from the cached SPMD template"; return SCAN_E_UNSUPPORTED; }
+  c.matched = c.detected = c.localized = true;
+  c.fused_used = true;
+  return SCAN_OK;
+}
+
 // ---- the fused SPMD path (K9); returns 2 when the trace is not SPMD (caller falls back)
 scan_status ms::fused_all(Ctx& c) {
   c.matched = c.detected = c.localized = false;

@@ -238,6 +238,7 @@ scan_status alloc_detect(Ctx& c);
 scan_status alloc_localize(Ctx& c);
 scan_status sharded_all(Ctx& c);
 scan_status fused_all(Ctx& c);
+scan_status fused_rerun(Ctx& c);
 int launch_shard_head(Ctx& c, unsigned long long* out);
 int launch_shard_fixup(Ctx& c, int G, const unsigned long long* ht);
 int launch_link_median_window(Ctx& c, const uint64_t* base, const uint32_t* nmax, const uint64_t* slot, const uint4* rec,

@@ -198,22 +198,49 @@ scan_status scan_stream_push(scan_ctx* ctx, const scan_event_columns* iteration,
   CK(cudaSetDevice(c.device));
   Ctx& u = S.sub->c;
   // 1. the new iteration, analysed alone (fused pass, partials only)
-  scan_comm_table ct{(uint32_t)(S.coff.size() - 1), S.coff.data(), S.cmem.data()};
-  scan_status st = scan_load_events(S.sub, &S.topo, &ct, iteration, flags & (SCAN_HOST_PTRS | SCAN_DEVICE_PTRS));
-  if (st) { c.err = std::string("streaming load: ") + u.err; return st; }
-  if (!u.spmd) { c.err = "streaming needs SPMD iterations"; return SCAN_E_UNSUPPORTED; }
-  u.dcfg = c.dcfg; u.lcfg = c.lcfg; u.partial_tail = true;
-  if ((st = fused_all(u))) { c.err = std::string("streaming analysis: ") + u.err; return st < 0 ? st : SCAN_E_UNSUPPORTED; }
+  scan_status st;
+  const uint64_t W0 = (uint64_t)S.topo.tp * S.topo.pp * S.topo.dp;
+  bool same = S.ready && iteration->rank_offsets && u.h_rank_off.size() == W0 + 1 &&
+              std::equal(u.h_rank_off.begin(), u.h_rank_off.end(), iteration->rank_offsets);
+  if (same) {  // same per-rank counts as the previous iteration: new columns, cached structure
+    const uint64_t N = u.N;
+    if (flags & SCAN_DEVICE_PTRS) {
+      const void* ptrs[] = {iteration->dur_ns, iteration->kind_op, iteration->meta, iteration->comm, iteration->payload_bytes};
+      for (const void* p : ptrs)
+        if (N && ((uintptr_t)p & 15)) { c.err = "device columns must be 16-byte aligned"; return SCAN_E_INVALID_ARG; }
+      u.d_dur = iteration->dur_ns; u.d_kind = iteration->kind_op; u.d_meta = iteration->meta;
+      u.d_comm = iteration->comm; u.d_pay = iteration->payload_bytes;
+    } else {
+      CK(u.own_dur.ensure(N * 4)); CK(u.own_kind.ensure(N * 2)); CK(u.own_meta.ensure(N * 2));
+      CK(u.own_comm.ensure(N * 4)); CK(u.own_pay.ensure(N * 4));
+      const cudaMemcpyKind hd = cudaMemcpyHostToDevice;
+      CK(cudaMemcpyAsync(u.own_dur.p, iteration->dur_ns, N * 4, hd, u.stream));
+      CK(cudaMemcpyAsync(u.own_kind.p, iteration->kind_op, N * 2, hd, u.stream));
+      CK(cudaMemcpyAsync(u.own_meta.p, iteration->meta, N * 2, hd, u.stream));
+      CK(cudaMemcpyAsync(u.own_comm.p, iteration->comm, N * 4, hd, u.stream));
+      CK(cudaMemcpyAsync(u.own_pay.p, iteration->payload_bytes, N * 4, hd, u.stream));
+      u.d_dur = u.own_dur.as<uint32_t>(); u.d_kind = u.own_kind.as<uint16_t>(); u.d_meta = u.own_meta.as<uint16_t>();
+      u.d_comm = u.own_comm.as<uint32_t>(); u.d_pay = u.own_pay.as<uint32_t>();
+    }
+    if ((st = fused_rerun(u))) { c.err = std::string("streaming analysis: ") + u.err; return st; }
+  } else {
+    scan_comm_table ct{(uint32_t)(S.coff.size() - 1), S.coff.data(), S.cmem.data()};
+    st = scan_load_events(S.sub, &S.topo, &ct, iteration, flags & (SCAN_HOST_PTRS | SCAN_DEVICE_PTRS));
+    if (st) { c.err = std::string("streaming load: ") + u.err; return st; }
+    if (!u.spmd) { c.err = "streaming needs SPMD iterations"; return SCAN_E_UNSUPPORTED; }
+    u.dcfg = c.dcfg; u.lcfg = c.lcfg; u.partial_tail = true;
+    if ((st = fused_all(u))) { c.err = std::string("streaming analysis: ") + u.err; return st < 0 ? st : SCAN_E_UNSUPPORTED; }
+  }
   if (!S.ready) {
     if ((st = establish(c, S, u))) return st;
-  } else {
+  } else if (!same) {  // a reloaded iteration: its channel structure must be the first one's
     std::vector<uint32_t> nl(S.np);
-    bool same = u.n_p2p == S.np && u.W == c.W && u.nnz_c == c.nnz_c;
-    if (same && S.np) {
+    bool ok = u.n_p2p == S.np && u.W == c.W && u.nnz_c == c.nnz_c;
+    if (ok && S.np) {
       CK(cudaMemcpy(nl.data(), u.ch_nmax.as<uint32_t>() + u.n_comms, S.np * 4ull, cudaMemcpyDeviceToHost));
-      same = nl == S.nl;
+      ok = nl == S.nl;
     }
-    if (!same) { c.err = "streaming: an iteration's channel structure differs from the first one"; return SCAN_E_UNSUPPORTED; }
+    if (!ok) { c.err = "streaming: an iteration's channel structure differs from the first one"; return SCAN_E_UNSUPPORTED; }
   }
   const uint64_t W = c.W, K = S.K, s = S.pushes % K;
   // 2. snapshot the iteration's partials into ring slot s
