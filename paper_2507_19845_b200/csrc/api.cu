@@ -94,7 +94,7 @@ static void release_all(Ctx& c) {
                     &c.rcomm_off, &c.rcomm, &c.nbc_off, &c.nbc, &c.tile_rank, &c.tile_start, &c.rank_tile0, &c.t_nkeys,
                     &c.t_keys, &c.t_cnt, &c.t_pref, &c.t_ncomm, &c.t_niter, &c.t_last, &c.t_commpre, &c.t_iterpre,
                     &c.t_prevj, &c.r_nkeys, &c.r_keys, &c.r_cnt, &c.r_ncomm, &c.r_niter, &c.r_ncomp, &c.r_lastit,
-                    &c.r_comm_off, &c.r_comp_off, &c.r_bits_off, &c.bitmap, &c.bitpre, &c.counters, &c.ch_nmax,
+                    &c.r_comm_off, &c.r_comp_off, &c.r_bits_off, &c.bitmap, &c.bitpre, &c.bmsum, &c.counters, &c.ch_nmax,
                     &c.ch_nmin, &c.ch_base, &c.ch_slot, &c.ch_nsend, &c.ch_nrecv, &c.inst_c, &c.wait_c, &c.cdur, &c.cop,
                     &c.sdur, &c.skind, &c.p2p_pay, &c.p2p_warm, &c.p2p_iter, &c.inst_rec, &c.citer, &c.nbp, &c.nbp_n,
                     &c.rk_sum, &c.bits, &c.cref, &c.cl_J, &c.cl_max, &c.cl_min, &c.wd_total, &c.wd_slow, &c.wd_cand,

@@ -96,7 +96,7 @@ struct Ctx {
   DevBuf t_nkeys, t_keys, t_cnt, t_pref, t_ncomm, t_niter, t_last, t_commpre, t_iterpre, t_prevj;
   DevBuf r_nkeys, r_keys, r_cnt, r_ncomm, r_niter, r_ncomp, r_lastit;
   DevBuf r_comm_off, r_comp_off, r_bits_off;          // u64 [W+1]
-  DevBuf bitmap, bitpre;                               // P2P channel bitmap (u32 words) + word prefix
+  DevBuf bitmap, bitpre, bmsum;                        // P2P channel bitmap (u32 words) + word prefix + block sums
   uint64_t n_bm_words = 0;
   DevBuf counters;                                     // Counters
   Counters hc{};

@@ -334,17 +334,43 @@ __global__ void __launch_bounds__(RP_NT) k_rank_prefix(int W, const uint32_t* r_
     __syncthreads();
   }
   if (threadIdx.x == 0) { r_comm_off[W] = carry[0]; r_comp_off[W] = carry[1]; r_bits_off[W] = carry[2]; cnt->n_bits_words = carry[2]; }
+}
+
+// P2P channel ids = popcount prefix of the W^2-bit bitmap, as a three-kernel multi-CTA scan
+// (the bitmap has W^2/32 words: 295K at W = 3072): block sums, one scan of the sums, block scans
+constexpr int BP_NT = 1024;
+__global__ void __launch_bounds__(BP_NT) k_bitmap_sums(const uint32_t* bitmap, uint64_t n_words, uint32_t* bsum) {
+  __shared__ uint32_t sm[33];
+  const uint64_t w = (uint64_t)blockIdx.x * BP_NT + threadIdx.x;
+  uint32_t tot;
+  block_excl_sum<BP_NT>(w < n_words ? (uint32_t)__popc(bitmap[w]) : 0u, tot, sm);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(BP_NT) k_bitmap_scan(uint32_t* bsum, uint32_t nb, Counters* cnt) {
+  __shared__ uint32_t sm[33];
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  unsigned long long pc = 0;
-  for (uint64_t b = 0; b < n_words; b += RP_NT) {
-    const uint64_t w = b + threadIdx.x;
-    const uint32_t v = w < n_words ? (uint32_t)__popc(bitmap[w]) : 0;
+  for (uint32_t b = 0; b < nb; b += BP_NT) {
+    const uint32_t i = b + threadIdx.x;
+    const uint32_t v = i < nb ? bsum[i] : 0u;
     uint32_t tot;
-    const uint32_t ex = block_excl_sum<RP_NT>(v, tot, sm);
-    if (w < n_words) bitpre[w] = (uint32_t)(pc + ex);
-    pc += tot;
+    const uint32_t ex = block_excl_sum<BP_NT>(v, tot, sm);
+    if (i < nb) bsum[i] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
   }
-  if (threadIdx.x == 0) cnt->n_p2p = pc;
+  if (threadIdx.x == 0) cnt->n_p2p = carry;
+}
+
+__global__ void __launch_bounds__(BP_NT) k_bitmap_pre(const uint32_t* bitmap, uint64_t n_words, const uint32_t* bsum, uint32_t* bitpre) {
+  __shared__ uint32_t sm[33];
+  const uint64_t w = (uint64_t)blockIdx.x * BP_NT + threadIdx.x;
+  uint32_t tot;
+  const uint32_t ex = block_excl_sum<BP_NT>(w < n_words ? (uint32_t)__popc(bitmap[w]) : 0u, tot, sm);
+  if (w < n_words) bitpre[w] = bsum[blockIdx.x] + ex;
 }
 
 int launch_rank_prefix(Ctx& c) {
@@ -352,7 +378,13 @@ int launch_rank_prefix(Ctx& c) {
                                            c.r_comm_off.as<uint64_t>(), c.r_comp_off.as<uint64_t>(),
                                            c.r_bits_off.as<uint64_t>(), c.bitmap.as<uint32_t>(), c.bitpre.as<uint32_t>(),
                                            c.n_bm_words, c.counters.as<Counters>());
-  return 1;
+  const uint32_t nb = (uint32_t)((c.n_bm_words + BP_NT - 1) / BP_NT);
+  if (c.bmsum.ensure((uint64_t)std::max<uint32_t>(nb, 1) * 4) != cudaSuccess) return 1;
+  k_bitmap_sums<<<std::max<uint32_t>(nb, 1), BP_NT, 0, c.stream>>>(c.bitmap.as<uint32_t>(), c.n_bm_words, c.bmsum.as<uint32_t>());
+  k_bitmap_scan<<<1, BP_NT, 0, c.stream>>>(c.bmsum.as<uint32_t>(), nb, c.counters.as<Counters>());
+  k_bitmap_pre<<<std::max<uint32_t>(nb, 1), BP_NT, 0, c.stream>>>(c.bitmap.as<uint32_t>(), c.n_bm_words, c.bmsum.as<uint32_t>(),
+                                                                  c.bitpre.as<uint32_t>());
+  return 4;
 }
 
 // ----------------------------------------------------------------------------- P2P channels

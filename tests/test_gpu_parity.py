@@ -282,3 +282,10 @@ def test_fused_generic_tile_kernel(name):
         g = _gpu_variant(tr, variant, d, l_)
         compare(o, g)
         assert g["_res"]["fused"]
+
+
+def test_c4_shape():
+    """configs[3] shape: 3072 ranks TP8xPP64xDP6 (non-power-of-two DP, 64 stages), a throttled rank
+    and a half-bandwidth link; 3 iterations (4.8 M events)."""
+    o, g = _run_both(tg.generate(configs.c4(iterations=3)), min_samples=5)
+    compare(o, g)
