@@ -190,6 +190,81 @@ def streaming_c5(ms, torch, local, stream) -> dict:
             "note": "every window analysed from scratch (scan_analyze); incremental streaming is SURVEY NEXT-3"}
 
 
+def json_io(ms, torch, local, stream, steps: int, warmup: int, cpu: bool) -> dict:
+    """NEXT-2 (scan_ingest_json / scan_emit_chrome): the per-rank Chrome-trace JSON files of the C2
+    job (TP8xPP4xDP2, 64 ranks, 40 iterations) parsed on the GPU into the event columns (device-
+    resident bytes, CUDA events around the call), then the merged, annotated document emitted."""
+    import ctypes
+    import tracegen as tg
+    from tracegen import chrome, configs
+    cfg = configs.c2(seed=1, iterations=40)
+    tr = tg.generate(cfg)
+    data, off = chrome.rank_documents_fast(tr)
+    nbytes = len(data)
+    host = torch.frombuffer(bytearray(data), dtype=torch.uint8).pin_memory()
+    dbuf = host.cuda(local)
+    lib = ms._load_lib()
+    s = ms.Scan(local, stream.cuda_stream)
+    topo = (cfg.tp, cfg.pp, cfg.dp)
+    for _ in range(max(1, warmup)):
+        res = ms.scan_ingest_json(s.ctx, *topo, dbuf, off, ms.SCAN_DEVICE_PTRS)
+    torch.cuda.synchronize()
+    s.set_timing(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        res = ms.scan_ingest_json(s.ctx, *topo, dbuf, off, ms.SCAN_DEVICE_PTRS)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ims = e0.elapsed_time(e1) / steps
+    ik = s.kernel_timing()
+    s.set_timing(False)
+    # e2e: pinned host bytes -> H2D inside the call -> parse -> load
+    t0 = time.perf_counter()
+    ms.scan_ingest_json(s.ctx, *topo, host.numpy(), off, ms.SCAN_HOST_PTRS)
+    e2e_s = time.perf_counter() - t0
+    # emit: analysis once (untimed), then the document build (size query) per step
+    s.analyze()
+    nb = ctypes.c_uint64()
+    for _ in range(max(1, warmup)):
+        ms._check(s.ctx, lib.scan_emit_chrome(s.ctx, 0, None, 0, 0, ctypes.byref(nb)))
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        ms._check(s.ctx, lib.scan_emit_chrome(s.ctx, 0, None, 0, 0, ctypes.byref(nb)))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1) / steps
+    t0 = time.perf_counter()
+    out = s.emit_chrome()
+    emit_e2e_s = time.perf_counter() - t0
+    s.close()
+    base = None
+    if cpu:  # oracle (Python json) on the first two ranks' files
+        from oracle import chrome_json as cj
+        docs = [data[int(off[r]):int(off[r + 1])] for r in range(2)]
+        t0 = time.perf_counter()
+        t_, _ = cj.parse(docs, *topo)
+        dt = time.perf_counter() - t0
+        nb_s = sum(len(d) for d in docs)
+        base = {"value": nb_s / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                "sample": f"oracle.chrome_json.parse of ranks 0-1's files ({nb_s / 1e6:.1f} MB, {t_.n_events} events), "
+                          "Python json module, one core"}
+    kern = {k: {"ms_per_call": round(v[0] / steps, 4), "launches": v[1]} for k, v in sorted(ik.items(), key=lambda kv: -kv[1][0])}
+    return {"metric": "Chrome-trace JSON parsed into event columns per second (scan_ingest_json)",
+            "value": nbytes / (ims / 1e3) / 1e9, "unit": "GB/s",
+            "events_per_s": res["n_events"] / (ims / 1e3), "ms_per_call": ims, "json_bytes": nbytes,
+            "events": int(res["n_events"]), "docs": int(len(off) - 1),
+            "workload": "C2 TP8xPP4xDP2 (64 per-rank files), 40 iterations, clean tracer format",
+            "kernels": kern,
+            "e2e": {"value": nbytes / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 0,
+                    "path": "pinned host bytes -> scan_ingest_json(SCAN_HOST_PTRS), wall clock"},
+            "emit": {"value": len(out) / (ems / 1e3) / 1e9, "unit": "GB/s (merged document built on the device)",
+                     "ms_per_call": ems, "bytes": len(out),
+                     "e2e_gb_s": len(out) / emit_e2e_s / 1e9},
+            "cpu_baseline": base}
+
+
 def cpu_oracle_rate(name: str, sample_iters: int, seed: int) -> dict:
     import oracle
     tr, _ = make_trace(name, sample_iters, seed, pinned=False)
@@ -237,6 +312,7 @@ def main():
     ap.add_argument("--breakdown", action="store_true", default=True)
     ap.add_argument("--no-align", action="store_true", help="skip the timeline-alignment measurement (N=1 only)")
     ap.add_argument("--no-stream", action="store_true", help="skip the C5 sliding-window measurement (N=1 only)")
+    ap.add_argument("--no-json", action="store_true", help="skip the JSON ingest / emit measurement (N=1 only)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -380,6 +456,8 @@ def main():
         del dev["start_ns"]
 
     streaming = streaming_c5(ms, torch, local, stream) if (world == 1 and not args.no_stream) else None
+    json_ingest = json_io(ms, torch, local, stream, args.steps, args.warmup, not args.no_cpu) if (
+        world == 1 and not args.no_json) else None
 
     if rank != 0:
         if dist:
@@ -439,6 +517,7 @@ def main():
         "verdicts": {"flagged": flagged},
         "alignment": alignment,
         "streaming_c5": streaming,
+        "json_ingest": json_ingest,
         "path": "fused SPMD stage-tile pass (K9)" if fused else "general path",
     }
     print(json.dumps(line), flush=True)

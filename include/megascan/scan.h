@@ -230,6 +230,68 @@ uint64_t    scan_stream_window(const scan_ctx* ctx);
 scan_status scan_create_sharded(scan_ctx** out, int cuda_device, void* cuda_stream, int n_shards, int shard,
                                 const uint8_t nccl_unique_id[128]);
 
+/* ---- NEXT-2: Chrome-trace JSON ingest and merged emit (DESIGN.md §10d J1-J12) -----
+   scan_ingest_json parses, ON THE DEVICE, one or more JSON documents: the per-rank files the
+   tracer writes ("every rank has its own recorded event sequence as a JSON file") or a
+   merged document. `bytes` holds the documents back to back, document i = [doc_offsets[i],
+   doc_offsets[i+1]) (doc_offsets: HOST, n_docs+1 entries, monotone, doc_offsets[0] = 0,
+   doc_offsets[n_docs] = n_bytes); `bytes` is HOST memory (copied H2D, pinned recommended) or,
+   with SCAN_DEVICE_PTRS in flags, device memory of the ctx device (borrowed for the call).
+   Schema (J1-J9): a document is {"traceEvents":[...], ...} or a bare array; an element with
+   "ph":"X" is a trace event with "ts"/"dur" (microseconds, <= 3 decimals, converted exactly to
+   ns), "pid" (rank < tp*pp*dp), "cat" (compute, all_reduce, all_gather, reduce_scatter,
+   broadcast, send, recv) and optional "args": op, iter_end, mb, chunk, bwd, warmup (tracers.scope
+   metadata), "group" (ascending participant ranks, required for collectives),
+   "peer" (required for send/recv), "bytes" (payload). Other elements ("ph" != "X") are skipped.
+   Events are put in program order per rank (ascending ts, ties by input position), every
+   distinct group becomes a communicator, numbered in order of first use in that order. On
+   success the context is loaded exactly as scan_load_events would load those columns (with
+   start_ns), so every analysis call and export follows; SCAN_OUT_EV_* input columns are
+   readable with scan_loaded_column().
+   Errors: SCAN_E_SCHEMA with out->err_kind = SCAN_JSON_SYNTAX (malformed JSON; offset = first
+   byte rejected) or SCAN_JSON_SCHEMA (out->err_field = SCAN_JF_*, offset = the '{' of the
+   offending element, or of the document root for SCAN_JF_TRACE_EVENTS); a syntax error anywhere
+   wins over any schema error, among schema errors the smallest offset wins (J11). SCAN_E_INVALID_ARG
+   (offsets), SCAN_E_UNSUPPORTED (> 2^32-1 elements; a 64-bit group-hash collision), load errors.
+   J10: bytes outside the event arrays are checked for bracket / quote balance only.           */
+#define SCAN_JSON_OK      0
+#define SCAN_JSON_SYNTAX  1
+#define SCAN_JSON_SCHEMA  2
+enum { SCAN_JF_TRACE_EVENTS = 1, SCAN_JF_EVENT, SCAN_JF_PH, SCAN_JF_TS, SCAN_JF_DUR, SCAN_JF_PID, SCAN_JF_CAT,
+       SCAN_JF_ARGS, SCAN_JF_OP, SCAN_JF_ITER_END, SCAN_JF_MB, SCAN_JF_CHUNK, SCAN_JF_BWD, SCAN_JF_WARMUP,
+       SCAN_JF_GROUP, SCAN_JF_PEER, SCAN_JF_BYTES };
+typedef struct scan_json_result {
+    uint64_t n_events;      /* trace events loaded                                               */
+    uint64_t n_skipped;     /* event-array elements with "ph" != "X"                              */
+    uint32_t n_comms;       /* distinct participant lists                                         */
+    int32_t  err_kind;      /* SCAN_JSON_*                                                        */
+    int32_t  err_field;     /* SCAN_JF_* of a schema error                                        */
+    uint32_t reserved;
+    uint64_t err_offset;    /* byte offset into `bytes`                                           */
+} scan_json_result;
+scan_status scan_ingest_json(scan_ctx* ctx, const scan_topology* topo, const uint8_t* bytes, uint64_t n_bytes,
+                             const uint64_t* doc_offsets, uint32_t n_docs, uint32_t flags, scan_json_result* out);
+
+/* The loaded event columns (any load path): 0 start_ns (i64; needs start times), 1 dur_ns (u32),
+   2 kind_op (u16), 3 meta (u16), 4 comm (u32), 5 payload (u32), 6 rank_offsets (u64 [W+1]),
+   7 comm offsets (u64), 8 comm members (u32). Copies into dst (host or device); *bytes = size.
+   dst NULL: size only. Errors: SCAN_E_ORDER (nothing loaded), SCAN_E_INVALID_ARG.            */
+scan_status scan_loaded_column(scan_ctx* ctx, int column, void* dst, uint64_t dst_bytes, int dst_is_device, uint64_t* bytes);
+
+/* scan_emit_chrome writes the merged Chrome Tracing document of the loaded job (P:L119-125:
+   "merges them-ordered by time-into a single JSON file"; pid = rank) with every communication
+   event's matched instance id in args.related_sync_op. Byte format J12: events ordered
+   by (timestamp, rank, program order), ts/dur in microseconds with exactly 3 decimals, args in
+   the fixed order op, iter_end, mb, chunk, bwd, warmup, group | peer, bytes, related_sync_op,
+   zero-valued metadata omitted. SCAN_EMIT_ALIGNED: timestamps of the last scan_align.
+   The document is built on the device: a call with dst NULL builds it and returns its size in
+   *n_bytes; a call with dst (host or device memory of dst_bytes >= *n_bytes) copies the document
+   built for the current state (load / analysis / alignment), building it first if needed. Requires start_ns at load and a match (scan_match_collectives or
+   scan_analyze); errors: SCAN_E_ORDER, SCAN_E_INVALID_ARG, SCAN_E_UNSUPPORTED (stream or
+   sharded context), SCAN_E_OOM, SCAN_E_CUDA.                                                 */
+#define SCAN_EMIT_ALIGNED 1u
+scan_status scan_emit_chrome(scan_ctx* ctx, uint32_t flags, void* dst, uint64_t dst_bytes, int dst_is_device, uint64_t* n_bytes);
+
 /* A0 ingest: validate sizes, place the columns on the device, build the comm tables.
    Per-event schema validation happens in scan_match_collectives (one pass).
    Errors: SCAN_E_INVALID_ARG (sizes, alignment, rank_order), SCAN_E_UNSUPPORTED

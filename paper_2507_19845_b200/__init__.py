@@ -66,6 +66,21 @@ class _Comms(ctypes.Structure):
     _fields_ = [("n_comms", ctypes.c_uint32), ("offsets", ctypes.c_void_p), ("members", ctypes.c_void_p)]
 
 
+class _JsonRes(ctypes.Structure):
+    _fields_ = [("n_events", ctypes.c_uint64), ("n_skipped", ctypes.c_uint64), ("n_comms", ctypes.c_uint32),
+                ("err_kind", ctypes.c_int32), ("err_field", ctypes.c_int32), ("reserved", ctypes.c_uint32),
+                ("err_offset", ctypes.c_uint64)]
+
+
+class JsonTraceError(RuntimeError):
+    """scan_ingest_json rejected the input: ``kind`` 1 syntax / 2 schema, ``field`` (SCAN_JF_*),
+    ``offset`` (byte offset into the concatenated documents)."""
+
+    def __init__(self, status: int, msg: str, kind: int, field: int, offset: int):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status, self.kind, self.field, self.offset = status, kind, field, offset
+
+
 class _AlignCfg(ctypes.Structure):
     _fields_ = [("reference", ctypes.c_int32), ("reserved", ctypes.c_uint32)]
 
@@ -161,9 +176,14 @@ def _load_lib():
     lib.scan_stream_window.argtypes = [P]
     lib.scan_stream_window.restype = ctypes.c_uint64
     lib.scan_create_sharded.argtypes = [ctypes.POINTER(P), ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P]
+    lib.scan_ingest_json.argtypes = [P, ctypes.POINTER(_Topo), P, ctypes.c_uint64, P, ctypes.c_uint32, ctypes.c_uint32,
+                                     ctypes.POINTER(_JsonRes)]
+    lib.scan_loaded_column.argtypes = [P, ctypes.c_int, P, ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]
+    lib.scan_emit_chrome.argtypes = [P, ctypes.c_uint32, P, ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]
     for f in ("scan_create", "scan_load_events", "scan_match_collectives", "scan_detect", "scan_localize",
               "scan_output_size", "scan_export", "scan_analyze", "scan_force_general", "scan_fused_variant",
-              "scan_nccl_unique_id", "scan_create_sharded", "scan_align", "scan_stream_open", "scan_stream_push"):
+              "scan_nccl_unique_id", "scan_create_sharded", "scan_align", "scan_stream_open", "scan_stream_push",
+              "scan_ingest_json", "scan_loaded_column", "scan_emit_chrome"):
         getattr(lib, f).restype = ctypes.c_int32
     _lib = lib
     return lib
@@ -174,7 +194,7 @@ EXPORTED_SYMBOLS = ["scan_create", "scan_destroy", "scan_last_error", "scan_load
                     "scan_kernel_launches", "scan_set_timing", "scan_timing_reset", "scan_kernel_timing",
                     "scan_analyze", "scan_used_fused", "scan_force_general", "scan_fused_variant",
                     "scan_nccl_unique_id", "scan_create_sharded", "scan_align", "scan_stream_open", "scan_stream_push",
-                    "scan_stream_window"]
+                    "scan_stream_window", "scan_ingest_json", "scan_loaded_column", "scan_emit_chrome"]
 
 
 @dataclass
@@ -271,6 +291,56 @@ def scan_align(ctx, reference: int = 0) -> dict:
     r = _AlignRes()
     _check(ctx, _load_lib().scan_align(ctx, ctypes.byref(_AlignCfg(int(reference), 0)), ctypes.byref(r)))
     return {n: getattr(r, n) for n, _ in r._fields_ if n != "reserved"}
+
+
+LOADED_COLUMNS = (("start_ns", np.int64), ("dur_ns", np.uint32), ("kind_op", np.uint16), ("meta", np.uint16),
+                  ("comm", np.uint32), ("payload", np.uint32), ("rank_offsets", np.uint64),
+                  ("comm_offsets", np.uint64), ("comm_members", np.uint32))
+SCAN_EMIT_ALIGNED = 1
+
+
+def scan_ingest_json(ctx, tp, pp, dp, data, doc_offsets, flags: int = SCAN_HOST_PTRS) -> dict:
+    """NEXT-2 (scan.h): parse JSON documents on the device and load them. ``data``: bytes / uint8
+    numpy array (host) or a uint8 CUDA tensor with ``flags=SCAN_DEVICE_PTRS``."""
+    lib = _load_lib()
+    if isinstance(data, (bytes, bytearray, memoryview)):
+        data = np.frombuffer(bytes(data), dtype=np.uint8)
+    n = int(data.numel() if hasattr(data, "numel") else data.size)
+    off = np.ascontiguousarray(doc_offsets, dtype=np.uint64)
+    r = _JsonRes()
+    st = lib.scan_ingest_json(ctx, ctypes.byref(_Topo(tp, pp, dp, 0)), _ptr(data) if n else None, n, off.ctypes.data,
+                              len(off) - 1, flags, ctypes.byref(r))
+    if st < 0:
+        raise JsonTraceError(st, lib.scan_last_error(ctx).decode(), r.err_kind, r.err_field, r.err_offset)
+    return {n_: getattr(r, n_) for n_, _ in r._fields_ if n_ != "reserved"}
+
+
+def scan_loaded_column(ctx, name: str) -> np.ndarray:
+    lib = _load_lib()
+    idx = [n for n, _ in LOADED_COLUMNS].index(name)
+    nb = ctypes.c_uint64()
+    _check(ctx, lib.scan_loaded_column(ctx, idx, None, 0, 0, ctypes.byref(nb)))
+    dt = dict(LOADED_COLUMNS)[name]
+    out = np.empty(nb.value // np.dtype(dt).itemsize, dtype=dt)
+    _check(ctx, lib.scan_loaded_column(ctx, idx, out.ctypes.data if out.size else None, nb.value, 0, ctypes.byref(nb)))
+    return out
+
+
+def scan_emit_chrome(ctx, aligned: bool = False, dst=None) -> bytes | int:
+    """Merged, annotated Chrome Tracing document (scan.h). Returns bytes, or the byte count when
+    ``dst`` (a uint8 CUDA tensor / numpy array large enough) receives it."""
+    lib = _load_lib()
+    flags = SCAN_EMIT_ALIGNED if aligned else 0
+    nb = ctypes.c_uint64()
+    _check(ctx, lib.scan_emit_chrome(ctx, flags, None, 0, 0, ctypes.byref(nb)))
+    if dst is not None:
+        dev = hasattr(dst, "is_cuda") and dst.is_cuda
+        _check(ctx, lib.scan_emit_chrome(ctx, flags, _ptr(dst), int(dst.numel() if hasattr(dst, "numel") else dst.size),
+                                         1 if dev else 0, ctypes.byref(nb)))
+        return nb.value
+    out = np.empty(nb.value, dtype=np.uint8)
+    _check(ctx, lib.scan_emit_chrome(ctx, flags, out.ctypes.data, nb.value, 0, ctypes.byref(nb)))
+    return out.tobytes()
 
 
 def scan_match_collectives(ctx) -> tuple[int, dict]:
@@ -403,6 +473,28 @@ class Scan:
     def align(self, reference: int = 0) -> dict:
         """Timeline alignment onto ``reference``'s clock (load with ``start=True`` first)."""
         return scan_align(self.ctx, reference)
+
+    # ---- NEXT-2 Chrome-trace JSON ingest / emit (scan.h)
+    def ingest_json(self, docs, tp: int, pp: int, dp: int, device: bool = False) -> dict:
+        """Parse JSON documents (a list of per-rank files' bytes, or one bytes object) on the GPU
+        and load the job; ``device=True`` stages the bytes in a CUDA tensor first (zero-copy ingest)."""
+        docs = [docs] if isinstance(docs, (bytes, bytearray)) else list(docs)
+        off = np.zeros(len(docs) + 1, dtype=np.uint64)
+        for i, d in enumerate(docs):
+            off[i + 1] = off[i] + len(d)
+        data = np.frombuffer(b"".join(docs), dtype=np.uint8)
+        if device:
+            import torch
+            data = torch.from_numpy(data.copy()).cuda()
+        self._keep = [data]
+        return scan_ingest_json(self.ctx, tp, pp, dp, data, off, SCAN_DEVICE_PTRS if device else SCAN_HOST_PTRS)
+
+    def loaded(self, name: str) -> np.ndarray:
+        """A loaded input column (``LOADED_COLUMNS``), e.g. after ``ingest_json``."""
+        return scan_loaded_column(self.ctx, name)
+
+    def emit_chrome(self, aligned: bool = False, dst=None):
+        return scan_emit_chrome(self.ctx, aligned, dst)
 
     # ---- NEXT-3 sliding-window streaming (scan.h)
     STREAM_OUTPUTS = tuple(n for n, _ in OUTPUTS if n.startswith(("rk_sum", "wd_", "wl_", "lk_", "lb_", "eg_")))

@@ -117,6 +117,7 @@ void scan_destroy(scan_ctx* ctx) {
   for (auto e : ctx->c.evpool) cudaEventDestroy(e);
   shard_release(ctx->c);
   stream_release(ctx->c);
+  json_release(ctx->c);
   release_all(ctx->c);
   delete ctx;
 }
@@ -160,6 +161,7 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
   CK(cudaSetDevice(c.device));
   c.loaded = c.matched = c.detected = c.localized = false;
   c.fused_used = false; c.tiles_ready = false; c.xwait_pending = false; c.aligned = false;
+  ++c.gen;
   if (c.stream_mode) { stream_release(c); c.stream_mode = false; }
   c.d_start = nullptr;
   c.err.clear();
@@ -704,6 +706,7 @@ extern "C" {
 scan_status scan_match_collectives(scan_ctx* ctx, scan_match_result* out) {
   if (!ctx) return SCAN_E_INVALID_ARG;
   Ctx& c = ctx->c;
+  ++c.gen;
   if (!c.loaded) { c.err = "scan_match_collectives before scan_load_events"; return SCAN_E_ORDER; }
   if (c.n_shards > 1) { c.err = "a sharded context runs scan_analyze only"; return SCAN_E_UNSUPPORTED; }
   CK(cudaSetDevice(c.device));
@@ -718,6 +721,7 @@ scan_status scan_match_collectives(scan_ctx* ctx, scan_match_result* out) {
 scan_status scan_detect(scan_ctx* ctx, const scan_detect_config* cfg, scan_detect_result* out) {
   if (!ctx) return SCAN_E_INVALID_ARG;
   Ctx& c = ctx->c;
+  ++c.gen;
   if (!c.matched) { c.err = "scan_detect before scan_match_collectives"; return SCAN_E_ORDER; }
   CK(cudaSetDevice(c.device));
   scan_detect_config d = cfg ? *cfg : kDefDetect;
@@ -733,6 +737,7 @@ scan_status scan_detect(scan_ctx* ctx, const scan_detect_config* cfg, scan_detec
 scan_status scan_localize(scan_ctx* ctx, const scan_localize_config* cfg, scan_localize_result* out) {
   if (!ctx) return SCAN_E_INVALID_ARG;
   Ctx& c = ctx->c;
+  ++c.gen;
   if (!c.detected || c.fused_used) { c.err = "scan_localize before scan_detect"; return SCAN_E_ORDER; }
   CK(cudaSetDevice(c.device));
   scan_localize_config L = cfg ? *cfg : kDefLocalize;
@@ -749,6 +754,7 @@ scan_status scan_analyze(scan_ctx* ctx, const scan_detect_config* dcfg, const sc
                          scan_match_result* mres, scan_detect_result* dres, scan_localize_result* lres) {
   if (!ctx) return SCAN_E_INVALID_ARG;
   Ctx& c = ctx->c;
+  ++c.gen;
   if (!c.loaded) { c.err = "scan_analyze before scan_load_events"; return SCAN_E_ORDER; }
   CK(cudaSetDevice(c.device));
   scan_detect_config d = dcfg ? *dcfg : kDefDetect;
@@ -784,6 +790,7 @@ int scan_used_fused(const scan_ctx* ctx) { return ctx && ctx->c.fused_used ? 1 :
 scan_status scan_align(scan_ctx* ctx, const scan_align_config* cfg, scan_align_result* out) {
   if (!ctx) return SCAN_E_INVALID_ARG;
   Ctx& c = ctx->c;
+  ++c.gen;
   if (!c.matched) { c.err = "scan_align before scan_analyze / scan_match_collectives"; return SCAN_E_ORDER; }
   if (c.n_shards > 1) { c.err = "scan_align on a sharded context is not supported"; return SCAN_E_UNSUPPORTED; }
   if (!c.d_start) { c.err = "scan_align needs start_ns at scan_load_events"; return SCAN_E_INVALID_ARG; }

@@ -174,6 +174,9 @@ struct Ctx {
   void* h_pin = nullptr;                 // pinned host scratch (exchange read-backs, table staging)
   size_t h_pin_cap = 0;
   cudaEvent_t ev_x1 = nullptr, ev_x2 = nullptr;
+  // JSON ingest / emit state (k_json.cu), owned; gen: bumped by every load / analysis / alignment
+  void* json_state = nullptr;
+  uint64_t gen = 0;
   // queued zero / byte fills, flushed as one k_fill launch before the next kernel (flush_fills)
   struct Fill { void* p; uint64_t n; uint32_t v; };
   std::vector<Fill> fills;
@@ -247,6 +250,7 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out);
 scan_status ensure_tiles(Ctx& c);
 void shard_release(Ctx& c);
 void stream_release(Ctx& c);
+void json_release(Ctx& c);
 
 }  // namespace ms
 

@@ -151,7 +151,9 @@ def schema_cases():
 
 SYNTAX = [b'{"traceEvents":[{"cat":"compute",}]}', b'[{"ts":01}]', b'[{"a":"\\x"}]', b'[{"a":"abc}]',
           b'[{}] x', b'', b'  ', b'[{"a":tru}]', b'[{"a":"\x01"}]', b'[NaN]', b'[{"a" 1}]', b'[{"a":1}',
-          b'[{"a":-}]', b'[{"a":1.}]', b'[{"a":[1,]}]', b'[{"ph":"X",}]']
+          b'[{"a":-}]', b'[{"a":1.}]', b'[{"a":[1,]}]', b'[{"ph":"X",}]', b'[5, 6x]', b'[5,]', b'[{"ph":"M"},]',
+          b'[{"ph":"M"} {"ph":"M"}]', b'[{"ph":"M"},[1,]]', b'{"traceEvents":[]', b'{"traceEvents":[]}}',
+          rb'[{"a\q":1}]', rb'[{"a":"\u12G4"}]', b'[{"a":{"b" 1}}]', b'[{"a":{"b":1,}}]', b'[]]']
 
 
 @pytest.mark.parametrize("i", range(len(SCHEMA) + 4))
@@ -192,3 +194,11 @@ def test_empty_input():
     t, skipped = cj.parse([], 2, 1, 1)
     assert t.n_events == 0 and skipped == 0 and t.rank_offsets.tolist() == [0, 0, 0]
     assert cj.emit(t, np.zeros(0, np.uint32)) == b'{"traceEvents":[\n]}\n'
+
+
+def test_fast_writer_is_the_clean_writer():
+    tr = tg.generate(configs.c2(seed=2, iterations=1))
+    b, off = chrome.rank_documents_fast(tr)
+    docs = chrome.rank_documents(tr, messy=False)
+    assert b == b"".join(docs)
+    assert [int(x) for x in np.diff(off)] == [len(d) for d in docs]

@@ -43,6 +43,8 @@
 #include <thread>
 #include <atomic>
 #include <algorithm>
+#include <cstdio>
+#include <string>
 
 extern "C" {
 
@@ -561,6 +563,79 @@ int gen_fill(const gen_config_c* g, const uint64_t* rank_offsets, int64_t* start
   for (int i = 0; i < nth; ++i) th.emplace_back(fixer);
   for (auto& x : th) x.join();
   return 0;
+}
+
+
+// Per-rank Chrome-trace JSON documents of given event columns (the clean form of
+// tracegen/chrome.py rank_documents(messy=False), byte for byte). Pass 1 (out == NULL): fills
+// doc_off[W+1] and returns the total size; pass 2: writes the documents. Test infrastructure.
+static void chrome_rank(std::string& o, uint32_t r, const uint64_t* ro, const int64_t* start, const uint32_t* dur,
+                        const uint16_t* kind_op, const uint16_t* meta, const uint32_t* comm, const uint32_t* payload,
+                        const uint64_t* coff, const uint32_t* cmem) {
+  static const char* names[7] = {"compute", "all_reduce", "all_gather", "reduce_scatter", "broadcast", "send", "recv"};
+  char tmp[64];
+  auto us = [&](int64_t ns) {
+    const bool neg = ns < 0;
+    const uint64_t a = neg ? 0ull - (uint64_t)ns : (uint64_t)ns;
+    if (a % 1000 == 0) snprintf(tmp, sizeof tmp, "%s%llu", neg ? "-" : "", (unsigned long long)(a / 1000));
+    else snprintf(tmp, sizeof tmp, "%s%llu.%03llu", neg ? "-" : "", (unsigned long long)(a / 1000), (unsigned long long)(a % 1000));
+    o += tmp;
+  };
+  auto num = [&](uint64_t v) { snprintf(tmp, sizeof tmp, "%llu", (unsigned long long)v); o += tmp; };
+  o += "{\"traceEvents\":[";
+  for (uint64_t i = ro[r]; i < ro[r + 1]; ++i) {
+    if (i > ro[r]) o += ',';
+    const uint32_t ko = kind_op[i], m = meta[i], kind = ko & 7u, iend = (ko >> 3) & 1u, op = ko >> 4;
+    o += "{\"name\":\""; o += names[kind]; o += "\",\"cat\":\""; o += names[kind]; o += "\",\"ph\":\"X\",\"ts\":";
+    us(start[i]);
+    o += ",\"dur\":"; us((int64_t)dur[i]);
+    o += ",\"pid\":"; num(r);
+    o += kind == 0 ? ",\"tid\":0,\"args\":{" : ",\"tid\":1,\"args\":{";
+    bool first = true;
+    auto key = [&](const char* k) { if (!first) o += ','; first = false; o += '"'; o += k; o += "\":"; };
+    if (op) { key("op"); num(op); }
+    if (iend) { key("iter_end"); num(iend); }
+    if (m & 1023u) { key("mb"); num(m & 1023u); }
+    if ((m >> 10) & 7u) { key("chunk"); num((m >> 10) & 7u); }
+    if ((m >> 13) & 1u) { key("bwd"); num(1); }
+    if ((m >> 14) & 1u) { key("warmup"); num(1); }
+    if (kind >= 1 && kind <= 4) {
+      key("group");
+      o += '[';
+      for (uint64_t q = coff[comm[i]]; q < coff[comm[i] + 1]; ++q) { if (q > coff[comm[i]]) o += ','; num(cmem[q]); }
+      o += ']';
+    } else if (kind >= 5) {
+      key("peer"); num(comm[i]);
+    }
+    if (payload[i]) { key("bytes"); num(payload[i]); }
+    o += "}}";
+  }
+  o += "]}";
+}
+
+int64_t gen_chrome(uint32_t W, const uint64_t* ro, const int64_t* start, const uint32_t* dur, const uint16_t* kind_op,
+                   const uint16_t* meta, const uint32_t* comm, const uint32_t* payload, const uint64_t* coff,
+                   const uint32_t* cmem, uint8_t* out, uint64_t* doc_off, int n_threads) {
+  if (n_threads <= 0) n_threads = (int)std::max(1u, std::thread::hardware_concurrency());
+  n_threads = (int)std::min<uint32_t>((uint32_t)n_threads, std::max<uint32_t>(W, 1));
+  std::vector<uint64_t> sz(W, 0);
+  std::vector<std::thread> th;
+  for (int t = 0; t < n_threads; ++t)
+    th.emplace_back([&, t] {
+      std::string o;
+      for (uint32_t r = t; r < W; r += n_threads) {
+        o.clear();
+        chrome_rank(o, r, ro, start, dur, kind_op, meta, comm, payload, coff, cmem);
+        sz[r] = o.size();
+        if (out) memcpy(out + doc_off[r], o.data(), o.size());
+      }
+    });
+  for (auto& x : th) x.join();
+  if (!out) {
+    doc_off[0] = 0;
+    for (uint32_t r = 0; r < W; ++r) doc_off[r + 1] = doc_off[r] + sz[r];
+  }
+  return (int64_t)doc_off[W];
 }
 
 }  // extern "C"
