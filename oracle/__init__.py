@@ -13,6 +13,8 @@ Parity status per function (DESIGN.md §Oracle pins):
   A6 stage 3 .......... pinned (SPEC arithmetic example, injected degraded link)
   A7-A8 walk .......... parity unpinned by the paper (definition is ours, reading R17);
                         pinned by hand-built chains and cycles only.
+  NEXT-4 blame ........ parity unpinned by the paper (definition is ours, readings EB1-EB6);
+                        pinned by hand-built chains / a cycle, wait conservation, DES throttles.
 """
 from __future__ import annotations
 
@@ -107,6 +109,8 @@ def _load():
         lib.orc_run_align.restype = ctypes.c_void_p
         lib.orc_run_align.argtypes = [ctypes.POINTER(_Input), ctypes.POINTER(_Config), ctypes.c_void_p, ctypes.c_int32,
                                       ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
+        lib.orc_run_blame.restype = ctypes.c_void_p
+        lib.orc_run_blame.argtypes = [ctypes.POINTER(_Input), ctypes.POINTER(_Config), ctypes.POINTER(ctypes.c_int32)]
         lib.orc_array.restype = ctypes.c_int
         lib.orc_array.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p),
                                   ctypes.POINTER(ctypes.c_uint64)]
@@ -131,7 +135,19 @@ def align(trace, reference: int = 0, cfg: Config | None = None) -> dict:
     return run(trace, cfg, _align=(start, int(reference)))
 
 
-def run(trace, cfg: Config | None = None, _align=None) -> dict:
+_BL_ARRAYS = {"bl_root": np.uint64, "bl_inflicted": np.uint64, "bl_self": np.uint64, "bl_unattributed": np.uint64,
+              "bl_suffered": np.uint64}
+
+
+def blame(trace, cfg: Config | None = None) -> dict:
+    """run() plus the NEXT-4 event-level blame (oracle.cpp ``blame``; DESIGN.md §10e EB1-EB6).
+    Adds bl_root (u64 per event: root event of a waiting event; 2^64-1 not waiting, 2^64-2 on a
+    cycle), per-rank bl_inflicted / bl_self / bl_unattributed / bl_suffered (ns) and the counts
+    bl_n_waiting / bl_n_cyclic."""
+    return run(trace, cfg, _blame=True)
+
+
+def run(trace, cfg: Config | None = None, _align=None, _blame: bool = False) -> dict:
     """Analyse ``trace`` (a tracegen.Trace or any object with the same columns). Returns a dict of
     numpy arrays (keys of ``_ARRAYS``) plus the scalar counters."""
     cfg = cfg or Config()
@@ -147,7 +163,9 @@ def run(trace, cfg: Config | None = None, _align=None) -> dict:
                 cfg.window_iters, cfg.stage2_classes, cfg.stage2_mode, 0)
     st = ctypes.c_int32(0)
     ast = ctypes.c_int32(0)
-    if _align is None:
+    if _blame:
+        h = lib.orc_run_blame(ctypes.byref(inp), ctypes.byref(c), ctypes.byref(st))
+    elif _align is None:
         h = lib.orc_run(ctypes.byref(inp), ctypes.byref(c), ctypes.byref(st))
     else:
         keep.append(_align[0])
@@ -171,7 +189,17 @@ def run(trace, cfg: Config | None = None, _align=None) -> dict:
                 n = nb.value // np.dtype(dt).itemsize
                 out[name] = np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_uint8)), shape=(nb.value,)).view(dt)[:n].copy() if n else np.zeros(0, dt)
             out["al_status"] = int(ast.value)
+        if _blame and st.value >= 0:
+            for name, dt in _BL_ARRAYS.items():
+                p = ctypes.c_void_p()
+                nb = ctypes.c_uint64()
+                if lib.orc_array(h, name.encode(), ctypes.byref(p), ctypes.byref(nb)) != 0:
+                    raise KeyError(name)
+                n = nb.value // np.dtype(dt).itemsize
+                out[name] = np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_uint8)), shape=(nb.value,)).view(dt)[:n].copy() if n else np.zeros(0, dt)
         sc = out.pop("scalars")
+        if _blame and st.value >= 0:
+            out["bl_n_waiting"], out["bl_n_cyclic"] = int(sc[len(_SCALARS)]), int(sc[len(_SCALARS) + 1])
         for i, k in enumerate(_SCALARS):
             out[k] = int(np.int64(sc[i])) if k == "status" else int(sc[i])
         return out

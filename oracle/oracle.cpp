@@ -56,6 +56,8 @@ struct Result {
   // NEXT-1 timeline alignment (orc_run_align)
   std::vector<int64_t> al_start; std::vector<int32_t> al_level; std::vector<uint32_t> al_nanchor;
   std::vector<uint64_t> al_residual;
+  std::vector<uint64_t> bl_root, bl_inflicted, bl_self, bl_unattributed, bl_suffered;
+  uint64_t bl_n_waiting = 0, bl_n_cyclic = 0;
   int32_t al_status = 0;
 };
 
@@ -614,6 +616,58 @@ struct Oracle {
     return 0;
   }
 
+  // NEXT-4 event-level blame (readings EB1-EB6; "ranks that merely
+  // suffer collateral slowdown will only lag because they are waiting for the faulty peer"):
+  // every waiting communication event is traced back through the happens-before structure to the
+  // event where its delay began.
+  void blame() {
+    const uint64_t N = in.n_events;
+    const uint64_t NONE = ~0ull, CYCLE = ~0ull - 1;
+    std::vector<int> rank(N);
+    for (int r = 0; r < W; ++r)
+      for (uint64_t e = in.rank_offsets[r]; e < in.rank_offsets[r + 1]; ++e) rank[e] = r;
+    // member event of every (instance, rank)
+    std::map<std::pair<uint32_t, int>, uint64_t> mev;
+    for (uint64_t e = 0; e < N; ++e)
+      if (kind(e) != KIND_COMPUTE) mev[{R.ev_inst[e], rank[e]}] = e;
+    // EB1: a waiting event is a communication event of a VALID instance with wait > 0
+    auto waiting = [&](uint64_t e) {
+      return kind(e) != KIND_COMPUTE && (R.in_flags[R.ev_inst[e]] & F_VALID) && R.ev_wait[e] > 0;
+    };
+    // EB2 / EB3: the pointer of every event
+    std::vector<uint64_t> ptr(N);
+    for (uint64_t e = 0; e < N; ++e) {
+      const bool first = e == in.rank_offsets[rank[e]];
+      if (kind(e) == KIND_COMPUTE) ptr[e] = e;                       // a compute event is a root
+      else if (waiting(e)) {                                         // delayed by the last arriver's
+        const uint32_t id = R.ev_inst[e];                            // previous event
+        const uint64_t le = mev.at({id, (int)R.in_last[id]});
+        ptr[e] = le == in.rank_offsets[rank[le]] ? le : le - 1;
+      } else ptr[e] = first ? e : e - 1;                             // its own rank's previous event
+    }
+    // EB4: follow the pointers to a fixed point; revisiting an event is a cycle
+    R.bl_root.assign(N, NONE);
+    R.bl_inflicted.assign(W, 0); R.bl_self.assign(W, 0); R.bl_unattributed.assign(W, 0); R.bl_suffered.assign(W, 0);
+    for (uint64_t e = 0; e < N; ++e) {
+      if (!waiting(e)) continue;
+      ++R.bl_n_waiting;
+      std::set<uint64_t> seen;
+      uint64_t x = e;
+      while (ptr[x] != x) {
+        if (!seen.insert(x).second) { x = CYCLE; break; }
+        x = ptr[x];
+      }
+      R.bl_root[e] = x;
+      // EB5: the wait is blamed on the root's rank
+      const int r = rank[e];
+      const uint64_t w = R.ev_wait[e];
+      R.bl_suffered[r] += w;
+      if (x == CYCLE) { R.bl_unattributed[r] += w; ++R.bl_n_cyclic; }
+      else if (rank[x] == r) R.bl_self[r] += w;
+      else R.bl_inflicted[rank[x]] += w;
+    }
+  }
+
   // stage-2 class of a communicator from the topology (reading R12): 1 = TP group, 2 = DP group
   uint8_t comm_class(const std::vector<uint32_t>& m) const {
     if (TP >= 2 && (int)m.size() == TP) {
@@ -667,6 +721,17 @@ void* orc_run_align(const orc_input* in, const orc_config* cfg, const int64_t* s
   return R;
 }
 
+// run() then the event-level blame (NEXT-4) on its instances
+void* orc_run_blame(const orc_input* in, const orc_config* cfg, int32_t* status) {
+  Result* R = static_cast<Result*>(orc_run(in, cfg, status));
+  if (*status < 0) return R;
+  Oracle o(*in, *cfg, *R);
+  o.blame();
+  R->scalars.push_back(R->bl_n_waiting);
+  R->scalars.push_back(R->bl_n_cyclic);
+  return R;
+}
+
 void orc_free(void* h) { delete (Result*)h; }
 
 // Named result arrays; returns 0 if found.
@@ -687,6 +752,7 @@ int orc_array(void* h, const char* name, void** ptr, uint64_t* nbytes) {
   X(lb_label) X(lb_root_kind) X(lb_root_rank) X(lb_root_src) X(lb_depth) X(lb_total_wait)
   X(eg_window) X(eg_src) X(eg_dst) X(eg_weight)
   X(al_start) X(al_level) X(al_nanchor) X(al_residual)
+  X(bl_root) X(bl_inflicted) X(bl_self) X(bl_unattributed) X(bl_suffered)
 #undef X
   return -1;
 }
