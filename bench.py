@@ -313,6 +313,7 @@ def main():
     ap.add_argument("--no-align", action="store_true", help="skip the timeline-alignment measurement (N=1 only)")
     ap.add_argument("--no-stream", action="store_true", help="skip the C5 sliding-window measurement (N=1 only)")
     ap.add_argument("--no-json", action="store_true", help="skip the JSON ingest / emit measurement (N=1 only)")
+    ap.add_argument("--no-blame", action="store_true", help="skip the event-level blame measurement (N=1 only)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -455,6 +456,41 @@ def main():
         }
         del dev["start_ns"]
 
+    # ---- NEXT-4 event-level blame (scan_blame) on the same resident trace, N=1 only ----
+    blame = None
+    if world == 1 and not args.no_blame:
+        s.analyze()
+        for _ in range(max(1, args.warmup)):
+            res_bl = s.blame()
+        torch.cuda.synchronize()
+        s.set_timing(True)
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for _ in range(args.steps):
+            res_bl = s.blame()
+        b1.record(stream)
+        torch.cuda.synchronize()
+        bkern = s.kernel_timing()
+        s.set_timing(False)
+        bms = b0.elapsed_time(b1) / args.steps
+        bl_k = {k: v for k, v in bkern.items() if k.startswith("k_bl_")}
+        jump = bl_k.get("k_bl_jump")
+        pk_b = float((json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}).get("hbm_gbs", 6650.0))
+        jump_ms = jump[0] / max(jump[1], 1) if jump else None
+        blame = {
+            "metric": "trace events blamed/sec (scan_blame: root event of every wait, per-rank blame)",
+            "value": N / (bms / 1e3), "unit": "events/s", "ms_per_call": bms,
+            "result": {k: int(v) for k, v in res_bl.items()},
+            "kernels": {k: {"ms_per_call": round(v[0] / args.steps, 4), "launches": v[1]}
+                        for k, v in sorted(bl_k.items(), key=lambda kv: -kv[1][0])},
+            "roofline": ({"bound": "hbm", "kernel": "k_bl_jump", "bytes_per_event": 12,
+                          "achieved": 12 * N / (jump_ms / 1e3) / 1e9, "peak": pk_b, "unit": "GB/s",
+                          "frac": 12 * N / (jump_ms / 1e3) / 1e9 / pk_b,
+                          "note": "per round: pointer read 4 B + gathered pointer 4 B + write 4 B per event"}
+                         if jump_ms else None),
+        }
+
     streaming = streaming_c5(ms, torch, local, stream) if (world == 1 and not args.no_stream) else None
     json_ingest = json_io(ms, torch, local, stream, args.steps, args.warmup, not args.no_cpu) if (
         world == 1 and not args.no_json) else None
@@ -518,6 +554,7 @@ def main():
         "alignment": alignment,
         "streaming_c5": streaming,
         "json_ingest": json_ingest,
+        "blame": blame,
         "path": "fused SPMD stage-tile pass (K9)" if fused else "general path",
     }
     print(json.dumps(line), flush=True)

@@ -230,6 +230,25 @@ uint64_t    scan_stream_window(const scan_ctx* ctx);
 scan_status scan_create_sharded(scan_ctx** out, int cuda_device, void* cuda_stream, int n_shards, int shard,
                                 const uint8_t nccl_unique_id[128]);
 
+/* ---- NEXT-4: event-level blame (DESIGN.md §10e EB1-EB6) ----
+   For every waiting communication event (an event of a VALID instance with wait > 0), the event
+   where its delay began: it waited for the instance's last arriver, whose previous event in program
+   order delayed it (EB2); a communication event that did not wait was itself delayed by its own
+   previous event (EB3); compute events and the first event of a rank are roots. The pointers are
+   followed to a root by pointer jumping on the device; a chain that never reaches a root (a pointer
+   cycle, possible only in inconsistent traces) is unattributed (EB4). Each wait is blamed on the
+   root's rank (EB5): BL_INFLICTED (on other ranks), BL_SELF, BL_UNATTRIBUTED, BL_SUFFERED; the
+   whole loaded trace is one window (EB6). Requires a completed analysis (scan_analyze or
+   scan_localize). Errors: SCAN_E_ORDER, SCAN_E_UNSUPPORTED (stream / sharded context, >= 2^32-16
+   events), SCAN_E_OOM, SCAN_E_CUDA.                                                              */
+typedef struct scan_blame_result {
+    uint64_t n_waiting, n_cyclic;   /* waiting events; of them on a pointer cycle                     */
+    uint64_t total_wait_ns;         /* sum of their waits                                             */
+    uint32_t rounds;                /* pointer-jumping rounds                                         */
+    uint32_t top_rank;              /* rank with the largest BL_INFLICTED (UINT32_MAX if none)        */
+} scan_blame_result;
+scan_status scan_blame(scan_ctx* ctx, scan_blame_result* out);
+
 /* ---- NEXT-2: Chrome-trace JSON ingest and merged emit (DESIGN.md §10d J1-J12) -----
    scan_ingest_json parses, ON THE DEVICE, one or more JSON documents: the per-rank files the
    tracer writes ("every rank has its own recorded event sequence as a JSON file") or a
@@ -377,6 +396,13 @@ typedef enum scan_output {
     SCAN_OUT_AL_LEVEL,         /* i32 per rank: BFS level from the reference, -1 = not reached     */
     SCAN_OUT_AL_NANCHOR,       /* u32 per rank: anchors of its clock map                           */
     SCAN_OUT_AL_RESIDUAL,      /* u64 per rank: max (instance aligned end - own aligned end), ns   */
+    /* event-level blame (scan_blame) */
+    SCAN_OUT_BL_ROOT,          /* u64 per event: root event of a waiting event; 2^64-1 = not waiting,
+                                  2^64-2 = on a pointer cycle (unattributed)                          */
+    SCAN_OUT_BL_INFLICTED,     /* u64 per rank: wait (ns) of OTHER ranks' events rooted on this rank   */
+    SCAN_OUT_BL_SELF,          /* u64 per rank: wait of its own events rooted on itself                */
+    SCAN_OUT_BL_UNATTRIBUTED,  /* u64 per rank: wait of its own events on a pointer cycle              */
+    SCAN_OUT_BL_SUFFERED,      /* u64 per rank: all wait of its waiting events                         */
     SCAN_OUT__COUNT
 } scan_output;
 

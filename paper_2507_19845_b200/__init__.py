@@ -45,9 +45,12 @@ OUTPUTS = [
     ("comm_inst", np.uint32), ("comm_wait", np.uint32), ("slow_bits", np.uint32),
     ("ch_shard_k0", np.uint64), ("ch_shard_n", np.uint32),
     ("al_start", np.int64), ("al_level", np.int32), ("al_nanchor", np.uint32), ("al_residual", np.uint64),
+    ("bl_root", np.uint64), ("bl_inflicted", np.uint64), ("bl_self", np.uint64), ("bl_unattributed", np.uint64),
+    ("bl_suffered", np.uint64),
 ]
 ALIGN_OUTPUTS = ("al_start", "al_level", "al_nanchor", "al_residual")
-NATIVE_ONLY = ("comm_inst", "comm_wait", "slow_bits", "ch_shard_k0", "ch_shard_n") + ALIGN_OUTPUTS
+BLAME_OUTPUTS = ("bl_root", "bl_inflicted", "bl_self", "bl_unattributed", "bl_suffered")
+NATIVE_ONLY = ("comm_inst", "comm_wait", "slow_bits", "ch_shard_k0", "ch_shard_n") + ALIGN_OUTPUTS + BLAME_OUTPUTS
 OUT_INDEX = {n: i for i, (n, _) in enumerate(OUTPUTS)}
 OUT_DTYPE = dict(OUTPUTS)
 
@@ -79,6 +82,11 @@ class JsonTraceError(RuntimeError):
     def __init__(self, status: int, msg: str, kind: int, field: int, offset: int):
         super().__init__(f"{_STATUS.get(status, status)}: {msg}")
         self.status, self.kind, self.field, self.offset = status, kind, field, offset
+
+
+class _BlameRes(ctypes.Structure):
+    _fields_ = [("n_waiting", ctypes.c_uint64), ("n_cyclic", ctypes.c_uint64), ("total_wait_ns", ctypes.c_uint64),
+                ("rounds", ctypes.c_uint32), ("top_rank", ctypes.c_uint32)]
 
 
 class _AlignCfg(ctypes.Structure):
@@ -176,6 +184,7 @@ def _load_lib():
     lib.scan_stream_window.argtypes = [P]
     lib.scan_stream_window.restype = ctypes.c_uint64
     lib.scan_create_sharded.argtypes = [ctypes.POINTER(P), ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P]
+    lib.scan_blame.argtypes = [P, ctypes.POINTER(_BlameRes)]
     lib.scan_ingest_json.argtypes = [P, ctypes.POINTER(_Topo), P, ctypes.c_uint64, P, ctypes.c_uint32, ctypes.c_uint32,
                                      ctypes.POINTER(_JsonRes)]
     lib.scan_loaded_column.argtypes = [P, ctypes.c_int, P, ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]
@@ -183,7 +192,7 @@ def _load_lib():
     for f in ("scan_create", "scan_load_events", "scan_match_collectives", "scan_detect", "scan_localize",
               "scan_output_size", "scan_export", "scan_analyze", "scan_force_general", "scan_fused_variant",
               "scan_nccl_unique_id", "scan_create_sharded", "scan_align", "scan_stream_open", "scan_stream_push",
-              "scan_ingest_json", "scan_loaded_column", "scan_emit_chrome"):
+              "scan_ingest_json", "scan_loaded_column", "scan_emit_chrome", "scan_blame"):
         getattr(lib, f).restype = ctypes.c_int32
     _lib = lib
     return lib
@@ -194,7 +203,8 @@ EXPORTED_SYMBOLS = ["scan_create", "scan_destroy", "scan_last_error", "scan_load
                     "scan_kernel_launches", "scan_set_timing", "scan_timing_reset", "scan_kernel_timing",
                     "scan_analyze", "scan_used_fused", "scan_force_general", "scan_fused_variant",
                     "scan_nccl_unique_id", "scan_create_sharded", "scan_align", "scan_stream_open", "scan_stream_push",
-                    "scan_stream_window", "scan_ingest_json", "scan_loaded_column", "scan_emit_chrome"]
+                    "scan_stream_window", "scan_ingest_json", "scan_loaded_column", "scan_emit_chrome",
+                    "scan_blame"]
 
 
 @dataclass
@@ -343,6 +353,13 @@ def scan_emit_chrome(ctx, aligned: bool = False, dst=None) -> bytes | int:
     return out.tobytes()
 
 
+def scan_blame(ctx) -> dict:
+    """NEXT-4 event-level blame (scan.h): needs a completed analysis."""
+    r = _BlameRes()
+    _check(ctx, _load_lib().scan_blame(ctx, ctypes.byref(r)))
+    return {n: getattr(r, n) for n, _ in r._fields_}
+
+
 def scan_match_collectives(ctx) -> tuple[int, dict]:
     r = _MatchRes()
     st = _check(ctx, _load_lib().scan_match_collectives(ctx, ctypes.byref(r)))
@@ -473,6 +490,10 @@ class Scan:
     def align(self, reference: int = 0) -> dict:
         """Timeline alignment onto ``reference``'s clock (load with ``start=True`` first)."""
         return scan_align(self.ctx, reference)
+
+    def blame(self) -> dict:
+        """Event-level blame of every wait (after ``analyze``); outputs ``BLAME_OUTPUTS``."""
+        return scan_blame(self.ctx)
 
     # ---- NEXT-2 Chrome-trace JSON ingest / emit (scan.h)
     def ingest_json(self, docs, tp: int, pp: int, dp: int, device: bool = False) -> dict:

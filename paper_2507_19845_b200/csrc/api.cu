@@ -105,7 +105,7 @@ static void release_all(Ctx& c) {
                     &c.ft_base, &c.ft_last, &c.st_tot, &c.sci, &c.sit, &c.dlate, &c.dinfo, &c.ft_posA, &c.ft_posB,
                     &c.ft_posK, &c.eidx, &c.tile_stage, &c.xbase, &c.lk_scratch, &c.g_base, &c.g_slot,
                     &c.g_nmax, &c.g_nmin, &c.g_k0, &c.p2p_eslot, &c.xe_off, &c.xe_col, &c.xbig, &c.own_start, &c.al_tend, &c.al_aend, &c.al_anct,
-                    &c.al_anco, &c.al_slotci, &c.al_level, &c.al_nanc, &c.al_resid, &c.al_flag, &c.al_start, &c.al_ranks, &c.al_cch, &c.al_tgt, &c.x_send, &c.x_recv, &c.x_recv2, &c.x_ep, &c.x_stage, &c.headtail, &c.lk_sendmap, &c.lk_recvmap};
+                    &c.al_anco, &c.al_slotci, &c.al_level, &c.al_nanc, &c.al_resid, &c.al_flag, &c.al_start, &c.al_ranks, &c.al_cch, &c.al_tgt, &c.x_send, &c.x_recv, &c.x_recv2, &c.x_ep, &c.x_stage, &c.headtail, &c.lk_sendmap, &c.lk_recvmap, &c.bl_inst, &c.bl_wait, &c.bl_p0, &c.bl_pa, &c.bl_pb, &c.bl_root, &c.bl_last, &c.bl_rank, &c.bl_rk};
   for (DevBuf* b : bufs) b->release();
 }
 
@@ -161,7 +161,7 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
   CK(cudaSetDevice(c.device));
   c.loaded = c.matched = c.detected = c.localized = false;
   c.fused_used = false; c.tiles_ready = false; c.xwait_pending = false; c.aligned = false;
-  ++c.gen;
+  ++c.gen; c.blamed = false;
   if (c.stream_mode) { stream_release(c); c.stream_mode = false; }
   c.d_start = nullptr;
   c.err.clear();
@@ -706,7 +706,7 @@ extern "C" {
 scan_status scan_match_collectives(scan_ctx* ctx, scan_match_result* out) {
   if (!ctx) return SCAN_E_INVALID_ARG;
   Ctx& c = ctx->c;
-  ++c.gen;
+  ++c.gen; c.blamed = false;
   if (!c.loaded) { c.err = "scan_match_collectives before scan_load_events"; return SCAN_E_ORDER; }
   if (c.n_shards > 1) { c.err = "a sharded context runs scan_analyze only"; return SCAN_E_UNSUPPORTED; }
   CK(cudaSetDevice(c.device));
@@ -721,7 +721,7 @@ scan_status scan_match_collectives(scan_ctx* ctx, scan_match_result* out) {
 scan_status scan_detect(scan_ctx* ctx, const scan_detect_config* cfg, scan_detect_result* out) {
   if (!ctx) return SCAN_E_INVALID_ARG;
   Ctx& c = ctx->c;
-  ++c.gen;
+  ++c.gen; c.blamed = false;
   if (!c.matched) { c.err = "scan_detect before scan_match_collectives"; return SCAN_E_ORDER; }
   CK(cudaSetDevice(c.device));
   scan_detect_config d = cfg ? *cfg : kDefDetect;
@@ -737,7 +737,7 @@ scan_status scan_detect(scan_ctx* ctx, const scan_detect_config* cfg, scan_detec
 scan_status scan_localize(scan_ctx* ctx, const scan_localize_config* cfg, scan_localize_result* out) {
   if (!ctx) return SCAN_E_INVALID_ARG;
   Ctx& c = ctx->c;
-  ++c.gen;
+  ++c.gen; c.blamed = false;
   if (!c.detected || c.fused_used) { c.err = "scan_localize before scan_detect"; return SCAN_E_ORDER; }
   CK(cudaSetDevice(c.device));
   scan_localize_config L = cfg ? *cfg : kDefLocalize;
@@ -754,7 +754,7 @@ scan_status scan_analyze(scan_ctx* ctx, const scan_detect_config* dcfg, const sc
                          scan_match_result* mres, scan_detect_result* dres, scan_localize_result* lres) {
   if (!ctx) return SCAN_E_INVALID_ARG;
   Ctx& c = ctx->c;
-  ++c.gen;
+  ++c.gen; c.blamed = false;
   if (!c.loaded) { c.err = "scan_analyze before scan_load_events"; return SCAN_E_ORDER; }
   CK(cudaSetDevice(c.device));
   scan_detect_config d = dcfg ? *dcfg : kDefDetect;
@@ -964,6 +964,11 @@ bool direct(Ctx& c, scan_output which, OutDesc& d) {
     case SCAN_OUT_AL_LEVEL: d = {&c.al_level, 0, c.aligned ? W * 4 : 0, 1}; return true;
     case SCAN_OUT_AL_NANCHOR: d = {&c.al_nanc, 0, c.aligned ? W * 4 : 0, 1}; return true;
     case SCAN_OUT_AL_RESIDUAL: d = {&c.al_resid, 0, c.aligned ? W * 8 : 0, 1}; return true;
+    case SCAN_OUT_BL_ROOT: d = {&c.bl_root, 0, c.blamed ? c.N * 8 : 0, 3}; return true;
+    case SCAN_OUT_BL_INFLICTED: d = {&c.bl_rank, 0, c.blamed ? W * 8 : 0, 3}; return true;
+    case SCAN_OUT_BL_SELF: d = {&c.bl_rank, W * 8, c.blamed ? W * 8 : 0, 3}; return true;
+    case SCAN_OUT_BL_UNATTRIBUTED: d = {&c.bl_rank, 2 * W * 8, c.blamed ? W * 8 : 0, 3}; return true;
+    case SCAN_OUT_BL_SUFFERED: d = {&c.bl_rank, 3 * W * 8, c.blamed ? W * 8 : 0, 3}; return true;
     default: return false;
   }
 }
@@ -1014,6 +1019,7 @@ scan_status scan_export(scan_ctx* ctx, scan_output which, void* dst, uint64_t ds
     return SCAN_E_UNSUPPORTED;
   }
   if (which >= SCAN_OUT_AL_START && which <= SCAN_OUT_AL_RESIDUAL && !c.aligned) { c.err = "scan_align not run"; return SCAN_E_ORDER; }
+  if (which >= SCAN_OUT_BL_ROOT && which <= SCAN_OUT_BL_SUFFERED && !c.blamed) { c.err = "scan_blame not run"; return SCAN_E_ORDER; }
   if ((which == SCAN_OUT_COMM_WAIT || which == SCAN_OUT_EV_WAIT) && c.xwait_pending && c.localized) {
     launch_xwait_scatter(c);  // comm-order view of the cross-stage waits (once per analysis)
     CK(cudaStreamSynchronize(c.stream));

@@ -174,6 +174,9 @@ struct Ctx {
   void* h_pin = nullptr;                 // pinned host scratch (exchange read-backs, table staging)
   size_t h_pin_cap = 0;
   cudaEvent_t ev_x1 = nullptr, ev_x2 = nullptr;
+  // event-level blame (k_blame.cu)
+  bool blamed = false;
+  DevBuf bl_inst, bl_wait, bl_p0, bl_pa, bl_pb, bl_root, bl_last, bl_rank, bl_rk;
   // JSON ingest / emit state (k_json.cu), owned; gen: bumped by every load / analysis / alignment
   void* json_state = nullptr;
   uint64_t gen = 0;
@@ -251,6 +254,7 @@ scan_status ensure_tiles(Ctx& c);
 void shard_release(Ctx& c);
 void stream_release(Ctx& c);
 void json_release(Ctx& c);
+scan_status blame_all(Ctx& c, scan_blame_result* out);
 
 }  // namespace ms
 

@@ -1,0 +1,236 @@
+// k_blame.cu — NEXT-4: event-level blame by pointer jumping (readings EB1-EB6).
+//
+// The paper's insight: ranks that suffer collateral slowdown "only lag because they are
+// waiting for the faulty peer". Every waiting communication event (valid instance, wait > 0) points
+// at the event that delayed the instance's last arriver (that rank's previous event); a communication
+// event that did not wait points at its own rank's previous event; compute events and the first
+// event of a rank are roots. Following the pointers gives, for every wait, the event where the delay
+// began; pointer jumping (ptr <- ptr[ptr]) resolves all chains in log2(longest chain) rounds.
+//   k_bl_last   per instance: the member event of its last arriver          (tile warps)
+//   k_bl_ptr    per event: the pointer (u32 event index)                      (tile warps)
+//   k_bl_jump   one jumping round, double-buffered, with a change flag
+//   k_bl_sum    terminal check (a fixed point of the ORIGINAL pointers; anything else is a cycle),
+//               per-event root, per-rank inflicted / self / unattributed / suffered wait
+#include "internal.cuh"
+
+namespace ms {
+namespace {
+
+constexpr unsigned long long BL_NONE = ~0ull, BL_CYCLE = ~0ull - 1;
+
+struct BA {
+  uint64_t n_tiles;
+  const uint32_t* tile_rank; const uint64_t* tile_start; const uint64_t* rank_off;
+  const uint16_t* kind; const uint32_t* inst; const uint32_t* wait; const uint4* rec;
+  uint32_t* last_ev; uint32_t* ptr0; uint16_t* rank16;
+};
+
+__device__ __forceinline__ bool waiting_ev(const BA& a, uint64_t x, uint16_t ko, uint4& rc) {
+  if ((ko & 7u) == 0) return false;
+  rc = a.rec[a.inst[x]];
+  return (rc.w & SCAN_F_VALID) && a.wait[x] > 0;
+}
+
+__global__ void __launch_bounds__(256) k_bl_last(BA a) {
+  const uint64_t tile = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (tile >= a.n_tiles) return;
+  const uint32_t r = a.tile_rank[tile];
+  const uint64_t s = a.tile_start[tile], e = min(s + (uint64_t)TILE_EV, a.rank_off[r + 1]);
+  for (uint64_t x = s + lane_id(); x < e; x += 32) {
+    if ((a.kind[x] & 7u) == 0) continue;
+    const uint32_t I = a.inst[x];
+    const uint4 rc = a.rec[I];
+    if ((rc.w & SCAN_F_VALID) && rc.z == r) a.last_ev[I] = (uint32_t)x;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bl_ptr(BA a) {
+  const uint64_t tile = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (tile >= a.n_tiles) return;
+  const uint32_t r = a.tile_rank[tile];
+  const uint64_t rs = a.rank_off[r];
+  const uint64_t s = a.tile_start[tile], e = min(s + (uint64_t)TILE_EV, a.rank_off[r + 1]);
+  for (uint64_t x = s + lane_id(); x < e; x += 32) {
+    const uint16_t ko = a.kind[x];
+    uint64_t p;
+    uint4 rc;
+    if ((ko & 7u) == 0) p = x;                                     // EB3: compute events are roots
+    else if (waiting_ev(a, x, ko, rc)) {                           // EB2: the last arriver's previous event
+      const uint64_t le = a.last_ev[a.inst[x]];
+      p = le == a.rank_off[rc.z] ? le : le - 1;
+    } else p = x == rs ? x : x - 1;                                // EB3: own previous event
+    a.ptr0[x] = (uint32_t)p;
+    a.rank16[x] = (uint16_t)r;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bl_jump(uint64_t N, const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                                                 unsigned int* changed) {
+  bool ch = false;
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < N; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = src[x];
+    const uint32_t q = src[p];
+    dst[x] = q;
+    ch |= q != p;
+  }
+  if (__any_sync(0xFFFFFFFFu, ch) && lane_id() == 0) atomicOr(changed, 1u);
+}
+
+struct SA {
+  BA b; uint32_t W; const uint32_t* ptr; unsigned long long* root;
+  unsigned long long* inflicted; unsigned long long* self_; unsigned long long* unattr; unsigned long long* suffered;
+  unsigned long long* counts;  // [0] waiting events, [1] on a cycle
+  int smem_hist;               // 1: inflicted wait accumulated in a shared-memory histogram over ranks
+};
+
+// Persistent over tiles (one warp per tile). Most waits of a job root on a few ranks, so the inflicted
+// wait goes through a block-local shared-memory histogram (one global atomic per block and rank);
+// same-address global atomics would serialise in L2.
+__global__ void __launch_bounds__(256) k_bl_sum(SA a) {
+  extern __shared__ unsigned long long sh_inf[];
+  if (a.smem_hist) {
+    for (uint32_t i = threadIdx.x; i < a.W; i += blockDim.x) sh_inf[i] = 0;
+    __syncthreads();
+  }
+  unsigned long long nw = 0, ncy = 0;
+  for (uint64_t tile = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5); tile < a.b.n_tiles; tile += (uint64_t)gridDim.x * 8) {
+    const uint32_t r = a.b.tile_rank[tile];
+    const uint64_t s = a.b.tile_start[tile], e = min(s + (uint64_t)TILE_EV, a.b.rank_off[r + 1]);
+    unsigned long long suf = 0, slf = 0, una = 0;
+    uint32_t run_r = 0xFFFFFFFFu;  // per-lane run of inflicted wait on one rank
+    unsigned long long run_w = 0;
+    for (uint64_t base = s; base < e; base += 32) {
+      const uint64_t x = base + lane_id();
+      if (x >= e) break;
+      const unsigned long long w = a.b.wait[x];  // EV_WAIT: 0 for compute events and invalid instances
+      unsigned long long root = BL_NONE;
+      if (w) {
+        const uint32_t p = a.ptr[x];
+        ++nw;
+        suf += w;
+        if (a.b.ptr0[p] == p) {  // a root of the original pointers
+          root = p;
+          const uint32_t rr = a.b.rank16[p];
+          if (rr == r) slf += w;
+          else {
+            if (rr != run_r) {
+              if (run_w) { if (a.smem_hist) atomicAdd(&sh_inf[run_r], run_w); else atomicAdd(&a.inflicted[run_r], run_w); }
+              run_r = rr; run_w = 0;
+            }
+            run_w += w;
+          }
+        } else {
+          root = BL_CYCLE;
+          una += w;
+          ++ncy;
+        }
+      }
+      a.root[x] = root;
+    }
+    if (run_w) { if (a.smem_hist) atomicAdd(&sh_inf[run_r], run_w); else atomicAdd(&a.inflicted[run_r], run_w); }
+    suf = warp_sum_u64(suf); slf = warp_sum_u64(slf); una = warp_sum_u64(una);
+    if (lane_id() == 0) {
+      if (suf) atomicAdd(&a.suffered[r], suf);
+      if (slf) atomicAdd(&a.self_[r], slf);
+      if (una) atomicAdd(&a.unattr[r], una);
+    }
+  }
+  nw = warp_sum_u64(nw); ncy = warp_sum_u64(ncy);
+  if (lane_id() == 0) {
+    if (nw) atomicAdd(&a.counts[0], nw);
+    if (ncy) atomicAdd(&a.counts[1], ncy);
+  }
+  if (a.smem_hist) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < a.W; i += blockDim.x)
+      if (sh_inf[i]) atomicAdd(&a.inflicted[i], sh_inf[i]);
+  }
+}
+
+inline unsigned nbk(uint64_t n, unsigned t) { return (unsigned)std::max<uint64_t>(1, (n + t - 1) / t); }
+
+}  // namespace
+
+scan_status blame_all(Ctx& c, scan_blame_result* out) {
+  const uint64_t N = c.N, W = c.W;
+  if (N >= 0xFFFFFFF0ull) { c.err = "event-level blame supports < 2^32 - 16 events"; return SCAN_E_UNSUPPORTED; }
+  scan_status st = ensure_tiles(c);
+  if (st) return st;
+  if (c.xwait_pending) {  // comm-order view of the cross-stage waits
+    launch_xwait_scatter(c);
+    c.xwait_pending = false;
+  }
+  const uint64_t N1 = std::max<uint64_t>(N, 1);
+  CK(c.bl_inst.ensure(N1 * 4)); CK(c.bl_wait.ensure(N1 * 4)); CK(c.bl_p0.ensure(N1 * 4)); CK(c.bl_pa.ensure(N1 * 4));
+  CK(c.bl_pb.ensure(N1 * 4)); CK(c.bl_root.ensure(N1 * 8)); CK(c.bl_rk.ensure(N1 * 2)); CK(c.bl_last.ensure(std::max<uint64_t>(c.n_inst, 1) * 4));
+  CK(c.bl_rank.ensure(4 * W * 8 + 16 + 8));
+  flush_fills(c);
+  CK(cudaMemsetAsync(c.bl_rank.p, 0, 4 * W * 8 + 16, c.stream));
+  int launches = 0;
+  launches += launch_expand_events(c, SCAN_OUT_EV_INST, c.bl_inst.p);
+  launches += launch_expand_events(c, SCAN_OUT_EV_WAIT, c.bl_wait.p);
+  BA b{c.n_tiles, c.tile_rank.as<uint32_t>(), c.tile_start.as<uint64_t>(), c.rank_off.as<uint64_t>(), c.d_kind,
+       c.bl_inst.as<uint32_t>(), c.bl_wait.as<uint32_t>(), c.inst_rec.as<uint4>(), c.bl_last.as<uint32_t>(),
+       c.bl_p0.as<uint32_t>(), c.bl_rk.as<uint16_t>()};
+  const unsigned tb = nbk(c.n_tiles, 8);
+  uint32_t rounds = 0;
+  unsigned int* changed = reinterpret_cast<unsigned int*>(c.bl_rank.as<uint8_t>() + 4 * W * 8 + 16);
+  if (N) {
+    launches += timed(c, "k_bl_ptr", [&] {
+      k_bl_last<<<tb, 256, 0, c.stream>>>(b);
+      k_bl_ptr<<<tb, 256, 0, c.stream>>>(b);
+      return 2;
+    });
+    // pointer jumping: p_{k+1} = p_k o p_k until no pointer changes (or 2^34 > N steps are covered)
+    const uint32_t* src = c.bl_p0.as<uint32_t>();
+    uint32_t* bufs[2] = {c.bl_pa.as<uint32_t>(), c.bl_pb.as<uint32_t>()};
+    const unsigned jb = (unsigned)std::min<uint64_t>(nbk(N, 256), 148ull * 8);
+    while (rounds < 34) {
+      uint32_t* dst = bufs[rounds & 1];
+      CK(cudaMemsetAsync(changed, 0, 4, c.stream));
+      launches += timed(c, "k_bl_jump", [&] { k_bl_jump<<<jb, 256, 0, c.stream>>>(N, src, dst, changed); return 1; });
+      ++rounds;
+      unsigned int h = 0;
+      CK(cudaMemcpyAsync(&h, changed, 4, cudaMemcpyDeviceToHost, c.stream));
+      CK(cudaStreamSynchronize(c.stream));
+      src = dst;
+      if (!h) break;
+    }
+    unsigned long long* R = c.bl_rank.as<unsigned long long>();
+    const bool sh = W * 8 <= 96 * 1024;
+    SA sa{b, (uint32_t)W, src, c.bl_root.as<unsigned long long>(), R, R + W, R + 2 * W, R + 3 * W, R + 4 * W, sh ? 1 : 0};
+    const size_t smem = sh ? W * 8 : 0;
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_bl_sum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const unsigned sb = (unsigned)std::min<uint64_t>(tb, 148ull * 4);
+    launches += timed(c, "k_bl_sum", [&] { k_bl_sum<<<sb, 256, smem, c.stream>>>(sa); return 1; });
+  }
+  c.launches += launches;
+  std::vector<unsigned long long> h(4 * W + 2);
+  CK(cudaMemcpyAsync(h.data(), c.bl_rank.p, (4 * W + 2) * 8, cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  CK(cudaGetLastError());
+  if (out) {
+    *out = scan_blame_result{};
+    out->n_waiting = h[4 * W]; out->n_cyclic = h[4 * W + 1]; out->rounds = rounds; out->top_rank = 0xFFFFFFFFu;
+    unsigned long long best = 0;
+    for (uint64_t r = 0; r < W; ++r) {
+      out->total_wait_ns += h[3 * W + r];
+      if (h[r] > best) { best = h[r]; out->top_rank = (uint32_t)r; }
+    }
+  }
+  c.blamed = true;
+  return SCAN_OK;
+}
+
+}  // namespace ms
+
+using namespace ms;
+
+extern "C" scan_status scan_blame(scan_ctx* ctx, scan_blame_result* out) {
+  if (!ctx) return SCAN_E_INVALID_ARG;
+  Ctx& c = ctx->c;
+  CK(cudaSetDevice(c.device));
+  if (c.stream_mode || c.n_shards > 1) { c.err = "event-level blame is unavailable on stream / sharded contexts"; return SCAN_E_UNSUPPORTED; }
+  if (!c.localized) { c.err = "scan_blame needs a completed analysis (scan_analyze or scan_localize)"; return SCAN_E_ORDER; }
+  return blame_all(c, out);
+}
