@@ -172,6 +172,7 @@ struct Ctx {
   uint64_t g_N = 0, g_ncomm = 0, g_ncomp = 0;  // job-wide totals (sharded)
   DevBuf x_send, x_recv, x_recv2, x_ep, x_stage, headtail, lk_sendmap, lk_recvmap;
   void* h_pin = nullptr;                 // pinned host scratch (exchange read-backs, table staging)
+  void* h_e = nullptr;                   // pinned: the X4 status words (checked after the final read-back)
   size_t h_pin_cap = 0;
   cudaEvent_t ev_x1 = nullptr, ev_x2 = nullptr;
   // event-level blame (k_blame.cu)

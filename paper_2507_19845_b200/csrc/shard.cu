@@ -280,6 +280,12 @@ __global__ void k_x4_status(const Counters* cnt, const uint32_t* cl_J, const uin
   e[2] = cnt->n_incomplete; e[3] = cnt->n_kind_mismatch; e[4] = cnt->n_payload_mismatch;
 }
 
+// after X4: the job-wide integrity counters into the replicated tail's counters (no host round trip)
+__global__ void k_x4_apply(const unsigned long long* e, Counters* cnt) {
+  if (threadIdx.x || blockIdx.x) return;
+  cnt->n_incomplete = e[2]; cnt->n_kind_mismatch = e[3]; cnt->n_payload_mismatch = e[4];
+}
+
 // all-gather of n u32 already packed in c.x_send; the gathered words land on the host
 // pinned host scratch of the shard path (exchange read-backs, table staging)
 scan_status pin_ensure(Ctx& c, size_t bytes) {
@@ -621,7 +627,6 @@ scan_status sharded_all(Ctx& c) {
     k_x4_status<<<1, 32, 0, c.stream>>>(c.counters.as<Counters>(), c.cl_J.as<uint32_t>(), c.cl_max.as<uint32_t>(),
                                         (uint32_t)ncl, (g + 1 < G && c.DP >= 2) ? 1 : 0, ht + (uint64_t)G * W);
     c.launches += 1;
-    unsigned long long e[16];
     // ---- X4: one grouped all-reduce (sum) of every partial result
     const uint64_t nnz_tot = c.nnz_c + W * PCAP;
     ncclResult_t xr = ncclSuccess;
@@ -640,20 +645,19 @@ scan_status sharded_all(Ctx& c) {
     });
     if (xr != ncclSuccess) { c.err = std::string("NCCL all-reduce: ") + ncclGetErrorString(xr); return SCAN_E_NCCL; }
     mark("x4enq");
-    CK(cudaMemcpyAsync(e, ht + (uint64_t)G * W, sizeof(e), cudaMemcpyDeviceToHost, c.stream));
-    CK(cudaStreamSynchronize(c.stream));
-    mark("x4");
-    if (e[0]) { c.err = "sharded analysis needs an SPMD trace on every shard (fused-pass verification failed)"; return SCAN_E_UNSUPPORTED; }
-    if (e[1]) { c.err = "a DP class has unequal compute counts inside a shard other than the last"; return SCAN_E_UNSUPPORTED; }
-    c.hc.n_incomplete = e[2]; c.hc.n_kind_mismatch = e[3]; c.hc.n_payload_mismatch = e[4];
   }
-  // ---- replicated tail on identical job-wide inputs
+  // ---- replicated tail on identical job-wide inputs, enqueued behind X4 without a host round trip:
+  // the X4 status words go to pinned memory and are checked after the final read-back
+  if (!c.h_e) CK(cudaMallocHost(&c.h_e, 16 * sizeof(unsigned long long)));
+  CK(cudaMemcpyAsync(c.h_e, ht + (uint64_t)G * W, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream));
   {
     Counters z = c.hc;
     z.n_compared = z.n_slow = z.n_candidates = z.n_class_mismatch = 0;
     z.n_link_slow = z.n_roots = z.n_victims = z.n_unattributed = 0;
     for (auto& v : z.v_count) v = 0;
     CK(cudaMemcpyAsync(c.counters.p, &z, sizeof(Counters), cudaMemcpyHostToDevice, c.stream));
+    k_x4_apply<<<1, 32, 0, c.stream>>>(ht + (uint64_t)G * W, c.counters.as<Counters>());
+    c.launches += 1;
   }
   if (c.lcfg.stage2_mode == 0 && G > 1) {
     k_shard_fixup<<<(unsigned)((W + 255) / 256), 256, 0, c.stream>>>(c.W, (int)G, ht, c.wl_joined.as<uint32_t>(),
@@ -665,6 +669,9 @@ scan_status sharded_all(Ctx& c) {
   c.launches += timed(c, "k_walk", [&] { return launch_verdict_walk(c); });
   if ((st = sync_read(c))) return st;
   mark("end");
+  const unsigned long long* e = static_cast<const unsigned long long*>(c.h_e);
+  if (e[0]) { c.err = "sharded analysis needs an SPMD trace on every shard (fused-pass verification failed)"; return SCAN_E_UNSUPPORTED; }
+  if (e[1]) { c.err = "a DP class has unequal compute counts inside a shard other than the last"; return SCAN_E_UNSUPPORTED; }
   if (c.hc.overflow & 24u) {
     c.err = "capacity exceeded: more than 16384 samples on a link / links in a direction class";
     return SCAN_E_UNSUPPORTED;
@@ -693,6 +700,8 @@ void shard_release(Ctx& c) {
   c.nccl = nullptr;
   if (c.h_pin) cudaFreeHost(c.h_pin);
   c.h_pin = nullptr; c.h_pin_cap = 0;
+  if (c.h_e) cudaFreeHost(c.h_e);
+  c.h_e = nullptr;
   if (c.ev_x1) { cudaEventDestroy(c.ev_x1); cudaEventDestroy(c.ev_x2); }
   c.ev_x1 = c.ev_x2 = nullptr;
 }
