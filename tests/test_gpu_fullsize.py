@@ -1,0 +1,114 @@
+"""Parity at BASELINE.json's full size, in the launch configuration bench.py times (-m gpu).
+
+C3 (1024 ranks, 1000 iterations, 960,768,000 events) is analysed exactly as the bench step does it
+(device-resident columns, scan_analyze, fused pass). The oracle cannot run the whole job in seconds,
+so:
+* sampled outputs: per-event outputs are iteration-local (instances never straddle an iteration,
+  reading R30; stage 1 compares the same position of the DP peers). The events of sampled iteration
+  windows must therefore equal the oracle run on those windows alone: waits, slow flags, stage-1
+  references and the instance partition. Windows: the start, inside rank 862's x2.5 throttle, and
+  the last iteration.
+* properties that hold at any size: per-rank compute / wait + transfer sums against numpy sums of
+  the raw durations, integrity counters, the injected throttle's verdict, and blame conservation.
+The JSON ingest workload of the bench (C2 shape, 64 files, 40 iterations) is checked the same way:
+two per-rank files parsed by the oracle against the same ranks of the GPU ingest of all 64."""
+import numpy as np
+import pytest
+
+import oracle
+import tracegen as tg
+from tracegen import configs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c3_full():
+    import torch
+    import paper_2507_19845_b200 as ms
+    cfg = configs.c3(seed=1)
+    tr = tg.generate(cfg, with_start=False)
+    dev = {k: torch.from_numpy(np.ascontiguousarray(getattr(tr, k)).view(
+        np.int16 if getattr(tr, k).dtype == np.uint16 else np.int32)).cuda() for k in ("dur_ns", "kind_op", "meta", "comm", "payload")}
+    s = ms.Scan(0)
+    s.load(tr, device_ptrs=True, cols=dev)
+    res = s.analyze(ms.DetectConfig(want_ref=True))
+    out = {k: s.export(k) for k in ("ev_inst", "ev_wait", "ev_slow", "ev_ref", "rk_sum_compute", "rk_sum_wait",
+                                    "rk_sum_transfer", "wl_verdict")}
+    bl = s.blame()
+    out["bl_suffered"] = s.export("bl_suffered")
+    out["bl_inflicted"] = s.export("bl_inflicted")
+    s.close()
+    del dev
+    torch.cuda.empty_cache()
+    return cfg, tr, res, out, bl
+
+
+@pytest.mark.parametrize("b,e", [(0, 2), (550, 552), (999, 1000)])
+def test_c3_sampled_iterations_equal_the_oracle(c3_full, b, e):
+    cfg, tr, res, out, _ = c3_full
+    assert res["fused"]  # the bench's path
+    sl = tg.generate(cfg, with_start=False, iter_range=(b, e))
+    o = oracle.run(sl, oracle.Config())
+    pre = tg.count(cfg, (0, b)).astype(np.int64) if b else np.zeros(tr.world + 1, np.int64)  # (0, 0) = whole trace
+    ro = tr.rank_offsets.astype(np.int64)
+    sro = sl.rank_offsets.astype(np.int64)
+    idx = np.concatenate([ro[r] + (pre[r + 1] - pre[r]) + np.arange(sro[r + 1] - sro[r]) for r in range(tr.world)])
+    assert np.array_equal(tr.dur_ns[idx], sl.dur_ns)  # the same events
+    for k in ("ev_wait", "ev_slow", "ev_ref"):
+        g = out[k][idx]
+        bad = np.flatnonzero(g != o[k])
+        assert len(bad) == 0, f"{k}: {len(bad)} diffs, first {bad[:5]}: gpu {g[bad[:5]]} oracle {o[k][bad[:5]]}"
+    comm = (sl.kind_op & 7) != 0
+    gi, oi = out["ev_inst"][idx][comm], o["ev_inst"][comm]
+    assert np.array_equal(np.unique(gi, return_inverse=True)[1], np.unique(oi, return_inverse=True)[1])
+    if b == 550:  # rank 862 (x2.5 on [500, 900)) is slow against its DP peers on every kernel
+        comp = (sl.kind_op & 7) == 0
+        r862 = np.zeros(sl.n_events, bool)
+        r862[sro[862]:sro[863]] = True
+        assert o["ev_slow"][r862 & comp].mean() > 0.9
+
+
+def test_c3_properties_at_full_size(c3_full):
+    cfg, tr, res, out, bl = c3_full
+    m = res["match"]
+    assert m["n_incomplete"] == 0 and m["n_kind_mismatch"] == 0 and m["n_payload_mismatch"] == 0
+    ro = tr.rank_offsets.astype(np.int64)
+    for r in range(tr.world):
+        d = tr.dur_ns[ro[r]:ro[r + 1]].astype(np.uint64)
+        comp = (tr.kind_op[ro[r]:ro[r + 1]] & 7) == 0
+        assert int(d[comp].sum()) == int(out["rk_sum_compute"][r])
+        assert int(d[~comp].sum()) == int(out["rk_sum_wait"][r] + out["rk_sum_transfer"][r])  # dur = wait + dmin
+    assert out["wl_verdict"][862] in (1, 3)  # ComputeSlow / Both
+    assert np.array_equal(out["bl_suffered"], out["rk_sum_wait"])  # blame conservation (EB5)
+    assert bl["top_rank"] == 862 and bl["n_cyclic"] == 0
+
+
+def test_json_bench_workload_sampled_files():
+    import paper_2507_19845_b200 as ms
+    from oracle import chrome_json as cj
+    from tracegen import chrome
+    cfg = configs.c2(seed=1, iterations=40)
+    tr = tg.generate(cfg)
+    data, off = chrome.rank_documents_fast(tr)
+    s = ms.Scan(0)
+    res = ms.scan_ingest_json(s.ctx, cfg.tp, cfg.pp, cfg.dp, data, off)
+    assert res["n_events"] == tr.n_events
+    g = {k: s.loaded(k) for k in ("rank_offsets", "start_ns", "dur_ns", "kind_op", "meta", "comm", "payload",
+                                  "comm_offsets", "comm_members")}
+    s.close()
+    docs = [data[int(off[r]):int(off[r + 1])] for r in (0, 1)]
+    t, _ = cj.parse(docs, cfg.tp, cfg.pp, cfg.dp)
+    gro, oro = g["rank_offsets"].astype(np.int64), t.rank_offsets.astype(np.int64)
+    for r in (0, 1):
+        gs, os_ = slice(gro[r], gro[r + 1]), slice(oro[r], oro[r + 1])
+        for k in ("start_ns", "dur_ns", "kind_op", "meta", "payload"):
+            assert np.array_equal(g[k][gs], getattr(t, k)[os_]), k
+        gk, ok = g["kind_op"][gs] & 7, t.kind_op[os_] & 7
+        gc, oc = g["comm"][gs], t.comm[os_]
+        gco, oco = g["comm_offsets"].astype(np.int64), t.comm_offsets.astype(np.int64)
+        for a, b_, kk in zip(gc, oc, gk):  # collectives: the same participant list; P2P: the same peer
+            if 1 <= kk <= 4:
+                assert g["comm_members"][gco[a]:gco[a + 1]].tolist() == t.comm_members[oco[b_]:oco[b_ + 1]].tolist()
+            else:
+                assert a == b_
