@@ -977,6 +977,9 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
     // a warp covers 4*lpr positions of 32/lpr rows (lpr = T/4 lanes per row when T < 128)
     const uint32_t lpr = T >= 128 ? 32u : T / 4u, rpw = 32u / lpr, rstep = FT_NW * rpw;
     const uint32_t rsub = lane / lpr, lpos = lane % lpr;
+#if defined(MS_EXP_SKIP) && (MS_EXP_SKIP & 32)
+    if (R == 0)  // timing experiment only (results invalid)
+#endif
     for (uint32_t pq = 0; pq < np; pq += 4 * lpr) {
       const uint32_t pbase = pq + lpos * 4;
       const bool pin = pbase < np;
@@ -997,6 +1000,9 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
   if (bad) { if (tid == 0) atomicOr(&a.cnt->overflow, NOT_SPMD); return; }
   // ---- (2) phase A: stage 1. Exact quick reject per DP group: den*max <= num*min -> nobody slow.
   const uint32_t nc = nlist[0];
+#if defined(MS_EXP_SKIP) && (MS_EXP_SKIP & 16)
+  if (R == 0)  // timing experiment only (results invalid)
+#endif
   if (DP >= 2) {
     bool sl_any = false;
     for (uint32_t i = wid; i < nc; i += FT_NW) {
@@ -1252,6 +1258,9 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
       }
     }
   }
+#if defined(MS_EXP_SKIP) && (MS_EXP_SKIP & 64)
+  if (R == 0)  // timing experiment only (results invalid)
+#endif
   for (uint32_t row = tid; row < R; row += FT_NT) {
     const uint32_t r = sbase + row;
     const uint32_t gt = row >> tpsh, gd = row & (TP - 1u), GO = DP + TP;
@@ -1265,6 +1274,9 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
     if (sjoin[row]) atomicAdd(&a.wl_joined[(uint64_t)w_tile * a.W + r], sjoin[row]);
     if (slate[row]) atomicAdd(&a.wl_late[(uint64_t)w_tile * a.W + r], slate[row]);
   }
+#if defined(MS_EXP_SKIP) && (MS_EXP_SKIP & 8)
+  if (R == 0)  // timing experiment only (results invalid)
+#endif
   {
     const FDiv fe = fdiv_make(ES);
     for (uint32_t i = tid; i < R * ES; i += FT_NT) {
