@@ -52,10 +52,24 @@ def obj_stale(src: str, obj: str) -> bool:
     return any(os.path.getmtime(p) > t for p in [src, *headers()])
 
 
+def _flags_changed(objdir: str) -> bool:
+    """True if the compile flags differ from the ones the objects were built with (then rebuild all)."""
+    stamp = os.path.join(objdir, "flags.txt")
+    cur = " ".join(ARCH + FLAGS)
+    old = open(stamp).read() if os.path.exists(stamp) else None
+    if old != cur:
+        os.makedirs(objdir, exist_ok=True)
+        with open(stamp, "w") as f:
+            f.write(cur)
+        return True
+    return False
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    objdir = os.path.join(HERE, "build")
+    force = _flags_changed(objdir) or force
     if not force and not stale():
         return SO
-    objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []

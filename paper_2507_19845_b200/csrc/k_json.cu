@@ -278,14 +278,15 @@ struct Cur {
   uint4 cv;
   __device__ __forceinline__ uint32_t c() {
     if (p >= end) return 0u;
-#if !MS_J_CACHE
-    return __ldg(b + p);
-#endif
+#if MS_J_CACHE
     const uint64_t blk = p & ~15ull;
     if (blk != cb) { cb = blk; cv = __ldg(reinterpret_cast<const uint4*>(b + blk)); }
     const uint32_t q = (uint32_t)(p >> 2) & 3u;
     const uint32_t w = (q & 2u) ? ((q & 1u) ? cv.w : cv.z) : ((q & 1u) ? cv.y : cv.x);
     return (w >> (8u * ((uint32_t)p & 3u))) & 0xFFu;
+#else
+    return __ldg(b + p);
+#endif
   }
   __device__ __forceinline__ void ws() { while (is_ws(c()) && p < end) ++p; }
   __device__ __forceinline__ bool fail() { if (bad == NONE64) bad = p; return false; }
