@@ -235,8 +235,10 @@ def json_io(ms, torch, local, stream, steps: int, warmup: int, cpu: bool) -> dic
     e1.record(stream)
     torch.cuda.synchronize()
     ems = e0.elapsed_time(e1) / steps
+    out = torch.empty(int(nb.value), dtype=torch.uint8, pin_memory=True).numpy()  # caller-owned, allocated once
+    s.emit_chrome(dst=out)
     t0 = time.perf_counter()
-    out = s.emit_chrome()
+    s.emit_chrome(dst=out)  # build on the device + one D2H into the pinned host buffer
     emit_e2e_s = time.perf_counter() - t0
     s.close()
     base = None
@@ -261,7 +263,8 @@ def json_io(ms, torch, local, stream, steps: int, warmup: int, cpu: bool) -> dic
                     "path": "pinned host bytes -> scan_ingest_json(SCAN_HOST_PTRS), wall clock"},
             "emit": {"value": len(out) / (ems / 1e3) / 1e9, "unit": "GB/s (merged document built on the device)",
                      "ms_per_call": ems, "bytes": len(out),
-                     "e2e_gb_s": len(out) / emit_e2e_s / 1e9},
+                     "e2e_gb_s": len(out) / emit_e2e_s / 1e9,
+                     "e2e_path": "scan_emit_chrome build + D2H into a caller-owned pinned buffer (s.emit_chrome(dst=...)), wall clock"},
             "cpu_baseline": base}
 
 

@@ -336,8 +336,9 @@ def scan_loaded_column(ctx, name: str) -> np.ndarray:
     return out
 
 
-def scan_emit_chrome(ctx, aligned: bool = False, dst=None) -> bytes | int:
-    """Merged, annotated Chrome Tracing document (scan.h). Returns bytes, or the byte count when
+def scan_emit_chrome(ctx, aligned: bool = False, dst=None, as_bytes: bool = True):
+    """Merged, annotated Chrome Tracing document (scan.h). Returns bytes; with ``as_bytes=False`` a
+    uint8 numpy array in pinned host memory (one D2H copy, no further copy); or the byte count when
     ``dst`` (a uint8 CUDA tensor / numpy array large enough) receives it."""
     lib = _load_lib()
     flags = SCAN_EMIT_ALIGNED if aligned else 0
@@ -348,9 +349,17 @@ def scan_emit_chrome(ctx, aligned: bool = False, dst=None) -> bytes | int:
         _check(ctx, lib.scan_emit_chrome(ctx, flags, _ptr(dst), int(dst.numel() if hasattr(dst, "numel") else dst.size),
                                          1 if dev else 0, ctypes.byref(nb)))
         return nb.value
-    out = np.empty(nb.value, dtype=np.uint8)
-    _check(ctx, lib.scan_emit_chrome(ctx, flags, out.ctypes.data, nb.value, 0, ctypes.byref(nb)))
-    return out.tobytes()
+    out = None
+    if not as_bytes:
+        try:
+            import torch
+            out = torch.empty(max(nb.value, 1), dtype=torch.uint8, pin_memory=True).numpy()[:nb.value]
+        except Exception:
+            out = None
+    if out is None:
+        out = np.empty(nb.value, dtype=np.uint8)
+    _check(ctx, lib.scan_emit_chrome(ctx, flags, out.ctypes.data if nb.value else None, nb.value, 0, ctypes.byref(nb)))
+    return out.tobytes() if as_bytes else out
 
 
 def scan_blame(ctx) -> dict:
@@ -514,8 +523,8 @@ class Scan:
         """A loaded input column (``LOADED_COLUMNS``), e.g. after ``ingest_json``."""
         return scan_loaded_column(self.ctx, name)
 
-    def emit_chrome(self, aligned: bool = False, dst=None):
-        return scan_emit_chrome(self.ctx, aligned, dst)
+    def emit_chrome(self, aligned: bool = False, dst=None, as_bytes: bool = True):
+        return scan_emit_chrome(self.ctx, aligned, dst, as_bytes)
 
     # ---- NEXT-3 sliding-window streaming (scan.h)
     STREAM_OUTPUTS = tuple(n for n, _ in OUTPUTS if n.startswith(("rk_sum", "wd_", "wl_", "lk_", "lb_", "eg_")))
