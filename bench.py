@@ -487,10 +487,12 @@ def main():
             "result": {k: int(v) for k, v in res_bl.items()},
             "kernels": {k: {"ms_per_call": round(v[0] / args.steps, 4), "launches": v[1]}
                         for k, v in sorted(bl_k.items(), key=lambda kv: -kv[1][0])},
-            "roofline": ({"bound": "hbm", "kernel": "k_bl_jump", "bytes_per_event": 12,
-                          "achieved": 12 * N / (jump_ms / 1e3) / 1e9, "peak": pk_b, "unit": "GB/s",
-                          "frac": 12 * N / (jump_ms / 1e3) / 1e9 / pk_b,
-                          "note": "per round: pointer read 4 B + gathered pointer 4 B + write 4 B per event"}
+            "roofline": ({"bound": "hbm", "kernel": "k_bl_jump",
+                          "bytes_per_round": 4 * N + 8 * res_bl["n_active"],
+                          "achieved": (4 * N + 8 * res_bl["n_active"]) / (jump_ms / 1e3) / 1e9, "peak": pk_b,
+                          "unit": "GB/s", "frac": (4 * N + 8 * res_bl["n_active"]) / (jump_ms / 1e3) / 1e9 / pk_b,
+                          "note": "per round: every event's pointer 4 B; events whose pointer is not a root "
+                                  "(n_active) also gather 4 B and write 4 B (upper bound: converged ones only read)"}
                          if jump_ms else None),
         }
 

@@ -246,6 +246,7 @@ typedef struct scan_blame_result {
     uint64_t total_wait_ns;         /* sum of their waits                                             */
     uint32_t rounds;                /* pointer-jumping rounds                                         */
     uint32_t top_rank;              /* rank with the largest BL_INFLICTED (UINT32_MAX if none)        */
+    uint64_t n_active;              /* events whose pointer is not a root (the jumping rounds' work)  */
 } scan_blame_result;
 scan_status scan_blame(scan_ctx* ctx, scan_blame_result* out);
 

@@ -86,7 +86,7 @@ class JsonTraceError(RuntimeError):
 
 class _BlameRes(ctypes.Structure):
     _fields_ = [("n_waiting", ctypes.c_uint64), ("n_cyclic", ctypes.c_uint64), ("total_wait_ns", ctypes.c_uint64),
-                ("rounds", ctypes.c_uint32), ("top_rank", ctypes.c_uint32)]
+                ("rounds", ctypes.c_uint32), ("top_rank", ctypes.c_uint32), ("n_active", ctypes.c_uint64)]
 
 
 class _AlignCfg(ctypes.Structure):

@@ -23,6 +23,7 @@ struct BA {
   const uint32_t* tile_rank; const uint64_t* tile_start; const uint64_t* rank_off;
   const uint16_t* kind; const uint32_t* inst; const uint32_t* wait; const uint4* rec;
   uint32_t* last_ev; uint32_t* ptr0; uint16_t* rank16;
+  uint32_t* ptr; unsigned int* n_active;  // working pointers (jumped in place), events that are not roots
 };
 
 __device__ __forceinline__ bool waiting_ev(const BA& a, uint64_t x, uint16_t ko, uint4& rc) {
@@ -45,33 +46,46 @@ __global__ void __launch_bounds__(256) k_bl_last(BA a) {
 }
 
 __global__ void __launch_bounds__(256) k_bl_ptr(BA a) {
+  __shared__ unsigned int blk_act;
+  if (threadIdx.x == 0) blk_act = 0;
+  __syncthreads();
   const uint64_t tile = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (tile >= a.n_tiles) return;
-  const uint32_t r = a.tile_rank[tile];
-  const uint64_t rs = a.rank_off[r];
-  const uint64_t s = a.tile_start[tile], e = min(s + (uint64_t)TILE_EV, a.rank_off[r + 1]);
-  for (uint64_t x = s + lane_id(); x < e; x += 32) {
-    const uint16_t ko = a.kind[x];
-    uint64_t p;
-    uint4 rc;
-    if ((ko & 7u) == 0) p = x;                                     // EB3: compute events are roots
-    else if (waiting_ev(a, x, ko, rc)) {                           // EB2: the last arriver's previous event
-      const uint64_t le = a.last_ev[a.inst[x]];
-      p = le == a.rank_off[rc.z] ? le : le - 1;
-    } else p = x == rs ? x : x - 1;                                // EB3: own previous event
-    a.ptr0[x] = (uint32_t)p;
-    a.rank16[x] = (uint16_t)r;
+  uint32_t n_act = 0;
+  if (tile < a.n_tiles) {
+    const uint32_t r = a.tile_rank[tile];
+    const uint64_t rs = a.rank_off[r];
+    const uint64_t s = a.tile_start[tile], e = min(s + (uint64_t)TILE_EV, a.rank_off[r + 1]);
+    for (uint64_t x = s + lane_id(); x < e; x += 32) {
+      const uint16_t ko = a.kind[x];
+      uint64_t p;
+      uint4 rc;
+      if ((ko & 7u) == 0) p = x;                                     // EB3: compute events are roots
+      else if (waiting_ev(a, x, ko, rc)) {                           // EB2: the last arriver's previous event
+        const uint64_t le = a.last_ev[a.inst[x]];
+        p = le == a.rank_off[rc.z] ? le : le - 1;
+      } else p = x == rs ? x : x - 1;                                // EB3: own previous event
+      a.ptr0[x] = (uint32_t)p;
+      a.ptr[x] = (uint32_t)p;
+      a.rank16[x] = (uint16_t)r;
+      n_act += p != x;
+    }
   }
+  n_act = warp_sum_u32(n_act);
+  if (lane_id() == 0 && n_act) atomicAdd(&blk_act, n_act);
+  __syncthreads();
+  if (threadIdx.x == 0 && blk_act) atomicAdd(a.n_active, blk_act);  // one global atomic per block
 }
 
-__global__ void __launch_bounds__(256) k_bl_jump(uint64_t N, const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
-                                                 unsigned int* changed) {
+// one in-place jumping round: p[x] <- p[p[x]] for every event whose pointer is not a root yet. In-place
+// updates only speed the convergence up (every pointer stays on its chain); the result is each
+// chain's root either way. Roots (p[x] == x) cost one 4-byte read.
+__global__ void __launch_bounds__(256) k_bl_jump(uint64_t N, uint32_t* ptr, unsigned int* changed) {
   bool ch = false;
   for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < N; x += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t p = src[x];
-    const uint32_t q = src[p];
-    dst[x] = q;
-    ch |= q != p;
+    const uint32_t p = ptr[x];
+    if (p == x) continue;
+    const uint32_t q = ptr[p];
+    if (q != p) { ptr[x] = q; ch = true; }
   }
   if (__any_sync(0xFFFFFFFFu, ch) && lane_id() == 0) atomicOr(changed, 1u);
 }
@@ -165,35 +179,39 @@ scan_status blame_all(Ctx& c, scan_blame_result* out) {
   CK(c.bl_pb.ensure(N1 * 4)); CK(c.bl_root.ensure(N1 * 8)); CK(c.bl_rk.ensure(N1 * 2)); CK(c.bl_last.ensure(std::max<uint64_t>(c.n_inst, 1) * 4));
   CK(c.bl_rank.ensure(4 * W * 8 + 16 + 8));
   flush_fills(c);
-  CK(cudaMemsetAsync(c.bl_rank.p, 0, 4 * W * 8 + 16, c.stream));
+  CK(cudaMemsetAsync(c.bl_rank.p, 0, 4 * W * 8 + 16 + 8, c.stream));
   int launches = 0;
   launches += launch_expand_events(c, SCAN_OUT_EV_INST, c.bl_inst.p);
   launches += launch_expand_events(c, SCAN_OUT_EV_WAIT, c.bl_wait.p);
+  unsigned int* counters2 = reinterpret_cast<unsigned int*>(c.bl_rank.as<uint8_t>() + 4 * W * 8 + 16);  // [0] changed, [1] n_active
   BA b{c.n_tiles, c.tile_rank.as<uint32_t>(), c.tile_start.as<uint64_t>(), c.rank_off.as<uint64_t>(), c.d_kind,
        c.bl_inst.as<uint32_t>(), c.bl_wait.as<uint32_t>(), c.inst_rec.as<uint4>(), c.bl_last.as<uint32_t>(),
-       c.bl_p0.as<uint32_t>(), c.bl_rk.as<uint16_t>()};
+       c.bl_p0.as<uint32_t>(), c.bl_rk.as<uint16_t>(), c.bl_pa.as<uint32_t>(), counters2 + 1};
   const unsigned tb = nbk(c.n_tiles, 8);
   uint32_t rounds = 0;
-  unsigned int* changed = reinterpret_cast<unsigned int*>(c.bl_rank.as<uint8_t>() + 4 * W * 8 + 16);
+  unsigned int n_act = 0;
+  unsigned int* changed = counters2;
+  const uint32_t* src = c.bl_pa.as<uint32_t>();
   if (N) {
     launches += timed(c, "k_bl_ptr", [&] {
       k_bl_last<<<tb, 256, 0, c.stream>>>(b);
       k_bl_ptr<<<tb, 256, 0, c.stream>>>(b);
       return 2;
     });
-    // pointer jumping: p_{k+1} = p_k o p_k until no pointer changes (or 2^34 > N steps are covered)
-    const uint32_t* src = c.bl_p0.as<uint32_t>();
-    uint32_t* bufs[2] = {c.bl_pa.as<uint32_t>(), c.bl_pb.as<uint32_t>()};
+    CK(cudaMemcpyAsync(&n_act, counters2 + 1, 4, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    // pointer jumping until no pointer changes (2^34 > N steps at most)
     const unsigned jb = (unsigned)std::min<uint64_t>(nbk(N, 256), 148ull * 8);
-    while (rounds < 34) {
-      uint32_t* dst = bufs[rounds & 1];
+    while (n_act && rounds < 34) {
       CK(cudaMemsetAsync(changed, 0, 4, c.stream));
-      launches += timed(c, "k_bl_jump", [&] { k_bl_jump<<<jb, 256, 0, c.stream>>>(N, src, dst, changed); return 1; });
+      launches += timed(c, "k_bl_jump", [&] {
+        k_bl_jump<<<jb, 256, 0, c.stream>>>(N, c.bl_pa.as<uint32_t>(), changed);
+        return 1;
+      });
       ++rounds;
       unsigned int h = 0;
       CK(cudaMemcpyAsync(&h, changed, 4, cudaMemcpyDeviceToHost, c.stream));
       CK(cudaStreamSynchronize(c.stream));
-      src = dst;
       if (!h) break;
     }
     unsigned long long* R = c.bl_rank.as<unsigned long long>();
@@ -212,6 +230,7 @@ scan_status blame_all(Ctx& c, scan_blame_result* out) {
   if (out) {
     *out = scan_blame_result{};
     out->n_waiting = h[4 * W]; out->n_cyclic = h[4 * W + 1]; out->rounds = rounds; out->top_rank = 0xFFFFFFFFu;
+    out->n_active = n_act;
     unsigned long long best = 0;
     for (uint64_t r = 0; r < W; ++r) {
       out->total_wait_ns += h[3 * W + r];
