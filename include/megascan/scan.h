@@ -273,7 +273,8 @@ scan_status scan_blame(scan_ctx* ctx, scan_blame_result* out);
    offending element, or of the document root for SCAN_JF_TRACE_EVENTS); a syntax error anywhere
    wins over any schema error, among schema errors the smallest offset wins (J11). SCAN_E_INVALID_ARG
    (offsets), SCAN_E_UNSUPPORTED (> 2^32-1 elements; a 64-bit group-hash collision), load errors.
-   J10: bytes outside the event arrays are checked for bracket / quote balance only.           */
+   J10: the whole input is validated JSON (UTF-8 excepted); keys, "cat" and "ph" are compared as
+   raw bytes.                                                                                   */
 #define SCAN_JSON_OK      0
 #define SCAN_JSON_SYNTAX  1
 #define SCAN_JSON_SCHEMA  2

@@ -467,11 +467,36 @@ __device__ void j_gap(Cur& u, uint64_t arr_close, bool after_comma, JErr* err) {
   }
 }
 
-// the elements before the first object of every event array (normally none)
+// per document (one thread): (1) an object root's members: keys, ':' and ',' and every member value
+// are validated (the traceEvents array is skipped through its known close, its elements have their
+// own parsers); (2) the elements before the first object of the event array (normally none)
 __global__ void k_j_docs3(JA a) {
   const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= a.n_docs) return;
   const DocInfo& I = a.di[d];
+  if (I.root != NONE64 && I.is_obj && I.root_close != NONE64) {
+    Cur u{a.b, I.root + 1, I.root_close + 1, NONE64};
+    u.ws();
+    if (u.c() == '}' && u.p == I.root_close) {
+      // empty root object (no traceEvents: reported by k_j_docs2)
+    } else {
+      while (true) {
+        u.ws();
+        Str k;
+        if (!j_string(u, k)) { syn(a.err, u.bad); break; }
+        u.ws();
+        if (u.c() != ':') { syn(a.err, u.p); break; }
+        ++u.p;
+        u.ws();
+        if (u.p == I.arr_open && I.arr_close != NONE64) u.p = I.arr_close + 1;  // the event array
+        else if (!j_skip(u)) { syn(a.err, u.bad); break; }
+        u.ws();
+        if (u.c() == ',') { ++u.p; continue; }
+        if (!(u.c() == '}' && u.p == I.root_close)) syn(a.err, u.p);
+        break;
+      }
+    }
+  }
   if (I.arr_open == NONE64 || I.arr_close == NONE64) return;
   Cur u{a.b, I.arr_open + 1, I.arr_close + 1, NONE64};
   j_gap(u, I.arr_close, false, a.err);
