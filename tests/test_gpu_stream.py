@@ -67,3 +67,34 @@ def test_stream_rejects_other_outputs_and_order():
     s.stream_push(ms.slice_iterations(full, 0, 1))
     with pytest.raises(ms.ScanError):
         s.export("ev_inst")
+
+
+@pytest.mark.parametrize("seed", range(401, 401 + int(__import__("os").environ.get("MS_STREAM_FUZZ_N", "8"))))
+def test_stream_fuzz(seed):
+    """Random SPMD jobs (TP, PP, DP in 1..3), window length, stage-2 mode and throttles: after every
+    push the window-level outputs equal the oracle on the window."""
+    import paper_2507_19845_b200 as ms
+    rng = np.random.default_rng(seed)
+    tp, pp, dp = (int(x) for x in rng.integers(1, 4, 3))
+    if tp * pp * dp == 1:
+        dp = 2
+    W = tp * pp * dp
+    iters = int(rng.integers(3, 7))
+    faults = [tg.Fault(tg.THROTTLE, int(rng.integers(0, W)), it0=int(rng.integers(0, iters)), factor=float(rng.choice([1.8, 2.5])))]
+    cfg = tg.GenConfig(tp, pp, dp, int(rng.integers(1, 3)), int(rng.integers(pp, pp + 3)), iters, seed=seed, faults=faults)
+    full = tg.generate(cfg)
+    K, mode, mins = int(rng.integers(1, 4)), int(rng.integers(0, 2)), int(rng.choice([3, 10]))
+    s = ms.Scan(0)
+    s.stream_open(full, K, ms.DetectConfig(min_samples=mins), ms.LocalizeConfig(stage2_mode=mode, min_samples=mins))
+    for i in range(iters):
+        s.stream_push(ms.slice_iterations(full, i, i + 1))
+        lo = max(0, i - K + 1)
+        o = oracle.run(ms.slice_iterations(full, lo, i + 1), oracle.Config(stage2_mode=mode, min_samples=mins))
+        for k in ms.Scan.STREAM_OUTPUTS:
+            v, g = o[k], s.export(k)
+            assert g.shape == v.shape, (i, k)
+            if k in FLOAT_KEYS:
+                assert np.allclose(g, v, rtol=1e-6, atol=0), (i, k)
+            else:
+                assert np.array_equal(g, v), (i, k, np.nonzero(g != v)[0][:5])
+    s.close()
