@@ -70,7 +70,7 @@ def _random_cfg(seed):
 
 # random SPMD jobs (TP, PP, DP in 1..4), random windows / stage-2 mode / min samples
 CASES += [(f"random_{sd}", (lambda sd=sd: _random_cfg(sd)), int([0, 2, 3, 5][sd % 4]), sd % 2, [3, 10][sd % 2], None, None)
-          for sd in range(301, 311)]
+          for sd in range(301, 301 + int(os.environ.get("MS_MULTI_FUZZ_N", "10")))]
 
 
 def main() -> int:
