@@ -997,6 +997,12 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
     if (__any_sync(0xFFFFFFFFu, mis) && lane == 0) bad = 1;
   }
   __syncthreads();
+#if defined(MS_EXP_SKIP) && (MS_EXP_SKIP & 128)
+  // timing experiment only (results invalid): a constant tile, so the compute phases cost the same
+  // with (bit 128) or without (bits 128 + 32) the row loads
+  for (uint32_t i = tid; i < np * RP; i += FT_NT) sd[i] = 1000u;
+  __syncthreads();
+#endif
   if (bad) { if (tid == 0) atomicOr(&a.cnt->overflow, NOT_SPMD); return; }
   // ---- (2) phase A: stage 1. Exact quick reject per DP group: den*max <= num*min -> nobody slow.
   const uint32_t nc = nlist[0];
