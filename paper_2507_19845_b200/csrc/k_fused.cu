@@ -18,6 +18,8 @@
 #include <type_traits>
 #include "internal.cuh"
 
+#include <cstdlib>
+
 namespace ms {
 
 enum { TY_COMPUTE = 0, TY_TP = 1, TY_DP = 2, TY_XCOLL = 3, TY_P2P = 4 };
@@ -284,6 +286,7 @@ struct FusedArgs {
   uint32_t slow_num, slow_den; unsigned long long slow_margin;
   uint32_t wi, classes, mode; unsigned long long late_margin, wait_margin; int want_ref;
   uint32_t it_off;  // global iteration of this shard's first iteration (0 unsharded)
+  uint32_t pf_dist; uint64_t n_events;  // k_fused_t: L2 prefetch of tile + pf_dist (0 = off); column length
   unsigned long long wi_m;  // ceil(2^64 / wi) for wi > 1: window = umulhi64(iteration, wi_m), exact for 32-bit iterations
   Counters* cnt;
   // byte offsets of the transposed kernel's shared-memory arrays (host-computed, fused_t_layout)
@@ -997,6 +1000,32 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
     if (__any_sync(0xFFFFFFFFu, mis) && lane == 0) bad = 1;
   }
   __syncthreads();
+  // L2 prefetch of the rows of a tile ahead (blocks start roughly in index order, so tile + pf_dist is
+  // loaded soon on some SM): its DRAM traffic overlaps this tile's compute phases instead of stalling
+  // that CTA's load pass. A hint only: no result depends on it.
+  if (a.pf_dist) {
+    const uint64_t nt = (uint64_t)tile + a.pf_dist;
+    if (nt < a.n_ftiles) {
+      const uint32_t s2 = a.tile_stage[nt];
+      const uint32_t p02 = ((uint32_t)nt - a.st_tile0[s2]) * T;
+      const uint32_t npos2 = a.st_npos[s2];
+      const uint32_t np2 = min(T, npos2 - p02);
+      const uint64_t rb2 = a.rank_off[s2 * R];
+      const uint32_t l4 = (np2 * 4 + 127) / 128 + 1, l2 = (np2 * 2 + 127) / 128 + 1, per_row = 2 * l4 + l2;
+      for (uint32_t i = tid; i < R * per_row; i += FT_NT) {
+        const uint32_t row = i / per_row, j = i - row * per_row;
+        const uint64_t g = rb2 + (uint64_t)row * npos2 + p02;
+        const char* ptr;
+        uint64_t lim;
+        if (j < l4) { ptr = reinterpret_cast<const char*>(a.dur + g) + 128ull * j; lim = 4 * a.n_events; }
+        else if (j < 2 * l4) { ptr = reinterpret_cast<const char*>(a.comm + g) + 128ull * (j - l4); lim = 4 * a.n_events; }
+        else { ptr = reinterpret_cast<const char*>(a.kind + g) + 128ull * (j - 2 * l4); lim = 2 * a.n_events; }
+        const char* col0 = j < l4 ? reinterpret_cast<const char*>(a.dur) : j < 2 * l4 ? reinterpret_cast<const char*>(a.comm)
+                                                                                       : reinterpret_cast<const char*>(a.kind);
+        if ((uint64_t)(ptr - col0) < lim) asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+      }
+    }
+  }
 #if defined(MS_EXP_SKIP) && (MS_EXP_SKIP & 128)
   // timing experiment only (results invalid): a constant tile, so the compute phases cost the same
   // with (bit 128) or without (bits 128 + 32) the row loads
@@ -1369,6 +1398,19 @@ int launch_fused(Ctx& c) {
   a.sdur = c.sdur.as<uint32_t>(); a.skind = c.skind.as<uint8_t>(); a.sci = c.sci.as<uint32_t>(); a.sit = c.sit.as<uint32_t>();
   a.p2p_pay = c.p2p_pay.as<uint32_t>(); a.p2p_warm = c.p2p_warm.as<uint8_t>(); a.p2p_iter = c.p2p_iter.as<uint32_t>();
   a.p2p_slot0 = c.p2p_slot0; a.p2p_inst0 = c.p2p_inst0; a.citer = c.citer.as<uint32_t>(); a.NIT1 = c.NIT + 1;
+  {  // L2 prefetch distance of the transposed kernel, in tiles. Measured on full C3 (k_fused_t ms):
+     // off 8.51, 48 8.59, 96 8.32, 148 8.35, 200 8.51, 296 8.93, 592 9.07 -> about 2/3 of a resident
+     // wave (SMs x 2 CTAs); MS_FT_PF overrides (0 = off)
+    static int pf = -1;
+    if (pf < 0) {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+      const char* e = std::getenv("MS_FT_PF");
+      pf = e ? std::atoi(e) : sms * FT_MINB / 3;
+    }
+    a.pf_dist = (uint32_t)pf;
+    a.n_events = c.N;
+  }
   a.nbc_off = c.nbc_off.as<uint64_t>(); a.nbc = c.nbc.as<uint32_t>(); a.nbp = c.nbp.as<uint32_t>();
   a.nbp_n = c.nbp_n.as<uint32_t>(); a.nnz_tot = c.nnz_c + (uint64_t)c.W * PCAP; a.nnz_c = c.nnz_c;
   a.ew = c.ewc.as<unsigned long long>(); a.rk_sum = c.rk_sum.as<unsigned long long>();
