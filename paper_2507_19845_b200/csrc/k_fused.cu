@@ -286,7 +286,7 @@ struct FusedArgs {
   uint32_t slow_num, slow_den; unsigned long long slow_margin;
   uint32_t wi, classes, mode; unsigned long long late_margin, wait_margin; int want_ref;
   uint32_t it_off;  // global iteration of this shard's first iteration (0 unsharded)
-  uint32_t pf_dist; uint64_t n_events;  // k_fused_t: L2 prefetch of tile + pf_dist (0 = off); column length
+  uint32_t pf_dist, pf_own; uint64_t n_events;  // k_fused_t: L2 prefetch of tile + pf_dist (0 = off), of its own tile; column length
   unsigned long long wi_m;  // ceil(2^64 / wi) for wi > 1: window = umulhi64(iteration, wi_m), exact for 32-bit iterations
   Counters* cnt;
   // byte offsets of the transposed kernel's shared-memory arrays (host-computed, fused_t_layout)
@@ -840,6 +840,30 @@ __device__ __forceinline__ void loo_dispatch(const FusedArgs& a, const uint32_t*
   else loo_group<32>(a, col, tp, TP, DP, j, sbits, SW, wb, sbase, any);
 }
 
+// L2 prefetch of every rank row of fused tile t (dur, comm, kind columns; 128-byte lines, clamped to
+// the columns). A hint only.
+__device__ __forceinline__ void ft_prefetch_tile(const FusedArgs& a, uint64_t t, uint32_t tid) {
+  if (t >= a.n_ftiles) return;
+  const uint32_t T = a.T, R = a.R;
+  const uint32_t s2 = a.tile_stage[t];
+  const uint32_t p02 = ((uint32_t)t - a.st_tile0[s2]) * T;
+  const uint32_t npos2 = a.st_npos[s2];
+  const uint32_t np2 = min(T, npos2 - p02);
+  const uint64_t rb2 = a.rank_off[s2 * R];
+  const uint32_t l4 = (np2 * 4 + 127) / 128 + 1, l2 = (np2 * 2 + 127) / 128 + 1, per_row = 2 * l4 + l2;
+  for (uint32_t i = tid; i < R * per_row; i += FT_NT) {
+    const uint32_t row = i / per_row, j = i - row * per_row;
+    const uint64_t g = rb2 + (uint64_t)row * npos2 + p02;
+    const char* col0;
+    const char* ptr;
+    uint64_t lim;
+    if (j < l4) { col0 = reinterpret_cast<const char*>(a.dur); ptr = reinterpret_cast<const char*>(a.dur + g) + 128ull * j; lim = 4 * a.n_events; }
+    else if (j < 2 * l4) { col0 = reinterpret_cast<const char*>(a.comm); ptr = reinterpret_cast<const char*>(a.comm + g) + 128ull * (j - l4); lim = 4 * a.n_events; }
+    else { col0 = reinterpret_cast<const char*>(a.kind); ptr = reinterpret_cast<const char*>(a.kind + g) + 128ull * (j - 2 * l4); lim = 2 * a.n_events; }
+    if ((uint64_t)(ptr - col0) < lim) asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+  }
+}
+
 template <int P, int NRB>
 __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -896,6 +920,9 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
   const uint32_t w_tile = win_of(a, itg0);
   const uint32_t ncr = a.ncroles[s];
 
+  // L2 prefetch of this tile's rows at kernel start: the DRAM requests are in flight while the tables
+  // and template info below are set up, so the load pass finds them in L2 (a hint only)
+  if (a.pf_own) ft_prefetch_tile(a, tile, tid);
   // ---- (0) tables and template info
   if (tid < ROLES) kbase[tid] = a.ft_base[(uint64_t)tid * n + tile];
   if (tid < 4) nlist[tid] = 0;
@@ -1003,29 +1030,7 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
   // L2 prefetch of the rows of a tile ahead (blocks start roughly in index order, so tile + pf_dist is
   // loaded soon on some SM): its DRAM traffic overlaps this tile's compute phases instead of stalling
   // that CTA's load pass. A hint only: no result depends on it.
-  if (a.pf_dist) {
-    const uint64_t nt = (uint64_t)tile + a.pf_dist;
-    if (nt < a.n_ftiles) {
-      const uint32_t s2 = a.tile_stage[nt];
-      const uint32_t p02 = ((uint32_t)nt - a.st_tile0[s2]) * T;
-      const uint32_t npos2 = a.st_npos[s2];
-      const uint32_t np2 = min(T, npos2 - p02);
-      const uint64_t rb2 = a.rank_off[s2 * R];
-      const uint32_t l4 = (np2 * 4 + 127) / 128 + 1, l2 = (np2 * 2 + 127) / 128 + 1, per_row = 2 * l4 + l2;
-      for (uint32_t i = tid; i < R * per_row; i += FT_NT) {
-        const uint32_t row = i / per_row, j = i - row * per_row;
-        const uint64_t g = rb2 + (uint64_t)row * npos2 + p02;
-        const char* ptr;
-        uint64_t lim;
-        if (j < l4) { ptr = reinterpret_cast<const char*>(a.dur + g) + 128ull * j; lim = 4 * a.n_events; }
-        else if (j < 2 * l4) { ptr = reinterpret_cast<const char*>(a.comm + g) + 128ull * (j - l4); lim = 4 * a.n_events; }
-        else { ptr = reinterpret_cast<const char*>(a.kind + g) + 128ull * (j - 2 * l4); lim = 2 * a.n_events; }
-        const char* col0 = j < l4 ? reinterpret_cast<const char*>(a.dur) : j < 2 * l4 ? reinterpret_cast<const char*>(a.comm)
-                                                                                       : reinterpret_cast<const char*>(a.kind);
-        if ((uint64_t)(ptr - col0) < lim) asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
-      }
-    }
-  }
+  if (a.pf_dist) ft_prefetch_tile(a, (uint64_t)tile + a.pf_dist, tid);
 #if defined(MS_EXP_SKIP) && (MS_EXP_SKIP & 128)
   // timing experiment only (results invalid): a constant tile, so the compute phases cost the same
   // with (bit 128) or without (bits 128 + 32) the row loads
@@ -1398,17 +1403,21 @@ int launch_fused(Ctx& c) {
   a.sdur = c.sdur.as<uint32_t>(); a.skind = c.skind.as<uint8_t>(); a.sci = c.sci.as<uint32_t>(); a.sit = c.sit.as<uint32_t>();
   a.p2p_pay = c.p2p_pay.as<uint32_t>(); a.p2p_warm = c.p2p_warm.as<uint8_t>(); a.p2p_iter = c.p2p_iter.as<uint32_t>();
   a.p2p_slot0 = c.p2p_slot0; a.p2p_inst0 = c.p2p_inst0; a.citer = c.citer.as<uint32_t>(); a.NIT1 = c.NIT + 1;
-  {  // L2 prefetch distance of the transposed kernel, in tiles. Measured on full C3 (k_fused_t ms):
-     // off 8.51, 48 8.59, 96 8.32, 148 8.35, 200 8.51, 296 8.93, 592 9.07 -> about 2/3 of a resident
-     // wave (SMs x 2 CTAs); MS_FT_PF overrides (0 = off)
+  {  // L2 prefetches of the transposed kernel. Measured on full C3 (k_fused_t ms): none 8.51; own tile
+     // at kernel start 8.22 (default); tile pf ahead after the load pass: 96 8.32, 148 8.35, 296 8.93;
+     // both together 8.60 (98 + own). MS_FT_PF (distance, default 0 = off) / MS_FT_PF_OWN (0/1) override
     static int pf = -1;
     if (pf < 0) {
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
       const char* e = std::getenv("MS_FT_PF");
-      pf = e ? std::atoi(e) : sms * FT_MINB / 3;
+      pf = e ? std::atoi(e) : 0;
+      (void)sms;
     }
+    static int own = -1;
+    if (own < 0) { const char* e = std::getenv("MS_FT_PF_OWN"); own = e ? std::atoi(e) : 1; }
     a.pf_dist = (uint32_t)pf;
+    a.pf_own = (uint32_t)own;
     a.n_events = c.N;
   }
   a.nbc_off = c.nbc_off.as<uint64_t>(); a.nbc = c.nbc.as<uint32_t>(); a.nbp = c.nbp.as<uint32_t>();
