@@ -30,6 +30,9 @@ constexpr uint64_t NONE64 = ~0ull;
 #ifndef MS_J_CACHE
 #define MS_J_CACHE 0   // 1: 16-byte register-cached cursor in k_j_parse (measured slower: registers)
 #endif
+#ifndef MS_J_PREFETCH
+#define MS_J_PREFETCH 0   // k_j_parse: L1 prefetch of this many lines after an element's first (timed below)
+#endif
 #ifndef MS_J_MINB
 #define MS_J_MINB 8    // k_j_parse: <= 64 registers, 16 warps per SM (measured: 1 -> 5.6 ms, 8 -> 3.2 ms on C2x40)
 #endif
@@ -668,6 +671,13 @@ __global__ void __launch_bounds__(128, MS_J_MINB) k_j_parse(PA a) {
   if (i >= a.n_el) return;
   const uint64_t p0 = a.epos[i];
   const DocInfo& I = a.di[a.edoc[i]];
+#if MS_J_PREFETCH
+  {  // the element's first lines (typical elements span 2-3): later misses overlap the first
+    const uint64_t lim = I.arr_close + 1;
+    for (uint32_t k = 1; k <= MS_J_PREFETCH; ++k)
+      if (p0 + 128ull * k < lim) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.b + p0 + 128ull * k));
+  }
+#endif
   Cur u{a.b, p0, I.arr_close + 1, NONE64};
   Ev v{};
   v.gpos = NONE64;
