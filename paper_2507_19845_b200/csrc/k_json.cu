@@ -412,7 +412,6 @@ __device__ bool j_skip(Cur& u) {
       want_key = false;
     }
     const uint32_t x = u.c();
-    bool closed_now = false;
     if (x == '{' || x == '[') {
       if (dep >= 64) return u.fail();
       const bool obj = x == '{';
@@ -420,7 +419,7 @@ __device__ bool j_skip(Cur& u) {
       ++dep;
       ++u.p;
       u.ws();
-      if (u.c() == (obj ? '}' : ']')) { ++u.p; --dep; closed_now = true; }
+      if (u.c() == (obj ? '}' : ']')) { ++u.p; --dep; }
       else if (obj) { want_key = true; continue; }
       else continue;
     } else if (x == '"') {
@@ -433,7 +432,6 @@ __device__ bool j_skip(Cur& u) {
     else if (x == 'f') { if (!j_literal(u, "false")) return false; }
     else if (x == 'n') { if (!j_literal(u, "null")) return false; }
     else return u.fail();
-    (void)closed_now;
     // after a value: close containers / next element
     while (true) {
       if (dep == 0) return true;
@@ -805,11 +803,6 @@ __global__ void k_j_rankkeys(uint64_t n, const uint32_t* perm, const uint32_t* r
   if (j >= n) return;
   const uint32_t r = rank[perm[j]];
   key[j] = r == SKIPPED ? W : r;
-}
-
-__global__ void k_j_gather_ts(uint64_t n, const uint32_t* idx, const int64_t* ts, int64_t* out) {
-  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < n) out[j] = ts[idx[j]];
 }
 
 // rank offsets from the rank-sorted keys

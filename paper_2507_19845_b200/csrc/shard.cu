@@ -286,7 +286,6 @@ __global__ void k_x4_apply(const unsigned long long* e, Counters* cnt) {
   cnt->n_incomplete = e[2]; cnt->n_kind_mismatch = e[3]; cnt->n_payload_mismatch = e[4];
 }
 
-// all-gather of n u32 already packed in c.x_send; the gathered words land on the host
 // pinned host scratch of the shard path (exchange read-backs, table staging)
 scan_status pin_ensure(Ctx& c, size_t bytes) {
   if (bytes <= c.h_pin_cap && c.h_pin) return SCAN_OK;
@@ -302,16 +301,6 @@ scan_status pin_ensure_keep(Ctx& c, size_t bytes) {
   CK(cudaMallocHost(&nb, bytes));
   if (c.h_pin) { std::memcpy(nb, c.h_pin, c.h_pin_cap); cudaFreeHost(c.h_pin); }
   c.h_pin = nb; c.h_pin_cap = bytes;
-  return SCAN_OK;
-}
-
-scan_status allgather_dev(Ctx& c, size_t n, std::vector<uint32_t>& all) {
-  const size_t G = (size_t)c.n_shards;
-  CK(c.x_recv.ensure(n * 4 * G));
-  NCK(ncclAllGather(c.x_send.p, c.x_recv.p, n, ncclUint32, (ncclComm_t)c.nccl, c.stream));
-  all.assign(n * G, 0);
-  CK(cudaMemcpyAsync(all.data(), c.x_recv.p, n * 4 * G, cudaMemcpyDeviceToHost, c.stream));
-  CK(cudaStreamSynchronize(c.stream));
   return SCAN_OK;
 }
 
