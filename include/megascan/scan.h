@@ -38,9 +38,9 @@ extern "C" {
 
 typedef int32_t scan_status;
 #define SCAN_OK               0
-#define SCAN_PARTIAL          1   /* success, but unmatched / inconsistent instances were reported (SPEC S:L181, S:L190) */
+#define SCAN_PARTIAL          1   /* success, but unmatched / inconsistent instances were reported (SPEC S:L200, S:L209) */
 #define SCAN_E_INVALID_ARG   -1
-#define SCAN_E_SCHEMA        -2   /* event fails the schema (kind, comm id, membership, peer); S:L117, S:L34 */
+#define SCAN_E_SCHEMA        -2   /* event fails the schema (kind, comm id, membership, peer); S:L136, S:L34, S:L53 */
 #define SCAN_E_INTEGRITY     -3   /* only with SCAN_STRICT: any unmatched / mismatched instance */
 #define SCAN_E_ORDER         -4   /* call sequence violated (detect before match, ...) */
 #define SCAN_E_CUDA          -5
@@ -64,7 +64,7 @@ typedef struct scan_ctx scan_ctx;
 
 typedef struct scan_topology {
     int32_t tp, pp, dp;      /* world = tp*pp*dp ranks                                         */
-    uint32_t rank_order;     /* must be 0: rank = tp + TP*(dp + DP*pp) (SPEC S:L81, reading R1) */
+    uint32_t rank_order;     /* must be 0: rank = tp + TP*(dp + DP*pp) (SPEC S:L100, reading R1) */
 } scan_topology;
 
 typedef struct scan_comm_table {     /* collective communicators ("global ID list")    */
@@ -100,7 +100,7 @@ typedef struct scan_match_result {
     uint64_t n_iters;
 } scan_match_result;
 
-typedef struct scan_detect_config {   /* stage 1; defaults from SPEC S:L294 as rationals */
+typedef struct scan_detect_config {   /* stage 1; defaults from SPEC S:L313 as rationals */
     uint32_t slow_num, slow_den;       /* slow iff slow_den*dur > slow_num*ref     (3, 2)            */
     uint64_t slow_margin_ns;           /*      and dur - ref > margin              (50000)           */
     uint32_t cand_num, cand_den;       /* candidate iff cand_den*slow > cand_num*total (3, 10)       */
@@ -120,7 +120,7 @@ typedef struct scan_localize_config {  /* stages 2-3 + walk
     uint32_t bw_num, bw_den;           /* LinkSlow iff bw_den*p_l*t_g < bw_num*p_g*t_l     (7, 10)    */
     uint32_t min_samples;              /* (10)                                                         */
     uint32_t stage2_classes;           /* bit0 TP groups, bit1 DP groups (3)                           */
-    uint32_t stage2_mode;              /* 0 CONDITIONAL (reading R11), 1 UNCONDITIONAL (SPEC S:L323)   */
+    uint32_t stage2_mode;              /* 0 CONDITIONAL (reading R11), 1 UNCONDITIONAL (SPEC S:L342)   */
     uint32_t pad;
     uint64_t wait_margin_ns;           /* wait-for edge iff wait > margin (100000)                     */
 } scan_localize_config;
@@ -163,7 +163,7 @@ const char* scan_last_error(const scan_ctx* ctx);   /* owned by ctx; "" if none 
    One process per GPU. Shard g of n_shards loads, with scan_load_events(), the events of EVERY
    rank for a contiguous block of whole iterations; shards are ordered by iteration (shard g's
    block follows shard g-1's). Iterations are the natural unit: no instance straddles an
-   iteration (the tracer records per-iteration step events; reading R23).
+   iteration (the tracer records per-iteration step events; reading R30).
    scan_analyze() on a sharded context is a COLLECTIVE call (every shard must call it, same
    configs) that returns the job-wide analysis:
      * per-event outputs (EV_*, COMM_*, SLOW_BITS) cover this shard's events, in its own order;

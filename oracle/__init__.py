@@ -55,7 +55,7 @@ class _Config(ctypes.Structure):
 
 @dataclass
 class Config:
-    """Thresholds (SPEC S:L294 defaults as exact rationals; readings R8-R14)."""
+    """Thresholds (SPEC S:L313 defaults as exact rationals; readings R8-R14)."""
     slow_num: int = 3
     slow_den: int = 2
     slow_margin_ns: int = 50_000
@@ -70,7 +70,7 @@ class Config:
     wait_margin_ns: int = 100_000
     window_iters: int = 0
     stage2_classes: int = 3
-    stage2_mode: int = 0  # 0 CONDITIONAL, 1 UNCONDITIONAL (SPEC S:L323 literal)
+    stage2_mode: int = 0  # 0 CONDITIONAL, 1 UNCONDITIONAL (SPEC S:L342 literal)
 
 
 _ARRAYS = {

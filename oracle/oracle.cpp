@@ -9,8 +9,8 @@
 // order of SURVEY.md §8(c) "Procedure" O1..O11. Containers are std::map / std::vector,
 // medians are full std::sort, every decision is integer or exact-rational arithmetic.
 //
-// Pins (tests/test_oracle_*.py, -m "not gpu"): SPEC.md examples (S:L183-194,
-// S:L317-346), brute-force enumeration of match sets on tiny traces, DES ground
+// Pins (tests/test_oracle_*.py, -m "not gpu"): SPEC.md examples (S:L202-213,
+// S:L336-365), brute-force enumeration of match sets on tiny traces, DES ground
 // truth (instance partition, closed-form waits, injected faults), clock-skew
 // invariance, stage-1 monotonicity.  The A7-A8 walk has no paper pin: its
 // definition is ours (reading R17) and is pinned by hand-built chains.
@@ -128,7 +128,7 @@ struct Oracle {
 
   int run() {
     const uint64_t N = in.n_events;
-    // ---- schema validation (SPEC S:L117 parse/schema errors; S:L34 invariants) ----
+    // ---- schema validation (SPEC S:L136 parse/schema errors; S:L34, S:L53 invariants) ----
     for (uint32_t c = 0; c < in.n_comms; ++c)
       if (in.comm_offsets[c + 1] < in.comm_offsets[c]) return -1;
     for (int r = 0; r < W; ++r) {
@@ -389,7 +389,7 @@ struct Oracle {
           if (!(R.in_flags[id] & F_VALID)) continue;
           uint64_t se = inst_members[id][0];  // SEND event decides the window and the warm-up flag
           if (win(se) != w) continue;
-          if (R.in_dmin[id] == 0) continue;  // non-positive latency: discarded (S:L333)
+          if (R.in_dmin[id] == 0) continue;  // non-positive latency: discarded (S:L352)
           S smp{R.in_payload[id], R.in_dmin[id], (uint32_t)id, (R.in_flags[id] & F_WARMUP) != 0};
           all.push_back(smp);
           if (smp.warm) warmv.push_back(smp);
@@ -429,7 +429,7 @@ struct Oracle {
         }
       }
 
-    // ---- verdicts (S:L341: ComputeSlow / LinkSlow / Both; candidates failing stage 2 exonerated) ----
+    // ---- verdicts (S:L360: ComputeSlow / LinkSlow / Both; candidates failing stage 2 exonerated) ----
     for (uint64_t w = 0; w < NW * W; ++w) {
       R.wl_late_frac[w] = R.wl_joined[w] ? (double)R.wl_late[w] / (double)R.wl_joined[w] : 0.0;
       int v = V_NONE;
@@ -516,10 +516,10 @@ struct Oracle {
   // same moment"; a reference rank; the others aligned to it "iteratively", anchors at the identified
   // instances; SPEC S:L243-300 ClockMap). Readings (AL1-AL6):
   //   AL1 anchors = ends (start + dur) of a rank's collective events (kinds 1-4) whose instance is
-  //       VALID; P2P excluded (S:L291)
+  //       VALID; P2P excluded (S:L294)
   //   AL2 "iteratively" = BFS levels from the reference over "shares a valid collective instance";
   //       level-k ranks use members of levels < k only (one level at a time)
-  //   AL3 target of an instance = the maximum aligned end over those members (S:L271); anchor =
+  //   AL3 target of an instance = the maximum aligned end over those members (S:L270); anchor =
   //       (local end, target - local end), in program order; an end equal to the previous
   //       anchor's is skipped; decreasing candidate ends on a rank -> status -9 (unsupported)
   //   AL4 offset(t): none -> 0; before the first / after the last anchor -> that anchor's offset;

@@ -209,7 +209,7 @@ EXPORTED_SYMBOLS = ["scan_create", "scan_destroy", "scan_last_error", "scan_load
 
 @dataclass
 class DetectConfig:
-    """Stage-1 thresholds (SPEC S:L294 defaults as exact rationals)."""
+    """Stage-1 thresholds (SPEC S:L313 defaults as exact rationals)."""
     slow_num: int = 3
     slow_den: int = 2
     slow_margin_ns: int = 50_000

@@ -715,7 +715,7 @@ __global__ void k_walk(WKArgs a) {
   const uint64_t items = (uint64_t)a.NW * a.W;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  // verdicts (S:L341) and rank roots
+  // verdicts (S:L360) and rank roots
   for (uint64_t it = t0; it < items; it += stride) {
     const uint32_t joined = a.wl_joined[it], late = a.wl_late[it];
     a.wl_frac[it] = joined ? (double)late / (double)joined : 0.0;

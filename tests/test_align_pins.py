@@ -18,7 +18,7 @@ def _with_start(tr, start):
 
 
 def test_spec_uniform_skew_one_allreduce():
-    """S:L283: two ranks, rank 1's clock uniformly +500 us ahead, one AllReduce -> offset -500 us."""
+    """S:L274: two ranks, rank 1's clock uniformly +500 us ahead, one AllReduce -> offset -500 us."""
     # true timeline: rank 0 computes 1000 ns, rank 1 1500 ns; the AllReduce ends for both at 3000 ns
     tr = tg.from_events(1, 1, 2, [[0, 1]], [[(C, 0, 1000), (AR, 0, 2000, 0)], [(C, 0, 1500), (AR, 0, 1500, 0)]])
     start = tr.start_ns.copy()
@@ -31,7 +31,7 @@ def test_spec_uniform_skew_one_allreduce():
 
 
 def test_spec_single_rank_zero_offset():
-    """S:L282: a single rank aligns to itself (zero offset, residual 0)."""
+    """S:L273: a single rank aligns to itself (zero offset, residual 0)."""
     tr = tg.from_events(1, 1, 1, [[0]], [[(C, 0, 10), (AR, 0, 5, 0), (C, 0, 7)]])
     o = oracle.align(_with_start(tr, tr.start_ns + 12345), 0)
     np.testing.assert_array_equal(o["al_start"], tr.start_ns + 12345)
@@ -39,7 +39,7 @@ def test_spec_single_rank_zero_offset():
 
 
 def test_unreached_rank_keeps_local_clock():
-    """S:L276 errors: a rank sharing no collective instance (P2P only, AL1) is not aligned."""
+    """S:L271 errors: a rank sharing no collective instance (P2P only, AL1) is not aligned."""
     tr = tg.from_events(1, 1, 2, [], [[(C, 0, 10), (SEND, 0, 5, 1, 64)], [(C, 0, 12), (RECV, 0, 3, 0, 64)]])
     start = tr.start_ns + np.array([0, 0, 999, 999])
     o = oracle.align(_with_start(tr, start), 0)

@@ -150,7 +150,7 @@ def test_bruteforce_unique_matching(seed):
 
 
 def test_truncated_trace_prefix_is_maximal():
-    """S:L181: unequal counts -> the oracle keeps the common prefix complete and reports the rest."""
+    """S:L200: unequal counts -> the oracle keeps the common prefix complete and reports the rest."""
     ranks = [[(AR, 0, 100, 0, 0, 0, 0)] * 3, [(AR, 0, 100, 0, 0, 0, 0)] * 2, [(AR, 0, 100, 0, 0, 0, 0)] * 3]
     tr = tg.from_events(3, 1, 1, [[0, 1, 2]], ranks)
     o = oracle.run(tr)
@@ -162,7 +162,7 @@ def test_truncated_trace_prefix_is_maximal():
 # ---------------------------------------------------------------- DES ground truth
 @pytest.mark.parametrize("seed", [1, 2, 3])
 def test_partition_equals_ground_truth(seed):
-    """S:L185/S:L645: matched instances equal the simulator's true instances exactly."""
+    """S:L204/S:L645: matched instances equal the simulator's true instances exactly."""
     tr = tiny_gen(seed=seed, tp=2, pp=4, dp=2, layers=2, mb=6, iters=3)
     o = oracle.run(tr)
     comm = (tr.kind_op & 7) != 0
@@ -231,14 +231,14 @@ def test_clock_skew_invariance():
 
 # ---------------------------------------------------------------- stage 1
 def test_stage1_dp1_empty():
-    """S:L317: dp_size == 1 -> empty stats."""
+    """S:L336: dp_size == 1 -> empty stats."""
     tr = dp_trace([[1000] * 20])
     o = oracle.run(tr)
     assert o["wd_total"].sum() == 0 and o["wd_cand"].sum() == 0
 
 
 def test_stage1_one_of_four_at_2x():
-    """S:L318: 4 DP peers, one rank's every kernel 2x median -> that rank's slow_fraction == 1.0."""
+    """S:L337: 4 DP peers, one rank's every kernel 2x median -> that rank's slow_fraction == 1.0."""
     base = [1_000_000 + 1000 * j for j in range(20)]
     durs = [base, base, [2 * x for x in base], base]
     o = oracle.run(dp_trace(durs, extra_comm=False))
@@ -259,7 +259,7 @@ def test_stage1_loo_median_closed_forms():
 
 
 def test_stage1_thresholds_exact():
-    """slow iff dur > 1.5 ref AND dur - ref > 50 us (S:L314), evaluated exactly at the edges."""
+    """slow iff dur > 1.5 ref AND dur - ref > 50 us (S:L333), evaluated exactly at the edges."""
     ref = 200_000
     o = oracle.run(dp_trace([[ref], [300_000], [300_001]], extra_comm=False))  # dp=3: refs = min(other two)
     # rank1: 300000 vs ref 200000 -> 1.5x exactly: not slow; rank2: 300001 -> slow
@@ -269,7 +269,7 @@ def test_stage1_thresholds_exact():
 
 
 def test_stage1_op_mismatch_common_prefix():
-    """S:L315 + reading R9: peers whose kernel sequences differ are compared on the common prefix."""
+    """S:L334 + reading R9: peers whose kernel sequences differ are compared on the common prefix."""
     ranks = [[(C, 1, 100), (C, 2, 100), (C, 3, 100)], [(C, 1, 100), (C, 5, 100), (C, 3, 100)]]
     tr = tg.from_events(1, 1, 2, [], ranks)
     o = oracle.run(tr)
@@ -278,7 +278,7 @@ def test_stage1_op_mismatch_common_prefix():
 
 
 def test_stage1_monotonicity():
-    """S:L350: increasing one event's duration never decreases its rank's slow count and never
+    """S:L369: increasing one event's duration never decreases its rank's slow count and never
     increases another rank's."""
     rng = np.random.default_rng(3)
     durs = [list(rng.integers(100_000, 200_000, 30)) for _ in range(5)]
@@ -295,7 +295,7 @@ def test_stage1_monotonicity():
 
 
 def test_stage1_downclock_unique_candidate():
-    """S:L319: topo(2,2,2), rank 5 downclocked x1.8 -> rank 5 is the unique candidate."""
+    """S:L338: topo(2,2,2), rank 5 downclocked x1.8 -> rank 5 is the unique candidate."""
     tr = tiny_gen(seed=2, tp=2, pp=2, dp=2, layers=4, mb=8, iters=3, faults=[tg.Fault(tg.THROTTLE, 5, factor=1.8)])
     o = oracle.run(tr)
     assert list(np.nonzero(o["wd_cand"])[0]) == [5]
@@ -325,7 +325,7 @@ def _tp_pair_trace(late_always: bool, n=20):
 
 
 def test_stage2_latest_in_all():
-    """S:L327: candidate latest in all 20 of its TP allreduces by > margin -> fraction 1.0, root cause."""
+    """S:L346: candidate latest in all 20 of its TP allreduces by > margin -> fraction 1.0, root cause."""
     o = oracle.run(_tp_pair_trace(True))
     assert o["wd_cand"][0] == 1
     assert o["wl_joined"][0] == 20 and o["wl_late"][0] == 20 and o["wl_late_frac"][0] == 1.0
@@ -333,14 +333,14 @@ def test_stage2_latest_in_all():
 
 
 def test_stage2_never_latest():
-    """S:L326: candidate never latest -> fraction 0, exonerated by this stage."""
+    """S:L345: candidate never latest -> fraction 0, exonerated by this stage."""
     o = oracle.run(_tp_pair_trace(False))
     assert o["wd_cand"][0] == 1 and o["wl_late"][0] == 0
     assert o["wl_verdict"][0] == V_EXON
 
 
 def test_stage2_insufficient():
-    """S:L324: candidate joins < min_samples collectives -> Insufficient, not exonerated."""
+    """S:L343: candidate joins < min_samples collectives -> Insufficient, not exonerated."""
     o = oracle.run(_tp_pair_trace(True, n=10), oracle.Config(min_samples=10))
     assert o["wd_cand"][0] == 1 and o["wl_joined"][0] == 10 and o["wl_verdict"][0] == V_COMPUTE
     o = oracle.run(_tp_pair_trace(True, n=10), oracle.Config(min_samples=11))
@@ -348,7 +348,7 @@ def test_stage2_insufficient():
 
 
 def test_stage2_downclock_fractions():
-    """S:L328: simulated downclock on rank 5 -> late_start_fraction(5) >= 0.7 while others < 0.3."""
+    """S:L347: simulated downclock on rank 5 -> late_start_fraction(5) >= 0.7 while others < 0.3."""
     tr = tg.generate(configs.c1(seed=3))
     o = oracle.run(tr)
     lf = o["wl_late_frac"]
@@ -358,7 +358,7 @@ def test_stage2_downclock_fractions():
 
 # ---------------------------------------------------------------- stage 3
 def test_stage3_degraded_link():
-    """S:L337: rank 2's egress link degraded x0.5 -> median warm-up bw on (2->3 stage) ~ 0.5x
+    """S:L356: rank 2's egress link degraded x0.5 -> median warm-up bw on (2->3 stage) ~ 0.5x
     median of the other links, within 10%; LinkSlow flagged on exactly that link."""
     # pp=4, tp=1, dp=1 -> ranks are stages; rank 1 -> rank 2 degraded (a forward link)
     cfg = tg.GenConfig(1, 4, 1, 2, 12, 4, seed=7, faults=[tg.Fault(tg.LINK_DEGRADE, 1, 2, factor=0.5)])
@@ -388,7 +388,7 @@ def test_stage3_warmup_rule():
             assert o["lk_used_warm"][i] == 0 and o["lk_n"][i] == 12 * 4
 
 
-# ---------------------------------------------------------------- diagnose (S:L344-346)
+# ---------------------------------------------------------------- diagnose (S:L363-365)
 @pytest.mark.parametrize("seed", [1, 2, 3, 4, 5])
 def test_healthy_no_root_causes(seed):
     tr = tiny_gen(seed=seed, tp=2, pp=4, dp=2, layers=2, mb=8, iters=3)
@@ -408,7 +408,7 @@ def test_single_downclock_exactly_that_rank(factor):
 
 
 def test_victim_exoneration_cascade():
-    """S:L351 + C5 shape: collateral slowdown of the source's TP peers makes them stage-1
+    """S:L370 + C5 shape: collateral slowdown of the source's TP peers makes them stage-1
     candidates; stage 2 must exonerate them (they are victims, not sources)."""
     src = 8 + 0
     peers = [9, 10, 11]
@@ -423,7 +423,7 @@ def test_victim_exoneration_cascade():
 
 
 def test_link_only():
-    """S:L346: injected link degrade only -> zero compute candidates, one LinkSlow rank."""
+    """S:L365: injected link degrade only -> zero compute candidates, one LinkSlow rank."""
     cfg = tg.GenConfig(2, 4, 2, 2, 8, 4, seed=5, faults=[tg.Fault(tg.LINK_DEGRADE, 4, 8, factor=0.5)])
     o = oracle.run(tg.generate(cfg))
     assert o["wd_cand"].sum() == 0

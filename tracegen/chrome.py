@@ -68,7 +68,7 @@ def rank_documents(trace, messy: bool = True, seed: int = 0) -> list[bytes]:
                              ("args", _obj([("name", _dumps_str(f"rank {r}"))], kv, it))], kv, it))
         b, e = int(ro[r]), int(ro[r + 1])
         order = list(range(b, e))
-        if messy:  # write some adjacent pairs out of time order (the parser sorts by ts, S:L136)
+        if messy:  # write some adjacent pairs out of time order (the parser sorts by ts, S:L135)
             j = 0
             while j + 1 < len(order):
                 if rng.random() < 0.05 and trace.start_ns[order[j]] != trace.start_ns[order[j + 1]]:

@@ -7,7 +7,7 @@
 // P:L105-114) with injectable faults ("GPU down-clocking or link jitter").
 //
 // Workload model:
-//  * rank = tp + TP*(dp + DP*pp)  (TP fastest, then DP, then PP; SPEC S:L81)
+//  * rank = tp + TP*(dp + DP*pp)  (TP fastest, then DP, then PP; SPEC S:L100)
 //  * non-interleaved 1F1B schedule with Megatron's grouped P2P
 //    (send_forward_recv_backward / send_backward_recv_forward).
 //  * per layer forward: qkv, attn, proj, TP-AR, fc1, fc2, TP-AR;
@@ -15,14 +15,14 @@
 //  * iteration end: L_s DP grad all-reduces, embedding-group AR (PP>1),
 //    model-parallel grad-norm AR, optimizer step (carries the iter_end bit).
 //  * collectives: all members wait for the latest arrival, then the
-//    collective's own duration (S:L407); every member's CUDA-event duration
+//    collective's own duration (S:L426); every member's CUDA-event duration
 //    is end - own arrival.  P2P pairs are rendezvous: both sides end at
 //    max(post) + transfer.  A rank resumes after all ops of its group end.
 //  * iterations are separated by a global barrier (the job-level
 //    optimizer/timer sync), so iterations simulate independently and in
 //    parallel; only start_ns depends on the previous iterations.
 //  * jitter: every duration x U[1-j, 1+j], counter-based RNG keyed by
-//    (seed, iteration, rank/comm/link, index)  (S:L408).
+//    (seed, iteration, rank/comm/link, index)  (S:L427).
 //  * faults: THROTTLE(rank, factor, [it0,it1), prob) scales compute ops;
 //    LINK_JITTER(src,dst,[it0,it1)) scales transfer by (1+Exp(1));
 //    LINK_DEGRADE(src,dst,factor,[it0,it1)) divides link bandwidth by factor.
