@@ -289,3 +289,16 @@ def test_c4_shape():
     and a half-bandwidth link; 3 iterations (4.8 M events)."""
     o, g = _run_both(tg.generate(configs.c4(iterations=3)), min_samples=5)
     compare(o, g)
+
+
+def test_round2_pin_traces():
+    """The hand-built traces of the round-2 oracle pins (kind mismatch; the pslow segment reset in
+    both stage-2 modes) through both GPU paths."""
+    import test_oracle_pins as pins
+    ag = tg.ALLGATHER
+    km = tg.from_events(2, 1, 1, [[0, 1]], [[(AR, 0, 700, 0), (AR, 0, 500, 0)], [(ag, 0, 400, 0), (AR, 0, 300, 0)]])
+    o, g = _run_both(km)
+    compare(o, g)
+    for mode in (0, 1):
+        o, g = _run_both(pins._segment_trace(), mode=mode)
+        compare(o, g)

@@ -514,3 +514,78 @@ def test_schema_errors():
     assert o["status"] == -2 and o["bad_event"] == 1  # rank 1 not a member of comm 0
     tr = tg.from_events(2, 1, 1, [], [[(SEND, 0, 1, 0)], []])
     assert oracle.run(tr)["status"] == -2  # peer == self
+
+
+# ---------------------------------------------------------------- round-2 pins: branches that only
+# GPU-vs-oracle parity checked before (kind mismatch, stage2_mode=1, the pslow segment reset)
+F_COMPLETE, F_KIND_OK, F_PAYLOAD_OK, F_VALID = 1, 2, 4, 8
+
+
+def test_kind_mismatch_is_reported_and_excluded():
+    """Reading R2 (occurrence counter per communicator) + S:L209 / S:L232: rank 0
+    posts an AllReduce where rank 1 posts an AllGather at occurrence 0 of the same communicator.
+    Hand-derived: two instances (k = 0, 1); k = 0 is complete but not kind-consistent, so it is
+    reported (n_kind_mismatch = 1, status PARTIAL) and excluded from the decomposition (no waits,
+    no transfer); k = 1 is a valid instance whose last arriver is rank 1 (duration 300 < 500)."""
+    ag = tg.ALLGATHER
+    ranks = [[(AR, 0, 700, 0), (AR, 0, 500, 0)],
+             [(ag, 0, 400, 0), (AR, 0, 300, 0)]]
+    o = oracle.run(tg.from_events(2, 1, 1, [[0, 1]], ranks))
+    assert o["n_instances"] == 2 and o["n_kind_mismatch"] == 1 and o["n_incomplete"] == 0
+    assert o["status"] == 1  # SCAN_PARTIAL: reported, never dropped (S:L232)
+    f0, f1 = int(o["in_flags"][0]), int(o["in_flags"][1])
+    assert f0 & F_COMPLETE and not f0 & F_KIND_OK and not f0 & F_VALID
+    assert f1 & F_COMPLETE and f1 & F_KIND_OK and f1 & F_VALID
+    assert list(o["ev_inst"]) == [0, 1, 0, 1]
+    # waits: instance 0 excluded (0, 0); instance 1: dmin = 300 -> rank 0 waits 200, rank 1 waits 0
+    assert list(o["ev_wait"]) == [0, 200, 0, 0]
+    assert int(o["in_dmin"][1]) == 300 and int(o["in_dmax"][1]) == 500 and int(o["in_last"][1]) == 1
+    assert list(o["rk_sum_wait"]) == [200, 0] and list(o["rk_sum_transfer"]) == [300, 300]
+
+
+def _segment_trace(reps=10):
+    """tp=2, pp=1, dp=2 (TP groups {0,1}, {2,3}; DP classes {0,2}, {1,3}). Rank 0 repeats three
+    segments, each two compute ops then a TP all-reduce:
+      A = [slow, fast, AR]  (slow op FIRST in the segment; rank 0 arrives last: late)
+      B = [fast, fast, AR]  (no slow op;                  rank 1 arrives last)
+      D = [fast, slow, AR]  (slow op LAST in the segment;  rank 0 arrives last: late)
+    slow = 2 ms vs the DP peer's 1 ms (2 x 2 > 3 x 1 and 1 ms > 50 us: slow); fast = 1 ms.
+    A late rank 0 has the shortest all-reduce duration (it arrived last, ends are simultaneous)."""
+    S, F = 2_000_000, 1_000_000
+    comms = [[0, 1], [2, 3]]
+    ranks = [[] for _ in range(4)]
+    for _ in range(reps):
+        for seg in ("A", "B", "D"):
+            c0 = {"A": (S, F), "B": (F, F), "D": (F, S)}[seg]
+            late0 = seg != "B"
+            ranks[0] += [(C, 1, c0[0]), (C, 2, c0[1]), (AR, 3, 150_000 if late0 else 160_000, 0)]
+            ranks[1] += [(C, 1, F), (C, 2, F), (AR, 3, 1_150_000 if late0 else 150_000, 0)]
+            for r in (2, 3):  # healthy TP group: equal durations, a tie -> nobody late (R20)
+                ranks[r] += [(C, 1, F), (C, 2, F), (AR, 3, 150_000, 1)]
+    return tg.from_events(2, 1, 2, comms, ranks)
+
+
+def test_pslow_is_the_segment_or_reset_at_each_comm_event():
+    """P:L149 "because its preceding computation is slower" (reading R11): pslow of a comm
+    event = OR of the slow bits of the rank's compute ops since its previous comm event. Hand count
+    over 10 x (A, B, D): stage 1 total 60, slow 20 (1/3 > 0.3: candidate). Stage 2 CONDITIONAL
+    joins the A and D all-reduces only: joined 20, late 20 -> 1.0 -> ComputeSlow. A sticky pslow
+    (no reset) would also join B (30 joined), and a last-op-only reading would miss A (10 joined)."""
+    o = oracle.run(_segment_trace())
+    assert o["wd_total"][0] == 60 and o["wd_slow"][0] == 20 and o["wd_cand"][0] == 1
+    assert o["wl_joined"][0] == 20 and o["wl_late"][0] == 20
+    assert o["wl_verdict"][0] == V_COMPUTE
+
+
+def test_stage2_unconditional_mode():
+    """S:L342 literal (stage2_mode = 1): every TP / DP instance a candidate joins counts, whatever
+    preceded it. On the same trace: joined 30, late 20 -> 0.667 < 0.7 -> Exonerated. The
+    CONDITIONAL default keeps the source (previous test)."""
+    o = oracle.run(_segment_trace(), oracle.Config(stage2_mode=1))
+    assert o["wd_cand"][0] == 1
+    assert o["wl_joined"][0] == 30 and o["wl_late"][0] == 20
+    assert abs(o["wl_late_frac"][0] - 20 / 30) < 1e-12
+    assert o["wl_verdict"][0] == V_EXON
+    # rank 1 (not a candidate) is the unique last arriver of the 10 B all-reduces, but its lag
+    # 160 - 150 = 10 us is below the 100 us late margin (S:L342): joined 30, late 0
+    assert o["wl_joined"][1] == 30 and o["wl_late"][1] == 0
