@@ -282,17 +282,54 @@ def scan_create_sharded(device: int, stream, n_shards: int, shard: int, unique_i
     return h
 
 
+# ABI width of every event column (scan.h scan_event_columns): the library copies / reads exactly
+# n_events * itemsize bytes per column, so a column of another width would be misread.
+COLUMN_DTYPES = {"dur_ns": np.uint32, "kind_op": np.uint16, "meta": np.uint16, "comm": np.uint32, "payload": np.uint32,
+                 "start_ns": np.int64}
+
+
+def _column(name: str, x, n: int, device: bool):
+    """Marshal one event column to the ABI width. Host arrays are converted (value-checked: a value that
+    does not fit the ABI width raises); device tensors must already have the width (any signedness of
+    that size), be contiguous and hold n elements, else ValueError (no silent copy on the device path)."""
+    if x is None:
+        return None
+    want = np.dtype(COLUMN_DTYPES[name])
+    if device:
+        if not hasattr(x, "data_ptr"):
+            raise ValueError(f"{name}: device_ptrs=True needs a CUDA tensor")
+        if x.element_size() != want.itemsize or not x.is_contiguous() or x.numel() != n:
+            raise ValueError(f"{name}: need a contiguous {want.itemsize}-byte-element tensor of {n} elements, got "
+                             f"{x.dtype} shape {tuple(x.shape)} contiguous={x.is_contiguous()}")
+        return x
+    a = np.asarray(x)
+    if a.shape != (n,):
+        raise ValueError(f"{name}: need shape ({n},), got {a.shape}")
+    if a.dtype != want:
+        if a.size and (a.dtype.kind not in "iub" or int(a.min()) < np.iinfo(want).min or int(a.max()) > np.iinfo(want).max):
+            raise ValueError(f"{name}: values of dtype {a.dtype} do not fit the ABI type {want}")
+        a = a.astype(want)
+    return np.ascontiguousarray(a)
+
+
 def scan_load_events(ctx, tp, pp, dp, rank_offsets, comm_offsets, comm_members, dur, kind_op, meta, comm, payload,
                      flags: int = SCAN_HOST_PTRS, keep: list | None = None, start_ns=None):
     lib = _load_lib()
     ro = np.ascontiguousarray(rank_offsets, dtype=np.uint64)
+    n = int(ro[-1]) if len(ro) else 0
+    dev = bool(flags & SCAN_DEVICE_PTRS)
+    dur, kind_op, meta, comm, payload, start_ns = (
+        _column(k, v, n, dev) for k, v in (("dur_ns", dur), ("kind_op", kind_op), ("meta", meta), ("comm", comm),
+                                           ("payload", payload), ("start_ns", start_ns)))
     co = np.ascontiguousarray(comm_offsets, dtype=np.uint64)
     cm = np.ascontiguousarray(comm_members, dtype=np.uint32)
     if keep is not None:
         keep += [ro, co, cm]
     topo = _Topo(tp, pp, dp, 0)
     comms = _Comms(len(co) - 1, co.ctypes.data, cm.ctypes.data if len(cm) else None)
-    cols = _Cols(int(ro[-1]), ro.ctypes.data, _ptr(start_ns), _ptr(dur), _ptr(kind_op), _ptr(meta), _ptr(comm), _ptr(payload))
+    if keep is not None:
+        keep += [dur, kind_op, meta, comm, payload, start_ns]
+    cols = _Cols(n, ro.ctypes.data, _ptr(start_ns), _ptr(dur), _ptr(kind_op), _ptr(meta), _ptr(comm), _ptr(payload))
     return _check(ctx, lib.scan_load_events(ctx, ctypes.byref(topo), ctypes.byref(comms), ctypes.byref(cols), flags))
 
 
@@ -470,8 +507,6 @@ class Scan:
         self._keep = [trace]
         names = ("dur_ns", "kind_op", "meta", "comm", "payload") + (("start_ns",) if start else ())
         c = cols or {k: getattr(trace, k) for k in names}
-        if not device_ptrs:
-            c = {k: np.ascontiguousarray(v) for k, v in c.items()}
         self._keep.append(c)
         flags = (SCAN_DEVICE_PTRS if device_ptrs else SCAN_HOST_PTRS) | (SCAN_STRICT if strict else 0)
         return scan_load_events(self.ctx, trace.tp, trace.pp, trace.dp, trace.rank_offsets, trace.comm_offsets,
@@ -547,8 +582,10 @@ class Scan:
     def stream_push(self, iteration, device_ptrs: bool = False, cols: dict | None = None) -> dict:
         """Push one whole iteration (a trace holding exactly one iteration of every rank)."""
         lib = _load_lib()
-        c = cols or {k: np.ascontiguousarray(getattr(iteration, k)) for k in ("dur_ns", "kind_op", "meta", "comm", "payload")}
         ro = np.ascontiguousarray(iteration.rank_offsets, dtype=np.uint64)
+        src = cols or {k: getattr(iteration, k) for k in ("dur_ns", "kind_op", "meta", "comm", "payload")}
+        c = {k: _column(k, v, int(ro[-1]), device_ptrs) for k, v in src.items()}
+        self._stream_cols = c  # alive until the call returns (the push copies them)
         cs = _Cols(int(ro[-1]), ro.ctypes.data, None, _ptr(c["dur_ns"]), _ptr(c["kind_op"]), _ptr(c["meta"]), _ptr(c["comm"]),
                    _ptr(c["payload"]))
         r = _LocRes()

@@ -34,7 +34,23 @@ def analyze(args) -> int:
                            "byte_offset": e.offset, "message": str(e)}
         print(json.dumps(report, indent=1))
         return 2
+    except ms.ScanError as e:  # the parsed job fails the load schema (e.g. a rank outside its group)
+        report["error"] = {"kind": "scan", "status": e.status, "message": str(e)}
+        print(json.dumps(report, indent=1))
+        return 2
     report["ingest"] = ing
+    try:
+        return _analyze_loaded(s, args, report)
+    except ms.ScanError as e:  # a rejected job (membership schema, capacity, alignment): exit 2 with the report
+        report["error"] = {"kind": "scan", "status": e.status, "message": str(e)}
+        print(json.dumps(report, indent=1, default=int))
+        return 2
+    finally:
+        s.close()
+
+
+def _analyze_loaded(s, args, report) -> int:
+    import paper_2507_19845_b200 as ms
     res = s.analyze(ms.DetectConfig(window_iters=args.window_iters), ms.LocalizeConfig())
     report["analysis"] = {"fused": bool(res.get("fused")), "match": res["match"], "detect": res["detect"],
                           "localize": res["localize"]}
@@ -64,7 +80,6 @@ def analyze(args) -> int:
         with open(args.emit, "wb") as f:
             f.write(doc)
         report["emitted"] = {"path": args.emit, "bytes": len(doc), "aligned": args.align_ref is not None}
-    s.close()
     print(json.dumps(report, indent=1, default=int))
     return 0
 

@@ -188,8 +188,8 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
   // comm table checks + stage-2 class per communicator (reading R12), rank -> comms CSR,
   // collective neighbour lists (for the wait-for edge arrays)
   const uint32_t nc = comms->n_comms;
-  std::vector<uint64_t> coff(comms->offsets, comms->offsets + (nc ? nc + 1 : 1));
-  if (!nc) coff[0] = 0;
+  // n_comms == 0 accepts offsets == NULL (nothing to read)
+  std::vector<uint64_t> coff = nc ? std::vector<uint64_t>(comms->offsets, comms->offsets + nc + 1) : std::vector<uint64_t>{0};
   if (coff[0] != 0) { c.err = "comm offsets must start at 0"; return SCAN_E_INVALID_ARG; }
   std::vector<uint32_t> cmem(comms->members, comms->members + coff[nc]);
   std::vector<uint8_t> ccls(nc, 0);

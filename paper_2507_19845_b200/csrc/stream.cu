@@ -169,14 +169,15 @@ extern "C" {
 scan_status scan_stream_open(scan_ctx* ctx, const scan_topology* topo, const scan_comm_table* comms, uint32_t window_iters,
                              const scan_detect_config* dcfg, const scan_localize_config* lcfg) {
   if (!ctx || !topo || !comms || window_iters == 0 || window_iters > 4096) return SCAN_E_INVALID_ARG;
+  if (comms->n_comms && (!comms->offsets || !comms->members)) return SCAN_E_INVALID_ARG;
   Ctx& c = ctx->c;
   if (c.n_shards > 1) { c.err = "streaming on a sharded context is not supported"; return SCAN_E_UNSUPPORTED; }
   stream_release(c);
   StreamState* S = new StreamState();
   c.stream_state = S;
   S->topo = *topo;
-  S->coff.assign(comms->offsets, comms->offsets + (comms->n_comms ? comms->n_comms + 1 : 1));
-  if (!comms->n_comms) S->coff.assign(1, 0);
+  if (comms->n_comms) S->coff.assign(comms->offsets, comms->offsets + comms->n_comms + 1);
+  else S->coff.assign(1, 0);  // n_comms == 0 accepts offsets == NULL
   S->cmem.assign(comms->members, comms->members + S->coff.back());
   S->K = window_iters;
   scan_status st = scan_create(&S->sub, c.device, c.stream);
