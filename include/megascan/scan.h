@@ -349,9 +349,11 @@ scan_status scan_analyze(scan_ctx* ctx, const scan_detect_config* dcfg, const sc
 int scan_used_fused(const scan_ctx* ctx);
 /* Disable (1) / re-enable (0) the fused path for this context (testing / comparison).          */
 scan_status scan_force_general(scan_ctx* ctx, int force);
-/* Fused-kernel variant for the next scan_load_events: -1 automatic (transposed warp-per-position
-   kernel when TP divides 32 and TP*DP <= 256, else the generic tile kernel), 0 generic, 1
-   transposed where applicable (testing / comparison).                                           */
+/* Fused-kernel variant for the next scan_load_events: -1 automatic (the persistent TMA-fed stage
+   kernel when TP divides 32, TP*DP <= 128 and every rank's first event index is a multiple of 4;
+   else the transposed warp-per-position kernel when TP divides 32 and TP*DP <= 256; else the
+   generic tile kernel), 0 generic, 1 transposed, 2 persistent where applicable (testing /
+   comparison).                                                                                  */
 scan_status scan_fused_variant(scan_ctx* ctx, int variant);
 
 /* ---- result export ------------------------------------------------------------------------ */

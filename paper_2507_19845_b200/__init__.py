@@ -597,7 +597,8 @@ class Scan:
         return out
 
     def fused_variant(self, variant: int):
-        """-1 automatic, 0 generic tile kernel, 1 transposed warp-per-position kernel (next load)."""
+        """-1 automatic, 0 generic tile kernel, 1 transposed warp-per-position kernel, 2 persistent TMA-fed
+        stage kernel (next load; falls back to the automatic choice where not applicable)."""
         _check(self.ctx, _load_lib().scan_fused_variant(self.ctx, variant))
 
     def force_general(self, on: bool = True):

@@ -7,6 +7,8 @@
 #include <sstream>
 #include "internal.cuh"
 
+#include <cstdlib>
+
 using namespace ms;
 
 void ms::resolve_timing(Ctx& c) {
@@ -161,7 +163,7 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
   CK(cudaSetDevice(c.device));
   c.loaded = c.matched = c.detected = c.localized = false;
   c.fused_used = false; c.tiles_ready = false; c.xwait_pending = false; c.aligned = false;
-  ++c.gen; c.blamed = false;
+  ++c.gen; ++c.load_id; c.blamed = false;
   if (c.stream_mode) { stream_release(c); c.stream_mode = false; }
   c.d_start = nullptr;
   c.err.clear();
@@ -338,6 +340,13 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
       };
       const size_t cap = c.fused_t ? fused_t_smem_cap() : 110u * 1024u;  // 2 (generic) / FT_MINB (transposed) CTAs per SM
       while (T > 32 && smem(T) > cap) T = T > 128 ? T - 32 : T / 2;  // below 128: powers of two (load lane mapping)
+      // the persistent TMA-fed kernel (k_stage.cu): 16-byte-aligned rank rows, R <= 128; its own tile size
+      c.use_stage = false;
+      const char* sge = std::getenv("MS_STAGE");  // experimental until it beats k_fused_t: variant 2 or MS_STAGE=1
+      if (aligned && c.fused_t && (c.fused_variant == 2 || (c.fused_variant == -1 && sge && std::atoi(sge) == 1))) {
+        const uint32_t Ts = stage_tile(R, (uint32_t)topo->tp, (uint32_t)topo->dp, ncrm, (uint32_t)topo->pp);
+        if (Ts) { c.use_stage = true; T = Ts; }
+      }
       c.NCRM = ncrm;
       if ((st = upload(c, c.eidx, eidx))) return st;
       uint32_t nt = 0;
@@ -632,7 +641,7 @@ scan_status ms::fused_rerun(Ctx& c) {
   for (auto& v : z.v_count) v = 0;
   CK(cudaMemcpyAsync(c.counters.p, &z, sizeof(Counters), cudaMemcpyHostToDevice, c.stream));
   c.launches += timed(c, "k_class_counts", [&] { return launch_class_counts(c); });
-  c.launches += timed(c, "k_fused", [&] { return launch_fused(c); });
+  c.launches += timed(c, stage_active(c) ? "k_stage" : "k_fused", [&] { return launch_fused(c); });
   c.launches += timed(c, "k_cross_reduce", [&] { return launch_cross_reduce(c); });
   c.launches += timed(c, "k_deferred", [&] { return launch_deferred(c); });
   if ((st = sync_read(c))) return st;
@@ -652,6 +661,7 @@ scan_status ms::fused_all(Ctx& c) {
   CK(c.st_tot.ensure((uint64_t)c.PP * FCOLS * 4));
   CK(c.ft_posA.ensure((uint64_t)c.n_ftiles * c.FT * 4)); CK(c.ft_posB.ensure((uint64_t)c.n_ftiles * c.FT * 4));
   CK(c.ft_posK.ensure((uint64_t)c.n_ftiles * c.FT * 2));
+  if (c.use_stage) CK(c.ft_tbase.ensure((uint64_t)c.n_ftiles * 40 * 4));
   c.launches += timed(c, "k_fused_prepass", [&] { return launch_fused_prepass(c); });
   c.launches += timed(c, "k_fused_census", [&] { return launch_fused_census(c); });
   c.launches += timed(c, "k_rank_prefix", [&] { return launch_rank_prefix(c); });
@@ -672,7 +682,7 @@ scan_status ms::fused_all(Ctx& c) {
     queue_fill(c, c.wd_slow.p, items * 4, 0);
   }
   c.launches += timed(c, "k_class_counts", [&] { return launch_class_counts(c); });
-  c.launches += timed(c, "k_fused", [&] { return launch_fused(c); });
+  c.launches += timed(c, stage_active(c) ? "k_stage" : "k_fused", [&] { return launch_fused(c); });
   c.launches += timed(c, "k_cross_reduce", [&] { return launch_cross_reduce(c); });
   c.launches += timed(c, "k_deferred", [&] { return launch_deferred(c); });
   if (c.partial_tail) {  // streaming: per-iteration partials only (stream.cu combines the window)
@@ -806,7 +816,7 @@ scan_status scan_align(scan_ctx* ctx, const scan_align_config* cfg, scan_align_r
 }
 
 scan_status scan_fused_variant(scan_ctx* ctx, int variant) {
-  if (!ctx || variant < -1 || variant > 1) return SCAN_E_INVALID_ARG;
+  if (!ctx || variant < -1 || variant > 2) return SCAN_E_INVALID_ARG;
   ctx->c.fused_variant = variant;
   return SCAN_OK;
 }

@@ -146,7 +146,12 @@ struct Ctx {
   bool rows_aligned = false, rows_aligned8 = false;
   bool force_general = false;
   bool fused_t = false;                  // transposed fused kernel (TP divides 32, R <= 256)
-  int fused_variant = -1;                // testing: -1 auto, 0 generic fused, 1 transposed
+  bool use_stage = false;                // persistent TMA-fed fused kernel (k_stage.cu): aligned rows, R <= 128
+  DevBuf ft_tbase;                       // [n_ftiles][40] tile-major bases / counts / stage (k_stage)
+  DevBuf tmaps;                          // [PP][3] CUtensorMap (dur, comm, kind) of k_stage, built on first use per load
+  uint64_t load_id = 0, tmap_load = ~0ull; // scan_load_events counter; load the maps were built for
+  bool kind2d = false;                   // kind rows of every stage 16-byte aligned with a 16-byte stride (2-D TMA)
+  int fused_variant = -1;                // testing: -1 auto, 0 generic fused, 1 transposed, 2 persistent (k_stage)
   uint32_t NCRM = 1;                     // max collective roles of a rank over the stages
   DevBuf eidx;                           // [W][TP+DP] edge slot of each TP-/DP-group partner
   DevBuf tile_stage;                     // [n_ftiles] stage of each fused tile (u8)
@@ -403,6 +408,10 @@ int launch_instance_export(Ctx& c, scan_output which, void* dst);
 int launch_fused_prepass(Ctx& c);
 int launch_fused_census(Ctx& c);
 int launch_fused(Ctx& c);
+int launch_stage(Ctx& c);
+// the analysis runs k_stage: selected at load and the channel bases fit its 32-bit tables
+inline bool stage_active(const Ctx& c) { return c.use_stage && c.n_inst < (1ull << 32) && c.n_slots < (1ull << 32); }
+uint32_t stage_tile(uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM, uint32_t PP);
 size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM);
 size_t fused_t_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM);
 size_t fused_t_smem_cap();

@@ -127,8 +127,10 @@ __global__ void __launch_bounds__(256) k_fused_prepass(PreArgs a) {
 // F0b: per (stage, column) exclusive scans over the stage's tiles; stage totals. The compute
 // column also yields jprev (compute index of the last comm event before the tile).
 constexpr int SC_NT = 1024;
+// tb (optional): the same bases tile-major, [tile][40] = FCOLS bases, comm count, compute count, stage
+// (one 160-byte record per tile, bulk-copied by k_stage)
 __global__ void __launch_bounds__(SC_NT) k_fused_scan(uint32_t n_ftiles, const uint32_t* st_tile0, const uint32_t* cols,
-                                                      uint32_t* base, uint32_t* st_tot) {
+                                                      uint32_t* base, uint32_t* st_tot, uint32_t* tb) {
   __shared__ uint32_t sm[33];
   __shared__ int32_t smi[33];
   const uint32_t s = blockIdx.x, col = blockIdx.y;
@@ -143,6 +145,11 @@ __global__ void __launch_bounds__(SC_NT) k_fused_scan(uint32_t n_ftiles, const u
   int32_t jl = -1;
   for (uint32_t t = a0; t < a1; ++t) {
     base[(uint64_t)col * n + t] = ex;
+    if (tb) {
+      tb[(uint64_t)t * 40 + col] = ex;
+      if (col == ROLES) { tb[(uint64_t)t * 40 + FCOLS + 1] = cols[(uint64_t)ROLES * n + t]; tb[(uint64_t)t * 40 + FCOLS + 2] = s; }
+      if (col == ROLES + 1) tb[(uint64_t)t * 40 + FCOLS] = cols[(uint64_t)(ROLES + 1) * n + t];
+    }
     if (col == ROLES) {  // compute column: last comm j of this tile = j0 + cc_last
       const uint32_t cc = cols[(uint64_t)(ROLES + 3) * n + t];
       if (cc != NONE32) jl = max(jl, (int32_t)(ex + cc));
@@ -157,6 +164,7 @@ __global__ void __launch_bounds__(SC_NT) k_fused_scan(uint32_t n_ftiles, const u
     int32_t run = exj;
     for (uint32_t t = a0; t < a1; ++t) {
       base[(uint64_t)(ROLES + 3) * n + t] = (uint32_t)max(0, run);
+      if (tb) tb[(uint64_t)t * 40 + ROLES + 3] = (uint32_t)max(0, run);
       const uint32_t cc = cols[(uint64_t)(ROLES + 3) * n + t];
       if (cc != NONE32) run = max(run, (int32_t)(base[(uint64_t)ROLES * n + t] + cc));
     }
@@ -170,7 +178,8 @@ int launch_fused_prepass(Ctx& c) {
             c.counters.as<Counters>()};
   k_fused_prepass<<<(c.n_ftiles + 7) / 8, 256, 0, c.stream>>>(a);
   k_fused_scan<<<dim3(c.PP, ROLES + 3), SC_NT, 0, c.stream>>>(c.n_ftiles, c.st_tile0.as<uint32_t>(), c.ft_cols.as<uint32_t>(),
-                                                              c.ft_base.as<uint32_t>(), c.st_tot.as<uint32_t>());
+                                                              c.ft_base.as<uint32_t>(), c.st_tot.as<uint32_t>(),
+                                                              c.use_stage ? c.ft_tbase.as<uint32_t>() : nullptr);
   return 2;
 }
 
@@ -1384,6 +1393,11 @@ size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32
 }
 
 int launch_fused(Ctx& c) {
+  if (stage_active(c)) {  // the persistent TMA-fed kernel (k_stage.cu)
+    const int n = launch_stage(c);
+    if (n >= 0) return n;
+    c.use_stage = false;  // no tensor maps (driver entry point): the transposed kernel, same tile size
+  }
   FusedArgs a;
   a.dur = c.d_dur; a.kind = c.d_kind; a.meta = c.d_meta; a.comm = c.d_comm; a.pay = c.d_pay;
   a.rank_off = c.rank_off.as<uint64_t>(); a.TP = c.TP; a.DP = c.DP; a.PP = c.PP; a.W = c.W; a.n_comms = c.n_comms;
@@ -1488,6 +1502,10 @@ struct XArgs {
   int xb_smem;                // xbase staged in shared memory (NCH + 1 entries)
   const uint64_t* xe_off;     // [n_comms] offset of a cross collective's member x member edge-column table, ~0 = none
   const uint32_t* xe_col;     // table[q * nm + t]: edge column of member q waiting on member t
+  // k_stage leaves each P2P member's position within its rank in p2p_pay: gather the payload and the
+  // sender's warm-up bit here (latency-tolerant grid) instead of between the fused kernel's barriers
+  int p2p_pos; const uint32_t* pay; const uint16_t* meta; const uint64_t* rank_off;
+  uint32_t* p2p_pay_w; uint8_t* p2p_warm_w;
 };
 
 constexpr uint32_t XBIG = 32;  // cross collectives with more members go to k_cross_big
@@ -1559,6 +1577,14 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
     };
     uint32_t flags = 0, dmin = 0, dmax = 0, last = NONE32, lsi = 0;
     bool valid = false;
+    if (act && isp && a.p2p_pos) {
+      for (uint32_t q = 0; q < 2; ++q) {
+        if (!(k < a.ch_nmin[ch] || present(q))) continue;
+        const uint64_t e = a.rank_off[member(q)] + a.p2p_pay[sb + q - a.p2p_slot0];
+        a.p2p_pay_w[sb + q - a.p2p_slot0] = a.pay[e];
+        if (q == 0) a.p2p_warm_w[i - a.p2p_inst0] = (uint8_t)((a.meta[e] >> 14) & 1u);
+      }
+    }
     if (act) {
       if (isp && a.p2p_warm[i - a.p2p_inst0]) flags |= SCAN_F_WARMUP;
       if (k < a.ch_nmin[ch]) {
@@ -1667,7 +1693,8 @@ int launch_cross_reduce(Ctx& c) {
           c.sdur.as<uint32_t>(), c.nbc_off.as<uint64_t>(), c.nbc.as<uint32_t>(), c.nbp.as<uint32_t>(), c.nbp_n.as<uint32_t>(),
           c.nnz_c + (uint64_t)c.W * PCAP, c.nnz_c, c.ewc.as<unsigned long long>(), c.rk_sum.as<unsigned long long>(),
           c.dcfg.window_iters, (unsigned long long)c.lcfg.wait_margin_ns, c.counters.as<Counters>(),
-          c.p2p_eslot.as<uint32_t>(), 0, c.xe_off.as<uint64_t>(), c.xe_col.as<uint32_t>()};
+          c.p2p_eslot.as<uint32_t>(), 0, c.xe_off.as<uint64_t>(), c.xe_col.as<uint32_t>(),
+          stage_active(c) ? 1 : 0, c.d_pay, c.d_meta, c.rank_off.as<uint64_t>(), c.p2p_pay.as<uint32_t>(), c.p2p_warm.as<uint8_t>()};
   if (c.n_xinst == 0) return 0;
   int n = 0;
   if (c.n_p2p) {
@@ -1845,7 +1872,7 @@ __global__ void k_deferred(uint32_t n_ftiles, int PP, uint32_t R, int W, const u
 }
 
 int launch_deferred(Ctx& c) {
-  if (c.lcfg.stage2_mode != 0) return 0;
+  if (c.lcfg.stage2_mode != 0 || stage_active(c)) return 0;  // k_stage carries the segments itself
   const uint64_t items = (uint64_t)c.n_ftiles * c.FR;
   k_deferred<<<(unsigned)((items + 255) / 256), 256, 0, c.stream>>>(
       c.n_ftiles, c.PP, c.FR, c.W, c.st_tile0.as<uint32_t>(), c.dinfo.as<uint32_t>(), c.dlate.as<uint32_t>(),

@@ -336,6 +336,7 @@ scan_status sharded_all(Ctx& c) {
     CK(c.ft_cols.ensure((uint64_t)FCOLS * c.n_ftiles * 4)); CK(c.ft_base.ensure((uint64_t)FCOLS * c.n_ftiles * 4));
     CK(c.st_tot.ensure((uint64_t)c.PP * FCOLS * 4));
     CK(c.ft_posA.ensure((uint64_t)c.n_ftiles * c.FT * 4)); CK(c.ft_posB.ensure((uint64_t)c.n_ftiles * c.FT * 4));
+    if (c.use_stage) CK(c.ft_tbase.ensure((uint64_t)c.n_ftiles * 40 * 4));
     CK(c.ft_posK.ensure((uint64_t)c.n_ftiles * c.FT * 2));
     c.launches += timed(c, "k_fused_prepass", [&] { return launch_fused_prepass(c); });
     c.launches += timed(c, "k_fused_census", [&] { return launch_fused_census(c); });
@@ -534,7 +535,7 @@ scan_status sharded_all(Ctx& c) {
   queue_fill(c, c.wd_slow.p, items * 4, 0);
   mark("tables");
   c.launches += timed(c, "k_class_counts", [&] { return launch_class_counts(c); });
-  c.launches += timed(c, "k_fused", [&] { return launch_fused(c); });
+  c.launches += timed(c, stage_active(c) ? "k_stage" : "k_fused", [&] { return launch_fused(c); });
   c.launches += timed(c, "k_cross_reduce", [&] { return launch_cross_reduce(c); });
   c.launches += timed(c, "k_deferred", [&] { return launch_deferred(c); });
   // ---- X3: P2P instance records to the owner of their link (pid % G)
