@@ -32,14 +32,15 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 #include <cstdio>
 
 namespace ms {
 
-constexpr int SG_NCW = 16;                // warps (16 x 32 threads: 128 registers per thread)
-constexpr int SG_NT = 32 * SG_NCW;        // the warp that finishes a tile last issues that slot's next loads
+constexpr int SG_NCW = 15;                // consumer warps (+1 producer = 16 warps: 128 registers per thread)
+constexpr int SG_NT = 32 * (SG_NCW + 1);  // + one producer warp (TMA issue)
 constexpr int SG_NS = 2;                  // ring stages
 constexpr uint32_t SG_NPR = 4;            // P2P roles per stage with a cached channel table
 constexpr uint32_t SG_TBW = 40;           // words of the tile-major record (k_fused_scan)
@@ -123,6 +124,14 @@ struct StageArgs {
 };
 
 namespace {
+
+// F(integral_constant<int, 0>) ... F(integral_constant<int, N-1>): compile-time indices into register arrays
+template <int I, int N, class F>
+__device__ __forceinline__ void static_for_i(F&& f) {
+  if constexpr (I < N) { f(std::integral_constant<int, I>{}); static_for_i<I + 1, N>(f); }
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) { static_for_i<0, N>(f); }
 
 __device__ __forceinline__ uint32_t sg_win(const StageArgs& a, uint32_t it) {
   return a.wi == 0 ? 0u : (a.wi == 1 ? it : (uint32_t)__umul64hi((unsigned long long)it, a.wi_m));
@@ -290,9 +299,8 @@ __global__ void __launch_bounds__(SG_NT, 1) k_stage(const __grid_constant__ Stag
   const uint32_t bar0 = smem_u32(sm + a.o_bar);  // full[s] at bar0 + 8s, empty[s] at bar0 + 8(NS + s)
   uint32_t* st_tab = reinterpret_cast<uint32_t*>(sm + a.o_st);  // [PP+1] st_tile0, then [PP] st_npos
   uint64_t* st_rb = reinterpret_cast<uint64_t*>(sm + a.o_strb);   // [PP] first event of each stage block
-  uint32_t* rel = reinterpret_cast<uint32_t*>(sm + a.o_rel);  // [NS] warps done with the slot's tile
   if (tid == 0) {
-    for (int s = 0; s < SG_NS; ++s) { mbar_init(bar0 + 8 * s, 32); rel[s] = 0; }
+    for (int s = 0; s < SG_NS; ++s) { mbar_init(bar0 + 8 * s, 32); mbar_init(bar0 + 8 * (SG_NS + s), SG_NCW); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int s = 0; s < SG_NS; ++s) {  // per-stage slow bits and flags start clear (then kept clear after each use)
@@ -363,8 +371,14 @@ __global__ void __launch_bounds__(SG_NT, 1) k_stage(const __grid_constant__ Stag
     }
     mbar_arrive(bar);
   };
-  if (wid == 0) {
-    for (uint32_t q = 0; q < SG_NS && t_begin + q < t_end; ++q) issue(t_begin + q, q);
+  // =========================================================================== producer warp
+  if (wid == SG_NCW) {
+    for (uint32_t t = t_begin, i = 0; t < t_end; ++t, ++i) {
+      const uint32_t s = i % SG_NS, use = i / SG_NS;
+      if (use) mbar_wait(bar0 + 8 * (SG_NS + s), (use - 1) & 1u);  // the consumers released this slot
+      issue(t, s);
+    }
+    return;
   }
 
   // =========================================================================== consumer warps
@@ -583,13 +597,17 @@ __global__ void __launch_bounds__(SG_NT, 1) k_stage(const __grid_constant__ Stag
         if (a.exp & 1u) need = 0;
         if (need) {
           // transposed full stage 1 (rare): lane task (q, g) sorts the DP group g at position pbase + q in
-          // registers (16-byte rows of one swizzle chunk: the DP values of 4 positions x TP groups are
-          // conflict-free), then decides every member of the group
-#pragma unroll 1
-          for (uint32_t task = lane; task < 4 * TP; task += 32) {
+          // registers (the DP values of 4 positions x TP groups sit in distinct banks), then decides every
+          // member of the group; the slow decisions are gathered by ballots, one shared-memory update per
+          // (row, micro-tile) by lane 0
+          uint32_t wmask = 0;  // positions of the micro-tile in the tile's window (their counts go to slowc)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) wmask |= (sg_win(a, itg0 + (Bq[q] & 1023u)) == w_edge) ? (1u << q) : 0u;
+          for (uint32_t tb0 = 0; tb0 < 4 * TP; tb0 += 32) {
+            const uint32_t task = tb0 + lane;
             const uint32_t q = task / TP, g = task - q * TP;
-            if (!((need >> q) & 1u)) continue;
-            const uint32_t p = pbase + q;
+            const bool act = task < 4 * TP && ((need >> q) & 1u);
+            const uint32_t p = pbase + (q & 3u);
             const uint32_t pwp = pw(p);
             const int qm = ((int)DP - 2) / 2;
             const int L = P / 2 - 1 - qm;
@@ -597,7 +615,7 @@ __global__ void __launch_bounds__(SG_NT, 1) k_stage(const __grid_constant__ Stag
 #pragma unroll
             for (int d = 0; d < P; ++d) {
               const uint32_t row = g + TP * (uint32_t)d;
-              v[d] = d < (int)DP ? dur_s[(pwp ^ ((row & 7u) << 2)) + row * 32u] : (d < (int)DP + L ? 0u : 0xFFFFFFFFu);
+              v[d] = (act && d < (int)DP) ? dur_s[(pwp ^ ((row & 7u) << 2)) + row * 32u] : (d < (int)DP + L ? 0u : 0xFFFFFFFFu);
             }
 #pragma unroll
             for (int kk = 2; kk <= P; kk <<= 1)
@@ -613,22 +631,39 @@ __global__ void __launch_bounds__(SG_NT, 1) k_stage(const __grid_constant__ Stag
                   }
                 }
             const uint32_t va = v[P / 2 - 1], vb = v[P / 2];
-            const uint32_t j = j0 + (Aq[q] & 1023u);
-            const uint32_t wq = sg_win(a, itg0 + (Bq[q] & 1023u));
+            const uint32_t q3 = q & 3u;  // selects, not an indexed (local-memory) array
+            const uint32_t Asel = q3 == 0 ? Aq[0] : (q3 == 1 ? Aq[1] : (q3 == 2 ? Aq[2] : Aq[3]));
+            const uint32_t j = j0 + (Asel & 1023u);
 #pragma unroll 1
-            for (int d = 0; d < (int)DP; ++d) {
-              const uint32_t row = g + TP * (uint32_t)d, r = sbase + row;
-              const uint32_t x = dur_s[(pwp ^ ((row & 7u) << 2)) + row * 32u];
-              const uint32_t ref = x > va ? va : vb;
-              const unsigned long long du = x;
-              if (a.want_ref) a.cref[a.comp_off[r] + j] = ref;
-              if (!(a.exp & 2u) && (unsigned long long)a.slow_den * du > (unsigned long long)a.slow_num * ref && du > (unsigned long long)ref + a.slow_margin) {
-                // the tile's bit (global bit words are written once per word at the tile's end); the count in
-                // shared memory for the tile's window (another window's position: straight to global)
-                if (!(a.exp & 128u)) {
-                  atomicOr(&sbits[row * a.SWD + (p >> 5)], 1u << (p & 31));
-                  if (wq == w_edge) atomicAdd(&slowc[row], 1u);
-                  else atomicAdd(&a.wd_slow[(uint64_t)wq * a.W + r], 1u);
+            for (uint32_t d = 0; d < DP; ++d) {
+              const uint32_t row = g + TP * d;
+              bool sl = false;
+              if (act) {
+                const uint32_t x = dur_s[(pwp ^ ((row & 7u) << 2)) + row * 32u];
+                const uint32_t ref = x > va ? va : vb;
+                const unsigned long long du = x;
+                if (a.want_ref) a.cref[a.comp_off[sbase + row] + j] = ref;
+                sl = !(a.exp & 2u) && (unsigned long long)a.slow_den * du > (unsigned long long)a.slow_num * ref &&
+                     du > (unsigned long long)ref + a.slow_margin;
+              }
+              uint32_t b = __ballot_sync(0xFFFFFFFFu, sl);
+              while (b) {  // one group g (one row) at a time: its slow positions of the micro-tile as a nibble
+                const uint32_t l0 = (uint32_t)(__ffs(b) - 1), t0 = tb0 + l0;
+                const uint32_t g0 = t0 - (t0 / TP) * TP, row0 = g0 + TP * d;
+                uint32_t nib = 0;
+#pragma unroll
+                for (uint32_t q2 = 0; q2 < 4; ++q2) {
+                  const int l2 = (int)(q2 * TP + g0) - (int)tb0;
+                  if (l2 >= 0 && l2 < 32 && ((b >> l2) & 1u)) { nib |= 1u << q2; b &= ~(1u << l2); }
+                }
+                if (lane == 0 && !(a.exp & 128u)) {
+                  atomicOr(&sbits[row0 * a.SWD + (pbase >> 5)], nib << (pbase & 31u));
+                  if (nib & wmask) atomicAdd(&slowc[row0], (uint32_t)__popc(nib & wmask));
+                  for (uint32_t m2 = nib & ~wmask; m2; m2 &= m2 - 1) {
+                    const uint32_t q2 = (uint32_t)(__ffs(m2) - 1);
+                    const uint32_t Bsel = q2 == 0 ? Bq[0] : (q2 == 1 ? Bq[1] : (q2 == 2 ? Bq[2] : Bq[3]));
+                    atomicAdd(&a.wd_slow[(uint64_t)sg_win(a, itg0 + (Bsel & 1023u)) * a.W + sbase + row0], 1u);
+                  }
                 }
                 tslow = true;
               }
@@ -736,7 +771,8 @@ __global__ void __launch_bounds__(SG_NT, 1) k_stage(const __grid_constant__ Stag
       const bool trans = istp ? TP > 1 : DP > 1;  // group size 1: no transfer (as k_fused_t)
       const int prevp = j ? (int)(cpos[j - 1] & 0xFFFu) : -1;  // previous comm position of this tile
       // one member: instance record (group leader), wait staged for the flush, sums, edge, stage 2
-      auto apply = [&](int k, uint32_t mn, uint32_t mx, uint32_t lastrow, uint32_t nat, uint32_t slot, bool lead) {
+      auto apply = [&](auto KC, uint32_t mn, uint32_t mx, uint32_t lastrow, uint32_t nat, uint32_t slot, bool lead) {
+        constexpr int k = decltype(KC)::value;  // compile-time row block: the register arrays stay registers
         const uint32_t row = lane + 32u * k;
         const uint32_t inst = base[k] + kinst;
         const bool islast = row == lastrow;
@@ -766,19 +802,27 @@ __global__ void __launch_bounds__(SG_NT, 1) k_stage(const __grid_constant__ Stag
         if (islast && nat == 1 && (unsigned long long)(mx - mn) > a.late_margin) ++acc.late[k];
       };
       if (istp) {
-        const uint32_t gm = gmt;
+        // the NRB TP reductions interleaved (independent shuffle chains), then the members
+        uint32_t mnv[NRB], mxv[NRB];
 #pragma unroll
         for (int k = 0; k < NRB; ++k) {
           const bool valid = (vmask >> k) & 1u;
-          uint32_t mn = valid ? d[k] : 0xFFFFFFFFu, mx = valid ? d[k] : 0u;
-          for (uint32_t m = 1; m < TP; m <<= 1) {
-            mn = min(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, m));
-            mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, m));
-          }
-          const unsigned eq = __ballot_sync(0xFFFFFFFFu, valid && d[k] == mn) & gm;
-          const uint32_t ls = eq ? (uint32_t)(__ffs(eq) - 1) : 0u;
-          if (valid) apply(k, mn, mx, ls + 32u * k, __popc(eq), ls & (TP - 1u), tp == 0);
+          mnv[k] = valid ? d[k] : 0xFFFFFFFFu; mxv[k] = valid ? d[k] : 0u;
         }
+        for (uint32_t m = 1; m < TP; m <<= 1)
+#pragma unroll
+          for (int k = 0; k < NRB; ++k) {
+            mnv[k] = min(mnv[k], __shfl_xor_sync(0xFFFFFFFFu, mnv[k], m));
+            mxv[k] = max(mxv[k], __shfl_xor_sync(0xFFFFFFFFu, mxv[k], m));
+          }
+        unsigned eqv[NRB];
+#pragma unroll
+        for (int k = 0; k < NRB; ++k) eqv[k] = __ballot_sync(0xFFFFFFFFu, ((vmask >> k) & 1u) && d[k] == mnv[k]) & gmt;
+        static_for<NRB>([&](auto KC) {
+          constexpr int k = decltype(KC)::value;
+          const uint32_t ls = eqv[k] ? (uint32_t)(__ffs(eqv[k]) - 1) : 0u;
+          if ((vmask >> k) & 1u) apply(KC, mnv[k], mxv[k], ls + 32u * k, __popc(eqv[k]), ls & (TP - 1u), tp == 0);
+        });
       } else {
         uint32_t mn = 0xFFFFFFFFu, mx = 0;
 #pragma unroll
@@ -796,9 +840,10 @@ __global__ void __launch_bounds__(SG_NT, 1) k_stage(const __grid_constant__ Stag
           lsd = min(lsd, __shfl_xor_sync(0xFFFFFFFFu, lsd, m));
           nat += __shfl_xor_sync(0xFFFFFFFFu, nat, m);
         }
-#pragma unroll
-        for (int k = 0; k < NRB; ++k)
-          if ((vmask >> k) & 1u) apply(k, mn, mx, tp + (lsd << tpsh), nat, TP + lsd, lane + 32u * k < TP);
+        static_for<NRB>([&](auto KC) {
+          constexpr int k = decltype(KC)::value;
+          if ((vmask >> k) & 1u) apply(KC, mn, mx, tp + (lsd << tpsh), nat, TP + lsd, lane + 32u * k < TP);
+        });
       }
     }
     SG_T(4);
@@ -813,27 +858,37 @@ __global__ void __launch_bounds__(SG_NT, 1) k_stage(const __grid_constant__ Stag
       const bool tbits = ctl[0] != 0;
       const uint32_t lastp = cT ? (cpos[cT - 1] & 0xFFFu) : 0u;
       bool any = false;
+      if (tbits && !(a.exp & 8u)) {
+        // slow bits of the tile -> the global per-rank bit words (by compute index): lanes over positions,
+        // one OR-reduction and one atomic per touched word, for each row holding a slow bit
+#pragma unroll
+        for (int k = 0; k < NRB; ++k) {
+          bool has = false;
+          if ((vmask >> k) & 1u)
+            for (uint32_t w = 0; w < a.SWD; ++w) has |= sbits[(lane + 32u * k) * a.SWD + w] != 0;
+          for (uint32_t hm = __ballot_sync(0xFFFFFFFFu, has); hm; hm &= hm - 1) {
+            const uint32_t row = 32u * k + (uint32_t)(__ffs(hm) - 1);
+            uint32_t* gb = a.bits + boff[row];
+            for (uint32_t c0 = 0; c0 < np; c0 += 32) {
+              const uint32_t pp = c0 + lane;
+              const bool bit = pp < np && ((sbits[row * a.SWD + (pp >> 5)] >> (pp & 31u)) & 1u);
+              const uint32_t jj = j0 + (pp < np ? (pa[pp] & 1023u) : 0u);
+              const uint32_t wlo = __reduce_min_sync(0xFFFFFFFFu, bit ? (jj >> 5) : 0xFFFFFFFFu);
+              if (wlo == 0xFFFFFFFFu) continue;
+              const uint32_t whi = __reduce_max_sync(0xFFFFFFFFu, bit ? (jj >> 5) : 0u);
+              for (uint32_t w = wlo; w <= whi; ++w) {
+                const uint32_t v = __reduce_or_sync(0xFFFFFFFFu, (bit && (jj >> 5) == w) ? (1u << (jj & 31u)) : 0u);
+                if (v && lane == 0) atomicOr(gb + w, v);
+              }
+            }
+          }
+        }
+      }
 #pragma unroll
       for (int k = 0; k < NRB; ++k) {
         const uint32_t row = lane + 32u * k;
         if (!((vmask >> k) & 1u)) continue;
         uint32_t* rb = sbits + row * a.SWD;
-        if (tbits && !(a.exp & 8u)) {
-          uint32_t cw = 0xFFFFFFFFu, cm = 0;
-          uint32_t* gb = nullptr;
-          for (uint32_t w = 0; w < a.SWD; ++w)
-            for (uint32_t m = rb[w]; m; m &= m - 1) {
-              const uint32_t pp = 32u * w + (uint32_t)(__ffs(m) - 1);
-              const uint32_t jj = j0 + (pa[pp] & 1023u);
-              if ((jj >> 5) != cw) {
-                if (cm) atomicOr(gb + cw, cm);
-                if (!gb) gb = a.bits + boff[row];
-                cw = jj >> 5; cm = 0;
-              }
-              cm |= 1u << (jj & 31);
-            }
-          if (cm) atomicOr(gb + cw, cm);
-        }
         if (a.mode == 0 && !(a.exp & 16u)) {
           const bool f = cT ? seg_any(rb, lastp + 1, np) : (cflag[row] != 0 || seg_any(rb, 0, np));
           cflag[row] = f ? 1u : 0u;
@@ -861,19 +916,9 @@ __global__ void __launch_bounds__(SG_NT, 1) k_stage(const __grid_constant__ Stag
         if ((cv >> 12) < 2) a.wait_c[o] = dur_s[off];
       }
     }
-    // release the slot: the last warp to finish this tile issues the slot's next tile (the other warps'
-    // reads and staged writes are ordered before its TMA by the block fences around the counter)
-    __threadfence_block();
+    fence_proxy_async();  // generic-proxy accesses of the slot before the next TMA overwrites it
     __syncwarp();
-    uint32_t old = 0;
-    if (lane == 0) old = atomicAdd(&rel[s], 1u);
-    old = __shfl_sync(0xFFFFFFFFu, old, 0);
-    if (old == SG_NCW - 1) {
-      if (lane == 0) rel[s] = 0;
-      __threadfence_block();
-      fence_proxy_async();  // generic-proxy accesses of the slot before the async-proxy TMA writes
-      if (t + SG_NS < t_end) issue(t + SG_NS, s);
-    }
+    if (lane == 0) mbar_arrive(bar0 + 8 * (SG_NS + s));
   }
   // ---- end of the range
   SG_T(7);
