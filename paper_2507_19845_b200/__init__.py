@@ -464,6 +464,26 @@ def scan_export(ctx, name: str) -> np.ndarray:
     return out
 
 
+def scan_export_device(ctx, name: str, dst) -> int:
+    """Export a result array into a caller-owned CUDA tensor (device to device, no host copy); returns
+    the bytes written. ``dst`` must hold at least ``scan_output_size`` bytes."""
+    lib = _load_lib()
+    idx = OUT_INDEX[name]
+    nb = ctypes.c_uint64()
+    _check(ctx, lib.scan_output_size(ctx, idx, ctypes.byref(nb)))
+    if nb.value > dst.numel() * dst.element_size():
+        raise ValueError(f"{name}: destination holds {dst.numel() * dst.element_size()} bytes, need {nb.value}")
+    if nb.value:
+        _check(ctx, lib.scan_export(ctx, idx, dst.data_ptr(), nb.value, 1))
+    return int(nb.value)
+
+
+def scan_output_bytes(ctx, name: str) -> int:
+    nb = ctypes.c_uint64()
+    _check(ctx, _load_lib().scan_output_size(ctx, OUT_INDEX[name], ctypes.byref(nb)))
+    return int(nb.value)
+
+
 def scan_destroy(ctx):
     if ctx:
         _load_lib().scan_destroy(ctx)

@@ -865,11 +865,13 @@ __device__ __forceinline__ void ft_prefetch_tile(const FusedArgs& a, uint64_t t,
     const uint64_t g = rb2 + (uint64_t)row * npos2 + p02;
     const char* col0;
     const char* ptr;
+    const char* pe;  // end of the row's segment: a line is fetched only if it holds a byte before it
     uint64_t lim;
-    if (j < l4) { col0 = reinterpret_cast<const char*>(a.dur); ptr = reinterpret_cast<const char*>(a.dur + g) + 128ull * j; lim = 4 * a.n_events; }
-    else if (j < 2 * l4) { col0 = reinterpret_cast<const char*>(a.comm); ptr = reinterpret_cast<const char*>(a.comm + g) + 128ull * (j - l4); lim = 4 * a.n_events; }
-    else { col0 = reinterpret_cast<const char*>(a.kind); ptr = reinterpret_cast<const char*>(a.kind + g) + 128ull * (j - 2 * l4); lim = 2 * a.n_events; }
-    if ((uint64_t)(ptr - col0) < lim) asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+    if (j < l4) { col0 = reinterpret_cast<const char*>(a.dur); ptr = reinterpret_cast<const char*>(a.dur + g) + 128ull * j; pe = reinterpret_cast<const char*>(a.dur + g + np2); lim = 4 * a.n_events; }
+    else if (j < 2 * l4) { col0 = reinterpret_cast<const char*>(a.comm); ptr = reinterpret_cast<const char*>(a.comm + g) + 128ull * (j - l4); pe = reinterpret_cast<const char*>(a.comm + g + np2); lim = 4 * a.n_events; }
+    else { col0 = reinterpret_cast<const char*>(a.kind); ptr = reinterpret_cast<const char*>(a.kind + g) + 128ull * (j - 2 * l4); pe = reinterpret_cast<const char*>(a.kind + g + np2); lim = 2 * a.n_events; }
+    if ((uint64_t)(ptr - col0) < lim && (reinterpret_cast<uintptr_t>(ptr) & ~(uintptr_t)127) < reinterpret_cast<uintptr_t>(pe))
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
   }
 }
 
