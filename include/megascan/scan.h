@@ -230,6 +230,18 @@ uint64_t    scan_stream_window(const scan_ctx* ctx);
 scan_status scan_create_sharded(scan_ctx** out, int cuda_device, void* cuda_stream, int n_shards, int shard,
                                 const uint8_t nccl_unique_id[128]);
 
+/* In-process shard group (exchange back-end for testing and single-process use): n_shards (1..16)
+   sharded contexts of ONE process, each driven by its own host thread, exchange through host barriers
+   and device copies instead of NCCL; they may share a GPU. scan_create_sharded_local creates shard
+   `shard` of `group` (same semantics and preconditions as scan_create_sharded). The group is owned by
+   the caller and must outlive its contexts; scan_analyze on the shards must be called concurrently
+   (one thread per shard), else it blocks. Not a performance path.                */
+typedef struct scan_local_group scan_local_group;
+scan_status scan_local_group_create(scan_local_group** out, int n_shards);
+void scan_local_group_destroy(scan_local_group* group);
+scan_status scan_create_sharded_local(scan_ctx** out, int cuda_device, void* cuda_stream, scan_local_group* group,
+                                      int shard);
+
 /* ---- NEXT-4: event-level blame (DESIGN.md §10e EB1-EB6) ----
    For every waiting communication event (an event of a VALID instance with wait > 0), the event
    where its delay began: it waited for the instance's last arriver, whose previous event in program

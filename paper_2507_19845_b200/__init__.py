@@ -184,6 +184,9 @@ def _load_lib():
     lib.scan_stream_window.argtypes = [P]
     lib.scan_stream_window.restype = ctypes.c_uint64
     lib.scan_create_sharded.argtypes = [ctypes.POINTER(P), ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P]
+    lib.scan_local_group_create.argtypes = [ctypes.POINTER(P), ctypes.c_int]
+    lib.scan_local_group_destroy.argtypes = [P]
+    lib.scan_create_sharded_local.argtypes = [ctypes.POINTER(P), ctypes.c_int, P, P, ctypes.c_int]
     lib.scan_blame.argtypes = [P, ctypes.POINTER(_BlameRes)]
     lib.scan_ingest_json.argtypes = [P, ctypes.POINTER(_Topo), P, ctypes.c_uint64, P, ctypes.c_uint32, ctypes.c_uint32,
                                      ctypes.POINTER(_JsonRes)]
@@ -192,7 +195,8 @@ def _load_lib():
     for f in ("scan_create", "scan_load_events", "scan_match_collectives", "scan_detect", "scan_localize",
               "scan_output_size", "scan_export", "scan_analyze", "scan_force_general", "scan_fused_variant",
               "scan_nccl_unique_id", "scan_create_sharded", "scan_align", "scan_stream_open", "scan_stream_push",
-              "scan_ingest_json", "scan_loaded_column", "scan_emit_chrome", "scan_blame"):
+              "scan_ingest_json", "scan_loaded_column", "scan_emit_chrome", "scan_blame", "scan_local_group_create",
+              "scan_create_sharded_local"):
         getattr(lib, f).restype = ctypes.c_int32
     _lib = lib
     return lib
@@ -204,7 +208,7 @@ EXPORTED_SYMBOLS = ["scan_create", "scan_destroy", "scan_last_error", "scan_load
                     "scan_analyze", "scan_used_fused", "scan_force_general", "scan_fused_variant",
                     "scan_nccl_unique_id", "scan_create_sharded", "scan_align", "scan_stream_open", "scan_stream_push",
                     "scan_stream_window", "scan_ingest_json", "scan_loaded_column", "scan_emit_chrome",
-                    "scan_blame"]
+                    "scan_blame", "scan_local_group_create", "scan_local_group_destroy", "scan_create_sharded_local"]
 
 
 @dataclass
@@ -310,6 +314,40 @@ def _column(name: str, x, n: int, device: bool):
             raise ValueError(f"{name}: values of dtype {a.dtype} do not fit the ABI type {want}")
         a = a.astype(want)
     return np.ascontiguousarray(a)
+
+
+class LocalGroup:
+    """In-process shard group (scan.h scan_local_group_create): G sharded contexts of this process,
+    one host thread per shard, exchanging through the library's in-process back-end (no NCCL). For
+    testing the sharded path on one GPU; the group must outlive its Scan objects."""
+
+    def __init__(self, n_shards: int):
+        lib = _load_lib()
+        h = ctypes.c_void_p()
+        st = lib.scan_local_group_create(ctypes.byref(h), int(n_shards))
+        if st < 0:
+            raise ScanError(st, "scan_local_group_create failed")
+        self.h, self.n = h, int(n_shards)
+
+    def close(self):
+        if self.h:
+            _load_lib().scan_local_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def scan_create_sharded_local(device: int, stream, group: LocalGroup, shard: int):
+    lib = _load_lib()
+    h = ctypes.c_void_p()
+    st = lib.scan_create_sharded_local(ctypes.byref(h), device, stream, group.h, int(shard))
+    if st < 0:
+        raise ScanError(st, "scan_create_sharded_local failed")
+    return h
 
 
 def scan_load_events(ctx, tp, pp, dp, rank_offsets, comm_offsets, comm_members, dur, kind_op, meta, comm, payload,
@@ -504,7 +542,9 @@ class Scan:
                     stream = torch.cuda.current_stream(device).cuda_stream
             except Exception:
                 stream = None
-        if shards is not None and shards[0] > 1:
+        if shards is not None and isinstance(shards[2], LocalGroup):
+            self.ctx = scan_create_sharded_local(device, stream, shards[2], int(shards[1]))
+        elif shards is not None and shards[0] > 1:
             self.ctx = scan_create_sharded(device, stream, int(shards[0]), int(shards[1]), shards[2])
         else:
             self.ctx = scan_create(device, stream)

@@ -64,6 +64,10 @@ struct Counters {
   unsigned int n_end_ranks;          // ranks whose last event ends an iteration
 };
 
+// one collective operation of a grouped exchange on the in-process back-end (xch.cu)
+enum { XU8 = 0, XU32 = 1, XU64 = 2, XF64 = 3 };
+struct XOp { int kind; const void* send; void* recv; size_t n; int type; int peer; };  // kind: 0 send, 1 recv, 2 all-reduce
+
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -164,6 +168,9 @@ struct Ctx {
   // multi-GPU iteration-window shards (row A9, shard.cu); n_shards == 1: unsharded
   int n_shards = 1, shard = 0;
   void* nccl = nullptr;                  // ncclComm_t owned by the context
+  void* lgroup = nullptr;                // in-process exchange group (xch.cu), not owned; nccl == nullptr then
+  std::vector<XOp> xops;                 // pending ops of an in-process grouped exchange
+  DevBuf xtmp;                           // in-process all-reduce scratch
   uint32_t it_off = 0;                   // global iteration of this shard's first iteration
   DevBuf g_base, g_slot, g_nmax, g_nmin, g_k0; // global channel tables + this shard's first occurrence per channel; (kernels use the shard-shifted ch_base/ch_slot)
   std::vector<uint64_t> h_shard_k0;      // [NCH] global occurrence index of this shard's first instance
@@ -252,6 +259,14 @@ scan_status sharded_all(Ctx& c);
 scan_status fused_all(Ctx& c);
 scan_status fused_rerun(Ctx& c);
 int launch_shard_head(Ctx& c, unsigned long long* out);
+// exchange layer of the sharded analysis (xch.cu): NCCL communicator or in-process group; 0 = ok
+int xch_allgather(Ctx& c, const void* send, void* recv, size_t n_u32);
+void xch_group_start(Ctx& c);
+void xch_send(Ctx& c, const void* p, size_t n_u32, int peer);
+void xch_recv(Ctx& c, void* p, size_t n_u32, int peer);
+void xch_allreduce(Ctx& c, void* p, size_t n, int type);
+int xch_group_end(Ctx& c);
+const char* xch_error(int rc);
 int launch_shard_fixup(Ctx& c, int G, const unsigned long long* ht);
 int launch_link_median_window(Ctx& c, const uint64_t* base, const uint32_t* nmax, const uint64_t* slot, const uint4* rec,
                               const uint32_t* iter, const uint32_t* pay, uint64_t n_inst);

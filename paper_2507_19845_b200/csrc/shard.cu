@@ -328,7 +328,6 @@ scan_status sharded_all(Ctx& c) {
   c.fused_used = false; c.tiles_ready = false; c.xwait_pending = false;
   const uint32_t G = (uint32_t)c.n_shards, g = (uint32_t)c.shard, nc = c.n_comms;
   const uint64_t W = c.W;
-  ncclComm_t comm = (ncclComm_t)c.nccl;
   scan_status st;
   if ((st = prep_ws(c, false))) return st;
   // ---- local census (the fused pre-pass of this shard) + X1, packed on the device (one sync)
@@ -362,9 +361,9 @@ scan_status sharded_all(Ctx& c) {
       c.bitmap.as<uint32_t>(), nc, nbm, c.x_send.as<uint32_t>());
   c.launches += 1;
   mark("launch");
-  ncclResult_t xr = ncclSuccess;
-  timed(c, "x1_allgather", [&] { xr = ncclAllGather(c.x_send.p, c.x_recv.p, LA, ncclUint32, comm, c.stream); return 0; });
-  if (xr != ncclSuccess) { c.err = std::string("NCCL all-gather: ") + ncclGetErrorString(xr); return SCAN_E_NCCL; }
+  int xr = 0;
+  timed(c, "x1_allgather", [&] { xr = xch_allgather(c, c.x_send.p, c.x_recv.p, LA); return 0; });
+  if (xr) { c.err = std::string("exchange all-gather: ") + xch_error(xr); return SCAN_E_NCCL; }
   CK(cudaMemcpy2DAsync(pin + offA, HL * 4, c.x_recv.p, LA * 4, HL * 4, G, cudaMemcpyDeviceToHost, c.stream));
   CK(cudaEventRecord(c.ev_x1, c.stream));
   c.launches += timed(c, "k_p2p_set", [&] {
@@ -383,8 +382,8 @@ scan_status sharded_all(Ctx& c) {
   });
   CK(cudaMemcpyAsync(pin + offC, c.counters.p, sizeof(Counters), cudaMemcpyDeviceToHost, c.stream));
   CK(cudaEventRecord(c.ev_x2, c.stream));
-  timed(c, "x2_allgather", [&] { xr = ncclAllGather(c.x_send.p, c.x_recv2.p, LB, ncclUint32, comm, c.stream); return 0; });
-  if (xr != ncclSuccess) { c.err = std::string("NCCL all-gather: ") + ncclGetErrorString(xr); return SCAN_E_NCCL; }
+  timed(c, "x2_allgather", [&] { xr = xch_allgather(c, c.x_send.p, c.x_recv2.p, LB); return 0; });
+  if (xr) { c.err = std::string("exchange all-gather: ") + xch_error(xr); return SCAN_E_NCCL; }
   // host: X1 headers while the device works on the P2P channel set (identical data on every shard ->
   // identical decisions; every shard has enqueued the same collectives before any early return)
   CK(cudaEventSynchronize(c.ev_x1));
@@ -580,18 +579,18 @@ scan_status sharded_all(Ctx& c) {
                                                               c.p2p_inst0, c.p2p_slot0, c.x_send.as<uint32_t>());
       c.launches += 1;
     }
-    ncclResult_t xr = ncclSuccess;
+    int xr = 0;
     timed(c, "x3_alltoall", [&] {
-      ncclGroupStart();
+      xch_group_start(c);
       for (uint32_t d = 0; d < G; ++d) {
         if (d == g) continue;
-        if (scount[d]) ncclSend(c.x_send.as<uint32_t>() + soff[d] * LREC, scount[d] * LREC, ncclUint32, (int)d, comm, c.stream);
-        if (rcount[d]) ncclRecv(c.x_recv.as<uint32_t>() + roff[d] * LREC, rcount[d] * LREC, ncclUint32, (int)d, comm, c.stream);
+        if (scount[d]) xch_send(c, c.x_send.as<uint32_t>() + soff[d] * LREC, scount[d] * LREC, (int)d);
+        if (rcount[d]) xch_recv(c, c.x_recv.as<uint32_t>() + roff[d] * LREC, rcount[d] * LREC, (int)d);
       }
-      xr = ncclGroupEnd();
+      xr = xch_group_end(c);
       return 0;
     });
-    if (xr != ncclSuccess) { c.err = std::string("NCCL all-to-all: ") + ncclGetErrorString(xr); return SCAN_E_NCCL; }
+    if (xr) { c.err = std::string("exchange all-to-all: ") + xch_error(xr); return SCAN_E_NCCL; }
     if (!rmap.empty()) {
       k_link_unpack<<<(unsigned)rmap.size(), 256, 0, c.stream>>>(c.lk_recvmap.as<LinkMap>(), c.x_recv.as<uint32_t>(),
                                                                 c.inst_rec.as<uint4>(), c.p2p_iter.as<uint32_t>(),
@@ -619,21 +618,21 @@ scan_status sharded_all(Ctx& c) {
     c.launches += 1;
     // ---- X4: one grouped all-reduce (sum) of every partial result
     const uint64_t nnz_tot = c.nnz_c + W * PCAP;
-    ncclResult_t xr = ncclSuccess;
+    int xr = 0;
     timed(c, "x4_allreduce", [&] {
-      ncclGroupStart();
-      auto ar = [&](DevBuf& b, uint64_t n, ncclDataType_t t) { if (n) ncclAllReduce(b.p, b.p, n, t, ncclSum, comm, c.stream); };
-      ar(c.wd_total, items, ncclUint32); ar(c.wd_slow, items, ncclUint32);
-      ar(c.wl_joined, items, ncclUint32); ar(c.wl_late, items, ncclUint32);
-      ar(c.lk_n, nlk, ncclUint32); ar(c.lk_medp, nlk, ncclUint32); ar(c.lk_medt, nlk, ncclUint32);
-      ar(c.lk_used, nlk, ncclUint8); ar(c.lk_elig, nlk, ncclUint8); ar(c.lk_bw, nlk, ncclFloat64);
-      ar(c.cl_J, ncl, ncclUint32); ar(c.cl_max, ncl, ncclUint32);
-      ar(c.ewc, (uint64_t)c.NW * nnz_tot, ncclUint64); ar(c.rk_sum, 3 * W, ncclUint64);
-      ar(c.headtail, (uint64_t)G * W + 16, ncclUint64);
-      xr = ncclGroupEnd();
+      xch_group_start(c);
+      auto ar = [&](DevBuf& b, uint64_t n, int t) { if (n) xch_allreduce(c, b.p, n, t); };
+      ar(c.wd_total, items, XU32); ar(c.wd_slow, items, XU32);
+      ar(c.wl_joined, items, XU32); ar(c.wl_late, items, XU32);
+      ar(c.lk_n, nlk, XU32); ar(c.lk_medp, nlk, XU32); ar(c.lk_medt, nlk, XU32);
+      ar(c.lk_used, nlk, XU8); ar(c.lk_elig, nlk, XU8); ar(c.lk_bw, nlk, XF64);
+      ar(c.cl_J, ncl, XU32); ar(c.cl_max, ncl, XU32);
+      ar(c.ewc, (uint64_t)c.NW * nnz_tot, XU64); ar(c.rk_sum, 3 * W, XU64);
+      ar(c.headtail, (uint64_t)G * W + 16, XU64);
+      xr = xch_group_end(c);
       return 0;
     });
-    if (xr != ncclSuccess) { c.err = std::string("NCCL all-reduce: ") + ncclGetErrorString(xr); return SCAN_E_NCCL; }
+    if (xr) { c.err = std::string("exchange all-reduce: ") + xch_error(xr); return SCAN_E_NCCL; }
     mark("x4enq");
   }
   // ---- replicated tail on identical job-wide inputs, enqueued behind X4 without a host round trip:

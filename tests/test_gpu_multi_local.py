@@ -1,0 +1,90 @@
+"""Sharded analysis on ONE GPU (-m gpu, row A9): G logical shards of the same job, each a sharded
+context of an in-process group (scan_create_sharded_local), driven by one host thread each with its
+own CUDA stream. The exchange layer (xch.cu) replaces NCCL by host barriers and device copies, so
+every step of the sharded path (census, X1 / X2 numbering, the X3 regroup of P2P instance records to
+the link owner, the X4 reduction, the stage-2 boundary fix-up and the replicated tail) runs exactly as
+on G GPUs. The per-shard exports are reassembled (tests/shard_merge.py) and compared element by
+element with the oracle run on the whole trace -- the same cases as tests/multigpu_parity.py."""
+import os
+import sys
+import threading
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+import oracle  # noqa: E402
+import tracegen as tg  # noqa: E402
+from shard_merge import coverage, merge  # noqa: E402
+from multigpu_parity import CASES  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_shards(G, cfg, wi, mode, mins, transform):
+    import torch
+    import paper_2507_19845_b200 as ms
+    group = ms.LocalGroup(G)
+    streams = [torch.cuda.Stream(0) for _ in range(G)]
+    scans = [ms.Scan(0, streams[g].cuda_stream, shards=(G, g, group)) for g in range(G)]
+    full = transform(tg.generate(cfg)) if transform is not None else None
+    traces = []
+    for g in range(G):
+        b, e = ms.shard_iterations(cfg.iterations, G, g)
+        traces.append(tg.generate(cfg, with_start=False, iter_range=(b, e)) if full is None else
+                      ms.slice_iterations(full, b, e))
+    d = ms.DetectConfig(window_iters=wi, want_ref=True, min_samples=mins)
+    l_ = ms.LocalizeConfig(stage2_mode=mode, min_samples=mins)
+    parts = [None] * G
+
+    def work(g):
+        part = {"ro": np.asarray(traces[g].rank_offsets), "err": None, "out": None, "res": None}
+        try:
+            scans[g].load(traces[g])
+            part["res"] = scans[g].analyze(d, l_)
+            out = scans[g].export_all()
+            out["ch_shard_k0"] = scans[g].export("ch_shard_k0")
+            out["ch_shard_n"] = scans[g].export("ch_shard_n")
+            part["out"] = out
+        except ms.ScanError as x:
+            part["err"] = (x.status, str(x))
+        parts[g] = part
+
+    th = [threading.Thread(target=work, args=(g,)) for g in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not any(t.is_alive() for t in th), "a shard thread did not finish (exchange deadlock)"
+    for s in scans:
+        s.close()
+    group.close()
+    return parts, full
+
+
+@pytest.mark.parametrize("G", [2, 3, 4])
+@pytest.mark.parametrize("case", CASES[:7] + CASES[7:10], ids=lambda c: c[0])
+def test_local_shards_equal_the_oracle(G, case):
+    name, mk, wi, mode, mins, transform, expect = case
+    cfg = mk()
+    if cfg.iterations < G:
+        pytest.skip("fewer iterations than shards")
+    parts, full = _run_shards(G, cfg, wi, mode, mins, transform)
+    if expect is not None:
+        errs = [p["err"] for p in parts]
+        assert all(e is not None and e[0] == expect for e in errs), f"expected status {expect}, got {errs}"
+        return
+    errs = [p["err"] for p in parts if p["err"]]
+    assert not errs, f"shard errors: {errs}"
+    if full is None:
+        full = tg.generate(cfg)
+    o = oracle.run(full, oracle.Config(window_iters=wi, stage2_mode=mode, min_samples=mins))
+    merged, issues = merge(parts)
+    assert not issues, "\n".join(issues)
+    cov = coverage(parts, int(o["n_instances"]))
+    assert (cov == 1).all(), f"instance coverage: {np.unique(cov, return_counts=True)}"
+    merged["_res"] = parts[0]["res"]
+    from test_gpu_parity import compare
+    compare(o, merged)
