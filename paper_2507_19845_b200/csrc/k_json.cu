@@ -2,7 +2,9 @@
 //
 // Ingest (P:L117-118 per-rank JSON files; P:L112 tracers.scope metadata; P:L131 participant lists;
 // DESIGN.md §10d readings J1-J11). Data-parallel plan:
-//   J-a  k_j_words   per 64-byte word: unescaped-quote / open / close bit masks (64 B read per word)
+//   J-a  k_j_words   per 64-byte word: unescaped-quote / open / close bit masks (64 B read per word), the
+//                    word's escape transfer code; a scan of the codes gives each word's entry state and
+//                    k_j_escfix flips the one quote it changes (no look-back over backslash runs)
 //   J-b  xor-scan of the per-word quote parity -> in-string state at every word start (CUB scan)
 //   J-c  k_j_struct  string-filtered structural masks + depth delta per word; sum-scan -> depth
 //   J-d  k_j_docs1 / k_j_marks / k_j_docs2 / k_j_arrclose / k_j_docs3: roots, the traceEvents
@@ -52,7 +54,7 @@ struct DocInfo {
 
 struct JsonState {
   DevBuf buf, docs, dinfo, err;
-  DevBuf qm, om, cm, par, carry, delta, dbase, wcnt, wpre;
+  DevBuf qm, om, cm, par, carry, delta, dbase, wcnt, wpre, esc, lead, ein;
   DevBuf epos, edoc;
   DevBuf e_rank, e_ts, e_dur, e_ko, e_meta, e_cp, e_pay, e_gh, e_gpos, e_gn;
   DevBuf keys_a, keys_b, vals_a, vals_b, tmp, flags, sel, nsel;
@@ -87,13 +89,20 @@ __device__ __forceinline__ uint64_t prefix_xor(uint64_t x) {
 }
 
 // ------------------------------------------------------------------------------------- J-a .. J-c
+// Escapes cross word boundaries: whether the first byte of a word is escaped depends on the
+// backslash run ending the previous bytes. Each word is classified assuming it is NOT entered
+// escaped; the only byte whose meaning flips when it is entered escaped is the first byte after its
+// leading backslash run (a quote there toggles). The entry state itself comes from a scan of
+// per-word transfer codes (esc): a word holding a non-backslash byte leaves the state given by the
+// parity of its trailing run (0 / 1), an all-backslash word (64, even) passes it through (2). O(n).
 __global__ void __launch_bounds__(256) k_j_words(const uint8_t* __restrict__ b, uint64_t n, uint64_t nw, uint64_t* qm,
-                                                 uint64_t* om, uint64_t* cm, uint8_t* par) {
+                                                 uint64_t* om, uint64_t* cm, uint8_t* esc, uint8_t* lead) {
   const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= nw) return;
   const uint64_t p0 = w * 64;
-  uint32_t run = 0;  // backslashes immediately before the word (escape state carried in)
-  for (uint64_t p = p0; p > 0 && b[p - 1] == '\\'; --p) ++run;
+  uint32_t run = 0;      // backslashes since the last other byte
+  uint32_t ld = 0xFFu;   // position of the first non-backslash byte if it is a quote (0x40 | pos), else none
+  bool other = false;    // a non-backslash byte seen
   uint64_t q = 0, o = 0, cl = 0;
   const uint4* v = reinterpret_cast<const uint4*>(b + p0);
 #pragma unroll
@@ -106,6 +115,8 @@ __global__ void __launch_bounds__(256) k_j_words(const uint8_t* __restrict__ b, 
       const int bit = k * 16 + j;
       if (p0 + bit >= n) continue;
       if (ch == '\\') { ++run; continue; }
+      if (!other && ch == '"') ld = 0x40u | (uint32_t)bit;
+      other = true;
       if (ch == '"' && !(run & 1)) q |= 1ull << bit;
       if (ch == '{' || ch == '[') o |= 1ull << bit;
       if (ch == '}' || ch == ']') cl |= 1ull << bit;
@@ -113,6 +124,23 @@ __global__ void __launch_bounds__(256) k_j_words(const uint8_t* __restrict__ b, 
     }
   }
   qm[w] = q; om[w] = o; cm[w] = cl;
+  esc[w] = other ? (uint8_t)(run & 1) : (uint8_t)2;
+  lead[w] = (uint8_t)ld;
+}
+
+// escape-state composition for the scan: a later constant wins, identity passes the earlier state
+struct EscOp {
+  __device__ __forceinline__ uint8_t operator()(uint8_t a, uint8_t b) const { return b == 2 ? a : b; }
+};
+
+// entered escaped: the leading quote flips; then the quote parity of the word
+__global__ void __launch_bounds__(256) k_j_escfix(uint64_t nw, uint64_t* qm, const uint8_t* ein, const uint8_t* lead,
+                                                  uint8_t* par) {
+  const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= nw) return;
+  uint64_t q = qm[w];
+  const uint8_t ld = lead[w];
+  if (ein[w] == 1 && (ld & 0x40u)) { q ^= 1ull << (ld & 63u); qm[w] = q; }
   par[w] = (uint8_t)(__popcll(q) & 1);
 }
 
@@ -1040,6 +1068,7 @@ void json_release(Ctx& c) {
   JsonState* s = static_cast<JsonState*>(c.json_state);
   if (!s) return;
   DevBuf* all[] = {&s->buf, &s->docs, &s->dinfo, &s->err, &s->qm, &s->om, &s->cm, &s->par, &s->carry, &s->delta,
+                   &s->esc, &s->lead, &s->ein,
                    &s->dbase, &s->wcnt, &s->wpre, &s->epos, &s->edoc, &s->e_rank, &s->e_ts, &s->e_dur, &s->e_ko,
                    &s->e_meta, &s->e_cp, &s->e_pay, &s->e_gh, &s->e_gpos, &s->e_gn, &s->keys_a, &s->keys_b,
                    &s->vals_a, &s->vals_b, &s->tmp, &s->flags, &s->sel, &s->nsel, &s->seg, &s->segstart,
@@ -1080,6 +1109,7 @@ scan_status json_ingest(Ctx& c, const scan_topology* topo, const uint8_t* bytes,
   const uint64_t nw1 = std::max<uint64_t>(nw, 1);
   CK(S.qm.ensure(nw1 * 8)); CK(S.om.ensure(nw1 * 8)); CK(S.cm.ensure(nw1 * 8));
   CK(S.par.ensure(nw1)); CK(S.carry.ensure(nw1)); CK(S.delta.ensure(nw1 * 4)); CK(S.dbase.ensure(nw1 * 4));
+  CK(S.esc.ensure(nw1)); CK(S.lead.ensure(nw1)); CK(S.ein.ensure(nw1));
   CK(S.wcnt.ensure(nw1 * 4)); CK(S.wpre.ensure(nw1 * 4));
   const uint8_t* B = S.buf.as<uint8_t>();
   JErr* ER = S.err.as<JErr>();
@@ -1098,7 +1128,17 @@ scan_status json_ingest(Ctx& c, const scan_topology* topo, const uint8_t* bytes,
   if (nw) {
     launches += timed(c, "k_j_words", [&] {
       k_j_words<<<nb(nw, 256), 256, 0, c.stream>>>(B, n, nw, S.qm.as<uint64_t>(), S.om.as<uint64_t>(), S.cm.as<uint64_t>(),
-                                                   S.par.as<uint8_t>());
+                                                   S.esc.as<uint8_t>(), S.lead.as<uint8_t>());
+      return 1;
+    });
+    if ((st = cub2([&](void* t, size_t& tb) {  // escape state entering every word (start: not escaped)
+           return cub::DeviceScan::ExclusiveScan(t, tb, S.esc.as<uint8_t>(), S.ein.as<uint8_t>(), EscOp(), (uint8_t)0,
+                                                 (int64_t)nw, c.stream);
+         })))
+      return st;
+    launches += timed(c, "k_j_escfix", [&] {
+      k_j_escfix<<<nb(nw, 256), 256, 0, c.stream>>>(nw, S.qm.as<uint64_t>(), S.ein.as<uint8_t>(), S.lead.as<uint8_t>(),
+                                                    S.par.as<uint8_t>());
       return 1;
     });
     if ((st = cub2([&](void* t, size_t& tb) {

@@ -175,3 +175,21 @@ def test_fuzz_random_jobs(seed):
     s.analyze(ms.DetectConfig(min_samples=3), ms.LocalizeConfig(min_samples=3))
     assert s.emit_chrome() == cj.emit(t, o["ev_inst"])
     s.close()
+
+
+@pytest.mark.parametrize("run", [1, 2, 63, 64, 65, 127, 128, 129, 1 << 20])
+def test_long_backslash_runs(run):
+    """Escapes across 64-byte words: a string holding `run` escaped backslashes (2*run backslash bytes)
+    then an escaped quote, inside an unknown args key of the first event, and a second document whose
+    first string starts right after a run boundary. The entry escape state of every word comes from a
+    scan (no look-back), so a 2 MB run costs the same per byte as any other input."""
+    cfg = configs.c1(seed=3, iterations=2)
+    docs = chrome.rank_documents(tg.generate(cfg), messy=False, seed=1)
+    d0 = docs[0].decode()
+    k = d0.index('"args":{') + len('"args":{')
+    pad = '"note":"' + '\\\\' * run + '\\"x",'
+    docs = [(d0[:k] + pad + d0[k:]).encode()] + list(docs[1:])
+    t, skipped = cj.parse(docs, cfg.tp, cfg.pp, cfg.dp)
+    s, res = _ingest(docs, (cfg.tp, cfg.pp, cfg.dp))
+    _check_columns(s, res, t, skipped)
+    s.close()
