@@ -53,6 +53,16 @@ def needed_bytes_per_event(comm_frac: float, p2p_frac: float) -> float:
     return 10.0 + 6.0 * p2p_frac + 8.0 * comm_frac + (1.0 - comm_frac) / 8.0
 
 
+def peak_of() -> float:
+    """Measured HBM copy bandwidth (MEASURED_PEAKS.json), else the profiling guide's fallback."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    return float(json.load(open(path)).get("hbm_gbs", 6650.0)) if os.path.exists(path) else 6650.0
+
+
+def bpe_of(comm_frac: float) -> float:
+    return alg_bytes_per_event(comm_frac)
+
+
 def host_cpu() -> dict:
     """The host the oracle baseline ran on: logical CPUs, this process's affinity, CPU model."""
     model = None
@@ -352,6 +362,7 @@ def main():
     ap.add_argument("--no-stream", action="store_true", help="skip the C5 sliding-window measurement (N=1 only)")
     ap.add_argument("--no-json", action="store_true", help="skip the JSON ingest / emit measurement (N=1 only)")
     ap.add_argument("--no-blame", action="store_true", help="skip the event-level blame measurement (N=1 only)")
+    ap.add_argument("--no-general", action="store_true", help="skip the general-path measurement (N=1 only)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -551,6 +562,47 @@ def main():
                          if jump_ms else None),
         }
 
+    # ---- the general path on the same resident trace, N=1 only: forced, and as the fallback after one
+    # SPMD violation (an op id changed on one rank: the fused pass rejects the trace, the general path reruns)
+    general = None
+    if world == 1 and not args.no_general:
+        def timed_steps(n):
+            s.set_timing(True)
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            for _ in range(n):
+                r_ = s.analyze()
+            g1.record(stream)
+            torch.cuda.synchronize()
+            kt = s.kernel_timing()
+            s.set_timing(False)
+            top = sorted(kt.items(), key=lambda kv: -kv[1][0])[:6]
+            return g0.elapsed_time(g1) / n, r_, {k: round(v[0] / n, 4) for k, v in top}
+        gsteps = max(2, min(args.steps, 3))
+        s.force_general(True)
+        s.analyze()
+        gms, gres, gk = timed_steps(gsteps)
+        s.force_general(False)
+        e_bad = int(tr.rank_offsets[min(300, tr.world - 1)]) + 5000
+        old_k = dev["kind_op"][e_bad].item()
+        new_k = ((old_k & 0xFFFF) ^ (9 << 4)) & 0xFFFF
+        dev["kind_op"][e_bad] = new_k - 0x10000 if new_k >= 0x8000 else new_k
+        s.analyze()
+        vms, vres, vk = timed_steps(gsteps)
+        dev["kind_op"][e_bad] = old_k
+        torch.cuda.synchronize()
+        general = {
+            "metric": "trace events analysed/sec on the general (non-SPMD) path",
+            "forced": {"value": N / (gms / 1e3), "unit": "events/s", "ms_per_step": gms,
+                       "hbm_frac": bpe_of(comm_frac) * N / (gms / 1e3) / 1e9 / peak_of(), "fused": bool(gres["fused"]),
+                       "kernels_ms": gk},
+            "one_violation": {"value": N / (vms / 1e3), "unit": "events/s", "ms_per_step": vms,
+                              "hbm_frac": bpe_of(comm_frac) * N / (vms / 1e3) / 1e9 / peak_of(), "fused": bool(vres["fused"]),
+                              "kernels_ms": vk,
+                              "note": f"op id of event {e_bad} (rank {min(300, tr.world - 1)}) changed: the fused pass "
+                                      "verifies, rejects, and the call reruns the general path (both inside the time)"},
+        }
+
     streaming = streaming_c5(ms, torch, local, stream) if (world == 1 and not args.no_stream) else None
     json_ingest = json_io(ms, torch, local, stream, args.steps, args.warmup, not args.no_cpu) if (
         world == 1 and not args.no_json) else None
@@ -621,6 +673,7 @@ def main():
         "json_ingest": json_ingest,
         "blame": blame,
         "exports": exports,
+        "general_path": general,
         "path": "fused SPMD stage-tile pass (K9)" if fused else "general path",
     }
     print(json.dumps(line), flush=True)

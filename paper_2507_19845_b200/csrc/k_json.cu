@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(256) k_j_words(const uint8_t* __restrict__ b, 
   if (w >= nw) return;
   const uint64_t p0 = w * 64;
   uint32_t run = 0;      // backslashes since the last other byte
-  uint32_t ld = 0xFFu;   // position of the first non-backslash byte if it is a quote (0x40 | pos), else none
+  uint32_t ld = 0;       // 0x80 | position of the first non-backslash byte if it is a quote, else 0
   bool other = false;    // a non-backslash byte seen
   uint64_t q = 0, o = 0, cl = 0;
   const uint4* v = reinterpret_cast<const uint4*>(b + p0);
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256) k_j_words(const uint8_t* __restrict__ b, 
       const int bit = k * 16 + j;
       if (p0 + bit >= n) continue;
       if (ch == '\\') { ++run; continue; }
-      if (!other && ch == '"') ld = 0x40u | (uint32_t)bit;
+      if (!other && ch == '"') ld = 0x80u | (uint32_t)bit;
       other = true;
       if (ch == '"' && !(run & 1)) q |= 1ull << bit;
       if (ch == '{' || ch == '[') o |= 1ull << bit;
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(256) k_j_escfix(uint64_t nw, uint64_t* qm, con
   if (w >= nw) return;
   uint64_t q = qm[w];
   const uint8_t ld = lead[w];
-  if (ein[w] == 1 && (ld & 0x40u)) { q ^= 1ull << (ld & 63u); qm[w] = q; }
+  if (ein[w] == 1 && (ld & 0x80u)) { q ^= 1ull << (ld & 63u); qm[w] = q; }
   par[w] = (uint8_t)(__popcll(q) & 1);
 }
 
