@@ -267,9 +267,11 @@ int launch_fused_census(Ctx& c) {
 
 // ----------------------------------------------------------------------------- F1 fused tile kernel
 // q = x / d by multiply-high with m = ceil(2^32 / d); exact for x < 2^22 and d <= 1024 (x * (m*d - 2^32) < 2^32).
+// ceil(2^32 / d) = floor((2^32 - 1) / d) + 1 for d >= 2 (d | 2^32 or not): one 32-bit division, not
+// the 64-bit software division every thread of a tile would otherwise run
 struct FDiv { uint32_t d, m; };
 __host__ __device__ __forceinline__ FDiv fdiv_make(uint32_t d) {
-  return FDiv{d, d <= 1 ? 0u : (uint32_t)((0x100000000ull + d - 1) / d)};
+  return FDiv{d, d <= 1 ? 0u : 0xFFFFFFFFu / d + 1u};
 }
 __device__ __forceinline__ uint32_t fdiv(uint32_t x, FDiv f) { return f.d <= 1 ? x : __umulhi(x, f.m); }
 
@@ -1329,11 +1331,24 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
   if (R == 0)  // timing experiment only (results invalid)
 #endif
   {
+    // the tile's wait-for edge sums -> global: every edge column index loaded first (independent L2
+    // hits in flight together), then the atomics, instead of one dependent load per atomic
     const FDiv fe = fdiv_make(ES);
-    for (uint32_t i = tid; i < R * ES; i += FT_NT) {
-      const uint32_t row = fdiv(i, fe), slot = i - row * ES;
-      const uint32_t v = slot < E ? sedge[i] : 0u;
-      if (v) atomicAdd(&a.ew[(uint64_t)w_tile * a.nnz_tot + a.eidx[(uint64_t)(sbase + row) * E + slot]], (unsigned long long)v);
+    constexpr int EK = 8;
+    for (uint32_t i0 = tid; i0 < R * ES; i0 += EK * FT_NT) {
+      uint32_t v[EK], col[EK];
+#pragma unroll
+      for (int q = 0; q < EK; ++q) {
+        const uint32_t i = i0 + (uint32_t)q * FT_NT;
+        v[q] = 0; col[q] = 0;
+        if (i < R * ES) {
+          const uint32_t row = fdiv(i, fe), slot = i - row * ES;
+          if (slot < E) { v[q] = sedge[i]; if (v[q]) col[q] = a.eidx[(uint64_t)(sbase + row) * E + slot]; }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < EK; ++q)
+        if (v[q]) atomicAdd(&a.ew[(uint64_t)w_tile * a.nnz_tot + col[q]], (unsigned long long)v[q]);
     }
   }
   if (nc && tslow) {
