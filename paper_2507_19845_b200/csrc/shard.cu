@@ -366,7 +366,9 @@ scan_status sharded_all(Ctx& c) {
   if (xr) { c.err = std::string("exchange all-gather: ") + xch_error(xr); return SCAN_E_NCCL; }
   CK(cudaMemcpy2DAsync(pin + offA, HL * 4, c.x_recv.p, LA * 4, HL * 4, G, cudaMemcpyDeviceToHost, c.stream));
   CK(cudaEventRecord(c.ev_x1, c.stream));
-  c.launches += timed(c, "k_p2p_set", [&] {
+  // the device-side P2P channel set needs this shard's census: a shard that is not SPMD skips it (its X1
+  // header makes every shard return UNSUPPORTED right after X2; the X2 words it sends are zeros)
+  if (c.spmd) c.launches += timed(c, "k_p2p_set", [&] {
     k_bitmap_or<<<(unsigned)std::min<uint64_t>((nbm + 255) / 256, 4096), 256, 0, c.stream>>>(
         c.x_recv.as<uint32_t>(), LA, HL, nbm, G, c.bitmap.as<uint32_t>());
     launch_rank_prefix(c);  // channel ids = popcount prefix of the job-wide bitmap; n_p2p
@@ -376,10 +378,11 @@ scan_status sharded_all(Ctx& c) {
                                                               c.nbp_n.as<uint32_t>(), c.counters.as<Counters>());
     launch_p2p_counts_to(c, c.ch_nsend.as<uint32_t>(), c.ch_nrecv.as<uint32_t>(), c.x_ep.as<uint32_t>(),
                          c.x_ep.as<uint32_t>() + NPMAX);
-    k_x2_pack<<<(unsigned)std::min<uint64_t>((LB + 255) / 256, 4096), 256, 0, c.stream>>>(
-        c.counters.as<Counters>(), c.ch_nsend.as<uint32_t>(), c.ch_nrecv.as<uint32_t>(), NPMAX, c.x_send.as<uint32_t>());
-    return 6;
+    return 5;
   });
+  k_x2_pack<<<(unsigned)std::min<uint64_t>((LB + 255) / 256, 4096), 256, 0, c.stream>>>(
+      c.counters.as<Counters>(), c.ch_nsend.as<uint32_t>(), c.ch_nrecv.as<uint32_t>(), NPMAX, c.x_send.as<uint32_t>());
+  c.launches += 1;
   CK(cudaMemcpyAsync(pin + offC, c.counters.p, sizeof(Counters), cudaMemcpyDeviceToHost, c.stream));
   CK(cudaEventRecord(c.ev_x2, c.stream));
   timed(c, "x2_allgather", [&] { xr = xch_allgather(c, c.x_send.p, c.x_recv2.p, LB); return 0; });
