@@ -1527,6 +1527,14 @@ struct XArgs {
 
 constexpr uint32_t XBIG = 32;  // cross collectives with more members go to k_cross_big
 
+// warp sum of values < 2^32 (one per lane) as 16-bit halves with single-instruction full-warp
+// reductions: each half sums to < 2^21, no overflow
+__device__ __forceinline__ unsigned long long warp_sum_small(unsigned long long v) {
+  const uint32_t x = (uint32_t)v;
+  const uint32_t lo = __reduce_add_sync(0xFFFFFFFFu, x & 0xFFFFu), hi = __reduce_add_sync(0xFFFFFFFFu, x >> 16);
+  return (unsigned long long)lo + ((unsigned long long)hi << 16);
+}
+
 // edge column of every P2P link direction (the search x_edge would do), once per analysis
 __global__ void k_p2p_eslot(uint32_t n_p2p, const uint32_t* psrc, const uint32_t* pdst, const uint64_t* nbc_off,
                             const uint32_t* nbc, const uint32_t* nbp, const uint32_t* nbp_n, uint64_t nnz_c, uint32_t* out) {
@@ -1561,15 +1569,23 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
   const uint64_t* XB = a.xb_smem ? reinterpret_cast<const uint64_t*>(xb_s) : a.xbase;
   uint32_t inc = 0, kmis = 0, pmis = 0;
   const uint32_t lane = lane_id();
-  const uint64_t wstride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t wbase = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wbase < a.n_xinst; wbase += wstride) {
+  // each warp walks a contiguous chunk of instances (32 per step): consecutive steps stay in one channel,
+  // so the channel search runs only when a step leaves the cached channel
+  const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const uint64_t per = ((a.n_xinst + nwarps - 1) / nwarps + 31) & ~31ull;
+  const uint64_t wend = min(a.n_xinst, (gw + 1) * per);
+  uint64_t ch0 = 0, beg0 = 1, end0 = 0;
+  for (uint64_t wbase = gw * per; wbase < wend; wbase += 32) {
     const uint64_t xi = wbase + lane;
-    bool act = xi < a.n_xinst;
-    // channel of the warp's first instance (one search per warp); lanes past its end search alone
-    uint64_t ch0 = 0, end0 = 0;
-    if (lane == 0) { ch0 = upper_bound_u64(XB, a.NCH + 1, wbase) - 1; end0 = XB[ch0 + 1]; }
-    ch0 = __shfl_sync(0xFFFFFFFFu, ch0, 0);
-    end0 = __shfl_sync(0xFFFFFFFFu, end0, 0);
+    bool act = xi < wend;
+    // channel of the warp's first instance; lanes past its end search alone
+    if (!(wbase >= beg0 && wbase < end0)) {
+      if (lane == 0) { ch0 = upper_bound_u64(XB, a.NCH + 1, wbase) - 1; beg0 = XB[ch0]; end0 = XB[ch0 + 1]; }
+      ch0 = __shfl_sync(0xFFFFFFFFu, ch0, 0);
+      beg0 = __shfl_sync(0xFFFFFFFFu, beg0, 0);
+      end0 = __shfl_sync(0xFFFFFFFFu, end0, 0);
+    }
     uint64_t ch = 0, k = 0, i = 0;
     if (act) {
       ch = xi < end0 ? ch0 : upper_bound_u64(XB, a.NCH + 1, xi) - 1;
@@ -1660,7 +1676,7 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
           const uint32_t tl = __shfl_sync(0xFFFFFFFFu, last, L0), tw = __shfl_sync(0xFFFFFFFFu, ewin, L0);
           const uint32_t tli = __shfl_sync(0xFFFFFFFFu, lsi, L0);
           if (__all_sync(0xFFFFFFFFu, !eg || (last == tl && ewin == tw))) {
-            const unsigned long long ws = warp_sum_u64(eg ? (unsigned long long)ewait : 0ull);
+            const unsigned long long ws = warp_sum_small(eg ? (unsigned long long)ewait : 0ull);
             if (lane == (uint32_t)L0) {
               if (isp) atomicAdd(&a.ew[(uint64_t)tw * a.nnz_tot + a.p2p_eslot[2 * (ch - a.n_comms) + q]], ws);
               else if (a.xe_off[ch] != ~0ull) atomicAdd(&a.ew[(uint64_t)tw * a.nnz_tot + a.xe_col[a.xe_off[ch] + (uint64_t)q * nm + tli]], ws);
@@ -1670,7 +1686,7 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
             x_edge(a, member(q), last, ewin, ewait);
           }
         }
-        w = warp_sum_u64(w); t = warp_sum_u64(t);
+        w = warp_sum_small(w); t = warp_sum_small(t);
         if (lane == 0) {
           const uint32_t m = member(q);
           if (w) atomicAdd(&a.rk_sum[a.W + m], w);
