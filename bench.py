@@ -411,19 +411,33 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # per-kernel CUDA events (library timing mode, recorded on the launch stream) over the timed steps
-    s.set_timing(args.breakdown)
     with ClockSampler(local) as clk:
+        # the step time: K steps with nothing but the analysis between the two events
         ev0.record(stream)
         for _ in range(args.steps):
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
+        launches = s.kernel_launches()
+        # the kernel breakdown: another K steps with the library's per-kernel CUDA events (recorded on the
+        # launch stream around every launch), so their cost never enters the step time above
+        kernels, ms_total_ev = {}, None
+        if args.breakdown:
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            s.set_timing(True)
+            e2a, e2b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e2a.record(stream)
+            for _ in range(args.steps):
+                step()
+            e2b.record(stream)
+            torch.cuda.synchronize()
+            kernels = s.kernel_timing()
+            s.set_timing(False)
+            ms_total_ev = e2a.elapsed_time(e2b)
     gc.enable()
     ms_total = ev0.elapsed_time(ev1)
-    launches = s.kernel_launches()
-    kernels = s.kernel_timing() if args.breakdown else {}
-    s.set_timing(False)
     t_local = torch.tensor([ms_total], dtype=torch.float64, device=f"cuda:{local}")
     n_tot = torch.tensor([float(N)], dtype=torch.float64, device=f"cuda:{local}")
     if dist:
@@ -648,6 +662,9 @@ def main():
                                    "NCCL all-gather + all-to-all + all-reduce inside scan_analyze") if world > 1
                                   else "1 GPU, whole trace",
                    "l2": "inputs (16 B/event, %.1f GB) >> 126 MB L2: no flush needed" % (16 * N / 1e9),
+                   "timing": "step time: K steps between two CUDA events, nothing else recorded; kernel breakdown "
+                             "and roofline: a second K steps with per-kernel CUDA events on the launch stream"
+                             + (f" ({ms_total_ev / args.steps:.3f} ms/step with them)" if ms_total_ev else ""),
                    "generator_s": round(t_gen, 1)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",

@@ -38,16 +38,35 @@ def c3_full():
     bl = s.blame()
     out["bl_suffered"] = s.export("bl_suffered")
     out["bl_inflicted"] = s.export("bl_inflicted")
+    # the general path on the same resident job with one SPMD violation in the LAST iteration (an op id
+    # changed on rank 300): the fused pass rejects the job and the call reruns the general path; the
+    # sampled windows before it are unaffected by the change
+    ro = tr.rank_offsets.astype(np.int64)
+    tail = tr.kind_op[int(ro[301]) - 200:int(ro[301])]
+    e_bad = int(ro[301]) - 200 + int(np.flatnonzero(((tail & 7) == 0) & ((tail & 8) == 0))[-1])
+    old_k = dev["kind_op"][e_bad].item()
+    new_k = ((old_k & 0xFFFF) ^ (9 << 4)) & 0xFFFF
+    dev["kind_op"][e_bad] = new_k - 0x10000 if new_k >= 0x8000 else new_k
+    res_g = s.analyze(ms.DetectConfig(want_ref=True))
+    out_g = {k: s.export(k) for k in ("ev_wait", "ev_slow", "ev_ref", "rk_sum_compute", "rk_sum_wait", "rk_sum_transfer",
+                                      "wl_verdict", "wd_total")}
+    out_g["_res"] = res_g
+    dev["kind_op"][e_bad] = old_k
     s.close()
     del dev
     torch.cuda.empty_cache()
+    out["_general"] = out_g
     return cfg, tr, res, out, bl
 
 
-@pytest.mark.parametrize("b,e", [(0, 2), (550, 552), (999, 1000)])
-def test_c3_sampled_iterations_equal_the_oracle(c3_full, b, e):
+@pytest.mark.parametrize("b,e,path", [(0, 2, "fused"), (550, 552, "fused"), (999, 1000, "fused"),
+                                       (0, 2, "general"), (550, 552, "general")])
+def test_c3_sampled_iterations_equal_the_oracle(c3_full, b, e, path):
     cfg, tr, res, out, _ = c3_full
     assert res["fused"]  # the bench's path
+    if path == "general":
+        assert not out["_general"]["_res"]["fused"]  # the violation sent the job to the general path
+        out = out["_general"]
     sl = tg.generate(cfg, with_start=False, iter_range=(b, e))
     o = oracle.run(sl, oracle.Config())
     pre = tg.count(cfg, (0, b)).astype(np.int64) if b else np.zeros(tr.world + 1, np.int64)  # (0, 0) = whole trace
@@ -60,6 +79,8 @@ def test_c3_sampled_iterations_equal_the_oracle(c3_full, b, e):
         bad = np.flatnonzero(g != o[k])
         assert len(bad) == 0, f"{k}: {len(bad)} diffs, first {bad[:5]}: gpu {g[bad[:5]]} oracle {o[k][bad[:5]]}"
     comm = (sl.kind_op & 7) != 0
+    if "ev_inst" not in out:
+        return
     gi, oi = out["ev_inst"][idx][comm], o["ev_inst"][comm]
     assert np.array_equal(np.unique(gi, return_inverse=True)[1], np.unique(oi, return_inverse=True)[1])
     if b == 550:  # rank 862 (x2.5 on [500, 900)) is slow against its DP peers on every kernel
@@ -82,6 +103,18 @@ def test_c3_properties_at_full_size(c3_full):
     assert out["wl_verdict"][862] in (1, 3)  # ComputeSlow / Both
     assert np.array_equal(out["bl_suffered"], out["rk_sum_wait"])  # blame conservation (EB5)
     assert bl["top_rank"] == 862 and bl["n_cyclic"] == 0
+
+
+def test_c3_general_path_rank_level(c3_full):
+    """The general path's rank-level outputs at full size: compute / wait + transfer sums equal numpy
+    sums of the raw durations (the changed op id leaves durations and instances as they are), the same
+    stage-1 totals and the same verdicts as the fused pass on the unmodified job."""
+    cfg, tr, res, out, _ = c3_full
+    g = out["_general"]
+    assert not g["_res"]["fused"]
+    for k in ("rk_sum_compute", "rk_sum_wait", "rk_sum_transfer"):
+        assert np.array_equal(g[k], out[k]), k
+    assert g["wl_verdict"][862] in (1, 3) and int(g["wd_total"].sum()) > 0
 
 
 def test_json_bench_workload_sampled_files():
