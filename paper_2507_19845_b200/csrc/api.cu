@@ -98,13 +98,13 @@ static void release_all(Ctx& c) {
                     &c.t_prevj, &c.r_nkeys, &c.r_keys, &c.r_cnt, &c.r_ncomm, &c.r_niter, &c.r_ncomp, &c.r_lastit,
                     &c.r_comm_off, &c.r_comp_off, &c.r_bits_off, &c.bitmap, &c.bitpre, &c.bmsum, &c.counters, &c.ch_nmax,
                     &c.ch_nmin, &c.ch_base, &c.ch_slot, &c.ch_nsend, &c.ch_nrecv, &c.inst_c, &c.wait_c, &c.cdur, &c.cop,
-                    &c.sdur, &c.skind, &c.p2p_pay, &c.p2p_warm, &c.p2p_iter, &c.inst_rec, &c.citer, &c.nbp, &c.nbp_n,
+                    &c.slots, &c.inst_rec, &c.citer, &c.nbp, &c.nbp_n,
                     &c.rk_sum, &c.bits, &c.cref, &c.cl_J, &c.cl_max, &c.cl_min, &c.wd_total, &c.wd_slow, &c.wd_cand,
                     &c.wd_frac, &c.wl_joined, &c.wl_late, &c.wl_frac, &c.wl_verdict, &c.wl_link_slow, &c.ewc, &c.ewp,
                     &c.lk_n, &c.lk_used, &c.lk_medp, &c.lk_medt, &c.lk_bw, &c.lk_slow, &c.lk_dir, &c.lk_elig,
                     &c.lb_label, &c.lb_rkind, &c.lb_rrank, &c.lb_rsrc, &c.lb_depth, &c.lb_twait, &c.scratch,
                     &c.st_tile0, &c.st_npos, &c.role_comm, &c.role_slot, &c.role_type, &c.ncroles, &c.ft_cols,
-                    &c.ft_base, &c.ft_last, &c.st_tot, &c.sci, &c.sit, &c.dlate, &c.dinfo, &c.ft_posA, &c.ft_posB,
+                    &c.ft_base, &c.ft_last, &c.st_tot, &c.p2p_rbase, &c.dlate, &c.dinfo, &c.ft_posA, &c.ft_posB,
                     &c.ft_posK, &c.eidx, &c.tile_stage, &c.xbase, &c.lk_scratch, &c.g_base, &c.g_slot,
                     &c.g_nmax, &c.g_nmin, &c.g_k0, &c.p2p_eslot, &c.xe_off, &c.xe_col, &c.xbig, &c.own_start, &c.al_tend, &c.al_aend, &c.al_anct,
                     &c.al_anco, &c.al_slotci, &c.al_level, &c.al_nanc, &c.al_resid, &c.al_flag, &c.al_start, &c.al_ranks, &c.al_cch, &c.al_tgt, &c.x_send, &c.x_recv, &c.x_recv2, &c.x_ep, &c.x_stage, &c.headtail, &c.lk_sendmap, &c.lk_recvmap, &c.bl_inst, &c.bl_wait, &c.bl_p0, &c.bl_pa, &c.bl_pb, &c.bl_root, &c.bl_last, &c.bl_rank, &c.bl_rk};
@@ -474,14 +474,12 @@ scan_status ms::alloc_match_buffers(Ctx& c, bool fused) {
   const uint64_t W = c.W;
   CK(c.inst_c.ensure(c.n_comm * 4)); CK(c.wait_c.ensure(c.n_comm * 4));
   if (!fused) { CK(c.cdur.ensure(c.n_comp * 4)); CK(c.cop.ensure(c.n_comp * 2)); }
-  CK(c.sdur.ensure(c.n_slots * 4)); CK(c.skind.ensure(c.n_slots));
-  if (fused) { CK(c.sci.ensure(c.n_slots * 4)); CK(c.sit.ensure(c.n_slots * 4)); }
-  const uint64_t np_slots = c.n_slots - c.p2p_slot0, np_inst = c.n_inst - c.p2p_inst0;
-  CK(c.p2p_pay.ensure(np_slots * 4)); CK(c.p2p_warm.ensure(np_inst)); CK(c.p2p_iter.ensure(np_inst * 4));
+  if ((uint64_t)c.it_off + c.n_iters >= SLOT_MAX_ITERS) { c.err = "more than 2^28 iterations"; return SCAN_E_UNSUPPORTED; }
+  CK(c.slots.ensure(c.n_slots * 16));
+  if (fused) CK(c.p2p_rbase.ensure(W * 16 * 4));
   CK(c.inst_rec.ensure(c.n_inst * 16));
   const uint32_t NIT1 = c.NIT + 1;
   CK(c.citer.ensure(W * NIT1 * 4));
-  queue_fill(c, c.p2p_warm.p, np_inst, 0);
   const uint64_t n = W * NIT1;
   if (fused) return SCAN_OK;  // citer (compute index of each iteration start) is read by the general path only
   flush_fills(c);
@@ -682,6 +680,7 @@ scan_status ms::fused_all(Ctx& c) {
     queue_fill(c, c.wd_slow.p, items * 4, 0);
   }
   c.launches += timed(c, "k_class_counts", [&] { return launch_class_counts(c); });
+  c.launches += timed(c, "k_p2p_roles", [&] { return launch_p2p_roles(c); });
   c.launches += timed(c, stage_active(c) ? "k_stage" : "k_fused", [&] { return launch_fused(c); });
   c.launches += timed(c, "k_cross_reduce", [&] { return launch_cross_reduce(c); });
   c.launches += timed(c, "k_deferred", [&] { return launch_deferred(c); });

@@ -24,6 +24,24 @@ constexpr int CROLES = 16;
 constexpr int FCOLS = ROLES + 4;  // per-tile pre-pass columns: roles, ncomp, ncomm, niter, cc_last
 constexpr uint32_t NOT_SPMD = 32u;  // Counters.overflow bit: fused path not applicable
 
+// Member slot record (uint4), one per member slot of every instance, in slot order
+// (slot = slot_base(channel) + k * |members| + member; a P2P instance i has its send slot at
+// p2p_slot0 + 2 (i - p2p_inst0) and its receive slot right after it):
+//   x  the member event's duration; after the instance reduction (k_inst_reduce / k_cross_reduce)
+//      the member's wait
+//   y  fused path: the member event's index among its rank's comm events (k_xwait_scatter)
+//   z  global iteration (bits 0-27) | kind (bits 28-30) | sender's warm-up flag (bit 31, P2P send slot)
+//   w  P2P slots: payload bytes (k_stage leaves the event's position in its rank there and
+//      k_cross_reduce gathers the payload)
+// One 16-byte store per member instead of five scattered arrays: a P2P instance's two slots are one
+// 32-byte sector.
+constexpr uint32_t SLOT_IT_MASK = 0x0FFFFFFFu;
+constexpr uint32_t SLOT_MAX_ITERS = 1u << 28;
+__device__ __forceinline__ uint32_t slot_z(uint32_t it, uint32_t kind, uint32_t warm) {
+  return it | ((kind & 7u) << 28) | (warm << 31);
+}
+__device__ __forceinline__ uint32_t slot_kind(uint32_t z) { return (z >> 28) & 7u; }
+
 // ----------------------------------------------------------------------------- device buffers
 struct DevBuf {
   void* p = nullptr;
@@ -110,7 +128,7 @@ struct Ctx {
   uint32_t n_iters = 0;
   DevBuf inst_c, wait_c;                 // per comm event
   DevBuf cdur, cop;                      // per compute event (rank-compacted)
-  DevBuf sdur, skind, p2p_pay, p2p_warm, p2p_iter;  // per slot / per P2P instance
+  DevBuf slots;                          // SlotRec (uint4) per member slot, slot order
   DevBuf inst_rec;                       // uint4 per instance {dmin, dmax, last_rank, flags | cls<<8}
   DevBuf citer;                          // u32 [W][NIT+1]
   DevBuf nbp, nbp_n;                     // P2P neighbours per rank [W][PCAP]
@@ -145,7 +163,7 @@ struct Ctx {
   DevBuf st_tile0, st_npos, role_comm, role_slot, role_type, ncroles;
   DevBuf ft_cols, ft_base, ft_last, st_tot;   // pre-pass counts [FCOLS][tiles], scanned bases, last comm, stage totals
   DevBuf ft_posA, ft_posB, ft_posK;           // per template position packed info + template kind_op
-  DevBuf sci, sit;                       // per slot: comm index, iteration of the member event (cross instances)
+  DevBuf p2p_rbase;                      // u32 [W][16]: instance base of the P2P channel behind each P2P role
   DevBuf dlate, dinfo;                   // deferred stage-2 positions (first comm position of a tile)
   bool rows_aligned = false, rows_aligned8 = false;
   bool force_general = false;
@@ -423,6 +441,7 @@ int launch_instance_export(Ctx& c, scan_output which, void* dst);
 int launch_fused_prepass(Ctx& c);
 int launch_fused_census(Ctx& c);
 int launch_fused(Ctx& c);
+int launch_p2p_roles(Ctx& c);
 int launch_stage(Ctx& c);
 // the analysis runs k_stage: selected at load and the channel bases fit its 32-bit tables
 inline bool stage_active(const Ctx& c) { return c.use_stage && c.n_inst < (1ull << 32) && c.n_slots < (1ull << 32); }

@@ -76,7 +76,7 @@ int launch_expand_events(Ctx& c, scan_output which, void* dst) {
 __global__ void k_inst_export(uint64_t n_inst, uint64_t NCH, uint32_t n_comms, const uint64_t* ch_base,
                               const uint64_t* ch_slot, const uint32_t* ch_nmin, const uint64_t* coff, const uint32_t* cmem,
                               const uint32_t* nsend, const uint32_t* nrecv, const uint32_t* r_nkeys, const uint32_t* r_keys,
-                              const uint32_t* r_cnt, const uint4* rec, const uint32_t* p2p_pay, uint64_t p2p_slot0,
+                              const uint32_t* r_cnt, const uint4* rec, const uint4* slots,
                               const uint64_t* kshift, int which, void* dst) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_inst; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t ch = upper_bound_u64(ch_base, NCH + 1, i) - 1;
@@ -112,9 +112,9 @@ __global__ void k_inst_export(uint64_t n_inst, uint64_t NCH, uint32_t n_comms, c
       case SCAN_OUT_IN_PAYLOAD: {
         uint32_t v = 0;
         if (isp) {
-          const uint64_t sb = ch_slot[ch] + k * 2 - p2p_slot0;
-          if (nsend[ch - n_comms] > kl) v = p2p_pay[sb];
-          else if (nrecv[ch - n_comms] > kl) v = p2p_pay[sb + 1];
+          const uint64_t sb = ch_slot[ch] + k * 2;
+          if (nsend[ch - n_comms] > kl) v = slots[sb].w;
+          else if (nrecv[ch - n_comms] > kl) v = slots[sb + 1].w;
         }
         ((uint32_t*)dst)[i] = v;
         break;
@@ -134,7 +134,7 @@ int launch_instance_export(Ctx& c, scan_output which, void* dst) {
                                               c.ch_nmin.as<uint32_t>(), c.coff.as<uint64_t>(), c.cmem.as<uint32_t>(),
                                               c.ch_nsend.as<uint32_t>(), c.ch_nrecv.as<uint32_t>(), c.r_nkeys.as<uint32_t>(),
                                               c.r_keys.as<uint32_t>(), c.r_cnt.as<uint32_t>(), c.inst_rec.as<uint4>(),
-                                              c.p2p_pay.as<uint32_t>(), c.p2p_slot0, sh ? c.g_k0.as<uint64_t>() : nullptr,
+                                              c.slots.as<uint4>(), sh ? c.g_k0.as<uint64_t>() : nullptr,
                                               (int)which, dst);
   return 1;
 }

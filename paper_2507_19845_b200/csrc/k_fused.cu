@@ -287,7 +287,7 @@ struct FusedArgs {
   const uint64_t* ch_base; const uint64_t* ch_slot; const uint32_t* bitmap; const uint32_t* bitpre;
   const uint64_t* comm_off; const uint64_t* comp_off; const uint64_t* bits_off;
   uint32_t* inst_c; uint32_t* wait_c; uint32_t* bits; uint32_t* cref; uint4* rec;
-  uint32_t* sdur; uint8_t* skind; uint32_t* sci; uint32_t* sit; uint32_t* p2p_pay; uint8_t* p2p_warm; uint32_t* p2p_iter;
+  uint4* slots; const uint32_t* p2p_rbase;  // SlotRec per member slot; instance base per (rank, P2P role)
   uint64_t p2p_slot0, p2p_inst0;
   uint32_t* citer; uint32_t NIT1;
   const uint64_t* nbc_off; const uint32_t* nbc; const uint32_t* nbp; const uint32_t* nbp_n; uint64_t nnz_tot, nnz_c;
@@ -653,37 +653,25 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
       const uint32_t A = pa[p], B = pb[p];
       const uint32_t role = (B >> 20) & 31u;
       const uint64_t e = rbase + (uint64_t)row * npos + p0 + p;
-      uint64_t ch; uint32_t nm, slot;
-      bool send = false;
+      const uint32_t kk = kbase[role] + ((B >> 10) & 1023u);
+      uint64_t inst, si;
+      uint32_t pay = 0, warm = 0;
       if (role < 16) {
         const uint32_t cid = rcs[row * NCRM + role];
-        ch = cid; nm = (uint32_t)(a.coff[cid + 1] - a.coff[cid]); slot = a.role_slot[(uint64_t)r * CROLES + role];
-      } else {
-        const int ds = (int)(role & 7u) - 4;
-        send = (role >> 3) & 1u;
-        const uint32_t peer = (uint32_t)((int)r + ds * (int)R);
-        const uint32_t src = send ? r : peer, dst = send ? peer : r;
-        const uint32_t xk = src * (uint32_t)a.W + dst;
-        ch = a.n_comms + a.bitpre[xk >> 5] + __popc(a.bitmap[xk >> 5] & ((1u << (xk & 31)) - 1u));
-        nm = 2; slot = send ? 0 : 1;
+        const uint32_t nm = (uint32_t)(a.coff[cid + 1] - a.coff[cid]);
+        inst = a.ch_base[cid] + kk;
+        si = a.ch_slot[cid] + (uint64_t)kk * nm + a.role_slot[(uint64_t)r * CROLES + role];
+      } else {  // a P2P instance's send / receive slots sit at p2p_slot0 + 2 (inst - p2p_inst0) + 0 / 1
+        const bool send = (role >> 3) & 1u;
+        inst = (uint64_t)a.p2p_rbase[(uint64_t)r * 16 + (role - 16)] + kk;
+        si = a.p2p_slot0 + 2 * (inst - a.p2p_inst0) + (send ? 0 : 1);
+        pay = a.pay[e];
+        if (send) warm = ((uint32_t)a.meta[e] >> 14) & 1u;
       }
-      const uint32_t kk = kbase[role] + ((B >> 10) & 1023u);
-      const uint64_t inst = a.ch_base[ch] + kk;
-      const uint64_t si = a.ch_slot[ch] + (uint64_t)kk * nm + slot;
       const uint32_t idx = sw_idx(row, p, T);
       const uint32_t itp = itg0 + (B & 1023u);
-      a.sdur[si] = sd[idx];
-      a.skind[si] = (uint8_t)(pk[p] & 7u);
-      a.sci[si] = (uint32_t)(coffr[row] + m0 + ((A >> 10) & 1023u));
-      a.sit[si] = itp;
+      a.slots[si] = make_uint4(sd[idx], (uint32_t)(coffr[row] + m0 + ((A >> 10) & 1023u)), slot_z(itp, pk[p], warm), pay);
       sd[idx] = (uint32_t)inst;  // cross positions: the tile now holds the instance id
-      if (role >= 16) {
-        a.p2p_pay[si - a.p2p_slot0] = a.pay[e];
-        if (send) {
-          a.p2p_warm[inst - a.p2p_inst0] = (uint8_t)((a.meta[e] >> 14) & 1u);
-          a.p2p_iter[inst - a.p2p_inst0] = itp;
-        }
-      }
     }
   }
   __syncthreads();
@@ -1113,35 +1101,23 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
         const uint32_t row = lane + 32 * kb;
         if (row >= R) continue;
         const uint32_t r = sbase + row;
-        uint64_t ch; uint32_t nm, slot;
-        bool send = false;
+        uint64_t inst, si;
+        uint32_t pay = 0, warm = 0;
         if (role < 16) {
           const uint32_t cid = rcs[row * NCRM + role];
-          ch = cid; nm = (uint32_t)(a.coff[cid + 1] - a.coff[cid]); slot = a.role_slot[(uint64_t)r * CROLES + role];
-        } else {
-          const int ds = (int)(role & 7u) - 4;
-          send = (role >> 3) & 1u;
-          const uint32_t peer = (uint32_t)((int)r + ds * (int)R);
-          const uint32_t src = send ? r : peer, dst = send ? peer : r;
-          const uint32_t xk = src * (uint32_t)a.W + dst;
-          ch = a.n_comms + a.bitpre[xk >> 5] + __popc(a.bitmap[xk >> 5] & ((1u << (xk & 31)) - 1u));
-          nm = 2; slot = send ? 0 : 1;
+          const uint32_t nm = (uint32_t)(a.coff[cid + 1] - a.coff[cid]);
+          inst = rcb[row * NCRM + role] + kk;
+          si = a.ch_slot[cid] + (uint64_t)kk * nm + a.role_slot[(uint64_t)r * CROLES + role];
+        } else {  // a P2P instance's send / receive slots sit at p2p_slot0 + 2 (inst - p2p_inst0) + 0 / 1
+          const bool send = (role >> 3) & 1u;
+          const uint64_t e = rbase + (uint64_t)row * npos + p0 + p;
+          inst = (uint64_t)a.p2p_rbase[(uint64_t)r * 16 + (role - 16)] + kk;
+          si = a.p2p_slot0 + 2 * (inst - a.p2p_inst0) + (send ? 0 : 1);
+          pay = a.pay[e];
+          if (send) warm = ((uint32_t)a.meta[e] >> 14) & 1u;
         }
-        const uint64_t inst = a.ch_base[ch] + kk;
-        const uint64_t si = a.ch_slot[ch] + (uint64_t)kk * nm + slot;
-        const uint64_t e = rbase + (uint64_t)row * npos + p0 + p;
-        a.sdur[si] = col[row];
-        a.skind[si] = (uint8_t)(pk[p] & 7u);
-        a.sci[si] = (uint32_t)(coffr[row] + m0 + jj);
-        a.sit[si] = itp;
+        a.slots[si] = make_uint4(col[row], (uint32_t)(coffr[row] + m0 + jj), slot_z(itp, pk[p], warm), pay);
         col[row] = (uint32_t)inst;  // cross positions: the tile now holds the instance id
-        if (role >= 16) {
-          a.p2p_pay[si - a.p2p_slot0] = a.pay[e];
-          if (send) {
-            a.p2p_warm[inst - a.p2p_inst0] = (uint8_t)((a.meta[e] >> 14) & 1u);
-            a.p2p_iter[inst - a.p2p_inst0] = itp;
-          }
-        }
       }
       continue;
     }
@@ -1409,6 +1385,34 @@ size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32
   return (b + 15) & ~size_t(15);
 }
 
+// Instance base of the P2P channel behind every (rank, P2P role) -- role 16 + 8 send + stage delta + 4 --
+// or NONE32 where the role names no channel, so the fused kernels place a P2P member without the
+// per-event bitmap search and channel lookups
+__global__ void k_p2p_roles(int W, uint32_t R, uint32_t n_comms, const uint32_t* bitmap, const uint32_t* bitpre,
+                            const uint64_t* ch_base, uint32_t* out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (uint32_t)W * 16u) return;
+  const uint32_t r = i >> 4, x = i & 15u;
+  const bool send = x >> 3;
+  const int peer = (int)r + ((int)(x & 7u) - 4) * (int)R;
+  uint32_t v = NONE32;
+  if (peer >= 0 && peer < W) {
+    const uint32_t src = send ? r : (uint32_t)peer, dst = send ? (uint32_t)peer : r;
+    const uint32_t xk = src * (uint32_t)W + dst;
+    const uint32_t bm = bitmap[xk >> 5];
+    if ((bm >> (xk & 31)) & 1u) v = (uint32_t)ch_base[n_comms + bitpre[xk >> 5] + __popc(bm & ((1u << (xk & 31)) - 1u))];
+  }
+  out[i] = v;
+}
+
+int launch_p2p_roles(Ctx& c) {  // c.p2p_rbase sized by alloc_match_buffers
+  if (c.n_p2p == 0) return 0;
+  const uint32_t n = (uint32_t)c.W * 16u;
+  k_p2p_roles<<<(n + 255) / 256, 256, 0, c.stream>>>(c.W, c.FR, c.n_comms, c.bitmap.as<uint32_t>(), c.bitpre.as<uint32_t>(),
+                                                     c.ch_base.as<uint64_t>(), c.p2p_rbase.as<uint32_t>());
+  return 1;
+}
+
 int launch_fused(Ctx& c) {
   if (stage_active(c)) {  // the persistent TMA-fed kernel (k_stage.cu)
     const int n = launch_stage(c);
@@ -1431,8 +1435,7 @@ int launch_fused(Ctx& c) {
   a.bitpre = c.bitpre.as<uint32_t>(); a.comm_off = c.r_comm_off.as<uint64_t>(); a.comp_off = c.r_comp_off.as<uint64_t>();
   a.bits_off = c.r_bits_off.as<uint64_t>(); a.inst_c = c.inst_c.as<uint32_t>(); a.wait_c = c.wait_c.as<uint32_t>();
   a.bits = c.bits.as<uint32_t>(); a.cref = c.cref.as<uint32_t>(); a.rec = c.inst_rec.as<uint4>();
-  a.sdur = c.sdur.as<uint32_t>(); a.skind = c.skind.as<uint8_t>(); a.sci = c.sci.as<uint32_t>(); a.sit = c.sit.as<uint32_t>();
-  a.p2p_pay = c.p2p_pay.as<uint32_t>(); a.p2p_warm = c.p2p_warm.as<uint8_t>(); a.p2p_iter = c.p2p_iter.as<uint32_t>();
+  a.slots = c.slots.as<uint4>(); a.p2p_rbase = c.p2p_rbase.as<uint32_t>();
   a.p2p_slot0 = c.p2p_slot0; a.p2p_inst0 = c.p2p_inst0; a.citer = c.citer.as<uint32_t>(); a.NIT1 = c.NIT + 1;
   {  // L2 prefetches of the transposed kernel. Measured on full C3 (k_fused_t ms): none 8.51; own tile
      // at kernel start 8.22 (default); tile pf ahead after the load pass: 96 8.32, 148 8.35, 296 8.93;
@@ -1508,10 +1511,8 @@ struct XArgs {
   const uint64_t* ch_base; const uint64_t* ch_slot; const uint32_t* ch_nmin; const uint64_t* coff; const uint32_t* cmem;
   const uint8_t* ccls; const uint32_t* nsend; const uint32_t* nrecv; const uint32_t* psrc; const uint32_t* pdst;
   const uint32_t* r_nkeys; const uint32_t* r_keys; const uint32_t* r_cnt;
-  const uint32_t* sdur; const uint8_t* skind; const uint32_t* sci; const uint32_t* sit; const uint32_t* p2p_pay;
-  const uint8_t* p2p_warm; uint64_t p2p_slot0, p2p_inst0;
+  uint4* slots;  // SlotRec; after the reduction a member slot's x holds that member's wait (instance order)
   uint4* rec; uint32_t* wait_c;
-  uint32_t* swait;  // = sdur: after the reduction a member slot holds that member's wait (instance order)
   const uint64_t* nbc_off; const uint32_t* nbc; const uint32_t* nbp; const uint32_t* nbp_n; uint64_t nnz_tot, nnz_c;
   unsigned long long* ew; unsigned long long* rk_sum; uint32_t wi; unsigned long long wait_margin;
   Counters* cnt;
@@ -1519,11 +1520,14 @@ struct XArgs {
   int xb_smem;                // xbase staged in shared memory (NCH + 1 entries)
   const uint64_t* xe_off;     // [n_comms] offset of a cross collective's member x member edge-column table, ~0 = none
   const uint32_t* xe_col;     // table[q * nm + t]: edge column of member q waiting on member t
-  // k_stage leaves each P2P member's position within its rank in p2p_pay: gather the payload and the
-  // sender's warm-up bit here (latency-tolerant grid) instead of between the fused kernel's barriers
+  // k_stage leaves each P2P member's position within its rank in the slot's w: gather the payload and
+  // the sender's warm-up bit here (latency-tolerant grid) instead of between the fused kernel's barriers
   int p2p_pos; const uint32_t* pay; const uint16_t* meta; const uint64_t* rank_off;
-  uint32_t* p2p_pay_w; uint8_t* p2p_warm_w;
 };
+
+__device__ __forceinline__ void slot_set_wait(uint4* slots, uint64_t si, uint32_t wait) {
+  reinterpret_cast<uint32_t*>(slots + si)[0] = wait;
+}
 
 constexpr uint32_t XBIG = 32;  // cross collectives with more members go to k_cross_big
 
@@ -1610,24 +1614,37 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
     };
     uint32_t flags = 0, dmin = 0, dmax = 0, last = NONE32, lsi = 0;
     bool valid = false;
-    if (act && isp && a.p2p_pos) {
-      for (uint32_t q = 0; q < 2; ++q) {
-        if (!(k < a.ch_nmin[ch] || present(q))) continue;
-        const uint64_t e = a.rank_off[member(q)] + a.p2p_pay[sb + q - a.p2p_slot0];
-        a.p2p_pay_w[sb + q - a.p2p_slot0] = a.pay[e];
-        if (q == 0) a.p2p_warm_w[i - a.p2p_inst0] = (uint8_t)((a.meta[e] >> 14) & 1u);
+    // a P2P instance's send and receive slots: one 32-byte sector, read once
+    uint4 s0 = make_uint4(0, 0, 0, 0), s1 = s0;
+    if (act && isp) {
+      const bool h0 = a.nsend[ch - a.n_comms] > k, h1 = a.nrecv[ch - a.n_comms] > k;
+      if (h0) s0 = a.slots[sb];
+      if (h1) s1 = a.slots[sb + 1];
+      if (a.p2p_pos) {
+        if (h0) {
+          const uint64_t e = a.rank_off[member(0)] + s0.w;
+          s0.w = a.pay[e];
+          s0.z = (s0.z & 0x7FFFFFFFu) | (((uint32_t)a.meta[e] >> 14) & 1u) << 31;
+          reinterpret_cast<uint32_t*>(a.slots + sb)[3] = s0.w;
+        }
+        if (h1) {
+          s1.w = a.pay[a.rank_off[member(1)] + s1.w];
+          reinterpret_cast<uint32_t*>(a.slots + sb + 1)[3] = s1.w;
+        }
       }
+      if (s0.z >> 31) flags |= SCAN_F_WARMUP;  // the sender's flag (0 when the send is absent)
     }
+    auto sdur = [&](uint32_t q) -> uint32_t { return isp ? (q ? s1.x : s0.x) : a.slots[sb + q].x; };
+    auto sit = [&](uint32_t q) -> uint32_t { return (isp ? (q ? s1.z : s0.z) : a.slots[sb + q].z) & SLOT_IT_MASK; };
     if (act) {
-      if (isp && a.p2p_warm[i - a.p2p_inst0]) flags |= SCAN_F_WARMUP;
       if (k < a.ch_nmin[ch]) {
         flags |= SCAN_F_COMPLETE;
         bool kind_ok = true, pay_ok = true;
         if (!isp) {
-          const uint8_t k0 = a.skind[sb];
-          for (uint32_t q = 1; q < nm; ++q) if (a.skind[sb + q] != k0) kind_ok = false;
+          const uint32_t k0 = slot_kind(a.slots[sb].z);
+          for (uint32_t q = 1; q < nm; ++q) if (slot_kind(a.slots[sb + q].z) != k0) kind_ok = false;
         } else {
-          pay_ok = a.p2p_pay[sb - a.p2p_slot0] == a.p2p_pay[sb + 1 - a.p2p_slot0];
+          pay_ok = s0.w == s1.w;
         }
         if (kind_ok) flags |= SCAN_F_KIND_OK; else ++kmis;
         if (pay_ok) flags |= SCAN_F_PAYLOAD_OK; else ++pmis;
@@ -1637,7 +1654,7 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
           dmin = NONE32;
           uint32_t ls = 0, nat = 0;
           for (uint32_t q = 0; q < nm; ++q) {
-            const uint32_t d = a.sdur[sb + q];
+            const uint32_t d = sdur(q);
             if (d < dmin) { dmin = d; ls = q; nat = 1; } else if (d == dmin) ++nat;
             dmax = max(dmax, d);
           }
@@ -1659,14 +1676,14 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
         bool eg = false;
         uint32_t ewin = 0, ewait = 0;
         if (act && (flags & SCAN_F_COMPLETE || present(q))) {
-          if (!valid) a.swait[sb + q] = 0;
+          if (!valid) slot_set_wait(a.slots, sb + q, 0);
           else {
             const uint32_t m = member(q);
-            const uint32_t wait = a.sdur[sb + q] - dmin;
-            a.swait[sb + q] = wait;
+            const uint32_t wait = sdur(q) - dmin;
+            slot_set_wait(a.slots, sb + q, wait);
             w = wait; t = dmin;
             if (m != last && (unsigned long long)wait > a.wait_margin) {
-              eg = true; ewait = wait; ewin = a.wi ? a.sit[sb + q] / a.wi : 0;
+              eg = true; ewait = wait; ewin = a.wi ? sit(q) / a.wi : 0;
             }
           }
         }
@@ -1696,13 +1713,13 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
     } else if (act) {
       for (uint32_t q = 0; q < nm; ++q) {
         if (!(flags & SCAN_F_COMPLETE) && !present(q)) continue;
-        if (!valid) { a.swait[sb + q] = 0; continue; }
+        if (!valid) { slot_set_wait(a.slots, sb + q, 0); continue; }
         const uint32_t m = member(q);
-        const uint32_t wait = a.sdur[sb + q] - dmin;
-        a.swait[sb + q] = wait;
+        const uint32_t wait = sdur(q) - dmin;
+        slot_set_wait(a.slots, sb + q, wait);
         if (wait) atomicAdd(&a.rk_sum[a.W + m], (unsigned long long)wait);
         if (dmin) atomicAdd(&a.rk_sum[2 * a.W + m], (unsigned long long)dmin);
-        if (m != last && (unsigned long long)wait > a.wait_margin) x_edge(a, m, last, a.wi ? a.sit[sb + q] / a.wi : 0, wait);
+        if (m != last && (unsigned long long)wait > a.wait_margin) x_edge(a, m, last, a.wi ? sit(q) / a.wi : 0, wait);
       }
     }
   }
@@ -1716,18 +1733,26 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
 
 __global__ void k_cross_big(XArgs a, const uint32_t* big, uint32_t n_big);
 
+static XArgs cross_args(Ctx& c) {
+  XArgs a{};
+  a.n_xinst = c.n_xinst; a.NCH = c.NCH; a.n_comms = c.n_comms; a.W = c.W; a.xbase = c.xbase.as<uint64_t>();
+  a.ch_base = c.ch_base.as<uint64_t>(); a.ch_slot = c.ch_slot.as<uint64_t>(); a.ch_nmin = c.ch_nmin.as<uint32_t>();
+  a.coff = c.coff.as<uint64_t>(); a.cmem = c.cmem.as<uint32_t>(); a.ccls = c.ccls.as<uint8_t>();
+  a.nsend = c.ch_nsend.as<uint32_t>(); a.nrecv = c.ch_nrecv.as<uint32_t>();
+  a.psrc = c.ch_nsend.as<uint32_t>() + c.n_p2p; a.pdst = c.ch_nrecv.as<uint32_t>() + c.n_p2p;
+  a.r_nkeys = c.r_nkeys.as<uint32_t>(); a.r_keys = c.r_keys.as<uint32_t>(); a.r_cnt = c.r_cnt.as<uint32_t>();
+  a.slots = c.slots.as<uint4>(); a.rec = c.inst_rec.as<uint4>(); a.wait_c = c.wait_c.as<uint32_t>();
+  a.nbc_off = c.nbc_off.as<uint64_t>(); a.nbc = c.nbc.as<uint32_t>(); a.nbp = c.nbp.as<uint32_t>(); a.nbp_n = c.nbp_n.as<uint32_t>();
+  a.nnz_tot = c.nnz_c + (uint64_t)c.W * PCAP; a.nnz_c = c.nnz_c;
+  a.ew = c.ewc.as<unsigned long long>(); a.rk_sum = c.rk_sum.as<unsigned long long>();
+  a.wi = c.dcfg.window_iters; a.wait_margin = (unsigned long long)c.lcfg.wait_margin_ns; a.cnt = c.counters.as<Counters>();
+  a.p2p_eslot = c.p2p_eslot.as<uint32_t>(); a.xb_smem = 0; a.xe_off = c.xe_off.as<uint64_t>(); a.xe_col = c.xe_col.as<uint32_t>();
+  a.p2p_pos = stage_active(c) ? 1 : 0; a.pay = c.d_pay; a.meta = c.d_meta; a.rank_off = c.rank_off.as<uint64_t>();
+  return a;
+}
+
 int launch_cross_reduce(Ctx& c) {
-  XArgs a{c.n_xinst, c.NCH, c.n_comms, c.W, c.xbase.as<uint64_t>(), c.ch_base.as<uint64_t>(), c.ch_slot.as<uint64_t>(), c.ch_nmin.as<uint32_t>(),
-          c.coff.as<uint64_t>(), c.cmem.as<uint32_t>(), c.ccls.as<uint8_t>(), c.ch_nsend.as<uint32_t>(),
-          c.ch_nrecv.as<uint32_t>(), c.ch_nsend.as<uint32_t>() + c.n_p2p, c.ch_nrecv.as<uint32_t>() + c.n_p2p,
-          c.r_nkeys.as<uint32_t>(), c.r_keys.as<uint32_t>(), c.r_cnt.as<uint32_t>(), c.sdur.as<uint32_t>(),
-          c.skind.as<uint8_t>(), c.sci.as<uint32_t>(), c.sit.as<uint32_t>(), c.p2p_pay.as<uint32_t>(),
-          c.p2p_warm.as<uint8_t>(), c.p2p_slot0, c.p2p_inst0, c.inst_rec.as<uint4>(), c.wait_c.as<uint32_t>(),
-          c.sdur.as<uint32_t>(), c.nbc_off.as<uint64_t>(), c.nbc.as<uint32_t>(), c.nbp.as<uint32_t>(), c.nbp_n.as<uint32_t>(),
-          c.nnz_c + (uint64_t)c.W * PCAP, c.nnz_c, c.ewc.as<unsigned long long>(), c.rk_sum.as<unsigned long long>(),
-          c.dcfg.window_iters, (unsigned long long)c.lcfg.wait_margin_ns, c.counters.as<Counters>(),
-          c.p2p_eslot.as<uint32_t>(), 0, c.xe_off.as<uint64_t>(), c.xe_col.as<uint32_t>(),
-          stage_active(c) ? 1 : 0, c.d_pay, c.d_meta, c.rank_off.as<uint64_t>(), c.p2p_pay.as<uint32_t>(), c.p2p_warm.as<uint8_t>()};
+  XArgs a = cross_args(c);
   if (c.n_xinst == 0) return 0;
   int n = 0;
   if (c.n_p2p) {
@@ -1768,26 +1793,26 @@ __global__ void __launch_bounds__(256) k_cross_big(XArgs a, const uint32_t* big,
     bool valid = false;
     if (complete) {
       flags |= SCAN_F_COMPLETE;
-      const uint8_t k0 = a.skind[sb];
+      const uint32_t k0 = slot_kind(a.slots[sb].z);
       bool kok = true;
-      for (uint32_t q = lane; q < nm; q += 32) kok &= a.skind[sb + q] == k0;
+      for (uint32_t q = lane; q < nm; q += 32) kok &= slot_kind(a.slots[sb + q].z) == k0;
       kok = __all_sync(0xFFFFFFFFu, kok);
       if (kok) flags |= SCAN_F_KIND_OK; else ++kmis;
       flags |= SCAN_F_PAYLOAD_OK;  // collectives carry no payload check
       if (!kok)
-        for (uint32_t q = lane; q < nm; q += 32) a.swait[sb + q] = 0;  // invalid instance: members wait 0
+        for (uint32_t q = lane; q < nm; q += 32) slot_set_wait(a.slots, sb + q, 0);  // invalid instance: members wait 0
       if (kok) {
         valid = true;
         flags |= SCAN_F_VALID;
         uint32_t mn = NONE32, mx = 0;
-        for (uint32_t q = lane; q < nm; q += 32) { const uint32_t d = a.sdur[sb + q]; mn = min(mn, d); mx = max(mx, d); }
+        for (uint32_t q = lane; q < nm; q += 32) { const uint32_t d = a.slots[sb + q].x; mn = min(mn, d); mx = max(mx, d); }
         for (int o = 16; o > 0; o >>= 1) {
           mn = min(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, o));
           mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
         }
         uint32_t ls = NONE32, nat = 0;  // lowest member with the minimum, tie count
         for (uint32_t q = lane; q < nm; q += 32)
-          if (a.sdur[sb + q] == mn) { ls = min(ls, q); ++nat; }
+          if (a.slots[sb + q].x == mn) { ls = min(ls, q); ++nat; }
         for (int o = 16; o > 0; o >>= 1) {
           ls = min(ls, __shfl_xor_sync(0xFFFFFFFFu, ls, o));
           nat += __shfl_xor_sync(0xFFFFFFFFu, nat, o);
@@ -1797,12 +1822,13 @@ __global__ void __launch_bounds__(256) k_cross_big(XArgs a, const uint32_t* big,
         const uint64_t xo = a.xe_off[ch];
         for (uint32_t q = lane; q < nm; q += 32) {
           const uint32_t m = mem[q];
-          const uint32_t wait = a.sdur[sb + q] - dmin;
-          a.swait[sb + q] = wait;
+          const uint4 sq = a.slots[sb + q];
+          const uint32_t wait = sq.x - dmin;
+          slot_set_wait(a.slots, sb + q, wait);
           if (wait) atomicAdd(&a.rk_sum[a.W + m], (unsigned long long)wait);
           if (dmin) atomicAdd(&a.rk_sum[2 * a.W + m], (unsigned long long)dmin);
           if (m != last && (unsigned long long)wait > a.wait_margin) {
-            const uint32_t win = a.wi ? a.sit[sb + q] / a.wi : 0;
+            const uint32_t win = a.wi ? (sq.z & SLOT_IT_MASK) / a.wi : 0;
             if (xo != ~0ull) atomicAdd(&a.ew[(uint64_t)win * a.nnz_tot + a.xe_col[xo + (uint64_t)q * nm + ls]], (unsigned long long)wait);
             else x_edge(a, m, last, win, wait);
           }
@@ -1814,7 +1840,7 @@ __global__ void __launch_bounds__(256) k_cross_big(XArgs a, const uint32_t* big,
         const uint32_t m = mem[q];
         const uint32_t C = a.r_nkeys[m];
         const uint32_t p = lower_bound_u32(a.r_keys + (uint64_t)m * RCAP, C, ch);
-        if (p < C && a.r_keys[(uint64_t)m * RCAP + p] == ch && a.r_cnt[(uint64_t)m * RCAP + p] > k) a.swait[sb + q] = 0;
+        if (p < C && a.r_keys[(uint64_t)m * RCAP + p] == ch && a.r_cnt[(uint64_t)m * RCAP + p] > k) slot_set_wait(a.slots, sb + q, 0);
       }
     }
     if (lane == 0) a.rec[i] = make_uint4(dmin, dmax, last, flags | ((uint32_t)a.ccls[ch] << 8));
@@ -1850,20 +1876,17 @@ __global__ void __launch_bounds__(256) k_xwait_scatter(XArgs a) {
           present = p < C && a.r_keys[(uint64_t)m * RCAP + p] == (uint32_t)ch && a.r_cnt[(uint64_t)m * RCAP + p] > k;
         }
       }
-      if (present) a.wait_c[a.sci[sb + q]] = a.swait[sb + q];
+      if (present) {
+        const uint4 sq = a.slots[sb + q];
+        a.wait_c[sq.y] = sq.x;
+      }
     }
   }
 }
 
 int launch_xwait_scatter(Ctx& c) {
   if (c.n_xinst == 0) return 0;
-  XArgs a{c.n_xinst, c.NCH, c.n_comms, c.W, c.xbase.as<uint64_t>(), c.ch_base.as<uint64_t>(), c.ch_slot.as<uint64_t>(), c.ch_nmin.as<uint32_t>(),
-          c.coff.as<uint64_t>(), c.cmem.as<uint32_t>(), c.ccls.as<uint8_t>(), c.ch_nsend.as<uint32_t>(),
-          c.ch_nrecv.as<uint32_t>(), c.ch_nsend.as<uint32_t>() + c.n_p2p, c.ch_nrecv.as<uint32_t>() + c.n_p2p,
-          c.r_nkeys.as<uint32_t>(), c.r_keys.as<uint32_t>(), c.r_cnt.as<uint32_t>(), c.sdur.as<uint32_t>(),
-          c.skind.as<uint8_t>(), c.sci.as<uint32_t>(), c.sit.as<uint32_t>(), c.p2p_pay.as<uint32_t>(),
-          c.p2p_warm.as<uint8_t>(), c.p2p_slot0, c.p2p_inst0, c.inst_rec.as<uint4>(), c.wait_c.as<uint32_t>(),
-          c.sdur.as<uint32_t>()};
+  XArgs a = cross_args(c);
   unsigned blocks = (unsigned)std::min<uint64_t>((c.n_xinst + 255) / 256, 148ull * 8);
   k_xwait_scatter<<<blocks, 256, 0, c.stream>>>(a);
   return 1;

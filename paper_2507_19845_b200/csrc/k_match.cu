@@ -544,7 +544,7 @@ struct AssignArgs {
   const uint64_t* r_comm_off; const uint64_t* r_comp_off;
   const uint32_t* bitmap; const uint32_t* bitpre;
   const uint64_t* ch_base; const uint64_t* ch_slot;
-  uint32_t* inst_c; uint32_t* sdur; uint8_t* skind; uint32_t* p2p_pay; uint8_t* p2p_warm; uint32_t* p2p_iter;
+  uint32_t* inst_c; uint4* slots;
   uint32_t* cdur; uint16_t* cop; uint32_t* citer; uint32_t NIT1;
   uint64_t p2p_slot0, p2p_inst0;
 };
@@ -656,16 +656,9 @@ __global__ void __launch_bounds__(256) k_assign(AssignArgs A) {
         const uint32_t cb = cex + __popc(commm & ((1u << q) - 1u));
         A.inst_c[comm_off + cb] = (uint32_t)inst;
         const uint64_t si = sb + (uint64_t)k * nmem + mslot;
-        A.sdur[si] = du[q];
-        A.skind[si] = (uint8_t)(ko[q] & 7u);
-        if (isp) {
-          A.p2p_pay[si - A.p2p_slot0] = a.pay[ev];
-          if ((ko[q] & 7u) == 5) {
-            const uint64_t pi = inst - A.p2p_inst0;
-            A.p2p_warm[pi] = (uint8_t)((a.meta[ev] >> 14) & 1u);
-            A.p2p_iter[pi] = iex + __popc(itm & ((1u << q) - 1u));
-          }
-        }
+        const uint32_t kind = ko[q] & 7u;
+        const uint32_t warm = kind == 5 ? (a.meta[ev] >> 14) & 1u : 0u;
+        A.slots[si] = make_uint4(du[q], 0u, slot_z(iex + __popc(itm & ((1u << q) - 1u)), kind, warm), isp ? a.pay[ev] : 0u);
       }
     }
     comm_carry += ctot;
@@ -684,8 +677,7 @@ int launch_assign(Ctx& c) {
   A.r_comm_off = c.r_comm_off.as<uint64_t>(); A.r_comp_off = c.r_comp_off.as<uint64_t>();
   A.bitmap = c.bitmap.as<uint32_t>(); A.bitpre = c.bitpre.as<uint32_t>();
   A.ch_base = c.ch_base.as<uint64_t>(); A.ch_slot = c.ch_slot.as<uint64_t>();
-  A.inst_c = c.inst_c.as<uint32_t>(); A.sdur = c.sdur.as<uint32_t>(); A.skind = c.skind.as<uint8_t>();
-  A.p2p_pay = c.p2p_pay.as<uint32_t>(); A.p2p_warm = c.p2p_warm.as<uint8_t>(); A.p2p_iter = c.p2p_iter.as<uint32_t>();
+  A.inst_c = c.inst_c.as<uint32_t>(); A.slots = c.slots.as<uint4>();
   A.cdur = c.cdur.as<uint32_t>(); A.cop = c.cop.as<uint16_t>(); A.citer = c.citer.as<uint32_t>(); A.NIT1 = c.NIT + 1;
   A.p2p_slot0 = c.p2p_slot0; A.p2p_inst0 = c.p2p_inst0;
   unsigned blocks = (unsigned)((c.n_tiles + 7) / 8);
@@ -700,11 +692,8 @@ __global__ void __launch_bounds__(256) k_inst_reduce(uint64_t n_inst, uint64_t N
                                                      const uint64_t* ch_base, const uint64_t* ch_slot,
                                                      const uint32_t* ch_nmin, const uint64_t* coff,
                                                      const uint32_t* cmem, const uint8_t* ccls,
-                                                     const uint32_t* psrc, const uint32_t* pdst,
-                                                     const uint32_t* sdur, const uint8_t* skind,
-                                                     const uint32_t* p2p_pay, const uint8_t* p2p_warm,
-                                                     uint64_t p2p_slot0, uint64_t p2p_inst0, uint4* rec,
-                                                     Counters* cnt) {
+                                                     const uint32_t* nsend, const uint32_t* psrc, const uint32_t* pdst,
+                                                     const uint4* slots, uint4* rec, Counters* cnt) {
   uint32_t inc = 0, kmis = 0, pmis = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_inst; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t ch = upper_bound_u64(ch_base, NCH + 1, i) - 1;
@@ -713,17 +702,17 @@ __global__ void __launch_bounds__(256) k_inst_reduce(uint64_t n_inst, uint64_t N
     uint32_t nm, cls = 0;
     if (!isp) { nm = (uint32_t)(coff[ch + 1] - coff[ch]); cls = ccls[ch]; } else nm = 2;
     uint32_t flags = 0;
-    if (isp && p2p_warm[i - p2p_inst0]) flags |= SCAN_F_WARMUP;
+    const uint64_t sb = ch_slot[ch] + k * nm;
+    if (isp && k < nsend[ch - n_comms] && (slots[sb].z >> 31)) flags |= SCAN_F_WARMUP;  // the sender's flag
     uint32_t dmin = 0, dmax = 0, last = NONE32;
     if (k < ch_nmin[ch]) {
       flags |= SCAN_F_COMPLETE;
-      const uint64_t sb = ch_slot[ch] + k * nm;
       bool kind_ok = true, pay_ok = true;
       if (!isp) {
-        const uint8_t k0 = skind[sb];
-        for (uint32_t q = 1; q < nm; ++q) if (skind[sb + q] != k0) kind_ok = false;
+        const uint32_t k0 = slot_kind(slots[sb].z);
+        for (uint32_t q = 1; q < nm; ++q) if (slot_kind(slots[sb + q].z) != k0) kind_ok = false;
       } else {
-        pay_ok = p2p_pay[sb - p2p_slot0] == p2p_pay[sb + 1 - p2p_slot0];
+        pay_ok = slots[sb].w == slots[sb + 1].w;
       }
       if (kind_ok) flags |= SCAN_F_KIND_OK; else ++kmis;
       if (pay_ok) flags |= SCAN_F_PAYLOAD_OK; else ++pmis;
@@ -732,7 +721,7 @@ __global__ void __launch_bounds__(256) k_inst_reduce(uint64_t n_inst, uint64_t N
         dmin = NONE32; dmax = 0;
         uint32_t ls = 0, nat = 0;
         for (uint32_t q = 0; q < nm; ++q) {
-          const uint32_t d = sdur[sb + q];
+          const uint32_t d = slots[sb + q].x;
           if (d < dmin) { dmin = d; ls = q; nat = 1; } else if (d == dmin) ++nat;
           dmax = max(dmax, d);
         }
@@ -758,10 +747,9 @@ int launch_inst_reduce(Ctx& c) {
   unsigned blocks = (unsigned)std::min<uint64_t>((c.n_inst + 255) / 256, 148ull * 16);
   k_inst_reduce<<<blocks, 256, 0, c.stream>>>(c.n_inst, c.NCH, c.n_comms, c.ch_base.as<uint64_t>(), c.ch_slot.as<uint64_t>(),
                                               c.ch_nmin.as<uint32_t>(), c.coff.as<uint64_t>(), c.cmem.as<uint32_t>(),
-                                              c.ccls.as<uint8_t>(), c.ch_nsend.as<uint32_t>() + c.n_p2p,
-                                              c.ch_nrecv.as<uint32_t>() + c.n_p2p, c.sdur.as<uint32_t>(),
-                                              c.skind.as<uint8_t>(), c.p2p_pay.as<uint32_t>(), c.p2p_warm.as<uint8_t>(),
-                                              c.p2p_slot0, c.p2p_inst0, c.inst_rec.as<uint4>(), c.counters.as<Counters>());
+                                              c.ccls.as<uint8_t>(), c.ch_nsend.as<uint32_t>(), c.ch_nsend.as<uint32_t>() + c.n_p2p,
+                                              c.ch_nrecv.as<uint32_t>() + c.n_p2p, c.slots.as<uint4>(), c.inst_rec.as<uint4>(),
+                                              c.counters.as<Counters>());
   return 1;
 }
 

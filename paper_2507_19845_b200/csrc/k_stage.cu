@@ -98,7 +98,7 @@ struct StageArgs {
   const uint64_t* ch_base; const uint64_t* ch_slot; const uint32_t* bitmap; const uint32_t* bitpre;
   const uint64_t* comm_off; const uint64_t* comp_off; const uint64_t* bits_off;
   uint32_t* inst_c; uint32_t* wait_c; uint32_t* bits; uint32_t* cref; uint4* rec;
-  uint32_t* sdur; uint8_t* skind; uint32_t* sci; uint32_t* sit; uint32_t* p2p_pos; uint32_t* p2p_iter;
+  uint4* slots;  // SlotRec per member slot (P2P: w = the event's position in its rank, k_cross_reduce gathers)
   uint64_t p2p_slot0, p2p_inst0;
   uint32_t* citer; uint32_t NIT1;
   uint64_t nnz_tot;
@@ -753,15 +753,8 @@ __global__ void __launch_bounds__(SG_NT, 1) k_stage(const __grid_constant__ Stag
           }
           const uint64_t inst = bch + kinst;
           const uint64_t si = sch + (uint64_t)kinst * nm + slot;
-          a.sdur[si] = d[k];
-          a.skind[si] = (uint8_t)(pk[p] & 7u);
-          a.sci[si] = (uint32_t)(coffr[row] + m0 + j);
-          a.sit[si] = itp;
+          a.slots[si] = make_uint4(d[k], (uint32_t)(coffr[row] + m0 + j), slot_z(itp, pk[p], 0u), role >= 16 ? p0 + p : 0u);
           comm_s[wo + 1024u * k] = (uint32_t)inst;
-          if (role >= 16) {
-            a.p2p_pos[si - a.p2p_slot0] = p0 + p;  // k_cross_reduce gathers the payload / warm-up bit
-            if (send) a.p2p_iter[inst - a.p2p_inst0] = itp;
-          }
         }
         continue;
       }
@@ -1067,8 +1060,7 @@ int launch_stage(Ctx& c) {
   a.bitpre = c.bitpre.as<uint32_t>(); a.comm_off = c.r_comm_off.as<uint64_t>(); a.comp_off = c.r_comp_off.as<uint64_t>();
   a.bits_off = c.r_bits_off.as<uint64_t>(); a.inst_c = c.inst_c.as<uint32_t>(); a.wait_c = c.wait_c.as<uint32_t>();
   a.bits = c.bits.as<uint32_t>(); a.cref = c.cref.as<uint32_t>(); a.rec = c.inst_rec.as<uint4>();
-  a.sdur = c.sdur.as<uint32_t>(); a.skind = c.skind.as<uint8_t>(); a.sci = c.sci.as<uint32_t>(); a.sit = c.sit.as<uint32_t>();
-  a.p2p_pos = c.p2p_pay.as<uint32_t>(); a.p2p_iter = c.p2p_iter.as<uint32_t>();
+  a.slots = c.slots.as<uint4>();
   a.p2p_slot0 = c.p2p_slot0; a.p2p_inst0 = c.p2p_inst0; a.citer = c.citer.as<uint32_t>(); a.NIT1 = c.NIT + 1;
   a.nnz_tot = c.nnz_c + (uint64_t)c.W * PCAP;
   a.ew = c.ewc.as<unsigned long long>(); a.rk_sum = c.rk_sum.as<unsigned long long>();

@@ -398,13 +398,15 @@ __device__ void smem_bitonic(uint32_t* sp, uint32_t* st, uint32_t* si, uint32_t 
 
 struct LKArgs {
   uint32_t n_comms, n_p2p, NW, wi; int W, TP, DP;
-  const uint64_t* ch_base; const uint32_t* ch_nmax; const uint32_t* psrc; const uint32_t* pdst;
-  const uint4* rec; const uint32_t* p2p_iter; const uint32_t* p2p_pay; const uint64_t* ch_slot;
-  uint64_t p2p_inst0, p2p_slot0;
+  const uint64_t* ch_base; const uint32_t* ch_nmax; const uint32_t* ch_nmin; const uint32_t* psrc; const uint32_t* pdst;
+  const uint4* rec;
+  // per P2P instance i (index i - p2p_inst0): payload pay[. * pay_stride], send iteration iter[. * iter_stride] & it_mask
+  const uint32_t* pay; const uint32_t* iter; uint32_t pay_stride, iter_stride, it_mask;
+  uint64_t p2p_inst0;
   uint32_t min_samples;
   uint32_t* lk_n; uint8_t* lk_used; uint32_t* lk_medp; uint32_t* lk_medt; double* lk_bw; uint8_t* lk_dir; uint8_t* lk_elig;
   Counters* cnt;
-  unsigned long long* gkey; uint32_t* gid;  // global scratch for links with more than LM_CAP samples
+  unsigned long long* gkey; uint32_t* gid;  // global scratch for links with more than LM_CAP instances
   uint32_t n_shards, shard;                 // sharded: this shard computes the links with pid % n_shards == shard
 };
 
@@ -414,8 +416,10 @@ __device__ __forceinline__ unsigned long long ratio_key(uint32_t p, uint32_t t) 
   return (unsigned long long)__double_as_longlong((double)p / (double)t);  // positive: bit order = value order
 }
 
-constexpr int LM_NT = 512;  // 2 CTAs x 16 warps per SM with the 96 KB sample buffer
-constexpr uint32_t LM_CAP = 8192;  // samples per link held in shared memory (larger links use global scratch)
+constexpr int LM_NT = 512;         // 2 CTAs x 16 warps per SM
+constexpr uint32_t LM_CAP = 8192;  // instances per link whose samples are held in shared memory (else global scratch)
+constexpr uint32_t LM_NB = 2048;   // bins of one selection pass over a key range
+constexpr uint32_t LM_CC = 512;    // candidates ranked directly
 
 // warp 0 finds the bin holding rank tgt in a 256-bin histogram: returns (bin, count below it)
 __device__ __forceinline__ void hist_find(const uint32_t* hist, uint32_t tgt, uint32_t& bin, uint32_t& below) {
@@ -435,53 +439,125 @@ __device__ __forceinline__ void hist_find(const uint32_t* hist, uint32_t tgt, ui
   below = __shfl_sync(0xFFFFFFFFu, acc, L);
 }
 
-// shared 256-bin histogram add with the lanes of a warp that share a bin combined (bin 256 = none);
-// samples of one link cluster in a few bins in the top radix passes
-__device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t bin) {
-  const unsigned peers = __match_any_sync(0xFFFFFFFFu, bin);
-  if (bin < 256u && (lane_id() == (uint32_t)(__ffs(peers) - 1))) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
+// the same over LM_NB bins (64 per lane)
+__device__ __forceinline__ void hist_find_nb(const uint32_t* hist, uint32_t tgt, uint32_t& bin, uint32_t& below) {
+  const uint32_t lane = lane_id();
+  const uint4* h4 = reinterpret_cast<const uint4*>(hist + lane * 64);
+  uint32_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) { const uint4 v = h4[i]; sum += v.x + v.y + v.z + v.w; }
+  const uint32_t inc = warp_incl_scan(sum), ex = inc - sum;
+  const unsigned hit = __ballot_sync(0xFFFFFFFFu, ex <= tgt && tgt < inc);
+  const uint32_t L = __ffs(hit) - 1;
+  uint32_t acc = __shfl_sync(0xFFFFFFFFu, ex, L), b = 0;
+  if (lane == L) {
+    for (int i = 0; i < 64; ++i) { const uint32_t v = hist[L * 64 + i]; if (acc + v > tgt) { b = i; break; } acc += v; }
+  }
+  bin = L * 64 + __shfl_sync(0xFFFFFFFFu, b, L);
+  below = __shfl_sync(0xFFFFFFFFu, acc, L);
 }
 
+// shared histogram add with the lanes of a warp that share a bin combined (bin >= nb = none);
+// samples of one link cluster in a few bins
+__device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t bin, uint32_t nb = 256u) {
+  const unsigned peers = __match_any_sync(0xFFFFFFFFu, bin);
+  if (bin < nb && (lane_id() == (uint32_t)(__ffs(peers) - 1))) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
+}
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+  for (int o = 16; o > 0; o >>= 1) v = min(v, (unsigned long long)__shfl_xor_sync(0xFFFFFFFFu, v, o));
+  return v;
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+  for (int o = 16; o > 0; o >>= 1) v = max(v, (unsigned long long)__shfl_xor_sync(0xFFFFFFFFu, v, o));
+  return v;
+}
+
+// One CTA per (window, link). (1) One pass over the link's instances: the samples (valid, transfer
+// > 0, send in the window) go to shared memory as (f64 ratio key, instance index), warm-up samples
+// from the front, the others from the back, with the key range of each group. (2) Lower-median rank
+// (n-1)/2 of the chosen group (warm-up if >= min_samples, reading R13): histogram passes of LM_NB bins
+// over the shrinking key range until the target bin holds <= LM_CC samples, which are ranked
+// directly. (3) Ties on the f64 key: the exact order (p/t, instance id), as before.
 __global__ void __launch_bounds__(LM_NT) k_link_median(LKArgs a) {
   extern __shared__ __align__(8) uint8_t lsm[];
-  __shared__ uint32_t scan_sm[33];
-  __shared__ uint32_t cnt_all, cnt_warm;
-  __shared__ uint32_t hist[256];
-  __shared__ unsigned long long s_prefix;
-  __shared__ uint32_t s_target, s_tie, s_pick, s_exact_eq, s_ref;
+  __shared__ __align__(16) uint32_t hist[LM_NB];
+  __shared__ unsigned long long cand[LM_CC];
+  __shared__ unsigned long long s_min[2], s_max[2], s_lo, s_hi, s_prefix, s_K;
+  __shared__ uint32_t s_nw, s_nn, s_target, s_cnt, s_nc, s_tg, s_tie, s_pick, s_exact_eq, s_ref;
   const uint32_t o = blockIdx.x;
   const uint32_t w = o / a.n_p2p, pid = o % a.n_p2p;
   const uint64_t ch = a.n_comms + pid;
   const uint64_t b = a.ch_base[ch];
   const uint32_t n = a.ch_nmax[ch];
-  const uint64_t sb = a.ch_slot[ch];
+  const uint32_t nmin = a.ch_nmin ? a.ch_nmin[ch] : n;  // a valid instance is complete: k < nmin
+  const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
+  const uint32_t src = a.psrc[pid], dst = a.pdst[pid];
   if (a.n_shards > 1 && pid % a.n_shards != a.shard) {  // another shard owns this link: zeros for the all-reduce
-    if (threadIdx.x == 0) {
-      const uint32_t src = a.psrc[pid], dst = a.pdst[pid];
+    if (tid == 0) {
       const int dpp = (int)(dst / (uint32_t)(a.TP * a.DP)) - (int)(src / (uint32_t)(a.TP * a.DP));
       a.lk_dir[o] = dpp == 1 ? 0 : (dpp == -1 ? 1 : 2);
       a.lk_n[o] = 0; a.lk_used[o] = 0; a.lk_elig[o] = 0; a.lk_medp[o] = 0; a.lk_medt[o] = 0; a.lk_bw[o] = 0.0;
     }
     return;
   }
-  if (threadIdx.x == 0) { cnt_all = 0; cnt_warm = 0; }
+  if (tid == 0) { s_nw = 0; s_nn = 0; s_min[0] = s_min[1] = ~0ull; s_max[0] = s_max[1] = 0; }
   __syncthreads();
-  auto sample = [&](uint32_t k, bool& in, bool& warm) {
-    in = false; warm = false;
-    const uint4 rc = a.rec[b + k];
-    if (!(rc.w & SCAN_F_VALID) || rc.x == 0) return;
-    if (a.wi && a.p2p_iter[b + k - a.p2p_inst0] / a.wi != w) return;
-    in = true; warm = (rc.w & SCAN_F_WARMUP) != 0;
-  };
-  uint32_t la = 0, lw = 0;
-  for (uint32_t k = threadIdx.x; k < n; k += LM_NT) { bool in, wm; sample(k, in, wm); la += in; lw += (in && wm); }
-  la = warp_sum_u32(la); lw = warp_sum_u32(lw);
-  if (lane_id() == 0) { atomicAdd(&cnt_all, la); atomicAdd(&cnt_warm, lw); }
+  const bool in_smem = n <= LM_CAP;
+  const uint32_t cap = in_smem ? LM_CAP : n;
+  unsigned long long* sk = in_smem ? (unsigned long long*)lsm : a.gkey + (b - a.p2p_inst0);
+  uint32_t* si = in_smem ? (uint32_t*)(lsm + (size_t)LM_CAP * 8) : a.gid + (b - a.p2p_inst0);
+  const uint64_t rel0 = b - a.p2p_inst0;
+  // (1) samples: each warp takes 32-instance chunks, four chunks' loads in flight
+  unsigned long long mnw = ~0ull, mxw = 0, mnn = ~0ull, mxn = 0;
+  for (uint32_t kb = wid * 32; kb < n; kb += 4 * LM_NT) {
+    uint4 rc[4];
+    uint32_t pv[4], iv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t k = kb + u * LM_NT + lane;
+      rc[u] = make_uint4(0, 0, 0, 0); pv[u] = 0; iv[u] = 0;
+      if (k < n) {
+        rc[u] = a.rec[b + k];
+        if (k < nmin) {
+          pv[u] = a.pay[(rel0 + k) * a.pay_stride];
+          if (a.wi) iv[u] = a.iter[(rel0 + k) * a.iter_stride] & a.it_mask;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t k = kb + u * LM_NT + lane;
+      const bool in = k < n && (rc[u].w & SCAN_F_VALID) && rc[u].x != 0 && (!a.wi || iv[u] / a.wi == w);
+      const bool warm = in && (rc[u].w & SCAN_F_WARMUP);
+      const unsigned bw = __ballot_sync(0xFFFFFFFFu, warm), bn = __ballot_sync(0xFFFFFFFFu, in && !warm);
+      if (!(bw | bn)) continue;
+      uint32_t ow = 0, on = 0;
+      if (lane == 0) {
+        if (bw) ow = atomicAdd(&s_nw, (uint32_t)__popc(bw));
+        if (bn) on = atomicAdd(&s_nn, (uint32_t)__popc(bn));
+      }
+      ow = __shfl_sync(0xFFFFFFFFu, ow, 0); on = __shfl_sync(0xFFFFFFFFu, on, 0);
+      if (in) {
+        const unsigned long long key = ratio_key(pv[u], rc[u].x);
+        const unsigned lt = (1u << lane) - 1u;
+        const uint32_t pos = warm ? ow + __popc(bw & lt) : cap - 1u - (on + __popc(bn & lt));
+        sk[pos] = key; si[pos] = k;
+        if (warm) { mnw = min(mnw, key); mxw = max(mxw, key); }
+        else { mnn = min(mnn, key); mxn = max(mxn, key); }
+      }
+    }
+  }
+  mnw = warp_min_u64(mnw); mxw = warp_max_u64(mxw); mnn = warp_min_u64(mnn); mxn = warp_max_u64(mxn);
+  if (lane == 0) {
+    if (mnw != ~0ull) { atomicMin(&s_min[0], mnw); atomicMax(&s_max[0], mxw); }
+    if (mnn != ~0ull) { atomicMin(&s_min[1], mnn); atomicMax(&s_max[1], mxn); }
+  }
   __syncthreads();
-  const bool use_warm = cnt_warm >= a.min_samples;
-  const uint32_t nu = use_warm ? cnt_warm : cnt_all;
-  const uint32_t src = a.psrc[pid], dst = a.pdst[pid];
-  if (threadIdx.x == 0) {
+  const uint32_t nw = s_nw, nn = s_nn;
+  const bool use_warm = nw >= a.min_samples;
+  const uint32_t nu = use_warm ? nw : nw + nn;
+  if (tid == 0) {
     const int dpp = (int)(dst / (uint32_t)(a.TP * a.DP)) - (int)(src / (uint32_t)(a.TP * a.DP));
     a.lk_dir[o] = dpp == 1 ? 0 : (dpp == -1 ? 1 : 2);
     a.lk_n[o] = nu; a.lk_used[o] = use_warm ? 1 : 0;
@@ -489,108 +565,128 @@ __global__ void __launch_bounds__(LM_NT) k_link_median(LKArgs a) {
     a.lk_medp[o] = 0; a.lk_medt[o] = 0; a.lk_bw[o] = 0.0;
   }
   if (nu == 0) return;
-  // selected samples as (f64 key, instance id); shared memory, or this link's global scratch slice
-  unsigned long long* sk;
-  uint32_t* si;
-  if (nu <= LM_CAP) { sk = (unsigned long long*)lsm; si = (uint32_t*)(lsm + (size_t)LM_CAP * 8); }
-  else { sk = a.gkey + (b - a.p2p_inst0); si = a.gid + (b - a.p2p_inst0); }
-  uint32_t carry = 0;
-  for (uint32_t kb = 0; kb < n; kb += LM_NT) {
-    const uint32_t k = kb + threadIdx.x;
-    bool in = false, wm = false;
-    if (k < n) sample(k, in, wm);
-    const bool sel = in && (!use_warm || wm);
-    uint32_t tot;
-    const uint32_t ex = block_excl_sum<LM_NT>(sel ? 1u : 0u, tot, scan_sm);
-    if (sel) {
-      const uint32_t pos = carry + ex;
-      sk[pos] = ratio_key(a.p2p_pay[sb + (uint64_t)k * 2 - a.p2p_slot0], a.rec[b + k].x);
-      si[pos] = k;
-    }
-    carry += tot;
+  // sample i of the chosen group, i < nu: the warm-up samples, then (all samples) the others
+  auto at = [&](uint32_t i) -> uint32_t { return i < nw ? i : cap - nn + (i - nw); };
+  // (2) lower-median rank over the key range [lo, hi]
+  if (tid == 0) {
+    s_lo = use_warm ? s_min[0] : min(s_min[0], s_min[1]);
+    s_hi = use_warm ? s_max[0] : max(s_max[0], s_max[1]);
+    s_target = (nu - 1) / 2;
   }
-  // radix select of the lower-median rank (nu-1)/2 on the key, 8 bits per pass
-  if (threadIdx.x == 0) { s_prefix = 0; s_target = (nu - 1) / 2; }
   __syncthreads();
-  for (int shift = 56; shift >= 0; shift -= 8) {
-    if (threadIdx.x < 256) hist[threadIdx.x] = 0;
+  for (;;) {
+    const unsigned long long lo = s_lo, hi = s_hi;
+    const uint32_t tgt = s_target;
+    if (lo == hi) { if (tid == 0) { s_K = lo; s_tg = tgt; } break; }
+    const int sh = max(0, 64 - __clzll((long long)(hi - lo)) - 11);  // (hi - lo) >> sh < LM_NB
+    for (uint32_t i = tid; i < LM_NB; i += LM_NT) hist[i] = 0;
     __syncthreads();
-    const unsigned long long pre = s_prefix;
-    const unsigned long long hmask = shift == 56 ? 0ull : (~0ull << (shift + 8));
     for (uint32_t ib = 0; ib < nu; ib += LM_NT) {  // whole warps per round: lanes with one bin add once
-      const uint32_t i = ib + threadIdx.x;
-      uint32_t bin = 256u;
+      const uint32_t i = ib + tid;
+      uint32_t bin = LM_NB;
       if (i < nu) {
-        const unsigned long long key = sk[i];
-        if ((key & hmask) == pre) bin = (uint32_t)(key >> shift) & 0xFFu;
+        const unsigned long long key = sk[at(i)];
+        if (key >= lo && key <= hi) bin = (uint32_t)((key - lo) >> sh);
       }
-      hist_add(hist, bin);
+      hist_add(hist, bin, LM_NB);
     }
     __syncthreads();
-    if (threadIdx.x < 32) {
+    if (wid == 0) {
       uint32_t bin, below;
-      hist_find(hist, s_target, bin, below);
-      if (threadIdx.x == 0) { s_target -= below; s_prefix = pre | ((unsigned long long)bin << shift); }
+      hist_find_nb(hist, tgt, bin, below);
+      if (lane == 0) {
+        const unsigned long long nlo = lo + ((unsigned long long)bin << sh);
+        const unsigned long long nhi = sh >= 64 ? hi : min(hi, nlo + ((1ull << sh) - 1ull));
+        s_lo = nlo; s_hi = nhi; s_target = tgt - below; s_cnt = hist[bin]; s_nc = 0;
+      }
     }
     __syncthreads();
+    if (s_lo == s_hi || s_cnt > LM_CC) continue;
+    // <= LM_CC samples in [lo, hi]: gather their keys and rank them directly
+    {
+      const unsigned long long l2 = s_lo, h2 = s_hi;
+      for (uint32_t ib = 0; ib < nu; ib += LM_NT) {
+        const uint32_t i = ib + tid;
+        bool c = false;
+        unsigned long long key = 0;
+        if (i < nu) { key = sk[at(i)]; c = key >= l2 && key <= h2; }
+        const unsigned bm = __ballot_sync(0xFFFFFFFFu, c);
+        if (!bm) continue;
+        uint32_t off = 0;
+        if (lane == 0) off = atomicAdd(&s_nc, (uint32_t)__popc(bm));
+        off = __shfl_sync(0xFFFFFFFFu, off, 0);
+        if (c) cand[off + __popc(bm & ((1u << lane) - 1u))] = key;
+      }
+      __syncthreads();
+      const uint32_t nc = s_nc, t2 = s_target;
+      for (uint32_t j = tid; j < nc; j += LM_NT) {
+        const unsigned long long kj = cand[j];
+        uint32_t less = 0, eq = 0;
+        for (uint32_t q = 0; q < nc; ++q) { const unsigned long long kq = cand[q]; less += kq < kj; eq += kq == kj; }
+        if (less <= t2 && t2 < less + eq) { s_K = kj; s_tg = t2 - less; }  // equal keys write equal values
+      }
+      __syncthreads();
+      break;
+    }
   }
-  // tie group = samples with the selected key; order inside it is (exact p/t, instance id)
-  const unsigned long long K = s_prefix;
-  const uint32_t tg = s_target;
-  if (threadIdx.x == 0) { s_tie = 0; s_exact_eq = 1; s_ref = NONE32; s_pick = NONE32; }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < nu; i += LM_NT)
-    if (sk[i] == K) { atomicAdd(&s_tie, 1u); atomicMin(&s_ref, i); }
+  // (3) tie group = samples with the selected key; order inside it is (exact p/t, instance id)
+  const unsigned long long K = s_K;
+  const uint32_t tg = s_tg;
+  if (tid == 0) { s_tie = 0; s_exact_eq = 1; s_ref = NONE32; s_pick = NONE32; }
   __syncthreads();
-  auto P_ = [&](uint32_t i) { return a.p2p_pay[sb + (uint64_t)si[i] * 2 - a.p2p_slot0]; };
-  auto T_ = [&](uint32_t i) { return a.rec[b + si[i]].x; };
+  for (uint32_t i = tid; i < nu; i += LM_NT)
+    if (sk[at(i)] == K) { atomicAdd(&s_tie, 1u); atomicMin(&s_ref, i); }
+  __syncthreads();
+  auto P_ = [&](uint32_t i) { return a.pay[(rel0 + si[at(i)]) * a.pay_stride]; };
+  auto T_ = [&](uint32_t i) { return a.rec[b + si[at(i)]].x; };
+  auto I_ = [&](uint32_t i) { return si[at(i)]; };
   if (s_tie == 1) {
-    if (sk[threadIdx.x < nu ? threadIdx.x : 0] == K && threadIdx.x < nu) s_pick = threadIdx.x;
-    for (uint32_t i = threadIdx.x + LM_NT; i < nu; i += LM_NT) if (sk[i] == K) s_pick = i;
+    if (tid == 0) s_pick = s_ref;
   } else {
     const uint32_t ref = s_ref;
     const uint32_t pr = P_(ref), tr = T_(ref);
-    for (uint32_t i = threadIdx.x; i < nu; i += LM_NT)
-      if (sk[i] == K && (unsigned long long)P_(i) * tr != (unsigned long long)pr * T_(i)) s_exact_eq = 0;
+    for (uint32_t i = tid; i < nu; i += LM_NT)
+      if (sk[at(i)] == K && (unsigned long long)P_(i) * tr != (unsigned long long)pr * T_(i)) s_exact_eq = 0;
     __syncthreads();
     if (s_exact_eq) {
       // one exact ratio: the tg-th smallest instance id of the tie group (radix select on ids)
       uint32_t tgt = tg, pre = 0;
       for (int shift = 24; shift >= 0; shift -= 8) {
-        if (threadIdx.x < 256) hist[threadIdx.x] = 0;
+        if (tid < 256) hist[tid] = 0;
         __syncthreads();
         const uint32_t hmask = shift == 24 ? 0u : (0xFFFFFFFFu << (shift + 8));
         for (uint32_t ib = 0; ib < nu; ib += LM_NT) {
-          const uint32_t i = ib + threadIdx.x;
+          const uint32_t i = ib + tid;
           uint32_t bin = 256u;
-          if (i < nu && sk[i] == K && (si[i] & hmask) == pre) bin = (si[i] >> shift) & 0xFFu;
+          if (i < nu && sk[at(i)] == K && (I_(i) & hmask) == pre) bin = (I_(i) >> shift) & 0xFFu;
           hist_add(hist, bin);
         }
         __syncthreads();
-        if (threadIdx.x < 32) {
+        if (tid < 32) {
           uint32_t bin, below;
           hist_find(hist, tgt, bin, below);
-          if (threadIdx.x == 0) { s_target = tgt - below; s_prefix = pre | (bin << shift); }
+          if (tid == 0) { s_target = tgt - below; s_prefix = pre | (bin << shift); }
         }
         __syncthreads();
         tgt = s_target; pre = (uint32_t)s_prefix;
       }
-      for (uint32_t i = threadIdx.x; i < nu; i += LM_NT)
-        if (sk[i] == K && si[i] == pre) s_pick = i;
+      for (uint32_t i = tid; i < nu; i += LM_NT)
+        if (sk[at(i)] == K && I_(i) == pre) s_pick = i;
     } else {
       // distinct exact ratios behind one f64 value (rare): rank the tie group exactly
-      for (uint32_t i = threadIdx.x; i < nu; i += LM_NT) {
-        if (sk[i] != K) continue;
+      for (uint32_t i = tid; i < nu; i += LM_NT) {
+        if (sk[at(i)] != K) continue;
         const uint32_t pi = P_(i), ti = T_(i);
         uint32_t rk = 0;
         for (uint32_t j2 = 0; j2 < nu; ++j2)
-          if (j2 != i && sk[j2] == K && samp_less(P_(j2), T_(j2), si[j2], pi, ti, si[i])) ++rk;
+          if (j2 != i && sk[at(j2)] == K && samp_less(P_(j2), T_(j2), I_(j2), pi, ti, I_(i))) ++rk;
         if (rk == tg) s_pick = i;
       }
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0 && s_pick != NONE32) {
+  if (tid == 0 && s_pick != NONE32) {
     const uint32_t pm = P_(s_pick), tm = T_(s_pick);
     a.lk_medp[o] = pm; a.lk_medt[o] = tm;
     a.lk_bw[o] = (double)pm / (double)tm;
@@ -641,39 +737,54 @@ __global__ void __launch_bounds__(LK_NT) k_link_flags(uint32_t n_p2p, int W, con
 
 // Per-(window, link) medians. Sharded contexts read the job-wide channel tables: the instances of
 // an owned link are all present after the shard exchange (shard.cu).
+static void link_median_go(Ctx& c, LKArgs& a) {
+  const size_t smm = (size_t)LM_CAP * 12;
+  cudaFuncSetAttribute(k_link_median, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smm);
+  k_link_median<<<(unsigned)(c.NW * c.n_p2p), LM_NT, smm, c.stream>>>(a);
+}
+
+static LKArgs link_args(Ctx& c, uint64_t np_inst) {
+  LKArgs a{};
+  a.n_comms = c.n_comms; a.n_p2p = (uint32_t)c.n_p2p; a.NW = c.NW; a.wi = c.dcfg.window_iters; a.W = c.W; a.TP = c.TP; a.DP = c.DP;
+  a.psrc = c.ch_nsend.as<uint32_t>() + c.n_p2p; a.pdst = c.ch_nrecv.as<uint32_t>() + c.n_p2p;
+  a.min_samples = c.lcfg.min_samples; a.lk_n = c.lk_n.as<uint32_t>(); a.lk_used = c.lk_used.as<uint8_t>();
+  a.lk_medp = c.lk_medp.as<uint32_t>(); a.lk_medt = c.lk_medt.as<uint32_t>(); a.lk_bw = c.lk_bw.as<double>();
+  a.lk_dir = c.lk_dir.as<uint8_t>(); a.lk_elig = c.lk_elig.as<uint8_t>(); a.cnt = c.counters.as<Counters>();
+  a.gkey = c.lk_scratch.as<unsigned long long>(); a.gid = (uint32_t*)(c.lk_scratch.as<unsigned long long>() + np_inst);
+  a.n_shards = 1; a.shard = 0;
+  return a;
+}
+
 int launch_link_median(Ctx& c) {
   if (c.n_p2p == 0) return 0;
   const uint64_t np_inst = std::max<uint64_t>(c.n_inst - c.p2p_inst0, 1);
   if (c.lk_scratch.ensure(np_inst * 12) != cudaSuccess) return 0;
   const bool sh = c.n_shards > 1;
-  LKArgs a{c.n_comms, (uint32_t)c.n_p2p, c.NW, c.dcfg.window_iters, c.W, c.TP, c.DP, (sh ? c.g_base : c.ch_base).as<uint64_t>(),
-           (sh ? c.g_nmax : c.ch_nmax).as<uint32_t>(), c.ch_nsend.as<uint32_t>() + c.n_p2p, c.ch_nrecv.as<uint32_t>() + c.n_p2p,
-           c.inst_rec.as<uint4>(), c.p2p_iter.as<uint32_t>(), c.p2p_pay.as<uint32_t>(), (sh ? c.g_slot : c.ch_slot).as<uint64_t>(),
-           c.p2p_inst0, c.p2p_slot0, c.lcfg.min_samples, c.lk_n.as<uint32_t>(), c.lk_used.as<uint8_t>(),
-           c.lk_medp.as<uint32_t>(), c.lk_medt.as<uint32_t>(), c.lk_bw.as<double>(), c.lk_dir.as<uint8_t>(),
-           c.lk_elig.as<uint8_t>(), c.counters.as<Counters>(), c.lk_scratch.as<unsigned long long>(),
-           (uint32_t*)(c.lk_scratch.as<unsigned long long>() + np_inst), (uint32_t)c.n_shards, (uint32_t)c.shard};
-  const size_t smm = (size_t)LM_CAP * 12;
-  cudaFuncSetAttribute(k_link_median, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smm);
-  k_link_median<<<(unsigned)(c.NW * c.n_p2p), LM_NT, smm, c.stream>>>(a);
+  LKArgs a = link_args(c, np_inst);
+  a.ch_base = (sh ? c.g_base : c.ch_base).as<uint64_t>(); a.ch_nmax = (sh ? c.g_nmax : c.ch_nmax).as<uint32_t>();
+  a.ch_nmin = (sh ? c.g_nmin : c.ch_nmin).as<uint32_t>();
+  a.rec = c.inst_rec.as<uint4>();
+  // the send slot of P2P instance i is slot p2p_slot0 + 2 (i - p2p_inst0): payload in w, iteration in z
+  const uint32_t* sw = reinterpret_cast<const uint32_t*>(c.slots.as<uint4>() + c.p2p_slot0);
+  a.pay = sw + 3; a.iter = sw + 2; a.pay_stride = 8; a.iter_stride = 8; a.it_mask = SLOT_IT_MASK;
+  a.p2p_inst0 = c.p2p_inst0; a.n_shards = (uint32_t)c.n_shards; a.shard = (uint32_t)c.shard;
+  link_median_go(c, a);
   return 1;
 }
 
 // Per-link medians over a caller-provided instance layout (streaming: the window's samples in
-// link-major, age-minor order; base / nmax / slot indexed by channel id n_comms + pid)
+// link-major, age-minor order; base / nmax / slot indexed by channel id n_comms + pid; instance i's
+// payload at pay[2 i], its iteration at iter[i])
 int launch_link_median_window(Ctx& c, const uint64_t* base, const uint32_t* nmax, const uint64_t* slot, const uint4* rec,
                               const uint32_t* iter, const uint32_t* pay, uint64_t n_inst) {
+  (void)slot;
   if (c.n_p2p == 0) return 0;
   const uint64_t np_inst = std::max<uint64_t>(n_inst, 1);
   if (c.lk_scratch.ensure(np_inst * 12) != cudaSuccess) return 0;
-  LKArgs a{c.n_comms, (uint32_t)c.n_p2p, c.NW, c.dcfg.window_iters, c.W, c.TP, c.DP, base, nmax,
-           c.ch_nsend.as<uint32_t>() + c.n_p2p, c.ch_nrecv.as<uint32_t>() + c.n_p2p, rec, iter, pay, slot, 0, 0,
-           c.lcfg.min_samples, c.lk_n.as<uint32_t>(), c.lk_used.as<uint8_t>(), c.lk_medp.as<uint32_t>(), c.lk_medt.as<uint32_t>(),
-           c.lk_bw.as<double>(), c.lk_dir.as<uint8_t>(), c.lk_elig.as<uint8_t>(), c.counters.as<Counters>(),
-           c.lk_scratch.as<unsigned long long>(), (uint32_t*)(c.lk_scratch.as<unsigned long long>() + np_inst), 1u, 0u};
-  const size_t smm = (size_t)LM_CAP * 12;
-  cudaFuncSetAttribute(k_link_median, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smm);
-  k_link_median<<<(unsigned)(c.NW * c.n_p2p), LM_NT, smm, c.stream>>>(a);
+  LKArgs a = link_args(c, np_inst);
+  a.ch_base = base; a.ch_nmax = nmax; a.ch_nmin = nullptr; a.rec = rec;
+  a.pay = pay; a.iter = iter; a.pay_stride = 2; a.iter_stride = 1; a.it_mask = 0xFFFFFFFFu; a.p2p_inst0 = 0;
+  link_median_go(c, a);
   return 1;
 }
 

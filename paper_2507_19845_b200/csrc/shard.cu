@@ -45,31 +45,35 @@ constexpr uint32_t LREC = 3;
 struct LinkMap { unsigned long long flat, inst0, slot0; uint32_t n, pad; };
 
 // X3 pack / unpack: one CTA per (link, shard range); instance k of the range at flat + k
-__global__ void k_link_pack(const LinkMap* map, const uint4* rec, const uint32_t* p2p_iter, const uint32_t* p2p_pay,
-                            uint64_t p2p_inst0, uint64_t p2p_slot0, uint32_t* buf) {
+// (a P2P instance i's send slot, SlotRec: p2p_slot0 + 2 (i - p2p_inst0), payload in w, iteration in z)
+__global__ void k_link_pack(const LinkMap* map, const uint4* rec, const uint4* slots, uint64_t p2p_inst0, uint64_t p2p_slot0,
+                            uint32_t* buf) {
   const LinkMap m = map[blockIdx.x];
   for (uint32_t k = threadIdx.x; k < m.n; k += blockDim.x) {
     const uint64_t i = m.inst0 + k;
     const uint4 r = rec[i];
     uint32_t* o = buf + (m.flat + k) * LREC;
+    uint4 sl = make_uint4(0, 0, 0, 0);
+    if (r.w & SCAN_F_VALID) sl = slots[p2p_slot0 + 2 * (i - p2p_inst0)];  // the median reads valid samples only
     o[0] = r.x;
-    o[1] = p2p_pay[m.slot0 + 2ull * k - p2p_slot0];
-    o[2] = (p2p_iter[i - p2p_inst0] << 8) | (r.w & 0xFFu);
+    o[1] = sl.w;
+    o[2] = ((sl.z & SLOT_IT_MASK) << 8) | (r.w & 0xFFu);
   }
 }
 
 // rows of links this shard owns; only the fields the median reads are written (the rest of an
 // unowned-range row stays unspecified, scan.h)
-__global__ void k_link_unpack(const LinkMap* map, const uint32_t* buf, uint4* rec, uint32_t* p2p_iter, uint32_t* p2p_pay,
-                              uint64_t p2p_inst0, uint64_t p2p_slot0) {
+__global__ void k_link_unpack(const LinkMap* map, const uint32_t* buf, uint4* rec, uint4* slots, uint64_t p2p_inst0,
+                              uint64_t p2p_slot0) {
   const LinkMap m = map[blockIdx.x];
   for (uint32_t k = threadIdx.x; k < m.n; k += blockDim.x) {
     const uint64_t i = m.inst0 + k;
     const uint32_t* v = buf + (m.flat + k) * LREC;
     rec[i].x = v[0];
     rec[i].w = v[2] & 0xFFu;
-    p2p_pay[m.slot0 + 2ull * k - p2p_slot0] = v[1];
-    p2p_iter[i - p2p_inst0] = v[2] >> 8;
+    uint32_t* sw = reinterpret_cast<uint32_t*>(slots + p2p_slot0 + 2 * (i - p2p_inst0));
+    sw[2] = v[2] >> 8;  // iteration (the warm-up flag travels in the record's flags)
+    sw[3] = v[1];
   }
 }
 
@@ -537,6 +541,7 @@ scan_status sharded_all(Ctx& c) {
   queue_fill(c, c.wd_slow.p, items * 4, 0);
   mark("tables");
   c.launches += timed(c, "k_class_counts", [&] { return launch_class_counts(c); });
+  c.launches += timed(c, "k_p2p_roles", [&] { return launch_p2p_roles(c); });
   c.launches += timed(c, stage_active(c) ? "k_stage" : "k_fused", [&] { return launch_fused(c); });
   c.launches += timed(c, "k_cross_reduce", [&] { return launch_cross_reduce(c); });
   c.launches += timed(c, "k_deferred", [&] { return launch_deferred(c); });
@@ -578,8 +583,8 @@ scan_status sharded_all(Ctx& c) {
     flush_fills(c);
     if (!smap.empty()) {
       k_link_pack<<<(unsigned)smap.size(), 256, 0, c.stream>>>(c.lk_sendmap.as<LinkMap>(), c.inst_rec.as<uint4>(),
-                                                              c.p2p_iter.as<uint32_t>(), c.p2p_pay.as<uint32_t>(),
-                                                              c.p2p_inst0, c.p2p_slot0, c.x_send.as<uint32_t>());
+                                                              c.slots.as<uint4>(), c.p2p_inst0, c.p2p_slot0,
+                                                              c.x_send.as<uint32_t>());
       c.launches += 1;
     }
     int xr = 0;
@@ -596,8 +601,8 @@ scan_status sharded_all(Ctx& c) {
     if (xr) { c.err = std::string("exchange all-to-all: ") + xch_error(xr); return SCAN_E_NCCL; }
     if (!rmap.empty()) {
       k_link_unpack<<<(unsigned)rmap.size(), 256, 0, c.stream>>>(c.lk_recvmap.as<LinkMap>(), c.x_recv.as<uint32_t>(),
-                                                                c.inst_rec.as<uint4>(), c.p2p_iter.as<uint32_t>(),
-                                                                c.p2p_pay.as<uint32_t>(), c.p2p_inst0, c.p2p_slot0);
+                                                                c.inst_rec.as<uint4>(), c.slots.as<uint4>(),
+                                                                c.p2p_inst0, c.p2p_slot0);
       c.launches += 1;
     }
   }

@@ -44,15 +44,14 @@ struct StreamState {
 namespace {
 
 __global__ void k_stream_pack(uint32_t n_comms, const uint32_t* nl, const uint32_t* loff, const uint64_t* ch_base,
-                              const uint64_t* ch_slot, const uint4* rec, const uint32_t* pay, uint64_t p2p_slot0,
-                              uint32_t* out) {
+                              const uint64_t* ch_slot, const uint4* rec, const uint4* slots, uint32_t* out) {
   const uint32_t l = blockIdx.x;
   const uint64_t b = ch_base[n_comms + l], sb = ch_slot[n_comms + l];
   for (uint32_t k = threadIdx.x; k < nl[l]; k += blockDim.x) {
     const uint4 r = rec[b + k];
     uint32_t* o = out + 3ull * (loff[l] + k);
     o[0] = r.x;
-    o[1] = pay[sb + 2ull * k - p2p_slot0];
+    o[1] = (r.w & SCAN_F_VALID) ? slots[sb + 2ull * k].w : 0u;  // the send slot's payload (valid samples only)
     o[2] = r.w & 0xFFu;
   }
 }
@@ -256,8 +255,8 @@ scan_status scan_stream_push(scan_ctx* ctx, const scan_event_columns* iteration,
   c.launches += launch_shard_head(u, S.rg_ht.as<unsigned long long>() + s * W);
   if (S.np) {
     k_stream_pack<<<S.np, 128, 0, c.stream>>>(u.n_comms, S.d_nl.as<uint32_t>(), S.d_loff.as<uint32_t>(), u.ch_base.as<uint64_t>(),
-                                             u.ch_slot.as<uint64_t>(), u.inst_rec.as<uint4>(), u.p2p_pay.as<uint32_t>(),
-                                             u.p2p_slot0, S.rg_smp.as<uint32_t>() + 3 * s * S.npi);
+                                             u.ch_slot.as<uint64_t>(), u.inst_rec.as<uint4>(), u.slots.as<uint4>(),
+                                             S.rg_smp.as<uint32_t>() + 3 * s * S.npi);
     c.launches += 1;
   }
   S.cnt[s] = {u.hc.n_incomplete, u.hc.n_kind_mismatch, u.hc.n_payload_mismatch, u.n_inst};
