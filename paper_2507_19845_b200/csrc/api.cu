@@ -1,6 +1,7 @@
 // api.cu — C ABI (include/megascan/scan.h): context, ingest, and the host orchestration of the
 // A1-A8 kernels. No CPU fallback: every analysis step runs in the kernels of k_match.cu,
 // k_stats.cu; this file only sizes buffers, launches, and reads back counters.
+#include <cstdio>
 #include <algorithm>
 #include <cstring>
 #include <numeric>
@@ -98,14 +99,14 @@ static void release_all(Ctx& c) {
                     &c.t_prevj, &c.r_nkeys, &c.r_keys, &c.r_cnt, &c.r_ncomm, &c.r_niter, &c.r_ncomp, &c.r_lastit,
                     &c.r_comm_off, &c.r_comp_off, &c.r_bits_off, &c.bitmap, &c.bitpre, &c.bmsum, &c.counters, &c.ch_nmax,
                     &c.ch_nmin, &c.ch_base, &c.ch_slot, &c.ch_nsend, &c.ch_nrecv, &c.inst_c, &c.wait_c, &c.cdur, &c.cop,
-                    &c.slots, &c.inst_rec, &c.citer, &c.nbp, &c.nbp_n,
+                    &c.slots, &c.lk_key, &c.inst_rec, &c.citer, &c.nbp, &c.nbp_n,
                     &c.rk_sum, &c.bits, &c.cref, &c.cl_J, &c.cl_max, &c.cl_min, &c.wd_total, &c.wd_slow, &c.wd_cand,
                     &c.wd_frac, &c.wl_joined, &c.wl_late, &c.wl_frac, &c.wl_verdict, &c.wl_link_slow, &c.ewc, &c.ewp,
                     &c.lk_n, &c.lk_used, &c.lk_medp, &c.lk_medt, &c.lk_bw, &c.lk_slow, &c.lk_dir, &c.lk_elig,
                     &c.lb_label, &c.lb_rkind, &c.lb_rrank, &c.lb_rsrc, &c.lb_depth, &c.lb_twait, &c.scratch,
                     &c.st_tile0, &c.st_npos, &c.role_comm, &c.role_slot, &c.role_type, &c.ncroles, &c.ft_cols,
                     &c.ft_base, &c.ft_last, &c.st_tot, &c.p2p_rbase, &c.dlate, &c.dinfo, &c.ft_posA, &c.ft_posB,
-                    &c.ft_posK, &c.eidx, &c.tile_stage, &c.xbase, &c.lk_scratch, &c.g_base, &c.g_slot,
+                    &c.ft_posK, &c.eidx, &c.tile_stage, &c.xbase, &c.g_base, &c.g_slot,
                     &c.g_nmax, &c.g_nmin, &c.g_k0, &c.p2p_eslot, &c.xe_off, &c.xe_col, &c.xbig, &c.own_start, &c.al_tend, &c.al_aend, &c.al_anct,
                     &c.al_anco, &c.al_slotci, &c.al_level, &c.al_nanc, &c.al_resid, &c.al_flag, &c.al_start, &c.al_ranks, &c.al_cch, &c.al_tgt, &c.x_send, &c.x_recv, &c.x_recv2, &c.x_ep, &c.x_stage, &c.headtail, &c.lk_sendmap, &c.lk_recvmap, &c.bl_inst, &c.bl_wait, &c.bl_p0, &c.bl_pa, &c.bl_pb, &c.bl_root, &c.bl_last, &c.bl_rank, &c.bl_rk};
   for (DevBuf* b : bufs) b->release();
@@ -476,6 +477,7 @@ scan_status ms::alloc_match_buffers(Ctx& c, bool fused) {
   if (!fused) { CK(c.cdur.ensure(c.n_comp * 4)); CK(c.cop.ensure(c.n_comp * 2)); }
   if ((uint64_t)c.it_off + c.n_iters >= SLOT_MAX_ITERS) { c.err = "more than 2^28 iterations"; return SCAN_E_UNSUPPORTED; }
   CK(c.slots.ensure(c.n_slots * 16));
+  CK(c.lk_key.ensure(std::max<uint64_t>(c.n_inst - c.p2p_inst0, 1) * 8));
   if (fused) CK(c.p2p_rbase.ensure(W * 16 * 4));
   CK(c.inst_rec.ensure(c.n_inst * 16));
   const uint32_t NIT1 = c.NIT + 1;
@@ -607,7 +609,8 @@ scan_status general_localize(Ctx& c) {
   for (auto& v : z.v_count) v = 0;
   CK(cudaMemcpyAsync(c.counters.p, &z, sizeof(Counters), cudaMemcpyHostToDevice, c.stream));
   c.launches += timed(c, "k_event_pass", [&] { return launch_event_pass(c); });
-  c.launches += timed(c, "k_links", [&] { return launch_links(c); });
+  c.launches += timed(c, "k_link_median", [&] { return launch_link_median(c); });
+  c.launches += timed(c, "k_link_flags", [&] { return launch_link_flags(c); });
   c.launches += timed(c, "k_walk", [&] { return launch_verdict_walk(c); });
   if ((st = sync_read(c))) return st;
   if (c.hc.overflow & 24u) {
@@ -624,6 +627,16 @@ scan_status general_localize(Ctx& c) {
 // per-rank event counts (a new iteration of an SPMD job): the template, tile bases, channel tables
 // and buffer sizes are reused; the fused kernel re-verifies every event against the cached
 // template (a deviation is reported, never silently analysed). Partials only (partial_tail).
+bool ms::sync_check_on() {
+  static const bool on = [] { const char* e = std::getenv("MS_SYNC_CHECK"); return e && *e == '1'; }();
+  return on;
+}
+
+void ms::sync_check(Ctx& c, const char* name) {
+  const cudaError_t e = cudaStreamSynchronize(c.stream);
+  if (e != cudaSuccess) std::fprintf(stderr, "[MS_SYNC_CHECK] %s: %s\n", name, cudaGetErrorString(e));
+}
+
 scan_status ms::fused_rerun(Ctx& c) {
   c.matched = c.detected = c.localized = false;
   scan_status st;
@@ -694,7 +707,8 @@ scan_status ms::fused_all(Ctx& c) {
   c.launches += timed(c, "k_wd_finish", [&] { return launch_wd_finish(c); });
   // links and walk run before the SPMD verification result is read (one host sync less): on a
   // failed verification their inputs are garbage but in bounds, and the call reruns the general path
-  c.launches += timed(c, "k_links", [&] { return launch_links(c); });
+  c.launches += timed(c, "k_link_median", [&] { return launch_link_median(c); });
+  c.launches += timed(c, "k_link_flags", [&] { return launch_link_flags(c); });
   c.launches += timed(c, "k_walk", [&] { return launch_verdict_walk(c); });
   if ((st = sync_read(c))) return st;
   if (c.hc.overflow & 32u) return 2;

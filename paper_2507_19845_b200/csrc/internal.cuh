@@ -42,6 +42,20 @@ __device__ __forceinline__ uint32_t slot_z(uint32_t it, uint32_t kind, uint32_t 
 }
 __device__ __forceinline__ uint32_t slot_kind(uint32_t z) { return (z >> 28) & 7u; }
 
+// Stage-3 sample key of a P2P instance (k_link_median): the f64 ratio payload / transfer as sortable
+// bits (positive: bit order = value order; exactly rounded, so monotone in the exact ratio), bit 63 =
+// warm-up flag; LK_NONE when the instance is not a sample (invalid, or transfer 0). Written by the
+// instance reduction (k_cross_reduce / k_inst_reduce), the X3 unpack and the stream window.
+constexpr unsigned long long LK_NONE = 0x7FFFFFFFFFFFFFFFull;  // a NaN pattern: no finite ratio has it
+constexpr unsigned long long LK_WARM = 1ull << 63;
+__device__ __forceinline__ unsigned long long ratio_key(uint32_t p, uint32_t t) {
+  return (unsigned long long)__double_as_longlong((double)p / (double)t);
+}
+__device__ __forceinline__ unsigned long long lk_sample_key(uint32_t flags, uint32_t t, uint32_t p) {
+  if (!(flags & SCAN_F_VALID) || t == 0) return LK_NONE;
+  return ratio_key(p, t) | ((flags & SCAN_F_WARMUP) ? LK_WARM : 0ull);
+}
+
 // ----------------------------------------------------------------------------- device buffers
 struct DevBuf {
   void* p = nullptr;
@@ -129,6 +143,7 @@ struct Ctx {
   DevBuf inst_c, wait_c;                 // per comm event
   DevBuf cdur, cop;                      // per compute event (rank-compacted)
   DevBuf slots;                          // SlotRec (uint4) per member slot, slot order
+  DevBuf lk_key;                         // u64 per P2P instance: stage-3 sample key (lk_sample_key)
   DevBuf inst_rec;                       // uint4 per instance {dmin, dmax, last_rank, flags | cls<<8}
   DevBuf citer;                          // u32 [W][NIT+1]
   DevBuf nbp, nbp_n;                     // P2P neighbours per rank [W][PCAP]
@@ -178,7 +193,6 @@ struct Ctx {
   DevBuf eidx;                           // [W][TP+DP] edge slot of each TP-/DP-group partner
   DevBuf tile_stage;                     // [n_ftiles] stage of each fused tile (u8)
   DevBuf xbase;                          // [NCH+1] cross-stage instance index
-  DevBuf lk_scratch;                     // link-median scratch for links above the shared-memory capacity
   DevBuf p2p_eslot;                      // [n_p2p][2] wait-for edge column per P2P link direction
   DevBuf xe_off, xe_col;                 // cross collectives: member x member edge-column tables (built at load)
   DevBuf xbig; uint32_t n_big = 0;       // cross collectives with more than 32 members (k_cross_big)
@@ -232,9 +246,12 @@ inline void queue_fill(Ctx& c, void* p, uint64_t bytes, uint8_t v) { if (p && by
 int flush_fills(Ctx& c);
 
 // Launch wrapper: records an event pair around a launcher when timing is on.
+bool sync_check_on();  // MS_SYNC_CHECK=1: synchronise after every launcher and name the one that faulted (diagnostics)
+void sync_check(Ctx& c, const char* name);
 template <class F>
 int timed(Ctx& c, const char* name, F&& f) {
   flush_fills(c);
+  if (sync_check_on()) { const int n = f(); sync_check(c, name); return n; }
   if (!c.timing) return f();
   int k = -1;
   for (size_t i = 0; i < c.knames.size(); ++i) if (c.knames[i] == name) k = (int)i;
@@ -287,7 +304,7 @@ int xch_group_end(Ctx& c);
 const char* xch_error(int rc);
 int launch_shard_fixup(Ctx& c, int G, const unsigned long long* ht);
 int launch_link_median_window(Ctx& c, const uint64_t* base, const uint32_t* nmax, const uint64_t* slot, const uint4* rec,
-                              const uint32_t* iter, const uint32_t* pay, uint64_t n_inst);
+                              const uint32_t* iter, const uint32_t* pay, const unsigned long long* key, uint64_t n_inst);
 scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out);
 scan_status ensure_tiles(Ctx& c);
 void shard_release(Ctx& c);

@@ -663,7 +663,9 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
         si = a.ch_slot[cid] + (uint64_t)kk * nm + a.role_slot[(uint64_t)r * CROLES + role];
       } else {  // a P2P instance's send / receive slots sit at p2p_slot0 + 2 (inst - p2p_inst0) + 0 / 1
         const bool send = (role >> 3) & 1u;
-        inst = (uint64_t)a.p2p_rbase[(uint64_t)r * 16 + (role - 16)] + kk;
+        const uint32_t rb = a.p2p_rbase[(uint64_t)r * 16 + (role - 16)];
+        if (rb == NONE32) { atomicOr(&a.cnt->overflow, NOT_SPMD); continue; }  // no such link: not the template's trace
+        inst = (uint64_t)rb + kk;
         si = a.p2p_slot0 + 2 * (inst - a.p2p_inst0) + (send ? 0 : 1);
         pay = a.pay[e];
         if (send) warm = ((uint32_t)a.meta[e] >> 14) & 1u;
@@ -694,7 +696,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
       const uint32_t si = sinst[cls < 2 ? p * G + (cls == 0 ? (rg & 0xFFFFu) : (rg >> 16)) : 0u];
       uint32_t* dst = a.inst_c + coffr[row] + m0 + j;
       *dst = cls < 2 ? si : v;
-      if (cls < 2) a.wait_c[dst - a.inst_c] = v;
+      a.wait_c[dst - a.inst_c] = cls < 2 ? v : 0u;  // cross positions: placeholder (k_xwait_scatter), full sectors
     }
     if (__any_sync(0xFFFFFFFFu, mis) && lane == 0) atomicOr(&a.cnt->overflow, NOT_SPMD);
   }
@@ -1111,11 +1113,22 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
         } else {  // a P2P instance's send / receive slots sit at p2p_slot0 + 2 (inst - p2p_inst0) + 0 / 1
           const bool send = (role >> 3) & 1u;
           const uint64_t e = rbase + (uint64_t)row * npos + p0 + p;
-          inst = (uint64_t)a.p2p_rbase[(uint64_t)r * 16 + (role - 16)] + kk;
+          const uint32_t rb = a.p2p_rbase[(uint64_t)r * 16 + (role - 16)];
+          if (rb == NONE32) {  // no such link: the trace is not what the template says
+#ifdef MS_DEBUG_CHECKS
+            printf("k_fused_t: row %u role %u has no P2P channel (tile %u)\n", row, role, tile);
+#endif
+            atomicOr(&a.cnt->overflow, NOT_SPMD);
+            continue;
+          }
+          inst = (uint64_t)rb + kk;
           si = a.p2p_slot0 + 2 * (inst - a.p2p_inst0) + (send ? 0 : 1);
           pay = a.pay[e];
           if (send) warm = ((uint32_t)a.meta[e] >> 14) & 1u;
         }
+#if defined(MS_EXP_SKIP) && (MS_EXP_SKIP & 256)
+        if (R == 0)  // timing experiment only (results invalid)
+#endif
         a.slots[si] = make_uint4(col[row], (uint32_t)(coffr[row] + m0 + jj), slot_z(itp, pk[p], warm), pay);
         col[row] = (uint32_t)inst;  // cross positions: the tile now holds the instance id
       }
@@ -1138,6 +1151,9 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
       const bool islast = row == lastrow;
       if (leader) {
         const uint64_t inst = rcb[row0 * NCRM + role] + kinst;
+#if defined(MS_EXP_SKIP) && (MS_EXP_SKIP & 512)
+        if (R == 0)  // timing experiment only (results invalid)
+#endif
         a.rec[inst] = make_uint4(mn, mx, last, (SCAN_F_COMPLETE | SCAN_F_KIND_OK | SCAN_F_PAYLOAD_OK | SCAN_F_VALID |
                                                 (nat == 1 ? SCAN_F_UNIQUE_LAST : 0u)) | (clsid << 8));
         sinst[p * GS + g] = (uint32_t)inst;
@@ -1239,6 +1255,7 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
         a.wait_c[o] = v;
       } else {
         a.inst_c[o] = v;  // cross positions: the tile holds the instance id
+        a.wait_c[o] = 0;  // placeholder until k_xwait_scatter: no holes, so no partial-sector (read-modify-write) stores
       }
     }
   }
@@ -1513,6 +1530,7 @@ struct XArgs {
   const uint32_t* r_nkeys; const uint32_t* r_keys; const uint32_t* r_cnt;
   uint4* slots;  // SlotRec; after the reduction a member slot's x holds that member's wait (instance order)
   uint4* rec; uint32_t* wait_c;
+  unsigned long long* lk_key; uint64_t p2p_inst0;  // stage-3 sample key per P2P instance
   const uint64_t* nbc_off; const uint32_t* nbc; const uint32_t* nbp; const uint32_t* nbp_n; uint64_t nnz_tot, nnz_c;
   unsigned long long* ew; unsigned long long* rk_sum; uint32_t wi; unsigned long long wait_margin;
   Counters* cnt;
@@ -1666,6 +1684,7 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
         ++inc;
       }
       a.rec[i] = make_uint4(dmin, dmax, last, flags | ((isp ? 0u : a.ccls[ch]) << 8));
+      if (isp) a.lk_key[i - a.p2p_inst0] = lk_sample_key(flags, dmin, s0.w);
     }
     if (uni) {
       // aggregated per-member sums (members identical across lanes); the wait-for edge too when
@@ -1742,6 +1761,7 @@ static XArgs cross_args(Ctx& c) {
   a.psrc = c.ch_nsend.as<uint32_t>() + c.n_p2p; a.pdst = c.ch_nrecv.as<uint32_t>() + c.n_p2p;
   a.r_nkeys = c.r_nkeys.as<uint32_t>(); a.r_keys = c.r_keys.as<uint32_t>(); a.r_cnt = c.r_cnt.as<uint32_t>();
   a.slots = c.slots.as<uint4>(); a.rec = c.inst_rec.as<uint4>(); a.wait_c = c.wait_c.as<uint32_t>();
+  a.lk_key = c.lk_key.as<unsigned long long>(); a.p2p_inst0 = c.p2p_inst0;
   a.nbc_off = c.nbc_off.as<uint64_t>(); a.nbc = c.nbc.as<uint32_t>(); a.nbp = c.nbp.as<uint32_t>(); a.nbp_n = c.nbp_n.as<uint32_t>();
   a.nnz_tot = c.nnz_c + (uint64_t)c.W * PCAP; a.nnz_c = c.nnz_c;
   a.ew = c.ewc.as<unsigned long long>(); a.rk_sum = c.rk_sum.as<unsigned long long>();

@@ -693,7 +693,8 @@ __global__ void __launch_bounds__(256) k_inst_reduce(uint64_t n_inst, uint64_t N
                                                      const uint32_t* ch_nmin, const uint64_t* coff,
                                                      const uint32_t* cmem, const uint8_t* ccls,
                                                      const uint32_t* nsend, const uint32_t* psrc, const uint32_t* pdst,
-                                                     const uint4* slots, uint4* rec, Counters* cnt) {
+                                                     const uint4* slots, uint4* rec, unsigned long long* lk_key,
+                                                     uint64_t p2p_inst0, Counters* cnt) {
   uint32_t inc = 0, kmis = 0, pmis = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_inst; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t ch = upper_bound_u64(ch_base, NCH + 1, i) - 1;
@@ -733,6 +734,7 @@ __global__ void __launch_bounds__(256) k_inst_reduce(uint64_t n_inst, uint64_t N
       ++inc;
     }
     rec[i] = make_uint4(dmin, dmax, last, flags | (cls << 8));
+    if (isp) lk_key[i - p2p_inst0] = lk_sample_key(flags, dmin, (flags & SCAN_F_VALID) ? slots[sb].w : 0u);
   }
   inc = warp_sum_u32(inc); kmis = warp_sum_u32(kmis); pmis = warp_sum_u32(pmis);
   if (lane_id() == 0) {
@@ -749,7 +751,7 @@ int launch_inst_reduce(Ctx& c) {
                                               c.ch_nmin.as<uint32_t>(), c.coff.as<uint64_t>(), c.cmem.as<uint32_t>(),
                                               c.ccls.as<uint8_t>(), c.ch_nsend.as<uint32_t>(), c.ch_nsend.as<uint32_t>() + c.n_p2p,
                                               c.ch_nrecv.as<uint32_t>() + c.n_p2p, c.slots.as<uint4>(), c.inst_rec.as<uint4>(),
-                                              c.counters.as<Counters>());
+                                              c.lk_key.as<unsigned long long>(), c.p2p_inst0, c.counters.as<Counters>());
   return 1;
 }
 

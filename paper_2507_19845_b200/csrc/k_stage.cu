@@ -906,7 +906,7 @@ __global__ void __launch_bounds__(SG_NT, 1) k_stage(const __grid_constant__ Stag
         const uint32_t off = (pw(cv & 0xFFFu) ^ ((row & 7u) << 2)) + row * 32u;
         const uint64_t o = coffr[row] + m0 + jj;
         a.inst_c[o] = comm_s[off];
-        if ((cv >> 12) < 2) a.wait_c[o] = dur_s[off];
+        a.wait_c[o] = (cv >> 12) < 2 ? dur_s[off] : 0u;  // cross: placeholder until k_xwait_scatter
       }
     }
     fence_proxy_async();  // generic-proxy accesses of the slot before the next TMA overwrites it

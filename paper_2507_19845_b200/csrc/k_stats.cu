@@ -383,7 +383,10 @@ __device__ void smem_bitonic(uint32_t* sp, uint32_t* st, uint32_t* si, uint32_t 
         const uint32_t ixj = i ^ j;
         if (ixj > i) {
           const bool up = (i & k) == 0;
-          const bool gt = samp_less(sp[ixj], st[ixj], si[ixj], sp[i], st[i], si[i]);
+          // element ixj before element i; the padding (index NONE32) after every element, whatever
+          // its ratio (a transfer of 0 would otherwise order a pad first)
+          const bool gt = si[i] == NONE32 ? si[ixj] != NONE32
+                                          : (si[ixj] != NONE32 && samp_less(sp[ixj], st[ixj], si[ixj], sp[i], st[i], si[i]));
           if (gt == up) {
             uint32_t t;
             t = sp[i]; sp[i] = sp[ixj]; sp[ixj] = t;
@@ -400,46 +403,21 @@ struct LKArgs {
   uint32_t n_comms, n_p2p, NW, wi; int W, TP, DP;
   const uint64_t* ch_base; const uint32_t* ch_nmax; const uint32_t* ch_nmin; const uint32_t* psrc; const uint32_t* pdst;
   const uint4* rec;
-  // per P2P instance i (index i - p2p_inst0): payload pay[. * pay_stride], send iteration iter[. * iter_stride] & it_mask
+  const unsigned long long* key;  // per P2P instance (index i - p2p_inst0): lk_sample_key
+  // per P2P instance: payload pay[. * pay_stride] (exact tie order), send iteration iter[. * iter_stride] & it_mask
   const uint32_t* pay; const uint32_t* iter; uint32_t pay_stride, iter_stride, it_mask;
   uint64_t p2p_inst0;
   uint32_t min_samples;
   uint32_t* lk_n; uint8_t* lk_used; uint32_t* lk_medp; uint32_t* lk_medt; double* lk_bw; uint8_t* lk_dir; uint8_t* lk_elig;
   Counters* cnt;
-  unsigned long long* gkey; uint32_t* gid;  // global scratch for links with more than LM_CAP instances
-  uint32_t n_shards, shard;                 // sharded: this shard computes the links with pid % n_shards == shard
+  uint32_t n_shards, shard;  // sharded: this shard computes the links with pid % n_shards == shard
 };
 
-// Order key of a sample: the f64 ratio p/t (exactly rounded, monotone in the exact ratio) as
-// sortable bits; exact ties between distinct ratios with equal f64 are resolved afterwards.
-__device__ __forceinline__ unsigned long long ratio_key(uint32_t p, uint32_t t) {
-  return (unsigned long long)__double_as_longlong((double)p / (double)t);  // positive: bit order = value order
-}
-
-constexpr int LM_NT = 512;         // 2 CTAs x 16 warps per SM
-constexpr uint32_t LM_CAP = 8192;  // instances per link whose samples are held in shared memory (else global scratch)
+constexpr int LM_NT = 128;         // 4 warps, up to 16 CTAs per SM: every (window, link) of C3 in one wave
 constexpr uint32_t LM_NB = 2048;   // bins of one selection pass over a key range
 constexpr uint32_t LM_CC = 512;    // candidates ranked directly
 
-// warp 0 finds the bin holding rank tgt in a 256-bin histogram: returns (bin, count below it)
-__device__ __forceinline__ void hist_find(const uint32_t* hist, uint32_t tgt, uint32_t& bin, uint32_t& below) {
-  const uint32_t lane = lane_id();
-  uint32_t v[8], sum = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) { v[i] = hist[lane * 8 + i]; sum += v[i]; }
-  const uint32_t inc = warp_incl_scan(sum), ex = inc - sum;
-  const unsigned hit = __ballot_sync(0xFFFFFFFFu, ex <= tgt && tgt < inc);
-  const uint32_t L = __ffs(hit) - 1;
-  uint32_t acc = __shfl_sync(0xFFFFFFFFu, ex, L), b = 0;
-  if (lane == L) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) { if (acc + v[i] > tgt) { b = i; break; } acc += v[i]; }
-  }
-  bin = L * 8 + __shfl_sync(0xFFFFFFFFu, b, L);
-  below = __shfl_sync(0xFFFFFFFFu, acc, L);
-}
-
-// the same over LM_NB bins (64 per lane)
+// warp 0 finds the bin holding rank tgt in an LM_NB-bin histogram (64 bins per lane): (bin, count below it)
 __device__ __forceinline__ void hist_find_nb(const uint32_t* hist, uint32_t tgt, uint32_t& bin, uint32_t& below) {
   const uint32_t lane = lane_id();
   const uint4* h4 = reinterpret_cast<const uint4*>(hist + lane * 64);
@@ -448,6 +426,13 @@ __device__ __forceinline__ void hist_find_nb(const uint32_t* hist, uint32_t tgt,
   for (int i = 0; i < 16; ++i) { const uint4 v = h4[i]; sum += v.x + v.y + v.z + v.w; }
   const uint32_t inc = warp_incl_scan(sum), ex = inc - sum;
   const unsigned hit = __ballot_sync(0xFFFFFFFFu, ex <= tgt && tgt < inc);
+  if (!hit) {  // tgt beyond the histogram's total (inconsistent inputs): no bin
+#ifdef MS_DEBUG_CHECKS
+    if (lane == 0) printf("k_link_median: rank %u beyond the histogram total %u (block %u)\n", tgt, __shfl_sync(0xFFFFFFFFu, inc, 31), blockIdx.x);
+#endif
+    bin = LM_NB; below = 0;
+    return;
+  }
   const uint32_t L = __ffs(hit) - 1;
   uint32_t acc = __shfl_sync(0xFFFFFFFFu, ex, L), b = 0;
   if (lane == L) {
@@ -457,11 +442,10 @@ __device__ __forceinline__ void hist_find_nb(const uint32_t* hist, uint32_t tgt,
   below = __shfl_sync(0xFFFFFFFFu, acc, L);
 }
 
-// shared histogram add with the lanes of a warp that share a bin combined (bin >= nb = none);
-// samples of one link cluster in a few bins
-__device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t bin, uint32_t nb = 256u) {
+// shared histogram add with the lanes of a warp that share a bin combined (bin >= LM_NB = none)
+__device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t bin) {
   const unsigned peers = __match_any_sync(0xFFFFFFFFu, bin);
-  if (bin < nb && (lane_id() == (uint32_t)(__ffs(peers) - 1))) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
+  if (bin < LM_NB && (lane_id() == (uint32_t)(__ffs(peers) - 1))) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
 }
 
 __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
@@ -473,106 +457,94 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
   return v;
 }
 
-// One CTA per (window, link). (1) One pass over the link's instances: the samples (valid, transfer
-// > 0, send in the window) go to shared memory as (f64 ratio key, instance index), warm-up samples
-// from the front, the others from the back, with the key range of each group. (2) Lower-median rank
-// (n-1)/2 of the chosen group (warm-up if >= min_samples, reading R13): histogram passes of LM_NB bins
-// over the shrinking key range until the target bin holds <= LM_CC samples, which are ranked
-// directly. (3) Ties on the f64 key: the exact order (p/t, instance id), as before.
+// One CTA per (window, link), reading the instances' sample keys (lk_sample_key, written by the
+// instance reduction). (1) The window's instances are a contiguous occurrence range (the send
+// iteration is nondecreasing in the occurrence index): two binary searches. One pass counts the
+// samples (warm-up / all) and their key ranges. (2) Lower-median rank (n-1)/2 of the chosen group
+// (warm-up if >= min_samples, reading R13): histogram passes of LM_NB bins over the shrinking key
+// range until the target bin holds <= LM_CC samples, which are ranked directly. (3) Ties on the f64
+// key: the exact order (p/t, instance index) of reading R13.
 __global__ void __launch_bounds__(LM_NT) k_link_median(LKArgs a) {
-  extern __shared__ __align__(8) uint8_t lsm[];
+  // a job the fused pass rejected (the general path reruns it): its inputs are not instance records
+  if (*((volatile const unsigned*)&a.cnt->overflow) & NOT_SPMD) return;
   __shared__ __align__(16) uint32_t hist[LM_NB];
   __shared__ unsigned long long cand[LM_CC];
-  __shared__ unsigned long long s_min[2], s_max[2], s_lo, s_hi, s_prefix, s_K;
-  __shared__ uint32_t s_nw, s_nn, s_target, s_cnt, s_nc, s_tg, s_tie, s_pick, s_exact_eq, s_ref;
+  __shared__ unsigned long long s_min[2], s_max[2], s_lo, s_hi, s_K;
+  __shared__ uint32_t s_nw, s_na, s_target, s_cnt, s_nc, s_tg, s_tie, s_pick, s_exact_eq, s_ref, s_k0, s_k1;
+  __shared__ uint32_t scan_sm[33];
+  __shared__ uint32_t s_bad;
   const uint32_t o = blockIdx.x;
   const uint32_t w = o / a.n_p2p, pid = o % a.n_p2p;
   const uint64_t ch = a.n_comms + pid;
   const uint64_t b = a.ch_base[ch];
   const uint32_t n = a.ch_nmax[ch];
-  const uint32_t nmin = a.ch_nmin ? a.ch_nmin[ch] : n;  // a valid instance is complete: k < nmin
+  const uint32_t nmin = a.ch_nmin ? a.ch_nmin[ch] : n;  // samples are valid, hence complete: k < nmin
   const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
   const uint32_t src = a.psrc[pid], dst = a.pdst[pid];
-  if (a.n_shards > 1 && pid % a.n_shards != a.shard) {  // another shard owns this link: zeros for the all-reduce
-    if (tid == 0) {
-      const int dpp = (int)(dst / (uint32_t)(a.TP * a.DP)) - (int)(src / (uint32_t)(a.TP * a.DP));
-      a.lk_dir[o] = dpp == 1 ? 0 : (dpp == -1 ? 1 : 2);
-      a.lk_n[o] = 0; a.lk_used[o] = 0; a.lk_elig[o] = 0; a.lk_medp[o] = 0; a.lk_medt[o] = 0; a.lk_bw[o] = 0.0;
-    }
-    return;
-  }
-  if (tid == 0) { s_nw = 0; s_nn = 0; s_min[0] = s_min[1] = ~0ull; s_max[0] = s_max[1] = 0; }
-  __syncthreads();
-  const bool in_smem = n <= LM_CAP;
-  const uint32_t cap = in_smem ? LM_CAP : n;
-  unsigned long long* sk = in_smem ? (unsigned long long*)lsm : a.gkey + (b - a.p2p_inst0);
-  uint32_t* si = in_smem ? (uint32_t*)(lsm + (size_t)LM_CAP * 8) : a.gid + (b - a.p2p_inst0);
-  const uint64_t rel0 = b - a.p2p_inst0;
-  // (1) samples: each warp takes 32-instance chunks, four chunks' loads in flight
-  unsigned long long mnw = ~0ull, mxw = 0, mnn = ~0ull, mxn = 0;
-  for (uint32_t kb = wid * 32; kb < n; kb += 4 * LM_NT) {
-    uint4 rc[4];
-    uint32_t pv[4], iv[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t k = kb + u * LM_NT + lane;
-      rc[u] = make_uint4(0, 0, 0, 0); pv[u] = 0; iv[u] = 0;
-      if (k < n) {
-        rc[u] = a.rec[b + k];
-        if (k < nmin) {
-          pv[u] = a.pay[(rel0 + k) * a.pay_stride];
-          if (a.wi) iv[u] = a.iter[(rel0 + k) * a.iter_stride] & a.it_mask;
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t k = kb + u * LM_NT + lane;
-      const bool in = k < n && (rc[u].w & SCAN_F_VALID) && rc[u].x != 0 && (!a.wi || iv[u] / a.wi == w);
-      const bool warm = in && (rc[u].w & SCAN_F_WARMUP);
-      const unsigned bw = __ballot_sync(0xFFFFFFFFu, warm), bn = __ballot_sync(0xFFFFFFFFu, in && !warm);
-      if (!(bw | bn)) continue;
-      uint32_t ow = 0, on = 0;
-      if (lane == 0) {
-        if (bw) ow = atomicAdd(&s_nw, (uint32_t)__popc(bw));
-        if (bn) on = atomicAdd(&s_nn, (uint32_t)__popc(bn));
-      }
-      ow = __shfl_sync(0xFFFFFFFFu, ow, 0); on = __shfl_sync(0xFFFFFFFFu, on, 0);
-      if (in) {
-        const unsigned long long key = ratio_key(pv[u], rc[u].x);
-        const unsigned lt = (1u << lane) - 1u;
-        const uint32_t pos = warm ? ow + __popc(bw & lt) : cap - 1u - (on + __popc(bn & lt));
-        sk[pos] = key; si[pos] = k;
-        if (warm) { mnw = min(mnw, key); mxw = max(mxw, key); }
-        else { mnn = min(mnn, key); mxn = max(mxn, key); }
-      }
-    }
-  }
-  mnw = warp_min_u64(mnw); mxw = warp_max_u64(mxw); mnn = warp_min_u64(mnn); mxn = warp_max_u64(mxn);
-  if (lane == 0) {
-    if (mnw != ~0ull) { atomicMin(&s_min[0], mnw); atomicMax(&s_max[0], mxw); }
-    if (mnn != ~0ull) { atomicMin(&s_min[1], mnn); atomicMax(&s_max[1], mxn); }
-  }
-  __syncthreads();
-  const uint32_t nw = s_nw, nn = s_nn;
-  const bool use_warm = nw >= a.min_samples;
-  const uint32_t nu = use_warm ? nw : nw + nn;
   if (tid == 0) {
     const int dpp = (int)(dst / (uint32_t)(a.TP * a.DP)) - (int)(src / (uint32_t)(a.TP * a.DP));
     a.lk_dir[o] = dpp == 1 ? 0 : (dpp == -1 ? 1 : 2);
+    a.lk_n[o] = 0; a.lk_used[o] = 0; a.lk_elig[o] = 0; a.lk_medp[o] = 0; a.lk_medt[o] = 0; a.lk_bw[o] = 0.0;
+  }
+  if (a.n_shards > 1 && pid % a.n_shards != a.shard) return;  // another shard owns this link: zeros for the all-reduce
+  const uint64_t rel0 = b - a.p2p_inst0;
+  const unsigned long long* key = a.key + rel0;
+  if (tid == 0) {
+    uint32_t k0 = 0, k1 = nmin;
+    if (a.wi) {  // first k with iteration / wi >= w, then >= w + 1
+      auto win = [&](uint32_t k) { return (a.iter[(rel0 + k) * a.iter_stride] & a.it_mask) / a.wi; };
+      uint32_t lo = 0, hi = nmin;
+      while (lo < hi) { const uint32_t m = (lo + hi) >> 1; if (win(m) < w) lo = m + 1; else hi = m; }
+      k0 = lo; hi = nmin;
+      while (lo < hi) { const uint32_t m = (lo + hi) >> 1; if (win(m) <= w) lo = m + 1; else hi = m; }
+      k1 = lo;
+    }
+    s_k0 = k0; s_k1 = k1; s_bad = 0;
+#ifdef MS_DEBUG_CHECKS
+    if (k1 > n || k0 > k1) printf("k_link_median[%u]: range [%u, %u) beyond %u instances (nmin %u)\n", o, k0, k1, n, nmin);
+#endif
+    s_nw = 0; s_na = 0; s_min[0] = s_min[1] = ~0ull; s_max[0] = s_max[1] = 0;
+  }
+  __syncthreads();
+  const uint32_t k0 = s_k0, k1 = s_k1;
+  // (1) counts and key ranges, four loads in flight per thread
+  {
+    unsigned long long mnw = ~0ull, mxw = 0, mna = ~0ull, mxa = 0;
+    uint32_t cw = 0, ca = 0;
+    for (uint32_t kb = k0 + tid; kb < k1; kb += 4 * LM_NT) {
+      unsigned long long v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { const uint32_t k = kb + u * LM_NT; v[u] = k < k1 ? key[k] : LK_NONE; }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (v[u] == LK_NONE) continue;
+        const unsigned long long kk = v[u] & ~LK_WARM;
+        ++ca; mna = min(mna, kk); mxa = max(mxa, kk);
+        if (v[u] & LK_WARM) { ++cw; mnw = min(mnw, kk); mxw = max(mxw, kk); }
+      }
+    }
+    cw = warp_sum_u32(cw); ca = warp_sum_u32(ca);
+    mnw = warp_min_u64(mnw); mxw = warp_max_u64(mxw); mna = warp_min_u64(mna); mxa = warp_max_u64(mxa);
+    if (lane == 0) {
+      atomicAdd(&s_nw, cw); atomicAdd(&s_na, ca);
+      atomicMin(&s_min[0], mnw); atomicMax(&s_max[0], mxw); atomicMin(&s_min[1], mna); atomicMax(&s_max[1], mxa);
+    }
+  }
+  __syncthreads();
+  const uint32_t nw = s_nw;
+  const bool use_warm = nw >= a.min_samples;
+  const uint32_t nu = use_warm ? nw : s_na;
+  if (tid == 0) {
     a.lk_n[o] = nu; a.lk_used[o] = use_warm ? 1 : 0;
     a.lk_elig[o] = nu >= a.min_samples ? 1 : 0;
-    a.lk_medp[o] = 0; a.lk_medt[o] = 0; a.lk_bw[o] = 0.0;
   }
   if (nu == 0) return;
-  // sample i of the chosen group, i < nu: the warm-up samples, then (all samples) the others
-  auto at = [&](uint32_t i) -> uint32_t { return i < nw ? i : cap - nn + (i - nw); };
+  // the chosen group's key of instance k, or ~0 (above every key) when k is not in it
+  auto gkey = [&](unsigned long long v) -> unsigned long long {
+    return (v == LK_NONE || (use_warm && !(v & LK_WARM))) ? ~0ull : (v & ~LK_WARM);
+  };
   // (2) lower-median rank over the key range [lo, hi]
-  if (tid == 0) {
-    s_lo = use_warm ? s_min[0] : min(s_min[0], s_min[1]);
-    s_hi = use_warm ? s_max[0] : max(s_max[0], s_max[1]);
-    s_target = (nu - 1) / 2;
-  }
+  if (tid == 0) { s_lo = s_min[use_warm ? 0 : 1]; s_hi = s_max[use_warm ? 0 : 1]; s_target = (nu - 1) / 2; }
   __syncthreads();
   for (;;) {
     const unsigned long long lo = s_lo, hi = s_hi;
@@ -581,115 +553,115 @@ __global__ void __launch_bounds__(LM_NT) k_link_median(LKArgs a) {
     const int sh = max(0, 64 - __clzll((long long)(hi - lo)) - 11);  // (hi - lo) >> sh < LM_NB
     for (uint32_t i = tid; i < LM_NB; i += LM_NT) hist[i] = 0;
     __syncthreads();
-    for (uint32_t ib = 0; ib < nu; ib += LM_NT) {  // whole warps per round: lanes with one bin add once
-      const uint32_t i = ib + tid;
-      uint32_t bin = LM_NB;
-      if (i < nu) {
-        const unsigned long long key = sk[at(i)];
-        if (key >= lo && key <= hi) bin = (uint32_t)((key - lo) >> sh);
-      }
-      hist_add(hist, bin, LM_NB);
+    for (uint32_t kb = k0; kb < k1; kb += 4 * LM_NT) {  // whole warps per round: lanes with one bin add once
+      unsigned long long v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { const uint32_t k = kb + u * LM_NT + tid; v[u] = k < k1 ? gkey(key[k]) : ~0ull; }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        hist_add(hist, (v[u] >= lo && v[u] <= hi) ? (uint32_t)((v[u] - lo) >> sh) : LM_NB);
     }
     __syncthreads();
     if (wid == 0) {
       uint32_t bin, below;
       hist_find_nb(hist, tgt, bin, below);
-      if (lane == 0) {
+      if (lane == 0 && bin == LM_NB) { s_lo = s_hi = lo; s_cnt = 0; s_nc = 0; s_bad = 1; }
+      else if (lane == 0) {
         const unsigned long long nlo = lo + ((unsigned long long)bin << sh);
-        const unsigned long long nhi = sh >= 64 ? hi : min(hi, nlo + ((1ull << sh) - 1ull));
-        s_lo = nlo; s_hi = nhi; s_target = tgt - below; s_cnt = hist[bin]; s_nc = 0;
+        s_lo = nlo; s_hi = min(hi, nlo + ((1ull << sh) - 1ull)); s_target = tgt - below; s_cnt = hist[bin]; s_nc = 0;
       }
     }
     __syncthreads();
+    if (s_bad) break;
     if (s_lo == s_hi || s_cnt > LM_CC) continue;
     // <= LM_CC samples in [lo, hi]: gather their keys and rank them directly
-    {
-      const unsigned long long l2 = s_lo, h2 = s_hi;
-      for (uint32_t ib = 0; ib < nu; ib += LM_NT) {
-        const uint32_t i = ib + tid;
-        bool c = false;
-        unsigned long long key = 0;
-        if (i < nu) { key = sk[at(i)]; c = key >= l2 && key <= h2; }
-        const unsigned bm = __ballot_sync(0xFFFFFFFFu, c);
-        if (!bm) continue;
-        uint32_t off = 0;
-        if (lane == 0) off = atomicAdd(&s_nc, (uint32_t)__popc(bm));
-        off = __shfl_sync(0xFFFFFFFFu, off, 0);
-        if (c) cand[off + __popc(bm & ((1u << lane) - 1u))] = key;
-      }
-      __syncthreads();
-      const uint32_t nc = s_nc, t2 = s_target;
-      for (uint32_t j = tid; j < nc; j += LM_NT) {
-        const unsigned long long kj = cand[j];
-        uint32_t less = 0, eq = 0;
-        for (uint32_t q = 0; q < nc; ++q) { const unsigned long long kq = cand[q]; less += kq < kj; eq += kq == kj; }
-        if (less <= t2 && t2 < less + eq) { s_K = kj; s_tg = t2 - less; }  // equal keys write equal values
-      }
-      __syncthreads();
-      break;
+    const unsigned long long l2 = s_lo, h2 = s_hi;
+    for (uint32_t kb = k0; kb < k1; kb += LM_NT) {
+      const uint32_t k = kb + tid;
+      const unsigned long long v = k < k1 ? gkey(key[k]) : ~0ull;
+      const bool c = v >= l2 && v <= h2;
+      const unsigned bm = __ballot_sync(0xFFFFFFFFu, c);
+      if (!bm) continue;
+      uint32_t off = 0;
+      if (lane == 0) off = atomicAdd(&s_nc, (uint32_t)__popc(bm));
+      off = __shfl_sync(0xFFFFFFFFu, off, 0);
+      if (c) cand[off + __popc(bm & ((1u << lane) - 1u))] = v;
     }
+    __syncthreads();
+    const uint32_t nc = s_nc, t2 = s_target;
+#ifdef MS_DEBUG_CHECKS
+    if (tid == 0 && (nc > LM_CC || nc != s_cnt)) printf("k_link_median[%u]: %u candidates, histogram said %u\n", o, nc, s_cnt);
+#endif
+    for (uint32_t j = tid; j < nc; j += LM_NT) {
+      const unsigned long long kj = cand[j];
+      uint32_t less = 0, eq = 0;
+      for (uint32_t q = 0; q < nc; ++q) { const unsigned long long kq = cand[q]; less += kq < kj; eq += kq == kj; }
+      if (less <= t2 && t2 < less + eq) { s_K = kj; s_tg = t2 - less; }  // equal keys write equal values
+    }
+    break;
   }
   __syncthreads();
-  // (3) tie group = samples with the selected key; order inside it is (exact p/t, instance id)
+  if (s_bad) return;  // inconsistent inputs (only on a job the fused pass rejects; the call reruns)
+  // (3) tie group = the chosen group's instances with the selected key, ordered by (exact p/t, k)
   const unsigned long long K = s_K;
   const uint32_t tg = s_tg;
   if (tid == 0) { s_tie = 0; s_exact_eq = 1; s_ref = NONE32; s_pick = NONE32; }
   __syncthreads();
-  for (uint32_t i = tid; i < nu; i += LM_NT)
-    if (sk[at(i)] == K) { atomicAdd(&s_tie, 1u); atomicMin(&s_ref, i); }
+  {
+    uint32_t nt = 0, first = NONE32;
+    for (uint32_t k = k0 + tid; k < k1; k += LM_NT)
+      if (gkey(key[k]) == K) { ++nt; first = min(first, k); }
+    nt = warp_sum_u32(nt);
+    first = __reduce_min_sync(0xFFFFFFFFu, first);
+    if (lane == 0 && nt) { atomicAdd(&s_tie, nt); atomicMin(&s_ref, first); }
+  }
   __syncthreads();
-  auto P_ = [&](uint32_t i) { return a.pay[(rel0 + si[at(i)]) * a.pay_stride]; };
-  auto T_ = [&](uint32_t i) { return a.rec[b + si[at(i)]].x; };
-  auto I_ = [&](uint32_t i) { return si[at(i)]; };
+  auto P_ = [&](uint32_t k) { return a.pay[(rel0 + k) * a.pay_stride]; };
+  auto T_ = [&](uint32_t k) { return a.rec[b + k].x; };
+#ifdef MS_DEBUG_CHECKS
+  if (tid == 0 && (s_tie == 0 || s_ref >= k1)) printf("k_link_median[%u]: tie %u ref %u k1 %u\n", o, s_tie, s_ref, k1);
+#endif
+  if (s_tie == 0) return;
   if (s_tie == 1) {
     if (tid == 0) s_pick = s_ref;
   } else {
     const uint32_t ref = s_ref;
     const uint32_t pr = P_(ref), tr = T_(ref);
-    for (uint32_t i = tid; i < nu; i += LM_NT)
-      if (sk[at(i)] == K && (unsigned long long)P_(i) * tr != (unsigned long long)pr * T_(i)) s_exact_eq = 0;
+    for (uint32_t k = k0 + tid; k < k1; k += LM_NT)
+      if (gkey(key[k]) == K && (unsigned long long)P_(k) * tr != (unsigned long long)pr * T_(k)) s_exact_eq = 0;
     __syncthreads();
     if (s_exact_eq) {
-      // one exact ratio: the tg-th smallest instance id of the tie group (radix select on ids)
-      uint32_t tgt = tg, pre = 0;
-      for (int shift = 24; shift >= 0; shift -= 8) {
-        if (tid < 256) hist[tid] = 0;
-        __syncthreads();
-        const uint32_t hmask = shift == 24 ? 0u : (0xFFFFFFFFu << (shift + 8));
-        for (uint32_t ib = 0; ib < nu; ib += LM_NT) {
-          const uint32_t i = ib + tid;
-          uint32_t bin = 256u;
-          if (i < nu && sk[at(i)] == K && (I_(i) & hmask) == pre) bin = (I_(i) >> shift) & 0xFFu;
-          hist_add(hist, bin);
-        }
-        __syncthreads();
-        if (tid < 32) {
-          uint32_t bin, below;
-          hist_find(hist, tgt, bin, below);
-          if (tid == 0) { s_target = tgt - below; s_prefix = pre | (bin << shift); }
-        }
-        __syncthreads();
-        tgt = s_target; pre = (uint32_t)s_prefix;
+      // one exact ratio: the tg-th tie member in occurrence order (each thread a contiguous chunk of k)
+      const uint32_t chunk = (k1 - k0 + LM_NT - 1) / LM_NT;
+      const uint32_t c0 = k0 + tid * chunk, c1 = min(k1, c0 + chunk);
+      uint32_t cnt = 0;
+      for (uint32_t k = c0; k < c1; ++k) cnt += gkey(key[k]) == K;
+      uint32_t tot;
+      const uint32_t ex = block_excl_sum<LM_NT>(cnt, tot, scan_sm);
+      if (ex <= tg && tg < ex + cnt) {
+        uint32_t r = tg - ex;
+        for (uint32_t k = c0; k < c1; ++k)
+          if (gkey(key[k]) == K) { if (r == 0) { s_pick = k; break; } --r; }
       }
-      for (uint32_t i = tid; i < nu; i += LM_NT)
-        if (sk[at(i)] == K && I_(i) == pre) s_pick = i;
     } else {
       // distinct exact ratios behind one f64 value (rare): rank the tie group exactly
-      for (uint32_t i = tid; i < nu; i += LM_NT) {
-        if (sk[at(i)] != K) continue;
-        const uint32_t pi = P_(i), ti = T_(i);
+      for (uint32_t k = k0 + tid; k < k1; k += LM_NT) {
+        if (gkey(key[k]) != K) continue;
+        const uint32_t pi = P_(k), ti = T_(k);
         uint32_t rk = 0;
-        for (uint32_t j2 = 0; j2 < nu; ++j2)
-          if (j2 != i && sk[at(j2)] == K && samp_less(P_(j2), T_(j2), I_(j2), pi, ti, I_(i))) ++rk;
-        if (rk == tg) s_pick = i;
+        for (uint32_t j2 = k0; j2 < k1; ++j2)
+          if (j2 != k && gkey(key[j2]) == K && samp_less(P_(j2), T_(j2), j2, pi, ti, k)) ++rk;
+        if (rk == tg) s_pick = k;
       }
     }
   }
   __syncthreads();
   if (tid == 0 && s_pick != NONE32) {
     const uint32_t pm = P_(s_pick), tm = T_(s_pick);
-    a.lk_medp[o] = pm; a.lk_medt[o] = tm;
-    a.lk_bw[o] = (double)pm / (double)tm;
+    if (tm != 0) {  // always, unless the keys and records disagree (a job the fused pass rejects)
+      a.lk_medp[o] = pm; a.lk_medt[o] = tm;
+      a.lk_bw[o] = (double)pm / (double)tm;
+    }
   }
 }
 
@@ -699,6 +671,7 @@ __global__ void __launch_bounds__(LK_NT) k_link_flags(uint32_t n_p2p, int W, con
                                                       uint8_t* lk_slow, uint8_t* wl_link_slow, uint32_t bw_num, uint32_t bw_den,
                                                       Counters* cnt) {
   extern __shared__ uint32_t smem[];
+  if (*((volatile const unsigned*)&cnt->overflow) & NOT_SPMD) return;  // rejected by the fused pass (rerun follows)
   uint32_t* sp = smem;
   uint32_t* st = smem + LINK_CAP;
   uint32_t* si = smem + 2 * LINK_CAP;
@@ -738,32 +711,27 @@ __global__ void __launch_bounds__(LK_NT) k_link_flags(uint32_t n_p2p, int W, con
 // Per-(window, link) medians. Sharded contexts read the job-wide channel tables: the instances of
 // an owned link are all present after the shard exchange (shard.cu).
 static void link_median_go(Ctx& c, LKArgs& a) {
-  const size_t smm = (size_t)LM_CAP * 12;
-  cudaFuncSetAttribute(k_link_median, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smm);
-  k_link_median<<<(unsigned)(c.NW * c.n_p2p), LM_NT, smm, c.stream>>>(a);
+  k_link_median<<<(unsigned)(c.NW * c.n_p2p), LM_NT, 0, c.stream>>>(a);
 }
 
-static LKArgs link_args(Ctx& c, uint64_t np_inst) {
+static LKArgs link_args(Ctx& c) {
   LKArgs a{};
   a.n_comms = c.n_comms; a.n_p2p = (uint32_t)c.n_p2p; a.NW = c.NW; a.wi = c.dcfg.window_iters; a.W = c.W; a.TP = c.TP; a.DP = c.DP;
   a.psrc = c.ch_nsend.as<uint32_t>() + c.n_p2p; a.pdst = c.ch_nrecv.as<uint32_t>() + c.n_p2p;
   a.min_samples = c.lcfg.min_samples; a.lk_n = c.lk_n.as<uint32_t>(); a.lk_used = c.lk_used.as<uint8_t>();
   a.lk_medp = c.lk_medp.as<uint32_t>(); a.lk_medt = c.lk_medt.as<uint32_t>(); a.lk_bw = c.lk_bw.as<double>();
   a.lk_dir = c.lk_dir.as<uint8_t>(); a.lk_elig = c.lk_elig.as<uint8_t>(); a.cnt = c.counters.as<Counters>();
-  a.gkey = c.lk_scratch.as<unsigned long long>(); a.gid = (uint32_t*)(c.lk_scratch.as<unsigned long long>() + np_inst);
   a.n_shards = 1; a.shard = 0;
   return a;
 }
 
 int launch_link_median(Ctx& c) {
   if (c.n_p2p == 0) return 0;
-  const uint64_t np_inst = std::max<uint64_t>(c.n_inst - c.p2p_inst0, 1);
-  if (c.lk_scratch.ensure(np_inst * 12) != cudaSuccess) return 0;
   const bool sh = c.n_shards > 1;
-  LKArgs a = link_args(c, np_inst);
+  LKArgs a = link_args(c);
   a.ch_base = (sh ? c.g_base : c.ch_base).as<uint64_t>(); a.ch_nmax = (sh ? c.g_nmax : c.ch_nmax).as<uint32_t>();
   a.ch_nmin = (sh ? c.g_nmin : c.ch_nmin).as<uint32_t>();
-  a.rec = c.inst_rec.as<uint4>();
+  a.rec = c.inst_rec.as<uint4>(); a.key = c.lk_key.as<unsigned long long>();
   // the send slot of P2P instance i is slot p2p_slot0 + 2 (i - p2p_inst0): payload in w, iteration in z
   const uint32_t* sw = reinterpret_cast<const uint32_t*>(c.slots.as<uint4>() + c.p2p_slot0);
   a.pay = sw + 3; a.iter = sw + 2; a.pay_stride = 8; a.iter_stride = 8; a.it_mask = SLOT_IT_MASK;
@@ -773,16 +741,14 @@ int launch_link_median(Ctx& c) {
 }
 
 // Per-link medians over a caller-provided instance layout (streaming: the window's samples in
-// link-major, age-minor order; base / nmax / slot indexed by channel id n_comms + pid; instance i's
-// payload at pay[2 i], its iteration at iter[i])
+// link-major, age-minor order; base / nmax indexed by channel id n_comms + pid; instance i's payload
+// at pay[2 i], its iteration at iter[i], its sample key at key[i])
 int launch_link_median_window(Ctx& c, const uint64_t* base, const uint32_t* nmax, const uint64_t* slot, const uint4* rec,
-                              const uint32_t* iter, const uint32_t* pay, uint64_t n_inst) {
-  (void)slot;
+                              const uint32_t* iter, const uint32_t* pay, const unsigned long long* key, uint64_t n_inst) {
+  (void)slot; (void)n_inst;
   if (c.n_p2p == 0) return 0;
-  const uint64_t np_inst = std::max<uint64_t>(n_inst, 1);
-  if (c.lk_scratch.ensure(np_inst * 12) != cudaSuccess) return 0;
-  LKArgs a = link_args(c, np_inst);
-  a.ch_base = base; a.ch_nmax = nmax; a.ch_nmin = nullptr; a.rec = rec;
+  LKArgs a = link_args(c);
+  a.ch_base = base; a.ch_nmax = nmax; a.ch_nmin = nullptr; a.rec = rec; a.key = key;
   a.pay = pay; a.iter = iter; a.pay_stride = 2; a.iter_stride = 1; a.it_mask = 0xFFFFFFFFu; a.p2p_inst0 = 0;
   link_median_go(c, a);
   return 1;
@@ -823,6 +789,7 @@ struct WKArgs {
 
 __global__ void k_walk(WKArgs a) {
   cg::grid_group grid = cg::this_grid();
+  if (*((volatile const unsigned*)&a.cnt->overflow) & NOT_SPMD) return;  // every block: rejected job, rerun follows
   const uint64_t items = (uint64_t)a.NW * a.W;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;

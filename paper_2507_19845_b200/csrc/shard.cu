@@ -54,7 +54,8 @@ __global__ void k_link_pack(const LinkMap* map, const uint4* rec, const uint4* s
     const uint4 r = rec[i];
     uint32_t* o = buf + (m.flat + k) * LREC;
     uint4 sl = make_uint4(0, 0, 0, 0);
-    if (r.w & SCAN_F_VALID) sl = slots[p2p_slot0 + 2 * (i - p2p_inst0)];  // the median reads valid samples only
+    if (r.w & SCAN_F_COMPLETE) sl = slots[p2p_slot0 + 2 * (i - p2p_inst0)];  // both slots written: the window
+                                                                              // search reads complete instances
     o[0] = r.x;
     o[1] = sl.w;
     o[2] = ((sl.z & SLOT_IT_MASK) << 8) | (r.w & 0xFFu);
@@ -63,8 +64,8 @@ __global__ void k_link_pack(const LinkMap* map, const uint4* rec, const uint4* s
 
 // rows of links this shard owns; only the fields the median reads are written (the rest of an
 // unowned-range row stays unspecified, scan.h)
-__global__ void k_link_unpack(const LinkMap* map, const uint32_t* buf, uint4* rec, uint4* slots, uint64_t p2p_inst0,
-                              uint64_t p2p_slot0) {
+__global__ void k_link_unpack(const LinkMap* map, const uint32_t* buf, uint4* rec, uint4* slots, unsigned long long* lk_key,
+                              uint64_t p2p_inst0, uint64_t p2p_slot0) {
   const LinkMap m = map[blockIdx.x];
   for (uint32_t k = threadIdx.x; k < m.n; k += blockDim.x) {
     const uint64_t i = m.inst0 + k;
@@ -74,6 +75,7 @@ __global__ void k_link_unpack(const LinkMap* map, const uint32_t* buf, uint4* re
     uint32_t* sw = reinterpret_cast<uint32_t*>(slots + p2p_slot0 + 2 * (i - p2p_inst0));
     sw[2] = v[2] >> 8;  // iteration (the warm-up flag travels in the record's flags)
     sw[3] = v[1];
+    lk_key[i - p2p_inst0] = lk_sample_key(v[2] & 0xFFu, v[0], v[1]);
   }
 }
 
@@ -602,7 +604,7 @@ scan_status sharded_all(Ctx& c) {
     if (!rmap.empty()) {
       k_link_unpack<<<(unsigned)rmap.size(), 256, 0, c.stream>>>(c.lk_recvmap.as<LinkMap>(), c.x_recv.as<uint32_t>(),
                                                                 c.inst_rec.as<uint4>(), c.slots.as<uint4>(),
-                                                                c.p2p_inst0, c.p2p_slot0);
+                                                                c.lk_key.as<unsigned long long>(), c.p2p_inst0, c.p2p_slot0);
       c.launches += 1;
     }
   }

@@ -38,7 +38,7 @@ struct StreamState {
   std::vector<uint32_t> nl, loff;  // per link: instances per iteration, offset in an iteration block
   std::vector<std::array<uint64_t, 4>> cnt;  // per slot: incomplete, kind / payload mismatch, instances
   DevBuf rg_w32, rg_ew, rg_rk, rg_ht, rg_smp, d_nl, d_loff, d_slots, ht_age;
-  DevBuf w_base, w_slot, w_nmax, w_rec, w_pay, w_iter;
+  DevBuf w_base, w_slot, w_nmax, w_rec, w_pay, w_iter, w_key;
 };
 
 namespace {
@@ -92,7 +92,7 @@ __global__ void k_stream_ht(uint32_t Kv, const uint32_t* slots, uint64_t W, cons
 
 // window samples of link l, age a, occurrence k at Kv * loff[l] + a * nl[l] + k
 __global__ void k_stream_window(uint32_t Kv, const uint32_t* slots, uint64_t npi, const uint32_t* nl, const uint32_t* loff,
-                                const uint32_t* rg_smp, uint4* w_rec, uint32_t* w_pay) {
+                                const uint32_t* rg_smp, uint4* w_rec, uint32_t* w_pay, unsigned long long* w_key) {
   const uint32_t l = blockIdx.x, a = blockIdx.y;
   const uint64_t src0 = (uint64_t)slots[a] * npi + loff[l], dst0 = (uint64_t)Kv * loff[l] + (uint64_t)a * nl[l];
   for (uint32_t k = threadIdx.x; k < nl[l]; k += blockDim.x) {
@@ -100,6 +100,7 @@ __global__ void k_stream_window(uint32_t Kv, const uint32_t* slots, uint64_t npi
     w_rec[dst0 + k] = make_uint4(v[0], 0u, 0u, v[2]);
     w_pay[2 * (dst0 + k)] = v[1];
     w_pay[2 * (dst0 + k) + 1] = 0u;
+    w_key[dst0 + k] = lk_sample_key(v[2], v[0], v[1]);
   }
 }
 
@@ -137,7 +138,7 @@ scan_status establish(Ctx& c, StreamState& S, Ctx& u) {
   CK(S.d_slots.ensure(K * 4));
   CK(S.w_base.ensure((c.NCH + 1) * 8)); CK(S.w_slot.ensure((c.NCH + 1) * 8)); CK(S.w_nmax.ensure((c.NCH + 1) * 4));
   CK(S.w_rec.ensure(std::max<uint64_t>(K * S.npi * 16, 16))); CK(S.w_pay.ensure(std::max<uint64_t>(K * S.npi * 8, 16)));
-  CK(S.w_iter.ensure(std::max<uint64_t>(K * S.npi * 4, 16)));
+  CK(S.w_iter.ensure(std::max<uint64_t>(K * S.npi * 4, 16))); CK(S.w_key.ensure(std::max<uint64_t>(K * S.npi * 8, 16)));
   CK(cudaMemsetAsync(S.w_iter.p, 0, std::max<uint64_t>(K * S.npi * 4, 16), c.stream));
   S.cnt.assign(K, {0, 0, 0, 0});
   if ((st = alloc_detect(c)) || (st = alloc_localize(c))) return st;
@@ -153,7 +154,7 @@ void stream_release(Ctx& c) {
   if (!S) return;
   if (S->sub) scan_destroy(S->sub);
   for (DevBuf* b : {&S->rg_w32, &S->rg_ew, &S->rg_rk, &S->rg_ht, &S->rg_smp, &S->d_nl, &S->d_loff, &S->d_slots, &S->ht_age,
-                    &S->w_base, &S->w_slot, &S->w_nmax, &S->w_rec, &S->w_pay, &S->w_iter})
+                    &S->w_base, &S->w_slot, &S->w_nmax, &S->w_rec, &S->w_pay, &S->w_iter, &S->w_key})
     b->release();
   delete S;
   c.stream_state = nullptr;
@@ -289,7 +290,7 @@ scan_status scan_stream_push(scan_ctx* ctx, const scan_event_columns* iteration,
     if ((st = upload(c, S.w_base, wb)) || (st = upload(c, S.w_slot, ws)) || (st = upload(c, S.w_nmax, wn))) return st;
     k_stream_window<<<dim3(S.np, Kv), 128, 0, c.stream>>>(Kv, S.d_slots.as<uint32_t>(), S.npi, S.d_nl.as<uint32_t>(),
                                                          S.d_loff.as<uint32_t>(), S.rg_smp.as<uint32_t>(), S.w_rec.as<uint4>(),
-                                                         S.w_pay.as<uint32_t>());
+                                                         S.w_pay.as<uint32_t>(), S.w_key.as<unsigned long long>());
     c.launches += 1;
   }
   // 4. candidates, links, verdicts and the walk on the window
@@ -304,7 +305,8 @@ scan_status scan_stream_push(scan_ctx* ctx, const scan_event_columns* iteration,
   c.launches += timed(c, "k_wd_finish", [&] { return launch_wd_finish(c); });
   c.launches += timed(c, "k_link_median", [&] {
     return launch_link_median_window(c, S.w_base.as<uint64_t>(), S.w_nmax.as<uint32_t>(), S.w_slot.as<uint64_t>(),
-                                     S.w_rec.as<uint4>(), S.w_iter.as<uint32_t>(), S.w_pay.as<uint32_t>(), (uint64_t)Kv * S.npi);
+                                     S.w_rec.as<uint4>(), S.w_iter.as<uint32_t>(), S.w_pay.as<uint32_t>(),
+                                     S.w_key.as<unsigned long long>(), (uint64_t)Kv * S.npi);
   });
   c.launches += timed(c, "k_link_flags", [&] { return launch_link_flags(c); });
   c.launches += timed(c, "k_walk", [&] { return launch_verdict_walk(c); });
