@@ -84,6 +84,12 @@ scan_status scan_create(scan_ctx** out, int cuda_device, void* cuda_stream) {
   if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return SCAN_E_CUDA;
   if (cuda_device < 0 || cuda_device >= n) return SCAN_E_INVALID_ARG;
   if (cudaSetDevice(cuda_device) != cudaSuccess) return SCAN_E_CUDA;
+  if (const char* e = std::getenv("MS_L2_FETCH")) {  // experiment: L2 fetch granularity hint (bytes)
+    const cudaError_t le = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)std::atoi(e));
+    size_t v = 0;
+    cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity);
+    std::fprintf(stderr, "[MS_L2_FETCH] set %s: %s, now %zu\n", e, cudaGetErrorString(le), v);
+  }
   scan_ctx* s = new scan_ctx();
   s->c.device = cuda_device;
   s->c.stream = (cudaStream_t)cuda_stream;

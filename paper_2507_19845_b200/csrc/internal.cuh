@@ -27,8 +27,7 @@ constexpr uint32_t NOT_SPMD = 32u;  // Counters.overflow bit: fused path not app
 // Member slot record (uint4), one per member slot of every instance, in slot order
 // (slot = slot_base(channel) + k * |members| + member; a P2P instance i has its send slot at
 // p2p_slot0 + 2 (i - p2p_inst0) and its receive slot right after it):
-//   x  the member event's duration; after the instance reduction (k_inst_reduce / k_cross_reduce)
-//      the member's wait
+//   x  the member event's duration (its wait is x - the instance's dmin, computed where it is needed)
 //   y  fused path: the member event's index among its rank's comm events (k_xwait_scatter)
 //   z  global iteration (bits 0-27) | kind (bits 28-30) | sender's warm-up flag (bit 31, P2P send slot)
 //   w  P2P slots: payload bytes (k_stage leaves the event's position in its rank there and

@@ -297,7 +297,7 @@ struct FusedArgs {
   uint32_t slow_num, slow_den; unsigned long long slow_margin;
   uint32_t wi, classes, mode; unsigned long long late_margin, wait_margin; int want_ref;
   uint32_t it_off;  // global iteration of this shard's first iteration (0 unsharded)
-  uint32_t pf_dist, pf_own; uint64_t n_events;  // k_fused_t: L2 prefetch of tile + pf_dist (0 = off), of its own tile; column length
+  uint32_t pf_dist, pf_own, pf_p2p; uint64_t n_events;  // k_fused_t: L2 prefetch of tile + pf_dist (0 = off), of its own tile, of its P2P payload / meta words; column length
   unsigned long long wi_m;  // ceil(2^64 / wi) for wi > 1: window = umulhi64(iteration, wi_m), exact for 32-bit iterations
   Counters* cnt;
   // byte offsets of the transposed kernel's shared-memory arrays (host-computed, fused_t_layout)
@@ -967,6 +967,20 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
     }
   }
   __syncthreads();
+  // L2 prefetch of the payload (and the sender's meta) word of every P2P event of the tile: the phase-B
+  // cross units gather them; requested here, the DRAM fetches overlap the load pass below
+  if (a.pf_p2p) {
+    const uint32_t nx = nlist[3];
+    for (uint32_t i = tid; i < nx * R; i += FT_NT) {
+      const uint32_t xi = fdiv(i, a.fR), row = i - xi * R;
+      const uint32_t p = lst[3 * T + xi];
+      const uint32_t role = (pb[p] >> 20) & 31u;
+      if (role < 16) continue;
+      const uint64_t e = rbase + (uint64_t)row * npos + p0 + p;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.pay + e));
+      if ((role >> 3) & 1u) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.meta + e));
+    }
+  }
   // ---- (1) load every rank row of the tile: warps over rows, lanes along positions (fully coalesced),
   // two rows in flight per warp; verify kind_op / comm against the template, transpose into sd[p][row]
   {
@@ -1123,8 +1137,13 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
           }
           inst = (uint64_t)rb + kk;
           si = a.p2p_slot0 + 2 * (inst - a.p2p_inst0) + (send ? 0 : 1);
-          pay = a.pay[e];
-          if (send) warm = ((uint32_t)a.meta[e] >> 14) & 1u;
+#if defined(MS_EXP_SKIP) && (MS_EXP_SKIP & 1024)
+          if (R == 0)  // timing experiment only (results invalid)
+#endif
+          {
+            pay = a.pay[e];
+            if (send) warm = ((uint32_t)a.meta[e] >> 14) & 1u;
+          }
         }
 #if defined(MS_EXP_SKIP) && (MS_EXP_SKIP & 256)
         if (R == 0)  // timing experiment only (results invalid)
@@ -1467,6 +1486,9 @@ int launch_fused(Ctx& c) {
     }
     static int own = -1;
     if (own < 0) { const char* e = std::getenv("MS_FT_PF_OWN"); own = e ? std::atoi(e) : 1; }
+    static int pp = -1;
+    if (pp < 0) { const char* e = std::getenv("MS_FT_PF_P2P"); pp = e ? std::atoi(e) : 0; }
+    a.pf_p2p = (uint32_t)pp;
     a.pf_dist = (uint32_t)pf;
     a.pf_own = (uint32_t)own;
     a.n_events = c.N;
@@ -1543,9 +1565,7 @@ struct XArgs {
   int p2p_pos; const uint32_t* pay; const uint16_t* meta; const uint64_t* rank_off;
 };
 
-__device__ __forceinline__ void slot_set_wait(uint4* slots, uint64_t si, uint32_t wait) {
-  reinterpret_cast<uint32_t*>(slots + si)[0] = wait;
-}
+
 
 constexpr uint32_t XBIG = 32;  // cross collectives with more members go to k_cross_big
 
@@ -1694,16 +1714,12 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
         unsigned long long w = 0, t = 0;
         bool eg = false;
         uint32_t ewin = 0, ewait = 0;
-        if (act && (flags & SCAN_F_COMPLETE || present(q))) {
-          if (!valid) slot_set_wait(a.slots, sb + q, 0);
-          else {
-            const uint32_t m = member(q);
-            const uint32_t wait = sdur(q) - dmin;
-            slot_set_wait(a.slots, sb + q, wait);
-            w = wait; t = dmin;
-            if (m != last && (unsigned long long)wait > a.wait_margin) {
-              eg = true; ewait = wait; ewin = a.wi ? sit(q) / a.wi : 0;
-            }
+        if (act && valid) {  // (a member's wait, duration - dmin, is recomputed where it is exported: k_xwait_scatter)
+          const uint32_t m = member(q);
+          const uint32_t wait = sdur(q) - dmin;
+          w = wait; t = dmin;
+          if (m != last && (unsigned long long)wait > a.wait_margin) {
+            eg = true; ewait = wait; ewin = a.wi ? sit(q) / a.wi : 0;
           }
         }
         const unsigned em = __ballot_sync(0xFFFFFFFFu, eg);
@@ -1731,11 +1747,9 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
       }
     } else if (act) {
       for (uint32_t q = 0; q < nm; ++q) {
-        if (!(flags & SCAN_F_COMPLETE) && !present(q)) continue;
-        if (!valid) { slot_set_wait(a.slots, sb + q, 0); continue; }
+        if (!valid) continue;
         const uint32_t m = member(q);
         const uint32_t wait = sdur(q) - dmin;
-        slot_set_wait(a.slots, sb + q, wait);
         if (wait) atomicAdd(&a.rk_sum[a.W + m], (unsigned long long)wait);
         if (dmin) atomicAdd(&a.rk_sum[2 * a.W + m], (unsigned long long)dmin);
         if (m != last && (unsigned long long)wait > a.wait_margin) x_edge(a, m, last, a.wi ? sit(q) / a.wi : 0, wait);
@@ -1819,8 +1833,6 @@ __global__ void __launch_bounds__(256) k_cross_big(XArgs a, const uint32_t* big,
       kok = __all_sync(0xFFFFFFFFu, kok);
       if (kok) flags |= SCAN_F_KIND_OK; else ++kmis;
       flags |= SCAN_F_PAYLOAD_OK;  // collectives carry no payload check
-      if (!kok)
-        for (uint32_t q = lane; q < nm; q += 32) slot_set_wait(a.slots, sb + q, 0);  // invalid instance: members wait 0
       if (kok) {
         valid = true;
         flags |= SCAN_F_VALID;
@@ -1844,7 +1856,6 @@ __global__ void __launch_bounds__(256) k_cross_big(XArgs a, const uint32_t* big,
           const uint32_t m = mem[q];
           const uint4 sq = a.slots[sb + q];
           const uint32_t wait = sq.x - dmin;
-          slot_set_wait(a.slots, sb + q, wait);
           if (wait) atomicAdd(&a.rk_sum[a.W + m], (unsigned long long)wait);
           if (dmin) atomicAdd(&a.rk_sum[2 * a.W + m], (unsigned long long)dmin);
           if (m != last && (unsigned long long)wait > a.wait_margin) {
@@ -1855,13 +1866,7 @@ __global__ void __launch_bounds__(256) k_cross_big(XArgs a, const uint32_t* big,
         }
       }
     } else {
-      ++inc;
-      for (uint32_t q = lane; q < nm; q += 32) {  // present members of an incomplete instance: wait 0
-        const uint32_t m = mem[q];
-        const uint32_t C = a.r_nkeys[m];
-        const uint32_t p = lower_bound_u32(a.r_keys + (uint64_t)m * RCAP, C, ch);
-        if (p < C && a.r_keys[(uint64_t)m * RCAP + p] == ch && a.r_cnt[(uint64_t)m * RCAP + p] > k) slot_set_wait(a.slots, sb + q, 0);
-      }
+      ++inc;  // present members of an incomplete instance wait 0 (k_xwait_scatter)
     }
     if (lane == 0) a.rec[i] = make_uint4(dmin, dmax, last, flags | ((uint32_t)a.ccls[ch] << 8));
     (void)valid;
@@ -1872,9 +1877,9 @@ __global__ void __launch_bounds__(256) k_cross_big(XArgs a, const uint32_t* big,
   }
 }
 
-// Comm-order view of the cross-stage members' waits (COMM_WAIT / EV_WAIT exports): k_cross_reduce
-// leaves each member's wait in its slot (instance order, coalesced); this scatters them to
-// wait_c[comm index] once, on the first export that needs them. A sparse update of the comm-order
+// Comm-order view of the cross-stage members' waits (COMM_WAIT / EV_WAIT exports): a member's wait is
+// its slot's duration minus the instance's dmin (record), scattered to wait_c[comm index of the slot]
+// once, on the first export that needs them. A sparse update of the comm-order
 // array costs a sector read + write per member, which the analysis itself does not pay.
 __global__ void __launch_bounds__(256) k_xwait_scatter(XArgs a) {
   for (uint64_t xi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; xi < a.n_xinst; xi += (uint64_t)gridDim.x * blockDim.x) {
@@ -1884,6 +1889,7 @@ __global__ void __launch_bounds__(256) k_xwait_scatter(XArgs a) {
     const uint32_t nm = isp ? 2u : (uint32_t)(a.coff[ch + 1] - a.coff[ch]);
     const uint64_t sb = a.ch_slot[ch] + k * nm;
     const bool complete = k < a.ch_nmin[ch];
+    const uint4 rc = a.rec[a.ch_base[ch] + k];
     for (uint32_t q = 0; q < nm; ++q) {
       bool present = complete;
       if (!present) {
@@ -1896,9 +1902,9 @@ __global__ void __launch_bounds__(256) k_xwait_scatter(XArgs a) {
           present = p < C && a.r_keys[(uint64_t)m * RCAP + p] == (uint32_t)ch && a.r_cnt[(uint64_t)m * RCAP + p] > k;
         }
       }
-      if (present) {
+      if (present) {  // wait = duration - dmin of a valid instance, else 0
         const uint4 sq = a.slots[sb + q];
-        a.wait_c[sq.y] = sq.x;
+        a.wait_c[sq.y] = (rc.w & SCAN_F_VALID) ? sq.x - rc.x : 0u;
       }
     }
   }
