@@ -1487,7 +1487,7 @@ int launch_fused(Ctx& c) {
     static int own = -1;
     if (own < 0) { const char* e = std::getenv("MS_FT_PF_OWN"); own = e ? std::atoi(e) : 1; }
     static int pp = -1;
-    if (pp < 0) { const char* e = std::getenv("MS_FT_PF_P2P"); pp = e ? std::atoi(e) : 0; }
+    if (pp < 0) { const char* e = std::getenv("MS_FT_PF_P2P"); pp = e ? std::atoi(e) : 1; }
     a.pf_p2p = (uint32_t)pp;
     a.pf_dist = (uint32_t)pf;
     a.pf_own = (uint32_t)own;

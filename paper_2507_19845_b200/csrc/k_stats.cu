@@ -413,7 +413,8 @@ struct LKArgs {
   uint32_t n_shards, shard;  // sharded: this shard computes the links with pid % n_shards == shard
 };
 
-constexpr int LM_NT = 128;         // 4 warps, up to 16 CTAs per SM: every (window, link) of C3 in one wave
+constexpr int LM_NT = 256;         // 8 warps, up to 8 CTAs per SM
+constexpr int LM_U = 8;            // keys in flight per thread
 constexpr uint32_t LM_NB = 2048;   // bins of one selection pass over a key range
 constexpr uint32_t LM_CC = 512;    // candidates ranked directly
 
@@ -464,7 +465,7 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
 // (warm-up if >= min_samples, reading R13): histogram passes of LM_NB bins over the shrinking key
 // range until the target bin holds <= LM_CC samples, which are ranked directly. (3) Ties on the f64
 // key: the exact order (p/t, instance index) of reading R13.
-__global__ void __launch_bounds__(LM_NT) k_link_median(LKArgs a) {
+__global__ void __launch_bounds__(LM_NT, 4) k_link_median(LKArgs a) {
   // a job the fused pass rejected (the general path reruns it): its inputs are not instance records
   if (*((volatile const unsigned*)&a.cnt->overflow) & NOT_SPMD) return;
   __shared__ __align__(16) uint32_t hist[LM_NB];
@@ -511,12 +512,12 @@ __global__ void __launch_bounds__(LM_NT) k_link_median(LKArgs a) {
   {
     unsigned long long mnw = ~0ull, mxw = 0, mna = ~0ull, mxa = 0;
     uint32_t cw = 0, ca = 0;
-    for (uint32_t kb = k0 + tid; kb < k1; kb += 4 * LM_NT) {
-      unsigned long long v[4];
+    for (uint32_t kb = k0 + tid; kb < k1; kb += LM_U * LM_NT) {
+      unsigned long long v[LM_U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) { const uint32_t k = kb + u * LM_NT; v[u] = k < k1 ? key[k] : LK_NONE; }
+      for (int u = 0; u < LM_U; ++u) { const uint32_t k = kb + u * LM_NT; v[u] = k < k1 ? key[k] : LK_NONE; }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < LM_U; ++u) {
         if (v[u] == LK_NONE) continue;
         const unsigned long long kk = v[u] & ~LK_WARM;
         ++ca; mna = min(mna, kk); mxa = max(mxa, kk);
@@ -553,12 +554,12 @@ __global__ void __launch_bounds__(LM_NT) k_link_median(LKArgs a) {
     const int sh = max(0, 64 - __clzll((long long)(hi - lo)) - 11);  // (hi - lo) >> sh < LM_NB
     for (uint32_t i = tid; i < LM_NB; i += LM_NT) hist[i] = 0;
     __syncthreads();
-    for (uint32_t kb = k0; kb < k1; kb += 4 * LM_NT) {  // whole warps per round: lanes with one bin add once
-      unsigned long long v[4];
+    for (uint32_t kb = k0; kb < k1; kb += LM_U * LM_NT) {  // whole warps per round: lanes with one bin add once
+      unsigned long long v[LM_U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) { const uint32_t k = kb + u * LM_NT + tid; v[u] = k < k1 ? gkey(key[k]) : ~0ull; }
+      for (int u = 0; u < LM_U; ++u) { const uint32_t k = kb + u * LM_NT + tid; v[u] = k < k1 ? gkey(key[k]) : ~0ull; }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < LM_U; ++u)
         hist_add(hist, (v[u] >= lo && v[u] <= hi) ? (uint32_t)((v[u] - lo) >> sh) : LM_NB);
     }
     __syncthreads();
@@ -576,16 +577,21 @@ __global__ void __launch_bounds__(LM_NT) k_link_median(LKArgs a) {
     if (s_lo == s_hi || s_cnt > LM_CC) continue;
     // <= LM_CC samples in [lo, hi]: gather their keys and rank them directly
     const unsigned long long l2 = s_lo, h2 = s_hi;
-    for (uint32_t kb = k0; kb < k1; kb += LM_NT) {
-      const uint32_t k = kb + tid;
-      const unsigned long long v = k < k1 ? gkey(key[k]) : ~0ull;
-      const bool c = v >= l2 && v <= h2;
-      const unsigned bm = __ballot_sync(0xFFFFFFFFu, c);
-      if (!bm) continue;
-      uint32_t off = 0;
-      if (lane == 0) off = atomicAdd(&s_nc, (uint32_t)__popc(bm));
-      off = __shfl_sync(0xFFFFFFFFu, off, 0);
-      if (c) cand[off + __popc(bm & ((1u << lane) - 1u))] = v;
+    for (uint32_t kb = k0; kb < k1; kb += LM_U * LM_NT) {
+      unsigned long long vv[LM_U];
+#pragma unroll
+      for (int u = 0; u < LM_U; ++u) { const uint32_t k = kb + u * LM_NT + tid; vv[u] = k < k1 ? gkey(key[k]) : ~0ull; }
+#pragma unroll
+      for (int u = 0; u < LM_U; ++u) {
+        const unsigned long long v = vv[u];
+        const bool c = v >= l2 && v <= h2;
+        const unsigned bm = __ballot_sync(0xFFFFFFFFu, c);
+        if (!bm) continue;
+        uint32_t off = 0;
+        if (lane == 0) off = atomicAdd(&s_nc, (uint32_t)__popc(bm));
+        off = __shfl_sync(0xFFFFFFFFu, off, 0);
+        if (c) cand[off + __popc(bm & ((1u << lane) - 1u))] = v;
+      }
     }
     __syncthreads();
     const uint32_t nc = s_nc, t2 = s_target;
@@ -609,8 +615,14 @@ __global__ void __launch_bounds__(LM_NT) k_link_median(LKArgs a) {
   __syncthreads();
   {
     uint32_t nt = 0, first = NONE32;
-    for (uint32_t k = k0 + tid; k < k1; k += LM_NT)
-      if (gkey(key[k]) == K) { ++nt; first = min(first, k); }
+    for (uint32_t kb = k0 + tid; kb < k1; kb += LM_U * LM_NT) {
+      unsigned long long vv[LM_U];
+#pragma unroll
+      for (int u = 0; u < LM_U; ++u) { const uint32_t k = kb + u * LM_NT; vv[u] = k < k1 ? gkey(key[k]) : ~0ull; }
+#pragma unroll
+      for (int u = 0; u < LM_U; ++u)
+        if (vv[u] == K) { ++nt; first = min(first, kb + u * LM_NT); }
+    }
     nt = warp_sum_u32(nt);
     first = __reduce_min_sync(0xFFFFFFFFu, first);
     if (lane == 0 && nt) { atomicAdd(&s_tie, nt); atomicMin(&s_ref, first); }
