@@ -1601,7 +1601,7 @@ __device__ __forceinline__ void x_edge(const XArgs& a, uint32_t r, uint32_t L, u
   atomicAdd(&a.ew[(uint64_t)win * a.nnz_tot + idx], wait);
 }
 
-__global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
+__global__ void __launch_bounds__(256, 4) k_cross_reduce(XArgs a) {
   if (*((volatile unsigned*)&a.cnt->overflow) & NOT_SPMD) return;  // fused results void: general path reruns
   extern __shared__ unsigned long long xb_s[];
   if (a.xb_smem) {
@@ -1617,34 +1617,102 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
   const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const uint64_t per = ((a.n_xinst + nwarps - 1) / nwarps + 31) & ~31ull;
   const uint64_t wend = min(a.n_xinst, (gw + 1) * per);
-  uint64_t ch0 = 0, beg0 = 1, end0 = 0;
+  // the warp's current channel, its instance range [beg0, end0) in cross order, and (P2P) its tables
+  uint64_t ch0 = 0, beg0 = 1, end0 = 0, ib0 = 0, sl0 = 0;
+  uint32_t src0 = 0, dst0 = 0, nsd0 = 0, nrc0 = 0;
+  // P2P fast path (whole warp on one link, one window): per-lane sums over the warp's steps on the
+  // cached link -- member waits, transfer, wait-for edges src -> dst / dst -> src -- flushed with one
+  // atomic each when the warp leaves the link
+  unsigned long long acc_w0 = 0, acc_w1 = 0, acc_t = 0, acc_e0 = 0, acc_e1 = 0;
+  auto flush_link = [&]() {
+    const unsigned long long w0 = warp_sum_u64(acc_w0), w1 = warp_sum_u64(acc_w1), t = warp_sum_u64(acc_t);
+    const unsigned long long e0 = warp_sum_u64(acc_e0), e1 = warp_sum_u64(acc_e1);
+    if (lane == 0 && ch0 >= a.n_comms) {
+      const uint64_t p = ch0 - a.n_comms;
+      if (w0) atomicAdd(&a.rk_sum[a.W + src0], w0);
+      if (w1) atomicAdd(&a.rk_sum[a.W + dst0], w1);
+      if (t) { atomicAdd(&a.rk_sum[2 * a.W + src0], t); atomicAdd(&a.rk_sum[2 * a.W + dst0], t); }
+      if (e0) atomicAdd(&a.ew[a.p2p_eslot[2 * p]], e0);
+      if (e1) atomicAdd(&a.ew[a.p2p_eslot[2 * p + 1]], e1);
+    }
+    acc_w0 = acc_w1 = acc_t = acc_e0 = acc_e1 = 0;
+  };
   for (uint64_t wbase = gw * per; wbase < wend; wbase += 32) {
     const uint64_t xi = wbase + lane;
     bool act = xi < wend;
     // channel of the warp's first instance; lanes past its end search alone
     if (!(wbase >= beg0 && wbase < end0)) {
-      if (lane == 0) { ch0 = upper_bound_u64(XB, a.NCH + 1, wbase) - 1; beg0 = XB[ch0]; end0 = XB[ch0 + 1]; }
-      ch0 = __shfl_sync(0xFFFFFFFFu, ch0, 0);
-      beg0 = __shfl_sync(0xFFFFFFFFu, beg0, 0);
-      end0 = __shfl_sync(0xFFFFFFFFu, end0, 0);
+      flush_link();
+      if (lane == 0) {
+        ch0 = upper_bound_u64(XB, a.NCH + 1, wbase) - 1; beg0 = XB[ch0]; end0 = XB[ch0 + 1];
+        ib0 = a.ch_base[ch0]; sl0 = a.ch_slot[ch0];
+        if (ch0 >= a.n_comms) {
+          const uint64_t p = ch0 - a.n_comms;
+          src0 = a.psrc[p]; dst0 = a.pdst[p]; nsd0 = a.nsend[p]; nrc0 = a.nrecv[p];
+        }
+      }
+      ch0 = __shfl_sync(0xFFFFFFFFu, ch0, 0); beg0 = __shfl_sync(0xFFFFFFFFu, beg0, 0); end0 = __shfl_sync(0xFFFFFFFFu, end0, 0);
+      ib0 = __shfl_sync(0xFFFFFFFFu, ib0, 0); sl0 = __shfl_sync(0xFFFFFFFFu, sl0, 0);
+      src0 = __shfl_sync(0xFFFFFFFFu, src0, 0); dst0 = __shfl_sync(0xFFFFFFFFu, dst0, 0);
+      nsd0 = __shfl_sync(0xFFFFFFFFu, nsd0, 0); nrc0 = __shfl_sync(0xFFFFFFFFu, nrc0, 0);
     }
-    uint64_t ch = 0, k = 0, i = 0;
+    if (ch0 >= a.n_comms) {  // P2P channel: L2 prefetch of the slot sector two steps ahead (same channel)
+      const uint64_t xp = xi + 64;
+      if (xp < end0 && xp < wend) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.slots + sl0 + 2 * (xp - beg0)));
+    }
+    uint64_t ch = 0, k = 0, i = 0, slb = 0;
+    uint32_t psrc_ = 0, pdst_ = 0, nsd = 0, nrc = 0;
     if (act) {
-      ch = xi < end0 ? ch0 : upper_bound_u64(XB, a.NCH + 1, xi) - 1;
-      k = xi - XB[ch];
-      i = a.ch_base[ch] + k;
+      if (xi < end0) {
+        ch = ch0; k = xi - beg0; i = ib0 + k; slb = sl0; psrc_ = src0; pdst_ = dst0; nsd = nsd0; nrc = nrc0;
+      } else {
+        ch = upper_bound_u64(XB, a.NCH + 1, xi) - 1;
+        k = xi - XB[ch];
+        i = a.ch_base[ch] + k; slb = a.ch_slot[ch];
+        if (ch >= a.n_comms) {
+          const uint64_t p = ch - a.n_comms;
+          psrc_ = a.psrc[p]; pdst_ = a.pdst[p]; nsd = a.nsend[p]; nrc = a.nrecv[p];
+        }
+      }
       if (ch < a.n_comms && a.coff[ch + 1] - a.coff[ch] > XBIG) act = false;  // k_cross_big (lanes over members)
     }
     // one channel across the whole warp (the common case): its members are the same for every lane
     const bool uni = __all_sync(0xFFFFFFFFu, act && ch == ch0);
     const bool isp = ch >= a.n_comms;
     const uint32_t nm = isp ? 2u : (uint32_t)(a.coff[ch + 1] - a.coff[ch]);
-    const uint64_t sb = a.ch_slot[ch] + k * nm;
-    auto member = [&](uint32_t q) -> uint32_t {
-      return isp ? (q == 0 ? a.psrc[ch - a.n_comms] : a.pdst[ch - a.n_comms]) : a.cmem[a.coff[ch] + q];
-    };
+    const uint64_t sb = slb + k * nm;
+    auto member = [&](uint32_t q) -> uint32_t { return isp ? (q == 0 ? psrc_ : pdst_) : a.cmem[a.coff[ch] + q]; };
+    if (uni && isp && !a.p2p_pos && !a.wi) {
+      // P2P fast path: both slots in one 32-byte sector; complete = both present (ch_nmin = min(sends, recvs))
+      const bool h0 = nsd > k, h1 = nrc > k;
+      uint4 s0 = make_uint4(0, 0, 0, 0), s1 = s0;
+      if (h0) s0 = a.slots[sb];
+      if (h1) s1 = a.slots[sb + 1];
+      uint32_t flags = (s0.z >> 31) ? SCAN_F_WARMUP : 0u, dmin = 0, dmax = 0, last = NONE32;
+      if (h0 && h1) {
+        flags |= SCAN_F_COMPLETE | SCAN_F_KIND_OK;
+        if (s0.w == s1.w) {
+          flags |= SCAN_F_PAYLOAD_OK | SCAN_F_VALID;
+          dmin = min(s0.x, s1.x); dmax = max(s0.x, s1.x);
+          if (s0.x != s1.x) flags |= SCAN_F_UNIQUE_LAST;
+          const bool l1 = s1.x < s0.x;  // last arriver: lowest member with the minimum
+          last = l1 ? pdst_ : psrc_;
+          const uint32_t w0 = s0.x - dmin, w1 = s1.x - dmin;
+          acc_w0 += w0; acc_w1 += w1; acc_t += dmin;
+          if (l1 && (unsigned long long)w0 > a.wait_margin) acc_e0 += w0;   // src waits on dst
+          if (!l1 && (unsigned long long)w1 > a.wait_margin) acc_e1 += w1;  // dst waits on src
+        } else {
+          ++pmis;
+        }
+      } else {
+        ++inc;
+      }
+      a.rec[i] = make_uint4(dmin, dmax, last, flags);
+      a.lk_key[i - a.p2p_inst0] = lk_sample_key(flags, dmin, s0.w);
+      continue;
+    }
     auto present = [&](uint32_t q) -> bool {
-      if (isp) return (q == 0 ? a.nsend[ch - a.n_comms] : a.nrecv[ch - a.n_comms]) > k;
+      if (isp) return (q == 0 ? nsd : nrc) > k;
       const uint32_t m = a.cmem[a.coff[ch] + q];
       const uint32_t C = a.r_nkeys[m];
       const uint32_t p = lower_bound_u32(a.r_keys + (uint64_t)m * RCAP, C, (uint32_t)ch);
@@ -1655,7 +1723,7 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
     // a P2P instance's send and receive slots: one 32-byte sector, read once
     uint4 s0 = make_uint4(0, 0, 0, 0), s1 = s0;
     if (act && isp) {
-      const bool h0 = a.nsend[ch - a.n_comms] > k, h1 = a.nrecv[ch - a.n_comms] > k;
+      const bool h0 = nsd > k, h1 = nrc > k;
       if (h0) s0 = a.slots[sb];
       if (h1) s1 = a.slots[sb + 1];
       if (a.p2p_pos) {
@@ -1756,6 +1824,7 @@ __global__ void __launch_bounds__(256) k_cross_reduce(XArgs a) {
       }
     }
   }
+  flush_link();
   inc = warp_sum_u32(inc); kmis = warp_sum_u32(kmis); pmis = warp_sum_u32(pmis);
   if (lane_id() == 0) {
     if (inc) atomicAdd(&a.cnt->n_incomplete, (unsigned long long)inc);
@@ -1799,7 +1868,10 @@ int launch_cross_reduce(Ctx& c) {
   }
   const size_t xsm = (c.NCH + 1) * 8;
   a.xb_smem = xsm <= 48 * 1024 ? 1 : 0;
-  unsigned blocks = (unsigned)std::min<uint64_t>((c.n_xinst + 255) / 256, 148ull * 8);
+  static int sms = 0;
+  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+  // one resident wave (4 CTAs of 256 threads per SM at <= 64 registers): each warp walks one contiguous chunk
+  unsigned blocks = (unsigned)std::min<uint64_t>((c.n_xinst + 255) / 256, (uint64_t)std::max(sms, 1) * 4);
   k_cross_reduce<<<blocks, 256, a.xb_smem ? xsm : 0, c.stream>>>(a);
   if (c.n_big) {
     k_cross_big<<<dim3(c.n_big, 32), 256, 0, c.stream>>>(a, c.xbig.as<uint32_t>(), c.n_big);
