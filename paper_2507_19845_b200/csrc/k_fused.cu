@@ -1993,20 +1993,10 @@ int launch_xwait_scatter(Ctx& c) {
 // ----------------------------------------------------------------------------- deferred stage 2
 // The first comm position of a tile whose preceding compute segment starts in an earlier tile:
 // pslow from the global slow bits (complete after k_fused), late flags from dlate.
-__global__ void k_deferred(uint32_t n_ftiles, int PP, uint32_t R, int W, const uint32_t* st_tile0, const uint32_t* dinfo,
-                           const uint32_t* dlate, const uint64_t* bits_off, const uint32_t* bits, uint32_t classes,
-                           uint32_t* wl_joined, uint32_t* wl_late, const Counters* cnt) {
-  const uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (it >= (uint64_t)n_ftiles * R) return;
-  if (*((volatile const unsigned*)&cnt->overflow) & NOT_SPMD) return;
-  const uint32_t tile = (uint32_t)(it / R), row = (uint32_t)(it % R);
-  const uint32_t* di = dinfo + (uint64_t)tile * 4;
-  if (!(di[3] & 1u)) return;
-  const uint32_t cls = di[3] >> 8;
-  if (!((classes >> (cls - 1)) & 1u)) return;
-  uint32_t s = 0;
-  while (s + 1 < (uint32_t)PP && st_tile0[s + 1] <= tile) ++s;
-  const uint32_t r = s * R + row;
+__device__ __forceinline__ void k_deferred_row(uint32_t tile, uint32_t row, uint32_t r, uint32_t R, int W, uint4 d4,
+                                               const uint32_t* dlate, const uint64_t* bits_off, const uint32_t* bits,
+                                               uint32_t* wl_joined, uint32_t* wl_late) {
+  const uint32_t di[4] = {d4.x, d4.y, d4.z, d4.w};
   const uint32_t* b = bits + bits_off[r];
   const uint32_t lo = di[1], hi = di[0];
   bool any = false;
@@ -2025,11 +2015,25 @@ __global__ void k_deferred(uint32_t n_ftiles, int PP, uint32_t R, int W, const u
   if ((dlate[(uint64_t)tile * ((R + 31) / 32) + row / 32] >> (row & 31)) & 1u) atomicAdd(&wl_late[(uint64_t)win * W + r], 1u);
 }
 
+// one CTA per tile (most tiles have no deferred position and leave at once), threads over its rows
+__global__ void __launch_bounds__(128) k_deferred(uint32_t R, int W, const uint8_t* tile_stage, const uint32_t* dinfo,
+                                                  const uint32_t* dlate, const uint64_t* bits_off, const uint32_t* bits,
+                                                  uint32_t classes, uint32_t* wl_joined, uint32_t* wl_late, const Counters* cnt) {
+  const uint32_t tile = blockIdx.x;
+  const uint4 d4 = reinterpret_cast<const uint4*>(dinfo)[tile];
+  if (!(d4.w & 1u)) return;
+  const uint32_t cls = d4.w >> 8;
+  if (!((classes >> (cls - 1)) & 1u)) return;
+  if (*((volatile const unsigned*)&cnt->overflow) & NOT_SPMD) return;
+  const uint32_t s = tile_stage[tile];
+  for (uint32_t row = threadIdx.x; row < R; row += blockDim.x) k_deferred_row(tile, row, s * R + row, R, W, d4, dlate,
+                                                                               bits_off, bits, wl_joined, wl_late);
+}
+
 int launch_deferred(Ctx& c) {
   if (c.lcfg.stage2_mode != 0 || stage_active(c)) return 0;  // k_stage carries the segments itself
-  const uint64_t items = (uint64_t)c.n_ftiles * c.FR;
-  k_deferred<<<(unsigned)((items + 255) / 256), 256, 0, c.stream>>>(
-      c.n_ftiles, c.PP, c.FR, c.W, c.st_tile0.as<uint32_t>(), c.dinfo.as<uint32_t>(), c.dlate.as<uint32_t>(),
+  k_deferred<<<c.n_ftiles, 128, 0, c.stream>>>(
+      c.FR, c.W, c.tile_stage.as<uint8_t>(), c.dinfo.as<uint32_t>(), c.dlate.as<uint32_t>(),
       c.r_bits_off.as<uint64_t>(), c.bits.as<uint32_t>(), c.lcfg.stage2_classes, c.wl_joined.as<uint32_t>(),
       c.wl_late.as<uint32_t>(), c.counters.as<Counters>());
   return 1;

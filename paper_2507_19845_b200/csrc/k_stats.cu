@@ -677,7 +677,7 @@ __global__ void __launch_bounds__(LM_NT, 4) k_link_median(LKArgs a) {
   }
 }
 
-// g per (window, direction class) and LinkSlow flags; one CTA per window.
+// g per (window, direction class) and LinkSlow flags; one CTA per (window, direction class).
 __global__ void __launch_bounds__(LK_NT) k_link_flags(uint32_t n_p2p, int W, const uint32_t* psrc, const uint32_t* lk_medp,
                                                       const uint32_t* lk_medt, const uint8_t* lk_dir, const uint8_t* lk_elig,
                                                       uint8_t* lk_slow, uint8_t* wl_link_slow, uint32_t bw_num, uint32_t bw_den,
@@ -689,9 +689,11 @@ __global__ void __launch_bounds__(LK_NT) k_link_flags(uint32_t n_p2p, int W, con
   uint32_t* si = smem + 2 * LINK_CAP;
   __shared__ uint32_t scan_sm[33];
   const uint32_t w = blockIdx.x;
+  const uint32_t dir = blockIdx.y;  // one CTA per (window, direction class)
   const uint64_t o0 = (uint64_t)w * n_p2p;
-  for (uint32_t i = threadIdx.x; i < n_p2p; i += LK_NT) lk_slow[o0 + i] = 0;
-  for (int dir = 0; dir < 3; ++dir) {
+  for (uint32_t i = threadIdx.x; i < n_p2p; i += LK_NT)
+    if (lk_dir[o0 + i] == dir) lk_slow[o0 + i] = 0;
+  {
     uint32_t carry = 0;
     __syncthreads();
     for (uint32_t kb = 0; kb < n_p2p; kb += LK_NT) {
@@ -703,8 +705,8 @@ __global__ void __launch_bounds__(LK_NT) k_link_flags(uint32_t n_p2p, int W, con
       carry += tot;
     }
     __syncthreads();
-    if (carry == 0) continue;
-    if (carry > LINK_CAP) { if (threadIdx.x == 0) atomicOr(&cnt->overflow, 16u); continue; }
+    if (carry == 0) return;
+    if (carry > LINK_CAP) { if (threadIdx.x == 0) atomicOr(&cnt->overflow, 16u); return; }
     smem_bitonic<LK_NT>(sp, st, si, carry);
     const uint32_t m = (carry - 1) / 2;
     const unsigned __int128 pg = sp[m], tg = st[m];
@@ -770,7 +772,7 @@ int launch_link_flags(Ctx& c) {
   if (c.n_p2p == 0) return 0;
   const size_t sm = 3 * LINK_CAP * sizeof(uint32_t);
   cudaFuncSetAttribute(k_link_flags, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_link_flags<<<c.NW, LK_NT, sm, c.stream>>>((uint32_t)c.n_p2p, c.W, c.ch_nsend.as<uint32_t>() + c.n_p2p,
+  k_link_flags<<<dim3(c.NW, 3), LK_NT, sm, c.stream>>>((uint32_t)c.n_p2p, c.W, c.ch_nsend.as<uint32_t>() + c.n_p2p,
                                                c.lk_medp.as<uint32_t>(), c.lk_medt.as<uint32_t>(), c.lk_dir.as<uint8_t>(),
                                                c.lk_elig.as<uint8_t>(), c.lk_slow.as<uint8_t>(), c.wl_link_slow.as<uint8_t>(),
                                                c.lcfg.bw_num, c.lcfg.bw_den, c.counters.as<Counters>());
