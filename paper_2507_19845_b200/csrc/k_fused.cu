@@ -56,37 +56,56 @@ struct PreArgs {
   uint32_t T, R, n_ftiles; const uint32_t* st_tile0; const uint32_t* st_npos;
   const uint32_t* role_comm; const uint32_t* ncroles; const uint8_t* role_type;
   uint32_t* cols; uint32_t* posA; uint32_t* posB; uint16_t* posK; Counters* cnt;
+  const uint8_t* tile_stage;
 };
 
 __global__ void __launch_bounds__(256) k_fused_prepass(PreArgs a) {
   __shared__ uint32_t rcnt[8][ROLES];
+  __shared__ uint32_t rcs[8][CROLES];
   const uint32_t wid = threadIdx.x >> 5, lane = lane_id();
   const uint32_t tile = blockIdx.x * 8 + wid;
   rcnt[wid][lane] = 0;
   __syncwarp();
   if (tile >= a.n_ftiles) return;
-  uint32_t s = 0;
-  while (s + 1 < (uint32_t)a.PP && a.st_tile0[s + 1] <= tile) ++s;
+  const uint32_t s = a.tile_stage[tile];
   const uint32_t p0 = (tile - a.st_tile0[s]) * a.T;
   const uint32_t np = min(a.T, a.st_npos[s] - p0);
   const uint32_t r0 = s * a.R;
   const uint64_t g0 = a.rank_off[r0] + p0;
-  const uint32_t* rc = a.role_comm + (uint64_t)r0 * CROLES;
   const uint32_t ncr = a.ncroles[s];
+  if (lane < CROLES) rcs[wid][lane] = a.role_comm[(uint64_t)r0 * CROLES + lane];  // the template's roles, staged
+  __syncwarp();
+  const uint32_t* rc = rcs[wid];
+  // the template row's kind_op / comm words of the whole tile, loaded up front (independent requests)
+  constexpr int PC = 4;  // chunks of 32 positions in flight
+  uint16_t kpre[PC];
+  uint32_t cpre[PC];
   uint32_t cj = 0, cm = 0, ci = 0;
   int32_t lastj = -1;
   bool bad = false;
   const unsigned lt = (1u << lane) - 1u;
   for (uint32_t base = 0; base < np; base += 32) {
+    const uint32_t u = (base >> 5) % PC;
+    if (u == 0) {
+#pragma unroll
+      for (int v = 0; v < PC; ++v) {
+        const uint32_t pv = base + 32u * v + lane;
+        kpre[v] = pv < np ? a.kind[g0 + pv] : (uint16_t)0;
+        cpre[v] = pv < np ? a.comm[g0 + pv] : 0u;
+      }
+    }
+    uint16_t ko = 0;
+    uint32_t cmw = 0;
+#pragma unroll
+    for (int v = 0; v < PC; ++v) if ((uint32_t)v == u) { ko = kpre[v]; cmw = cpre[v]; }
     const uint32_t p = base + lane;
     const bool in = p < np;
-    const uint16_t ko = in ? a.kind[g0 + p] : 0;
     const uint32_t kind = ko & 7u;
     const bool isc = in && kind == 0, iscomm = in && kind != 0, ie = in && ((ko >> 3) & 1u);
     int role = 31;
     uint32_t type = 0;
     if (iscomm) {
-      role = role_of(kind, a.comm[g0 + p], r0, rc, ncr, a.R, a.W);
+      role = role_of(kind, cmw, r0, rc, ncr, a.R, a.W);
       if (role < 0) { bad = true; role = 0; }
       type = role >= 16 ? 4u : a.role_type[s * ROLES + role];
     }
@@ -175,7 +194,7 @@ int launch_fused_prepass(Ctx& c) {
   PreArgs a{c.d_kind, c.d_comm, c.rank_off.as<uint64_t>(), c.W, c.PP, c.FT, c.FR, c.n_ftiles, c.st_tile0.as<uint32_t>(),
             c.st_npos.as<uint32_t>(), c.role_comm.as<uint32_t>(), c.ncroles.as<uint32_t>(), c.role_type.as<uint8_t>(),
             c.ft_cols.as<uint32_t>(), c.ft_posA.as<uint32_t>(), c.ft_posB.as<uint32_t>(), c.ft_posK.as<uint16_t>(),
-            c.counters.as<Counters>()};
+            c.counters.as<Counters>(), c.tile_stage.as<uint8_t>()};
   k_fused_prepass<<<(c.n_ftiles + 7) / 8, 256, 0, c.stream>>>(a);
   k_fused_scan<<<dim3(c.PP, ROLES + 3), SC_NT, 0, c.stream>>>(c.n_ftiles, c.st_tile0.as<uint32_t>(), c.ft_cols.as<uint32_t>(),
                                                               c.ft_base.as<uint32_t>(), c.st_tot.as<uint32_t>(),
