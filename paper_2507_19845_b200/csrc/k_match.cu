@@ -550,8 +550,11 @@ struct AssignArgs {
 };
 
 __global__ void __launch_bounds__(256) k_assign(AssignArgs A) {
+  __shared__ uint32_t cdb[8][256];  // per warp: the round's compute durations / op ids, compacted
+  __shared__ uint16_t cob[8][256];
   const TileArgs& a = A.t;
-  const uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const uint32_t wid = threadIdx.x >> 5;
+  const uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wid;
   if (tile >= a.n_tiles) return;
   const uint32_t lane = lane_id();
   const uint32_t r = a.tile_rank[tile];
@@ -597,10 +600,22 @@ __global__ void __launch_bounds__(256) k_assign(AssignArgs A) {
       if (ko[q] & 7u) commm |= 1u << q;
       if (ko[q] & 8u) itm |= 1u << q;
     }
+    // the P2P events' payload / meta words are gathered below: request them now (L2 prefetch)
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (((commm >> q) & 1u) && (ko[q] & 7u) >= 5) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.pay + g + q));
+        if ((ko[q] & 7u) == 5) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.meta + g + q));
+      }
     uint32_t ctot, itot;
     const uint32_t cex = warp_excl_scan(__popc(commm), ctot) + comm_carry;
     const uint32_t iex = warp_excl_scan(__popc(itm), itot) + iter_carry;
-    // compute events and iteration boundaries
+    // compute events (compacted through shared memory: the round's compute events are one contiguous
+    // range of the rank's compute index, stored coalesced) and iteration boundaries
+    const uint64_t ev0 = base > s ? base : s;  // the round's first event
+    const uint32_t jbase = (uint32_t)(ev0 - rstart) - comm_carry;
+    uint32_t ncomp = __popc(valid & ~commm);
+    ncomp = warp_sum_u32(ncomp);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       if (!((valid >> q) & 1u)) continue;
@@ -608,12 +623,15 @@ __global__ void __launch_bounds__(256) k_assign(AssignArgs A) {
       const uint32_t cb = cex + __popc(commm & ((1u << q) - 1u));
       const uint32_t j = (uint32_t)(ev - rstart) - cb;
       const bool isc = !((commm >> q) & 1u);
-      if (isc) { A.cdur[comp_off + j] = du[q]; A.cop[comp_off + j] = (uint16_t)(ko[q] >> 4); }
+      if (isc) { cdb[wid][j - jbase] = du[q]; cob[wid][j - jbase] = (uint16_t)(ko[q] >> 4); }
       if ((itm >> q) & 1u) {
         const uint32_t ib = iex + __popc(itm & ((1u << q) - 1u));
         citer_r[ib + 1] = j + (isc ? 1u : 0u);
       }
     }
+    __syncwarp();
+    for (uint32_t i = lane; i < ncomp; i += 32) { A.cdur[comp_off + jbase + i] = cdb[wid][i]; A.cop[comp_off + jbase + i] = cob[wid][i]; }
+    __syncwarp();
     // comm events, one pass per distinct key of the round
     uint32_t keys[8];
 #pragma unroll
