@@ -457,6 +457,7 @@ int launch_instance_export(Ctx& c, scan_output which, void* dst);
 int launch_fused_prepass(Ctx& c);
 int launch_fused_census(Ctx& c);
 int launch_fused(Ctx& c);
+bool p2p_defer_on(Ctx& c);
 int launch_p2p_roles(Ctx& c);
 int launch_stage(Ctx& c);
 // the analysis runs k_stage: selected at load and the channel bases fit its 32-bit tables

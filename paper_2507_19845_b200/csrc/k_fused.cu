@@ -316,7 +316,7 @@ struct FusedArgs {
   uint32_t slow_num, slow_den; unsigned long long slow_margin;
   uint32_t wi, classes, mode; unsigned long long late_margin, wait_margin; int want_ref;
   uint32_t it_off;  // global iteration of this shard's first iteration (0 unsharded)
-  uint32_t pf_dist, pf_own, pf_p2p; uint64_t n_events;  // k_fused_t: L2 prefetch of tile + pf_dist (0 = off), of its own tile, of its P2P payload / meta words; column length
+  uint32_t pf_dist, pf_own, pf_p2p, p2p_defer; uint64_t n_events;  // k_fused_t: L2 prefetch of tile + pf_dist (0 = off), of its own tile, of its P2P payload / meta words; column length
   unsigned long long wi_m;  // ceil(2^64 / wi) for wi > 1: window = umulhi64(iteration, wi_m), exact for 32-bit iterations
   Counters* cnt;
   // byte offsets of the transposed kernel's shared-memory arrays (host-computed, fused_t_layout)
@@ -988,7 +988,7 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
   __syncthreads();
   // L2 prefetch of the payload (and the sender's meta) word of every P2P event of the tile: the phase-B
   // cross units gather them; requested here, the DRAM fetches overlap the load pass below
-  if (a.pf_p2p) {
+  if (a.pf_p2p && !a.p2p_defer) {
     const uint32_t nx = nlist[3];
     for (uint32_t i = tid; i < nx * R; i += FT_NT) {
       const uint32_t xi = fdiv(i, a.fR), row = i - xi * R;
@@ -1159,7 +1159,9 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
 #if defined(MS_EXP_SKIP) && (MS_EXP_SKIP & 1024)
           if (R == 0)  // timing experiment only (results invalid)
 #endif
-          {
+          if (a.p2p_defer) {
+            pay = p0 + p;  // the event's position in its rank: k_cross_reduce gathers payload and warm-up bit
+          } else {
             pay = a.pay[e];
             if (send) warm = ((uint32_t)a.meta[e] >> 14) & 1u;
           }
@@ -1468,6 +1470,13 @@ int launch_p2p_roles(Ctx& c) {  // c.p2p_rbase sized by alloc_match_buffers
   return 1;
 }
 
+// MS_P2P_DEFER=1: the transposed fused kernel leaves P2P payload / meta to k_cross_reduce (experiment)
+bool p2p_defer_on(Ctx& c) {
+  static int v = -1;
+  if (v < 0) { const char* e = std::getenv("MS_P2P_DEFER"); v = e ? std::atoi(e) : 0; }
+  return v == 1 && c.fused_t && !stage_active(c);
+}
+
 int launch_fused(Ctx& c) {
   if (stage_active(c)) {  // the persistent TMA-fed kernel (k_stage.cu)
     const int n = launch_stage(c);
@@ -1508,6 +1517,7 @@ int launch_fused(Ctx& c) {
     static int pp = -1;
     if (pp < 0) { const char* e = std::getenv("MS_FT_PF_P2P"); pp = e ? std::atoi(e) : 1; }
     a.pf_p2p = (uint32_t)pp;
+    a.p2p_defer = p2p_defer_on(c) ? 1u : 0u;
     a.pf_dist = (uint32_t)pf;
     a.pf_own = (uint32_t)own;
     a.n_events = c.N;
@@ -1637,7 +1647,7 @@ __global__ void __launch_bounds__(256, 4) k_cross_reduce(XArgs a) {
   const uint64_t per = ((a.n_xinst + nwarps - 1) / nwarps + 31) & ~31ull;
   const uint64_t wend = min(a.n_xinst, (gw + 1) * per);
   // the warp's current channel, its instance range [beg0, end0) in cross order, and (P2P) its tables
-  uint64_t ch0 = 0, beg0 = 1, end0 = 0, ib0 = 0, sl0 = 0;
+  uint64_t ch0 = 0, beg0 = 1, end0 = 0, ib0 = 0, sl0 = 0, ro_src0 = 0, ro_dst0 = 0;
   uint32_t src0 = 0, dst0 = 0, nsd0 = 0, nrc0 = 0;
   // P2P fast path (whole warp on one link, one window): per-lane sums over the warp's steps on the
   // cached link -- member waits, transfer, wait-for edges src -> dst / dst -> src -- flushed with one
@@ -1668,11 +1678,13 @@ __global__ void __launch_bounds__(256, 4) k_cross_reduce(XArgs a) {
         if (ch0 >= a.n_comms) {
           const uint64_t p = ch0 - a.n_comms;
           src0 = a.psrc[p]; dst0 = a.pdst[p]; nsd0 = a.nsend[p]; nrc0 = a.nrecv[p];
+          if (a.p2p_pos) { ro_src0 = a.rank_off[src0]; ro_dst0 = a.rank_off[dst0]; }
         }
       }
       ch0 = __shfl_sync(0xFFFFFFFFu, ch0, 0); beg0 = __shfl_sync(0xFFFFFFFFu, beg0, 0); end0 = __shfl_sync(0xFFFFFFFFu, end0, 0);
       ib0 = __shfl_sync(0xFFFFFFFFu, ib0, 0); sl0 = __shfl_sync(0xFFFFFFFFu, sl0, 0);
       src0 = __shfl_sync(0xFFFFFFFFu, src0, 0); dst0 = __shfl_sync(0xFFFFFFFFu, dst0, 0);
+      ro_src0 = __shfl_sync(0xFFFFFFFFu, ro_src0, 0); ro_dst0 = __shfl_sync(0xFFFFFFFFu, ro_dst0, 0);
       nsd0 = __shfl_sync(0xFFFFFFFFu, nsd0, 0); nrc0 = __shfl_sync(0xFFFFFFFFu, nrc0, 0);
     }
     if (ch0 >= a.n_comms) {  // P2P channel: L2 prefetch of the slot sector two steps ahead (same channel)
@@ -1701,12 +1713,24 @@ __global__ void __launch_bounds__(256, 4) k_cross_reduce(XArgs a) {
     const uint32_t nm = isp ? 2u : (uint32_t)(a.coff[ch + 1] - a.coff[ch]);
     const uint64_t sb = slb + k * nm;
     auto member = [&](uint32_t q) -> uint32_t { return isp ? (q == 0 ? psrc_ : pdst_) : a.cmem[a.coff[ch] + q]; };
-    if (uni && isp && !a.p2p_pos && !a.wi) {
+    if (uni && isp && !a.wi) {
       // P2P fast path: both slots in one 32-byte sector; complete = both present (ch_nmin = min(sends, recvs))
       const bool h0 = nsd > k, h1 = nrc > k;
       uint4 s0 = make_uint4(0, 0, 0, 0), s1 = s0;
       if (h0) s0 = a.slots[sb];
       if (h1) s1 = a.slots[sb + 1];
+      if (a.p2p_pos) {  // the fused pass left each member's position in its rank: gather payload and warm-up bit
+        if (h0) {
+          const uint64_t e0 = ro_src0 + s0.w;
+          s0.w = a.pay[e0];
+          s0.z = (s0.z & 0x7FFFFFFFu) | (((uint32_t)a.meta[e0] >> 14) & 1u) << 31;
+          reinterpret_cast<uint32_t*>(a.slots + sb)[3] = s0.w;
+        }
+        if (h1) {
+          s1.w = a.pay[ro_dst0 + s1.w];
+          reinterpret_cast<uint32_t*>(a.slots + sb + 1)[3] = s1.w;
+        }
+      }
       uint32_t flags = (s0.z >> 31) ? SCAN_F_WARMUP : 0u, dmin = 0, dmax = 0, last = NONE32;
       if (h0 && h1) {
         flags |= SCAN_F_COMPLETE | SCAN_F_KIND_OK;
@@ -1869,7 +1893,7 @@ static XArgs cross_args(Ctx& c) {
   a.ew = c.ewc.as<unsigned long long>(); a.rk_sum = c.rk_sum.as<unsigned long long>();
   a.wi = c.dcfg.window_iters; a.wait_margin = (unsigned long long)c.lcfg.wait_margin_ns; a.cnt = c.counters.as<Counters>();
   a.p2p_eslot = c.p2p_eslot.as<uint32_t>(); a.xb_smem = 0; a.xe_off = c.xe_off.as<uint64_t>(); a.xe_col = c.xe_col.as<uint32_t>();
-  a.p2p_pos = stage_active(c) ? 1 : 0; a.pay = c.d_pay; a.meta = c.d_meta; a.rank_off = c.rank_off.as<uint64_t>();
+  a.p2p_pos = (stage_active(c) || p2p_defer_on(c)) ? 1 : 0; a.pay = c.d_pay; a.meta = c.d_meta; a.rank_off = c.rank_off.as<uint64_t>();
   return a;
 }
 
