@@ -320,8 +320,10 @@ scan_status scan_loaded_column(scan_ctx* ctx, int column, void* dst, uint64_t ds
    The document is built on the device: a call with dst NULL builds it and returns its size in
    *n_bytes; a call with dst (host or device memory of dst_bytes >= *n_bytes) copies the document
    built for the current state (load / analysis / alignment), building it first if needed. Requires start_ns at load and a match (scan_match_collectives or
-   scan_analyze); errors: SCAN_E_ORDER, SCAN_E_INVALID_ARG, SCAN_E_UNSUPPORTED (stream or
-   sharded context), SCAN_E_OOM, SCAN_E_CUDA.                                                 */
+   scan_analyze); errors: SCAN_E_ORDER, SCAN_E_INVALID_ARG, SCAN_E_UNSUPPORTED (stream
+   context), SCAN_E_OOM, SCAN_E_CUDA. On a sharded context (scan_create_sharded*) the document
+   holds the shard's own events (its iteration block) with job-wide instance ids; the job's
+   document is the shards' event lists merged by (ts, pid, shard order).                       */
 #define SCAN_EMIT_ALIGNED 1u
 scan_status scan_emit_chrome(scan_ctx* ctx, uint32_t flags, void* dst, uint64_t dst_bytes, int dst_is_device, uint64_t* n_bytes);
 

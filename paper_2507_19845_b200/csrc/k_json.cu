@@ -1455,7 +1455,9 @@ scan_status scan_emit_chrome(scan_ctx* ctx, uint32_t flags, void* dst, uint64_t 
   if (!ctx || !n_bytes) return SCAN_E_INVALID_ARG;
   Ctx& c = ctx->c;
   CK(cudaSetDevice(c.device));
-  if (c.stream_mode || c.n_shards > 1) { c.err = "emit is unavailable on stream / sharded contexts"; return SCAN_E_UNSUPPORTED; }
+  // a sharded context emits its own iteration block (job-wide instance ids); the job's document is the
+  // shards' documents merged by (ts, pid, shard order)
+  if (c.stream_mode) { c.err = "emit is unavailable on stream contexts"; return SCAN_E_UNSUPPORTED; }
   if (!c.loaded || !c.matched) { c.err = "emit needs a loaded and matched trace"; return SCAN_E_ORDER; }
   if (flags & ~SCAN_EMIT_ALIGNED) { c.err = "unknown emit flags"; return SCAN_E_INVALID_ARG; }
   if ((flags & SCAN_EMIT_ALIGNED) && !c.aligned) { c.err = "SCAN_EMIT_ALIGNED needs scan_align"; return SCAN_E_ORDER; }

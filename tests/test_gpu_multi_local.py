@@ -88,3 +88,54 @@ def test_local_shards_equal_the_oracle(G, case):
     merged["_res"] = parts[0]["res"]
     from test_gpu_parity import compare
     compare(o, merged)
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_local_shards_emit_merges_to_the_whole_document(G):
+    """scan_emit_chrome on a sharded context writes the shard's own iteration block with job-wide
+    instance ids; merged by (ts, pid, shard order) the shards' event lists are the whole job's document
+    (one time-ordered merged trace)."""
+    import json
+    import torch
+    import paper_2507_19845_b200 as ms
+    from tracegen import configs
+    cfg = configs.c2(iterations=6)
+    full = tg.generate(cfg)
+    group = ms.LocalGroup(G)
+    streams = [torch.cuda.Stream(0) for _ in range(G)]
+    scans = [ms.Scan(0, streams[g].cuda_stream, shards=(G, g, group)) for g in range(G)]
+    slices = []
+    for g in range(G):
+        b, e = ms.shard_iterations(cfg.iterations, G, g)
+        slices.append(ms.slice_iterations(full, b, e))
+    docs, errs = [None] * G, []
+
+    def work(g):
+        try:
+            scans[g].load(slices[g], start=True)
+            scans[g].analyze()
+            docs[g] = scans[g].emit_chrome()
+        except ms.ScanError as x:
+            errs.append((g, x.status, str(x)))
+
+    th = [threading.Thread(target=work, args=(g,)) for g in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for s in scans:
+        s.close()
+    group.close()
+    assert not errs, errs
+    whole = ms.Scan(0)
+    whole.load(full, start=True)
+    whole.analyze()
+    ref = json.loads(whole.emit_chrome())["traceEvents"]
+    whole.close()
+    merged = []
+    for g, d in enumerate(docs):
+        for i, ev in enumerate(json.loads(d)["traceEvents"]):
+            merged.append(((ev["ts"], ev["pid"], g, i), ev))
+    merged.sort(key=lambda x: x[0])
+    assert len(merged) == len(ref)
+    assert [ev for _, ev in merged] == ref
