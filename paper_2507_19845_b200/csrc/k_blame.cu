@@ -6,7 +6,8 @@
 // event that did not wait points at its own rank's previous event; compute events and the first
 // event of a rank are roots. Following the pointers gives, for every wait, the event where the delay
 // began; pointer jumping (ptr <- ptr[ptr]) resolves all chains in log2(longest chain) rounds.
-//   k_bl_last   per instance: the member event of its last arriver          (tile warps)
+//   k_bl_last   per instance: where its waiting members point -- the previous event of its last
+//               arriver's member event (that event itself if it is its rank's first)   (tile warps)
 //   k_bl_ptr    per event: the pointer (u32 event index)                      (tile warps)
 //   k_bl_jump   one jumping round, double-buffered, with a change flag
 //   k_bl_sum    terminal check (a fixed point of the ORIGINAL pointers; anything else is a cycle),
@@ -22,26 +23,26 @@ struct BA {
   uint64_t n_tiles;
   const uint32_t* tile_rank; const uint64_t* tile_start; const uint64_t* rank_off;
   const uint16_t* kind; const uint32_t* inst; const uint32_t* wait; const uint4* rec;
-  uint32_t* last_ev; uint32_t* ptr0; uint16_t* rank16;
+  uint32_t* last_ev;  // per instance: the pointer target of its waiting members (EB2)
+  uint32_t* ptr0;    // unused (null)
+  uint16_t* rank16;  // per event: its rank if the event is a root of the ORIGINAL pointers, else 0xFFFF
   uint32_t* ptr; unsigned int* n_active;  // working pointers (jumped in place), events that are not roots
 };
 
-__device__ __forceinline__ bool waiting_ev(const BA& a, uint64_t x, uint16_t ko, uint4& rc) {
-  if ((ko & 7u) == 0) return false;
-  rc = a.rec[a.inst[x]];
-  return (rc.w & SCAN_F_VALID) && a.wait[x] > 0;
-}
-
+// A communication event waited iff its wait is > 0 (EB1): the wait is 0 for every member of an
+// invalid instance, and the last arriver of a valid one waits 0, so only events with wait 0 can be the
+// last arriver's member and need the instance record.
 __global__ void __launch_bounds__(256) k_bl_last(BA a) {
   const uint64_t tile = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (tile >= a.n_tiles) return;
   const uint32_t r = a.tile_rank[tile];
+  const uint64_t rs = a.rank_off[r];
   const uint64_t s = a.tile_start[tile], e = min(s + (uint64_t)TILE_EV, a.rank_off[r + 1]);
   for (uint64_t x = s + lane_id(); x < e; x += 32) {
-    if ((a.kind[x] & 7u) == 0) continue;
+    if ((a.kind[x] & 7u) == 0 || a.wait[x] != 0) continue;
     const uint32_t I = a.inst[x];
     const uint4 rc = a.rec[I];
-    if ((rc.w & SCAN_F_VALID) && rc.z == r) a.last_ev[I] = (uint32_t)x;
+    if ((rc.w & SCAN_F_VALID) && rc.z == r) a.last_ev[I] = (uint32_t)(x == rs ? x : x - 1);
   }
 }
 
@@ -58,15 +59,11 @@ __global__ void __launch_bounds__(256) k_bl_ptr(BA a) {
     for (uint64_t x = s + lane_id(); x < e; x += 32) {
       const uint16_t ko = a.kind[x];
       uint64_t p;
-      uint4 rc;
       if ((ko & 7u) == 0) p = x;                                     // EB3: compute events are roots
-      else if (waiting_ev(a, x, ko, rc)) {                           // EB2: the last arriver's previous event
-        const uint64_t le = a.last_ev[a.inst[x]];
-        p = le == a.rank_off[rc.z] ? le : le - 1;
-      } else p = x == rs ? x : x - 1;                                // EB3: own previous event
-      a.ptr0[x] = (uint32_t)p;
+      else if (a.wait[x] > 0) p = a.last_ev[a.inst[x]];             // EB2: the last arriver's previous event
+      else p = x == rs ? x : x - 1;                                  // EB3: own previous event
       a.ptr[x] = (uint32_t)p;
-      a.rank16[x] = (uint16_t)r;
+      a.rank16[x] = p == x ? (uint16_t)r : (uint16_t)0xFFFFu;  // W <= 65535: 0xFFFF is no rank
       n_act += p != x;
     }
   }
@@ -88,6 +85,65 @@ __global__ void __launch_bounds__(256) k_bl_jump(uint64_t N, uint32_t* ptr, unsi
     if (q != p) { ptr[x] = q; ch = true; }
   }
   if (__any_sync(0xFFFFFFFFu, ch) && lane_id() == 0) atomicOr(changed, 1u);
+}
+
+// Pointer jumping on compacted lists: round 1 visits every event; an event whose pointer moved stays
+// on its block's list for the next round (the others have reached a root, or will be found there next
+// round and dropped), so later rounds cost only what is still moving. Lists are segmented per block
+// (block b owns [b S, (b+1) S) of each list buffer): no global counter, no atomics on the append.
+constexpr int JB_NT = 256;
+
+// block-level append of the flagged threads' x to out[nout ...]; nout is block-uniform
+__device__ __forceinline__ void jb_append(bool act, uint32_t x, uint32_t* out, uint32_t& nout, uint32_t* wcnt) {
+  const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+  const unsigned bm = __ballot_sync(0xFFFFFFFFu, act);
+  if (lane == 0) wcnt[wid] = (uint32_t)__popc(bm);
+  __syncthreads();
+  uint32_t off = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < JB_NT / 32; ++w) { const uint32_t v = wcnt[w]; off += (w < (int)wid) ? v : 0u; tot += v; }
+  if (act) out[nout + off + __popc(bm & ((1u << lane) - 1u))] = x;
+  __syncthreads();  // wcnt is reused by the next call
+  nout += tot;
+}
+
+__device__ __forceinline__ bool jb_step(uint32_t* ptr, uint32_t x) {
+  const uint32_t p = ptr[x];
+  if (p == x) return false;
+  const uint32_t q = ptr[p];
+  if (q == p) return false;
+  ptr[x] = q;
+  return true;
+}
+
+__global__ void __launch_bounds__(JB_NT) k_bl_jump0(uint64_t N, uint64_t S, uint32_t* ptr, uint32_t* list_out, uint32_t* seg_out,
+                                                    unsigned int* changed) {
+  __shared__ uint32_t wcnt[JB_NT / 32];
+  uint32_t* out = list_out + (uint64_t)blockIdx.x * S;
+  uint32_t nout = 0;
+  for (uint64_t c0 = (uint64_t)blockIdx.x * JB_NT; c0 < N; c0 += (uint64_t)gridDim.x * JB_NT) {
+    const uint64_t x = c0 + threadIdx.x;
+    const bool act = x < N && jb_step(ptr, (uint32_t)x);
+    jb_append(act, (uint32_t)x, out, nout, wcnt);
+  }
+  if (threadIdx.x == 0) { seg_out[blockIdx.x] = nout; if (nout) atomicOr(changed, 1u); }
+}
+
+__global__ void __launch_bounds__(JB_NT) k_bl_jumpk(uint64_t S, uint32_t* ptr, const uint32_t* list_in, const uint32_t* seg_in,
+                                                    uint32_t* list_out, uint32_t* seg_out, unsigned int* changed) {
+  __shared__ uint32_t wcnt[JB_NT / 32];
+  const uint32_t nin = seg_in[blockIdx.x];
+  const uint32_t* in = list_in + (uint64_t)blockIdx.x * S;
+  uint32_t* out = list_out + (uint64_t)blockIdx.x * S;
+  uint32_t nout = 0;
+  for (uint32_t i0 = 0; i0 < nin; i0 += JB_NT) {
+    const uint32_t i = i0 + threadIdx.x;
+    uint32_t x = 0;
+    bool act = false;
+    if (i < nin) { x = in[i]; act = jb_step(ptr, x); }
+    jb_append(act, x, out, nout, wcnt);
+  }
+  if (threadIdx.x == 0) { seg_out[blockIdx.x] = nout; if (nout) atomicOr(changed, 1u); }
 }
 
 struct SA {
@@ -122,9 +178,9 @@ __global__ void __launch_bounds__(256) k_bl_sum(SA a) {
         const uint32_t p = a.ptr[x];
         ++nw;
         suf += w;
-        if (a.b.ptr0[p] == p) {  // a root of the original pointers
+        const uint32_t rr = a.b.rank16[p];  // one gather: the root's rank, or 0xFFFF (not a root: a cycle)
+        if (rr != 0xFFFFu) {  // a root of the original pointers
           root = p;
-          const uint32_t rr = a.b.rank16[p];
           if (rr == r) slf += w;
           else {
             if (rr != run_r) {
@@ -175,8 +231,12 @@ scan_status blame_all(Ctx& c, scan_blame_result* out) {
     c.xwait_pending = false;
   }
   const uint64_t N1 = std::max<uint64_t>(N, 1);
-  CK(c.bl_inst.ensure(N1 * 4)); CK(c.bl_wait.ensure(N1 * 4)); CK(c.bl_p0.ensure(N1 * 4)); CK(c.bl_pa.ensure(N1 * 4));
-  CK(c.bl_pb.ensure(N1 * 4)); CK(c.bl_root.ensure(N1 * 8)); CK(c.bl_rk.ensure(N1 * 2)); CK(c.bl_last.ensure(std::max<uint64_t>(c.n_inst, 1) * 4));
+  // jumping lists (bl_inst reused after k_bl_ptr, bl_pb): jb block segments of S entries
+  const unsigned jb = (unsigned)std::min<uint64_t>(nbk(N, JB_NT), 148ull * 8);
+  const uint64_t S = (N + (uint64_t)jb * JB_NT - 1) / ((uint64_t)jb * JB_NT) * JB_NT;  // elements per block in round 1
+  const uint64_t LCAP = std::max<uint64_t>(N1, (uint64_t)jb * S);
+  CK(c.bl_inst.ensure(LCAP * 4)); CK(c.bl_wait.ensure(N1 * 4)); CK(c.bl_pa.ensure(N1 * 4));
+  CK(c.bl_pb.ensure(LCAP * 4)); CK(c.bl_root.ensure(N1 * 8)); CK(c.bl_rk.ensure(N1 * 2)); CK(c.bl_last.ensure(std::max<uint64_t>(c.n_inst, 1) * 4));
   CK(c.bl_rank.ensure(4 * W * 8 + 16 + 8));
   flush_fills(c);
   CK(cudaMemsetAsync(c.bl_rank.p, 0, 4 * W * 8 + 16 + 8, c.stream));
@@ -186,7 +246,7 @@ scan_status blame_all(Ctx& c, scan_blame_result* out) {
   unsigned int* counters2 = reinterpret_cast<unsigned int*>(c.bl_rank.as<uint8_t>() + 4 * W * 8 + 16);  // [0] changed, [1] n_active
   BA b{c.n_tiles, c.tile_rank.as<uint32_t>(), c.tile_start.as<uint64_t>(), c.rank_off.as<uint64_t>(), c.d_kind,
        c.bl_inst.as<uint32_t>(), c.bl_wait.as<uint32_t>(), c.inst_rec.as<uint4>(), c.bl_last.as<uint32_t>(),
-       c.bl_p0.as<uint32_t>(), c.bl_rk.as<uint16_t>(), c.bl_pa.as<uint32_t>(), counters2 + 1};
+       nullptr, c.bl_rk.as<uint16_t>(), c.bl_pa.as<uint32_t>(), counters2 + 1};
   const unsigned tb = nbk(c.n_tiles, 8);
   uint32_t rounds = 0;
   unsigned int n_act = 0;
@@ -200,14 +260,22 @@ scan_status blame_all(Ctx& c, scan_blame_result* out) {
     });
     CK(cudaMemcpyAsync(&n_act, counters2 + 1, 4, cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
-    // pointer jumping until no pointer changes (2^34 > N steps at most)
-    const unsigned jb = (unsigned)std::min<uint64_t>(nbk(N, 256), 148ull * 8);
+    // pointer jumping until no pointer changes (2^34 > N steps at most): round 1 over every event,
+    // later rounds over the per-block lists of events whose pointer moved. The list buffers reuse the
+    // expanded instance ids (free after k_bl_ptr) and bl_pb.
+    CK(c.bl_seg.ensure(2ull * jb * 4));
+    uint32_t* lists[2] = {c.bl_inst.as<uint32_t>(), c.bl_pb.as<uint32_t>()};
+    uint32_t* segs[2] = {c.bl_seg.as<uint32_t>(), c.bl_seg.as<uint32_t>() + jb};
+    int cur = 0;
     while (n_act && rounds < 34) {
       CK(cudaMemsetAsync(changed, 0, 4, c.stream));
       launches += timed(c, "k_bl_jump", [&] {
-        k_bl_jump<<<jb, 256, 0, c.stream>>>(N, c.bl_pa.as<uint32_t>(), changed);
+        if (rounds == 0) k_bl_jump0<<<jb, JB_NT, 0, c.stream>>>(N, S, c.bl_pa.as<uint32_t>(), lists[0], segs[0], changed);
+        else k_bl_jumpk<<<jb, JB_NT, 0, c.stream>>>(S, c.bl_pa.as<uint32_t>(), lists[cur], segs[cur], lists[cur ^ 1],
+                                                    segs[cur ^ 1], changed);
         return 1;
       });
+      if (rounds > 0) cur ^= 1;
       ++rounds;
       unsigned int h = 0;
       CK(cudaMemcpyAsync(&h, changed, 4, cudaMemcpyDeviceToHost, c.stream));
