@@ -22,7 +22,10 @@ constexpr unsigned long long BL_NONE = ~0ull, BL_CYCLE = ~0ull - 1;
 struct BA {
   uint64_t n_tiles;
   const uint32_t* tile_rank; const uint64_t* tile_start; const uint64_t* rank_off;
+  // per comm event, comm order (inst_c / wait_c): event x of tile t is comm event
+  // comm_off[rank] + t_commpre[t] + (comm events of the tile before x)
   const uint16_t* kind; const uint32_t* inst; const uint32_t* wait; const uint4* rec;
+  const uint64_t* comm_off; const uint32_t* t_commpre;
   uint32_t* last_ev;  // per instance: the pointer target of its waiting members (EB2)
   uint32_t* ptr0;    // unused (null)
   uint16_t* rank16;  // per event: its rank if the event is a root of the ORIGINAL pointers, else 0xFFFF
@@ -38,9 +41,16 @@ __global__ void __launch_bounds__(256) k_bl_last(BA a) {
   const uint32_t r = a.tile_rank[tile];
   const uint64_t rs = a.rank_off[r];
   const uint64_t s = a.tile_start[tile], e = min(s + (uint64_t)TILE_EV, a.rank_off[r + 1]);
-  for (uint64_t x = s + lane_id(); x < e; x += 32) {
-    if ((a.kind[x] & 7u) == 0 || a.wait[x] != 0) continue;
-    const uint32_t I = a.inst[x];
+  const uint32_t lane = lane_id();
+  uint64_t ci0 = a.comm_off[r] + a.t_commpre[tile];  // comm index of the chunk's first comm event
+  for (uint64_t x0 = s; x0 < e; x0 += 32) {
+    const uint64_t x = x0 + lane;
+    const bool isc = x < e && (a.kind[x] & 7u) != 0;
+    const unsigned bm = __ballot_sync(0xFFFFFFFFu, isc);
+    const uint64_t ci = ci0 + __popc(bm & ((1u << lane) - 1u));
+    ci0 += __popc(bm);
+    if (!isc || a.wait[ci] != 0) continue;
+    const uint32_t I = a.inst[ci];
     const uint4 rc = a.rec[I];
     if ((rc.w & SCAN_F_VALID) && rc.z == r) a.last_ev[I] = (uint32_t)(x == rs ? x : x - 1);
   }
@@ -56,15 +66,40 @@ __global__ void __launch_bounds__(256) k_bl_ptr(BA a) {
     const uint32_t r = a.tile_rank[tile];
     const uint64_t rs = a.rank_off[r];
     const uint64_t s = a.tile_start[tile], e = min(s + (uint64_t)TILE_EV, a.rank_off[r + 1]);
-    for (uint64_t x = s + lane_id(); x < e; x += 32) {
-      const uint16_t ko = a.kind[x];
-      uint64_t p;
-      if ((ko & 7u) == 0) p = x;                                     // EB3: compute events are roots
-      else if (a.wait[x] > 0) p = a.last_ev[a.inst[x]];             // EB2: the last arriver's previous event
-      else p = x == rs ? x : x - 1;                                  // EB3: own previous event
-      a.ptr[x] = (uint32_t)p;
-      a.rank16[x] = p == x ? (uint16_t)r : (uint16_t)0xFFFFu;  // W <= 65535: 0xFFFF is no rank
-      n_act += p != x;
+    constexpr int U = 4;  // 4 x 32 events per step, every step's loads issued before they are used
+    const uint32_t lane = lane_id();
+    uint64_t ci0 = a.comm_off[r] + a.t_commpre[tile];
+    for (uint64_t xb = s; xb < e; xb += 32 * U) {  // warp-uniform bound (ballots below)
+      const uint64_t x0 = xb + lane;
+      uint16_t ko[U];
+      uint32_t wt[U], in[U];
+      uint64_t ci[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) { const uint64_t x = x0 + 32u * u; ko[u] = x < e ? a.kind[x] : (uint16_t)0; }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned bm = __ballot_sync(0xFFFFFFFFu, (ko[u] & 7u) != 0);
+        ci[u] = ci0 + __popc(bm & ((1u << lane) - 1u));
+        ci0 += __popc(bm);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) wt[u] = (ko[u] & 7u) ? a.wait[ci[u]] : 0u;
+#pragma unroll
+      for (int u = 0; u < U; ++u) in[u] = wt[u] > 0 ? a.inst[ci[u]] : 0u;
+#pragma unroll
+      for (int u = 0; u < U; ++u) in[u] = wt[u] > 0 ? a.last_ev[in[u]] : 0u;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t x = x0 + 32u * u;
+        if (x >= e) break;
+        uint64_t p;
+        if ((ko[u] & 7u) == 0) p = x;       // EB3: compute events are roots
+        else if (wt[u] > 0) p = in[u];      // EB2: the last arriver's previous event
+        else p = x == rs ? x : x - 1;       // EB3: own previous event
+        a.ptr[x] = (uint32_t)p;
+        a.rank16[x] = p == x ? (uint16_t)r : (uint16_t)0xFFFFu;  // W <= 65535: 0xFFFF is no rank
+        n_act += p != x;
+      }
     }
   }
   n_act = warp_sum_u32(n_act);
@@ -169,16 +204,39 @@ __global__ void __launch_bounds__(256) k_bl_sum(SA a) {
     unsigned long long suf = 0, slf = 0, una = 0;
     uint32_t run_r = 0xFFFFFFFFu;  // per-lane run of inflicted wait on one rank
     unsigned long long run_w = 0;
-    for (uint64_t base = s; base < e; base += 32) {
-      const uint64_t x = base + lane_id();
+    constexpr int U = 4;  // 4 x 32 events per step, the loads of a step issued together
+    const uint32_t lane = lane_id();
+    uint64_t ci0 = a.b.comm_off[r] + a.b.t_commpre[tile];
+    for (uint64_t base = s; base < e; base += 32 * U) {
+      uint32_t wv[U], pv[U], rv[U];
+      uint16_t ko[U];
+      uint64_t ci[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) { const uint64_t x = base + 32u * u + lane; ko[u] = x < e ? a.b.kind[x] : (uint16_t)0; }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned bm = __ballot_sync(0xFFFFFFFFu, (ko[u] & 7u) != 0);
+        ci[u] = ci0 + __popc(bm & ((1u << lane) - 1u));
+        ci0 += __popc(bm);
+      }
+      // the comm events' waits (comm order); compute events wait 0
+#pragma unroll
+      for (int u = 0; u < U; ++u) wv[u] = (ko[u] & 7u) ? a.b.wait[ci[u]] : 0u;
+#pragma unroll
+      for (int u = 0; u < U; ++u) pv[u] = wv[u] ? a.ptr[base + 32u * u + lane_id()] : 0u;
+#pragma unroll
+      for (int u = 0; u < U; ++u) rv[u] = wv[u] ? (uint32_t)a.b.rank16[pv[u]] : 0xFFFFu;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+      const uint64_t x = base + 32u * u + lane_id();
       if (x >= e) break;
-      const unsigned long long w = a.b.wait[x];  // EV_WAIT: 0 for compute events and invalid instances
+      const unsigned long long w = wv[u];  // EV_WAIT: 0 for compute events and invalid instances
       unsigned long long root = BL_NONE;
       if (w) {
-        const uint32_t p = a.ptr[x];
+        const uint32_t p = pv[u];
         ++nw;
         suf += w;
-        const uint32_t rr = a.b.rank16[p];  // one gather: the root's rank, or 0xFFFF (not a root: a cycle)
+        const uint32_t rr = rv[u];  // one gather: the root's rank, or 0xFFFF (not a root: a cycle)
         if (rr != 0xFFFFu) {  // a root of the original pointers
           root = p;
           if (rr == r) slf += w;
@@ -196,6 +254,7 @@ __global__ void __launch_bounds__(256) k_bl_sum(SA a) {
         }
       }
       a.root[x] = root;
+      }
     }
     if (run_w) { if (a.smem_hist) atomicAdd(&sh_inf[run_r], run_w); else atomicAdd(&a.inflicted[run_r], run_w); }
     suf = warp_sum_u64(suf); slf = warp_sum_u64(slf); una = warp_sum_u64(una);
@@ -231,22 +290,22 @@ scan_status blame_all(Ctx& c, scan_blame_result* out) {
     c.xwait_pending = false;
   }
   const uint64_t N1 = std::max<uint64_t>(N, 1);
-  // jumping lists (bl_inst reused after k_bl_ptr, bl_pb): jb block segments of S entries
+  // jumping lists (bl_inst, bl_pb): jb block segments of S entries
   const unsigned jb = (unsigned)std::min<uint64_t>(nbk(N, JB_NT), 148ull * 8);
   const uint64_t S = (N + (uint64_t)jb * JB_NT - 1) / ((uint64_t)jb * JB_NT) * JB_NT;  // elements per block in round 1
   const uint64_t LCAP = std::max<uint64_t>(N1, (uint64_t)jb * S);
-  CK(c.bl_inst.ensure(LCAP * 4)); CK(c.bl_wait.ensure(N1 * 4)); CK(c.bl_pa.ensure(N1 * 4));
+  CK(c.bl_inst.ensure(LCAP * 4)); CK(c.bl_pa.ensure(N1 * 4));
   CK(c.bl_pb.ensure(LCAP * 4)); CK(c.bl_root.ensure(N1 * 8)); CK(c.bl_rk.ensure(N1 * 2)); CK(c.bl_last.ensure(std::max<uint64_t>(c.n_inst, 1) * 4));
   CK(c.bl_rank.ensure(4 * W * 8 + 16 + 8));
   flush_fills(c);
   CK(cudaMemsetAsync(c.bl_rank.p, 0, 4 * W * 8 + 16 + 8, c.stream));
   int launches = 0;
-  launches += launch_expand_events(c, SCAN_OUT_EV_INST, c.bl_inst.p);
-  launches += launch_expand_events(c, SCAN_OUT_EV_WAIT, c.bl_wait.p);
+  // the blame kernels read the comm-order instance ids and waits directly (no event-order expansion)
   unsigned int* counters2 = reinterpret_cast<unsigned int*>(c.bl_rank.as<uint8_t>() + 4 * W * 8 + 16);  // [0] changed, [1] n_active
   BA b{c.n_tiles, c.tile_rank.as<uint32_t>(), c.tile_start.as<uint64_t>(), c.rank_off.as<uint64_t>(), c.d_kind,
-       c.bl_inst.as<uint32_t>(), c.bl_wait.as<uint32_t>(), c.inst_rec.as<uint4>(), c.bl_last.as<uint32_t>(),
-       nullptr, c.bl_rk.as<uint16_t>(), c.bl_pa.as<uint32_t>(), counters2 + 1};
+       c.inst_c.as<uint32_t>(), c.wait_c.as<uint32_t>(), c.inst_rec.as<uint4>(), c.r_comm_off.as<uint64_t>(),
+       c.t_commpre.as<uint32_t>(), c.bl_last.as<uint32_t>(), nullptr, c.bl_rk.as<uint16_t>(), c.bl_pa.as<uint32_t>(),
+       counters2 + 1};
   const unsigned tb = nbk(c.n_tiles, 8);
   uint32_t rounds = 0;
   unsigned int n_act = 0;
@@ -261,8 +320,7 @@ scan_status blame_all(Ctx& c, scan_blame_result* out) {
     CK(cudaMemcpyAsync(&n_act, counters2 + 1, 4, cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
     // pointer jumping until no pointer changes (2^34 > N steps at most): round 1 over every event,
-    // later rounds over the per-block lists of events whose pointer moved. The list buffers reuse the
-    // expanded instance ids (free after k_bl_ptr) and bl_pb.
+    // later rounds over the per-block lists of events whose pointer moved (list buffers bl_inst, bl_pb)
     CK(c.bl_seg.ensure(2ull * jb * 4));
     uint32_t* lists[2] = {c.bl_inst.as<uint32_t>(), c.bl_pb.as<uint32_t>()};
     uint32_t* segs[2] = {c.bl_seg.as<uint32_t>(), c.bl_seg.as<uint32_t>() + jb};
