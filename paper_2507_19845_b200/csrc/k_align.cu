@@ -18,6 +18,7 @@
 // communicator reachability, monotonicity (one CTA per rank), per-level anchors (one CTA per rank:
 // block scans keep program order and compact), per-level aligned ends, aligned starts, residuals.
 #include <algorithm>
+#include <cstdint>
 #include <sstream>
 #include "internal.cuh"
 
@@ -201,9 +202,33 @@ struct AnchorArgs {
   const long long* aend;  // aligned ends of earlier levels' candidates
   long long* tgt;         // [n_comm] scratch: target of a candidate, AL_NONE if none
   long long* anc_t; long long* anc_o; uint32_t* nanc;
+  const long long* imax;  // per instance: max aligned end over members of levels < k (k_al_instmax)
 };
 
-// AL3 targets for every candidate of the level-k ranks (AL_SPLIT CTAs per rank, fully parallel)
+// Per valid collective instance: the max aligned end over its members with 0 <= level < lim (AL3's
+// target for the members of level lim; lim = INT32_MAX: over every reached member, AL6). AL_SPLIT CTAs
+// per communicator, threads over its instances; a candidate event then reads its instance's value instead
+// of walking all members (an MP group of 64 ranks made that 64 x 64 reads per instance).
+__global__ void __launch_bounds__(256) k_al_instmax(AlArgs a, const int32_t* level, int32_t lim, const long long* aend,
+                                                    long long* out) {
+  const uint32_t ch = blockIdx.x;
+  const uint64_t b = a.ch_base[ch], nk = a.ch_base[ch + 1] - b;
+  const uint32_t nm = (uint32_t)(a.coff[ch + 1] - a.coff[ch]);
+  const uint32_t* mem = a.cmem + a.coff[ch];
+  for (uint64_t k = (uint64_t)blockIdx.y * blockDim.x + threadIdx.x; k < nk; k += (uint64_t)gridDim.y * blockDim.x) {
+    if (!(a.rec[b + k].w & SCAN_F_VALID)) continue;
+    const uint64_t s0 = a.ch_slot[ch] + k * nm;
+    long long v = AL_NONE;
+    for (uint32_t q = 0; q < nm; ++q) {
+      const int32_t lv = level[mem[q]];
+      if (lv >= 0 && lv < lim) v = max(v, aend[a.slotci[s0 + q]]);
+    }
+    out[b + k] = v;
+  }
+}
+
+// AL3 targets for every candidate of the level-k ranks (AL_SPLIT CTAs per rank, fully parallel): the
+// instance's max aligned end over members of lower levels (k_al_instmax)
 __global__ void __launch_bounds__(256) k_al_target(AnchorArgs A) {
   const AlArgs& a = A.a;
   const uint32_t r = A.ranks[blockIdx.x];
@@ -211,23 +236,8 @@ __global__ void __launch_bounds__(256) k_al_target(AnchorArgs A) {
   const uint64_t per = (c1 - c0 + AL_SPLIT - 1) / AL_SPLIT;
   const uint64_t b = c0 + per * blockIdx.y, e = min(c1, b + per);
   for (uint64_t ci = b + threadIdx.x; ci < e; ci += blockDim.x) {
-    long long tg = AL_NONE;
-    if (a.tend[ci] != AL_NONE) {
-      const uint32_t ch = a.cch[ci];
-      uint64_t kk, s0; uint32_t nm;
-      inst_slot(a, a.inst_c[ci], ch, kk, nm, s0);
-      bool have = false;
-      for (uint32_t q = 0; q < nm; ++q) {
-        const uint32_t m = a.cmem[a.coff[ch] + q];
-        const int32_t lv = A.level[m];
-        if (m == r || lv < 0 || lv >= A.k) continue;
-        const long long v = A.aend[a.slotci[s0 + q]];
-        if (!have || v > tg) tg = v;
-        have = true;
-      }
-      if (!have) tg = AL_NONE;
-    }
-    A.tgt[ci] = tg;
+    // own rank r is at level k, so the instance value (levels < k) excludes it
+    A.tgt[ci] = a.tend[ci] != AL_NONE ? A.imax[a.inst_c[ci]] : AL_NONE;
   }
 }
 
@@ -321,7 +331,7 @@ __global__ void __launch_bounds__(256) k_al_apply(uint64_t n_tiles, const uint32
 }
 
 // AL6 residuals: one CTA per reached rank, threads over its comm events
-__global__ void __launch_bounds__(256) k_al_residual(AlArgs a, const uint32_t* ranks, const int32_t* level,
+__global__ void __launch_bounds__(256) k_al_residual(AlArgs a, const uint32_t* ranks, const long long* imax,
                                                      const long long* aend, unsigned long long* resid) {
   __shared__ unsigned long long best;
   const uint32_t r = ranks[blockIdx.x];
@@ -332,14 +342,7 @@ __global__ void __launch_bounds__(256) k_al_residual(AlArgs a, const uint32_t* r
   const uint64_t b0 = c0 + per * blockIdx.y, e0 = min(c1, b0 + per);
   for (uint64_t ci = b0 + threadIdx.x; ci < e0; ci += blockDim.x) {
     if (a.tend[ci] == AL_NONE) continue;
-    const uint32_t ch = a.cch[ci];
-    uint64_t kk, s0; uint32_t nm;
-    inst_slot(a, a.inst_c[ci], ch, kk, nm, s0);
-    long long fin = AL_NONE;
-    for (uint32_t q = 0; q < nm; ++q) {
-      const uint32_t m = a.cmem[a.coff[ch] + q];
-      if (level[m] >= 0) fin = max(fin, aend[a.slotci[s0 + q]]);
-    }
+    const long long fin = imax[a.inst_c[ci]];  // the instance's max aligned end over reached members
     mine = max(mine, (unsigned long long)(fin - aend[ci]));
   }
   if (mine) atomicMax(&best, mine);
@@ -358,6 +361,7 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
   CK(c.al_flag.ensure(((c.n_comms + 3) & ~3u) + 4));  // per-comm flags, then the first bad rank (u32)
   CK(c.al_start.ensure(std::max<uint64_t>(c.N, 1) * 8)); CK(c.al_ranks.ensure(W * 4));
   CK(c.al_cch.ensure(std::max<uint64_t>(nc, 1) * 4)); CK(c.al_tgt.ensure(std::max<uint64_t>(nc, 1) * 8));
+  CK(c.al_imax.ensure(std::max<uint64_t>(c.p2p_inst0, 1) * 8));  // collective instances come first
   AlArgs a{c.tile_rank.as<uint32_t>(), c.tile_start.as<uint64_t>(), c.rank_off.as<uint64_t>(), c.d_kind, c.d_dur, c.d_start,
            c.N, c.n_tiles, c.t_commpre.as<uint32_t>(), c.r_comm_off.as<uint64_t>(), c.inst_c.as<uint32_t>(),
            c.inst_rec.as<uint4>(), c.ch_base.as<uint64_t>(), c.ch_slot.as<uint64_t>(), c.NCH, c.coff.as<uint64_t>(),
@@ -432,9 +436,16 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
   for (int32_t k = 1; k <= maxlev; ++k) {
     const uint32_t n = lvl_off[k + 1] - lvl_off[k];
     AnchorArgs A{a, c.al_ranks.as<uint32_t>() + lvl_off[k], c.al_level.as<int32_t>(), k, c.al_aend.as<long long>(),
-                 c.al_tgt.as<long long>(), c.al_anct.as<long long>(), c.al_anco.as<long long>(), c.al_nanc.as<uint32_t>()};
+                 c.al_tgt.as<long long>(), c.al_anct.as<long long>(), c.al_anco.as<long long>(), c.al_nanc.as<uint32_t>(),
+                 c.al_imax.as<long long>()};
     if (n) {
-      launches += timed(c, "k_al_target", [&] { k_al_target<<<dim3(n, AL_SPLIT), 256, 0, c.stream>>>(A); return 1; });
+      launches += timed(c, "k_al_target", [&] {
+        if (c.n_comms)
+          k_al_instmax<<<dim3(c.n_comms, AL_SPLIT), 256, 0, c.stream>>>(a, c.al_level.as<int32_t>(), k, c.al_aend.as<long long>(),
+                                                                        c.al_imax.as<long long>());
+        k_al_target<<<dim3(n, AL_SPLIT), 256, 0, c.stream>>>(A);
+        return 2;
+      });
       launches += timed(c, "k_al_anchor", [&] { k_al_anchor<<<n, AL_NT, 0, c.stream>>>(A); return 1; });
     }
     eval(k);
@@ -449,9 +460,12 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
     });
   if (nc && !by_level.empty())
     launches += timed(c, "k_al_residual", [&] {
-      k_al_residual<<<dim3((unsigned)by_level.size(), AL_SPLIT), 256, 0, c.stream>>>(a, c.al_ranks.as<uint32_t>(), c.al_level.as<int32_t>(),
+      if (c.n_comms)
+        k_al_instmax<<<dim3(c.n_comms, AL_SPLIT), 256, 0, c.stream>>>(a, c.al_level.as<int32_t>(), INT32_MAX,
+                                                                      c.al_aend.as<long long>(), c.al_imax.as<long long>());
+      k_al_residual<<<dim3((unsigned)by_level.size(), AL_SPLIT), 256, 0, c.stream>>>(a, c.al_ranks.as<uint32_t>(), c.al_imax.as<long long>(),
                                                                      c.al_aend.as<long long>(), c.al_resid.as<unsigned long long>());
-      return 1;
+      return 2;
     });
   std::vector<uint32_t> nanc(W);
   std::vector<uint64_t> resid(W);
