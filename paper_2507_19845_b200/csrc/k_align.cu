@@ -38,7 +38,16 @@ struct AlArgs {
   long long* tend;   // [n_comm] local end of a candidate (AL1), AL_NONE otherwise
   uint32_t* slotci;  // [n_slots] comm index of the member event of a candidate slot
   const uint32_t* comm; uint32_t* cch;  // event communicator id -> [n_comm] channel of a candidate
+  const uint32_t* vbits;  // one bit per instance: VALID (k_al_vbits; L2-resident, unlike the 16-byte records)
 };
+
+// VALID bit of every instance, packed 32 per word (a dense pass over the records)
+__global__ void k_al_vbits(uint64_t n_inst, const uint4* rec, uint32_t* vbits) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool v = i < n_inst && (rec[i].w & SCAN_F_VALID);
+  const unsigned bm = __ballot_sync(0xFFFFFFFFu, v);
+  if (lane_id() == 0 && i < n_inst) vbits[i >> 5] = bm;
+}
 
 // member slots of a collective instance: channel = communicator id (collective channels come first)
 __device__ __forceinline__ void inst_slot(const AlArgs& a, uint32_t inst, uint32_t ch, uint64_t& kk, uint32_t& nm, uint64_t& s0) {
@@ -80,7 +89,7 @@ __global__ void __launch_bounds__(256) k_al_ends(AlArgs a) {
       long long t = AL_NONE;
       if (k >= 1 && k <= 4) {
         const uint32_t inst = a.inst_c[ci];
-        if (a.rec[inst].w & SCAN_F_VALID) {
+        if ((a.vbits[inst >> 5] >> (inst & 31)) & 1u) {
           t = (long long)a.start[ev] + (long long)a.dur[ev];
           const uint32_t ch = a.comm[ev];
           uint64_t kk, s0; uint32_t nm;
@@ -362,11 +371,18 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
   CK(c.al_start.ensure(std::max<uint64_t>(c.N, 1) * 8)); CK(c.al_ranks.ensure(W * 4));
   CK(c.al_cch.ensure(std::max<uint64_t>(nc, 1) * 4)); CK(c.al_tgt.ensure(std::max<uint64_t>(nc, 1) * 8));
   CK(c.al_imax.ensure(std::max<uint64_t>(c.p2p_inst0, 1) * 8));  // collective instances come first
+  CK(c.al_vbits.ensure((c.n_inst + 31) / 32 * 4 + 4));
   AlArgs a{c.tile_rank.as<uint32_t>(), c.tile_start.as<uint64_t>(), c.rank_off.as<uint64_t>(), c.d_kind, c.d_dur, c.d_start,
            c.N, c.n_tiles, c.t_commpre.as<uint32_t>(), c.r_comm_off.as<uint64_t>(), c.inst_c.as<uint32_t>(),
            c.inst_rec.as<uint4>(), c.ch_base.as<uint64_t>(), c.ch_slot.as<uint64_t>(), c.NCH, c.coff.as<uint64_t>(),
-           c.cmem.as<uint32_t>(), c.al_tend.as<long long>(), c.al_slotci.as<uint32_t>(), c.d_comm, c.al_cch.as<uint32_t>()};
+           c.cmem.as<uint32_t>(), c.al_tend.as<long long>(), c.al_slotci.as<uint32_t>(), c.d_comm, c.al_cch.as<uint32_t>(),
+           c.al_vbits.as<uint32_t>()};
   int launches = 0;
+  if (c.n_inst)
+    launches += timed(c, "k_al_ends", [&] {
+      k_al_vbits<<<(unsigned)((c.n_inst + 255) / 256), 256, 0, c.stream>>>(c.n_inst, c.inst_rec.as<uint4>(), c.al_vbits.as<uint32_t>());
+      return 1;
+    });
   if (c.n_tiles) launches += timed(c, "k_al_ends", [&] { k_al_ends<<<(unsigned)((c.n_tiles + 7) / 8), 256, 0, c.stream>>>(a); return 1; });
   if (c.n_comms)
     launches += timed(c, "k_al_commflag", [&] {
