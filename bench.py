@@ -297,7 +297,20 @@ def json_io(ms, torch, local, stream, steps: int, warmup: int, cpu: bool) -> dic
                 "sample": f"oracle.chrome_json.parse of ranks 0-1's files ({nb_s / 1e6:.1f} MB, {t_.n_events} events), "
                           "Python json module, one core"}
     kern = {k: {"ms_per_call": round(v[0] / steps, 4), "launches": v[1]} for k, v in sorted(ik.items(), key=lambda kv: -kv[1][0])}
+    pk_j = float((json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}).get("hbm_gbs", 6650.0))
+    jp = ik.get("k_j_parse")
+    jp_ms = jp[0] / steps if jp else None
+    # k_j_parse reads every event object's text once and writes its columns (dur, kind_op, meta, comm,
+    # payload: 16 B, start_ns: 8 B)
+    jp_bytes = nbytes + 24 * int(res["n_events"])
+    roof = ({"bound": "hbm", "kernel": "k_j_parse", "bytes_per_call": jp_bytes, "achieved": jp_bytes / (jp_ms / 1e3) / 1e9,
+             "peak": pk_j, "unit": "GB/s", "frac": jp_bytes / (jp_ms / 1e3) / 1e9 / pk_j,
+             "call_frac": nbytes / (ims / 1e3) / 1e9 / pk_j,
+             "note": "k_j_parse: one thread per event object walking its bytes (latency-bound); call_frac: the "
+                     "whole call's JSON bytes over its time"} if jp_ms else None)
     return {"metric": "Chrome-trace JSON parsed into event columns per second (scan_ingest_json)",
+            "roofline": roof,
             "value": nbytes / (ims / 1e3) / 1e9, "unit": "GB/s",
             "events_per_s": res["n_events"] / (ims / 1e3), "ms_per_call": ims, "json_bytes": nbytes,
             "events": int(res["n_events"]), "docs": int(len(off) - 1),
