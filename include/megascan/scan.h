@@ -251,8 +251,12 @@ scan_status scan_create_sharded_local(scan_ctx** out, int cuda_device, void* cud
    cycle, possible only in inconsistent traces) is unattributed (EB4). Each wait is blamed on the
    root's rank (EB5): BL_INFLICTED (on other ranks), BL_SELF, BL_UNATTRIBUTED, BL_SUFFERED; the
    whole loaded trace is one window (EB6). Requires a completed analysis (scan_analyze or
-   scan_localize). Errors: SCAN_E_ORDER, SCAN_E_UNSUPPORTED (stream / sharded context, >= 2^32-16
-   events), SCAN_E_OOM, SCAN_E_CUDA.                                                              */
+   scan_localize). On a sharded context (scan_create_sharded*) it is a collective call: each shard
+   follows its chains locally, the chains that leave its iteration block are resolved over the
+   earlier shards' per-rank tables (one all-gather), the per-rank sums are all-reduced, and
+   BL_ROOT holds job-wide event ids (rank-major over the whole job) for the shard's own events;
+   rounds / n_active are the shard's. Errors: SCAN_E_ORDER, SCAN_E_UNSUPPORTED (stream context,
+   >= 2^32-16-world events per GPU), SCAN_E_NCCL, SCAN_E_OOM, SCAN_E_CUDA.                       */
 typedef struct scan_blame_result {
     uint64_t n_waiting, n_cyclic;   /* waiting events; of them on a pointer cycle                     */
     uint64_t total_wait_ns;         /* sum of their waits                                             */

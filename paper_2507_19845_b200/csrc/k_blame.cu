@@ -30,6 +30,9 @@ struct BA {
   uint32_t* ptr0;    // unused (null)
   uint16_t* rank16;  // per event: its rank if the event is a root of the ORIGINAL pointers, else 0xFFFF
   uint32_t* ptr; unsigned int* n_active;  // working pointers (jumped in place), events that are not roots
+  // sharded context, shard > 0: a rank's first local event is not its job-wide first one; what precedes
+  // it is the rank's last event on the previous shard, pointer value N + rank (resolved across shards)
+  uint32_t ext; uint64_t N;
 };
 
 // A communication event waited iff its wait is > 0 (EB1): the wait is 0 for every member of an
@@ -52,7 +55,7 @@ __global__ void __launch_bounds__(256) k_bl_last(BA a) {
     if (!isc || a.wait[ci] != 0) continue;
     const uint32_t I = a.inst[ci];
     const uint4 rc = a.rec[I];
-    if ((rc.w & SCAN_F_VALID) && rc.z == r) a.last_ev[I] = (uint32_t)(x == rs ? x : x - 1);
+    if ((rc.w & SCAN_F_VALID) && rc.z == r) a.last_ev[I] = (uint32_t)(x != rs ? x - 1 : (a.ext ? a.N + r : x));
   }
 }
 
@@ -95,7 +98,7 @@ __global__ void __launch_bounds__(256) k_bl_ptr(BA a) {
         uint64_t p;
         if ((ko[u] & 7u) == 0) p = x;       // EB3: compute events are roots
         else if (wt[u] > 0) p = in[u];      // EB2: the last arriver's previous event
-        else p = x == rs ? x : x - 1;       // EB3: own previous event
+        else p = x != rs ? x - 1 : (a.ext ? a.N + r : x);  // EB3: own previous event
         a.ptr[x] = (uint32_t)p;
         a.rank16[x] = p == x ? (uint16_t)r : (uint16_t)0xFFFFu;  // W <= 65535: 0xFFFF is no rank
         n_act += p != x;
@@ -142,9 +145,9 @@ __device__ __forceinline__ void jb_append(bool act, uint32_t x, uint32_t* out, u
   nout += tot;
 }
 
-__device__ __forceinline__ bool jb_step(uint32_t* ptr, uint32_t x) {
+__device__ __forceinline__ bool jb_step(uint32_t* ptr, uint32_t x, uint64_t N) {
   const uint32_t p = ptr[x];
-  if (p == x) return false;
+  if (p == x || p >= N) return false;  // a root, or a rank's entry from the previous shard (terminal here)
   const uint32_t q = ptr[p];
   if (q == p) return false;
   ptr[x] = q;
@@ -158,14 +161,15 @@ __global__ void __launch_bounds__(JB_NT) k_bl_jump0(uint64_t N, uint64_t S, uint
   uint32_t nout = 0;
   for (uint64_t c0 = (uint64_t)blockIdx.x * JB_NT; c0 < N; c0 += (uint64_t)gridDim.x * JB_NT) {
     const uint64_t x = c0 + threadIdx.x;
-    const bool act = x < N && jb_step(ptr, (uint32_t)x);
+    const bool act = x < N && jb_step(ptr, (uint32_t)x, N);
     jb_append(act, (uint32_t)x, out, nout, wcnt);
   }
   if (threadIdx.x == 0) { seg_out[blockIdx.x] = nout; if (nout) atomicOr(changed, 1u); }
 }
 
-__global__ void __launch_bounds__(JB_NT) k_bl_jumpk(uint64_t S, uint32_t* ptr, const uint32_t* list_in, const uint32_t* seg_in,
-                                                    uint32_t* list_out, uint32_t* seg_out, unsigned int* changed) {
+__global__ void __launch_bounds__(JB_NT) k_bl_jumpk(uint64_t N, uint64_t S, uint32_t* ptr, const uint32_t* list_in,
+                                                    const uint32_t* seg_in, uint32_t* list_out, uint32_t* seg_out,
+                                                    unsigned int* changed) {
   __shared__ uint32_t wcnt[JB_NT / 32];
   const uint32_t nin = seg_in[blockIdx.x];
   const uint32_t* in = list_in + (uint64_t)blockIdx.x * S;
@@ -175,7 +179,7 @@ __global__ void __launch_bounds__(JB_NT) k_bl_jumpk(uint64_t S, uint32_t* ptr, c
     const uint32_t i = i0 + threadIdx.x;
     uint32_t x = 0;
     bool act = false;
-    if (i < nin) { x = in[i]; act = jb_step(ptr, x); }
+    if (i < nin) { x = in[i]; act = jb_step(ptr, x, N); }
     jb_append(act, x, out, nout, wcnt);
   }
   if (threadIdx.x == 0) { seg_out[blockIdx.x] = nout; if (nout) atomicOr(changed, 1u); }
@@ -186,6 +190,9 @@ struct SA {
   unsigned long long* inflicted; unsigned long long* self_; unsigned long long* unattr; unsigned long long* suffered;
   unsigned long long* counts;  // [0] waiting events, [1] on a cycle
   int smem_hist;               // 1: inflicted wait accumulated in a shared-memory histogram over ranks
+  // sharded: job-wide event id of local event p of rank q = gbase[q] + p; ext[r] = the resolved root of
+  // pointer N + r: {id lo, id hi, rank, 1 = root / 0 = on a cycle}
+  const unsigned long long* gbase; const uint4* ext;
 };
 
 // Persistent over tiles (one warp per tile). Most waits of a job root on a few ranks, so the inflicted
@@ -225,7 +232,7 @@ __global__ void __launch_bounds__(256) k_bl_sum(SA a) {
 #pragma unroll
       for (int u = 0; u < U; ++u) pv[u] = wv[u] ? a.ptr[base + 32u * u + lane_id()] : 0u;
 #pragma unroll
-      for (int u = 0; u < U; ++u) rv[u] = wv[u] ? (uint32_t)a.b.rank16[pv[u]] : 0xFFFFu;
+      for (int u = 0; u < U; ++u) rv[u] = (wv[u] && pv[u] < a.b.N) ? (uint32_t)a.b.rank16[pv[u]] : 0xFFFFu;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
       const uint64_t x = base + 32u * u + lane_id();
@@ -236,9 +243,17 @@ __global__ void __launch_bounds__(256) k_bl_sum(SA a) {
         const uint32_t p = pv[u];
         ++nw;
         suf += w;
-        const uint32_t rr = rv[u];  // one gather: the root's rank, or 0xFFFF (not a root: a cycle)
+        uint32_t rr = rv[u];  // one gather: the root's rank, or 0xFFFF (not a root: a cycle)
+        unsigned long long rid = p;
+        if (p >= a.b.N) {  // the chain left the shard: its root, resolved on the earlier shards
+          const uint4 xe = a.ext[p - a.b.N];
+          rr = xe.w ? xe.z : 0xFFFFu;
+          rid = (unsigned long long)xe.y << 32 | xe.x;
+        } else if (a.gbase && rr != 0xFFFFu) {
+          rid = a.gbase[rr] + p;
+        }
         if (rr != 0xFFFFu) {  // a root of the original pointers
-          root = p;
+          root = rid;
           if (rr == r) slf += w;
           else {
             if (rr != run_r) {
@@ -278,11 +293,83 @@ __global__ void __launch_bounds__(256) k_bl_sum(SA a) {
 
 inline unsigned nbk(uint64_t n, unsigned t) { return (unsigned)std::max<uint64_t>(1, (n + t - 1) / t); }
 
+// Sharded blame: what the LAST local event of every rank resolves to after the local jumping, one row
+// of the all-gather: [4 r + 0..3] = {0 root: root rank, its offset within that rank's local events | 1
+// the rank's entry from the previous shard: rank | 2 on a cycle}, then [4 W + r] = local event count.
+// A rank without local events passes its entry through (type 1, itself).
+__global__ void k_bl_ltab(uint32_t W, uint64_t N, const uint64_t* rank_off, const uint32_t* ptr, const uint16_t* rank16,
+                          uint32_t* row) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= W) return;
+  const uint64_t b = rank_off[r], e = rank_off[r + 1];
+  uint32_t t = 1, v = r, k = 0;
+  if (e > b) {
+    const uint32_t p = ptr[e - 1];
+    if (p >= N) { t = 1; v = (uint32_t)(p - N); }
+    else if (rank16[p] != 0xFFFFu) { t = 0; v = rank16[p]; k = (uint32_t)(p - rank_off[rank16[p]]); }
+    else { t = 2; v = 0; }
+  }
+  row[4 * r] = t; row[4 * r + 1] = v; row[4 * r + 2] = k; row[4 * r + 3] = 0;
+  row[4 * W + r] = (uint32_t)(e - b);
+}
+
+// Sharded blame (collective): exchange every shard's per-rank table (k_bl_ltab) and resolve, for this
+// shard, where each rank's entry pointer (N + r) ends: follow the earlier shards' last events back until
+// a root, a cycle, or the rank's job-wide first event (a root). Job-wide event ids are rank-major over
+// the whole job (the unsharded numbering): id = job offset of the rank + its events on earlier shards +
+// the local offset.
+scan_status blame_shard_tables(Ctx& c, uint64_t N) {
+  const uint32_t W = (uint32_t)c.W, G = (uint32_t)c.n_shards, g = (uint32_t)c.shard;
+  const size_t row = 5 * (size_t)W;
+  CK(c.bl_xs.ensure(row * 4)); CK(c.bl_xr.ensure((size_t)G * row * 4));
+  CK(c.bl_gbase.ensure((size_t)W * 8)); CK(c.bl_ext.ensure((size_t)W * 16));
+  k_bl_ltab<<<nbk(W, 256), 256, 0, c.stream>>>(W, N, c.rank_off.as<uint64_t>(), c.bl_pa.as<uint32_t>(), c.bl_rk.as<uint16_t>(),
+                                                c.bl_xs.as<uint32_t>());
+  const int xr = xch_allgather(c, c.bl_xs.p, c.bl_xr.p, row);
+  if (xr) { c.err = std::string("blame exchange: ") + xch_error(xr); return SCAN_E_NCCL; }
+  std::vector<uint32_t> h((size_t)G * row);
+  CK(cudaMemcpyAsync(h.data(), c.bl_xr.p, h.size() * 4, cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  auto L = [&](uint32_t s, uint32_t r, int f) { return h[(size_t)s * row + 4 * (size_t)r + f]; };
+  auto cnt = [&](uint32_t s, uint32_t r) { return (uint64_t)h[(size_t)s * row + 4 * (size_t)W + r]; };
+  std::vector<uint64_t> jro(W + 1, 0), pre((size_t)G * W, 0);
+  for (uint32_t r = 0; r < W; ++r) {
+    uint64_t t = 0;
+    for (uint32_t s = 0; s < G; ++s) { pre[(size_t)s * W + r] = t; t += cnt(s, r); }
+    jro[r + 1] = jro[r] + t;
+  }
+  auto gid = [&](uint32_t s, uint32_t r, uint64_t k) { return jro[r] + pre[(size_t)s * W + r] + k; };
+  std::vector<uint64_t> gb(W);
+  std::vector<uint32_t> ext((size_t)W * 4, 0);
+  for (uint32_t r = 0; r < W; ++r) {
+    gb[r] = gid(g, r, 0) - c.h_rank_off[r];  // + local event index (wraps, then adds back)
+    uint32_t rr = r, from = g;
+    int64_t s = (int64_t)g - 1;
+    uint64_t root = 0;
+    uint32_t rrk = 0, ok = 1;
+    for (;;) {
+      if (s < 0) { root = gid(from, rr, 0); rrk = rr; break; }  // the rank's job-wide first event: a root
+      if (cnt((uint32_t)s, rr) == 0) { --s; continue; }       // no events of the rank on shard s
+      const uint32_t t = L((uint32_t)s, rr, 0);
+      if (t == 0) { rrk = L((uint32_t)s, rr, 1); root = gid((uint32_t)s, rrk, L((uint32_t)s, rr, 2)); break; }
+      if (t == 2) { ok = 0; break; }
+      from = (uint32_t)s; rr = L((uint32_t)s, rr, 1); --s;  // shard s's first event of rank rr: go on before it
+    }
+    ext[4 * (size_t)r] = (uint32_t)root; ext[4 * (size_t)r + 1] = (uint32_t)(root >> 32);
+    ext[4 * (size_t)r + 2] = rrk; ext[4 * (size_t)r + 3] = ok;
+  }
+  CK(cudaMemcpyAsync(c.bl_gbase.p, gb.data(), (size_t)W * 8, cudaMemcpyHostToDevice, c.stream));
+  CK(cudaMemcpyAsync(c.bl_ext.p, ext.data(), (size_t)W * 16, cudaMemcpyHostToDevice, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  return SCAN_OK;
+}
+
 }  // namespace
 
 scan_status blame_all(Ctx& c, scan_blame_result* out) {
   const uint64_t N = c.N, W = c.W;
-  if (N >= 0xFFFFFFF0ull) { c.err = "event-level blame supports < 2^32 - 16 events"; return SCAN_E_UNSUPPORTED; }
+  const bool sharded = c.n_shards > 1;
+  if (N + W >= 0xFFFFFFF0ull) { c.err = "event-level blame supports < 2^32 - 16 - world events per GPU"; return SCAN_E_UNSUPPORTED; }
   scan_status st = ensure_tiles(c);
   if (st) return st;
   if (c.xwait_pending) {  // comm-order view of the cross-stage waits
@@ -305,7 +392,7 @@ scan_status blame_all(Ctx& c, scan_blame_result* out) {
   BA b{c.n_tiles, c.tile_rank.as<uint32_t>(), c.tile_start.as<uint64_t>(), c.rank_off.as<uint64_t>(), c.d_kind,
        c.inst_c.as<uint32_t>(), c.wait_c.as<uint32_t>(), c.inst_rec.as<uint4>(), c.r_comm_off.as<uint64_t>(),
        c.t_commpre.as<uint32_t>(), c.bl_last.as<uint32_t>(), nullptr, c.bl_rk.as<uint16_t>(), c.bl_pa.as<uint32_t>(),
-       counters2 + 1};
+       counters2 + 1, (sharded && c.shard > 0) ? 1u : 0u, N};
   const unsigned tb = nbk(c.n_tiles, 8);
   uint32_t rounds = 0;
   unsigned int n_act = 0;
@@ -329,7 +416,7 @@ scan_status blame_all(Ctx& c, scan_blame_result* out) {
       CK(cudaMemsetAsync(changed, 0, 4, c.stream));
       launches += timed(c, "k_bl_jump", [&] {
         if (rounds == 0) k_bl_jump0<<<jb, JB_NT, 0, c.stream>>>(N, S, c.bl_pa.as<uint32_t>(), lists[0], segs[0], changed);
-        else k_bl_jumpk<<<jb, JB_NT, 0, c.stream>>>(S, c.bl_pa.as<uint32_t>(), lists[cur], segs[cur], lists[cur ^ 1],
+        else k_bl_jumpk<<<jb, JB_NT, 0, c.stream>>>(N, S, c.bl_pa.as<uint32_t>(), lists[cur], segs[cur], lists[cur ^ 1],
                                                     segs[cur ^ 1], changed);
         return 1;
       });
@@ -342,11 +429,25 @@ scan_status blame_all(Ctx& c, scan_blame_result* out) {
     }
     unsigned long long* R = c.bl_rank.as<unsigned long long>();
     const bool sh = W * 8 <= 96 * 1024;
-    SA sa{b, (uint32_t)W, src, c.bl_root.as<unsigned long long>(), R, R + W, R + 2 * W, R + 3 * W, R + 4 * W, sh ? 1 : 0};
+    SA sa{b, (uint32_t)W, src, c.bl_root.as<unsigned long long>(), R, R + W, R + 2 * W, R + 3 * W, R + 4 * W, sh ? 1 : 0,
+          nullptr, nullptr};
+    if (sharded) {  // the chains that leave the shard: resolved over the earlier shards' per-rank tables
+      if ((st = blame_shard_tables(c, N))) return st;
+      sa.gbase = c.bl_gbase.as<unsigned long long>(); sa.ext = c.bl_ext.as<uint4>();
+      launches += 1;
+    }
     const size_t smem = sh ? W * 8 : 0;
     if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_bl_sum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const unsigned sb = (unsigned)std::min<uint64_t>(tb, 148ull * 4);
     launches += timed(c, "k_bl_sum", [&] { k_bl_sum<<<sb, 256, smem, c.stream>>>(sa); return 1; });
+  } else if (sharded) {  // no local events: still take part in the exchange
+    if ((st = blame_shard_tables(c, 0))) return st;
+  }
+  if (sharded) {  // job-wide per-rank sums and counters
+    xch_group_start(c);
+    xch_allreduce(c, c.bl_rank.p, 4 * W + 2, XU64);
+    const int xr = xch_group_end(c);
+    if (xr) { c.err = std::string("blame all-reduce: ") + xch_error(xr); return SCAN_E_NCCL; }
   }
   c.launches += launches;
   std::vector<unsigned long long> h(4 * W + 2);
@@ -375,7 +476,8 @@ extern "C" scan_status scan_blame(scan_ctx* ctx, scan_blame_result* out) {
   if (!ctx) return SCAN_E_INVALID_ARG;
   Ctx& c = ctx->c;
   CK(cudaSetDevice(c.device));
-  if (c.stream_mode || c.n_shards > 1) { c.err = "event-level blame is unavailable on stream / sharded contexts"; return SCAN_E_UNSUPPORTED; }
+  // sharded contexts: a collective call (every shard), job-wide per-rank sums and event ids
+  if (c.stream_mode) { c.err = "event-level blame is unavailable on stream contexts"; return SCAN_E_UNSUPPORTED; }
   if (!c.localized) { c.err = "scan_blame needs a completed analysis (scan_analyze or scan_localize)"; return SCAN_E_ORDER; }
   return blame_all(c, out);
 }

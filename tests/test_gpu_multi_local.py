@@ -139,3 +139,62 @@ def test_local_shards_emit_merges_to_the_whole_document(G):
     merged.sort(key=lambda x: x[0])
     assert len(merged) == len(ref)
     assert [ev for _, ev in merged] == ref
+
+
+@pytest.mark.parametrize("G", [2, 3])
+@pytest.mark.parametrize("cfgname", ["c2", "c5"])
+def test_local_shards_blame_equals_the_oracle(G, cfgname):
+    """scan_blame on a sharded context (collective): chains that leave a shard's iteration block are
+    resolved over the earlier shards' per-rank tables; per-rank sums are job-wide and each shard's
+    BL_ROOT holds job-wide event ids for its own events -- merged, bit-exact against oracle.blame on
+    the whole trace (EB1-EB6)."""
+    import paper_2507_19845_b200 as ms
+    import torch
+    from tracegen import configs
+    cfg = configs.c2(iterations=6) if cfgname == "c2" else configs.c5(iterations=6)
+    full = tg.generate(cfg)
+    o = oracle.blame(full, oracle.Config())
+    group = ms.LocalGroup(G)
+    streams = [torch.cuda.Stream(0) for _ in range(G)]
+    scans = [ms.Scan(0, streams[g].cuda_stream, shards=(G, g, group)) for g in range(G)]
+    slices = []
+    for g in range(G):
+        b, e = ms.shard_iterations(cfg.iterations, G, g)
+        slices.append(ms.slice_iterations(full, b, e))
+    outs, errs = [None] * G, []
+
+    def work(g):
+        try:
+            scans[g].load(slices[g])
+            scans[g].analyze()
+            res = scans[g].blame()
+            outs[g] = (res, {k: scans[g].export(k) for k in ("bl_root", "bl_inflicted", "bl_self", "bl_unattributed",
+                                                               "bl_suffered")})
+        except ms.ScanError as x:
+            errs.append((g, x.status, str(x)))
+
+    th = [threading.Thread(target=work, args=(g,)) for g in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for s in scans:
+        s.close()
+    group.close()
+    assert not errs, errs
+    for g in range(G):
+        res, ex = outs[g]
+        for k in ("bl_inflicted", "bl_self", "bl_unattributed", "bl_suffered"):
+            assert np.array_equal(ex[k], o[k]), (g, k)
+        assert res["n_waiting"] == o["bl_n_waiting"] and res["n_cyclic"] == o["bl_n_cyclic"]
+        top = int(np.argmax(o["bl_inflicted"])) if o["bl_inflicted"].any() else 0xFFFFFFFF
+        assert res["top_rank"] == top
+    # job event order: rank-major, each rank's events shard after shard
+    parts = []
+    for r in range(full.world):
+        for g in range(G):
+            ro = np.asarray(slices[g].rank_offsets)
+            parts.append(outs[g][1]["bl_root"][int(ro[r]):int(ro[r + 1])])
+    root = np.concatenate(parts)
+    bad = np.nonzero(root != o["bl_root"])[0]
+    assert len(bad) == 0, f"bl_root: {len(bad)} diffs, first {bad[:5]}: gpu {root[bad[:5]]} oracle {o['bl_root'][bad[:5]]}"
