@@ -197,9 +197,12 @@ scan_status scan_nccl_unique_id(uint8_t out[128]);
    AL4 offset(t) piecewise linear between anchors (floor of the exact rational), constant outside.
    AL5 aligned start = start + offset(start); ranks not reached keep their clock (level -1).
    Requires: a completed scan_analyze (or scan_match_collectives) and start_ns given at load.
-   Outputs SCAN_OUT_AL_*. Errors: SCAN_E_ORDER (no instances yet), SCAN_E_INVALID_ARG (no
-   start_ns, reference out of range), SCAN_E_UNSUPPORTED (collective end times decrease along a
-   rank's program order; sharded context), SCAN_E_OOM, SCAN_E_CUDA.                            */
+   Outputs SCAN_OUT_AL_*. On a sharded context (scan_create_sharded*) it is a collective call:
+   AL_START covers the shard's own events, AL_LEVEL / AL_NANCHOR / AL_RESIDUAL and the result are
+   job-wide (small all-gathers between the shards). Errors: SCAN_E_ORDER (no
+   instances yet), SCAN_E_INVALID_ARG (no start_ns, reference out of range), SCAN_E_UNSUPPORTED
+   (collective end times decrease along a rank's program order), SCAN_E_NCCL, SCAN_E_OOM,
+   SCAN_E_CUDA.                                                                                  */
 typedef struct scan_align_config { int32_t reference; uint32_t reserved; } scan_align_config;
 typedef struct scan_align_result {
     uint64_t n_anchors;

@@ -18,6 +18,7 @@
 // communicator reachability, monotonicity (one CTA per rank), per-level anchors (one CTA per rank:
 // block scans keep program order and compact), per-level aligned ends, aligned starts, residuals.
 #include <algorithm>
+#include <climits>
 #include <cstdint>
 #include <sstream>
 #include "internal.cuh"
@@ -39,6 +40,7 @@ struct AlArgs {
   uint32_t* slotci;  // [n_slots] comm index of the member event of a candidate slot
   const uint32_t* comm; uint32_t* cch;  // event communicator id -> [n_comm] channel of a candidate
   const uint32_t* vbits;  // one bit per instance: VALID (k_al_vbits; L2-resident, unlike the 16-byte records)
+  const uint32_t* nmax;   // per channel: this context's occurrences (a shard's range starts at ch_base)
 };
 
 // VALID bit of every instance, packed 32 per word (a dense pass over the records)
@@ -106,11 +108,11 @@ __global__ void __launch_bounds__(256) k_al_ends(AlArgs a) {
 }
 
 // communicators with at least one valid instance connect their members (AL2)
-__global__ void k_al_commflag(uint32_t n_comms, const uint64_t* ch_base, const uint4* rec, uint8_t* flag) {
+__global__ void k_al_commflag(uint32_t n_comms, const uint64_t* ch_base, const uint32_t* nmax, const uint4* rec, uint8_t* flag) {
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n_comms) return;
   uint8_t f = 0;
-  for (uint64_t i = ch_base[c]; i < ch_base[c + 1] && !f; ++i) f = (rec[i].w & SCAN_F_VALID) ? 1 : 0;
+  for (uint64_t i = ch_base[c]; i < ch_base[c] + nmax[c] && !f; ++i) f = (rec[i].w & SCAN_F_VALID) ? 1 : 0;
   flag[c] = f;
 }
 
@@ -163,12 +165,35 @@ __global__ void __launch_bounds__(AL_NT) k_al_mono(const uint64_t* r_comm_off, c
   }
 }
 
-// index of the last anchor with at[i] <= t (-1 if none): binary search
-__device__ __forceinline__ int32_t al_find(const long long* at, uint32_t n, long long t) {
-  uint32_t lo = 0, hi = n;
+// A rank's anchors as one context sees them: its own list (PlainAnc), or (sharded, BndAnc) its own list
+// between the rank's last anchor on an earlier shard and its first anchor on a later one (AL_NONE: none)
+struct PlainAnc {
+  const long long* at; const long long* ao; uint32_t n;
+  __device__ __forceinline__ uint32_t size() const { return n; }
+  __device__ __forceinline__ long long t(uint32_t i) const { return at[i]; }
+  __device__ __forceinline__ long long o(uint32_t i) const { return ao[i]; }
+};
+struct BndAnc {
+  const long long* at; const long long* ao; uint32_t n;
+  long long pt, po, nt, no;
+  __device__ __forceinline__ uint32_t size() const { return n + (pt != AL_NONE) + (nt != AL_NONE); }
+  __device__ __forceinline__ long long t(uint32_t i) const {
+    if (pt != AL_NONE) { if (i == 0) return pt; --i; }
+    return i < n ? at[i] : nt;
+  }
+  __device__ __forceinline__ long long o(uint32_t i) const {
+    if (pt != AL_NONE) { if (i == 0) return po; --i; }
+    return i < n ? ao[i] : no;
+  }
+};
+
+// index of the last anchor with t(i) <= t (-1 if none): binary search
+template <class A>
+__device__ __forceinline__ int32_t al_find(const A& v, long long t) {
+  uint32_t lo = 0, hi = v.size();
   while (lo < hi) {
     const uint32_t m = (lo + hi) >> 1;
-    if (at[m] <= t) lo = m + 1; else hi = m;
+    if (v.t(m) <= t) lo = m + 1; else hi = m;
   }
   return (int32_t)lo - 1;
 }
@@ -187,19 +212,28 @@ __device__ __forceinline__ __int128 floor_div128(__int128 num, __int128 den) {
   while (r >= den) { q += 1; r -= den; }
   return q;
 }
-// offset at t given i = al_find(at, n, t): AL4
-__device__ __forceinline__ long long al_offset_at(const long long* at, const long long* ao, uint32_t n, int32_t i, long long t) {
+// offset at t given i = al_find(v, t): AL4
+template <class A>
+__device__ __forceinline__ long long al_offset_at(const A& v, int32_t i, long long t) {
+  const uint32_t n = v.size();
   if (n == 0) return 0;
-  if (i < 0) return ao[0];
-  if ((uint32_t)i >= n - 1) return ao[n - 1];
-  const __int128 o0 = ao[i], o1 = ao[i + 1], t0 = at[i], t1 = at[i + 1];
+  if (i < 0) return v.o(0);
+  if ((uint32_t)i >= n - 1) return v.o(n - 1);
+  const __int128 o0 = v.o(i), o1 = v.o(i + 1), t0 = v.t(i), t1 = v.t(i + 1);
   return (long long)(o0 + floor_div128((o1 - o0) * ((__int128)t - t0), t1 - t0));
 }
 // advance i to the interval of t when t did not decrease (program-order walk), else search
-__device__ __forceinline__ int32_t al_walk(const long long* at, uint32_t n, int32_t i, long long tprev, long long t) {
-  if (t < tprev) return al_find(at, n, t);
-  while (i + 1 < (int32_t)n && at[i + 1] <= t) ++i;
+template <class A>
+__device__ __forceinline__ int32_t al_walk(const A& v, int32_t i, long long tprev, long long t) {
+  if (t < tprev) return al_find(v, t);
+  const int32_t n = (int32_t)v.size();
+  while (i + 1 < n && v.t(i + 1) <= t) ++i;
   return i;
+}
+template <bool SH>
+__device__ __forceinline__ auto rank_anchors(const long long* at, const long long* ao, uint32_t n, const long long* bnd, uint32_t r) {
+  if constexpr (SH) return BndAnc{at, ao, n, bnd[4 * r], bnd[4 * r + 1], bnd[4 * r + 2], bnd[4 * r + 3]};
+  else return PlainAnc{at, ao, n};
 }
 
 constexpr uint32_t AL_SPLIT = 16;  // CTAs per rank in the per-rank passes (blockIdx.y)
@@ -212,6 +246,7 @@ struct AnchorArgs {
   long long* tgt;         // [n_comm] scratch: target of a candidate, AL_NONE if none
   long long* anc_t; long long* anc_o; uint32_t* nanc;
   const long long* imax;  // per instance: max aligned end over members of levels < k (k_al_instmax)
+  const long long* init;  // sharded: per rank, the largest candidate end with a target on earlier shards (dedupe)
 };
 
 // Per valid collective instance: the max aligned end over its members with 0 <= level < lim (AL3's
@@ -221,7 +256,7 @@ struct AnchorArgs {
 __global__ void __launch_bounds__(256) k_al_instmax(AlArgs a, const int32_t* level, int32_t lim, const long long* aend,
                                                     long long* out) {
   const uint32_t ch = blockIdx.x;
-  const uint64_t b = a.ch_base[ch], nk = a.ch_base[ch + 1] - b;
+  const uint64_t b = a.ch_base[ch], nk = a.nmax[ch];
   const uint32_t nm = (uint32_t)(a.coff[ch + 1] - a.coff[ch]);
   const uint32_t* mem = a.cmem + a.coff[ch];
   for (uint64_t k = (uint64_t)blockIdx.y * blockDim.x + threadIdx.x; k < nk; k += (uint64_t)gridDim.y * blockDim.x) {
@@ -260,7 +295,7 @@ __global__ void __launch_bounds__(AL_NT) k_al_anchor(AnchorArgs A) {
   __shared__ uint32_t n_anc;
   const uint32_t r = A.ranks[blockIdx.x];
   const uint64_t c0 = a.r_comm_off[r], c1 = a.r_comm_off[r + 1];
-  if (threadIdx.x == 0) { last_t = AL_NONE; n_anc = 0; }
+  if (threadIdx.x == 0) { last_t = A.init ? A.init[r] : AL_NONE; n_anc = 0; }
   __syncthreads();
   for (uint64_t b = c0; b < c1; b += AL_NT) {
     const uint64_t ci = b + threadIdx.x;
@@ -286,14 +321,14 @@ __global__ void __launch_bounds__(AL_NT) k_al_anchor(AnchorArgs A) {
 // aligned ends of the candidates of level-k ranks (level 0: the reference, offset 0): one CTA per
 // rank; a warp takes 1024-event chunks, lane l the events l, l+32, ... (coalesced), one interval
 // search per lane and chunk, then a walk (candidate ends are non-decreasing)
+template <bool SH>
 __global__ void __launch_bounds__(256) k_al_eval(const uint32_t* ranks, const uint64_t* r_comm_off, const long long* tend,
                                                  const long long* anc_t, const long long* anc_o, const uint32_t* nanc,
-                                                 long long* aend) {
+                                                 const long long* bnd, long long* aend) {
   const uint32_t r = ranks[blockIdx.x];
   const uint64_t c0 = r_comm_off[r], c1 = r_comm_off[r + 1];
-  const long long* at = anc_t + c0;
-  const long long* ao = anc_o + c0;
-  const uint32_t n = nanc[r], lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const auto A = rank_anchors<SH>(anc_t + c0, anc_o + c0, nanc[r], bnd, r);
+  const uint32_t lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint32_t part = blockIdx.y, warp_g = part * nw + wid, nwg = nw * gridDim.y;
   for (uint64_t b = c0 + 1024ull * warp_g; b < c1; b += 1024ull * nwg) {
     int32_t i = -2;
@@ -301,19 +336,20 @@ __global__ void __launch_bounds__(256) k_al_eval(const uint32_t* ranks, const ui
     for (uint64_t ci = b + lane; ci < min(c1, b + 1024); ci += 32) {
       const long long t = tend[ci];
       if (t == AL_NONE) continue;
-      i = i == -2 ? al_find(at, n, t) : al_walk(at, n, i, tp, t);
+      i = i == -2 ? al_find(A, t) : al_walk(A, i, tp, t);
       tp = t;
-      aend[ci] = t + al_offset_at(at, ao, n, i, t);
+      aend[ci] = t + al_offset_at(A, i, t);
     }
   }
 }
 
 // AL5: aligned start of every event; one warp per 2048-event tile (rank known), a lane 8
 // consecutive events: one interval search, then a program-order walk
+template <bool SH>
 __global__ void __launch_bounds__(256) k_al_apply(uint64_t n_tiles, const uint32_t* tile_rank, const uint64_t* tile_start,
                                                   const uint64_t* rank_off, const uint64_t* r_comm_off, const int32_t* level,
                                                   const int64_t* start, const long long* anc_t, const long long* anc_o,
-                                                  const uint32_t* nanc, long long* out) {
+                                                  const uint32_t* nanc, const long long* bnd, long long* out) {
   const uint64_t tile = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (tile >= n_tiles) return;
   const uint32_t lane = lane_id();
@@ -322,9 +358,8 @@ __global__ void __launch_bounds__(256) k_al_apply(uint64_t n_tiles, const uint32
   const uint64_t e = min(s + (uint64_t)TILE_EV, rank_off[r + 1]);
   const bool on = level[r] >= 0;
   const uint64_t c0 = r_comm_off[r];
-  const long long* at = anc_t + c0;
-  const long long* ao = anc_o + c0;
-  const uint32_t n = on ? nanc[r] : 0u;
+  const auto A = rank_anchors<SH>(anc_t + c0, anc_o + c0, nanc[r], bnd, r);
+  const uint32_t n = on ? A.size() : 0u;
   for (uint64_t g = s + 8ull * lane; g < e; g += 256) {
     const uint64_t ge = min(g + 8, e);
     int32_t i = -2;
@@ -332,11 +367,55 @@ __global__ void __launch_bounds__(256) k_al_apply(uint64_t n_tiles, const uint32
     for (uint64_t ev = g; ev < ge; ++ev) {
       const long long t = start[ev];
       if (!on || n == 0) { out[ev] = t; continue; }
-      i = i == -2 ? al_find(at, n, t) : al_walk(at, n, i, tp, t);
+      i = i == -2 ? al_find(A, t) : al_walk(A, i, tp, t);
       tp = t;
-      out[ev] = t + al_offset_at(at, ao, n, i, t);
+      out[ev] = t + al_offset_at(A, i, t);
     }
   }
+}
+
+// ---- sharded alignment: per-rank values exchanged between the shards
+// first / last candidate end of every rank (non-decreasing along program order, so min / max)
+__global__ void __launch_bounds__(256) k_al_firstlast(const uint64_t* r_comm_off, const long long* tend, long long* out) {
+  __shared__ long long f, l;
+  const uint32_t r = blockIdx.x;
+  if (threadIdx.x == 0) { f = LLONG_MAX; l = AL_NONE; }
+  __syncthreads();
+  long long mn = LLONG_MAX, mx = AL_NONE;
+  for (uint64_t ci = r_comm_off[r] + threadIdx.x; ci < r_comm_off[r + 1]; ci += blockDim.x) {
+    const long long t = tend[ci];
+    if (t != AL_NONE) { mn = min(mn, t); mx = max(mx, t); }
+  }
+  atomicMin(&f, mn); atomicMax(&l, mx);
+  __syncthreads();
+  if (threadIdx.x == 0) { out[2 * r] = f == LLONG_MAX ? AL_NONE : f; out[2 * r + 1] = l; }
+}
+
+// per level-k rank: the largest end of a candidate that has a target (the anchor dedupe's carry)
+__global__ void __launch_bounds__(256) k_al_lastT(const uint32_t* ranks, const uint64_t* r_comm_off, const long long* tend,
+                                                  const long long* tgt, long long* out) {
+  __shared__ long long l;
+  const uint32_t r = ranks[blockIdx.x];
+  if (threadIdx.x == 0) l = AL_NONE;
+  __syncthreads();
+  long long mx = AL_NONE;
+  for (uint64_t ci = r_comm_off[r] + threadIdx.x; ci < r_comm_off[r + 1]; ci += blockDim.x)
+    if (tgt[ci] != AL_NONE) mx = max(mx, tend[ci]);
+  atomicMax(&l, mx);
+  __syncthreads();
+  if (threadIdx.x == 0) out[r] = l;
+}
+
+// per level-k rank: its first and last anchor (t, o), AL_NONE if it has none
+__global__ void k_al_bounds(uint32_t n, const uint32_t* ranks, const uint64_t* r_comm_off, const long long* anc_t,
+                            const long long* anc_o, const uint32_t* nanc, long long* out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t r = ranks[i];
+  const uint64_t c0 = r_comm_off[r];
+  const uint32_t m = nanc[r];
+  out[4 * r] = m ? anc_t[c0] : AL_NONE; out[4 * r + 1] = m ? anc_o[c0] : 0;
+  out[4 * r + 2] = m ? anc_t[c0 + m - 1] : AL_NONE; out[4 * r + 3] = m ? anc_o[c0 + m - 1] : 0;
 }
 
 // AL6 residuals: one CTA per reached rank, threads over its comm events
@@ -372,11 +451,14 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
   CK(c.al_cch.ensure(std::max<uint64_t>(nc, 1) * 4)); CK(c.al_tgt.ensure(std::max<uint64_t>(nc, 1) * 8));
   CK(c.al_imax.ensure(std::max<uint64_t>(c.p2p_inst0, 1) * 8));  // collective instances come first
   CK(c.al_vbits.ensure((c.n_inst + 31) / 32 * 4 + 4));
+  if (c.n_shards > 1) {
+    CK(c.al_lt.ensure(W * 8)); CK(c.al_init.ensure(W * 8)); CK(c.al_bx.ensure(W * 32)); CK(c.al_bnd.ensure(W * 32));
+  }
   AlArgs a{c.tile_rank.as<uint32_t>(), c.tile_start.as<uint64_t>(), c.rank_off.as<uint64_t>(), c.d_kind, c.d_dur, c.d_start,
            c.N, c.n_tiles, c.t_commpre.as<uint32_t>(), c.r_comm_off.as<uint64_t>(), c.inst_c.as<uint32_t>(),
            c.inst_rec.as<uint4>(), c.ch_base.as<uint64_t>(), c.ch_slot.as<uint64_t>(), c.NCH, c.coff.as<uint64_t>(),
            c.cmem.as<uint32_t>(), c.al_tend.as<long long>(), c.al_slotci.as<uint32_t>(), c.d_comm, c.al_cch.as<uint32_t>(),
-           c.al_vbits.as<uint32_t>()};
+           c.al_vbits.as<uint32_t>(), c.ch_nmax.as<uint32_t>()};
   int launches = 0;
   if (c.n_inst)
     launches += timed(c, "k_al_ends", [&] {
@@ -386,8 +468,8 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
   if (c.n_tiles) launches += timed(c, "k_al_ends", [&] { k_al_ends<<<(unsigned)((c.n_tiles + 7) / 8), 256, 0, c.stream>>>(a); return 1; });
   if (c.n_comms)
     launches += timed(c, "k_al_commflag", [&] {
-      k_al_commflag<<<(c.n_comms + 255) / 256, 256, 0, c.stream>>>(c.n_comms, c.ch_base.as<uint64_t>(), c.inst_rec.as<uint4>(),
-                                                                   c.al_flag.as<uint8_t>());
+      k_al_commflag<<<(c.n_comms + 255) / 256, 256, 0, c.stream>>>(c.n_comms, c.ch_base.as<uint64_t>(), c.ch_nmax.as<uint32_t>(),
+                                                                   c.inst_rec.as<uint4>(), c.al_flag.as<uint8_t>());
       return 1;
     });
   uint32_t* bad = reinterpret_cast<uint32_t*>(c.al_flag.as<uint8_t>() + ((c.n_comms + 3) & ~3u));
@@ -398,9 +480,54 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
   });
   std::vector<uint8_t> flag(c.n_comms + 8);
   uint32_t bad_rank = 0;
-  if (c.n_comms) CK(cudaMemcpyAsync(flag.data(), c.al_flag.p, c.n_comms, cudaMemcpyDeviceToHost, c.stream));
-  CK(cudaMemcpyAsync(&bad_rank, bad, 4, cudaMemcpyDeviceToHost, c.stream));
-  CK(cudaStreamSynchronize(c.stream));
+  const bool sh = c.n_shards > 1;
+  const uint32_t G = (uint32_t)c.n_shards, g = (uint32_t)c.shard;
+  // sharded: one all-gather of a per-shard row and the host reductions every shard makes alike
+  auto gather = [&](const void* src_dev, size_t n_u32, std::vector<uint32_t>& h) -> scan_status {
+    CK(c.al_xs.ensure(n_u32 * 4)); CK(c.al_xr.ensure((size_t)G * n_u32 * 4));
+    CK(cudaMemcpyAsync(c.al_xs.p, src_dev, n_u32 * 4, cudaMemcpyDeviceToDevice, c.stream));
+    const int xr = xch_allgather(c, c.al_xs.p, c.al_xr.p, n_u32);
+    if (xr) { c.err = std::string("alignment exchange: ") + xch_error(xr); return SCAN_E_NCCL; }
+    h.resize((size_t)G * n_u32);
+    CK(cudaMemcpyAsync(h.data(), c.al_xr.p, h.size() * 4, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    return SCAN_OK;
+  };
+  auto i64at = [](const std::vector<uint32_t>& h, size_t w) { return (long long)((uint64_t)h[w] | ((uint64_t)h[w + 1] << 32)); };
+  scan_status gst;
+  if (sh) {
+    // flags (padded to words) + first bad rank + per-rank first / last candidate end: communicators
+    // with a valid instance on any shard connect their members; ends must not decrease across shards
+    const size_t fw = ((size_t)c.n_comms + 3) / 4, fe = (fw + 2) & ~size_t(1);  // i64 part 8-byte aligned
+    const size_t rowu = fe + 4 * (size_t)W;
+    CK(c.al_row.ensure(rowu * 4));
+    CK(cudaMemcpyAsync(c.al_row.p, c.al_flag.p, fw * 4 + 4, cudaMemcpyDeviceToDevice, c.stream));
+    k_al_firstlast<<<(unsigned)W, 256, 0, c.stream>>>(c.r_comm_off.as<uint64_t>(), c.al_tend.as<long long>(),
+                                                      reinterpret_cast<long long*>(c.al_row.as<uint32_t>() + fe));
+    launches += 1;
+    std::vector<uint32_t> h;
+    if ((gst = gather(c.al_row.p, rowu, h))) return gst;
+    bad_rank = NONE32;
+    for (uint32_t q = 0; q < G; ++q) {
+      const uint8_t* fb = reinterpret_cast<const uint8_t*>(h.data() + (size_t)q * rowu);
+      for (uint32_t k = 0; k < c.n_comms; ++k) flag[k] |= fb[k];
+      bad_rank = std::min(bad_rank, h[(size_t)q * rowu + fw]);
+    }
+    for (uint64_t r = 0; r < W; ++r) {
+      long long prev = AL_NONE;
+      for (uint32_t q = 0; q < G; ++q) {
+        const size_t w = (size_t)q * rowu + fe + 4 * r;
+        const long long f = i64at(h, w), l = i64at(h, w + 2);
+        if (f == AL_NONE) continue;
+        if (prev != AL_NONE && f < prev) bad_rank = std::min<uint32_t>(bad_rank, (uint32_t)r);
+        prev = l;
+      }
+    }
+  } else {
+    if (c.n_comms) CK(cudaMemcpyAsync(flag.data(), c.al_flag.p, c.n_comms, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(&bad_rank, bad, 4, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+  }
   CK(cudaGetLastError());
   if (bad_rank != NONE32) {
     std::ostringstream m;
@@ -438,13 +565,20 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
   if ((st = upload(c, c.al_level, level)) || (st = upload(c, c.al_ranks, by_level))) return st;
   CK(cudaMemsetAsync(c.al_nanc.p, 0, W * 4, c.stream));
   CK(cudaMemsetAsync(c.al_resid.p, 0, W * 8, c.stream));
+  std::vector<long long> bnd(sh ? 4 * (size_t)W : 0);  // per rank: anchors on the neighbouring shards (sharded)
+  for (size_t i = 0; i < bnd.size(); i += 4) { bnd[i] = AL_NONE; bnd[i + 1] = 0; bnd[i + 2] = AL_NONE; bnd[i + 3] = 0; }
+  if (sh) CK(cudaMemcpyAsync(c.al_bnd.p, bnd.data(), W * 32, cudaMemcpyHostToDevice, c.stream));
   auto eval = [&](int32_t k) {
     const uint32_t n = lvl_off[k + 1] - lvl_off[k];
     if (nc && n)
       launches += timed(c, "k_al_eval", [&] {
-        k_al_eval<<<dim3(n, AL_SPLIT), 256, 0, c.stream>>>(c.al_ranks.as<uint32_t>() + lvl_off[k], c.r_comm_off.as<uint64_t>(),
-                                           c.al_tend.as<long long>(), c.al_anct.as<long long>(), c.al_anco.as<long long>(),
-                                           c.al_nanc.as<uint32_t>(), c.al_aend.as<long long>());
+        auto go = [&](auto kern) {
+          kern<<<dim3(n, AL_SPLIT), 256, 0, c.stream>>>(c.al_ranks.as<uint32_t>() + lvl_off[k], c.r_comm_off.as<uint64_t>(),
+                                                        c.al_tend.as<long long>(), c.al_anct.as<long long>(),
+                                                        c.al_anco.as<long long>(), c.al_nanc.as<uint32_t>(),
+                                                        c.al_bnd.as<long long>(), c.al_aend.as<long long>());
+        };
+        if (sh) go(k_al_eval<true>); else go(k_al_eval<false>);
         return 1;
       });
   };
@@ -453,7 +587,7 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
     const uint32_t n = lvl_off[k + 1] - lvl_off[k];
     AnchorArgs A{a, c.al_ranks.as<uint32_t>() + lvl_off[k], c.al_level.as<int32_t>(), k, c.al_aend.as<long long>(),
                  c.al_tgt.as<long long>(), c.al_anct.as<long long>(), c.al_anco.as<long long>(), c.al_nanc.as<uint32_t>(),
-                 c.al_imax.as<long long>()};
+                 c.al_imax.as<long long>(), nullptr};
     if (n) {
       launches += timed(c, "k_al_target", [&] {
         if (c.n_comms)
@@ -462,16 +596,56 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
         k_al_target<<<dim3(n, AL_SPLIT), 256, 0, c.stream>>>(A);
         return 2;
       });
+      if (sh) {  // the anchor dedupe carries over from the earlier shards: their largest candidate end
+        std::vector<long long> zero(W, AL_NONE);
+        CK(cudaMemcpyAsync(c.al_lt.p, zero.data(), W * 8, cudaMemcpyHostToDevice, c.stream));
+        k_al_lastT<<<n, 256, 0, c.stream>>>(A.ranks, c.r_comm_off.as<uint64_t>(), c.al_tend.as<long long>(),
+                                            c.al_tgt.as<long long>(), c.al_lt.as<long long>());
+        std::vector<uint32_t> h;
+        if ((gst = gather(c.al_lt.p, 2 * W, h))) return gst;
+        std::vector<long long> init(W, AL_NONE);
+        for (uint64_t r = 0; r < W; ++r)
+          for (uint32_t q = 0; q < g; ++q) init[r] = std::max(init[r], i64at(h, (size_t)q * 2 * W + 2 * r));
+        CK(cudaMemcpyAsync(c.al_init.p, init.data(), W * 8, cudaMemcpyHostToDevice, c.stream));
+        A.init = c.al_init.as<long long>();
+        launches += 1;
+      }
       launches += timed(c, "k_al_anchor", [&] { k_al_anchor<<<n, AL_NT, 0, c.stream>>>(A); return 1; });
+    }
+    if (sh && n) {  // the level-k ranks' neighbouring anchors on the other shards (interpolation across blocks)
+      k_al_bounds<<<(n + 255) / 256, 256, 0, c.stream>>>(n, A.ranks, c.r_comm_off.as<uint64_t>(), c.al_anct.as<long long>(),
+                                                         c.al_anco.as<long long>(), c.al_nanc.as<uint32_t>(),
+                                                         c.al_bx.as<long long>());
+      std::vector<uint32_t> h;
+      if ((gst = gather(c.al_bx.p, 8 * W, h))) return gst;
+      for (uint32_t i = lvl_off[k]; i < lvl_off[k + 1]; ++i) {
+        const uint32_t r = by_level[i];
+        long long* b = &bnd[4 * (size_t)r];
+        b[0] = AL_NONE; b[1] = 0; b[2] = AL_NONE; b[3] = 0;
+        for (int64_t q = (int64_t)g - 1; q >= 0; --q) {  // the last anchor of the nearest earlier shard that has one
+          const size_t w = (size_t)q * 8 * W + 8 * (size_t)r;
+          if (i64at(h, w + 4) != AL_NONE) { b[0] = i64at(h, w + 4); b[1] = i64at(h, w + 6); break; }
+        }
+        for (uint32_t q = g + 1; q < G; ++q) {  // the first anchor of the nearest later shard that has one
+          const size_t w = (size_t)q * 8 * W + 8 * (size_t)r;
+          if (i64at(h, w) != AL_NONE) { b[2] = i64at(h, w); b[3] = i64at(h, w + 2); break; }
+        }
+      }
+      CK(cudaMemcpyAsync(c.al_bnd.p, bnd.data(), W * 32, cudaMemcpyHostToDevice, c.stream));
+      CK(cudaStreamSynchronize(c.stream));
+      launches += 1;
     }
     eval(k);
   }
   if (c.n_tiles)
     launches += timed(c, "k_al_apply", [&] {
-      k_al_apply<<<(unsigned)((c.n_tiles + 7) / 8), 256, 0, c.stream>>>(
-          c.n_tiles, c.tile_rank.as<uint32_t>(), c.tile_start.as<uint64_t>(), c.rank_off.as<uint64_t>(),
-          c.r_comm_off.as<uint64_t>(), c.al_level.as<int32_t>(), c.d_start, c.al_anct.as<long long>(),
-          c.al_anco.as<long long>(), c.al_nanc.as<uint32_t>(), c.al_start.as<long long>());
+      auto go = [&](auto kern) {
+        kern<<<(unsigned)((c.n_tiles + 7) / 8), 256, 0, c.stream>>>(
+            c.n_tiles, c.tile_rank.as<uint32_t>(), c.tile_start.as<uint64_t>(), c.rank_off.as<uint64_t>(),
+            c.r_comm_off.as<uint64_t>(), c.al_level.as<int32_t>(), c.d_start, c.al_anct.as<long long>(),
+            c.al_anco.as<long long>(), c.al_nanc.as<uint32_t>(), c.al_bnd.as<long long>(), c.al_start.as<long long>());
+      };
+      if (sh) go(k_al_apply<true>); else go(k_al_apply<false>);
       return 1;
     });
   if (nc && !by_level.empty())
@@ -485,9 +659,29 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
     });
   std::vector<uint32_t> nanc(W);
   std::vector<uint64_t> resid(W);
-  CK(cudaMemcpyAsync(nanc.data(), c.al_nanc.p, W * 4, cudaMemcpyDeviceToHost, c.stream));
-  CK(cudaMemcpyAsync(resid.data(), c.al_resid.p, W * 8, cudaMemcpyDeviceToHost, c.stream));
-  CK(cudaStreamSynchronize(c.stream));
+  if (sh) {  // job-wide anchor counts (sum) and residuals (max); the exports hold the job's values
+    CK(c.al_row.ensure(W * 12));
+    CK(cudaMemcpyAsync(c.al_row.p, c.al_nanc.p, W * 4, cudaMemcpyDeviceToDevice, c.stream));
+    CK(cudaMemcpyAsync(c.al_row.as<uint32_t>() + W, c.al_resid.p, W * 8, cudaMemcpyDeviceToDevice, c.stream));
+    std::vector<uint32_t> h;
+    if ((gst = gather(c.al_row.p, 3 * W, h))) return gst;
+    for (uint64_t r = 0; r < W; ++r) {
+      uint32_t na = 0;
+      uint64_t rs = 0;
+      for (uint32_t q = 0; q < G; ++q) {
+        na += h[(size_t)q * 3 * W + r];
+        rs = std::max<uint64_t>(rs, (uint64_t)i64at(h, (size_t)q * 3 * W + W + 2 * r));
+      }
+      nanc[r] = na; resid[r] = rs;
+    }
+    CK(cudaMemcpyAsync(c.al_nanc.p, nanc.data(), W * 4, cudaMemcpyHostToDevice, c.stream));
+    CK(cudaMemcpyAsync(c.al_resid.p, resid.data(), W * 8, cudaMemcpyHostToDevice, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+  } else {
+    CK(cudaMemcpyAsync(nanc.data(), c.al_nanc.p, W * 4, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(resid.data(), c.al_resid.p, W * 8, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+  }
   CK(cudaGetLastError());
   resolve_timing(c);
   c.launches += launches;

@@ -198,3 +198,60 @@ def test_local_shards_blame_equals_the_oracle(G, cfgname):
     root = np.concatenate(parts)
     bad = np.nonzero(root != o["bl_root"])[0]
     assert len(bad) == 0, f"bl_root: {len(bad)} diffs, first {bad[:5]}: gpu {root[bad[:5]]} oracle {o['bl_root'][bad[:5]]}"
+
+
+@pytest.mark.parametrize("G", [2, 3])
+@pytest.mark.parametrize("cfgname,ref", [("c2", 0), ("c5", 0), ("c5", 77)])
+def test_local_shards_align_equals_the_oracle(G, cfgname, ref):
+    """scan_align on a sharded context (collective): BFS levels from the communicators valid on any
+    shard, the anchor dedupe carried across shards, interpolation between the anchors of neighbouring
+    shards; each shard's aligned starts merged in job order, and the job-wide levels, anchor counts and
+    residuals, bit-exact against oracle.align on the whole trace (AL1-AL6)."""
+    import paper_2507_19845_b200 as ms
+    import torch
+    from tracegen import configs
+    cfg = configs.c2(iterations=6) if cfgname == "c2" else configs.c5(iterations=6)
+    full = tg.generate(cfg)
+    o = oracle.align(full, ref)
+    assert o["al_status"] == 0
+    group = ms.LocalGroup(G)
+    streams = [torch.cuda.Stream(0) for _ in range(G)]
+    scans = [ms.Scan(0, streams[g].cuda_stream, shards=(G, g, group)) for g in range(G)]
+    slices = []
+    for g in range(G):
+        b, e = ms.shard_iterations(cfg.iterations, G, g)
+        slices.append(ms.slice_iterations(full, b, e))
+    outs, errs = [None] * G, []
+
+    def work(g):
+        try:
+            scans[g].load(slices[g], start=True)
+            scans[g].analyze()
+            res = scans[g].align(ref)
+            outs[g] = (res, {k: scans[g].export(k) for k in ms.ALIGN_OUTPUTS})
+        except ms.ScanError as x:
+            errs.append((g, x.status, str(x)))
+
+    th = [threading.Thread(target=work, args=(g,)) for g in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for s in scans:
+        s.close()
+    group.close()
+    assert not errs, errs
+    for g in range(G):
+        res, ex = outs[g]
+        for k in ("al_level", "al_nanchor", "al_residual"):
+            bad = np.nonzero(ex[k] != o[k])[0]
+            assert len(bad) == 0, f"shard {g} {k}: {len(bad)} diffs, first {bad[:5]}: gpu {ex[k][bad[:5]]} oracle {o[k][bad[:5]]}"
+        assert res["n_anchors"] == int(o["al_nanchor"].sum())
+    parts = []
+    for r in range(full.world):
+        for g in range(G):
+            ro = np.asarray(slices[g].rank_offsets)
+            parts.append(outs[g][1]["al_start"][int(ro[r]):int(ro[r + 1])])
+    st = np.concatenate(parts)
+    bad = np.nonzero(st != o["al_start"])[0]
+    assert len(bad) == 0, f"al_start: {len(bad)} diffs, first {bad[:5]}: gpu {st[bad[:5]]} oracle {o['al_start'][bad[:5]]}"
