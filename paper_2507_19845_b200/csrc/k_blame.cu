@@ -9,7 +9,8 @@
 //   k_bl_last   per instance: where its waiting members point -- the previous event of its last
 //               arriver's member event (that event itself if it is its rank's first)   (tile warps)
 //   k_bl_ptr    per event: the pointer (u32 event index)                      (tile warps)
-//   k_bl_jump   one jumping round, double-buffered, with a change flag
+//   k_bl_jump0 / k_bl_jumpk  one jumping round (in place; round 1 over every event, later rounds over the
+//               per-block lists of pointers that moved), with a change flag
 //   k_bl_sum    terminal check (a fixed point of the ORIGINAL pointers; anything else is a cycle),
 //               per-event root, per-rank inflicted / self / unattributed / suffered wait
 #include "internal.cuh"
@@ -109,20 +110,6 @@ __global__ void __launch_bounds__(256) k_bl_ptr(BA a) {
   if (lane_id() == 0 && n_act) atomicAdd(&blk_act, n_act);
   __syncthreads();
   if (threadIdx.x == 0 && blk_act) atomicAdd(a.n_active, blk_act);  // one global atomic per block
-}
-
-// one in-place jumping round: p[x] <- p[p[x]] for every event whose pointer is not a root yet. In-place
-// updates only speed the convergence up (every pointer stays on its chain); the result is each
-// chain's root either way. Roots (p[x] == x) cost one 4-byte read.
-__global__ void __launch_bounds__(256) k_bl_jump(uint64_t N, uint32_t* ptr, unsigned int* changed) {
-  bool ch = false;
-  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < N; x += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t p = ptr[x];
-    if (p == x) continue;
-    const uint32_t q = ptr[p];
-    if (q != p) { ptr[x] = q; ch = true; }
-  }
-  if (__any_sync(0xFFFFFFFFu, ch) && lane_id() == 0) atomicOr(changed, 1u);
 }
 
 // Pointer jumping on compacted lists: round 1 visits every event; an event whose pointer moved stays
