@@ -64,7 +64,7 @@ def _run_shards(G, cfg, wi, mode, mins, transform):
     return parts, full
 
 
-@pytest.mark.parametrize("G", [2, 3, 4])
+@pytest.mark.parametrize("G", [2, 3, 4, 8])
 @pytest.mark.parametrize("case", CASES[:7] + CASES[7:10], ids=lambda c: c[0])
 def test_local_shards_equal_the_oracle(G, case):
     name, mk, wi, mode, mins, transform, expect = case
