@@ -98,11 +98,24 @@ class ClockSampler:
         self.dev = dev
         self.rows: list[list[str]] = []
         self.p = None
+        self.i0, self.i1 = 0, None
+
+    def wait_ready(self, timeout: float = 10.0):
+        """nvidia-smi takes a while to start: wait for its first sample before the timed region."""
+        t0 = time.time()
+        while self.p and not self.rows and time.time() - t0 < timeout:
+            time.sleep(0.02)
+
+    def mark_start(self):
+        self.i0 = len(self.rows)
+
+    def mark_end(self):
+        self.i1 = len(self.rows)
 
     def __enter__(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "20"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -126,7 +139,9 @@ class ClockSampler:
     def summary(self) -> dict:
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+        # the samples taken during the timed region (at least the first one after it began)
+        i1 = len(self.rows) if self.i1 is None else max(self.i1, self.i0 + 1)
+        for r in self.rows[self.i0:i1]:
             try:
                 sm.append(float(r[0]))
                 mx.append(float(r[1]))
@@ -415,6 +430,8 @@ def main():
     def step():
         s.analyze()
 
+    clk = ClockSampler(local).__enter__()  # started before the warm-up, so it samples from the timed region's start
+    clk.wait_ready()
     for _ in range(args.warmup):
         step()
     import gc
@@ -424,7 +441,8 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    if True:
+        clk.mark_start()
         # the step time: K steps with nothing but the analysis between the two events
         ev0.record(stream)
         for _ in range(args.steps):
@@ -449,6 +467,9 @@ def main():
             kernels = s.kernel_timing()
             s.set_timing(False)
             ms_total_ev = e2a.elapsed_time(e2b)
+        clk.mark_end()
+    time.sleep(0.05)
+    clk.__exit__(None, None, None)
     gc.enable()
     ms_total = ev0.elapsed_time(ev1)
     t_local = torch.tensor([ms_total], dtype=torch.float64, device=f"cuda:{local}")
