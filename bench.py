@@ -467,6 +467,10 @@ def main():
             kernels = s.kernel_timing()
             s.set_timing(False)
             ms_total_ev = e2a.elapsed_time(e2b)
+            if os.environ.get("MS_BENCH_RANK_KERNELS"):  # diagnostics: every rank's fused-pass and exchange times
+                print(f"[rank {rank}] " + " ".join(f"{k}={v[0] / max(v[1], 1):.3f}" for k, v in kernels.items()
+                                                   if k in ("k_fused", "x3_alltoall", "k_cross_reduce", "k_link_median")),
+                      file=sys.stderr, flush=True)
         clk.mark_end()
     time.sleep(0.05)
     clk.__exit__(None, None, None)
