@@ -177,7 +177,9 @@ const char* scan_last_error(const scan_ctx* ctx);   /* owned by ctx; "" if none 
    per-rank / per-window / per-link partial results.
    Preconditions (else SCAN_E_UNSUPPORTED on every shard): the trace is SPMD (fused path), and
    every shard but the last ends on an iteration boundary of every rank with all members of
-   every communicator / P2P pair / DP class in step. Only scan_analyze is available.
+   every communicator / P2P pair / DP class in step. Besides scan_analyze, scan_align,
+   scan_blame (collective calls) and scan_emit_chrome (the shard's own events) run on a sharded
+   context; streaming and JSON ingest do not.
    scan_nccl_unique_id: ncclGetUniqueId into out[128]; the caller broadcasts it (e.g. over a
    torch.distributed group) and every shard passes it to scan_create_sharded, which creates
    the context's own NCCL communicator (destroyed by scan_destroy).
