@@ -100,3 +100,18 @@ def test_fuzz_alignment(seed):
     cfg = tg.GenConfig(tp, pp, dp, int(rng.integers(1, 4)), int(rng.integers(pp, pp + 4)), int(rng.integers(2, 6)), seed=seed,
                        faults=[tg.Fault(tg.THROTTLE, int(rng.integers(0, tp * pp * dp)), factor=2.0)])
     _check(tg.generate(cfg), int(rng.integers(0, tp * pp * dp)), "fused" if seed % 2 else "general")
+
+
+@pytest.mark.parametrize("shift", [12, 29])
+def test_extreme_drift_interpolation(shift):
+    """One rank's clock runs 2^shift times fast: at 2^12 the offset change between anchors exceeds 2^31
+    but stays below 2^50 (the kernels' 64-bit exact interpolation; the other tests run their 32-bit
+    one), at 2^29 most intervals exceed 2^50 (their 128-bit fallback); every mode must equal the
+    oracle's exact floor (AL4) to the nanosecond."""
+    tr = tg.generate(configs.c1(seed=5, iterations=6))
+    st = tr.start_ns.copy()
+    r = 3
+    a, b = int(tr.rank_offsets[r]), int(tr.rank_offsets[r + 1])
+    st[a:b] = st[a:b] * (1 << shift) + 12345
+    from dataclasses import replace
+    _check(replace(tr, start_ns=st), 0, "fused")
