@@ -211,7 +211,7 @@ struct Ctx {
   std::vector<uint32_t> h_cmem, h_rcomm, h_rcomm_off;  // host copies: comm members, rank -> comms CSR
   // timeline alignment (k_align.cu)
   bool aligned = false;
-  DevBuf al_tend, al_aend, al_anct, al_anco, al_slotci, al_level, al_nanc, al_resid, al_flag, al_start, al_ranks, al_cch, al_tgt;
+  DevBuf al_tend, al_aend, al_anct, al_anco, al_level, al_nanc, al_resid, al_flag, al_start, al_ranks, al_tgt;
   uint64_t g_N = 0, g_ncomm = 0, g_ncomp = 0;  // job-wide totals (sharded)
   DevBuf x_send, x_recv, x_recv2, x_ep, x_stage, headtail, lk_sendmap, lk_recvmap;
   void* h_pin = nullptr;                 // pinned host scratch (exchange read-backs, table staging)

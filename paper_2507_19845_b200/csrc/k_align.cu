@@ -37,8 +37,6 @@ struct AlArgs {
   const uint64_t* ch_base; const uint64_t* ch_slot; uint64_t NCH;
   const uint64_t* coff; const uint32_t* cmem;
   long long* tend;   // [n_comm] local end of a candidate (AL1), AL_NONE otherwise
-  uint32_t* slotci;  // [n_slots] comm index of the member event of a candidate slot
-  const uint32_t* comm; uint32_t* cch;  // event communicator id -> [n_comm] channel of a candidate
   const uint32_t* vbits;  // one bit per instance: VALID (k_al_vbits; L2-resident, unlike the 16-byte records)
   const uint32_t* nmax;   // per channel: this context's occurrences (a shard's range starts at ch_base)
 };
@@ -51,14 +49,7 @@ __global__ void k_al_vbits(uint64_t n_inst, const uint4* rec, uint32_t* vbits) {
   if (lane_id() == 0 && i < n_inst) vbits[i >> 5] = bm;
 }
 
-// member slots of a collective instance: channel = communicator id (collective channels come first)
-__device__ __forceinline__ void inst_slot(const AlArgs& a, uint32_t inst, uint32_t ch, uint64_t& kk, uint32_t& nm, uint64_t& s0) {
-  kk = inst - a.ch_base[ch];
-  nm = (uint32_t)(a.coff[ch + 1] - a.coff[ch]);
-  s0 = a.ch_slot[ch] + kk * nm;
-}
-
-// candidate ends and the slot -> comm index map (AL1)
+// candidate ends (AL1)
 __global__ void __launch_bounds__(256) k_al_ends(AlArgs a) {
   const uint64_t tile = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (tile >= a.n_tiles) return;
@@ -91,15 +82,7 @@ __global__ void __launch_bounds__(256) k_al_ends(AlArgs a) {
       long long t = AL_NONE;
       if (k >= 1 && k <= 4) {
         const uint32_t inst = a.inst_c[ci];
-        if ((a.vbits[inst >> 5] >> (inst & 31)) & 1u) {
-          t = (long long)a.start[ev] + (long long)a.dur[ev];
-          const uint32_t ch = a.comm[ev];
-          uint64_t kk, s0; uint32_t nm;
-          inst_slot(a, inst, ch, kk, nm, s0);
-          const uint32_t m = lower_bound_u32(a.cmem + a.coff[ch], nm, r);
-          a.slotci[s0 + m] = (uint32_t)ci;
-          a.cch[ci] = ch;
-        }
+        if ((a.vbits[inst >> 5] >> (inst & 31)) & 1u) t = (long long)a.start[ev] + (long long)a.dur[ev];
       }
       a.tend[ci] = t;
     }
@@ -351,34 +334,29 @@ struct AnchorArgs {
   const long long* aend;  // aligned ends of earlier levels' candidates
   long long* tgt;         // [n_comm] scratch: target of a candidate, AL_NONE if none
   long long* anc_t; long long* anc_o; uint32_t* nanc;
-  const long long* imax;  // per instance: max aligned end over members of levels < k (k_al_instmax)
+  const long long* imax;  // per instance: max aligned end over members of levels < k (k_al_imax_add)
   const long long* init;  // sharded: per rank, the largest candidate end with a target on earlier shards (dedupe)
 };
 
-// Per valid collective instance: the max aligned end over its members with 0 <= level < lim (AL3's
-// target for the members of level lim; lim = INT32_MAX: over every reached member, AL6). AL_SPLIT CTAs
-// per communicator, threads over its instances; a candidate event then reads its instance's value instead
-// of walking all members (an MP group of 64 ranks made that 64 x 64 reads per instance).
-__global__ void __launch_bounds__(256) k_al_instmax(AlArgs a, const int32_t* level, int32_t lim, const long long* aend,
-                                                    long long* out) {
-  const uint32_t ch = blockIdx.x;
-  const uint64_t b = a.ch_base[ch], nk = a.nmax[ch];
-  const uint32_t nm = (uint32_t)(a.coff[ch + 1] - a.coff[ch]);
-  const uint32_t* mem = a.cmem + a.coff[ch];
-  for (uint64_t k = (uint64_t)blockIdx.y * blockDim.x + threadIdx.x; k < nk; k += (uint64_t)gridDim.y * blockDim.x) {
-    if (!(a.rec[b + k].w & SCAN_F_VALID)) continue;
-    const uint64_t s0 = a.ch_slot[ch] + k * nm;
-    long long v = AL_NONE;
-    for (uint32_t q = 0; q < nm; ++q) {
-      const int32_t lv = level[mem[q]];
-      if (lv >= 0 && lv < lim) v = max(v, aend[a.slotci[s0 + q]]);
-    }
-    out[b + k] = v;
-  }
+// Per valid collective instance: the max aligned end over its members of the levels added so far
+// (AL3's target for the members of the next level; every reached member for AL6's residual). The
+// levels' ranks scatter their candidates' aligned ends with a 64-bit atomic max (AL_SPLIT CTAs per
+// rank), one level at a time as the BFS proceeds; a candidate event then reads its instance's value.
+__global__ void k_al_imax_fill(uint64_t n, long long* out) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = AL_NONE;
+}
+__global__ void __launch_bounds__(256) k_al_imax_add(AlArgs a, const uint32_t* ranks, const long long* aend, long long* out) {
+  const uint32_t r = ranks[blockIdx.x];
+  const uint64_t c0 = a.r_comm_off[r], c1 = a.r_comm_off[r + 1];
+  const uint64_t per = (c1 - c0 + AL_SPLIT - 1) / AL_SPLIT;
+  const uint64_t b = c0 + per * blockIdx.y, e = min(c1, b + per);
+  for (uint64_t ci = b + threadIdx.x; ci < e; ci += blockDim.x)
+    if (a.tend[ci] != AL_NONE) atomicMax(&out[a.inst_c[ci]], aend[ci]);
 }
 
 // AL3 targets for every candidate of the level-k ranks (AL_SPLIT CTAs per rank, fully parallel): the
-// instance's max aligned end over members of lower levels (k_al_instmax)
+// instance's max aligned end over members of lower levels (k_al_imax_add)
 __global__ void __launch_bounds__(256) k_al_target(AnchorArgs A) {
   const AlArgs& a = A.a;
   const uint32_t r = A.ranks[blockIdx.x];
@@ -557,11 +535,11 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
   const uint64_t W = c.W, nc = c.n_comm;
   CK(c.al_tend.ensure(std::max<uint64_t>(nc, 1) * 8)); CK(c.al_aend.ensure(std::max<uint64_t>(nc, 1) * 8));
   CK(c.al_anct.ensure(std::max<uint64_t>(nc, 1) * 8)); CK(c.al_anco.ensure(std::max<uint64_t>(nc, 1) * 8));
-  CK(c.al_slotci.ensure(std::max<uint64_t>(c.n_slots, 1) * 4)); CK(c.al_level.ensure(W * 4));
+  CK(c.al_level.ensure(W * 4));
   CK(c.al_nanc.ensure(W * 4)); CK(c.al_resid.ensure(W * 8));
   CK(c.al_flag.ensure(((c.n_comms + 3) & ~3u) + 4));  // per-comm flags, then the first bad rank (u32)
   CK(c.al_start.ensure(std::max<uint64_t>(c.N, 1) * 8)); CK(c.al_ranks.ensure(W * 4));
-  CK(c.al_cch.ensure(std::max<uint64_t>(nc, 1) * 4)); CK(c.al_tgt.ensure(std::max<uint64_t>(nc, 1) * 8));
+  CK(c.al_tgt.ensure(std::max<uint64_t>(nc, 1) * 8));
   CK(c.al_imax.ensure(std::max<uint64_t>(c.p2p_inst0, 1) * 8));  // collective instances come first
   CK(c.al_vbits.ensure((c.n_inst + 31) / 32 * 4 + 4));
   if (c.n_shards > 1) {
@@ -570,8 +548,7 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
   AlArgs a{c.tile_rank.as<uint32_t>(), c.tile_start.as<uint64_t>(), c.rank_off.as<uint64_t>(), c.d_kind, c.d_dur, c.d_start,
            c.N, c.n_tiles, c.t_commpre.as<uint32_t>(), c.r_comm_off.as<uint64_t>(), c.inst_c.as<uint32_t>(),
            c.inst_rec.as<uint4>(), c.ch_base.as<uint64_t>(), c.ch_slot.as<uint64_t>(), c.NCH, c.coff.as<uint64_t>(),
-           c.cmem.as<uint32_t>(), c.al_tend.as<long long>(), c.al_slotci.as<uint32_t>(), c.d_comm, c.al_cch.as<uint32_t>(),
-           c.al_vbits.as<uint32_t>(), c.ch_nmax.as<uint32_t>()};
+           c.cmem.as<uint32_t>(), c.al_tend.as<long long>(), c.al_vbits.as<uint32_t>(), c.ch_nmax.as<uint32_t>()};
   int launches = 0;
   if (c.n_inst)
     launches += timed(c, "k_al_ends", [&] {
@@ -696,6 +673,24 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
       });
   };
   eval(0);
+  // instance maxima over the levels added so far: levels [0, added) scattered into al_imax
+  int32_t added = 0;
+  auto add_levels = [&](int32_t upto) {
+    if (!c.n_comms || !nc) { added = upto; return 0; }
+    int l = 0;
+    if (added == 0) {
+      k_al_imax_fill<<<(unsigned)((c.p2p_inst0 + 255) / 256), 256, 0, c.stream>>>(c.p2p_inst0, c.al_imax.as<long long>());
+      ++l;
+    }
+    const uint32_t n = lvl_off[upto] - lvl_off[added];
+    if (n) {
+      k_al_imax_add<<<dim3(n, AL_SPLIT), 256, 0, c.stream>>>(a, c.al_ranks.as<uint32_t>() + lvl_off[added], c.al_aend.as<long long>(),
+                                                             c.al_imax.as<long long>());
+      ++l;
+    }
+    added = upto;
+    return l;
+  };
   for (int32_t k = 1; k <= maxlev; ++k) {
     const uint32_t n = lvl_off[k + 1] - lvl_off[k];
     AnchorArgs A{a, c.al_ranks.as<uint32_t>() + lvl_off[k], c.al_level.as<int32_t>(), k, c.al_aend.as<long long>(),
@@ -703,11 +698,9 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
                  c.al_imax.as<long long>(), nullptr};
     if (n) {
       launches += timed(c, "k_al_target", [&] {
-        if (c.n_comms)
-          k_al_instmax<<<dim3(c.n_comms, AL_SPLIT), 256, 0, c.stream>>>(a, c.al_level.as<int32_t>(), k, c.al_aend.as<long long>(),
-                                                                        c.al_imax.as<long long>());
+        const int l = add_levels(k);
         k_al_target<<<dim3(n, AL_SPLIT), 256, 0, c.stream>>>(A);
-        return 2;
+        return l + 1;
       });
       if (sh) {  // the anchor dedupe carries over from the earlier shards: their largest candidate end
         std::vector<long long> zero(W, AL_NONE);
@@ -763,12 +756,10 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
     });
   if (nc && !by_level.empty())
     launches += timed(c, "k_al_residual", [&] {
-      if (c.n_comms)
-        k_al_instmax<<<dim3(c.n_comms, AL_SPLIT), 256, 0, c.stream>>>(a, c.al_level.as<int32_t>(), INT32_MAX,
-                                                                      c.al_aend.as<long long>(), c.al_imax.as<long long>());
+      const int l = add_levels(maxlev + 1);
       k_al_residual<<<dim3((unsigned)by_level.size(), AL_SPLIT), 256, 0, c.stream>>>(a, c.al_ranks.as<uint32_t>(), c.al_imax.as<long long>(),
                                                                      c.al_aend.as<long long>(), c.al_resid.as<unsigned long long>());
-      return 2;
+      return l + 1;
     });
   std::vector<uint32_t> nanc(W);
   std::vector<uint64_t> resid(W);
