@@ -114,7 +114,7 @@ static void release_all(Ctx& c) {
                     &c.ft_base, &c.ft_last, &c.st_tot, &c.p2p_rbase, &c.dlate, &c.dinfo, &c.ft_posA, &c.ft_posB,
                     &c.ft_posK, &c.eidx, &c.tile_stage, &c.xbase, &c.g_base, &c.g_slot,
                     &c.g_nmax, &c.g_nmin, &c.g_k0, &c.p2p_eslot, &c.xe_off, &c.xe_col, &c.xbig, &c.own_start, &c.al_tend, &c.al_aend, &c.al_anct,
-                    &c.al_anco, &c.al_level, &c.al_nanc, &c.al_resid, &c.al_flag, &c.al_start, &c.al_ranks, &c.al_tgt, &c.x_send, &c.x_recv, &c.x_recv2, &c.x_ep, &c.x_stage, &c.headtail, &c.lk_sendmap, &c.lk_recvmap, &c.al_xs, &c.al_xr, &c.al_row, &c.al_lt, &c.al_init, &c.al_bx, &c.al_bnd, &c.bl_xs, &c.bl_xr, &c.bl_gbase, &c.bl_ext, &c.al_imax, &c.al_vbits, &c.bl_seg, &c.bl_inst, &c.bl_pa, &c.bl_pb, &c.bl_root, &c.bl_last, &c.bl_rank, &c.bl_rk};
+                    &c.al_anco, &c.al_level, &c.al_nanc, &c.al_resid, &c.al_flag, &c.al_start, &c.al_ranks, &c.al_tgt, &c.x_send, &c.x_recv, &c.x_recv2, &c.x_ep, &c.x_stage, &c.headtail, &c.lk_sendmap, &c.lk_recvmap, &c.al_xs, &c.al_xr, &c.al_row, &c.al_lt, &c.al_init, &c.al_bx, &c.al_bnd, &c.bl_xs, &c.bl_xr, &c.bl_gbase, &c.bl_ext, &c.al_imax, &c.al_vbits, &c.al_seg, &c.bl_seg, &c.bl_inst, &c.bl_pa, &c.bl_pb, &c.bl_root, &c.bl_last, &c.bl_rank, &c.bl_rk};
   for (DevBuf* b : bufs) b->release();
 }
 

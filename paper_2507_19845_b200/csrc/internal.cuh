@@ -220,7 +220,7 @@ struct Ctx {
   cudaEvent_t ev_x1 = nullptr, ev_x2 = nullptr;
   // event-level blame (k_blame.cu)
   bool blamed = false;
-  DevBuf al_xs, al_xr, al_row, al_lt, al_init, al_bx, al_bnd, bl_xs, bl_xr, bl_gbase, bl_ext, al_imax, al_vbits, bl_seg, bl_inst, bl_pa, bl_pb, bl_root, bl_last, bl_rank, bl_rk;
+  DevBuf al_xs, al_xr, al_row, al_lt, al_init, al_bx, al_bnd, bl_xs, bl_xr, bl_gbase, bl_ext, al_imax, al_vbits, al_seg, bl_seg, bl_inst, bl_pa, bl_pb, bl_root, bl_last, bl_rank, bl_rk;
   // JSON ingest / emit state (k_json.cu), owned; gen: bumped by every load / analysis / alignment
   void* json_state = nullptr;
   uint64_t gen = 0;

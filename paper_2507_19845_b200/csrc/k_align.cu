@@ -327,6 +327,10 @@ __device__ __forceinline__ auto rank_anchors(const long long* at, const long lon
 
 constexpr uint32_t AL_SPLIT = 16;  // CTAs per rank in the per-rank passes (blockIdx.y)
 
+// one segment (1/AL_SPLIT of a rank's candidates) for the split anchor dedupe: its first and last
+// end with a target (AL_NONE if none) and its anchors counted from an empty carry
+struct AlSegStat { long long first, last; unsigned long long cnt; };
+
 struct AnchorArgs {
   AlArgs a;
   const uint32_t* ranks;  // ranks of this level
@@ -336,6 +340,7 @@ struct AnchorArgs {
   long long* anc_t; long long* anc_o; uint32_t* nanc;
   const long long* imax;  // per instance: max aligned end over members of levels < k (k_al_imax_add)
   const long long* init;  // sharded: per rank, the largest candidate end with a target on earlier shards (dedupe)
+  AlSegStat* seg;         // [ranks of the level][AL_SPLIT] per-segment statistics (k_al_target -> k_al_anchor)
 };
 
 // Per valid collective instance: the max aligned end over its members of the levels added so far
@@ -356,22 +361,46 @@ __global__ void __launch_bounds__(256) k_al_imax_add(AlArgs a, const uint32_t* r
 }
 
 // AL3 targets for every candidate of the level-k ranks (AL_SPLIT CTAs per rank, fully parallel): the
-// instance's max aligned end over members of lower levels (k_al_imax_add)
+// instance's max aligned end over members of lower levels (k_al_imax_add). Each CTA also counts its
+// segment's anchors as if no end preceded it, with its first and last end that has a target: the
+// candidate ends of a rank are non-decreasing (k_al_mono, job-wide on sharded contexts), so a carry c
+// from the earlier segments only removes the segment's first anchor, when its end is <= c.
 __global__ void __launch_bounds__(256) k_al_target(AnchorArgs A) {
   const AlArgs& a = A.a;
+  __shared__ long long sm[33];
+  __shared__ long long run, first;
+  __shared__ uint32_t cnt;
   const uint32_t r = A.ranks[blockIdx.x];
   const uint64_t c0 = a.r_comm_off[r], c1 = a.r_comm_off[r + 1];
   const uint64_t per = (c1 - c0 + AL_SPLIT - 1) / AL_SPLIT;
   const uint64_t b = c0 + per * blockIdx.y, e = min(c1, b + per);
-  for (uint64_t ci = b + threadIdx.x; ci < e; ci += blockDim.x) {
-    // own rank r is at level k, so the instance value (levels < k) excludes it
-    A.tgt[ci] = a.tend[ci] != AL_NONE ? A.imax[a.inst_c[ci]] : AL_NONE;
+  if (threadIdx.x == 0) { run = AL_NONE; first = AL_NONE; cnt = 0; }
+  __syncthreads();
+  for (uint64_t cb = b; cb < e; cb += blockDim.x) {
+    const uint64_t ci = cb + threadIdx.x;
+    long long t = AL_NONE;
+    if (ci < e) {
+      // own rank r is at level k, so the instance value (levels < k) excludes it
+      const long long te = a.tend[ci];
+      const long long tg = te != AL_NONE ? A.imax[a.inst_c[ci]] : AL_NONE;
+      A.tgt[ci] = tg;
+      if (tg != AL_NONE) t = te;
+    }
+    long long tot;
+    const long long prev = max(block_excl_max_i64(t, tot, sm), run);
+    const bool anc = t != AL_NONE && t > prev;
+    const int na = __syncthreads_count(anc);
+    if (anc && prev == AL_NONE) first = t;  // the segment's first end with a target (one thread)
+    if (threadIdx.x == 0) { run = max(run, tot); cnt += (uint32_t)na; }
+    __syncthreads();
   }
+  if (threadIdx.x == 0) A.seg[(uint64_t)blockIdx.x * AL_SPLIT + blockIdx.y] = AlSegStat{first, run, cnt};
 }
 
-// AL3 anchors of the level-k ranks: one CTA per rank, program order kept by block scans (dedupe
-// against the previous anchor's end, stable compaction)
-__global__ void __launch_bounds__(AL_NT) k_al_anchor(AnchorArgs A) {
+// AL3 anchors of the level-k ranks: AL_SPLIT CTAs per rank, each over its segment; its carry (the
+// largest earlier end with a target) and its output offset follow from the earlier segments'
+// statistics; program order kept by block scans (dedupe against the previous end, stable compaction)
+__global__ void __launch_bounds__(256) k_al_anchor(AnchorArgs A) {
   const AlArgs& a = A.a;
   __shared__ long long sm[33];
   __shared__ uint32_t smu[33];
@@ -379,18 +408,30 @@ __global__ void __launch_bounds__(AL_NT) k_al_anchor(AnchorArgs A) {
   __shared__ uint32_t n_anc;
   const uint32_t r = A.ranks[blockIdx.x];
   const uint64_t c0 = a.r_comm_off[r], c1 = a.r_comm_off[r + 1];
-  if (threadIdx.x == 0) { last_t = A.init ? A.init[r] : AL_NONE; n_anc = 0; }
+  const uint64_t per = (c1 - c0 + AL_SPLIT - 1) / AL_SPLIT;
+  const uint64_t b0 = c0 + per * blockIdx.y, e0 = min(c1, b0 + per);
+  if (threadIdx.x == 0) {
+    long long carry = A.init ? A.init[r] : AL_NONE;
+    uint32_t off = 0;
+    for (uint32_t j = 0; j < blockIdx.y; ++j) {
+      const AlSegStat st = A.seg[(uint64_t)blockIdx.x * AL_SPLIT + j];
+      if (st.last == AL_NONE) continue;
+      off += (uint32_t)st.cnt - (st.first <= carry ? 1u : 0u);
+      carry = max(carry, st.last);
+    }
+    last_t = carry; n_anc = off;
+  }
   __syncthreads();
-  for (uint64_t b = c0; b < c1; b += AL_NT) {
+  for (uint64_t b = b0; b < e0; b += 256) {
     const uint64_t ci = b + threadIdx.x;
-    const long long tg = ci < c1 ? A.tgt[ci] : AL_NONE;
+    const long long tg = ci < e0 ? A.tgt[ci] : AL_NONE;
     const bool have = tg != AL_NONE;
     const long long t = have ? a.tend[ci] : AL_NONE;
     long long tot;
     const long long prev = max(block_excl_max_i64(t, tot, sm), last_t);
     const bool anc = have && t > prev;
     uint32_t ntot;
-    const uint32_t pos = block_excl_sum<AL_NT>(anc ? 1u : 0u, ntot, smu);
+    const uint32_t pos = block_excl_sum<256>(anc ? 1u : 0u, ntot, smu);
     if (anc) {
       A.anc_t[c0 + n_anc + pos] = t;
       A.anc_o[c0 + n_anc + pos] = tg - t;
@@ -399,7 +440,7 @@ __global__ void __launch_bounds__(AL_NT) k_al_anchor(AnchorArgs A) {
     if (threadIdx.x == 0) { last_t = max(last_t, tot); n_anc += ntot; }
     __syncthreads();
   }
-  if (threadIdx.x == 0) A.nanc[r] = n_anc;
+  if (threadIdx.x == 0 && blockIdx.y == AL_SPLIT - 1) A.nanc[r] = n_anc;
 }
 
 // aligned ends of the candidates of level-k ranks (level 0: the reference, offset 0): one CTA per
@@ -542,6 +583,7 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
   CK(c.al_tgt.ensure(std::max<uint64_t>(nc, 1) * 8));
   CK(c.al_imax.ensure(std::max<uint64_t>(c.p2p_inst0, 1) * 8));  // collective instances come first
   CK(c.al_vbits.ensure((c.n_inst + 31) / 32 * 4 + 4));
+  CK(c.al_seg.ensure(W * AL_SPLIT * sizeof(AlSegStat)));
   if (c.n_shards > 1) {
     CK(c.al_lt.ensure(W * 8)); CK(c.al_init.ensure(W * 8)); CK(c.al_bx.ensure(W * 32)); CK(c.al_bnd.ensure(W * 32));
   }
@@ -695,7 +737,7 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
     const uint32_t n = lvl_off[k + 1] - lvl_off[k];
     AnchorArgs A{a, c.al_ranks.as<uint32_t>() + lvl_off[k], c.al_level.as<int32_t>(), k, c.al_aend.as<long long>(),
                  c.al_tgt.as<long long>(), c.al_anct.as<long long>(), c.al_anco.as<long long>(), c.al_nanc.as<uint32_t>(),
-                 c.al_imax.as<long long>(), nullptr};
+                 c.al_imax.as<long long>(), nullptr, reinterpret_cast<AlSegStat*>(c.al_seg.p)};
     if (n) {
       launches += timed(c, "k_al_target", [&] {
         const int l = add_levels(k);
@@ -716,7 +758,7 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
         A.init = c.al_init.as<long long>();
         launches += 1;
       }
-      launches += timed(c, "k_al_anchor", [&] { k_al_anchor<<<n, AL_NT, 0, c.stream>>>(A); return 1; });
+      launches += timed(c, "k_al_anchor", [&] { k_al_anchor<<<dim3(n, AL_SPLIT), 256, 0, c.stream>>>(A); return 1; });
     }
     if (sh && n) {  // the level-k ranks' neighbouring anchors on the other shards (interpolation across blocks)
       k_al_bounds<<<(n + 255) / 256, 256, 0, c.stream>>>(n, A.ranks, c.r_comm_off.as<uint64_t>(), c.al_anct.as<long long>(),
