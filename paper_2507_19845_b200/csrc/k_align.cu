@@ -27,7 +27,6 @@ namespace ms {
 namespace {
 
 constexpr long long AL_NONE = (long long)0x8000000000000000ull;  // INT64_MIN: not a candidate
-constexpr int AL_NT = 1024;
 
 struct AlArgs {
   const uint32_t* tile_rank; const uint64_t* tile_start; const uint64_t* rank_off; const uint16_t* kind;
@@ -128,23 +127,47 @@ __device__ long long block_excl_max_i64(long long v, long long& total, long long
   return max(before_warp, ex);
 }
 
-// AL3 precondition: candidate ends non-decreasing along each rank's program order
-__global__ void __launch_bounds__(AL_NT) k_al_mono(const uint64_t* r_comm_off, const long long* tend, uint32_t* bad_rank) {
+constexpr uint32_t AL_SPLIT = 16;  // CTAs per rank in the per-rank passes (blockIdx.y)
+// one segment (1/AL_SPLIT of a rank's candidates) of the split per-rank passes: its first and last
+// (largest) end -- in the anchor dedupe only ends with a target, AL_NONE if none -- and its anchors
+// counted from an empty carry
+struct AlSegStat { long long first, last; unsigned long long cnt; };
+
+// AL3 precondition: candidate ends non-decreasing along each rank's program order (AL_SPLIT CTAs per
+// rank, each checks its segment; k_al_mono_bnd checks the segment boundaries)
+__global__ void __launch_bounds__(256) k_al_mono(const uint64_t* r_comm_off, const long long* tend, uint32_t* bad_rank,
+                                                 AlSegStat* seg) {
   __shared__ long long sm[33];
-  __shared__ long long carry;
+  __shared__ long long carry, first;
   const uint32_t r = blockIdx.x;
   const uint64_t c0 = r_comm_off[r], c1 = r_comm_off[r + 1];
-  if (threadIdx.x == 0) carry = AL_NONE;
+  const uint64_t per = (c1 - c0 + AL_SPLIT - 1) / AL_SPLIT;
+  const uint64_t b0 = c0 + per * blockIdx.y, e0 = min(c1, b0 + per);
+  if (threadIdx.x == 0) { carry = AL_NONE; first = AL_NONE; }
   __syncthreads();
-  for (uint64_t b = c0; b < c1; b += AL_NT) {
+  for (uint64_t b = b0; b < e0; b += 256) {
     const uint64_t ci = b + threadIdx.x;
-    const long long t = ci < c1 ? tend[ci] : AL_NONE;
+    const long long t = ci < e0 ? tend[ci] : AL_NONE;
     long long tot;
     const long long prev = max(block_excl_max_i64(t, tot, sm), carry);
     if (t != AL_NONE && t < prev) atomicMin(bad_rank, r);
+    if (t != AL_NONE && prev == AL_NONE) first = t;  // the segment's first candidate end (one thread)
     __syncthreads();
     if (threadIdx.x == 0) carry = max(carry, tot);
     __syncthreads();
+  }
+  if (threadIdx.x == 0) seg[(uint64_t)r * AL_SPLIT + blockIdx.y] = AlSegStat{first, carry, 0};
+}
+// the segments of a rank in order: each one's first end must not be below the earlier ones' largest
+__global__ void k_al_mono_bnd(uint32_t W, const AlSegStat* seg, uint32_t* bad_rank) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= W) return;
+  long long prev = AL_NONE;
+  for (uint32_t j = 0; j < AL_SPLIT; ++j) {
+    const AlSegStat st = seg[(uint64_t)r * AL_SPLIT + j];
+    if (st.last == AL_NONE) continue;
+    if (st.first < prev) atomicMin(bad_rank, r);
+    prev = max(prev, st.last);
   }
 }
 
@@ -325,11 +348,6 @@ __device__ __forceinline__ auto rank_anchors(const long long* at, const long lon
   else return PlainAnc{at, ao, n};
 }
 
-constexpr uint32_t AL_SPLIT = 16;  // CTAs per rank in the per-rank passes (blockIdx.y)
-
-// one segment (1/AL_SPLIT of a rank's candidates) for the split anchor dedupe: its first and last
-// end with a target (AL_NONE if none) and its anchors counted from an empty carry
-struct AlSegStat { long long first, last; unsigned long long cnt; };
 
 struct AnchorArgs {
   AlArgs a;
@@ -607,8 +625,10 @@ scan_status align_all(Ctx& c, int32_t ref, scan_align_result* out) {
   uint32_t* bad = reinterpret_cast<uint32_t*>(c.al_flag.as<uint8_t>() + ((c.n_comms + 3) & ~3u));
   CK(cudaMemsetAsync(bad, 0xFF, 4, c.stream));
   launches += timed(c, "k_al_mono", [&] {
-    k_al_mono<<<(unsigned)W, AL_NT, 0, c.stream>>>(c.r_comm_off.as<uint64_t>(), c.al_tend.as<long long>(), bad);
-    return 1;
+    AlSegStat* seg = reinterpret_cast<AlSegStat*>(c.al_seg.p);
+    k_al_mono<<<dim3((unsigned)W, AL_SPLIT), 256, 0, c.stream>>>(c.r_comm_off.as<uint64_t>(), c.al_tend.as<long long>(), bad, seg);
+    k_al_mono_bnd<<<(unsigned)((W + 255) / 256), 256, 0, c.stream>>>((uint32_t)W, seg, bad);
+    return 2;
   });
   std::vector<uint8_t> flag(c.n_comms + 8);
   uint32_t bad_rank = 0;
