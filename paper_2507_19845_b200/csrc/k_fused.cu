@@ -942,6 +942,15 @@ __global__ void __launch_bounds__(FT_NT, FT_MINB) k_fused_t(FusedArgs a) {
   const uint32_t w_tile = win_of(a, itg0);
   const uint32_t ncr = a.ncroles[s];
 
+  // a tile that failed the template verification voids the whole pass (the call reruns the general
+  // path): tiles that start after that return at once. One thread reads the flag and the CTA follows
+  // its value (another CTA may set it between two threads' reads: every thread must agree)
+  {
+    __shared__ uint32_t s_void;
+    if (tid == 0) s_void = *((volatile const unsigned*)&a.cnt->overflow) & NOT_SPMD;
+    __syncthreads();
+    if (s_void) return;
+  }
   // L2 prefetch of this tile's rows at kernel start: the DRAM requests are in flight while the tables
   // and template info below are set up, so the load pass finds them in L2 (a hint only)
   if (a.pf_own) ft_prefetch_tile(a, tile, tid);
