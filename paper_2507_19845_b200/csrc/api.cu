@@ -55,6 +55,12 @@ int ms::flush_fills(Ctx& c) {
   return 0;
 }
 
+const uint32_t* ms::tile_order_ptr(Ctx& c) {
+  static int on = -1;
+  if (on < 0) { const char* e = std::getenv("MS_TILE_ORDER"); on = e ? std::atoi(e) : 1; }
+  return on ? c.tile_order.as<uint32_t>() : nullptr;
+}
+
 scan_status ms::sync_read(Ctx& c) {
   flush_fills(c);
   CK(cudaMemcpyAsync(&c.hc, c.counters.p, sizeof(Counters), cudaMemcpyDeviceToHost, c.stream));
@@ -100,7 +106,7 @@ scan_status scan_create(scan_ctx** out, int cuda_device, void* cuda_stream) {
 
 static void release_all(Ctx& c) {
   DevBuf* bufs[] = {&c.own_dur, &c.own_kind, &c.own_meta, &c.own_comm, &c.own_pay, &c.rank_off, &c.coff, &c.cmem, &c.ccls,
-                    &c.rcomm_off, &c.rcomm, &c.nbc_off, &c.nbc, &c.tile_rank, &c.tile_start, &c.rank_tile0, &c.t_nkeys,
+                    &c.rcomm_off, &c.rcomm, &c.nbc_off, &c.nbc, &c.tile_rank, &c.tile_start, &c.rank_tile0, &c.tile_order, &c.t_nkeys,
                     &c.t_keys, &c.t_cnt, &c.t_pref, &c.t_ncomm, &c.t_niter, &c.t_last, &c.t_commpre, &c.t_iterpre,
                     &c.t_prevj, &c.r_nkeys, &c.r_keys, &c.r_cnt, &c.r_ncomm, &c.r_niter, &c.r_ncomp, &c.r_lastit,
                     &c.r_comm_off, &c.r_comp_off, &c.r_bits_off, &c.bitmap, &c.bitpre, &c.bmsum, &c.counters, &c.ch_nmax,
@@ -250,6 +256,18 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
     for (uint64_t s = ro[r]; s < ro[r + 1]; s += TILE_EV) { trank.push_back((uint32_t)r); tstart.push_back(s); }
   }
   rt0[W] = (uint32_t)trank.size();
+  // interleaved processing order of the tiles: chunk 0 of every rank, then chunk 1, ... -- the members
+  // of an instance are then processed at about the same time, so the general path's per-instance
+  // gathers (records) and scatters (member slots) meet in L2 instead of each fetching the sector
+  std::vector<uint32_t> torder;
+  torder.reserve(trank.size());
+  {
+    uint32_t maxc = 0;
+    for (uint64_t r = 0; r < W; ++r) maxc = std::max(maxc, rt0[r + 1] - rt0[r]);
+    for (uint32_t k = 0; k < maxc; ++k)
+      for (uint64_t r = 0; r < W; ++r)
+        if (rt0[r] + k < rt0[r + 1]) torder.push_back(rt0[r] + k);
+  }
   c.TP = topo->tp; c.PP = topo->pp; c.DP = topo->dp; c.W = W; c.n_comms = nc; c.N = N; c.flags = flags;
   c.h_ccls = ccls; c.h_coff = coff; c.h_cmem = cmem; c.h_rcomm = rcm; c.h_rcomm_off = rco;
   {  // cross collectives (not TP/DP class) with <= 128 members: edge column of member q waiting on
@@ -284,7 +302,7 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
   if ((st = upload(c, c.rank_off, ro)) || (st = upload(c, c.coff, coff)) || (st = upload(c, c.cmem, cmem)) ||
       (st = upload(c, c.ccls, ccls)) || (st = upload(c, c.rcomm_off, rco)) || (st = upload(c, c.rcomm, rcm)) ||
       (st = upload(c, c.nbc_off, nbo)) || (st = upload(c, c.nbc, nb)) || (st = upload(c, c.tile_rank, trank)) ||
-      (st = upload(c, c.tile_start, tstart)) || (st = upload(c, c.rank_tile0, rt0)))
+      (st = upload(c, c.tile_start, tstart)) || (st = upload(c, c.rank_tile0, rt0)) || (st = upload(c, c.tile_order, torder)))
     return st;
   // fused-path (K9) tables: every stage block SPMD-compatible? role -> communicator / slot
   {

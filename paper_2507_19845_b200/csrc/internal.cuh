@@ -124,7 +124,7 @@ struct Ctx {
   uint64_t nnz_c = 0;
   // tiles
   uint64_t n_tiles = 0;
-  DevBuf tile_rank, tile_start, rank_tile0;  // u32, u64, u32 [W+1]
+  DevBuf tile_rank, tile_order, tile_start, rank_tile0;  // u32, u64, u32 [W+1]
   std::vector<uint32_t> h_rank_tile0;
 
   // match workspaces
@@ -458,6 +458,9 @@ int launch_fused_prepass(Ctx& c);
 int launch_fused_census(Ctx& c);
 int launch_fused(Ctx& c);
 bool p2p_defer_on(Ctx& c);
+// general-path tile kernels walk the tiles interleaved across ranks (Ctx::tile_order) unless
+// MS_TILE_ORDER=0 (index order, rank-major)
+const uint32_t* tile_order_ptr(Ctx& c);
 int launch_p2p_roles(Ctx& c);
 int launch_stage(Ctx& c);
 // the analysis runs k_stage: selected at load and the channel bases fit its 32-bit tables

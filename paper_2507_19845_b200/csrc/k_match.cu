@@ -21,6 +21,7 @@ struct TileArgs {
   uint64_t N; uint64_t n_tiles; int W; uint32_t n_comms;
   const uint64_t* coff; const uint32_t* cmem;
   Counters* cnt;
+  const uint32_t* order;  // processing order of the tiles (tile_order_ptr), null = index order
 };
 
 __device__ __forceinline__ bool is_member(const uint64_t* coff, const uint32_t* cmem, uint32_t c, uint32_t r) {
@@ -554,8 +555,9 @@ __global__ void __launch_bounds__(256) k_assign(AssignArgs A) {
   __shared__ uint16_t cob[8][256];
   const TileArgs& a = A.t;
   const uint32_t wid = threadIdx.x >> 5;
-  const uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wid;
+  uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wid;
   if (tile >= a.n_tiles) return;
+  if (a.order) tile = a.order[tile];
   const uint32_t lane = lane_id();
   const uint32_t r = a.tile_rank[tile];
   const uint64_t rstart = a.rank_off[r];
@@ -695,6 +697,7 @@ int launch_assign(Ctx& c) {
   A.r_comm_off = c.r_comm_off.as<uint64_t>(); A.r_comp_off = c.r_comp_off.as<uint64_t>();
   A.bitmap = c.bitmap.as<uint32_t>(); A.bitpre = c.bitpre.as<uint32_t>();
   A.ch_base = c.ch_base.as<uint64_t>(); A.ch_slot = c.ch_slot.as<uint64_t>();
+  A.t.order = tile_order_ptr(c);
   A.inst_c = c.inst_c.as<uint32_t>(); A.slots = c.slots.as<uint4>();
   A.cdur = c.cdur.as<uint32_t>(); A.cop = c.cop.as<uint16_t>(); A.citer = c.citer.as<uint32_t>(); A.NIT1 = c.NIT + 1;
   A.p2p_slot0 = c.p2p_slot0; A.p2p_inst0 = c.p2p_inst0;

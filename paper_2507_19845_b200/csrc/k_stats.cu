@@ -233,6 +233,7 @@ struct EPArgs {
   uint32_t* wl_joined; uint32_t* wl_late;
   uint32_t wi, classes, mode;
   unsigned long long late_margin, wait_margin;
+  const uint32_t* order;  // processing order of the tiles (tile_order_ptr), null = index order
 };
 
 constexpr int EHT = 32;   // edge hash entries per warp
@@ -243,11 +244,12 @@ __global__ void __launch_bounds__(256) k_event_pass(EPArgs a) {
   __shared__ unsigned long long hval[8][EHT];
   __shared__ uint32_t snb[8][ENB + PCAP];  // the rank's sorted collective / P2P neighbour lists
   const uint32_t wid = threadIdx.x >> 5;
-  const uint64_t tile = (uint64_t)blockIdx.x * 8 + wid;
+  uint64_t tile = (uint64_t)blockIdx.x * 8 + wid;
   const uint32_t lane = lane_id();
   hkey[wid][lane] = ~0ull; hval[wid][lane] = 0;
   __syncwarp();
   if (tile >= a.n_tiles) return;
+  if (a.order) tile = a.order[tile];
   const uint32_t r = a.tile_rank[tile];
   const uint64_t rstart = a.rank_off[r];
   const uint64_t s = a.tile_start[tile];
@@ -364,7 +366,7 @@ int launch_event_pass(Ctx& c) {
            c.nbc.as<uint32_t>(), c.nbp.as<uint32_t>(), c.nbp_n.as<uint32_t>(), c.nnz_c + (uint64_t)c.W * PCAP, c.nnz_c,
            c.ewc.as<unsigned long long>(), c.rk_sum.as<unsigned long long>(), c.wl_joined.as<uint32_t>(),
            c.wl_late.as<uint32_t>(), c.dcfg.window_iters, c.lcfg.stage2_classes, c.lcfg.stage2_mode,
-           (unsigned long long)c.lcfg.late_margin_ns, (unsigned long long)c.lcfg.wait_margin_ns};
+           (unsigned long long)c.lcfg.late_margin_ns, (unsigned long long)c.lcfg.wait_margin_ns, tile_order_ptr(c)};
   k_event_pass<<<(unsigned)((c.n_tiles + 7) / 8), 256, 0, c.stream>>>(a);
   return 1;
 }
