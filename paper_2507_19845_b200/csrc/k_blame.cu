@@ -34,14 +34,16 @@ struct BA {
   // sharded context, shard > 0: a rank's first local event is not its job-wide first one; what precedes
   // it is the rank's last event on the previous shard, pointer value N + rank (resolved across shards)
   uint32_t ext; uint64_t N;
+  const uint32_t* order;  // processing order of the tiles (tile_order_ptr), null = index order
 };
 
 // A communication event waited iff its wait is > 0 (EB1): the wait is 0 for every member of an
 // invalid instance, and the last arriver of a valid one waits 0, so only events with wait 0 can be the
 // last arriver's member and need the instance record.
 __global__ void __launch_bounds__(256) k_bl_last(BA a) {
-  const uint64_t tile = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  uint64_t tile = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (tile >= a.n_tiles) return;
+  if (a.order) tile = a.order[tile];
   const uint32_t r = a.tile_rank[tile];
   const uint64_t rs = a.rank_off[r];
   const uint64_t s = a.tile_start[tile], e = min(s + (uint64_t)TILE_EV, a.rank_off[r + 1]);
@@ -64,9 +66,10 @@ __global__ void __launch_bounds__(256) k_bl_ptr(BA a) {
   __shared__ unsigned int blk_act;
   if (threadIdx.x == 0) blk_act = 0;
   __syncthreads();
-  const uint64_t tile = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  uint64_t tile = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   uint32_t n_act = 0;
   if (tile < a.n_tiles) {
+    if (a.order) tile = a.order[tile];
     const uint32_t r = a.tile_rank[tile];
     const uint64_t rs = a.rank_off[r];
     const uint64_t s = a.tile_start[tile], e = min(s + (uint64_t)TILE_EV, a.rank_off[r + 1]);
@@ -192,7 +195,8 @@ __global__ void __launch_bounds__(256) k_bl_sum(SA a) {
     __syncthreads();
   }
   unsigned long long nw = 0, ncy = 0;
-  for (uint64_t tile = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5); tile < a.b.n_tiles; tile += (uint64_t)gridDim.x * 8) {
+  for (uint64_t ti = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5); ti < a.b.n_tiles; ti += (uint64_t)gridDim.x * 8) {
+    const uint64_t tile = a.b.order ? a.b.order[ti] : ti;
     const uint32_t r = a.b.tile_rank[tile];
     const uint64_t s = a.b.tile_start[tile], e = min(s + (uint64_t)TILE_EV, a.b.rank_off[r + 1]);
     unsigned long long suf = 0, slf = 0, una = 0;
@@ -379,7 +383,7 @@ scan_status blame_all(Ctx& c, scan_blame_result* out) {
   BA b{c.n_tiles, c.tile_rank.as<uint32_t>(), c.tile_start.as<uint64_t>(), c.rank_off.as<uint64_t>(), c.d_kind,
        c.inst_c.as<uint32_t>(), c.wait_c.as<uint32_t>(), c.inst_rec.as<uint4>(), c.r_comm_off.as<uint64_t>(),
        c.t_commpre.as<uint32_t>(), c.bl_last.as<uint32_t>(), nullptr, c.bl_rk.as<uint16_t>(), c.bl_pa.as<uint32_t>(),
-       counters2 + 1, (sharded && c.shard > 0) ? 1u : 0u, N};
+       counters2 + 1, (sharded && c.shard > 0) ? 1u : 0u, N, tile_order_ptr(c)};
   const unsigned tb = nbk(c.n_tiles, 8);
   uint32_t rounds = 0;
   unsigned int n_act = 0;
