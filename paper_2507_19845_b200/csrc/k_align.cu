@@ -464,8 +464,11 @@ __global__ void __launch_bounds__(256) k_al_anchor(AnchorArgs A) {
 // aligned ends of the candidates of level-k ranks (level 0: the reference, offset 0): one CTA per
 // rank; a warp takes 1024-event chunks, lane l the events l, l+32, ... (coalesced), one interval
 // search per lane and chunk, then a walk (candidate ends are non-decreasing)
+#ifndef MS_EV_MINB
+#define MS_EV_MINB 4  // 4 CTAs per SM (64 registers)
+#endif
 template <bool SH>
-__global__ void __launch_bounds__(256) k_al_eval(const uint32_t* ranks, const uint64_t* r_comm_off, const long long* tend,
+__global__ void __launch_bounds__(256, MS_EV_MINB) k_al_eval(const uint32_t* ranks, const uint64_t* r_comm_off, const long long* tend,
                                                  const long long* anc_t, const long long* anc_o, const uint32_t* nanc,
                                                  const long long* bnd, long long* aend) {
   __shared__ long long swt[8][AW], swo[8][AW];
@@ -498,8 +501,11 @@ __global__ void __launch_bounds__(256) k_al_eval(const uint32_t* ranks, const ui
 // consecutive events 8l..8l+7 of every 256; the lane's interval is cached across its events (a
 // shared-memory anchor window as in k_al_eval, the 8 loads held in registers, shared-memory staging
 // of the loads and stores, a 32-bit interpolation mode: each measured no faster, 7.0-9.0 ms on C3)
+#ifndef MS_AP_MINB
+#define MS_AP_MINB 4  // 4 CTAs per SM (64 registers): 6.7 -> 6.2 ms on C3
+#endif
 template <bool SH>
-__global__ void __launch_bounds__(256) k_al_apply(uint64_t n_tiles, const uint32_t* tile_rank, const uint64_t* tile_start,
+__global__ void __launch_bounds__(256, MS_AP_MINB) k_al_apply(uint64_t n_tiles, const uint32_t* tile_rank, const uint64_t* tile_start,
                                                   const uint64_t* rank_off, const uint64_t* r_comm_off, const int32_t* level,
                                                   const int64_t* start, const long long* anc_t, const long long* anc_o,
                                                   const uint32_t* nanc, const long long* bnd, long long* out) {

@@ -550,7 +550,10 @@ struct AssignArgs {
   uint64_t p2p_slot0, p2p_inst0;
 };
 
-__global__ void __launch_bounds__(256) k_assign(AssignArgs A) {
+#ifndef MS_ASSIGN_MINB
+#define MS_ASSIGN_MINB 4  // 4 CTAs per SM (64 registers, a few spills): 14.1 -> 11.5 ms on C3's general path
+#endif
+__global__ void __launch_bounds__(256, MS_ASSIGN_MINB) k_assign(AssignArgs A) {
   __shared__ uint32_t cdb[8][256];  // per warp: the round's compute durations / op ids, compacted
   __shared__ uint16_t cob[8][256];
   const TileArgs& a = A.t;
