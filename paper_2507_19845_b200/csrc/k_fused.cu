@@ -1639,7 +1639,10 @@ __device__ __forceinline__ void x_edge(const XArgs& a, uint32_t r, uint32_t L, u
   atomicAdd(&a.ew[(uint64_t)win * a.nnz_tot + idx], wait);
 }
 
-__global__ void __launch_bounds__(256, 4) k_cross_reduce(XArgs a) {
+#ifndef MS_XR_MINB
+#define MS_XR_MINB 4  // 3 or 2 CTAs per SM (more registers, no spills) measured slower: 0.36 -> 0.40 / 0.51 ms
+#endif
+__global__ void __launch_bounds__(256, MS_XR_MINB) k_cross_reduce(XArgs a) {
   if (*((volatile unsigned*)&a.cnt->overflow) & NOT_SPMD) return;  // fused results void: general path reruns
   extern __shared__ unsigned long long xb_s[];
   if (a.xb_smem) {
@@ -1922,8 +1925,8 @@ int launch_cross_reduce(Ctx& c) {
   a.xb_smem = xsm <= 48 * 1024 ? 1 : 0;
   static int sms = 0;
   if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-  // one resident wave (4 CTAs of 256 threads per SM at <= 64 registers): each warp walks one contiguous chunk
-  unsigned blocks = (unsigned)std::min<uint64_t>((c.n_xinst + 255) / 256, (uint64_t)std::max(sms, 1) * 4);
+  // one resident wave (MS_XR_MINB CTAs of 256 threads per SM): each warp walks one contiguous chunk
+  unsigned blocks = (unsigned)std::min<uint64_t>((c.n_xinst + 255) / 256, (uint64_t)std::max(sms, 1) * MS_XR_MINB);
   k_cross_reduce<<<blocks, 256, a.xb_smem ? xsm : 0, c.stream>>>(a);
   if (c.n_big) {
     k_cross_big<<<dim3(c.n_big, 32), 256, 0, c.stream>>>(a, c.xbig.as<uint32_t>(), c.n_big);
