@@ -357,6 +357,7 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
       const bool tp_pow2 = topo->tp <= 32 && (32 % topo->tp) == 0;
       c.fused_t = tp_pow2 && R <= 256 && c.fused_variant != 0;
       uint32_t T = (16384u / R) / 32u * 32u;
+      if (const char* e = std::getenv("MS_FT_T")) T = (uint32_t)std::atoi(e) / 32u * 32u;  // experiment: tile positions
       T = std::max(64u, std::min(1024u, T));
       if (T < 128) T = 64;  // below 128 positions the load lane mapping needs a power of two
       // two CTAs per SM: keep the fused kernel's shared memory under ~110 KB
@@ -365,6 +366,7 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
       };
       const size_t cap = c.fused_t ? fused_t_smem_cap() : 110u * 1024u;  // 2 (generic) / FT_MINB (transposed) CTAs per SM
       while (T > 32 && smem(T) > cap) T = T > 128 ? T - 32 : T / 2;  // below 128: powers of two (load lane mapping)
+      if (std::getenv("MS_FT_T")) std::fprintf(stderr, "[MS_FT_T] tile positions %u, shared memory %zu of %zu\n", T, smem(T), cap);
       // the persistent TMA-fed kernel (k_stage.cu): 16-byte-aligned rank rows, R <= 128; its own tile size
       c.use_stage = false;
       const char* sge = std::getenv("MS_STAGE");  // experimental until it beats k_fused_t: variant 2 or MS_STAGE=1
