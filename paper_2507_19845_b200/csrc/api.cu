@@ -356,7 +356,7 @@ scan_status scan_load_events(scan_ctx* ctx, const scan_topology* topo, const sca
     if (ok) {
       const bool tp_pow2 = topo->tp <= 32 && (32 % topo->tp) == 0;
       c.fused_t = tp_pow2 && R <= 256 && c.fused_variant != 0;
-      uint32_t T = (16384u / R) / 32u * 32u;
+      uint32_t T = ((c.fused_t ? fused_t_tile_events() : 16384u) / R) / 32u * 32u;
       if (const char* e = std::getenv("MS_FT_T")) T = (uint32_t)std::atoi(e) / 32u * 32u;  // experiment: tile positions
       T = std::max(64u, std::min(1024u, T));
       if (T < 128) T = 64;  // below 128 positions the load lane mapping needs a power of two

@@ -469,6 +469,7 @@ uint32_t stage_tile(uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM, uint32_
 size_t fused_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM);
 size_t fused_t_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM);
 size_t fused_t_smem_cap();
+uint32_t fused_t_tile_events();
 int launch_cross_reduce(Ctx& c);
 int launch_xwait_scatter(Ctx& c);
 int launch_deferred(Ctx& c);

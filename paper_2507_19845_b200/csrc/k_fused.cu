@@ -804,7 +804,7 @@ __global__ void __launch_bounds__(F_NT, 2) k_fused(FusedArgs a) {
 // reductions are butterflies of shuffles. The load pass transposes in registers and verifies the
 // kind_op and comm columns while the data is in registers.
 #ifndef MS_FT_NT
-#define MS_FT_NT 512
+#define MS_FT_NT 1024
 #endif
 #ifndef MS_FT_MINB
 #define MS_FT_MINB (1024 / MS_FT_NT)
@@ -1437,6 +1437,10 @@ static size_t fused_t_layout(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, u
 
 // shared-memory budget per CTA so that FT_MINB CTAs of the transposed kernel fit on one SM
 size_t fused_t_smem_cap() { return (size_t)220 * 1024 / FT_MINB; }
+
+// events per tile of the transposed kernel: 32 per thread (16384 at 512 threads; 32768 at the default
+// 1024: R = 128 rows x 256 positions on C3, half the per-tile set-up per event of 128 positions)
+uint32_t fused_t_tile_events() { return 32u * (uint32_t)FT_NT; }
 
 size_t fused_t_smem_bytes(uint32_t T, uint32_t R, uint32_t TP, uint32_t DP, uint32_t NCRM) {
   return fused_t_layout(T, R, TP, DP, NCRM, nullptr);
