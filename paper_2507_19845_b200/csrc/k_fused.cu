@@ -1514,9 +1514,11 @@ int launch_fused(Ctx& c) {
   a.bits = c.bits.as<uint32_t>(); a.cref = c.cref.as<uint32_t>(); a.rec = c.inst_rec.as<uint4>();
   a.slots = c.slots.as<uint4>(); a.p2p_rbase = c.p2p_rbase.as<uint32_t>();
   a.p2p_slot0 = c.p2p_slot0; a.p2p_inst0 = c.p2p_inst0; a.citer = c.citer.as<uint32_t>(); a.NIT1 = c.NIT + 1;
-  {  // L2 prefetches of the transposed kernel. Measured on full C3 (k_fused_t ms): none 8.51; own tile
-     // at kernel start 8.22 (default); tile pf ahead after the load pass: 96 8.32, 148 8.35, 296 8.93;
-     // both together 8.60 (98 + own). MS_FT_PF (distance, default 0 = off) / MS_FT_PF_OWN (0/1) override
+  {  // L2 prefetches of the transposed kernel. Round 1 (512 x 128 tiles, 2 CTAs per SM; k_fused_t ms): none
+     // 8.51; own tile at kernel start 8.22; tile pf ahead after the load pass: 96 8.32, 148 8.35, 296 8.93.
+     // With 1024 x 256 tiles (one CTA per SM, round 2) every prefetch costs: own tile + P2P words 6.86,
+     // own only 6.78, P2P only 6.70, none 6.61 (default); pf 74 / 148 ahead 7.40 / 7.45.
+     // MS_FT_PF (distance, 0 = off) / MS_FT_PF_OWN / MS_FT_PF_P2P (0/1) override
     static int pf = -1;
     if (pf < 0) {
       int sms = 148;
@@ -1526,9 +1528,9 @@ int launch_fused(Ctx& c) {
       (void)sms;
     }
     static int own = -1;
-    if (own < 0) { const char* e = std::getenv("MS_FT_PF_OWN"); own = e ? std::atoi(e) : 1; }
+    if (own < 0) { const char* e = std::getenv("MS_FT_PF_OWN"); own = e ? std::atoi(e) : 0; }
     static int pp = -1;
-    if (pp < 0) { const char* e = std::getenv("MS_FT_PF_P2P"); pp = e ? std::atoi(e) : 1; }
+    if (pp < 0) { const char* e = std::getenv("MS_FT_PF_P2P"); pp = e ? std::atoi(e) : 0; }
     a.pf_p2p = (uint32_t)pp;
     a.p2p_defer = p2p_defer_on(c) ? 1u : 0u;
     a.pf_dist = (uint32_t)pf;
